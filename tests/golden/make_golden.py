@@ -1,0 +1,176 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE itself.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the reference ``pathtrace`` package from /root/reference/pkg/src
+(numba CPU library) and records its outputs on small, seeded inputs.  The
+fixtures pin the float64 oracle (oracle/, checked bit-exactly in
+tests/test_oracle_golden.py) and give the GPU tests reference answers that do
+not need /root/reference at run time.
+"""
+
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+
+
+def import_reference():
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "numba_ref_cache"))
+    if REF not in sys.path:
+        sys.path.insert(0, REF)
+    import pathtrace  # noqa: F401
+    return pathtrace
+
+
+def ref_scene(pt, desc, quality="balanced"):
+    from pathtrace.scene import compile_scene
+    return compile_scene(desc, quality)
+
+
+def ref_desc_from_mesh(pt, V, F, origin, right, up, color=(0.8, 0.8, 0.8)):
+    from pathtrace.scene_io import SceneDescription, TriangleMesh, InstanceDecl
+    from pathtrace.integrators import Material
+    cam = pt.Camera(np.asarray(origin, float), np.asarray(right, float), np.asarray(up, float))
+    return SceneDescription(cam, {"mesh": TriangleMesh(V, F)}, {"mesh": "<synthetic>"},
+                            {"m": Material(np.array(color, float))}, [InstanceDecl("mesh", "m")], [],
+                            np.zeros(3), np.zeros(3))
+
+
+def primary_rays(pt, scene, W, H, seed=0, s=0, jitter=True):
+    """Exactly the reference's raygen (integrators.py:345-351, camera.py:81-97), float64."""
+    cam = scene.camera
+    O = np.tile(cam.origin, (W * H, 1))
+    D = np.empty((W * H, 3))
+    for pix in range(W * H):
+        xi, yi = pix % W, pix // W
+        st = pt.RandomStream.for_sample(seed, pix, s)
+        ju = st.uniform() if jitter else 0.0
+        jv = st.uniform() if jitter else 0.0
+        u, v = pt.pixel_to_uv(xi, yi, W, H, ju, jv)
+        D[pix] = pt.primary_ray(cam, u, v).direction
+    return O, D
+
+
+def main():
+    pt = import_reference()
+    from pathtrace.accel import _build_bvh
+    from pathtrace.integrators import IntegratorConfig
+    sys.path.insert(0, ROOT)
+    from paper_2603_00292_b200 import scenes
+
+    out = {}
+    # 1. RNG -----------------------------------------------------------------
+    streams = [(0, 0, 0), (0, 1, 0), (1, 12345, 63), (2**64 - 1, 7, 3), (123456789, 2**40, 1000),
+               (0, 65535, 0), (5, 2073599, 1023)]
+    uni = []
+    states = []
+    for (sd, px, s) in streams:
+        st = pt.RandomStream.for_sample(sd, px, s)
+        states.append((st._state, st._inc))
+        uni.append([st.uniform() for _ in range(8)])
+    kat = pt.RandomStream(42, 54)
+    np.savez_compressed(os.path.join(HERE, "pcg.npz"),
+                        streams=np.array(streams, dtype=np.uint64), uniforms=np.array(uni),
+                        states=np.array(states, dtype=np.uint64),
+                        kat_u32=np.array([kat.next_u32() for _ in range(6)], dtype=np.uint64))
+
+    # 2. Cornell box ------------------------------------------------------------
+    desc = pt.load_scene("/root/reference/pkg/scenes/cornell.scn")
+    sc = ref_scene(pt, desc)
+    W = H = 64
+    O, D = primary_rays(pt, sc, W, H)
+    t, inst, prim, u, v, n, stats = pt.closest_hit_batch(sc.tlas, O, D, with_stats=True)
+    rng = np.random.default_rng(1)
+    m = 3000
+    RO = rng.uniform(0.02, 0.98, (m, 3))
+    RD = rng.normal(size=(m, 3))
+    RD /= np.linalg.norm(RD, axis=1, keepdims=True)
+    RD[:100, 0] = 0.0                       # exact-zero direction components
+    RD[100:150, 1] = 0.0
+    tmin = np.where(np.arange(m) % 7 == 0, 0.05, 0.0)
+    tmax = np.where(np.arange(m) % 5 == 0, 0.5, 1e30)
+    rt, ri, rp, ru, rv, rn, rs = pt.closest_hit_batch(sc.tlas, RO, RD, tmin, tmax, with_stats=True)
+    rany = pt.any_hit_batch(sc.tlas, RO, RD, tmin, tmax)
+    mt, mi, mp, _, _, _ = pt.closest_hit_batch(sc.tlas, RO, RD, tmin, tmax, ray_mask=0x0)
+    meta = dict(inverses=sc.tlas.inverses, matrices=sc.tlas.matrices, cam=np.array([*sc.camera.origin,
+                *sc.camera.right, *sc.camera.up, *sc.camera.forward, sc.camera.distortion]),
+                diag=np.array(sc.diagonal()), lv0=sc.lights.v0, lv1=sc.lights.v1, lv2=sc.lights.v2,
+                ln=sc.lights.normal, lemis=sc.lights.emissive, larea=sc.lights.area,
+                inst_material=sc.inst_material, mat_color=sc.mat_color, mat_emissive=sc.mat_emissive,
+                root_box=sc.tlas.nodes["bounds"][0])
+    np.savez_compressed(os.path.join(HERE, "cornell_hits.npz"), O=O, D=D, t=t, inst=inst, prim=prim, u=u, v=v,
+                        n=n, stats=stats, RO=RO, RD=RD, tmin=tmin, tmax=tmax, rt=rt, ri=ri, rp=rp, ru=ru, rv=rv,
+                        rn=rn, rs=rs, rany=rany, masked_t=mt, **{"meta_" + k: v for k, v in meta.items()})
+
+    # 3. Cornell renders (render_frame) ----------------------------------------
+    renders = {}
+    jobs = [("eye32", "eye", 32, 32, 2, 0, True, 8), ("eye16c", "eye", 16, 16, 1, 0, False, 8),
+            ("pt24", "pt", 24, 24, 4, 0, True, 5), ("pt16s7", "pt", 16, 16, 3, 7, True, 8),
+            ("ao16", "ao", 16, 16, 2, 0, True, 8), ("nee16", "pt-nee", 16, 16, 4, 0, True, 5)]
+    for name, integ, w, h, spp, seed, jit, md in jobs:
+        cfg = IntegratorConfig(max_depth=md, ao_ray_count=8)
+        acc, st = pt.render_frame(sc, w, h, spp, integ, seed=seed, workers=2, cfg=cfg, jitter=jit,
+                                  return_stats=True)
+        renders[name] = acc.data
+        renders[name + "_rays"] = np.array(st["rays"])
+        renders[name + "_args"] = np.array([w, h, spp, seed, int(jit), md])
+    np.savez_compressed(os.path.join(HERE, "cornell_render.npz"), **renders)
+
+    # 4. SAH build arrays --------------------------------------------------------
+    bv = {}
+    soup = scenes.random_soup(500, seed=3)
+    sph = scenes.uv_sphere(10, 20)
+    for tag, mesh in (("soup", soup), ("sphere", sph)):
+        tri = mesh.vertices[mesh.faces]
+        lo, hi = tri.min(axis=1), tri.max(axis=1)
+        bv[tag + "_lo"], bv[tag + "_hi"] = lo, hi
+        for q in ("balanced", "fast"):
+            nd = _build_bvh(lo, hi, q)
+            for k in ("bounds", "left", "right", "count", "axis", "order"):
+                bv[f"{tag}_{q}_{k}"] = nd[k]
+            bv[f"{tag}_{q}_depth"] = np.array(nd["depth"])
+    np.savez_compressed(os.path.join(HERE, "bvh_sah.npz"), **bv)
+
+    # 5. sphere + soup primary hits (synthetic configs at test size) -------------
+    syn = {}
+    for tag, mesh, cam in (("sphere", scenes.uv_sphere(50, 100), ((0, 0, 2.5), (0.8, 0, 0), (0, 0.45, 0))),
+                           ("soup", scenes.random_soup(4000, seed=0),
+                            ((0.5, 0.5, 2.5), (0.6222, 0, 0), (0, 0.35, 0)))):
+        d2 = ref_desc_from_mesh(pt, mesh.vertices, mesh.faces, *cam)
+        s2 = ref_scene(pt, d2)
+        O2, D2 = primary_rays(pt, s2, 48, 27)
+        r = pt.closest_hit_batch(s2.tlas, O2, D2, with_stats=True)
+        for k, val in zip(("t", "inst", "prim", "u", "v", "n", "stats"), r):
+            syn[f"{tag}_{k}"] = val
+        syn[f"{tag}_O"], syn[f"{tag}_D"] = O2, D2
+        acc = pt.render_frame(s2, 48, 27, 1, "eye", seed=0)
+        syn[f"{tag}_eye"] = acc.data
+    np.savez_compressed(os.path.join(HERE, "synthetic_hits.npz"), **syn)
+
+    # 6. scalar triangle test incl. SPEC.md:63-71 examples ---------------------
+    from pathtrace.geometry import intersect_ray_triangle_batch
+    k = 4000
+    g = np.random.default_rng(2)
+    v0, v1, v2 = (g.normal(size=(k, 3)) for _ in range(3))
+    o = g.normal(size=(k, 3)) * 2
+    tgt = (v0 + v1 + v2) / 3 + g.normal(size=(k, 3)) * 0.5
+    d = tgt - o
+    tmn = np.zeros(k)
+    tmx = np.full(k, 1e30)
+    o[0], d[0], v0[0], v1[0], v2[0] = (0.25, 0.25, -1), (0, 0, 1), (0, 0, 0), (1, 0, 0), (0, 1, 0)
+    o[1], d[1] = (0.25, 0.25, -1), (1, 0, 0)
+    res = intersect_ray_triangle_batch(o, d, tmn, tmx, v0, v1, v2)
+    np.savez_compressed(os.path.join(HERE, "tri_hit.npz"), o=o, d=d, v0=v0, v1=v1, v2=v2, out=res)
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
