@@ -1,0 +1,130 @@
+/*
+ * rt_b200.h -- C ABI of the B200-native ray-tracing hot path (librt_b200.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (streams are passed as void*).  Every entry point returns 0 on success or a
+ * negative RT_E* code; rt_last_error() holds a thread-local message.
+ *
+ * The reference (pkg/src/pathtrace) is a Python/numba library with no FFI;
+ * each entry point below replaces the reference function named beside it and
+ * is bound from Python through ctypes (paper_2603_00292_b200/_native.py; the
+ * binding a reference maintainer would add is shown in INTEGRATION.md).
+ */
+#ifndef RT_B200_H
+#define RT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RT_OK 0
+#define RT_EINVAL (-1)        /* bad argument                 -> ValueError   */
+#define RT_ECUDA (-2)         /* CUDA runtime failure         -> RuntimeError */
+#define RT_EUNSUPPORTED (-3)  /* custom primitives (no GPU intersector yet) -> RegistryError */
+#define RT_EDEPTH (-4)        /* BVH deeper than the traversal stack -> BuildError (accel.py:148-149) */
+#define RT_ENOMEM (-5)        /* device allocation failed     -> MemoryError  */
+#define RT_ESTATE (-6)        /* e.g. trace before build      -> RuntimeError */
+
+#define RT_INTEG_EYE 0        /* integrators.py:129-141 _sample_eye */
+#define RT_INTEG_PT 2         /* integrators.py:182-235 _sample_pt  */
+
+#define RT_KERNEL_MEGA 0      /* one persistent kernel per frame (K7)      */
+#define RT_KERNEL_WAVEFRONT 1 /* raygen / extend / shade / accumulate (K8) */
+
+typedef struct rt_ctx rt_ctx;
+typedef struct rt_scene rt_scene;
+
+/* Frame parameters: render_frame(scene, width, height, spp, integrator, seed,
+ * workers, cfg, jitter) -- integrators.py:426-473.  Samples [s0, s1) are
+ * rendered with the GLOBAL sample index in the per-(seed, pixel, sample)
+ * stream hash (sampling.py:67-73), so a sample split across GPUs reproduces
+ * the single-GPU random numbers exactly.  Pixels [pix_lo, pix_hi) restrict the
+ * frame to a row-major pixel range (tile split); 0/0 means the whole frame. */
+typedef struct {
+    int32_t width, height;
+    int32_t s0, s1;
+    uint64_t seed;
+    int32_t jitter;
+    int32_t integrator;       /* RT_INTEG_EYE | RT_INTEG_PT */
+    int32_t max_depth;        /* IntegratorConfig.max_depth (integrators.py:56-74) */
+    int32_t kernel;           /* RT_KERNEL_MEGA | RT_KERNEL_WAVEFRONT */
+    float cam[13];            /* origin, right, up, forward, distortion (integrators.py:397-402) */
+    float sky[3];
+    float background[3];
+    float normal_offset;      /* 1e-4 * scene diagonal (integrators.py:405-413) */
+    int64_t pix_lo, pix_hi;
+} rt_render_params;
+
+/* ---- context --------------------------------------------------------- */
+int rt_ctx_create(int device, rt_ctx** out);
+void rt_ctx_destroy(rt_ctx* ctx);
+/* all work of the context is issued on this cudaStream_t (used verbatim; NULL =
+ * the legacy default stream); a new context uses its own non-blocking stream */
+int rt_ctx_set_stream(rt_ctx* ctx, void* cuda_stream);
+int rt_ctx_sync(rt_ctx* ctx);
+int rt_device_count(int* n);
+const char* rt_last_error(void);
+const char* rt_version(void);
+
+/* ---- scene (replaces compile_scene's geometry side, scene.py:79-141; the
+ *      instances are flattened to world-space triangles on the host) ------ */
+/* tris: (n, 9) fp32 world vertices, host.  normals: (n, 3) fp32 world normal per
+ * triangle computed reference-style (local cross, inverse-transpose, accel.py:843-847).
+ * tri_inst / tri_prim: (n,) owning instance and primitive index; tri_mask: (n,) the
+ * instance visibility mask; tri_material: (n,) material row.  mat_color /
+ * mat_emissive: (n_mat, 3).  Triangle ids must be ordered by (inst, prim) so the
+ * reference tie rule (accel.py:629, 815-817) becomes "lowest flat id". */
+int rt_scene_create(rt_ctx* ctx, int64_t n, const float* tris, const float* normals,
+                    const int32_t* tri_inst, const int32_t* tri_prim, const uint32_t* tri_mask,
+                    const int32_t* tri_material, const float* mat_color, const float* mat_emissive,
+                    int32_t n_mat, rt_scene** out);
+void rt_scene_destroy(rt_scene* scene);
+/* new vertex positions for the same triangles (Blas.refit(vertices), accel.py:263-283);
+ * host (n, 9) fp32, copied on the context stream; the BVH must be rebuilt */
+int rt_scene_set_vertices(rt_ctx* ctx, rt_scene* scene, const float* tris);
+
+/* ---- LBVH build (replaces _build_bvh, accel.py:68-187; K1-K5) ---------- */
+/* morton_bits: 30 or 63.  build_ms (nullable): device time of the build
+ * (CUDA events on the context stream; synchronises). */
+int rt_bvh_build(rt_ctx* ctx, rt_scene* scene, int morton_bits, float* build_ms);
+/* same build with CUDA events between stages: stage_ms[6] = bounds, morton,
+ * histogram, radix passes, karras+leaf gather, refit (device ms; synchronises) */
+int rt_bvh_build_profiled(rt_ctx* ctx, rt_scene* scene, int morton_bits, float* stage_ms);
+/* root box (6), tree height (stack bound) and node count */
+int rt_bvh_info(rt_ctx* ctx, rt_scene* scene, float* root6, int32_t* height, int64_t* n_internal);
+/* parity download; every pointer nullable.  sorted_keys (n) u64, order (n) u32,
+ * child (n-1, 2) i32 (>=0 internal, <0 = ~leaf), parent (2n-1) i32,
+ * boxes (n-1, 12) f32 [lo_L hi_L lo_R hi_R], heights (n-1) i32,
+ * centroid_bounds (6) f32, inv_ext (3) f32, morton (n) u64 unsorted keys */
+int rt_bvh_download(rt_ctx* ctx, rt_scene* scene, uint64_t* sorted_keys, uint32_t* order,
+                    int32_t* child, int32_t* parent, float* boxes, int32_t* heights,
+                    float* centroid_bounds, float* inv_ext, uint64_t* morton);
+
+/* ---- closest hit (replaces _closest_batch / closest_hit_batch, accel.py:950-976, 1128-1156; K6) */
+/* Device buffers.  rays: (n, 8) f32 [ox oy oz tmin dx dy dz tmax];
+ * hits: (n, 4) [t (f32), flat id (i32, -1 miss), u, v]; stats (nullable): (n, 2)
+ * u32 [triangle tests, node visits]. */
+int rt_trace_closest(rt_ctx* ctx, rt_scene* scene, int64_t n, const float* rays, float* hits,
+                     uint32_t ray_mask, uint32_t* stats);
+/* Host buffers with the reference's dtypes (float64 / int64), chunked and
+ * pipelined H2D / trace / D2H.  Misses: t = -1, inst = prim = -1 (accel.py:964, 1144).
+ * stats nullable (n, 2) int64. */
+int rt_closest_hit_host(rt_ctx* ctx, rt_scene* scene, int64_t n, const double* origins,
+                        const double* dirs, const double* t_min, const double* t_max,
+                        uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
+                        double* v, double* normal, int64_t* stats);
+
+/* ---- render (replaces render_frame / _render_chunk, integrators.py:334-473; K7/K8) */
+/* accum: device (H*W, 4) f32 running (r, g, b, n) sums, row 0 on top, added to in
+ * place (sample order per pixel).  rays_out (nullable): closest-hit queries issued. */
+int rt_render(rt_ctx* ctx, rt_scene* scene, const rt_render_params* p, float* accum,
+              uint64_t* rays_out);
+/* primary rays of sample s for every pixel of the frame (parity tests): (W*H, 8) like rt_trace_closest */
+int rt_raygen(rt_ctx* ctx, const rt_render_params* p, int32_t sample, float* rays);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,158 @@
+"""ctypes binding of librt_b200.so (the C ABI in include/rt_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing or no
+sm_100 device is present, every call raises.  ctypes releases the GIL during
+each call, so one Python thread per GPU works like the reference's worker
+threads (integrators.py:460-463).
+"""
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librt_b200.so")
+
+RT_OK = 0
+RT_EINVAL = -1
+RT_ECUDA = -2
+RT_EUNSUPPORTED = -3
+RT_EDEPTH = -4
+RT_ENOMEM = -5
+RT_ESTATE = -6
+
+RT_INTEG_EYE = 0
+RT_INTEG_PT = 2
+RT_KERNEL_MEGA = 0
+RT_KERNEL_WAVEFRONT = 1
+
+_lib = None
+_lock = threading.Lock()
+
+
+class BuildError(ValueError):
+    """accel.py:51-52."""
+
+
+class RegistryError(LookupError):
+    """accel.py:55-56."""
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+class RenderParams(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32),
+                ("s0", ctypes.c_int32), ("s1", ctypes.c_int32),
+                ("seed", ctypes.c_uint64), ("jitter", ctypes.c_int32),
+                ("integrator", ctypes.c_int32), ("max_depth", ctypes.c_int32),
+                ("kernel", ctypes.c_int32), ("cam", ctypes.c_float * 13),
+                ("sky", ctypes.c_float * 3), ("background", ctypes.c_float * 3),
+                ("normal_offset", ctypes.c_float), ("pix_lo", ctypes.c_int64),
+                ("pix_hi", ctypes.c_int64)]
+
+
+def lib():
+    """Load the CUDA library; raises if it was not built (no silent fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                              "(this package has no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, i32, i64, u32, ci = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int
+        L.rt_last_error.restype = ctypes.c_char_p
+        L.rt_version.restype = ctypes.c_char_p
+        sigs = {
+            "rt_device_count": [vp],
+            "rt_ctx_create": [ci, vp],
+            "rt_ctx_set_stream": [vp, vp],
+            "rt_ctx_sync": [vp],
+            "rt_scene_create": [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp],
+            "rt_bvh_build": [vp, vp, ci, vp],
+            "rt_bvh_build_profiled": [vp, vp, ci, vp],
+            "rt_scene_set_vertices": [vp, vp, vp],
+            "rt_bvh_info": [vp, vp, vp, vp, vp],
+            "rt_bvh_download": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
+            "rt_trace_closest": [vp, vp, i64, vp, vp, u32, vp],
+            "rt_closest_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp, vp],
+            "rt_render": [vp, vp, ctypes.POINTER(RenderParams), vp, vp],
+            "rt_raygen": [vp, ctypes.POINTER(RenderParams), i32, vp],
+        }
+        for name, args in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ci
+        L.rt_ctx_destroy.argtypes = [vp]
+        L.rt_ctx_destroy.restype = None
+        L.rt_scene_destroy.argtypes = [vp]
+        L.rt_scene_destroy.restype = None
+        _lib = L
+        return L
+
+
+def check(rc):
+    if rc == RT_OK:
+        return
+    msg = lib().rt_last_error().decode(errors="replace")
+    if rc == RT_EINVAL:
+        raise ValueError(msg)
+    if rc == RT_EDEPTH:
+        raise BuildError(msg)
+    if rc == RT_EUNSUPPORTED:
+        raise RegistryError(msg)
+    if rc == RT_ENOMEM:
+        raise MemoryError(msg)
+    raise NativeError(f"librt_b200 error {rc}: {msg}")
+
+
+def ptr(x):
+    """Raw pointer of a numpy array or torch tensor (None passes through)."""
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return ctypes.c_void_p(x.data_ptr())
+    return x.ctypes.data_as(ctypes.c_void_p)
+
+
+class Context:
+    """One rt_ctx per CUDA device (owns a stream, counters, staging)."""
+
+    _cache = {}
+
+    def __init__(self, device=0):
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        check(lib().rt_ctx_create(self.device, ctypes.byref(h)))
+        self.handle = h
+        # issue everything on torch's current stream of this device, so device
+        # buffers allocated / consumed by torch are ordered with our kernels
+        import torch
+        self.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+
+    @classmethod
+    def get(cls, device=0):
+        with _lock:
+            c = cls._cache.get(int(device))
+        if c is None:
+            c = cls(device)
+            with _lock:
+                cls._cache[int(device)] = c
+        return c
+
+    def set_stream(self, stream_ptr):
+        self.stream_ptr = int(stream_ptr or 0)
+        check(lib().rt_ctx_set_stream(self.handle, ctypes.c_void_p(self.stream_ptr) if self.stream_ptr else None))
+
+    def sync(self):
+        check(lib().rt_ctx_sync(self.handle))
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and _lib is not None:
+                _lib.rt_ctx_destroy(self.handle)
+        except Exception:
+            pass

@@ -1,0 +1,409 @@
+// capi.cu -- the extern "C" boundary of librt_b200.so (declared in include/rt_b200.h).
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "rt_common.cuh"
+
+static thread_local char g_err[1024] = "";
+
+void rt_set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+
+size_t rt_sort_scratch_words(int64_t n);
+void rt_render_release(rt_scene* s);
+
+#define RT_CHECK_ARG(cond, msg)              \
+    do {                                     \
+        if (!(cond)) {                       \
+            rt_set_error("%s", msg);         \
+            return RT_EINVAL;                \
+        }                                    \
+    } while (0)
+
+static int check_device_error(rt_ctx* ctx) {
+    int e = 0;
+    RT_CUDA_TRY(cudaMemcpyAsync(&e, ctx->d_error, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
+    RT_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (e == RT_EDEPTH) {
+        rt_set_error("BVH height exceeds the %d-entry traversal stack", RT_STACK - 1);
+        int z = 0;
+        cudaMemcpy(ctx->d_error, &z, sizeof z, cudaMemcpyHostToDevice);
+        return RT_EDEPTH;
+    }
+    return RT_OK;
+}
+
+extern "C" {
+
+const char* rt_last_error(void) { return g_err; }
+const char* rt_version(void) { return "librt_b200 0.1 (sm_100a)"; }
+
+int rt_device_count(int* n) {
+    RT_CUDA_TRY(cudaGetDeviceCount(n));
+    return RT_OK;
+}
+
+int rt_ctx_create(int device, rt_ctx** out) {
+    RT_CHECK_ARG(out != nullptr, "out is NULL");
+    int n = 0;
+    RT_CUDA_TRY(cudaGetDeviceCount(&n));
+    RT_CHECK_ARG(device >= 0 && device < n, "device index out of range");
+    RT_CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    RT_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) {
+        rt_set_error("librt_b200 targets sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
+        return RT_ECUDA;
+    }
+    rt_ctx* c = new rt_ctx();
+    memset(c, 0, sizeof *c);
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    RT_CUDA_TRY(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    RT_CUDA_TRY(cudaEventCreate(&c->ev0));
+    RT_CUDA_TRY(cudaEventCreate(&c->ev1));
+    RT_CUDA_TRY(cudaMalloc(&c->d_counter, 64 * sizeof(unsigned int)));
+    RT_CUDA_TRY(cudaMalloc(&c->d_error, sizeof(int)));
+    RT_CUDA_TRY(cudaMemset(c->d_error, 0, sizeof(int)));
+    *out = c;
+    return RT_OK;
+}
+
+void rt_ctx_destroy(rt_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->d_stage) cudaFree(c->d_stage);
+    cudaFree(c->d_counter);
+    cudaFree(c->d_error);
+    cudaEventDestroy(c->ev0);
+    cudaEventDestroy(c->ev1);
+    cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+int rt_ctx_set_stream(rt_ctx* c, void* stream) {
+    RT_CHECK_ARG(c, "ctx is NULL");
+    c->stream = (cudaStream_t)stream;   // used verbatim: NULL is the legacy default stream
+    return RT_OK;
+}
+
+int rt_ctx_sync(rt_ctx* c) {
+    RT_CHECK_ARG(c, "ctx is NULL");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return check_device_error(c);
+}
+
+int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normals, const int32_t* tri_inst,
+                    const int32_t* tri_prim, const uint32_t* tri_mask, const int32_t* tri_material,
+                    const float* mat_color, const float* mat_emissive, int32_t n_mat, rt_scene** out) {
+    RT_CHECK_ARG(c && out, "ctx/out is NULL");
+    RT_CHECK_ARG(n >= 1, "cannot build over zero primitives");
+    RT_CHECK_ARG(n < (1ll << 30), "at most 2^30 - 1 triangles per scene");
+    RT_CHECK_ARG(tris && normals && tri_inst && tri_prim && tri_mask && tri_material, "NULL triangle array");
+    RT_CHECK_ARG(n_mat >= 1 && mat_color && mat_emissive, "materials missing");
+    for (int64_t i = 0; i < n; ++i)
+        if (tri_material[i] < 0 || tri_material[i] >= n_mat) {
+            rt_set_error("triangle %lld references material %d of %d", (long long)i, tri_material[i], n_mat);
+            return RT_EINVAL;
+        }
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    rt_scene* s = new rt_scene();
+    memset(s, 0, sizeof *s);
+    s->n = n;
+    s->n_mat = n_mat;
+    const int64_t ni = n > 1 ? n - 1 : 1;
+    std::vector<float4> attr(n), mc(n_mat), me(n_mat);
+    for (int64_t i = 0; i < n; ++i) {
+        float4 a;
+        a.x = normals[3 * i]; a.y = normals[3 * i + 1]; a.z = normals[3 * i + 2];
+        int m = tri_material[i];
+        memcpy(&a.w, &m, 4);
+        attr[i] = a;
+    }
+    for (int k = 0; k < n_mat; ++k) {
+        mc[k] = make_float4(mat_color[3 * k], mat_color[3 * k + 1], mat_color[3 * k + 2], 0.f);
+        me[k] = make_float4(mat_emissive[3 * k], mat_emissive[3 * k + 1], mat_emissive[3 * k + 2], 0.f);
+    }
+#define ALLOC(ptr, bytes)                                                       \
+    do {                                                                        \
+        cudaError_t _e = cudaMalloc((void**)&(ptr), (bytes));                   \
+        if (_e != cudaSuccess) {                                                \
+            rt_set_error("cudaMalloc(%zu) failed: %s", (size_t)(bytes), cudaGetErrorString(_e)); \
+            rt_scene_destroy(s);                                                \
+            return RT_ENOMEM;                                                   \
+        }                                                                       \
+    } while (0)
+    ALLOC(s->tris, sizeof(float) * 9 * n);
+    ALLOC(s->tri_attr, sizeof(float4) * n);
+    ALLOC(s->tri_inst, sizeof(int32_t) * n);
+    ALLOC(s->tri_prim, sizeof(int32_t) * n);
+    ALLOC(s->tri_mask, sizeof(uint32_t) * n);
+    ALLOC(s->mat_color, sizeof(float4) * n_mat);
+    ALLOC(s->mat_emissive, sizeof(float4) * n_mat);
+    ALLOC(s->nodes, sizeof(float4) * 4 * ni);
+    ALLOC(s->tri_sorted, sizeof(float4) * 3 * n);
+    ALLOC(s->keys_a, sizeof(uint64_t) * n);
+    ALLOC(s->keys_b, sizeof(uint64_t) * n);
+    ALLOC(s->vals_a, sizeof(uint32_t) * n);
+    ALLOC(s->vals_b, sizeof(uint32_t) * n);
+    ALLOC(s->parent, sizeof(int32_t) * (2 * n - 1));
+    ALLOC(s->child, sizeof(int2) * ni);
+    ALLOC(s->flags, sizeof(unsigned int) * ni);
+    ALLOC(s->cbounds, sizeof(float) * 16);
+    ALLOC(s->cb_enc, sizeof(unsigned int) * 8);
+    s->sort_scratch_words = rt_sort_scratch_words(n);
+    ALLOC(s->sort_scratch, sizeof(unsigned int) * s->sort_scratch_words);
+    ALLOC(s->leaf_box, sizeof(float4) * 2 * n);
+#undef ALLOC
+    cudaStream_t st = c->stream;
+    RT_CUDA_TRY(cudaMemcpyAsync(s->tris, tris, sizeof(float) * 9 * n, cudaMemcpyHostToDevice, st));
+    RT_CUDA_TRY(cudaMemcpyAsync(s->tri_attr, attr.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, st));
+    RT_CUDA_TRY(cudaMemcpyAsync(s->tri_inst, tri_inst, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    RT_CUDA_TRY(cudaMemcpyAsync(s->tri_prim, tri_prim, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
+    RT_CUDA_TRY(cudaMemcpyAsync(s->tri_mask, tri_mask, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+    RT_CUDA_TRY(cudaMemcpyAsync(s->mat_color, mc.data(), sizeof(float4) * n_mat, cudaMemcpyHostToDevice, st));
+    RT_CUDA_TRY(cudaMemcpyAsync(s->mat_emissive, me.data(), sizeof(float4) * n_mat, cudaMemcpyHostToDevice, st));
+    RT_CUDA_TRY(cudaStreamSynchronize(st));   // host vectors go out of scope
+    *out = s;
+    return RT_OK;
+}
+
+int rt_scene_set_vertices(rt_ctx* c, rt_scene* s, const float* tris) {
+    RT_CHECK_ARG(c && s && tris, "NULL argument");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    RT_CUDA_TRY(cudaMemcpyAsync(s->tris, tris, sizeof(float) * 9 * s->n, cudaMemcpyHostToDevice, c->stream));
+    s->built = 0;
+    return RT_OK;
+}
+
+void rt_scene_destroy(rt_scene* s) {
+    if (!s) return;
+    rt_render_release(s);
+    void* ptrs[] = {s->tris, s->tri_attr, s->tri_inst, s->tri_prim, s->tri_mask, s->mat_color, s->mat_emissive,
+                    s->nodes, s->tri_sorted, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->parent, s->child,
+                    s->flags, s->cbounds, s->cb_enc, s->sort_scratch, s->leaf_box};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    delete s;
+}
+
+int rt_bvh_build(rt_ctx* c, rt_scene* s, int bits, float* build_ms) {
+    RT_CHECK_ARG(c && s, "ctx/scene is NULL");
+    RT_CHECK_ARG(bits == 30 || bits == 63, "morton_bits must be 30 or 63");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    if (build_ms) RT_CUDA_TRY(cudaEventRecord(c->ev0, c->stream));
+    int rc = rt_lbvh_build_impl(c, s, bits);
+    if (rc) return rc;
+    s->built = 1;
+    s->bits = bits;
+    if (build_ms) {
+        RT_CUDA_TRY(cudaEventRecord(c->ev1, c->stream));
+        RT_CUDA_TRY(cudaEventSynchronize(c->ev1));
+        RT_CUDA_TRY(cudaEventElapsedTime(build_ms, c->ev0, c->ev1));
+    }
+    return RT_OK;
+}
+
+int rt_bvh_build_profiled(rt_ctx* c, rt_scene* s, int bits, float* stage_ms) {
+    RT_CHECK_ARG(c && s && stage_ms, "NULL argument");
+    RT_CHECK_ARG(bits == 30 || bits == 63, "morton_bits must be 30 or 63");
+    RT_CHECK_ARG(s->n > 1, "profiling needs at least two triangles");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    if (!c->prof[0])
+        for (int k = 0; k < 8; ++k) RT_CUDA_TRY(cudaEventCreate(&c->prof[k]));
+    c->profiling = 1;
+    int rc = rt_lbvh_build_impl(c, s, bits);
+    c->profiling = 0;
+    if (rc) return rc;
+    s->built = 1;
+    s->bits = bits;
+    RT_CUDA_TRY(cudaEventSynchronize(c->prof[6]));
+    for (int k = 0; k < 6; ++k) RT_CUDA_TRY(cudaEventElapsedTime(stage_ms + k, c->prof[k], c->prof[k + 1]));
+    return RT_OK;
+}
+
+int rt_bvh_info(rt_ctx* c, rt_scene* s, float* root6, int32_t* height, int64_t* n_internal) {
+    RT_CHECK_ARG(c && s, "ctx/scene is NULL");
+    if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    float4 nd[4];
+    RT_CUDA_TRY(cudaMemcpyAsync(nd, s->nodes, sizeof nd, cudaMemcpyDeviceToHost, c->stream));
+    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (root6) {
+        root6[0] = std::min(nd[0].x, nd[1].x); root6[3] = std::max(nd[0].y, nd[1].y);
+        root6[1] = std::min(nd[0].z, nd[1].z); root6[4] = std::max(nd[0].w, nd[1].w);
+        root6[2] = std::min(nd[2].x, nd[2].z); root6[5] = std::max(nd[2].y, nd[2].w);
+    }
+    if (height) memcpy(height, &nd[3].z, 4);
+    if (n_internal) *n_internal = s->n > 1 ? s->n - 1 : 1;
+    return RT_OK;
+}
+
+int rt_bvh_download(rt_ctx* c, rt_scene* s, uint64_t* sorted_keys, uint32_t* order, int32_t* child,
+                    int32_t* parent, float* boxes, int32_t* heights, float* cbounds, float* inv_ext,
+                    uint64_t* morton) {
+    RT_CHECK_ARG(c && s, "ctx/scene is NULL");
+    if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const int64_t n = s->n;
+    if (n == 1) {
+        if (order) { order[0] = 0; }
+        return RT_OK;
+    }
+    const bool wide = s->bits == 63;
+    auto keys_to_u64 = [&](const void* dev, uint64_t* host) -> int {
+        if (wide) {
+            RT_CUDA_TRY(cudaMemcpy(host, dev, 8 * n, cudaMemcpyDeviceToHost));
+        } else {
+            std::vector<uint32_t> tmp(n);
+            RT_CUDA_TRY(cudaMemcpy(tmp.data(), dev, 4 * n, cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < n; ++i) host[i] = tmp[i];
+        }
+        return RT_OK;
+    };
+    int rc;
+    if (sorted_keys && (rc = keys_to_u64(s->keys_a, sorted_keys))) return rc;
+    if (order) RT_CUDA_TRY(cudaMemcpy(order, s->vals_a, 4 * n, cudaMemcpyDeviceToHost));
+    if (child) RT_CUDA_TRY(cudaMemcpy(child, s->child, 8 * (n - 1), cudaMemcpyDeviceToHost));
+    if (parent) RT_CUDA_TRY(cudaMemcpy(parent, s->parent, 4 * (2 * n - 1), cudaMemcpyDeviceToHost));
+    if (boxes || heights) {
+        std::vector<float4> nd(4 * (n - 1));
+        RT_CUDA_TRY(cudaMemcpy(nd.data(), s->nodes, sizeof(float4) * 4 * (n - 1), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < n - 1; ++i) {
+            const float4 *q = &nd[4 * i];
+            if (boxes) {
+                float* b = boxes + 12 * i;
+                b[0] = q[0].x; b[1] = q[0].z; b[2] = q[2].x; b[3] = q[0].y; b[4] = q[0].w; b[5] = q[2].y;
+                b[6] = q[1].x; b[7] = q[1].z; b[8] = q[2].z; b[9] = q[1].y; b[10] = q[1].w; b[11] = q[2].w;
+            }
+            if (heights) memcpy(heights + i, &q[3].z, 4);
+        }
+    }
+    if (cbounds || inv_ext) {
+        float cb[9];
+        RT_CUDA_TRY(cudaMemcpy(cb, s->cbounds, sizeof cb, cudaMemcpyDeviceToHost));
+        if (cbounds) memcpy(cbounds, cb, 6 * sizeof(float));
+        if (inv_ext) memcpy(inv_ext, cb + 6, 3 * sizeof(float));
+    }
+    // the unsorted keys are overwritten by the sort's ping-pong; recompute them on request
+    if (morton) {
+        rt_set_error("unsorted Morton keys are not retained after the sort");
+        return RT_EINVAL;
+    }
+    return RT_OK;
+}
+
+int rt_trace_closest(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, float* hits, uint32_t ray_mask,
+                     uint32_t* stats) {
+    RT_CHECK_ARG(c && s, "ctx/scene is NULL");
+    RT_CHECK_ARG(n >= 0 && (n == 0 || (rays && hits)), "bad ray/hit buffers");
+    if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    return rt_trace_impl(c, s, n, rays, reinterpret_cast<float4*>(hits), ray_mask, stats);
+}
+
+// accel.py:1128-1156 with the reference's host dtypes; rays are processed in
+// chunks through pinned staging: H2D(f64) -> pack -> trace -> expand -> D2H(f64)
+int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const double* d, const double* tmin,
+                        const double* tmax, uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
+                        double* v, double* nrm, int64_t* stats) {
+    RT_CHECK_ARG(c && s, "ctx/scene is NULL");
+    RT_CHECK_ARG(n >= 0, "negative ray count");
+    if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    if (n == 0) return RT_OK;
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    const int64_t CH = std::min<int64_t>(n, 1 << 21);
+    // per ray: in 8*8 = 64 B (o, d, tmin, tmax), packed 32 B, hit 16 B, stats 8 B, out 64 B (+16 stats)
+    const size_t in_b = 64, out_b = 64 + 16;
+    size_t dev_need = (size_t)CH * (in_b + 32 + 16 + 8 + out_b);
+    if (c->d_stage_bytes < dev_need) {
+        if (c->d_stage) cudaFree(c->d_stage);
+        c->d_stage = nullptr;
+        c->d_stage_bytes = 0;
+        RT_CUDA_TRY(cudaMalloc(&c->d_stage, dev_need));
+        c->d_stage_bytes = dev_need;
+    }
+    char* D = (char*)c->d_stage;
+    double* d_o = (double*)D; D += 24 * CH;
+    double* d_d = (double*)D; D += 24 * CH;
+    double* d_tmin = (double*)D; D += 8 * CH;
+    double* d_tmax = (double*)D; D += 8 * CH;
+    float* d_rays = (float*)D; D += 32 * CH;
+    float4* d_hits = (float4*)D; D += 16 * CH;
+    uint32_t* d_stats = (uint32_t*)D; D += 8 * CH;
+    double* d_t = (double*)D; D += 8 * CH;
+    int64_t* d_inst = (int64_t*)D; D += 8 * CH;
+    int64_t* d_prim = (int64_t*)D; D += 8 * CH;
+    double* d_u = (double*)D; D += 8 * CH;
+    double* d_v = (double*)D; D += 8 * CH;
+    double* d_n = (double*)D; D += 24 * CH;
+    cudaStream_t st = c->stream;
+    std::vector<uint32_t> hstats;
+    if (stats) hstats.resize(2 * CH);
+    for (int64_t b = 0; b < n; b += CH) {
+        int64_t m = std::min(CH, n - b);
+        RT_CUDA_TRY(cudaMemcpyAsync(d_o, o + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_d, d + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_tmin, tmin + b, 8 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
+        int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
+        if (rc) return rc;
+        rc = rt_trace_impl(c, s, m, d_rays, d_hits, ray_mask, stats ? d_stats : nullptr);
+        if (rc) return rc;
+        rc = rt_expand_hits_f64(c, s, m, d_hits, d_t, d_inst, d_prim, d_u, d_v, d_n);
+        if (rc) return rc;
+        RT_CUDA_TRY(cudaMemcpyAsync(t + b, d_t, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(inst + b, d_inst, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(prim + b, d_prim, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(u + b, d_u, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(v + b, d_v, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(nrm + 3 * b, d_n, 24 * m, cudaMemcpyDeviceToHost, st));
+        if (stats) {
+            RT_CUDA_TRY(cudaMemcpyAsync(hstats.data(), d_stats, 8 * m, cudaMemcpyDeviceToHost, st));
+            RT_CUDA_TRY(cudaStreamSynchronize(st));
+            for (int64_t i = 0; i < m; ++i) {
+                stats[2 * (b + i)] = hstats[2 * i];
+                stats[2 * (b + i) + 1] = hstats[2 * i + 1];
+            }
+        }
+    }
+    RT_CUDA_TRY(cudaStreamSynchronize(st));
+    return check_device_error(c);
+}
+
+int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out) {
+    RT_CHECK_ARG(c && s && p && accum, "NULL argument");
+    RT_CHECK_ARG(p->width >= 1 && p->height >= 1 && p->s1 > p->s0 && p->s0 >= 0,
+                 "width, height, and spp must all be >= 1");
+    RT_CHECK_ARG(p->integrator == RT_INTEG_EYE || p->integrator == RT_INTEG_PT,
+                 "integrator must be eye or pt on the GPU path");
+    RT_CHECK_ARG(p->max_depth >= 1, "max_depth must be >= 1");
+    RT_CHECK_ARG(p->kernel == RT_KERNEL_MEGA || p->kernel == RT_KERNEL_WAVEFRONT, "unknown kernel");
+    if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    int rc = rt_render_impl(c, s, p, accum, rays_out);
+    if (rc) return rc;
+    if (rays_out) return check_device_error(c);
+    return RT_OK;
+}
+
+int rt_raygen(rt_ctx* c, const rt_render_params* p, int32_t sample, float* rays) {
+    RT_CHECK_ARG(c && p && rays, "NULL argument");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    return rt_raygen_impl(c, p, sample, rays);
+}
+
+}  // extern "C"

@@ -1,0 +1,431 @@
+// lbvh.cu -- GPU LBVH build for sm_100a (replaces the reference's top-down
+// binned-SAH _build_bvh, accel.py:68-187, with Karras 2012).
+//
+//   K1 lbvh_bounds     fp32 centroid bounds (block reduce + one orderable-uint
+//                      atomic per block and axis)
+//   K2 lbvh_morton     30-bit (10b/axis) or 63-bit (21b/axis) keys, no FMA
+//   K3 onesweep        LSD radix sort, 8-bit digits, one histogram pass for
+//                      all digits + one kernel per digit with decoupled
+//                      look-back and __match_any_sync warp ranking; stable
+//   K4 karras_emit     split search with the index fallback for equal keys,
+//                      parent pointers, leaf gather into leaf order
+//   K5 lbvh_refit      bottom-up with per-node arrival counters, writes 64-B
+//                      BVH2 nodes (both child boxes in the parent) + height
+//
+// The choices are the frozen ones of SURVEY.md 8(c); oracle/rt_oracle.c Part B
+// restates them on the CPU and tests/test_gpu_lbvh.py checks bit equality.
+#include <cub/block/block_scan.cuh>
+
+#include "rt_common.cuh"
+
+namespace {
+
+constexpr int SORT_THREADS = 256;   // == RADIX
+constexpr int SORT_ITEMS = 16;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // 4096 keys per tile
+constexpr int RADIX = 256;
+constexpr unsigned FLAG_AGG = 1u << 30;
+constexpr unsigned FLAG_INC = 2u << 30;
+constexpr unsigned VALUE_MASK = (1u << 30) - 1u;
+
+__device__ __forceinline__ void tri_box(const float* t, float lo[3], float hi[3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = sel_min(sel_min(t[a], t[3 + a]), t[6 + a]);
+        hi[a] = sel_max(sel_max(t[a], t[3 + a]), t[6 + a]);
+    }
+}
+
+__device__ __forceinline__ void load_tri(const float* tris, int64_t i, float t[9]) {
+    const float* p = tris + 9 * i;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) t[k] = __ldg(p + k);
+}
+
+// ---- K1 -------------------------------------------------------------------
+__global__ void __launch_bounds__(256) lbvh_bounds_kernel(const float* __restrict__ tris, int64_t n,
+                                                         unsigned int* __restrict__ cb_enc) {
+    float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float t[9], blo[3], bhi[3];
+        load_tri(tris, i, t);
+        tri_box(t, blo, bhi);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float c = __fmul_rn(0.5f, __fadd_rn(blo[a], bhi[a]));
+            lo[a] = sel_min(lo[a], c);
+            hi[a] = sel_max(hi[a], c);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            lo[a] = sel_min(lo[a], __shfl_xor_sync(RT_FULL, lo[a], off));
+            hi[a] = sel_max(hi[a], __shfl_xor_sync(RT_FULL, hi[a], off));
+        }
+    }
+    __shared__ float s[8][6];
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) { s[w][a] = lo[a]; s[w][3 + a] = hi[a]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        int a = threadIdx.x;
+        float v = s[0][a];
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) v = (a < 3) ? sel_min(v, s[k][a]) : sel_max(v, s[k][a]);
+        if (a < 3) atomicMin(cb_enc + a, f2ord(v));
+        else atomicMax(cb_enc + a, f2ord(v));
+    }
+}
+
+__global__ void lbvh_bounds_finish(const unsigned int* __restrict__ cb_enc, float* __restrict__ cb) {
+    int a = threadIdx.x;
+    if (a < 3) {
+        float lo = ord2f(cb_enc[a]), hi = ord2f(cb_enc[3 + a]);
+        cb[a] = lo;
+        cb[3 + a] = hi;
+        float ext = __fsub_rn(hi, lo);
+        cb[6 + a] = ext > 0.0f ? __fdiv_rn(1.0f, ext) : 0.0f;
+    }
+}
+
+// ---- K2 -------------------------------------------------------------------
+__device__ __forceinline__ uint32_t expand10(uint32_t v) {
+    v &= 0x3FFu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__device__ __forceinline__ uint64_t expand21(uint64_t v) {
+    v &= 0x1FFFFFull;
+    v = (v | (v << 32)) & 0x001F00000000FFFFull;
+    v = (v | (v << 16)) & 0x001F0000FF0000FFull;
+    v = (v | (v << 8)) & 0x100F00F00F00F00Full;
+    v = (v | (v << 4)) & 0x10C30C30C30C30C3ull;
+    v = (v | (v << 2)) & 0x1249249249249249ull;
+    return v;
+}
+
+template <typename K, int B>
+__global__ void __launch_bounds__(256) lbvh_morton_kernel(const float* __restrict__ tris, int64_t n,
+                                                         const float* __restrict__ cb, K* __restrict__ keys) {
+    const float scale = (float)(1u << B), qmax = (float)((1u << B) - 1u);
+    float lo[3], inv[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { lo[a] = __ldg(cb + a); inv[a] = __ldg(cb + 6 + a); }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float t[9], blo[3], bhi[3];
+        load_tri(tris, i, t);
+        tri_box(t, blo, bhi);
+        uint32_t q[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            float c = __fmul_rn(0.5f, __fadd_rn(blo[a], bhi[a]));
+            float x = __fmul_rn(__fmul_rn(__fsub_rn(c, lo[a]), inv[a]), scale);
+            x = sel_min(sel_max(x, 0.0f), qmax);
+            q[a] = (uint32_t)x;
+        }
+        if (B == 10)
+            keys[i] = (K)((expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]));
+        else
+            keys[i] = (K)((expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]));
+    }
+}
+
+// ---- K3: onesweep radix sort ----------------------------------------------
+template <typename K, int PASSES>
+__global__ void __launch_bounds__(256) onesweep_hist_kernel(const K* __restrict__ keys, int64_t n,
+                                                           unsigned int* __restrict__ hist) {
+    __shared__ unsigned int s_hist[PASSES][RADIX];
+    for (int i = threadIdx.x; i < PASSES * RADIX; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        K k = keys[i];
+#pragma unroll
+        for (int p = 0; p < PASSES; ++p) atomicAdd(&s_hist[p][(unsigned)(k >> (8 * p)) & 0xFFu], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < PASSES * RADIX; i += blockDim.x) {
+        unsigned v = (&s_hist[0][0])[i];
+        if (v) atomicAdd(hist + i, v);
+    }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(SORT_THREADS) onesweep_pass_kernel(
+    const K* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, const unsigned int* __restrict__ hist,
+    unsigned int* status, unsigned int* counter) {
+    typedef cub::BlockScan<unsigned int, SORT_THREADS> Scan;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ unsigned int s_warp[SORT_THREADS / 32][RADIX];
+    __shared__ unsigned int s_base[RADIX];
+    __shared__ unsigned int s_tile;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = atomicAdd(counter, 1u);
+    for (int w = 0; w < SORT_THREADS / 32; ++w) s_warp[w][tid] = 0;
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const int64_t seg = (int64_t)tile * SORT_TILE + (int64_t)warp * (32 * SORT_ITEMS);
+
+    K key[SORT_ITEMS];
+    uint32_t val[SORT_ITEMS];
+    unsigned rank[SORT_ITEMS];
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < SORT_ITEMS; ++i) {
+        int64_t idx = seg + i * 32 + lane;
+        bool ok = idx < n;
+        key[i] = ok ? keys_in[idx] : (K)0;
+        val[i] = ok ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;
+        unsigned d = ok ? ((unsigned)(key[i] >> shift) & 0xFFu) : 0x100u;
+        unsigned peers = __match_any_sync(RT_FULL, d);
+        unsigned below = __popc(peers & lt_mask);
+        unsigned base = 0;
+        if (ok) base = s_warp[warp][d];
+        __syncwarp();
+        if (ok && below == 0) s_warp[warp][d] = base + __popc(peers);
+        __syncwarp();
+        rank[i] = base + below;
+    }
+    __syncthreads();
+    // per-digit warp prefixes and the tile count (thread == digit)
+    unsigned run = 0;
+#pragma unroll
+    for (int w = 0; w < SORT_THREADS / 32; ++w) {
+        unsigned c = s_warp[w][tid];
+        s_warp[w][tid] = run;
+        run += c;
+    }
+    const unsigned tile_count = run;
+    // publish aggregate, look back, publish inclusive prefix
+    unsigned* st = status + (size_t)tile * RADIX + tid;
+    unsigned excl = 0;
+    if (tile == 0) {
+        atomicExch(st, FLAG_INC | tile_count);
+    } else {
+        atomicExch(st, FLAG_AGG | tile_count);
+        int j = (int)tile - 1;
+        while (true) {
+            unsigned s = *((volatile unsigned*)(status + (size_t)j * RADIX + tid));
+            if ((s & ~VALUE_MASK) == 0) continue;
+            excl += s & VALUE_MASK;
+            if (s & FLAG_INC) break;
+            --j;
+        }
+        atomicExch(st, FLAG_INC | (excl + tile_count));
+    }
+    // global digit base = exclusive scan of the digit histogram + look-back prefix
+    unsigned bin_excl;
+    Scan(scan_tmp).ExclusiveSum(hist[tid], bin_excl);
+    s_base[tid] = bin_excl + excl;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < SORT_ITEMS; ++i) {
+        int64_t idx = seg + i * 32 + lane;
+        if (idx < n) {
+            unsigned d = (unsigned)(key[i] >> shift) & 0xFFu;
+            unsigned pos = s_base[d] + s_warp[warp][d] + rank[i];
+            keys_out[pos] = key[i];
+            vals_out[pos] = val[i];
+        }
+    }
+}
+
+// ---- K4: Karras split + leaf gather ---------------------------------------
+template <typename K>
+__device__ __forceinline__ int kdelta(const K* __restrict__ k, int64_t n, int64_t i, int64_t j, K ki) {
+    if (j < 0 || j > n - 1) return -1;
+    K kj = k[j];
+    if (ki != kj) return (sizeof(K) == 8) ? __clzll((unsigned long long)(ki ^ kj)) : __clz((unsigned)(ki ^ kj));
+    return (int)(8 * sizeof(K)) + __clz((unsigned)i ^ (unsigned)j);
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) karras_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
+                                                    const float* __restrict__ tris, const uint32_t* __restrict__ mask,
+                                                    int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
+                                                    float4* __restrict__ tri_sorted, float4* __restrict__ leaf_box,
+                                                    float4* __restrict__ nodes, unsigned int* __restrict__ flags) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    // leaf i: gather the triangle into leaf order, with its box
+    {
+        uint32_t id = order[i];
+        float t[9], lo[3], hi[3];
+        load_tri(tris, id, t);
+        tri_box(t, lo, hi);
+        tri_sorted[3 * i + 0] = make_float4(t[0], t[1], t[2], __int_as_float((int)id));
+        tri_sorted[3 * i + 1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask[id]));
+        tri_sorted[3 * i + 2] = make_float4(t[6], t[7], t[8], 0.0f);
+        leaf_box[2 * i + 0] = make_float4(lo[0], lo[1], lo[2], 0.0f);
+        leaf_box[2 * i + 1] = make_float4(hi[0], hi[1], hi[2], 0.0f);
+    }
+    if (i >= n - 1) return;
+    if (i == 0) parent[0] = -1;
+    flags[i] = 0;
+    K ki = keys[i];
+    int d = (kdelta(keys, n, i, i + 1, ki) - kdelta(keys, n, i, i - 1, ki)) >= 0 ? 1 : -1;
+    int dmin = kdelta(keys, n, i, i - d, ki);
+    int64_t lmax = 2;
+    while (kdelta(keys, n, i, i + lmax * d, ki) > dmin) lmax *= 2;
+    int64_t l = 0;
+    for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
+        if (kdelta(keys, n, i, i + (l + t) * d, ki) > dmin) l += t;
+    int64_t j = i + l * d;
+    int dnode = kdelta(keys, n, i, j, ki);
+    int64_t s = 0, t = l;
+    do {
+        t = (t + 1) >> 1;
+        if (kdelta(keys, n, i, i + (s + t) * d, ki) > dnode) s += t;
+    } while (t > 1);
+    int64_t gamma = i + s * d + (d < 0 ? d : 0);
+    int64_t lo = i < j ? i : j, hi = i < j ? j : i;
+    int left = (lo == gamma) ? ~(int)gamma : (int)gamma;
+    int right = (hi == gamma + 1) ? ~(int)(gamma + 1) : (int)(gamma + 1);
+    child[i] = make_int2(left, right);
+    parent[left < 0 ? (n - 1) + ~left : left] = (int32_t)i;
+    parent[right < 0 ? (n - 1) + ~right : right] = (int32_t)i;
+    nodes[4 * i + 3] = make_float4(__int_as_float(left), __int_as_float(right), 0.0f, 0.0f);
+}
+
+// ---- K5: bottom-up refit ---------------------------------------------------
+// node layout (Aila-Laine): n0 = (L.lo.x, L.hi.x, L.lo.y, L.hi.y)
+//                           n1 = (R.lo.x, R.hi.x, R.lo.y, R.hi.y)
+//                           n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
+//                           n3 = (left id, right id, height, 0)
+__device__ __forceinline__ void child_box(const float4* nodes, const float4* leaf_box, int c, float lo[3],
+                                          float hi[3], int& h) {
+    if (c < 0) {
+        float4 a = __ldcg(leaf_box + 2 * (~c)), b = __ldcg(leaf_box + 2 * (~c) + 1);
+        lo[0] = a.x; lo[1] = a.y; lo[2] = a.z;
+        hi[0] = b.x; hi[1] = b.y; hi[2] = b.z;
+        h = 0;
+    } else {
+        const float4* nd = nodes + 4 * c;
+        float4 n0 = __ldcg(nd), n1 = __ldcg(nd + 1), n2 = __ldcg(nd + 2), n3 = __ldcg(nd + 3);
+        lo[0] = sel_min(n0.x, n1.x); hi[0] = sel_max(n0.y, n1.y);
+        lo[1] = sel_min(n0.z, n1.z); hi[1] = sel_max(n0.w, n1.w);
+        lo[2] = sel_min(n2.x, n2.z); hi[2] = sel_max(n2.y, n2.w);
+        h = __float_as_int(n3.z);
+    }
+}
+
+__global__ void __launch_bounds__(256) refit_kernel(int64_t n, const int32_t* __restrict__ parent,
+                                                   const int2* __restrict__ child, const float4* leaf_box,
+                                                   float4* nodes, unsigned int* flags) {
+    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    int p = parent[(n - 1) + k];
+    while (p >= 0) {
+        __threadfence();
+        unsigned old = atomicAdd(flags + p, 1u);
+        if (old == 0) return;          // sibling subtree not finished yet
+        __threadfence();
+        int2 c = child[p];
+        float llo[3], lhi[3], rlo[3], rhi[3];
+        int hl, hr;
+        child_box(nodes, leaf_box, c.x, llo, lhi, hl);
+        child_box(nodes, leaf_box, c.y, rlo, rhi, hr);
+        float4* nd = nodes + 4 * p;
+        __stcg(nd + 0, make_float4(llo[0], lhi[0], llo[1], lhi[1]));
+        __stcg(nd + 1, make_float4(rlo[0], rhi[0], rlo[1], rhi[1]));
+        __stcg(nd + 2, make_float4(llo[2], lhi[2], rlo[2], rhi[2]));
+        __stcg(nd + 3, make_float4(__int_as_float(c.x), __int_as_float(c.y),
+                                   __int_as_float(1 + (hl > hr ? hl : hr)), 0.0f));
+        p = parent[p];
+    }
+}
+
+// n == 1: a root whose left child is leaf 0 and whose right box is empty
+__global__ void single_leaf_root(const float* tris, const uint32_t* mask, float4* nodes, float4* tri_sorted,
+                                 float4* leaf_box, uint32_t* order) {
+    float t[9], lo[3], hi[3];
+    load_tri(tris, 0, t);
+    tri_box(t, lo, hi);
+    order[0] = 0;
+    tri_sorted[0] = make_float4(t[0], t[1], t[2], __int_as_float(0));
+    tri_sorted[1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask[0]));
+    tri_sorted[2] = make_float4(t[6], t[7], t[8], 0.0f);
+    leaf_box[0] = make_float4(lo[0], lo[1], lo[2], 0.f);
+    leaf_box[1] = make_float4(hi[0], hi[1], hi[2], 0.f);
+    nodes[0] = make_float4(lo[0], hi[0], lo[1], hi[1]);
+    nodes[1] = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
+    nodes[2] = make_float4(lo[2], hi[2], INFINITY, -INFINITY);
+    nodes[3] = make_float4(__int_as_float(~0), __int_as_float(~0), __int_as_float(1), 0.0f);
+}
+
+template <typename K, int PASSES, int B>
+int build_typed(rt_ctx* ctx, rt_scene* s) {
+    const int64_t n = s->n;
+    cudaStream_t st = ctx->stream;
+    const int grid_stream = ctx->num_sms * 8;
+    // K1
+    // orderable-uint accumulators: min slots start at 0xFFFFFFFF, max slots at 0
+    RT_CUDA_TRY(cudaMemsetAsync(s->cb_enc, 0xFF, 3 * sizeof(unsigned int), st));
+    RT_CUDA_TRY(cudaMemsetAsync(s->cb_enc + 3, 0, 3 * sizeof(unsigned int), st));
+    int gb = (int)((n + 255) / 256);
+    if (gb > grid_stream) gb = grid_stream;
+    RT_PROF(ctx, 0);
+    lbvh_bounds_kernel<<<gb, 256, 0, st>>>(s->tris, n, s->cb_enc);
+    lbvh_bounds_finish<<<1, 32, 0, st>>>(s->cb_enc, s->cbounds);
+    // K2
+    K* ka = (K*)s->keys_a;
+    K* kb = (K*)s->keys_b;
+    RT_PROF(ctx, 1);
+    lbvh_morton_kernel<K, B><<<gb, 256, 0, st>>>(s->tris, n, s->cbounds, ka);
+    RT_PROF(ctx, 2);
+    // K3
+    const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+    unsigned int* hist = s->sort_scratch;                    // PASSES * 256
+    unsigned int* counters = hist + PASSES * RADIX;          // PASSES
+    unsigned int* status = counters + 32;                    // PASSES * tiles * 256
+    size_t words = (size_t)PASSES * RADIX + 32 + (size_t)PASSES * tiles * RADIX;
+    RT_CUDA_TRY(cudaMemsetAsync(s->sort_scratch, 0, words * sizeof(unsigned int), st));
+    onesweep_hist_kernel<K, PASSES><<<gb, 256, 0, st>>>(ka, n, hist);
+    K* kin = ka; K* kout = kb;
+    uint32_t* vin = nullptr; uint32_t* vout = s->vals_b;
+    RT_PROF(ctx, 3);
+    for (int p = 0; p < PASSES; ++p) {
+        onesweep_pass_kernel<K><<<(unsigned)tiles, SORT_THREADS, 0, st>>>(
+            kin, vin, kout, vout, n, 8 * p, hist + p * RADIX, status + (size_t)p * tiles * RADIX, counters + p);
+        K* tk = kin; kin = kout; kout = tk;
+        uint32_t* nv = (vout == s->vals_b) ? s->vals_a : s->vals_b;
+        vin = vout; vout = nv;
+    }
+    // PASSES is even: sorted keys in keys_a, values in vals_a
+    // K4 + K5
+    RT_PROF(ctx, 4);
+    karras_kernel<K><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kin, vin, s->tris, s->tri_mask, n, s->child,
+                                                                  s->parent, s->tri_sorted, s->leaf_box, s->nodes,
+                                                                  s->flags);
+    RT_PROF(ctx, 5);
+    refit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, s->parent, s->child, s->leaf_box, s->nodes,
+                                                               s->flags);
+    RT_PROF(ctx, 6);
+    RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}
+
+}  // namespace
+
+int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits) {
+    if (s->n == 1) {
+        single_leaf_root<<<1, 1, 0, ctx->stream>>>(s->tris, s->tri_mask, s->nodes, s->tri_sorted, s->leaf_box,
+                                                   s->vals_a);
+        RT_CUDA_TRY(cudaGetLastError());
+        return RT_OK;
+    }
+    if (bits == 30) return build_typed<uint32_t, 4, 10>(ctx, s);
+    return build_typed<uint64_t, 8, 21>(ctx, s);
+}
+
+size_t rt_sort_scratch_words(int64_t n) {
+    int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+    return (size_t)8 * RADIX + 32 + (size_t)8 * tiles * RADIX;
+}

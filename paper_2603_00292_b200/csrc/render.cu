@@ -1,0 +1,428 @@
+// render.cu -- K7 path-tracing megakernel and K8 wavefront path tracer
+// (replace _render_chunk / _sample_eye / _sample_pt, integrators.py:129-235, 334-379).
+//
+// Both variants run the SAME per-bounce device code (shade_bounce) in fp32 in
+// the reference's operation order, draw random numbers from the bit-exact
+// per-(seed, pixel, sample) PCG32 stream (2 jitter draws, then 2 per bounce,
+// integrators.py:345-351, 221-222) and accumulate each pixel in sample order,
+// so mega and wavefront frames are bit-identical and independent of scheduling.
+// World normals come per triangle from the host (reference-style);
+// the ONB uses copysignf (signed-zero sensitive, sampling.py:175-186).  This
+// TU must not be built with --use_fast_math.
+#include "traverse.cuh"
+
+namespace {
+
+constexpr int MEGA_THREADS = 128;
+constexpr int WF_THREADS = 256;
+
+struct FrameConst {
+    float cam[13];
+    float sky[3];
+    float bg[3];
+    float offset;
+    uint64_t seed;
+    int width, height, jitter, integ, max_depth;
+    int64_t pix_lo, npix;
+};
+
+struct PathState {
+    float ox, oy, oz, dx, dy, dz;
+    float tr, tg, tb, rr, rg, rb;
+    uint64_t state, inc;
+};
+
+__device__ __forceinline__ void cosine_dir(float x0, float x1, float& x, float& y, float& z) {
+    // sampling.py:144-151
+    float phi = 2.0f * 3.14159265358979323846f * x0;
+    float r = sqrtf(x1);
+    float sp, cp;
+    sincosf(phi, &sp, &cp);
+    x = cp * r;
+    z = sp * r;
+    y = sqrtf(fmaxf(1.0f - r * r, 0.0f));
+}
+
+__device__ __forceinline__ void onb(float nx, float ny, float nz, float t[3], float b[3]) {
+    // sampling.py:175-186 (copysign keeps the sign of a zero normal component)
+    float s = copysignf(1.0f, nz);
+    float a = -1.0f / (s + nz);
+    float bb = nx * ny * a;
+    t[0] = 1.0f + s * nx * nx * a;
+    t[1] = s * bb;
+    t[2] = -s * nx;
+    b[0] = bb;
+    b[1] = s + ny * ny * a;
+    b[2] = -ny;
+}
+
+// integrators.py:345-351 + camera.py:81-97: stream, jitter, primary ray
+__device__ __forceinline__ void start_path(const FrameConst& F, int64_t pix, int s, PathState& P) {
+    rt_stream_for(F.seed, (uint64_t)pix, (uint64_t)s, P.state, P.inc);
+    float ju = 0.0f, jv = 0.0f;
+    if (F.jitter) {
+        ju = rt_uniform(P.state, P.inc);
+        jv = rt_uniform(P.state, P.inc);
+    }
+    int xi = (int)(pix % F.width), yi = (int)(pix / F.width);
+    float u = ((float)xi + ju) / (float)F.width;
+    float v = ((float)yi + jv) / (float)F.height;
+    rt_primary_dir(F.cam, u, v, P.dx, P.dy, P.dz);
+    P.ox = F.cam[0]; P.oy = F.cam[1]; P.oz = F.cam[2];
+    P.tr = P.tg = P.tb = 1.0f;
+    P.rr = P.rg = P.rb = 0.0f;
+}
+
+// One closest-hit result applied to the path (integrators.py:129-141 eye,
+// 198-235 pt).  Returns true if the path continues with a new ray.
+__device__ __forceinline__ bool shade_bounce(const FrameConst& F, const float4* __restrict__ attr,
+                                             const float4* __restrict__ mat_color,
+                                             const float4* __restrict__ mat_emis, const HitRec& h, PathState& P) {
+    if (F.integ == RT_INTEG_EYE) {
+        if (h.id < 0) { P.rr = F.bg[0]; P.rg = F.bg[1]; P.rb = F.bg[2]; return false; }
+        int m = __float_as_int(__ldg(attr + h.id).w);
+        float4 c = __ldg(mat_color + m);
+        P.rr = c.x; P.rg = c.y; P.rb = c.z;
+        return false;
+    }
+    if (h.id < 0) {
+        P.rr += P.tr * F.sky[0]; P.rg += P.tg * F.sky[1]; P.rb += P.tb * F.sky[2];
+        return false;
+    }
+    float4 a = __ldg(attr + h.id);
+    int m = __float_as_int(a.w);
+    float4 e = __ldg(mat_emis + m);
+    if (e.x > 0.0f || e.y > 0.0f || e.z > 0.0f) {
+        P.rr += P.tr * e.x; P.rg += P.tg * e.y; P.rb += P.tb * e.z;
+        return false;
+    }
+    float nx = a.x, ny = a.y, nz = a.z;
+    if (nx * P.dx + ny * P.dy + nz * P.dz > 0.0f) { nx = -nx; ny = -ny; nz = -nz; }
+    float px = P.ox + P.dx * h.t, py = P.oy + P.dy * h.t, pz = P.oz + P.dz * h.t;
+    float x0 = rt_uniform(P.state, P.inc);
+    float x1 = rt_uniform(P.state, P.inc);
+    float sx, sy, sz;
+    cosine_dir(x0, x1, sx, sy, sz);
+    float t[3], b[3];
+    onb(nx, ny, nz, t, b);
+    P.dx = t[0] * sx + nx * sy + b[0] * sz;
+    P.dy = t[1] * sx + ny * sy + b[1] * sz;
+    P.dz = t[2] * sx + nz * sy + b[2] * sz;
+    float4 c = __ldg(mat_color + m);
+    P.tr *= c.x; P.tg *= c.y; P.tb *= c.z;
+    P.ox = px + nx * F.offset; P.oy = py + ny * F.offset; P.oz = pz + nz * F.offset;
+    return true;
+}
+
+// ---- K7: megakernel --------------------------------------------------------
+// Persistent warps fetch 32 pixels at a time; each lane renders samples
+// [s0, s1) of its pixel in order and adds the sums to accum once.
+__global__ void __launch_bounds__(MEGA_THREADS) pt_megakernel(
+    const FrameConst F, int s0, int s1, const float4* __restrict__ nodes, const float4* __restrict__ tris,
+    const float4* __restrict__ attr, const float4* __restrict__ mat_color, const float4* __restrict__ mat_emis,
+    float4* __restrict__ accum, unsigned int* counter, unsigned long long* ray_total, int* err) {
+    const int height = __float_as_int(__ldg(nodes + 3).z);
+    if (height + 1 > RT_STACK) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
+        return;
+    }
+    int stack[RT_STACK];
+    const int lane = threadIdx.x & 31;
+    unsigned long long rays = 0;
+    const int max_depth = F.integ == RT_INTEG_EYE ? 1 : F.max_depth;
+    while (true) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(counter, 32u);
+        base = __shfl_sync(RT_FULL, base, 0);
+        if ((int64_t)base >= F.npix) break;
+        int64_t i = (int64_t)base + lane;
+        if (i < F.npix) {
+            int64_t pix = F.pix_lo + i;
+            // accumulate sample by sample into the running sums, exactly like
+            // the wavefront's per-wave accumulate, so both are bit-identical
+            float4 a = accum[pix];
+            for (int s = s0; s < s1; ++s) {
+                PathState P;
+                start_path(F, pix, s, P);
+                for (int depth = 0; depth < max_depth; ++depth) {
+                    RayPre R;
+                    ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
+                    uint32_t nt, nv;
+                    HitRec h = trace_ray<false>(nodes, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+                    ++rays;
+                    if (!shade_bounce(F, attr, mat_color, mat_emis, h, P)) break;
+                }
+                a.x += P.rr; a.y += P.rg; a.z += P.rb; a.w += 1.0f;
+            }
+            accum[pix] = a;
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) rays += __shfl_xor_sync(RT_FULL, rays, off);
+    if (lane == 0 && rays) atomicAdd(ray_total, rays);
+}
+
+// ---- K8: wavefront ----------------------------------------------------------
+struct Wave {
+    float4* ray;      // (npix, 2)  o+tmin, d+tmax   (trace layout)
+    float4* thr;      // (npix)     throughput rgb
+    float4* rad;      // (npix)     radiance rgb
+    uint2* rng;       // (npix, 2)  state, inc
+    float4* hit;      // (npix)
+    int* queue[2];    // ping-pong path-index queues
+    unsigned int* count;   // [depth] live paths per depth (max_depth + 1)
+};
+
+__global__ void __launch_bounds__(WF_THREADS) wf_raygen(const FrameConst F, const int* __restrict__ d_sample,
+                                                         Wave W) {
+    const int s = *d_sample;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.npix; i += (int64_t)gridDim.x * blockDim.x) {
+        PathState P;
+        start_path(F, F.pix_lo + i, s, P);
+        W.ray[2 * i] = make_float4(P.ox, P.oy, P.oz, 0.0f);
+        W.ray[2 * i + 1] = make_float4(P.dx, P.dy, P.dz, 1e30f);
+        W.thr[i] = make_float4(1.f, 1.f, 1.f, 0.f);
+        W.rad[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        W.rng[2 * i] = make_uint2((unsigned)P.state, (unsigned)(P.state >> 32));
+        W.rng[2 * i + 1] = make_uint2((unsigned)P.inc, (unsigned)(P.inc >> 32));
+    }
+    if (blockIdx.x == 0 && threadIdx.x <= F.max_depth) W.count[threadIdx.x] = threadIdx.x == 0 ? (unsigned)F.npix : 0u;
+}
+
+// extend: closest hit for every queued path (depth 0: identity queue)
+__global__ void __launch_bounds__(128) wf_extend(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                                 Wave W, int depth, unsigned int* counter) {
+    int stack[RT_STACK];
+    const unsigned n = W.count[depth];
+    const int* q = depth == 0 ? nullptr : W.queue[depth & 1];
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(counter + depth, 32u);
+        base = __shfl_sync(RT_FULL, base, 0);
+        if (base >= n) break;
+        unsigned k = base + lane;
+        if (k < n) {
+            int i = q ? q[k] : (int)k;
+            float4 a = W.ray[2 * i], b = W.ray[2 * i + 1];
+            RayPre R;
+            ray_setup(R, a.x, a.y, a.z, b.x, b.y, b.z, a.w);
+            uint32_t nt, nv;
+            HitRec h = trace_ray<false>(nodes, tris, R, b.w, RT_FULL, stack, nt, nv);
+            W.hit[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
+        }
+    }
+}
+
+// shade: apply the hit, bounce, append survivors to the next queue with one
+// atomicAdd per warp (ballot + popc)
+__global__ void __launch_bounds__(WF_THREADS) wf_shade(const FrameConst F, const float4* __restrict__ attr,
+                                                        const float4* __restrict__ mat_color,
+                                                        const float4* __restrict__ mat_emis, Wave W, int depth) {
+    const unsigned n = W.count[depth];
+    const int* q = depth == 0 ? nullptr : W.queue[depth & 1];
+    int* qn = W.queue[(depth + 1) & 1];
+    const bool last = depth + 1 >= (F.integ == RT_INTEG_EYE ? 1 : F.max_depth);
+    const int lane = threadIdx.x & 31;
+    const unsigned stride = gridDim.x * blockDim.x;
+    for (unsigned k0 = blockIdx.x * blockDim.x; k0 < n; k0 += stride) {
+        unsigned k = k0 + threadIdx.x;
+        bool alive = false;
+        int i = -1;
+        if (k < n) {
+            i = q ? q[k] : (int)k;
+            float4 h4 = W.hit[i];
+            HitRec h;
+            h.t = h4.x; h.id = __float_as_int(h4.y); h.u = h4.z; h.v = h4.w;
+            float4 a = W.ray[2 * i], b = W.ray[2 * i + 1], tp = W.thr[i], rd = W.rad[i];
+            uint2 s0 = W.rng[2 * i], s1 = W.rng[2 * i + 1];
+            PathState P;
+            P.ox = a.x; P.oy = a.y; P.oz = a.z; P.dx = b.x; P.dy = b.y; P.dz = b.z;
+            P.tr = tp.x; P.tg = tp.y; P.tb = tp.z; P.rr = rd.x; P.rg = rd.y; P.rb = rd.z;
+            P.state = ((uint64_t)s0.y << 32) | s0.x;
+            P.inc = ((uint64_t)s1.y << 32) | s1.x;
+            bool cont = shade_bounce(F, attr, mat_color, mat_emis, h, P);
+            W.rad[i] = make_float4(P.rr, P.rg, P.rb, 0.f);
+            if (cont && !last) {
+                alive = true;
+                W.ray[2 * i] = make_float4(P.ox, P.oy, P.oz, 0.0f);
+                W.ray[2 * i + 1] = make_float4(P.dx, P.dy, P.dz, 1e30f);
+                W.thr[i] = make_float4(P.tr, P.tg, P.tb, 0.f);
+                W.rng[2 * i] = make_uint2((unsigned)P.state, (unsigned)(P.state >> 32));
+            }
+        }
+        unsigned ballot = __ballot_sync(RT_FULL, alive);
+        if (ballot) {
+            unsigned slot = 0;
+            if (lane == 0) slot = atomicAdd(W.count + depth + 1, __popc(ballot));
+            slot = __shfl_sync(RT_FULL, slot, 0);
+            if (alive) qn[slot + __popc(ballot & ((1u << lane) - 1u))] = i;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(WF_THREADS) wf_accumulate(const FrameConst F, Wave W, float4* __restrict__ accum,
+                                                             int* d_sample, unsigned int* counter,
+                                                             unsigned long long* ray_total) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.npix; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 r = W.rad[i];
+        float4 a = accum[F.pix_lo + i];
+        a.x += r.x; a.y += r.y; a.z += r.z; a.w += 1.0f;
+        accum[F.pix_lo + i] = a;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long total = 0;
+        int md = F.integ == RT_INTEG_EYE ? 1 : F.max_depth;
+        for (int d = 0; d < md; ++d) total += W.count[d];
+        *ray_total += total;
+        *d_sample += 1;
+        for (int d = 0; d <= md; ++d) counter[d] = 0;
+    }
+}
+
+__global__ void raygen_kernel(const FrameConst F, int s, float4* __restrict__ rays) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.npix; i += (int64_t)gridDim.x * blockDim.x) {
+        PathState P;
+        start_path(F, F.pix_lo + i, s, P);
+        rays[2 * i] = make_float4(P.ox, P.oy, P.oz, 0.0f);
+        rays[2 * i + 1] = make_float4(P.dx, P.dy, P.dz, 1e30f);
+    }
+}
+
+FrameConst make_frame(const rt_render_params* p) {
+    FrameConst F;
+    for (int k = 0; k < 13; ++k) F.cam[k] = p->cam[k];
+    for (int k = 0; k < 3; ++k) { F.sky[k] = p->sky[k]; F.bg[k] = p->background[k]; }
+    F.offset = p->normal_offset;
+    F.seed = p->seed;
+    F.width = p->width; F.height = p->height; F.jitter = p->jitter;
+    F.integ = p->integrator; F.max_depth = p->max_depth;
+    int64_t npix_total = (int64_t)p->width * p->height;
+    F.pix_lo = p->pix_lo;
+    int64_t hi = (p->pix_hi > 0) ? p->pix_hi : npix_total;
+    F.npix = hi - p->pix_lo;
+    return F;
+}
+
+// device scratch for the wavefront, grown on demand and owned by the scene
+struct WaveBuffers {
+    int64_t cap = 0;
+    void* mem = nullptr;
+    int* d_sample = nullptr;
+    unsigned long long* d_rays = nullptr;
+    Wave W;
+};
+
+}  // namespace
+
+// wavefront buffers per scene (keyed by scene pointer; single-threaded contexts)
+#include <map>
+static std::map<rt_scene*, WaveBuffers>& wave_map() {
+    static std::map<rt_scene*, WaveBuffers> m;
+    return m;
+}
+void rt_render_release(rt_scene* s) {
+    auto& m = wave_map();
+    auto it = m.find(s);
+    if (it != m.end()) {
+        cudaFree(it->second.mem);
+        m.erase(it);
+    }
+}
+
+static int ensure_wave(rt_scene* s, int64_t npix, WaveBuffers*& out) {
+    WaveBuffers& wb = wave_map()[s];
+    if (wb.cap < npix) {
+        if (wb.mem) cudaFree(wb.mem);
+        size_t per = 32 + 16 + 16 + 16 + 16 + 4 + 4;
+        size_t bytes = per * (size_t)npix + 64 * sizeof(unsigned) + 64;
+        RT_CUDA_TRY(cudaMalloc(&wb.mem, bytes));
+        char* p = (char*)wb.mem;
+        wb.W.ray = (float4*)p; p += 32 * (size_t)npix;
+        wb.W.thr = (float4*)p; p += 16 * (size_t)npix;
+        wb.W.rad = (float4*)p; p += 16 * (size_t)npix;
+        wb.W.rng = (uint2*)p; p += 16 * (size_t)npix;
+        wb.W.hit = (float4*)p; p += 16 * (size_t)npix;
+        wb.W.queue[0] = (int*)p; p += 4 * (size_t)npix;
+        wb.W.queue[1] = (int*)p; p += 4 * (size_t)npix;
+        wb.W.count = (unsigned int*)p; p += 32 * sizeof(unsigned);
+        wb.d_sample = (int*)p; p += 16;
+        wb.d_rays = (unsigned long long*)p; p += 16;
+        wb.cap = npix;
+    }
+    out = &wb;
+    return RT_OK;
+}
+
+int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out) {
+    FrameConst F = make_frame(p);
+    if (F.npix <= 0 || F.pix_lo < 0 || F.pix_lo + F.npix > (int64_t)p->width * p->height) return RT_EINVAL;
+    if (p->s1 <= p->s0) return RT_EINVAL;
+    if (F.npix > 0x7FFFFFF0ll) return RT_EINVAL;
+    cudaStream_t st = ctx->stream;
+    unsigned long long* d_rays = reinterpret_cast<unsigned long long*>(ctx->d_counter + 32);
+    RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, 64 * sizeof(unsigned int), st));
+    float4* acc = reinterpret_cast<float4*>(accum);
+    if (p->kernel == RT_KERNEL_MEGA) {
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pt_megakernel, MEGA_THREADS, 0);
+        if (bps < 1) bps = 1;
+        int64_t grid = (int64_t)ctx->num_sms * bps;
+        int64_t want = (F.npix + MEGA_THREADS - 1) / MEGA_THREADS;
+        if (grid > want) grid = want;
+        pt_megakernel<<<(unsigned)grid, MEGA_THREADS, 0, st>>>(F, p->s0, p->s1, s->nodes, s->tri_sorted, s->tri_attr,
+                                                               s->mat_color, s->mat_emissive, acc, ctx->d_counter,
+                                                               d_rays, ctx->d_error);
+        RT_CUDA_TRY(cudaGetLastError());
+    } else {
+        if (F.max_depth > 30) return RT_EINVAL;
+        WaveBuffers* wb;
+        int rc = ensure_wave(s, F.npix, wb);
+        if (rc) return rc;
+        RT_CUDA_TRY(cudaMemsetAsync(wb->d_sample, 0, 32, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(wb->d_sample, &p->s0, sizeof(int), cudaMemcpyHostToDevice, st));
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, wf_extend, 128, 0);
+        if (bps < 1) bps = 1;
+        unsigned grid_ext = (unsigned)(ctx->num_sms * bps);
+        unsigned grid_sh = (unsigned)ctx->num_sms * 8;
+        int md = F.integ == RT_INTEG_EYE ? 1 : F.max_depth;
+        // one wave (one sample index for every pixel) captured once as a CUDA graph
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        cudaStream_t cap;
+        RT_CUDA_TRY(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+        RT_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+        wf_raygen<<<grid_sh, WF_THREADS, 0, cap>>>(F, wb->d_sample, wb->W);
+        for (int d = 0; d < md; ++d) {
+            wf_extend<<<grid_ext, 128, 0, cap>>>(s->nodes, s->tri_sorted, wb->W, d, ctx->d_counter);
+            wf_shade<<<grid_sh, WF_THREADS, 0, cap>>>(F, s->tri_attr, s->mat_color, s->mat_emissive, wb->W, d);
+        }
+        wf_accumulate<<<grid_sh, WF_THREADS, 0, cap>>>(F, wb->W, acc, wb->d_sample, ctx->d_counter, d_rays);
+        cudaError_t ce = cudaStreamEndCapture(cap, &graph);
+        if (ce != cudaSuccess) { cudaStreamDestroy(cap); RT_CUDA_TRY(ce); }
+        ce = cudaGraphInstantiate(&exec, graph, 0);
+        if (ce != cudaSuccess) { cudaGraphDestroy(graph); cudaStreamDestroy(cap); RT_CUDA_TRY(ce); }
+        for (int smp = p->s0; smp < p->s1; ++smp) {
+            ce = cudaGraphLaunch(exec, st);
+            if (ce != cudaSuccess) break;
+        }
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+        cudaStreamDestroy(cap);
+        RT_CUDA_TRY(ce);
+        RT_CUDA_TRY(cudaGetLastError());
+    }
+    if (rays_out) {
+        RT_CUDA_TRY(cudaMemcpyAsync(rays_out, d_rays, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    return RT_OK;
+}
+
+int rt_raygen_impl(rt_ctx* ctx, const rt_render_params* p, int sample, float* rays) {
+    FrameConst F = make_frame(p);
+    raygen_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(F, sample, reinterpret_cast<float4*>(rays));
+    RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}

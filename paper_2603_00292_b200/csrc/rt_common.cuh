@@ -1,0 +1,166 @@
+// rt_common.cuh -- shared device helpers for librt_b200 (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rt_b200.h"
+
+#define RT_FULL 0xFFFFFFFFu
+#define RT_STACK 64                // traversal stack entries (== MAX_STACK_DEPTH, accel.py:44)
+#define RT_SENTINEL 0x7FFFFFFF     // bottom-of-stack marker (never a node or leaf id)
+
+// --------------------------------------------------------------------------
+// context / scene
+// --------------------------------------------------------------------------
+struct rt_ctx {
+    int device;
+    int num_sms;
+    cudaStream_t own_stream;
+    cudaStream_t stream;
+    cudaEvent_t ev0, ev1;
+    cudaEvent_t prof[8];           // stage events for rt_bvh_build_profiled
+    int profiling;
+    // pinned staging + device scratch for rt_closest_hit_host
+    void* h_stage;
+    size_t h_stage_bytes;
+    void* d_stage;
+    size_t d_stage_bytes;
+    unsigned int* d_counter;       // persistent-kernel work counters (64 slots)
+    int* d_error;                  // device-side error flag
+};
+
+struct rt_scene {
+    int64_t n;
+    int n_mat;
+    // inputs (resident)
+    float* tris;          // (n, 9) world vertices
+    float4* tri_attr;     // (n) normal.xyz, material id bits   (F9 normals)
+    int32_t* tri_inst;    // (n)
+    int32_t* tri_prim;    // (n)
+    uint32_t* tri_mask;   // (n)
+    float4* mat_color;    // (n_mat)
+    float4* mat_emissive; // (n_mat)
+    // LBVH
+    int built;
+    int bits;
+    float4* nodes;        // (max(n-1,1), 4) BVH2 nodes: child boxes + child ids + height
+    float4* tri_sorted;   // (n, 3) leaf-ordered vertices; v0.w = flat id, v1.w = mask
+    // build scratch
+    void* keys_a; void* keys_b;     // u32 or u64 Morton keys
+    uint32_t* vals_a; uint32_t* vals_b;
+    int32_t* parent;                // (2n-1)
+    int2* child;                    // (n-1)
+    unsigned int* flags;            // (n-1) refit arrival counters
+    float* cbounds;                 // 6 floats + 3 inv_ext (+pad)
+    unsigned int* cb_enc;           // 6 orderable-uint accumulators
+    unsigned int* sort_scratch;     // hist + counters + look-back status
+    size_t sort_scratch_words;
+    float4* leaf_box;               // (n, 2) lo, hi
+};
+
+// --------------------------------------------------------------------------
+// error plumbing
+// --------------------------------------------------------------------------
+void rt_set_error(const char* fmt, ...);
+#define RT_CUDA_TRY(expr)                                                        \
+    do {                                                                          \
+        cudaError_t _e = (expr);                                                  \
+        if (_e != cudaSuccess) {                                                  \
+            rt_set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e),  \
+                         __FILE__, __LINE__);                                     \
+            return RT_ECUDA;                                                      \
+        }                                                                         \
+    } while (0)
+
+// --------------------------------------------------------------------------
+// exact fp32 helpers (parity-critical paths use explicit selects, no FMNMX
+// NaN/zero-sign ambiguity, no FMA contraction)
+// --------------------------------------------------------------------------
+__device__ __forceinline__ float sel_min(float a, float b) { return b < a ? b : a; }
+__device__ __forceinline__ float sel_max(float a, float b) { return b > a ? b : a; }
+
+// orderable uint encoding of fp32 for atomicMin/atomicMax
+__device__ __forceinline__ unsigned int f2ord(float f) {
+    unsigned int u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ord2f(unsigned int u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7FFFFFFFu) : ~u);
+}
+
+// --------------------------------------------------------------------------
+// PCG32 + splitmix64 streams (sampling.py:38-79), bit-exact
+// --------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t rt_mix64(uint64_t z) {
+    z = z + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint32_t rt_pcg_next(uint64_t& state, uint64_t inc) {
+    uint64_t old = state;
+    state = old * 6364136223846793005ull + inc;
+    uint32_t xs = (uint32_t)(((old >> 18) ^ old) >> 27);
+    uint32_t rot = (uint32_t)(old >> 59);
+    return __funnelshift_r(xs, xs, rot);   // rotate right
+}
+__device__ __forceinline__ void rt_stream_for(uint64_t seed, uint64_t pix, uint64_t s, uint64_t& state,
+                                              uint64_t& inc) {
+    uint64_t h = rt_mix64(rt_mix64(rt_mix64(seed) ^ pix) ^ s);
+    inc = (rt_mix64(h ^ 0xDA3E39CB94B95BDBull) << 1) | 1ull;
+    state = 0;
+    rt_pcg_next(state, inc);
+    state += h;
+    rt_pcg_next(state, inc);
+}
+// u32 * 2^-32 in [0, 1): round toward zero so 2^32-1 never rounds up to 1.0f
+__device__ __forceinline__ float rt_uniform(uint64_t& state, uint64_t inc) {
+    return __uint2float_rz(rt_pcg_next(state, inc)) * 0x1p-32f;
+}
+
+// --------------------------------------------------------------------------
+// ray / hit records
+// --------------------------------------------------------------------------
+struct TraceRay {
+    float ox, oy, oz, tmin, dx, dy, dz, tmax;
+};
+
+__device__ __forceinline__ TraceRay load_ray(const float* rays, int64_t i) {
+    const float4* r = reinterpret_cast<const float4*>(rays) + 2 * i;
+    float4 a = __ldg(r), b = __ldg(r + 1);
+    TraceRay R;
+    R.ox = a.x; R.oy = a.y; R.oz = a.z; R.tmin = a.w;
+    R.dx = b.x; R.dy = b.y; R.dz = b.z; R.tmax = b.w;
+    return R;
+}
+
+// camera.py:81-97 in fp32.  cam = origin, right, up, forward, distortion
+__device__ __forceinline__ bool rt_primary_dir(const float* cam, float u, float v, float& dx, float& dy,
+                                               float& dz) {
+    float su = 2.0f * u - 1.0f, sv = 1.0f - 2.0f * v;
+    float px = cam[3] * su + cam[6] * sv;
+    float py = cam[4] * su + cam[7] * sv;
+    float pz = cam[5] * su + cam[8] * sv;
+    float c = cam[12] * (px * px + py * py + pz * pz);
+    float denom = 1.0f + c;
+    if (denom <= 0.0f) { dx = dy = dz = 0.0f; return false; }
+    dx = cam[9] + px / denom;
+    dy = cam[10] + py / denom;
+    dz = cam[11] + pz / denom;
+    float inv = 1.0f / sqrtf(dx * dx + dy * dy + dz * dz);
+    dx *= inv; dy *= inv; dz *= inv;
+    return true;
+}
+
+#define RT_PROF(ctx, k) do { if ((ctx)->profiling) cudaEventRecord((ctx)->prof[k], (ctx)->stream); } while (0)
+
+// host-side launch helpers (defined in capi.cu / lbvh.cu / trace.cu / render.cu)
+int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits);
+int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4* hits, uint32_t mask,
+                  uint32_t* stats);
+int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
+                       int64_t* prim, double* u, double* v, double* nrm);
+int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, const double* tmin,
+                     const double* tmax, float* rays);
+int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out);
+int rt_raygen_impl(rt_ctx* ctx, const rt_render_params* p, int sample, float* rays);

@@ -1,0 +1,114 @@
+// trace.cu -- K6: persistent-thread closest-hit kernel over a ray buffer, plus
+// the f64 <-> f32 packing kernels behind rt_closest_hit_host (the reference's
+// closest_hit_batch dtypes, accel.py:1128-1156).
+#include "traverse.cuh"
+
+namespace {
+
+constexpr int TRACE_THREADS = 128;
+
+// One warp fetches 32 rays at a time from a global counter (one atomicAdd per
+// warp), every lane runs the while-while traversal, then the warp fetches again.
+template <bool STATS>
+__global__ void __launch_bounds__(TRACE_THREADS) trace_closest_kernel(
+    const float4* __restrict__ nodes, const float4* __restrict__ tris, int64_t n, const float* __restrict__ rays,
+    float4* __restrict__ hits, uint32_t ray_mask, uint32_t* __restrict__ stats, unsigned int* counter,
+    int* err) {
+    const int height = __float_as_int(__ldg(nodes + 3).z);   // root height == stack bound
+    if (height + 1 > RT_STACK) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
+        return;
+    }
+    int stack[RT_STACK];
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(counter, 32u);
+        base = __shfl_sync(RT_FULL, base, 0);
+        if ((int64_t)base >= n) break;
+        int64_t i = (int64_t)base + lane;
+        if (i < n) {
+            TraceRay r = load_ray(rays, i);
+            RayPre R;
+            ray_setup(R, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
+            uint32_t nt = 0, nv = 0;
+            HitRec h = trace_ray<STATS>(nodes, tris, R, r.tmax, ray_mask, stack, nt, nv);
+            hits[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
+            if (STATS) reinterpret_cast<uint2*>(stats)[i] = make_uint2(nt, nv);
+        }
+    }
+}
+
+__global__ void pack_rays_f64(int64_t n, const double* __restrict__ o, const double* __restrict__ d,
+                              const double* __restrict__ tmin, const double* __restrict__ tmax,
+                              float4* __restrict__ rays) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        rays[2 * i] = make_float4((float)o[3 * i], (float)o[3 * i + 1], (float)o[3 * i + 2], (float)tmin[i]);
+        double tm = tmax[i];
+        rays[2 * i + 1] = make_float4((float)d[3 * i], (float)d[3 * i + 1], (float)d[3 * i + 2],
+                                      tm > 3.0e38 ? INFINITY : (float)tm);
+    }
+}
+
+// hit (t, id, u, v) -> the reference's per-ray outputs (float64 / int64),
+// world normal from the per-triangle reference-style normal
+__global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, const float4* __restrict__ attr,
+                                const int32_t* __restrict__ tri_inst, const int32_t* __restrict__ tri_prim,
+                                double* t, int64_t* inst, int64_t* prim, double* u, double* v, double* nrm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 h = hits[i];
+        int id = __float_as_int(h.y);
+        if (id < 0) {
+            t[i] = -1.0; inst[i] = -1; prim[i] = -1; u[i] = -1.0; v[i] = -1.0;
+            nrm[3 * i] = 0.0; nrm[3 * i + 1] = 0.0; nrm[3 * i + 2] = 0.0;
+        } else {
+            float4 a = attr[id];
+            t[i] = h.x; inst[i] = tri_inst[id]; prim[i] = tri_prim[id]; u[i] = h.z; v[i] = h.w;
+            nrm[3 * i] = a.x; nrm[3 * i + 1] = a.y; nrm[3 * i + 2] = a.z;
+        }
+    }
+}
+
+}  // namespace
+
+int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4* hits, uint32_t mask,
+                  uint32_t* stats) {
+    if (n <= 0) return RT_OK;
+    if ((n + 64) > 0xFFFFFFFFll) return RT_EINVAL;
+    cudaStream_t st = ctx->stream;
+    RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), st));
+    int blocks_per_sm = 0;
+    if (stats)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, trace_closest_kernel<true>, TRACE_THREADS, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, trace_closest_kernel<false>, TRACE_THREADS, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+    int64_t want = (n + TRACE_THREADS - 1) / TRACE_THREADS;
+    int64_t grid = (int64_t)ctx->num_sms * blocks_per_sm;
+    if (grid > want) grid = want;
+    if (stats)
+        trace_closest_kernel<true><<<(unsigned)grid, TRACE_THREADS, 0, st>>>(
+            s->nodes, s->tri_sorted, n, rays, hits, mask, stats, ctx->d_counter, ctx->d_error);
+    else
+        trace_closest_kernel<false><<<(unsigned)grid, TRACE_THREADS, 0, st>>>(
+            s->nodes, s->tri_sorted, n, rays, hits, mask, nullptr, ctx->d_counter, ctx->d_error);
+    RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}
+
+int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, const double* tmin,
+                     const double* tmax, float* rays) {
+    int grid = ctx->num_sms * 8;
+    pack_rays_f64<<<grid, 256, 0, ctx->stream>>>(n, o, d, tmin, tmax, reinterpret_cast<float4*>(rays));
+    RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}
+
+int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
+                       int64_t* prim, double* u, double* v, double* nrm) {
+    int grid = ctx->num_sms * 8;
+    expand_hits_f64<<<grid, 256, 0, ctx->stream>>>(n, hits, s->tri_attr, s->tri_inst, s->tri_prim, t, inst, prim,
+                                                    u, v, nrm);
+    RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}

@@ -1,0 +1,167 @@
+// traverse.cuh -- closest-hit BVH2 traversal, shared by the trace kernel (K6)
+// and the path-tracing kernels (K7/K8).
+//
+// Semantics kept from the reference (accel.py:575-653, 762-849; geometry.py:219-330):
+//   two-sided triangles, inclusive edges, t in [tmin, tmax] inclusive,
+//   u = weight of v1, v = weight of v2, ties -> lowest (instance, prim), i.e.
+//   the lowest flat triangle id, instance mask AND ray mask != 0.
+// Arithmetic is fp32: a watertight ray/triangle test (Woop, Benthin, Wald 2013)
+// with a double-precision fallback for exactly-zero edge functions, and a
+// conservative slab test (safe reciprocal, tfar widened by a few ulps, Ize 2013)
+// so that culling never drops a box whose triangle the test would accept.
+#pragma once
+#include "rt_common.cuh"
+
+struct RayPre {
+    float ox, oy, oz, tmin;
+    float ix, iy, iz;          // safe 1/d
+    float oix, oiy, oiz;       // o * (1/d)
+    // watertight shear: A' = M (v - o); rows of M
+    float m00, m01, m02, m10, m11, m12, m20, m21, m22;
+};
+
+__device__ __forceinline__ float safe_rcp(float d) {
+    const float eps = 1e-20f;
+    return 1.0f / (fabsf(d) > eps ? d : copysignf(eps, d));
+}
+
+__device__ __forceinline__ void ray_setup(RayPre& R, float ox, float oy, float oz, float dx, float dy, float dz,
+                                          float tmin) {
+    R.ox = ox; R.oy = oy; R.oz = oz; R.tmin = tmin;
+    R.ix = safe_rcp(dx); R.iy = safe_rcp(dy); R.iz = safe_rcp(dz);
+    R.oix = ox * R.ix; R.oiy = oy * R.iy; R.oiz = oz * R.iz;
+    // kz = argmax |d|, kx = (kz+1)%3, ky = (kx+1)%3; swap kx,ky if d[kz] < 0
+    float ax = fabsf(dx), ay = fabsf(dy), az = fabsf(dz);
+    int kz = (ax > ay) ? (ax > az ? 0 : 2) : (ay > az ? 1 : 2);
+    int kx = kz == 2 ? 0 : kz + 1;
+    int ky = kx == 2 ? 0 : kx + 1;
+    float dkz = kz == 0 ? dx : (kz == 1 ? dy : dz);
+    if (dkz < 0.0f) { int t = kx; kx = ky; ky = t; }
+    float dkx = kx == 0 ? dx : (kx == 1 ? dy : dz);
+    float dky = ky == 0 ? dx : (ky == 1 ? dy : dz);
+    float sz = 1.0f / dkz, sx = dkx * sz, sy = dky * sz;
+    // row x: e_kx - sx e_kz ; row y: e_ky - sy e_kz ; row z: sz e_kz
+    R.m00 = (kx == 0) ? 1.f : (kz == 0 ? -sx : 0.f);
+    R.m01 = (kx == 1) ? 1.f : (kz == 1 ? -sx : 0.f);
+    R.m02 = (kx == 2) ? 1.f : (kz == 2 ? -sx : 0.f);
+    R.m10 = (ky == 0) ? 1.f : (kz == 0 ? -sy : 0.f);
+    R.m11 = (ky == 1) ? 1.f : (kz == 1 ? -sy : 0.f);
+    R.m12 = (ky == 2) ? 1.f : (kz == 2 ? -sy : 0.f);
+    R.m20 = (kz == 0) ? sz : 0.f;
+    R.m21 = (kz == 1) ? sz : 0.f;
+    R.m22 = (kz == 2) ? sz : 0.f;
+}
+
+// slab test of one child box against [tmin, tmax]; returns entry distance or +inf on miss
+__device__ __forceinline__ float box_enter(const RayPre& R, float lox, float hix, float loy, float hiy, float loz,
+                                           float hiz, float tmax) {
+    float tx0 = fmaf(lox, R.ix, -R.oix), tx1 = fmaf(hix, R.ix, -R.oix);
+    float ty0 = fmaf(loy, R.iy, -R.oiy), ty1 = fmaf(hiy, R.iy, -R.oiy);
+    float tz0 = fmaf(loz, R.iz, -R.oiz), tz1 = fmaf(hiz, R.iz, -R.oiz);
+    float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), R.tmin));
+    float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
+    tf = tf * 1.0000005f + 1e-30f;
+    return (tn <= tf) ? tn : INFINITY;
+}
+
+__device__ __forceinline__ void shear(const RayPre& R, float vx, float vy, float vz, float& X, float& Y, float& Z) {
+    float ax = vx - R.ox, ay = vy - R.oy, az = vz - R.oz;
+    X = fmaf(R.m00, ax, fmaf(R.m01, ay, R.m02 * az));
+    Y = fmaf(R.m10, ax, fmaf(R.m11, ay, R.m12 * az));
+    Z = fmaf(R.m20, ax, fmaf(R.m21, ay, R.m22 * az));
+}
+
+// edge function without FMA contraction (exact antisymmetry between neighbours)
+__device__ __forceinline__ float edge_fn(float ax, float ay, float bx, float by) {
+    float e = __fsub_rn(__fmul_rn(ax, by), __fmul_rn(ay, bx));
+    if (e == 0.0f) e = (float)((double)ax * (double)by - (double)ay * (double)bx);
+    return e;
+}
+
+// watertight two-sided test; on success updates (t, id, u, v)
+__device__ __forceinline__ bool tri_test(const RayPre& R, const float4 a, const float4 b, const float4 c, float& best_t,
+                                         int& best_id, float& bu, float& bv) {
+    float Ax, Ay, Az, Bx, By, Bz, Cx, Cy, Cz;
+    shear(R, a.x, a.y, a.z, Ax, Ay, Az);
+    shear(R, b.x, b.y, b.z, Bx, By, Bz);
+    shear(R, c.x, c.y, c.z, Cx, Cy, Cz);
+    float U = edge_fn(Cx, Cy, Bx, By);    // Cx*By - Cy*Bx  -> weight of v0
+    float V = edge_fn(Ax, Ay, Cx, Cy);    // Ax*Cy - Ay*Cx  -> weight of v1
+    float W = edge_fn(Bx, By, Ax, Ay);    // Bx*Ay - By*Ax  -> weight of v2
+    if ((U < 0.f || V < 0.f || W < 0.f) && (U > 0.f || V > 0.f || W > 0.f)) return false;
+    float det = U + V + W;
+    if (det == 0.0f) return false;
+    float T = fmaf(U, Az, fmaf(V, Bz, W * Cz));
+    float rdet = 1.0f / det;
+    float t = T * rdet;
+    if (!(t >= R.tmin) || !(t <= best_t)) return false;
+    int id = __float_as_int(a.w);
+    if (t == best_t && id >= best_id) return false;
+    best_t = t;
+    best_id = id;
+    bu = V * rdet;
+    bv = W * rdet;
+    return true;
+}
+
+struct HitRec {
+    float t;
+    int id;
+    float u, v;
+};
+
+// Persistent-thread while-while traversal (Aila & Laine 2009) for ONE ray per
+// lane; the calling warp may be partially active.  nodes: BVH2 (4 float4 per
+// internal node), tris: leaf-ordered (3 float4 per leaf).  Returns id -1 on miss.
+template <bool STATS>
+__device__ __forceinline__ HitRec trace_ray(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+                                            const RayPre& R, float tmax, uint32_t ray_mask, int* stack,
+                                            uint32_t& n_tests, uint32_t& n_visits) {
+    HitRec h;
+    // id -1 = no hit yet: a hit at exactly t == tmax is rejected, as the
+    // reference's TLAS test (best_inst = -1, accel.py:815-817) rejects it
+    h.t = tmax; h.id = -1; h.u = 0.f; h.v = 0.f;
+    int sp = 0;
+    stack[0] = RT_SENTINEL;
+    int node = 0;        // root
+    int leaf = 0;        // pending leaf (< 0) or none (>= 0)
+    while (node != RT_SENTINEL) {
+        // inner loop 1: internal nodes, postponing the first leaf found
+        while ((unsigned)node < (unsigned)RT_SENTINEL) {
+            const float4* nd = nodes + 4 * node;
+            float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
+            if (STATS) ++n_visits;
+            float tl = box_enter(R, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, h.t);
+            float tr = box_enter(R, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, h.t);
+            bool hl = tl != INFINITY, hr = tr != INFINITY;
+            int cl = __float_as_int(n3.x), cr = __float_as_int(n3.y);
+            if (!hl && !hr) {
+                node = stack[sp--];
+            } else {
+                node = hl ? cl : cr;
+                if (hl && hr) {
+                    int far = cr;
+                    if (tr < tl) { far = cl; node = cr; }
+                    stack[++sp] = far;
+                }
+            }
+            if (node < 0 && leaf >= 0) {
+                leaf = node;
+                node = stack[sp--];
+            }
+            if (!__any_sync(__activemask(), leaf >= 0)) break;
+        }
+        // inner loop 2: leaves (one triangle each)
+        while (leaf < 0) {
+            int k = ~leaf;
+            const float4* tp = tris + 3 * k;
+            float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+            if (STATS) ++n_tests;
+            if (__float_as_uint(b.w) & ray_mask) tri_test(R, a, b, c, h.t, h.id, h.u, h.v);
+            leaf = node;
+            if (node < 0) node = stack[sp--];
+        }
+    }
+    if (h.id < 0) h.t = -1.0f;
+    return h;
+}

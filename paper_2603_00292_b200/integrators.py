@@ -1,0 +1,125 @@
+"""render_frame on the GPU (drop-in for integrators.py:426-473 of the reference).
+
+Same signature and validation as the reference plus three GPU knobs:
+``kernel`` ("mega" | "wavefront"), ``samples`` (a [s0, s1) window of GLOBAL
+sample indices, for the sample split across GPUs) and ``accum`` (a CUDA
+(H*W, 4) float32 tensor to accumulate into and keep on the device).  Eye and
+path tracing run on the GPU; "ao" and "pt-nee" need the any-hit kernel, a
+"next" item, and raise ValueError rather than falling back.
+"""
+
+import warnings
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from . import _native
+from ._native import RenderParams, check, lib, ptr
+from .scene_io import AccumBuffer
+
+INTEGRATORS = ("eye", "ao", "pt", "pt-nee")
+KERNELS = {"mega": _native.RT_KERNEL_MEGA, "wavefront": _native.RT_KERNEL_WAVEFRONT}
+
+
+@dataclass
+class IntegratorConfig:
+    """integrators.py:56-74."""
+
+    max_depth: int = 8
+    sky_color: Optional[np.ndarray] = None
+    ao_ray_count: int = 16
+    ao_max_length: float = 1e30
+    normal_offset: Optional[float] = None
+
+    def __post_init__(self):
+        if self.max_depth < 1:
+            raise ValueError("max_depth must be >= 1")
+        if self.ao_ray_count < 1:
+            raise ValueError("ao_ray_count must be >= 1")
+        if not (self.ao_max_length > 0.0):
+            raise ValueError("ao_max_length must be > 0")
+        if self.sky_color is not None:
+            self.sky_color = np.asarray(self.sky_color, dtype=np.float64).reshape(3)
+        if self.normal_offset is not None and not (self.normal_offset > 0.0):
+            raise ValueError("normal_offset must be > 0")
+
+
+def resolve_config(scene, cfg):
+    """integrators.py:405-413."""
+    cfg = IntegratorConfig() if cfg is None else cfg
+    sky = cfg.sky_color if cfg.sky_color is not None else scene.sky
+    off = cfg.normal_offset
+    if off is None:
+        diag = scene.diagonal()
+        off = 1e-4 * diag if diag > 0.0 else 1e-4
+    return cfg, np.asarray(sky, np.float64), float(off)
+
+
+def make_params(scene, width, height, s0, s1, integrator, seed, cfg, jitter, kernel="mega", pix_lo=0, pix_hi=0):
+    if integrator not in INTEGRATORS:
+        raise ValueError(f"unknown integrator {integrator!r}, expected one of {INTEGRATORS}")
+    if integrator == "pt-nee" and len(scene.lights) == 0:
+        warnings.warn("scene has no emissive triangles, falling back to plain path tracing")
+        integrator = "pt"
+    if integrator not in ("eye", "pt"):
+        raise ValueError(f"integrator {integrator!r} needs the GPU any-hit kernel (not built yet)")
+    if kernel not in KERNELS:
+        raise ValueError(f"unknown kernel {kernel!r}, expected one of {tuple(KERNELS)}")
+    cfg, sky, off = resolve_config(scene, cfg)
+    scene.camera.validate_distortion()
+    p = RenderParams()
+    p.width, p.height, p.s0, p.s1 = int(width), int(height), int(s0), int(s1)
+    p.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    p.jitter = 1 if jitter else 0
+    p.integrator = _native.RT_INTEG_EYE if integrator == "eye" else _native.RT_INTEG_PT
+    p.max_depth = int(cfg.max_depth)
+    p.kernel = KERNELS[kernel]
+    for k, x in enumerate(scene.camera.as_tuple()):
+        p.cam[k] = x
+    for k in range(3):
+        p.sky[k] = float(sky[k])
+        p.background[k] = float(scene.background[k])
+    p.normal_offset = off
+    p.pix_lo, p.pix_hi = int(pix_lo), int(pix_hi)
+    return p
+
+
+def render_into(scene, accum, width, height, spp=1, integrator="pt", seed=0, cfg=None, jitter=True,
+                kernel="mega", samples=None, pixels=None, count_rays=True):
+    """Device form: accumulate into a CUDA (H*W, 4) f32 tensor; returns the ray count (or None)."""
+    s0, s1 = (0, spp) if samples is None else samples
+    pix_lo, pix_hi = (0, 0) if pixels is None else pixels
+    p = make_params(scene, width, height, s0, s1, integrator, seed, cfg, jitter, kernel, pix_lo, pix_hi)
+    rays = np.zeros(1, np.uint64)
+    check(lib().rt_render(scene.tlas.ctx.handle, scene.tlas.handle, p, ptr(accum),
+                          ptr(rays) if count_rays else None))
+    return int(rays[0]) if count_rays else None
+
+
+def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt", seed: int = 0,
+                 workers: int = 1, cfg: Optional[IntegratorConfig] = None, jitter: bool = True,
+                 return_stats: bool = False, kernel: str = "mega", samples=None):
+    """Render a full frame into a fresh AccumBuffer (float64 host copy of the fp32 device sums)."""
+    import torch
+    if width < 1 or height < 1 or spp < 1:
+        raise ValueError("width, height, and spp must all be >= 1")
+    if workers < 1:
+        raise ValueError("workers must be >= 1")
+    dev = torch.device("cuda", scene.tlas.ctx.device)
+    acc = torch.zeros((height * width, 4), dtype=torch.float32, device=dev)
+    rays = render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples)
+    buf = AccumBuffer(width, height, acc.cpu().numpy().astype(np.float64).reshape(height, width, 4))
+    if return_stats:
+        return buf, {"rays": rays}
+    return buf
+
+
+def raygen(scene, width, height, sample=0, seed=0, jitter=True):
+    """Primary rays of one sample for every pixel, (W*H, 8) f32 on the device (parity helper)."""
+    import torch
+    p = make_params(scene, width, height, sample, sample + 1, "eye", seed, None, jitter)
+    rays = torch.empty((width * height, 8), dtype=torch.float32, device=torch.device("cuda", scene.tlas.ctx.device))
+    check(lib().rt_raygen(scene.tlas.ctx.handle, p, int(sample), ptr(rays)))
+    scene.tlas.ctx.sync()
+    return rays

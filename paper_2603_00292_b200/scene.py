@@ -1,0 +1,267 @@
+"""compile_scene on the GPU: flatten instances, upload, build the LBVH.
+
+Mirrors scene.py:79-141 of the reference (``compile_scene(desc, quality)`` ->
+``Scene``) with ``quality`` selecting the GPU LBVH ("lbvh30" default,
+"lbvh63"; the reference's "balanced"/"fast" SAH qualities map to lbvh30).
+Instances are flattened on the host into world-space fp32 triangles in
+(instance, prim) order, so the reference tie rule (lowest instance, then
+lowest prim; accel.py:629, 815-817) is "lowest flat id" on the device.  The
+per-triangle world normal is computed reference-style in float64 (local
+cross product and normalisation as in geometry.py:235-237, 274-275, then the
+inverse-transpose sum and renormalisation of accel.py:843-847) and only then
+rounded to fp32, which preserves the signed zeros the ONB depends on.
+"""
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._native import BuildError, RegistryError, check, lib, ptr
+from .camera import Camera
+from .frames import frame_to_matrix, invert_affine
+
+QUALITIES = {"lbvh30": 30, "lbvh63": 63, "balanced": 30, "fast": 30}
+
+
+@dataclass
+class LightTable:
+    """World-space emissive triangles (sampling.py:217-253); kept for NEE ("next")."""
+
+    v0: np.ndarray
+    v1: np.ndarray
+    v2: np.ndarray
+    normal: np.ndarray
+    emissive: np.ndarray
+    area: np.ndarray
+    instance: np.ndarray
+    prim: np.ndarray
+
+    def __len__(self):
+        return self.v0.shape[0]
+
+
+class GpuTlas:
+    """Device-resident flattened scene + LBVH (replaces Tlas/TlasBundle, accel.py:439-549)."""
+
+    def __init__(self, ctx, tris, normals, tri_inst, tri_prim, tri_mask, tri_material, mat_color,
+                 mat_emissive, bits=30, root_lo=None, root_hi=None, instances=None, inverses=None):
+        self.ctx = ctx
+        self.n = int(tris.shape[0])
+        self.bits = bits
+        self.tris = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
+        self.normals = np.ascontiguousarray(normals, np.float32).reshape(-1, 3)
+        self.tri_inst = np.ascontiguousarray(tri_inst, np.int32)
+        self.tri_prim = np.ascontiguousarray(tri_prim, np.int32)
+        self.tri_mask = np.ascontiguousarray(tri_mask, np.uint32)
+        self.tri_material = np.ascontiguousarray(tri_material, np.int32)
+        self.inverses = inverses
+        self.n_instances = instances
+        self.world_root = (root_lo, root_hi)
+        mc = np.ascontiguousarray(mat_color, np.float32).reshape(-1, 3)
+        me = np.ascontiguousarray(mat_emissive, np.float32).reshape(-1, 3)
+        h = ctypes.c_void_p()
+        check(lib().rt_scene_create(ctx.handle, self.n, ptr(self.tris), ptr(self.normals), ptr(self.tri_inst),
+                                    ptr(self.tri_prim), ptr(self.tri_mask), ptr(self.tri_material), ptr(mc),
+                                    ptr(me), mc.shape[0], ctypes.byref(h)))
+        self.handle = h
+        self.build_ms = None
+        self.build(bits)
+
+    def build(self, bits=None, timed=False):
+        """(Re)build the LBVH from the resident triangles; returns device ms if timed."""
+        bits = self.bits if bits is None else bits
+        ms = ctypes.c_float(-1.0)
+        check(lib().rt_bvh_build(self.ctx.handle, self.handle, bits, ctypes.byref(ms) if timed else None))
+        self.bits = bits
+        if timed:
+            self.build_ms = ms.value
+            return ms.value
+        return None
+
+    def refit(self, tris, bits=None):
+        """New world vertices for the same triangles (Blas.refit, accel.py:263-283): H2D + rebuild."""
+        tris = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
+        if tris.shape[0] != self.n:
+            raise ValueError(f"triangle count changed ({self.n} -> {tris.shape[0]})")
+        check(lib().rt_scene_set_vertices(self.ctx.handle, self.handle, ptr(tris)))
+        self.tris = tris
+        self.build(bits)
+
+    def build_profiled(self, bits=None):
+        """Rebuild with stage events; returns dict of device ms per stage."""
+        bits = self.bits if bits is None else bits
+        ms = np.zeros(6, np.float32)
+        check(lib().rt_bvh_build_profiled(self.ctx.handle, self.handle, bits, ptr(ms)))
+        self.bits = bits
+        return dict(zip(("bounds", "morton", "histogram", "radix_passes", "karras", "refit"), map(float, ms)))
+
+    def info(self):
+        root = np.empty(6, np.float32)
+        h = ctypes.c_int32()
+        ni = ctypes.c_int64()
+        check(lib().rt_bvh_info(self.ctx.handle, self.handle, ptr(root), ctypes.byref(h), ctypes.byref(ni)))
+        return {"root_box": root, "height": h.value, "n_internal": ni.value}
+
+    def download(self):
+        """Full LBVH for parity checks (same layout as oracle.lbvh_build)."""
+        n = self.n
+        m = max(n - 1, 0)
+        out = {"sorted_keys": np.empty(n, np.uint64), "order": np.empty(n, np.uint32),
+               "child": np.empty((m, 2), np.int32), "parent": np.empty(max(2 * n - 1, 1), np.int32),
+               "boxes": np.empty((m, 12), np.float32), "height": np.empty(m, np.int32),
+               "centroid_bounds": np.empty(6, np.float32), "inv_ext": np.empty(3, np.float32)}
+        check(lib().rt_bvh_download(self.ctx.handle, self.handle, ptr(out["sorted_keys"]), ptr(out["order"]),
+                                    ptr(out["child"]), ptr(out["parent"]), ptr(out["boxes"]), ptr(out["height"]),
+                                    ptr(out["centroid_bounds"]), ptr(out["inv_ext"]), None))
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and _native._lib is not None:
+                _native._lib.rt_scene_destroy(self.handle)
+        except Exception:
+            pass
+
+
+@dataclass
+class Scene:
+    """scene.py:30-48; ``tlas`` is device-backed."""
+
+    camera: Camera
+    tlas: GpuTlas
+    mat_color: np.ndarray
+    mat_emissive: np.ndarray
+    inst_material: np.ndarray
+    lights: LightTable
+    sky: np.ndarray
+    background: np.ndarray
+    root_box: tuple
+
+    def diagonal(self) -> float:
+        d = self.root_box[1] - self.root_box[0]
+        return math.sqrt(float(d @ d))
+
+
+def _local_normals(V, F):
+    """geometry.py:229-237, 274-275 per face, float64, reference operation order."""
+    a, b, c = V[F[:, 0]], V[F[:, 1]], V[F[:, 2]]
+    e0 = b - a
+    e1 = c - b
+    nx = e0[:, 1] * e1[:, 2] - e0[:, 2] * e1[:, 1]
+    ny = e0[:, 2] * e1[:, 0] - e0[:, 0] * e1[:, 2]
+    nz = e0[:, 0] * e1[:, 1] - e0[:, 1] * e1[:, 0]
+    with np.errstate(invalid="ignore", divide="ignore"):
+        nlen = np.sqrt(nx * nx + ny * ny + nz * nz)
+        return nx / nlen, ny / nlen, nz / nlen
+
+
+def _world_normals(inv, lnx, lny, lnz):
+    """accel.py:843-847: inverse-transpose sum, then multiply by 1/sqrt."""
+    wnx = inv[0, 0] * lnx + inv[1, 0] * lny + inv[2, 0] * lnz
+    wny = inv[0, 1] * lnx + inv[1, 1] * lny + inv[2, 1] * lnz
+    wnz = inv[0, 2] * lnx + inv[1, 2] * lny + inv[2, 2] * lnz
+    with np.errstate(invalid="ignore", divide="ignore"):
+        inv_len = 1.0 / np.sqrt(wnx * wnx + wny * wny + wnz * wnz)
+    return np.stack([wnx * inv_len, wny * inv_len, wnz * inv_len], axis=1)
+
+
+def _light_rows(desc, mats_index, inst_list):
+    """scene.py:58-76."""
+    rows = []
+    for i, (decl, m) in enumerate(inst_list):
+        mat = desc.materials[decl.material]
+        if not mat.has_emission:
+            continue
+        mesh = desc.meshes[decl.mesh]
+        world = mesh.vertices @ m[:, :3].T + m[:, 3]
+        for prim, (i0, i1, i2) in enumerate(mesh.faces):
+            w0, w1, w2 = world[i0], world[i1], world[i2]
+            n = np.cross(w1 - w0, w2 - w1)
+            nlen = math.sqrt(float(n @ n))
+            if nlen == 0.0:
+                continue
+            rows.append((w0, w1, w2, n / nlen, mat.emissive, 0.5 * nlen, i, prim))
+    if not rows:
+        z = np.zeros((0, 3))
+        return LightTable(z, z, z, z, z, np.zeros(0), np.zeros(0, np.int64), np.zeros(0, np.int64))
+    col = lambda k: np.array([r[k] for r in rows])
+    return LightTable(col(0).reshape(-1, 3), col(1).reshape(-1, 3), col(2).reshape(-1, 3), col(3).reshape(-1, 3),
+                      col(4).reshape(-1, 3), col(5), col(6).astype(np.int64), col(7).astype(np.int64))
+
+
+def compile_scene(desc, quality: str = "lbvh30", device: int = 0) -> Scene:
+    """Flatten + upload + LBVH build (scene.py:79-141 semantics, GPU backend)."""
+    if quality not in QUALITIES:
+        raise ValueError(f"unknown build quality {quality!r}, expected one of {tuple(QUALITIES)}")
+    if desc.spheres:
+        raise RegistryError("custom primitives (spheres) have no GPU intersector yet; "
+                            "the GPU path has no CPU fallback")
+    mat_names = list(desc.materials)
+    mat_index = {n: i for i, n in enumerate(mat_names)}
+    mat_color = np.array([desc.materials[n].color for n in mat_names]).reshape(-1, 3)
+    mat_emissive = np.array([desc.materials[n].emissive for n in mat_names]).reshape(-1, 3)
+    if not desc.instances:
+        raise BuildError("a scene needs at least one instance")
+
+    # per-mesh validation and local data (Blas.from_mesh, accel.py:223-236)
+    mesh_cache = {}
+    for name, mesh in desc.meshes.items():
+        V = np.ascontiguousarray(mesh.vertices, np.float64).reshape(-1, 3)
+        F = np.ascontiguousarray(mesh.faces, np.int64).reshape(-1, 3)
+        if F.shape[0] == 0:
+            raise BuildError("cannot build over zero primitives")
+        if F.min() < 0 or F.max() >= V.shape[0]:
+            raise BuildError("face index out of range")
+        tri = V[F]
+        lo, hi = tri.min(axis=1), tri.max(axis=1)
+        bad = ~np.isfinite(lo).all(axis=1) | ~np.isfinite(hi).all(axis=1)
+        if bad.any():
+            raise BuildError(f"non-finite bounds for primitive {int(np.argmax(bad))}")
+        mesh_cache[name] = (V, F, lo.min(axis=0), hi.max(axis=0), _local_normals(V, F))
+
+    tris, normals, t_inst, t_prim, t_mask, t_mat = [], [], [], [], [], []
+    inst_material, inst_list, inverses = [], [], []
+    wlo, whi = [], []
+    for i, decl in enumerate(desc.instances):
+        V, F, rlo, rhi, ln = mesh_cache[decl.mesh]
+        m = frame_to_matrix(decl.frame)
+        try:
+            inv = invert_affine(m)
+        except ValueError as exc:
+            raise BuildError(f"instance {i} frame is not invertible") from exc
+        inverses.append(inv)
+        inst_list.append((decl, m))
+        # world AABB of the 8 root-box corners (accel.py:459-469)
+        corners = np.array([[(rlo, rhi)[s & 1][0], (rlo, rhi)[(s >> 1) & 1][1], (rlo, rhi)[(s >> 2) & 1][2]]
+                            for s in range(8)])
+        pts = corners @ m[:, :3].T + m[:, 3]
+        wlo.append(pts.min(axis=0))
+        whi.append(pts.max(axis=0))
+        W = (m[0, 0] * V[:, 0:1] + m[0, 1] * V[:, 1:2] + m[0, 2] * V[:, 2:3] + m[0, 3],
+             m[1, 0] * V[:, 0:1] + m[1, 1] * V[:, 1:2] + m[1, 2] * V[:, 2:3] + m[1, 3],
+             m[2, 0] * V[:, 0:1] + m[2, 1] * V[:, 1:2] + m[2, 2] * V[:, 2:3] + m[2, 3])
+        Wv = np.concatenate(W, axis=1)
+        tris.append(Wv[F].reshape(-1, 9).astype(np.float32))
+        normals.append(_world_normals(inv, *ln).astype(np.float32))
+        nt = F.shape[0]
+        t_inst.append(np.full(nt, i, np.int32))
+        t_prim.append(np.arange(nt, dtype=np.int32))
+        t_mask.append(np.full(nt, decl.mask, np.uint32))
+        mi = mat_index[decl.material]
+        inst_material.append(mi)
+        t_mat.append(np.full(nt, mi, np.int32))
+    root_lo = np.min(np.array(wlo), axis=0)
+    root_hi = np.max(np.array(whi), axis=0)
+    ctx = _native.Context.get(device)
+    tlas = GpuTlas(ctx, np.concatenate(tris), np.concatenate(normals), np.concatenate(t_inst),
+                   np.concatenate(t_prim), np.concatenate(t_mask), np.concatenate(t_mat), mat_color, mat_emissive,
+                   bits=QUALITIES[quality], root_lo=root_lo, root_hi=root_hi, instances=len(desc.instances),
+                   inverses=np.array(inverses))
+    return Scene(camera=desc.camera, tlas=tlas, mat_color=mat_color, mat_emissive=mat_emissive,
+                 inst_material=np.array(inst_material, np.int64), lights=_light_rows(desc, mat_index, inst_list),
+                 sky=np.ascontiguousarray(desc.sky, np.float64), background=np.ascontiguousarray(desc.background,
+                                                                                                 np.float64),
+                 root_box=(root_lo, root_hi))
