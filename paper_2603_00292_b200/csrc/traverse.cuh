@@ -15,7 +15,6 @@
 struct RayPre {
     float ox, oy, oz, tmin;
     float ix, iy, iz;          // safe 1/d
-    float oix, oiy, oiz;       // o * (1/d)
     // watertight shear: A' = M (v - o); rows of M
     float m00, m01, m02, m10, m11, m12, m20, m21, m22;
 };
@@ -29,7 +28,6 @@ __device__ __forceinline__ void ray_setup(RayPre& R, float ox, float oy, float o
                                           float tmin) {
     R.ox = ox; R.oy = oy; R.oz = oz; R.tmin = tmin;
     R.ix = safe_rcp(dx); R.iy = safe_rcp(dy); R.iz = safe_rcp(dz);
-    R.oix = ox * R.ix; R.oiy = oy * R.iy; R.oiz = oz * R.iz;
     // kz = argmax |d|, kx = (kz+1)%3, ky = (kx+1)%3; swap kx,ky if d[kz] < 0
     float ax = fabsf(dx), ay = fabsf(dy), az = fabsf(dz);
     int kz = (ax > ay) ? (ax > az ? 0 : 2) : (ay > az ? 1 : 2);
@@ -55,12 +53,16 @@ __device__ __forceinline__ void ray_setup(RayPre& R, float ox, float oy, float o
 // slab test of one child box against [tmin, tmax]; returns entry distance or +inf on miss
 __device__ __forceinline__ float box_enter(const RayPre& R, float lox, float hix, float loy, float hiy, float loz,
                                            float hiz, float tmax) {
-    float tx0 = fmaf(lox, R.ix, -R.oix), tx1 = fmaf(hix, R.ix, -R.oix);
-    float ty0 = fmaf(loy, R.iy, -R.oiy), ty1 = fmaf(hiy, R.iy, -R.oiy);
-    float tz0 = fmaf(loz, R.iz, -R.oiz), tz1 = fmaf(hiz, R.iz, -R.oiz);
+    // (lo - o) * (1/d): each slab distance carries at most ~2 ulp of relative
+    // error, so widening tfar by a few ulp keeps the test conservative (Ize
+    // 2013).  The fma(lo, 1/d, -o/d) form is cheaper but its error scales with
+    // |o/d| rather than t and culls boxes the reference would enter.
+    float tx0 = __fmul_rn(__fsub_rn(lox, R.ox), R.ix), tx1 = __fmul_rn(__fsub_rn(hix, R.ox), R.ix);
+    float ty0 = __fmul_rn(__fsub_rn(loy, R.oy), R.iy), ty1 = __fmul_rn(__fsub_rn(hiy, R.oy), R.iy);
+    float tz0 = __fmul_rn(__fsub_rn(loz, R.oz), R.iz), tz1 = __fmul_rn(__fsub_rn(hiz, R.oz), R.iz);
     float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), R.tmin));
     float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
-    tf = tf * 1.0000005f + 1e-30f;
+    tf = tf * 1.0000008f + 1e-30f;
     return (tn <= tf) ? tn : INFINITY;
 }
 
