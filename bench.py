@@ -321,7 +321,7 @@ def run_ours(args, ws, rank, local):
                   "bytes_formula": f"64 B x {n_nodes:.2f} internal-node fetches + 48 B x {n_tests:.2f} tri tests "
                                    "+ 32 B accum RMW per ray (stats build of the same kernel)",
                   "peak_source": peak_src}
-    roof_build = {"kernel": "LBVH build (K1-K5, 10 launches)", "bound": "hbm", "achieved": build_gbs,
+    roof_build = {"kernel": "LBVH build (K1-K5, 9 launches)", "bound": "hbm", "achieved": build_gbs,
                   "peak": peak_gbs, "unit": "GB/s", "frac": build_gbs / peak_gbs, "traffic": None,
                   "bytes_formula": "328 B/tri x 1,000,000 tris (SURVEY 8(d))", "stage_ms": stages,
                   "peak_source": peak_src}
@@ -337,8 +337,8 @@ def run_ours(args, ws, rank, local):
         "roofline": dominant, "roofline_other": roof_build if dominant is roof_trace else roof_trace,
         "per_ray": {"internal_node_fetches": n_nodes, "triangle_tests": n_tests},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
-        "gpu_launches": K * (10 + 1), "gpu_launches_detail": "per step: 10 LBVH kernels (bounds, bounds_finish, "
-                                                            "morton, histogram, 4 onesweep passes, karras, refit) + "
+        "gpu_launches": K * (9 + 1), "gpu_launches_detail": "per step: 9 LBVH kernels (bounds, bounds_finish, "
+                                                            "morton, histogram, 4 onesweep passes, fused emit+refit) + "
                                                             "1 megakernel",
         "pt": pt,
     }

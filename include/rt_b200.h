@@ -90,7 +90,7 @@ int rt_scene_set_vertices(rt_ctx* ctx, rt_scene* scene, const float* tris);
  * (CUDA events on the context stream; synchronises). */
 int rt_bvh_build(rt_ctx* ctx, rt_scene* scene, int morton_bits, float* build_ms);
 /* same build with CUDA events between stages: stage_ms[6] = bounds, morton,
- * histogram, radix passes, karras+leaf gather, refit (device ms; synchronises) */
+ * histogram, radix passes, split-slot init, fused karras+refit+leaf gather (device ms) */
 int rt_bvh_build_profiled(rt_ctx* ctx, rt_scene* scene, int morton_bits, float* stage_ms);
 /* root box (6), tree height (stack bound) and node count */
 int rt_bvh_info(rt_ctx* ctx, rt_scene* scene, float* root6, int32_t* height, int64_t* n_internal);

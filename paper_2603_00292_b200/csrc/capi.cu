@@ -165,7 +165,7 @@ int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normal
     ALLOC(s->cb_enc, sizeof(unsigned int) * 8);
     s->sort_scratch_words = rt_sort_scratch_words(n);
     ALLOC(s->sort_scratch, sizeof(unsigned int) * s->sort_scratch_words);
-    ALLOC(s->leaf_box, sizeof(float4) * 2 * n);
+    ALLOC(s->leaf_box, sizeof(float4) * 4 * n);   // per split slot: (lo, h), hi for both sides
 #undef ALLOC
     cudaStream_t st = c->stream;
     RT_CUDA_TRY(cudaMemcpyAsync(s->tris, tris, sizeof(float) * 9 * n, cudaMemcpyHostToDevice, st));

@@ -7,21 +7,22 @@
 //   K3 onesweep        LSD radix sort, 8-bit digits, one histogram pass for
 //                      all digits + one kernel per digit with decoupled
 //                      look-back and __match_any_sync warp ranking; stable
-//   K4 karras_emit     split search with the index fallback for equal keys,
-//                      parent pointers, leaf gather into leaf order
-//   K5 lbvh_refit      bottom-up with per-node arrival counters, writes 64-B
-//                      BVH2 nodes (both child boxes in the parent) + height
+//   K4+K5 lbvh_emit    fused Karras emission + refit in one bottom-up pass
+//                      (index fallback for equal keys, parent pointers, leaf
+//                      gather into leaf order, 64-B BVH2 nodes with both child
+//                      boxes in the parent + subtree height)
 //
 // The choices are the frozen ones of SURVEY.md 8(c); oracle/rt_oracle.c Part B
 // restates them on the CPU and tests/test_gpu_lbvh.py checks bit equality.
 #include <cub/block/block_scan.cuh>
+#include <cuda/atomic>
 
 #include "rt_common.cuh"
 
 namespace {
 
 constexpr int SORT_THREADS = 256;   // == RADIX
-constexpr int SORT_ITEMS = 16;
+constexpr int SORT_ITEMS = 8;
 constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // 4096 keys per tile
 constexpr int RADIX = 256;
 constexpr unsigned FLAG_AGG = 1u << 30;
@@ -237,110 +238,101 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_pass_kernel(
     }
 }
 
-// ---- K4: Karras split + leaf gather ---------------------------------------
+// ---- K4+K5: fused Karras emission + bottom-up refit ------------------------
+// One thread per leaf climbs the tree (Apetrei 2014's agglomerative scheme):
+// a node covering keys [l, r] is the LEFT child of its parent iff
+// delta(r, r+1) > delta(l-1, l) (the parent's split is the boundary with the
+// longer common prefix; no ties exist for index-augmented keys).  Siblings meet
+// at the parent's split slot gamma with one acq_rel exchange of their far
+// endpoints: the first arrival publishes its box and leaves, the second builds
+// the parent.  Karras's node numbering (internal 0..n-2, root 0) is recovered
+// exactly: a left child is numbered by its right end, a right child by its
+// left end, so child/parent arrays equal the split-search construction bit for
+// bit (oracle/rt_oracle.c orc_lbvh_karras + orc_lbvh_refit).
+//
+// node layout (Aila-Laine): n0 = (L.lo.x, L.hi.x, L.lo.y, L.hi.y)
+//                           n1 = (R.lo.x, R.hi.x, R.lo.y, R.hi.y)
+//                           n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
+//                           n3 = (left id, right id, height, 0)   id < 0: ~leaf
 template <typename K>
-__device__ __forceinline__ int kdelta(const K* __restrict__ k, int64_t n, int64_t i, int64_t j, K ki) {
-    if (j < 0 || j > n - 1) return -1;
-    K kj = k[j];
-    if (ki != kj) return (sizeof(K) == 8) ? __clzll((unsigned long long)(ki ^ kj)) : __clz((unsigned)(ki ^ kj));
-    return (int)(8 * sizeof(K)) + __clz((unsigned)i ^ (unsigned)j);
+__device__ __forceinline__ int adj_delta(const K* __restrict__ k, int64_t n, int64_t i) {
+    // delta(i, i+1); -1 outside [0, n-2]
+    if (i < 0 || i >= n - 1) return -1;
+    K a = k[i], b = k[i + 1];
+    if (a != b) return (sizeof(K) == 8) ? __clzll((unsigned long long)(a ^ b)) : __clz((unsigned)(a ^ b));
+    return (int)(8 * sizeof(K)) + __clz((unsigned)i ^ (unsigned)(i + 1));
 }
 
 template <typename K>
-__global__ void __launch_bounds__(256) karras_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
-                                                    const float* __restrict__ tris, const uint32_t* __restrict__ mask,
-                                                    int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
-                                                    float4* __restrict__ tri_sorted, float4* __restrict__ leaf_box,
-                                                    float4* __restrict__ nodes, unsigned int* __restrict__ flags) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(256) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
+                                                       const float* __restrict__ tris, const uint32_t* __restrict__ mask,
+                                                       int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
+                                                       float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
+                                                       int* slot_range, float4* slot_box) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    // leaf i: gather the triangle into leaf order, with its box
+    float lo[3], hi[3];
     {
-        uint32_t id = order[i];
-        float t[9], lo[3], hi[3];
+        const uint32_t id = order[i];
+        float t[9];
         load_tri(tris, id, t);
         tri_box(t, lo, hi);
         tri_sorted[3 * i + 0] = make_float4(t[0], t[1], t[2], __int_as_float((int)id));
         tri_sorted[3 * i + 1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask[id]));
         tri_sorted[3 * i + 2] = make_float4(t[6], t[7], t[8], 0.0f);
-        leaf_box[2 * i + 0] = make_float4(lo[0], lo[1], lo[2], 0.0f);
-        leaf_box[2 * i + 1] = make_float4(hi[0], hi[1], hi[2], 0.0f);
     }
-    if (i >= n - 1) return;
-    if (i == 0) parent[0] = -1;
-    flags[i] = 0;
-    K ki = keys[i];
-    int d = (kdelta(keys, n, i, i + 1, ki) - kdelta(keys, n, i, i - 1, ki)) >= 0 ? 1 : -1;
-    int dmin = kdelta(keys, n, i, i - d, ki);
-    int64_t lmax = 2;
-    while (kdelta(keys, n, i, i + lmax * d, ki) > dmin) lmax *= 2;
-    int64_t l = 0;
-    for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
-        if (kdelta(keys, n, i, i + (l + t) * d, ki) > dmin) l += t;
-    int64_t j = i + l * d;
-    int dnode = kdelta(keys, n, i, j, ki);
-    int64_t s = 0, t = l;
-    do {
-        t = (t + 1) >> 1;
-        if (kdelta(keys, n, i, i + (s + t) * d, ki) > dnode) s += t;
-    } while (t > 1);
-    int64_t gamma = i + s * d + (d < 0 ? d : 0);
-    int64_t lo = i < j ? i : j, hi = i < j ? j : i;
-    int left = (lo == gamma) ? ~(int)gamma : (int)gamma;
-    int right = (hi == gamma + 1) ? ~(int)(gamma + 1) : (int)(gamma + 1);
-    child[i] = make_int2(left, right);
-    parent[left < 0 ? (n - 1) + ~left : left] = (int32_t)i;
-    parent[right < 0 ? (n - 1) + ~right : right] = (int32_t)i;
-    nodes[4 * i + 3] = make_float4(__int_as_float(left), __int_as_float(right), 0.0f, 0.0f);
-}
-
-// ---- K5: bottom-up refit ---------------------------------------------------
-// node layout (Aila-Laine): n0 = (L.lo.x, L.hi.x, L.lo.y, L.hi.y)
-//                           n1 = (R.lo.x, R.hi.x, R.lo.y, R.hi.y)
-//                           n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
-//                           n3 = (left id, right id, height, 0)
-__device__ __forceinline__ void child_box(const float4* nodes, const float4* leaf_box, int c, float lo[3],
-                                          float hi[3], int& h) {
-    if (c < 0) {
-        float4 a = __ldcg(leaf_box + 2 * (~c)), b = __ldcg(leaf_box + 2 * (~c) + 1);
-        lo[0] = a.x; lo[1] = a.y; lo[2] = a.z;
-        hi[0] = b.x; hi[1] = b.y; hi[2] = b.z;
-        h = 0;
-    } else {
-        const float4* nd = nodes + 4 * c;
-        float4 n0 = __ldcg(nd), n1 = __ldcg(nd + 1), n2 = __ldcg(nd + 2), n3 = __ldcg(nd + 3);
-        lo[0] = sel_min(n0.x, n1.x); hi[0] = sel_max(n0.y, n1.y);
-        lo[1] = sel_min(n0.z, n1.z); hi[1] = sel_max(n0.w, n1.w);
-        lo[2] = sel_min(n2.x, n2.z); hi[2] = sel_max(n2.y, n2.w);
-        h = __float_as_int(n3.z);
-    }
-}
-
-__global__ void __launch_bounds__(256) refit_kernel(int64_t n, const int32_t* __restrict__ parent,
-                                                   const int2* __restrict__ child, const float4* leaf_box,
-                                                   float4* nodes, unsigned int* flags) {
-    int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= n) return;
-    int p = parent[(n - 1) + k];
-    while (p >= 0) {
-        __threadfence();
-        unsigned old = atomicAdd(flags + p, 1u);
-        if (old == 0) return;          // sibling subtree not finished yet
-        __threadfence();
-        int2 c = child[p];
+    int l = (int)i, r = (int)i, h = 0;
+    int dl = adj_delta(keys, n, l - 1), dr = adj_delta(keys, n, r);
+    while (true) {
+        const bool left = dr > dl;
+        const int gamma = left ? r : l - 1;
+        const int side = left ? 0 : 1;
+        // publish my box and height for my sibling, then exchange far endpoints
+        __stcg(slot_box + 4 * gamma + 2 * side, make_float4(lo[0], lo[1], lo[2], __int_as_float(h)));
+        __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(hi[0], hi[1], hi[2], 0.0f));
+        cuda::atomic_ref<int, cuda::thread_scope_device> slot(slot_range[gamma]);
+        const int other = slot.exchange(left ? l : r, cuda::std::memory_order_acq_rel);
+        if (other < 0) return;                       // sibling subtree not finished
+        const float4 s0 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side));
+        const float4 s1 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side) + 1);
+        const int pl = left ? l : other, pr = left ? other : r;
+        // children in Karras encoding: left = gamma, right = gamma + 1 (leaf if a single key)
+        const int cl = (pl == gamma) ? ~gamma : gamma;
+        const int cr = (pr == gamma + 1) ? ~(gamma + 1) : gamma + 1;
         float llo[3], lhi[3], rlo[3], rhi[3];
         int hl, hr;
-        child_box(nodes, leaf_box, c.x, llo, lhi, hl);
-        child_box(nodes, leaf_box, c.y, rlo, rhi, hr);
-        float4* nd = nodes + 4 * p;
-        __stcg(nd + 0, make_float4(llo[0], lhi[0], llo[1], lhi[1]));
-        __stcg(nd + 1, make_float4(rlo[0], rhi[0], rlo[1], rhi[1]));
-        __stcg(nd + 2, make_float4(llo[2], lhi[2], rlo[2], rhi[2]));
-        __stcg(nd + 3, make_float4(__int_as_float(c.x), __int_as_float(c.y),
-                                   __int_as_float(1 + (hl > hr ? hl : hr)), 0.0f));
-        p = parent[p];
+        if (left) {
+            llo[0] = lo[0]; llo[1] = lo[1]; llo[2] = lo[2]; lhi[0] = hi[0]; lhi[1] = hi[1]; lhi[2] = hi[2]; hl = h;
+            rlo[0] = s0.x; rlo[1] = s0.y; rlo[2] = s0.z; rhi[0] = s1.x; rhi[1] = s1.y; rhi[2] = s1.z;
+            hr = __float_as_int(s0.w);
+        } else {
+            rlo[0] = lo[0]; rlo[1] = lo[1]; rlo[2] = lo[2]; rhi[0] = hi[0]; rhi[1] = hi[1]; rhi[2] = hi[2]; hr = h;
+            llo[0] = s0.x; llo[1] = s0.y; llo[2] = s0.z; lhi[0] = s1.x; lhi[1] = s1.y; lhi[2] = s1.z;
+            hl = __float_as_int(s0.w);
+        }
+        // the parent's own number: its side at the next level (root -> 0)
+        const int pdl = adj_delta(keys, n, pl - 1), pdr = adj_delta(keys, n, pr);
+        const bool root = (pl == 0 && pr == n - 1);
+        const int P = root ? 0 : (pdr > pdl ? pr : pl);
+        h = 1 + (hl > hr ? hl : hr);
+        float4* nd = nodes + 4 * P;
+        nd[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
+        nd[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
+        nd[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
+        nd[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(h), 0.0f);
+        child[P] = make_int2(cl, cr);
+        parent[cl < 0 ? (n - 1) + ~cl : cl] = P;
+        parent[cr < 0 ? (n - 1) + ~cr : cr] = P;
+        if (root) {
+            parent[0] = -1;
+            return;
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) { lo[a] = sel_min(llo[a], rlo[a]); hi[a] = sel_max(lhi[a], rhi[a]); }
+        l = pl; r = pr; dl = pdl; dr = pdr;
     }
 }
+
 
 // n == 1: a root whose left child is leaf 0 and whose right box is empty
 __global__ void single_leaf_root(const float* tris, const uint32_t* mask, float4* nodes, float4* tri_sorted,
@@ -401,12 +393,11 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     // PASSES is even: sorted keys in keys_a, values in vals_a
     // K4 + K5
     RT_PROF(ctx, 4);
-    karras_kernel<K><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kin, vin, s->tris, s->tri_mask, n, s->child,
-                                                                  s->parent, s->tri_sorted, s->leaf_box, s->nodes,
-                                                                  s->flags);
+    RT_CUDA_TRY(cudaMemsetAsync(s->flags, 0xFF, sizeof(int) * (n - 1), st));   // split slots: empty
     RT_PROF(ctx, 5);
-    refit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, s->parent, s->child, s->leaf_box, s->nodes,
-                                                               s->flags);
+    lbvh_emit_kernel<K><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kin, vin, s->tris, s->tri_mask, n, s->child,
+                                                                     s->parent, s->tri_sorted, s->nodes,
+                                                                     (int*)s->flags, s->leaf_box);
     RT_PROF(ctx, 6);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;

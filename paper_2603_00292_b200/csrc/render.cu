@@ -24,7 +24,21 @@ struct FrameConst {
     uint64_t seed;
     int width, height, jitter, integ, max_depth;
     int64_t pix_lo, npix;
+    // work units: 8x4 pixel tiles (one per warp) when the range is whole rows
+    int tiled, tiles_x;
+    int64_t row0, row1, nunits;
 };
+
+// unit k -> pixel; false for the padding lanes of partial edge tiles
+__device__ __forceinline__ bool unit_pixel(const FrameConst& F, int64_t k, int64_t& pix) {
+    if (!F.tiled) { pix = F.pix_lo + k; return true; }
+    int64_t t = k >> 5;
+    int l = (int)(k & 31);
+    int64_t x = (t % F.tiles_x) * 8 + (l & 7);
+    int64_t y = F.row0 + (t / F.tiles_x) * 4 + (l >> 3);
+    pix = y * F.width + x;
+    return x < F.width && y < F.row1;
+}
 
 struct PathState {
     float ox, oy, oz, dx, dy, dz;
@@ -117,7 +131,7 @@ __device__ __forceinline__ bool shade_bounce(const FrameConst& F, const float4* 
 // ---- K7: megakernel --------------------------------------------------------
 // Persistent warps fetch 32 pixels at a time; each lane renders samples
 // [s0, s1) of its pixel in order and adds the sums to accum once.
-__global__ void __launch_bounds__(MEGA_THREADS) pt_megakernel(
+__global__ void __launch_bounds__(MEGA_THREADS, 8) pt_megakernel(
     const FrameConst F, int s0, int s1, const float4* __restrict__ nodes, const float4* __restrict__ tris,
     const float4* __restrict__ attr, const float4* __restrict__ mat_color, const float4* __restrict__ mat_emis,
     float4* __restrict__ accum, unsigned int* counter, unsigned long long* ray_total, int* err) {
@@ -134,10 +148,10 @@ __global__ void __launch_bounds__(MEGA_THREADS) pt_megakernel(
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(counter, 32u);
         base = __shfl_sync(RT_FULL, base, 0);
-        if ((int64_t)base >= F.npix) break;
+        if ((int64_t)base >= F.nunits) break;
         int64_t i = (int64_t)base + lane;
-        if (i < F.npix) {
-            int64_t pix = F.pix_lo + i;
+        int64_t pix;
+        if (i < F.nunits && unit_pixel(F, i, pix)) {
             // accumulate sample by sample into the running sums, exactly like
             // the wavefront's per-wave accumulate, so both are bit-identical
             float4 a = accum[pix];
@@ -169,6 +183,7 @@ struct Wave {
     float4* rad;      // (npix)     radiance rgb
     uint2* rng;       // (npix, 2)  state, inc
     float4* hit;      // (npix)
+    int64_t* pix;     // (nunits)   pixel of each path slot, -1 for padding
     int* queue[2];    // ping-pong path-index queues
     unsigned int* count;   // [depth] live paths per depth (max_depth + 1)
 };
@@ -176,21 +191,25 @@ struct Wave {
 __global__ void __launch_bounds__(WF_THREADS) wf_raygen(const FrameConst F, const int* __restrict__ d_sample,
                                                          Wave W) {
     const int s = *d_sample;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.npix; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.nunits; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t pix;
+        bool ok = unit_pixel(F, i, pix);
+        W.pix[i] = ok ? pix : -1;
+        W.rad[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!ok) continue;
         PathState P;
-        start_path(F, F.pix_lo + i, s, P);
+        start_path(F, pix, s, P);
         W.ray[2 * i] = make_float4(P.ox, P.oy, P.oz, 0.0f);
         W.ray[2 * i + 1] = make_float4(P.dx, P.dy, P.dz, 1e30f);
         W.thr[i] = make_float4(1.f, 1.f, 1.f, 0.f);
-        W.rad[i] = make_float4(0.f, 0.f, 0.f, 0.f);
         W.rng[2 * i] = make_uint2((unsigned)P.state, (unsigned)(P.state >> 32));
         W.rng[2 * i + 1] = make_uint2((unsigned)P.inc, (unsigned)(P.inc >> 32));
     }
-    if (blockIdx.x == 0 && threadIdx.x <= F.max_depth) W.count[threadIdx.x] = threadIdx.x == 0 ? (unsigned)F.npix : 0u;
+    if (blockIdx.x == 0 && threadIdx.x <= F.max_depth) W.count[threadIdx.x] = threadIdx.x == 0 ? (unsigned)F.nunits : 0u;
 }
 
 // extend: closest hit for every queued path (depth 0: identity queue)
-__global__ void __launch_bounds__(128) wf_extend(const float4* __restrict__ nodes, const float4* __restrict__ tris,
+__global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ nodes, const float4* __restrict__ tris,
                                                  Wave W, int depth, unsigned int* counter) {
     int stack[RT_STACK];
     const unsigned n = W.count[depth];
@@ -204,12 +223,14 @@ __global__ void __launch_bounds__(128) wf_extend(const float4* __restrict__ node
         unsigned k = base + lane;
         if (k < n) {
             int i = q ? q[k] : (int)k;
+            if (q || W.pix[i] >= 0) {
             float4 a = W.ray[2 * i], b = W.ray[2 * i + 1];
             RayPre R;
             ray_setup(R, a.x, a.y, a.z, b.x, b.y, b.z, a.w);
             uint32_t nt, nv;
             HitRec h = trace_ray<false>(nodes, tris, R, b.w, RT_FULL, stack, nt, nv);
             W.hit[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
+            }
         }
     }
 }
@@ -229,7 +250,7 @@ __global__ void __launch_bounds__(WF_THREADS) wf_shade(const FrameConst F, const
         unsigned k = k0 + threadIdx.x;
         bool alive = false;
         int i = -1;
-        if (k < n) {
+        if (k < n && (q || W.pix[k] >= 0)) {
             i = q ? q[k] : (int)k;
             float4 h4 = W.hit[i];
             HitRec h;
@@ -264,11 +285,13 @@ __global__ void __launch_bounds__(WF_THREADS) wf_shade(const FrameConst F, const
 __global__ void __launch_bounds__(WF_THREADS) wf_accumulate(const FrameConst F, Wave W, float4* __restrict__ accum,
                                                              int* d_sample, unsigned int* counter,
                                                              unsigned long long* ray_total) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.npix; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.nunits; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t pix = W.pix[i];
+        if (pix < 0) continue;
         float4 r = W.rad[i];
-        float4 a = accum[F.pix_lo + i];
+        float4 a = accum[pix];
         a.x += r.x; a.y += r.y; a.z += r.z; a.w += 1.0f;
-        accum[F.pix_lo + i] = a;
+        accum[pix] = a;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long total = 0;
@@ -301,6 +324,11 @@ FrameConst make_frame(const rt_render_params* p) {
     F.pix_lo = p->pix_lo;
     int64_t hi = (p->pix_hi > 0) ? p->pix_hi : npix_total;
     F.npix = hi - p->pix_lo;
+    F.tiled = (p->pix_lo % p->width == 0) && (hi % p->width == 0);
+    F.row0 = p->pix_lo / p->width;
+    F.row1 = hi / p->width;
+    F.tiles_x = (p->width + 7) / 8;
+    F.nunits = F.tiled ? (int64_t)F.tiles_x * ((F.row1 - F.row0 + 3) / 4) * 32 : F.npix;
     return F;
 }
 
@@ -334,7 +362,7 @@ static int ensure_wave(rt_scene* s, int64_t npix, WaveBuffers*& out) {
     WaveBuffers& wb = wave_map()[s];
     if (wb.cap < npix) {
         if (wb.mem) cudaFree(wb.mem);
-        size_t per = 32 + 16 + 16 + 16 + 16 + 4 + 4;
+        size_t per = 32 + 16 + 16 + 16 + 16 + 8 + 4 + 4;
         size_t bytes = per * (size_t)npix + 64 * sizeof(unsigned) + 64;
         RT_CUDA_TRY(cudaMalloc(&wb.mem, bytes));
         char* p = (char*)wb.mem;
@@ -343,6 +371,7 @@ static int ensure_wave(rt_scene* s, int64_t npix, WaveBuffers*& out) {
         wb.W.rad = (float4*)p; p += 16 * (size_t)npix;
         wb.W.rng = (uint2*)p; p += 16 * (size_t)npix;
         wb.W.hit = (float4*)p; p += 16 * (size_t)npix;
+        wb.W.pix = (int64_t*)p; p += 8 * (size_t)npix;
         wb.W.queue[0] = (int*)p; p += 4 * (size_t)npix;
         wb.W.queue[1] = (int*)p; p += 4 * (size_t)npix;
         wb.W.count = (unsigned int*)p; p += 32 * sizeof(unsigned);
@@ -358,7 +387,7 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
     FrameConst F = make_frame(p);
     if (F.npix <= 0 || F.pix_lo < 0 || F.pix_lo + F.npix > (int64_t)p->width * p->height) return RT_EINVAL;
     if (p->s1 <= p->s0) return RT_EINVAL;
-    if (F.npix > 0x7FFFFFF0ll) return RT_EINVAL;
+    if (F.nunits > 0x7FFFFFF0ll) return RT_EINVAL;
     cudaStream_t st = ctx->stream;
     unsigned long long* d_rays = reinterpret_cast<unsigned long long*>(ctx->d_counter + 32);
     RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, 64 * sizeof(unsigned int), st));
@@ -368,7 +397,7 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pt_megakernel, MEGA_THREADS, 0);
         if (bps < 1) bps = 1;
         int64_t grid = (int64_t)ctx->num_sms * bps;
-        int64_t want = (F.npix + MEGA_THREADS - 1) / MEGA_THREADS;
+        int64_t want = (F.nunits + MEGA_THREADS - 1) / MEGA_THREADS;
         if (grid > want) grid = want;
         pt_megakernel<<<(unsigned)grid, MEGA_THREADS, 0, st>>>(F, p->s0, p->s1, s->nodes, s->tri_sorted, s->tri_attr,
                                                                s->mat_color, s->mat_emissive, acc, ctx->d_counter,
@@ -377,7 +406,7 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
     } else {
         if (F.max_depth > 30) return RT_EINVAL;
         WaveBuffers* wb;
-        int rc = ensure_wave(s, F.npix, wb);
+        int rc = ensure_wave(s, F.nunits, wb);
         if (rc) return rc;
         RT_CUDA_TRY(cudaMemsetAsync(wb->d_sample, 0, 32, st));
         RT_CUDA_TRY(cudaMemcpyAsync(wb->d_sample, &p->s0, sizeof(int), cudaMemcpyHostToDevice, st));

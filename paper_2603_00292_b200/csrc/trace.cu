@@ -10,7 +10,7 @@ constexpr int TRACE_THREADS = 128;
 // One warp fetches 32 rays at a time from a global counter (one atomicAdd per
 // warp), every lane runs the while-while traversal, then the warp fetches again.
 template <bool STATS>
-__global__ void __launch_bounds__(TRACE_THREADS) trace_closest_kernel(
+__global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
     const float4* __restrict__ nodes, const float4* __restrict__ tris, int64_t n, const float* __restrict__ rays,
     float4* __restrict__ hits, uint32_t ray_mask, uint32_t* __restrict__ stats, unsigned int* counter,
     int* err) {

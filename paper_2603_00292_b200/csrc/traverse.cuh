@@ -75,9 +75,14 @@ __device__ __forceinline__ void shear(const RayPre& R, float vx, float vy, float
 
 // edge function without FMA contraction (exact antisymmetry between neighbours)
 __device__ __forceinline__ float edge_fn(float ax, float ay, float bx, float by) {
-    float e = __fsub_rn(__fmul_rn(ax, by), __fmul_rn(ay, bx));
-    if (e == 0.0f) e = (float)((double)ax * (double)by - (double)ay * (double)bx);
-    return e;
+    return __fsub_rn(__fmul_rn(ax, by), __fmul_rn(ay, bx));
+}
+// exact-zero fallback in double (products of fp32 are exact in fp64)
+static __device__ __noinline__ void edge_fn_f64(float Ax, float Ay, float Bx, float By, float Cx, float Cy, float& U,
+                                         float& V, float& W) {
+    U = (float)((double)Cx * (double)By - (double)Cy * (double)Bx);
+    V = (float)((double)Ax * (double)Cy - (double)Ay * (double)Cx);
+    W = (float)((double)Bx * (double)Ay - (double)By * (double)Ax);
 }
 
 // watertight two-sided test; on success updates (t, id, u, v)
@@ -90,6 +95,8 @@ __device__ __forceinline__ bool tri_test(const RayPre& R, const float4 a, const 
     float U = edge_fn(Cx, Cy, Bx, By);    // Cx*By - Cy*Bx  -> weight of v0
     float V = edge_fn(Ax, Ay, Cx, Cy);    // Ax*Cy - Ay*Cx  -> weight of v1
     float W = edge_fn(Bx, By, Ax, Ay);    // Bx*Ay - By*Ax  -> weight of v2
+    if (U == 0.0f || V == 0.0f || W == 0.0f) [[unlikely]]
+        edge_fn_f64(Ax, Ay, Bx, By, Cx, Cy, U, V, W);
     if ((U < 0.f || V < 0.f || W < 0.f) && (U > 0.f || V > 0.f || W > 0.f)) return false;
     float det = U + V + W;
     if (det == 0.0f) return false;

@@ -62,10 +62,26 @@ def test_cornell_golden_primaries(native):
 
 
 def test_cornell_random_rays_tminmax_mask(native):
+    """Random rays from inside the box (incl. zero direction components, tmin/tmax windows).
+
+    Origins inside a cube see the cube's bottom face and the floor at the SAME
+    t (the cubes stand flush on y = 0): an exact geometric tie that float64
+    local-space and fp32 world-space rounding resolve differently.  Every
+    disagreement must be such a tie; all other rays must agree exactly.
+    """
     sc = compile_scene(scenes.cornell_description())
     gd = golden("cornell_hits")
-    g = closest_hit_batch(sc, gd["RO"], gd["RD"], gd["tmin"], gd["tmax"])
-    _compare(g, tuple(gd[k] for k in ("rt", "ri", "rp", "ru", "rv", "rn")), gd["RO"].shape[0], 1e-3)
+    t, inst, prim = closest_hit_batch(sc, gd["RO"], gd["RD"], gd["tmin"], gd["tmax"])[:3]
+    rt, ri, rp = gd["rt"], gd["ri"], gd["rp"]
+    diff = (inst != ri) | (prim != rp)
+    ties = diff & (inst >= 0) & (ri >= 0) & (np.abs(t - rt) <= 1e-6 * np.abs(rt))
+    assert np.array_equal(diff, ties), np.nonzero(diff & ~ties)[0][:10]
+    # the tied pairs are cube-bottom (inst 4/5, prims 0-1) vs floor (inst 0, prims 0-1) at y = 0
+    y = gd["RO"][:, 1] + rt * gd["RD"][:, 1]
+    assert np.all(np.abs(y[ties]) < 1e-6)
+    ok = ~ties
+    _compare(tuple(a[ok] for a in closest_hit_batch(sc, gd["RO"][ok], gd["RD"][ok], gd["tmin"][ok], gd["tmax"][ok])),
+             tuple(gd[k][ok] for k in ("rt", "ri", "rp", "ru", "rv", "rn")), int(ok.sum()), 1e-3)
     m = closest_hit_batch(sc, gd["RO"], gd["RD"], gd["tmin"], gd["tmax"], ray_mask=0)
     assert np.all(m[0] == -1.0) and np.all(m[1] == -1)
 
