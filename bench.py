@@ -1,20 +1,25 @@
-"""Benchmark: LBVH build + primary rays on the 1M-triangle UV sphere at 1920x1080
-(BASELINE.json configs[1]); path tracing of the Cornell box (configs[2]) as a
-secondary measurement.  Prints ONE JSON line (rank 0).
+"""Benchmark of the B200 ray-tracing hot path.  Prints ONE JSON line (rank 0).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config 2|3|4|5]
 
-Step (our arm): rebuild the 30-bit LBVH over the device-resident triangles
-(K1-K5) + render one 1920x1080 eye sample (raygen + closest-hit + shade fused in
-the persistent megakernel, K7) [+ one NCCL reduce of the (H*W,4) f32
+Default (the driver's run): BASELINE.json configs[1] = config 2, "LBVH build +
+primary rays on a synthetic 1M-triangle tessellated-sphere mesh at 1920x1080".
+One step = rebuild the 30-bit LBVH over the device-resident triangles (K1-K5,
+9 launches) + one 1920x1080 eye sample (raygen + closest hit + shade fused in
+the persistent megakernel K7) [+ one NCCL reduce of the (H*W, 4) f32
 accumulation buffer to rank 0 when N > 1].  Weak scaling: rank g renders
-sample index g of the same frame (global sample index in the stream hash), so
-N GPUs trace N * 2,073,600 rays per step; value = all rays / max-over-ranks time.
-Between timed steps a 256 MiB buffer is written to flush the 126 MB L2.
+global sample index g of the frame, so N GPUs trace N x 2,073,600 rays per step;
+value = all rays / max-over-ranks device time of the K timed steps.  A 256 MiB
+buffer is written between timed steps to flush the 126 MB L2.
 
---impl reference: the reference's algorithm ported to C (oracle/, float64, the
-reference itself is a numba library that cannot travel to the GPU box) on the
-host cores: SAH compile + render_frame('eye') of the same frame, rank 0 only.
+Other configs (BASELINE.json configs[2..4]; documented in DESIGN.md):
+  3  Cornell 1920x1080, 64 spp/GPU path tracing, max_depth 5, --kernel mega|wavefront (weak, sample split)
+  4  10M-triangle random soup, 3840x2160 primary rays, LBVH build + interleaved tile-band split (strong)
+  5  Cornell 1920x1080, 1024 spp total, sample split + one reduce (strong)
+
+--impl reference: the reference's algorithm (a numba CPU library that cannot
+travel to the GPU box) as its float64 C restatement oracle/ (bit-identical to
+the reference on the golden vectors) on the host cores, rank 0 only.
 """
 
 import argparse
@@ -30,11 +35,19 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-W, H = 1920, 1080
 METRIC = "Mrays/s (primary + diffuse bounce) & LBVH build ms at 1/2/4/8 B200 vs CPU ref"
-WORKLOAD = "config2: LBVH-30 build + 1920x1080 primary rays (eye, 1 spp/GPU, jitter, seed 0) on the synthetic " \
-           "1M-triangle UV sphere (stacks 500 x slices 1000), camera (0,0,2.5)"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FHD = (1920, 1080)
+UHD = (3840, 2160)
+
+WORKLOADS = {
+    2: "config2: LBVH-30 build + 1920x1080 primary rays (eye, 1 spp per GPU, jitter, seed 0) on the synthetic "
+       "1M-triangle UV sphere (500 stacks x 1000 slices), camera (0,0,2.5)",
+    3: "config3: cornell.scn 1920x1080, 64 spp per GPU, pt, max_depth 5 (4 diffuse bounces), seed 0",
+    4: "config4: LBVH-30 build + 3840x2160 primary rays (eye, 1 spp) on the synthetic 10M-triangle random soup "
+       "(default_rng(0)), tile split over GPUs",
+    5: "config5: cornell.scn 1920x1080, 1024 spp total, pt, max_depth 5, sample split over GPUs + one reduce",
+}
 
 
 def load_peaks():
@@ -64,8 +77,7 @@ class ClockSampler:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                                           "-i", str(self.device), "-lms", "50"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
+            threading.Thread(target=self._read, daemon=True).start()
         except Exception:
             self.proc = None
 
@@ -90,14 +102,17 @@ class ClockSampler:
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         lo, hi = (self.marks[0], self.marks[-1]) if len(self.marks) >= 2 else (0, 1e30)
-        inside = [s for t, s in self.samples if lo <= t <= hi] or [s for _, s in self.samples]
+        inside = [s for t, s in self.samples if lo <= t <= hi]
+        window = "timed region"
+        if not inside:   # timed region shorter than the 50 ms sampling period: nearest samples
+            inside = [min(self.samples, key=lambda ts: abs(ts[0] - lo))[1]]
+            window = "nearest sample to a timed region shorter than the sampling period"
         sm = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
         mx = [float(s[2]) for s in inside if s[2].replace(".", "").isdigit()]
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         reasons = sorted({names[k] for s in inside for k in range(4) if s[3 + k].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(inside),
-                "window": "warm-up + timed region" if len(self.marks) < 2 else "timed region"}
+                "reasons": reasons, "samples": len(inside), "window": window}
 
 
 def dist_setup():
@@ -112,50 +127,69 @@ def dist_setup():
     return ws, rank, local
 
 
+def scene_desc(config, soup_n=10_000_000):
+    from paper_2603_00292_b200 import scenes
+    if config == 2:
+        return scenes.sphere_description()
+    if config == 4:
+        return scenes.soup_description(soup_n, seed=0)
+    return scenes.cornell_description()
+
+
 # ---------------------------------------------------------------------------
-# CPU baseline / reference arm: the oracle port (float64 C restatement)
+# CPU side: the oracle port (float64 C restatement of the reference)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_step(orc_desc_fn, workers):
-    """One reference step: SAH compile (reference algorithm, 1 thread as in the reference)
-    + render_frame('eye') of the 1920x1080 frame on `workers` threads.  Returns (rays, secs, build_s)."""
+def cpu_sample(config, desc, cores):
+    """One bounded CPU measurement of the same workload; returns (Mrays/s, sample text, build ms)."""
     from oracle import oracle
+    oracle.build()
     t0 = time.perf_counter()
-    sc = oracle.scene_from_description(orc_desc_fn())
+    sc = oracle.scene_from_description(desc)
     t1 = time.perf_counter()
-    _, rays = sc.render_frame(W, H, 1, "eye", seed=0, workers=workers)
+    if config == 2:
+        W, H = FHD
+        _, rays = sc.render_frame(W, H, 1, "eye", seed=0, workers=cores)
+        t2 = time.perf_counter()
+        return rays / (t2 - t0) / 1e6, (f"full config-2 step: SAH compile (accel.py:68-187 restated, 1 thread, "
+                                         f"{1e3 * (t1 - t0):.0f} ms) + render_frame('eye') 1920x1080 on {cores} "
+                                         f"threads"), 1e3 * (t1 - t0)
+    if config == 4:
+        W, H = UHD
+        rows = H // 16
+        _, rays = sc.render_frame(W, H, 1, "eye", seed=0, workers=cores, pix_lo=0, pix_hi=rows * W)
+        t2 = time.perf_counter()
+        return rays / (t2 - t1) / 1e6, (f"SAH compile of the 10M soup ({1e3 * (t1 - t0):.0f} ms, 1 thread, not in "
+                                         f"the rate) + eye render of the top {rows} rows of 3840x2160 on {cores} "
+                                         f"threads"), 1e3 * (t1 - t0)
+    W, H = FHD
+    _, rays = sc.render_frame(W, H, 1, "pt", seed=0, workers=cores, max_depth=5)
     t2 = time.perf_counter()
-    return rays, t2 - t0, t1 - t0
+    return rays / (t2 - t1) / 1e6, (f"render_frame('pt', max_depth=5) 1920x1080 at 1 spp (sample 0 = the first "
+                                     f"sample of the full run; identical streams) on {cores} threads"), 1e3 * (t1 - t0)
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    from oracle import oracle
-    from paper_2603_00292_b200 import scenes
-    oracle.build()
     cores = os.cpu_count() or 1
-    desc = scenes.sphere_description()
-    fn = lambda: desc
-    for _ in range(args.warmup):
-        cpu_reference_step(fn, cores)
-    rays_tot, secs, builds = 0, 0.0, 0.0
-    for _ in range(args.steps):
-        r, s, b = cpu_reference_step(fn, cores)
-        rays_tot += r
-        secs += s
-        builds += b
-    value = rays_tot / secs / 1e6
-    sample = (f"full config-2 step on the host: C float64 restatement of compile_scene (binned-SAH build, "
-              f"accel.py:68-187, 1 thread) + render_frame('eye') 1920x1080 1 spp ({cores} threads); "
-              f"mean SAH build {1e3 * builds / args.steps:.0f} ms")
+    desc = scene_desc(args.config, args.soup_n)
+    for _ in range(args.warmup if args.config != 4 else 0):
+        cpu_sample(args.config, desc, cores)
+    vals, builds = [], []
+    steps = args.steps if args.config != 4 else 1
+    for _ in range(steps):
+        v, sample, b = cpu_sample(args.config, desc, cores)
+        vals.append(v)
+        builds.append(b)
+    value = float(np.mean(vals))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": ws,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": f"cpu{cores}"},
+            "steps": steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "weak" if args.config in (2, 3) else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": WORKLOADS[args.config], "parallelism": f"cpu x{cores}"},
             "cpu_baseline": {"value": value, "unit": "Mrays/s", "cores": cores, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "reference_build_ms": 1e3 * builds / args.steps}
+            "reference_build_ms": float(np.mean(builds))}
     print(json.dumps(line), flush=True)
 
 
@@ -166,51 +200,72 @@ def run_reference(args, ws, rank):
 def run_ours(args, ws, rank, local):
     import torch
     import torch.distributed as dist
-    from paper_2603_00292_b200 import IntegratorConfig, closest_hit_batch, compile_scene, render_into, scenes
-    from paper_2603_00292_b200 import accel
+    from paper_2603_00292_b200 import IntegratorConfig, closest_hit_batch, compile_scene, render_into
+    from paper_2603_00292_b200 import accel, distributed
     from paper_2603_00292_b200.integrators import raygen
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     peak_gbs, peak_src = load_peaks()
-    desc = scenes.sphere_description()
+    C = args.config
+    desc = scene_desc(C, args.soup_n)
     sc = compile_scene(desc, "lbvh30", device=local)
     tl = sc.tlas
-    n_tri = tl.n
+    W, H = UHD if C == 4 else FHD
     npix = W * H
-    sample = rank                      # weak scaling: sample split, global sample index
     accum = torch.zeros((npix, 4), dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    cfg = IntegratorConfig(max_depth=5)
 
-    # -- per-ray cost of this exact BVH (stats build of the trace kernel) -------
-    rays_dev = raygen(sc, W, H, sample=sample)
+    # -- work split of this rank ---------------------------------------------
+    if C == 2:
+        samples, bands, integ, spp_step, scaling = (rank, rank + 1), None, "eye", 1, "weak"
+    elif C == 3:
+        samples, bands, integ, spp_step, scaling = (64 * rank, 64 * rank + 64), None, "pt", 64, "weak"
+    elif C == 4:
+        samples, bands, integ, spp_step, scaling = (0, 1), distributed.band_split(rank, ws), "eye", 1, "strong"
+    else:
+        samples, bands, integ, spp_step, scaling = distributed.sample_slice(rank, ws, 1024), None, "pt", 1024, \
+            "strong"
+    with_build = C in (2, 4)
+    kernel = args.kernel
+
+    # rays of one step (all ranks), counted once outside the timed region
+    accum.zero_()
+    my_rays = render_into(sc, accum, W, H, 1, integ, 0, cfg, True, kernel, samples=samples, bands=bands)
+    rays_t = torch.tensor([float(my_rays)], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(rays_t)
+    rays_step = int(rays_t.item())
+
+    # per-ray cost of this exact BVH (stats build of the trace kernel, primary rays of this rank)
+    prim = raygen(sc, W, H, sample=samples[0])
     hits = torch.empty((npix, 4), dtype=torch.float32, device=dev)
     st = torch.empty((npix, 2), dtype=torch.int32, device=dev)
-    accel.trace_closest(tl, rays_dev, hits, stats=st)
+    accel.trace_closest(tl, prim, hits, stats=st)
     torch.cuda.synchronize()
     n_tests = float(st[:, 0].double().mean())
     n_nodes = float(st[:, 1].double().mean())
     hit_frac = float((hits[:, 1].view(torch.int32) >= 0).double().mean())
-    bytes_per_ray = 64.0 * n_nodes + 48.0 * n_tests + 32.0
-    build_bytes = 328.0 * n_tri          # SURVEY 8(d) algorithmic bytes, 30-bit keys
+    del hits, st
     stages = tl.build_profiled(30)
 
-    ev = lambda: torch.cuda.Event(enable_timing=True)
-
-    def step(timed=None):
-        if timed:
-            timed[0].record()
-        tl.build(30)
-        if timed:
-            timed[1].record()
-        render_into(sc, accum, W, H, 1, "eye", 0, None, True, "mega", samples=(sample, sample + 1),
+    def step(e=None):
+        if e:
+            e[0].record()
+        if with_build:
+            tl.build(30)
+        if e:
+            e[1].record()
+        render_into(sc, accum, W, H, 1, integ, 0, cfg, True, kernel, samples=samples, bands=bands,
                     count_rays=False)
-        if timed:
-            timed[2].record()
+        if e:
+            e[2].record()
         if ws > 1:
             dist.reduce(accum, 0)
-        if timed:
-            timed[3].record()
+        if e:
+            e[3].record()
 
     clocks = ClockSampler(local)
     clocks.start()
@@ -222,8 +277,9 @@ def run_ours(args, ws, rank, local):
         dist.barrier()
     torch.cuda.synchronize()
     clocks.mark()
-    evs = [[ev() for _ in range(4)] for _ in range(args.steps)]
-    for k in range(args.steps):
+    K = args.steps
+    evs = [[ev() for _ in range(4)] for _ in range(K)]
+    for k in range(K):
         flush.fill_(k & 0xFF)
         step(evs[k])
     torch.cuda.synchronize()
@@ -233,114 +289,139 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     time.sleep(0.12)
     clocks.stop()
-    t_build = sum(e[0].elapsed_time(e[1]) for e in evs)
-    t_trace = sum(e[1].elapsed_time(e[2]) for e in evs)
-    t_reduce = sum(e[2].elapsed_time(e[3]) for e in evs)
-    t_total = sum(e[0].elapsed_time(e[3]) for e in evs)
-    local_t = torch.tensor([t_total, t_build, t_trace, t_reduce], dtype=torch.float64, device=dev)
+    t = torch.tensor([sum(e[0].elapsed_time(e[3]) for e in evs), sum(e[0].elapsed_time(e[1]) for e in evs),
+                      sum(e[1].elapsed_time(e[2]) for e in evs), sum(e[2].elapsed_time(e[3]) for e in evs)],
+                     dtype=torch.float64, device=dev)
     if ws > 1:
-        dist.all_reduce(local_t, op=dist.ReduceOp.MAX)
-    t_total, t_build, t_trace, t_reduce = (float(x) for x in local_t.cpu())
-    K = args.steps
-    rays_all = ws * npix * K
-    value = rays_all / (t_total * 1e-3) / 1e6
-    trace_mrays = ws * npix * K / (t_trace * 1e-3) / 1e6
-    build_ms = t_build / K
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    t_total, t_build, t_render, t_reduce = (float(x) for x in t.cpu())
+    value = rays_step * K / (t_total * 1e-3) / 1e6
 
     # -- end to end through the public API with host buffers ---------------------
     e2e = None
     if not args.no_e2e:
-        r = rays_dev.cpu().numpy().astype(np.float64)
-        O, D = np.ascontiguousarray(r[:, 0:3]), np.ascontiguousarray(r[:, 4:7])
-        host_tris = tl.tris.copy()
-        closest_hit_batch(sc, O, D)       # warm (staging buffers)
-        ke = max(1, min(K, 5))
+        if C in (2, 4):
+            # GpuTlas.refit(host vertices) + closest_hit_batch(host float64 rays) of this rank's rays
+            r = prim.cpu().numpy().astype(np.float64)
+            if bands is not None:
+                rows = np.array(distributed.band_rows(H, rank, ws))
+                sel = (rows[:, None] * W + np.arange(W)[None, :]).ravel()
+                r = r[sel]
+            O, D = np.ascontiguousarray(r[:, 0:3]), np.ascontiguousarray(r[:, 4:7])
+            host_tris = tl.tris.copy()
+            closest_hit_batch(sc, O, D)
+            ke = max(1, min(K, 5))
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(ke):
+                tl.refit(host_tris, 30)
+                closest_hit_batch(sc, O, D)
+            torch.cuda.synchronize()
+            te = time.perf_counter() - t0
+            nr = O.shape[0]
+            h2d = int(host_tris.nbytes + nr * (24 + 24 + 8 + 8))
+            d2h = int(nr * (8 + 8 + 8 + 8 + 8 + 24))
+            path = ("GpuTlas.refit(host fp32 vertices, H2D + LBVH rebuild) + closest_hit_batch(host float64 rays) "
+                    "-> host float64/int64 (t, inst, prim, u, v, normal)")
+            rays_e2e = nr
+        else:
+            # render_frame (public API): H2D of the camera/params only, D2H of the (H, W, 4) accumulation
+            from paper_2603_00292_b200 import render_frame
+            ke = 1
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            render_frame(sc, W, H, spp_step, "pt", seed=0, cfg=cfg, kernel=kernel,
+                         samples=samples if C == 3 else samples)
+            torch.cuda.synchronize()
+            te = time.perf_counter() - t0
+            h2d, d2h = 0, npix * 16
+            path = "render_frame(...) -> host AccumBuffer (float64 copy of the f32 device sums)"
+            rays_e2e = my_rays
+        tt = torch.tensor([te, float(rays_e2e)], dtype=torch.float64, device=dev)
         if ws > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(ke):
-            tl.refit(host_tris, 30)
-            res = closest_hit_batch(sc, O, D)
-        torch.cuda.synchronize()
-        te = time.perf_counter() - t0
-        tt = torch.tensor([te], dtype=torch.float64, device=dev)
-        if ws > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        te = float(tt.item())
-        e2e = {"value": ws * npix * ke / te / 1e6, "unit": "Mrays/s",
-               "h2d_bytes_per_step": int(host_tris.nbytes + npix * (24 + 24 + 8 + 8)),
-               "d2h_bytes_per_step": int(npix * (8 + 8 + 8 + 8 + 8 + 24)),
-               "path": "GpuTlas.refit(host fp32 vertices) + closest_hit_batch(host float64 rays) -> host "
-                       "float64/int64 (t, inst, prim, u, v, normal)", "steps": ke}
+            dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+        e2e = {"value": float(tt[1]) * ke / float(tt[0]) / 1e6, "unit": "Mrays/s", "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "path": path, "steps": ke}
 
-    # -- secondary: config 3 path tracing (Cornell 1080p, max_depth 5), rank 0 ------
+    # -- secondary (config 2, N=1): config-3 path tracing, mega vs wavefront ------
     pt = None
-    if rank == 0 and not args.no_pt:
-        cfg = IntegratorConfig(max_depth=5)
-        cs = compile_scene(scenes.cornell_description(), device=local)
+    if rank == 0 and ws == 1 and C == 2 and not args.no_pt:
+        cs = compile_scene(scene_desc(3), device=local)
         acc = torch.zeros((npix, 4), dtype=torch.float32, device=dev)
-        pt = {"workload": f"config3: cornell 1920x1080, {args.pt_spp} spp, pt, max_depth 5, seed 0"}
+        exact = render_into(cs, acc, W, H, args.pt_spp, "pt", 0, cfg, kernel="mega")
+        pt = {"workload": f"config3: cornell 1920x1080, {args.pt_spp} spp, pt, max_depth 5, seed 0",
+              "rays_per_frame": exact, "rays_per_path": exact / (npix * args.pt_spp)}
         for kern in ("mega", "wavefront"):
-            render_into(cs, acc, W, H, 2, "pt", 0, cfg, kernel=kern)        # warm
+            render_into(cs, acc, W, H, 2, "pt", 0, cfg, kernel=kern)
             torch.cuda.synchronize()
             a, b = ev(), ev()
             a.record()
-            rays = render_into(cs, acc, W, H, args.pt_spp, "pt", 0, cfg, kernel=kern, count_rays=False)
+            render_into(cs, acc, W, H, args.pt_spp, "pt", 0, cfg, kernel=kern, count_rays=False)
             b.record()
             torch.cuda.synchronize()
             ms = a.elapsed_time(b)
-            rays = render_into(cs, acc, W, H, 1, "pt", 0, cfg, kernel=kern) * args.pt_spp  # count (1 spp probe)
-            pt[kern] = {"ms": ms, "mrays_s_est": rays / (ms * 1e-3) / 1e6}
-        acc.zero_()
-        exact = render_into(cs, acc, W, H, args.pt_spp, "pt", 0, cfg, kernel="mega")
-        for kern in ("mega", "wavefront"):
-            pt[kern]["mrays_s"] = exact / (pt[kern]["ms"] * 1e-3) / 1e6
-            pt[kern].pop("mrays_s_est")
-        pt["rays_per_frame"] = exact
-        pt["rays_per_path"] = exact / (npix * args.pt_spp)
+            pt[kern] = {"ms": ms, "mrays_s": exact / (ms * 1e-3) / 1e6}
 
     # -- CPU baseline (rank 0, N = 1): the oracle port on the host cores --------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
-        r, s, b = cpu_reference_step(lambda: desc, cores)
-        cpu = {"value": r / s / 1e6, "unit": "Mrays/s", "cores": cores, "kind": "port",
-               "sample": f"one full config-2 step: C float64 restatement of the reference (SAH compile "
-                         f"{1e3 * b:.0f} ms on 1 thread + render_frame('eye') 1920x1080 on {cores} threads)"}
+        v, sample, _ = cpu_sample(C, desc, cores)
+        cpu = {"value": v, "unit": "Mrays/s", "cores": cores, "kind": "port", "sample": sample}
 
     if rank != 0:
         return
-    trace_ms = t_trace / K
-    trace_bytes = bytes_per_ray * npix
-    trace_gbs = trace_bytes / (trace_ms * 1e-3) / 1e9
-    build_gbs = build_bytes / (build_ms * 1e-3) / 1e9
-    roof_trace = {"kernel": "pt_megakernel (eye: raygen + while-while trace + shade)", "bound": "hbm",
-                  "achieved": trace_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": trace_gbs / peak_gbs,
-                  "traffic": None, "bytes_per_ray": bytes_per_ray,
-                  "bytes_formula": f"64 B x {n_nodes:.2f} internal-node fetches + 48 B x {n_tests:.2f} tri tests "
-                                   "+ 32 B accum RMW per ray (stats build of the same kernel)",
-                  "peak_source": peak_src}
-    roof_build = {"kernel": "LBVH build (K1-K5, 9 launches)", "bound": "hbm", "achieved": build_gbs,
-                  "peak": peak_gbs, "unit": "GB/s", "frac": build_gbs / peak_gbs, "traffic": None,
-                  "bytes_formula": "328 B/tri x 1,000,000 tris (SURVEY 8(d))", "stage_ms": stages,
-                  "peak_source": peak_src}
-    dominant = roof_trace if t_trace >= t_build else roof_build
+    # -- roofline: algorithmic bytes / measured device time ---------------------
+    render_ms = t_render / K
+    bpr = 64.0 * n_nodes + 48.0 * n_tests + 32.0
+    rays_rank0 = my_rays
+    roof_trace = {"kernel": "pt_megakernel (raygen + while-while closest hit + shade, fused)", "bound": "hbm",
+                  "achieved": bpr * rays_rank0 / (render_ms * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
+                  "traffic": None, "bytes_per_ray": bpr, "peak_source": peak_src,
+                  "bytes_formula": f"64 B x {n_nodes:.2f} BVH2 node fetches + 48 B x {n_tests:.2f} triangle "
+                                   f"tests + 32 B accumulation RMW per ray (node/test counts: stats build of the "
+                                   f"trace kernel on this rank's primary rays{'' if C in (2, 4) else '; bounce rays assumed alike'})",
+                  "note": "node/triangle fetches mostly hit L1/L2 (ncu: DRAM 1-2% of peak); the bound that "
+                          "binds is SM issue/latency, see profiles/"}
+    roof_trace["frac"] = roof_trace["achieved"] / peak_gbs
+    line_extra = {}
+    dominant = roof_trace
+    if with_build:
+        build_ms = t_build / K
+        build_bytes = 328.0 * tl.n
+        roof_build = {"kernel": "LBVH build (K1-K5: bounds, morton, onesweep x4, fused emit+refit)", "bound": "hbm",
+                      "achieved": build_bytes / (build_ms * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
+                      "traffic": None, "bytes_formula": f"328 B/tri x {tl.n} tris (SURVEY 8(d), 30-bit keys)",
+                      "stage_ms": stages, "peak_source": peak_src}
+        roof_build["frac"] = roof_build["achieved"] / peak_gbs
+        if t_build > t_render:
+            dominant, other = roof_build, roof_trace
+        else:
+            other = roof_build
+        line_extra = {"lbvh_build_ms": build_ms, "trace_mrays_s": rays_step * K / (t_render * 1e-3) / 1e6,
+                      "roofline_other": other}
+        launches = 9 + 1
+        detail = "per step: 9 LBVH kernels (bounds, bounds_finish, morton, histogram, 4 onesweep passes, fused " \
+                 "emit+refit) + 1 megakernel"
+    else:
+        launches = 1 if kernel == "mega" else (samples[1] - samples[0]) * (2 + 2 * cfg.max_depth)
+        detail = "per step: 1 megakernel" if kernel == "mega" else \
+            "per step: per sample one CUDA-graph wave (raygen + 5 x (extend + shade) + accumulate)"
     line = {
         "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": ws, "steps": K, "warmup": args.warmup,
-        "ms_per_step": t_total / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (config-2 UV sphere generated in-process; no dataset)",
-        "config": {"workload": WORKLOAD, "triangles": n_tri, "rays_per_gpu_per_step": npix,
-                   "parallelism": f"sample-split x{ws} + NCCL reduce" if ws > 1 else "1 GPU",
-                   "l2": "256 MiB buffer written between timed steps (flush)", "hit_fraction": hit_frac},
-        "lbvh_build_ms": build_ms, "trace_mrays_s": trace_mrays, "reduce_ms": t_reduce / K,
-        "roofline": dominant, "roofline_other": roof_build if dominant is roof_trace else roof_trace,
-        "per_ray": {"internal_node_fetches": n_nodes, "triangle_tests": n_tests},
+        "ms_per_step": t_total / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (meshes generated in-process / built-in cornell.scn; no dataset)",
+        "config": {"workload": WORKLOADS[C], "triangles": tl.n, "rays_per_step": rays_step,
+                   "kernel": kernel, "parallelism": (f"{'sample' if bands is None else 'tile-band'} split x{ws}"
+                                                     f" + NCCL reduce") if ws > 1 else "1 GPU",
+                   "l2": "256 MiB buffer written between timed steps (flush)", "primary_hit_fraction": hit_frac},
+        **line_extra, "reduce_ms": t_reduce / K, "roofline": dominant,
+        "per_ray": {"bvh2_node_fetches": n_nodes, "triangle_tests": n_tests},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
-        "gpu_launches": K * (9 + 1), "gpu_launches_detail": "per step: 9 LBVH kernels (bounds, bounds_finish, "
-                                                            "morton, histogram, 4 onesweep passes, fused emit+refit) + "
-                                                            "1 megakernel",
-        "pt": pt,
+        "gpu_launches": K * launches, "gpu_launches_detail": detail, "pt": pt,
     }
     print(json.dumps(line), flush=True)
 
@@ -351,17 +432,17 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", type=int, choices=(2, 3, 4, 5), default=2)
+    ap.add_argument("--kernel", choices=("mega", "wavefront"), default="mega")
+    ap.add_argument("--soup-n", type=int, default=10_000_000)
     ap.add_argument("--pt-spp", type=int, default=64)
     ap.add_argument("--no-pt", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
-        ws = int(os.environ.get("WORLD_SIZE", "1"))
-        rank = int(os.environ.get("RANK", "0"))
-        run_reference(args, ws, rank)
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
         return
     ws, rank, local = dist_setup()
     run_ours(args, ws, rank, local)

@@ -55,6 +55,10 @@ typedef struct {
     float background[3];
     float normal_offset;      /* 1e-4 * scene diagonal (integrators.py:405-413) */
     int64_t pix_lo, pix_hi;
+    /* tile split across GPUs: with a whole-frame pixel range the frame is cut
+     * into rows of 8x4-pixel tiles; only tile rows r with r % band_stride ==
+     * band_offset are rendered (interleaved bands balance the load).  1/0 = all. */
+    int32_t band_stride, band_offset;
 } rt_render_params;
 
 /* ---- context --------------------------------------------------------- */

@@ -50,7 +50,7 @@ class RenderParams(ctypes.Structure):
                 ("kernel", ctypes.c_int32), ("cam", ctypes.c_float * 13),
                 ("sky", ctypes.c_float * 3), ("background", ctypes.c_float * 3),
                 ("normal_offset", ctypes.c_float), ("pix_lo", ctypes.c_int64),
-                ("pix_hi", ctypes.c_int64)]
+                ("pix_hi", ctypes.c_int64), ("band_stride", ctypes.c_int32), ("band_offset", ctypes.c_int32)]
 
 
 def lib():

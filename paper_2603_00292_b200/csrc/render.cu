@@ -26,6 +26,7 @@ struct FrameConst {
     int64_t pix_lo, npix;
     // work units: 8x4 pixel tiles (one per warp) when the range is whole rows
     int tiled, tiles_x;
+    int band_stride, band_offset;   // interleaved tile-row bands (multi-GPU tile split)
     int64_t row0, row1, nunits;
 };
 
@@ -35,7 +36,8 @@ __device__ __forceinline__ bool unit_pixel(const FrameConst& F, int64_t k, int64
     int64_t t = k >> 5;
     int l = (int)(k & 31);
     int64_t x = (t % F.tiles_x) * 8 + (l & 7);
-    int64_t y = F.row0 + (t / F.tiles_x) * 4 + (l >> 3);
+    int64_t trow = (t / F.tiles_x) * F.band_stride + F.band_offset;
+    int64_t y = F.row0 + trow * 4 + (l >> 3);
     pix = y * F.width + x;
     return x < F.width && y < F.row1;
 }
@@ -294,9 +296,11 @@ __global__ void __launch_bounds__(WF_THREADS) wf_accumulate(const FrameConst F, 
         accum[pix] = a;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        unsigned long long total = 0;
+        // closest-hit queries: every real pixel at depth 0 (count[0] also holds the
+        // padding lanes of partial edge tiles) + the live paths of later depths
+        unsigned long long total = (unsigned long long)F.npix;
         int md = F.integ == RT_INTEG_EYE ? 1 : F.max_depth;
-        for (int d = 0; d < md; ++d) total += W.count[d];
+        for (int d = 1; d < md; ++d) total += W.count[d];
         *ray_total += total;
         *d_sample += 1;
         for (int d = 0; d <= md; ++d) counter[d] = 0;
@@ -328,7 +332,22 @@ FrameConst make_frame(const rt_render_params* p) {
     F.row0 = p->pix_lo / p->width;
     F.row1 = hi / p->width;
     F.tiles_x = (p->width + 7) / 8;
-    F.nunits = F.tiled ? (int64_t)F.tiles_x * ((F.row1 - F.row0 + 3) / 4) * 32 : F.npix;
+    F.band_stride = p->band_stride > 0 ? p->band_stride : 1;
+    F.band_offset = p->band_offset;
+    if (!F.tiled) {
+        F.band_stride = 1;
+        F.band_offset = 0;
+    }
+    const int64_t trows = (F.row1 - F.row0 + 3) / 4;
+    const int64_t mine = trows > F.band_offset ? (trows - F.band_offset + F.band_stride - 1) / F.band_stride : 0;
+    F.nunits = F.tiled ? (int64_t)F.tiles_x * mine * 32 : F.npix;
+    if (F.tiled && F.band_stride > 1) {   // real pixels of this band set (ray counting)
+        F.npix = 0;
+        for (int64_t r = F.band_offset; r < trows; r += F.band_stride) {
+            int64_t y0 = F.row0 + 4 * r, y1 = y0 + 4 < F.row1 ? y0 + 4 : F.row1;
+            F.npix += (y1 - y0) * p->width;
+        }
+    }
     return F;
 }
 
@@ -385,9 +404,21 @@ static int ensure_wave(rt_scene* s, int64_t npix, WaveBuffers*& out) {
 
 int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out) {
     FrameConst F = make_frame(p);
-    if (F.npix <= 0 || F.pix_lo < 0 || F.pix_lo + F.npix > (int64_t)p->width * p->height) return RT_EINVAL;
+    const int64_t hi = (p->pix_hi > 0) ? p->pix_hi : (int64_t)p->width * p->height;
+    if (F.pix_lo < 0 || hi <= F.pix_lo || hi > (int64_t)p->width * p->height) {
+        rt_set_error("pixel range [%lld, %lld) outside the frame", (long long)p->pix_lo, (long long)hi);
+        return RT_EINVAL;
+    }
+    if (p->band_stride < 0 || (p->band_stride > 0 && (p->band_offset < 0 || p->band_offset >= p->band_stride))) {
+        rt_set_error("band_offset must be in [0, band_stride)");
+        return RT_EINVAL;
+    }
     if (p->s1 <= p->s0) return RT_EINVAL;
     if (F.nunits > 0x7FFFFFF0ll) return RT_EINVAL;
+    if (F.nunits == 0 || F.npix == 0) {          // e.g. more GPUs than tile rows
+        if (rays_out) *rays_out = 0;
+        return RT_OK;
+    }
     cudaStream_t st = ctx->stream;
     unsigned long long* d_rays = reinterpret_cast<unsigned long long*>(ctx->d_counter + 32);
     RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, 64 * sizeof(unsigned int), st));

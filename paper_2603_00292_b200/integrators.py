@@ -86,11 +86,17 @@ def make_params(scene, width, height, s0, s1, integrator, seed, cfg, jitter, ker
 
 
 def render_into(scene, accum, width, height, spp=1, integrator="pt", seed=0, cfg=None, jitter=True,
-                kernel="mega", samples=None, pixels=None, count_rays=True):
-    """Device form: accumulate into a CUDA (H*W, 4) f32 tensor; returns the ray count (or None)."""
+                kernel="mega", samples=None, pixels=None, count_rays=True, bands=None):
+    """Device form: accumulate into a CUDA (H*W, 4) f32 tensor; returns the ray count (or None).
+
+    samples: [s0, s1) global sample indices (sample split); pixels: row-major
+    [lo, hi) pixel range; bands: (stride, offset) interleaved 4-row tile bands
+    (tile split, whole-frame ranges only)."""
     s0, s1 = (0, spp) if samples is None else samples
     pix_lo, pix_hi = (0, 0) if pixels is None else pixels
     p = make_params(scene, width, height, s0, s1, integrator, seed, cfg, jitter, kernel, pix_lo, pix_hi)
+    if bands is not None:
+        p.band_stride, p.band_offset = int(bands[0]), int(bands[1])
     rays = np.zeros(1, np.uint64)
     check(lib().rt_render(scene.tlas.ctx.handle, scene.tlas.handle, p, ptr(accum),
                           ptr(rays) if count_rays else None))

@@ -103,6 +103,18 @@ def test_tile_split_equals_full_frame(cornell_gpu):
     assert torch.equal(full, tiles)
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_band_split_equals_full_frame(cornell_gpu, world):
+    """Config-4 tile split: interleaved 4-row tile bands over `world` GPUs cover every pixel once."""
+    W, H = 100, 70
+    cfg = IntegratorConfig(max_depth=5)
+    full = torch.zeros((W * H, 4), device="cuda")
+    r_full = render_into(cornell_gpu, full, W, H, 2, "pt", 0, cfg)
+    parts = torch.zeros((W * H, 4), device="cuda")
+    r_parts = sum(render_into(cornell_gpu, parts, W, H, 2, "pt", 0, cfg, bands=(world, g)) for g in range(world))
+    assert torch.equal(full, parts) and r_full == r_parts
+
+
 def test_furnace(native):
     """AC6: 0.5-albedo plane under a unit sky converges to 0.5 +- 0.02."""
     sc = compile_scene(scenes.furnace_description())

@@ -80,7 +80,7 @@ def test_cornell_random_rays_tminmax_mask(native):
     y = gd["RO"][:, 1] + rt * gd["RD"][:, 1]
     assert np.all(np.abs(y[ties]) < 1e-6)
     ok = ~ties
-    _compare(tuple(a[ok] for a in closest_hit_batch(sc, gd["RO"][ok], gd["RD"][ok], gd["tmin"][ok], gd["tmax"][ok])),
+    _compare(closest_hit_batch(sc, gd["RO"][ok], gd["RD"][ok], gd["tmin"][ok], gd["tmax"][ok]),
              tuple(gd[k][ok] for k in ("rt", "ri", "rp", "ru", "rv", "rn")), int(ok.sum()), 1e-3)
     m = closest_hit_batch(sc, gd["RO"], gd["RD"], gd["tmin"], gd["tmax"], ray_mask=0)
     assert np.all(m[0] == -1.0) and np.all(m[1] == -1)
