@@ -20,7 +20,7 @@ ID_AGREE = 0.9999   # hit-ID agreement bar (north_star)
 UV_ABS = 1e-3       # barycentric tolerance (not part of the north_star bar; reported)
 
 
-def _compare(res_gpu, res_orc, n_rays, allow_t_outliers=1e-4):
+def _compare(res_gpu, res_orc, n_rays, allow_t_outliers=1e-4, t_abs=0.0):
     t, inst, prim, u, v, n = res_gpu[:6]
     rt, ri, rp, ru, rv, rn = res_orc[:6]
     same = (inst == ri) & (prim == rp)
@@ -29,7 +29,7 @@ def _compare(res_gpu, res_orc, n_rays, allow_t_outliers=1e-4):
     detail = [(int(i), int(inst[i]), int(prim[i]), float(t[i]), int(ri[i]), int(rp[i]), float(rt[i])) for i in bad]
     assert agree >= ID_AGREE, f"ID agreement {agree:.6f} ({(~same).sum()} of {n_rays}); first: {detail}"
     both = same & (ri >= 0)
-    rel = np.abs(t[both] - rt[both]) / np.maximum(np.abs(rt[both]), 1e-30)
+    rel = np.maximum(np.abs(t[both] - rt[both]) - t_abs, 0.0) / np.maximum(np.abs(rt[both]), 1e-30)
     frac_bad = np.mean(rel > T_REL) if rel.size else 0.0
     assert frac_bad <= allow_t_outliers, f"{frac_bad:.2e} of hits exceed {T_REL} relative t (max {rel.max():.2e})"
     assert np.all(t[inst < 0] == -1.0) and np.all(prim[inst < 0] == -1)
@@ -80,8 +80,11 @@ def test_cornell_random_rays_tminmax_mask(native):
     y = gd["RO"][:, 1] + rt * gd["RD"][:, 1]
     assert np.all(np.abs(y[ties]) < 1e-6)
     ok = ~ties
+    # rays start inside the box (|o| <= 1) and many hits are close (t ~ 1e-2): fp32 t carries
+    # ~ulp(|o|) = 6e-8 absolute error, so t is checked to 1e-5 relative PLUS 4 ulp(1.0) absolute
     _compare(closest_hit_batch(sc, gd["RO"][ok], gd["RD"][ok], gd["tmin"][ok], gd["tmax"][ok]),
-             tuple(gd[k][ok] for k in ("rt", "ri", "rp", "ru", "rv", "rn")), int(ok.sum()), 1e-3)
+             tuple(gd[k][ok] for k in ("rt", "ri", "rp", "ru", "rv", "rn")), int(ok.sum()), 0.0,
+             t_abs=4 * 2.0 ** -23)
     m = closest_hit_batch(sc, gd["RO"], gd["RD"], gd["tmin"], gd["tmax"], ray_mask=0)
     assert np.all(m[0] == -1.0) and np.all(m[1] == -1)
 
