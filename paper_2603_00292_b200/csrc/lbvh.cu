@@ -112,9 +112,15 @@ __device__ __forceinline__ uint64_t expand21(uint64_t v) {
     return v;
 }
 
-template <typename K, int B>
+// K2 fused with the onesweep digit histogram of every pass (the keys are in
+// registers here, so the histogram costs no extra read of the key array)
+template <typename K, int B, int PASSES>
 __global__ void __launch_bounds__(256) lbvh_morton_kernel(const float* __restrict__ tris, int64_t n,
-                                                         const float* __restrict__ cb, K* __restrict__ keys) {
+                                                         const float* __restrict__ cb, K* __restrict__ keys,
+                                                         unsigned int* __restrict__ hist) {
+    __shared__ unsigned int s_hist[PASSES][256];
+    for (int i = threadIdx.x; i < PASSES * 256; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+    __syncthreads();
     const float scale = (float)(1u << B), qmax = (float)((1u << B) - 1u);
     float lo[3], inv[3];
 #pragma unroll
@@ -131,22 +137,12 @@ __global__ void __launch_bounds__(256) lbvh_morton_kernel(const float* __restric
             x = sel_min(sel_max(x, 0.0f), qmax);
             q[a] = (uint32_t)x;
         }
+        K k;
         if (B == 10)
-            keys[i] = (K)((expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]));
+            k = (K)((expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]));
         else
-            keys[i] = (K)((expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]));
-    }
-}
-
-// ---- K3: onesweep radix sort ----------------------------------------------
-template <typename K, int PASSES>
-__global__ void __launch_bounds__(256) onesweep_hist_kernel(const K* __restrict__ keys, int64_t n,
-                                                           unsigned int* __restrict__ hist) {
-    __shared__ unsigned int s_hist[PASSES][RADIX];
-    for (int i = threadIdx.x; i < PASSES * RADIX; i += blockDim.x) (&s_hist[0][0])[i] = 0;
-    __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        K k = keys[i];
+            k = (K)((expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]));
+        keys[i] = k;
 #pragma unroll
         for (int p = 0; p < PASSES; ++p) atomicAdd(&s_hist[p][(unsigned)(k >> (8 * p)) & 0xFFu], 1u);
     }
@@ -211,13 +207,26 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_pass_kernel(
         atomicExch(st, FLAG_INC | tile_count);
     } else {
         atomicExch(st, FLAG_AGG | tile_count);
+        // windowed look-back: LB_WIN independent status loads per round instead of
+        // one dependent L2 round trip per predecessor tile
+        constexpr int LB_WIN = 16;
         int j = (int)tile - 1;
-        while (true) {
-            unsigned s = *((volatile unsigned*)(status + (size_t)j * RADIX + tid));
-            if ((s & ~VALUE_MASK) == 0) continue;
-            excl += s & VALUE_MASK;
-            if (s & FLAG_INC) break;
-            --j;
+        bool done = false;
+        while (!done) {
+            unsigned w[LB_WIN];
+#pragma unroll
+            for (int k = 0; k < LB_WIN; ++k)
+                w[k] = (j - k >= 0) ? *((volatile unsigned*)(status + (size_t)(j - k) * RADIX + tid)) : (2u << 30);
+            // consume from the nearest predecessor down to the first inclusive prefix;
+            // stop at a not-yet-published entry and re-poll from there
+            int k = 0;
+            for (; k < LB_WIN; ++k) {
+                const unsigned s = w[k];
+                if ((s & ~VALUE_MASK) == 0) break;
+                excl += s & VALUE_MASK;
+                if (s & FLAG_INC) { done = true; break; }
+            }
+            if (!done) j -= k;
         }
         atomicExch(st, FLAG_INC | (excl + tile_count));
     }
@@ -263,74 +272,153 @@ __device__ __forceinline__ int adj_delta(const K* __restrict__ k, int64_t n, int
     return (int)(8 * sizeof(K)) + __clz((unsigned)i ^ (unsigned)(i + 1));
 }
 
-template <typename K>
-__global__ void __launch_bounds__(256) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
-                                                       const float* __restrict__ tris, const uint32_t* __restrict__ mask,
-                                                       int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
-                                                       float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
-                                                       int* slot_range, float4* slot_box) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= n) return;
+// One climbing node: keys [l, r], its box, subtree height and boundary deltas.
+struct EmitNode {
+    int l, r, h, dl, dr;
     float lo[3], hi[3];
-    {
-        const uint32_t id = order[i];
-        float t[9];
-        load_tri(tris, id, t);
-        tri_box(t, lo, hi);
-        tri_sorted[3 * i + 0] = make_float4(t[0], t[1], t[2], __int_as_float((int)id));
-        tri_sorted[3 * i + 1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask[id]));
-        tri_sorted[3 * i + 2] = make_float4(t[6], t[7], t[8], 0.0f);
+};
+
+// Second arrival at split slot gamma: emit the parent (Karras numbering) and
+// make it the current node.  Returns true when the parent is the root.
+template <typename K>
+__device__ __forceinline__ bool emit_parent(const K* __restrict__ keys, int64_t n, int2* __restrict__ child,
+                                            int32_t* __restrict__ parent, float4* __restrict__ nodes, EmitNode& N,
+                                            bool left, int gamma, int other, const float4 s0, const float4 s1) {
+    const int pl = left ? N.l : other, pr = left ? other : N.r;
+    // children in Karras encoding: left = gamma, right = gamma + 1 (leaf if a single key)
+    const int cl = (pl == gamma) ? ~gamma : gamma;
+    const int cr = (pr == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+    float llo[3], lhi[3], rlo[3], rhi[3];
+    const float so[3] = {s0.x, s0.y, s0.z}, sh[3] = {s1.x, s1.y, s1.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        llo[a] = left ? N.lo[a] : so[a]; lhi[a] = left ? N.hi[a] : sh[a];
+        rlo[a] = left ? so[a] : N.lo[a]; rhi[a] = left ? sh[a] : N.hi[a];
     }
-    int l = (int)i, r = (int)i, h = 0;
-    int dl = adj_delta(keys, n, l - 1), dr = adj_delta(keys, n, r);
+    const int hs = __float_as_int(s0.w);
+    // the parent's own number is its side at the next level (root -> 0)
+    const int pdl = adj_delta(keys, n, pl - 1), pdr = adj_delta(keys, n, pr);
+    const bool root = (pl == 0 && pr == n - 1);
+    const int P = root ? 0 : (pdr > pdl ? pr : pl);
+    N.h = 1 + (N.h > hs ? N.h : hs);
+    float4* nd = nodes + 4 * P;
+    nd[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
+    nd[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
+    nd[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
+    nd[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(N.h), 0.0f);
+    child[P] = make_int2(cl, cr);
+    parent[cl < 0 ? (n - 1) + ~cl : cl] = P;
+    parent[cr < 0 ? (n - 1) + ~cr : cr] = P;
+    if (root) parent[0] = -1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { N.lo[a] = sel_min(llo[a], rlo[a]); N.hi[a] = sel_max(lhi[a], rhi[a]); }
+    N.l = pl; N.r = pr; N.dl = pdl; N.dr = pdr;
+    return root;
+}
+
+// Global climb (nodes whose rendezvous crosses a block's leaf range)
+template <typename K>
+__device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __restrict__ child,
+                             int32_t* __restrict__ parent, float4* __restrict__ nodes, int* slot_range,
+                             float4* slot_box, EmitNode N) {
     while (true) {
-        const bool left = dr > dl;
-        const int gamma = left ? r : l - 1;
+        const bool left = N.dr > N.dl;
+        const int gamma = left ? N.r : N.l - 1;
         const int side = left ? 0 : 1;
-        // publish my box and height for my sibling, then exchange far endpoints
-        __stcg(slot_box + 4 * gamma + 2 * side, make_float4(lo[0], lo[1], lo[2], __int_as_float(h)));
-        __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(hi[0], hi[1], hi[2], 0.0f));
+        __stcg(slot_box + 4 * gamma + 2 * side, make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h)));
+        __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(N.hi[0], N.hi[1], N.hi[2], 0.0f));
         cuda::atomic_ref<int, cuda::thread_scope_device> slot(slot_range[gamma]);
-        const int other = slot.exchange(left ? l : r, cuda::std::memory_order_acq_rel);
+        const int other = slot.exchange(left ? N.l : N.r, cuda::std::memory_order_acq_rel);
         if (other < 0) return;                       // sibling subtree not finished
         const float4 s0 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side));
         const float4 s1 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side) + 1);
-        const int pl = left ? l : other, pr = left ? other : r;
-        // children in Karras encoding: left = gamma, right = gamma + 1 (leaf if a single key)
-        const int cl = (pl == gamma) ? ~gamma : gamma;
-        const int cr = (pr == gamma + 1) ? ~(gamma + 1) : gamma + 1;
-        float llo[3], lhi[3], rlo[3], rhi[3];
-        int hl, hr;
-        if (left) {
-            llo[0] = lo[0]; llo[1] = lo[1]; llo[2] = lo[2]; lhi[0] = hi[0]; lhi[1] = hi[1]; lhi[2] = hi[2]; hl = h;
-            rlo[0] = s0.x; rlo[1] = s0.y; rlo[2] = s0.z; rhi[0] = s1.x; rhi[1] = s1.y; rhi[2] = s1.z;
-            hr = __float_as_int(s0.w);
-        } else {
-            rlo[0] = lo[0]; rlo[1] = lo[1]; rlo[2] = lo[2]; rhi[0] = hi[0]; rhi[1] = hi[1]; rhi[2] = hi[2]; hr = h;
-            llo[0] = s0.x; llo[1] = s0.y; llo[2] = s0.z; lhi[0] = s1.x; lhi[1] = s1.y; lhi[2] = s1.z;
-            hl = __float_as_int(s0.w);
-        }
-        // the parent's own number: its side at the next level (root -> 0)
-        const int pdl = adj_delta(keys, n, pl - 1), pdr = adj_delta(keys, n, pr);
-        const bool root = (pl == 0 && pr == n - 1);
-        const int P = root ? 0 : (pdr > pdl ? pr : pl);
-        h = 1 + (hl > hr ? hl : hr);
-        float4* nd = nodes + 4 * P;
-        nd[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
-        nd[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
-        nd[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
-        nd[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(h), 0.0f);
-        child[P] = make_int2(cl, cr);
-        parent[cl < 0 ? (n - 1) + ~cl : cl] = P;
-        parent[cr < 0 ? (n - 1) + ~cr : cr] = P;
-        if (root) {
-            parent[0] = -1;
-            return;
-        }
-#pragma unroll
-        for (int a = 0; a < 3; ++a) { lo[a] = sel_min(llo[a], rlo[a]); hi[a] = sel_max(lhi[a], rhi[a]); }
-        l = pl; r = pr; dl = pdl; dr = pdr;
+        if (emit_parent(keys, n, child, parent, nodes, N, left, gamma, other, s0, s1)) return;
     }
+}
+
+// Phase A: a block owns leaves [B, E).  A pair of siblings that both start in
+// the block meets in a SHARED-memory slot (block-scope acq_rel exchange); a node
+// whose sibling starts outside the block is deferred.  Phase B (after one
+// __syncthreads): deferred nodes and smem slots that saw only one arrival (the
+// sibling extends past the block) move to the global slots and climb there.
+// All subtrees inside a block therefore finish with ~30-cycle smem rendezvous
+// instead of L2 atomics, and only O(log) boundary nodes per block go global.
+constexpr int EMIT_T = 256;
+
+template <typename K>
+__global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
+                                                           const float* __restrict__ tris, const uint32_t* __restrict__ mask,
+                                                           int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
+                                                           float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
+                                                           int* slot_range, float4* slot_box) {
+    __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
+    __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, side)]
+    __shared__ EmitNode s_def[EMIT_T];          // deferred (boundary-crossing) nodes
+    __shared__ int s_ndef;
+    const int tid = threadIdx.x;
+    const int64_t B = (int64_t)blockIdx.x * EMIT_T;
+    const int64_t E = (B + EMIT_T < n) ? B + EMIT_T : n;
+    s_range[tid] = -1;
+    if (tid == 0) s_ndef = 0;
+    __syncthreads();
+    const int64_t i = B + tid;
+    if (i < E) {
+        EmitNode N;
+        {
+            const uint32_t id = order[i];
+            float t[9];
+            load_tri(tris, id, t);
+            tri_box(t, N.lo, N.hi);
+            tri_sorted[3 * i + 0] = make_float4(t[0], t[1], t[2], __int_as_float((int)id));
+            tri_sorted[3 * i + 1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask[id]));
+            tri_sorted[3 * i + 2] = make_float4(t[6], t[7], t[8], 0.0f);
+        }
+        N.l = N.r = (int)i;
+        N.h = 0;
+        N.dl = adj_delta(keys, n, N.l - 1);
+        N.dr = adj_delta(keys, n, N.r);
+        while (true) {
+            const bool left = N.dr > N.dl;
+            const bool inside = left ? (N.r + 1 < E) : (N.l - 1 >= B);
+            if (!inside) {
+                s_def[atomicAdd(&s_ndef, 1)] = N;
+                break;
+            }
+            const int gamma = left ? N.r : N.l - 1;
+            const int g = gamma - (int)B, side = left ? 0 : 1;
+            s_box[g][side][0] = make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h));
+            s_box[g][side][1] = make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(side));
+            cuda::atomic_ref<int, cuda::thread_scope_block> slot(s_range[g]);
+            const int other = slot.exchange(left ? N.l : N.r, cuda::std::memory_order_acq_rel);
+            if (other < 0) break;                    // first arrival: pending in smem
+            s_range[g] = -2;                         // pair complete
+            if (emit_parent(keys, n, child, parent, nodes, N, left, gamma, other, s_box[g][1 - side][0],
+                            s_box[g][1 - side][1]))
+                break;                               // root (whole tree inside one block)
+        }
+    }
+    __syncthreads();
+    // phase B: smem slot `tid` left with a single arrival, then deferred node `tid`
+    if (tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0) {
+        const float4 a = s_box[tid][0][0], b = s_box[tid][0][1], c = s_box[tid][1][0], d = s_box[tid][1][1];
+        // the written side is the one whose hi.w carries its side tag (0 or 1); the slot
+        // data of the empty side is stale, so identify it from the exchanged endpoint
+        EmitNode N;
+        const int endpoint = s_range[tid];
+        const int gamma = (int)B + tid;
+        // left child: [endpoint, gamma]; right child: [gamma + 1, endpoint]
+        const bool left = endpoint <= gamma;
+        const float4 lo4 = left ? a : c, hi4 = left ? b : d;
+        N.l = left ? endpoint : gamma + 1;
+        N.r = left ? gamma : endpoint;
+        N.h = __float_as_int(lo4.w);
+        N.lo[0] = lo4.x; N.lo[1] = lo4.y; N.lo[2] = lo4.z;
+        N.hi[0] = hi4.x; N.hi[1] = hi4.y; N.hi[2] = hi4.z;
+        N.dl = adj_delta(keys, n, N.l - 1);
+        N.dr = adj_delta(keys, n, N.r);
+        climb_global(keys, n, child, parent, nodes, slot_range, slot_box, N);
+    }
+    if (tid < s_ndef) climb_global(keys, n, child, parent, nodes, slot_range, slot_box, s_def[tid]);
 }
 
 
@@ -363,23 +451,22 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     RT_CUDA_TRY(cudaMemsetAsync(s->cb_enc + 3, 0, 3 * sizeof(unsigned int), st));
     int gb = (int)((n + 255) / 256);
     if (gb > grid_stream) gb = grid_stream;
+    const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+    unsigned int* hist = s->sort_scratch;                    // PASSES * 256
+    unsigned int* counters = hist + PASSES * RADIX;          // PASSES
+    unsigned int* status = counters + 32;                    // PASSES * tiles * 256
+    size_t words = (size_t)PASSES * RADIX + 32 + (size_t)PASSES * tiles * RADIX;
     RT_PROF(ctx, 0);
+    RT_CUDA_TRY(cudaMemsetAsync(s->sort_scratch, 0, words * sizeof(unsigned int), st));
     lbvh_bounds_kernel<<<gb, 256, 0, st>>>(s->tris, n, s->cb_enc);
     lbvh_bounds_finish<<<1, 32, 0, st>>>(s->cb_enc, s->cbounds);
     // K2
     K* ka = (K*)s->keys_a;
     K* kb = (K*)s->keys_b;
     RT_PROF(ctx, 1);
-    lbvh_morton_kernel<K, B><<<gb, 256, 0, st>>>(s->tris, n, s->cbounds, ka);
+    lbvh_morton_kernel<K, B, PASSES><<<gb, 256, 0, st>>>(s->tris, n, s->cbounds, ka, hist);
     RT_PROF(ctx, 2);
-    // K3
-    const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
-    unsigned int* hist = s->sort_scratch;                    // PASSES * 256
-    unsigned int* counters = hist + PASSES * RADIX;          // PASSES
-    unsigned int* status = counters + 32;                    // PASSES * tiles * 256
-    size_t words = (size_t)PASSES * RADIX + 32 + (size_t)PASSES * tiles * RADIX;
-    RT_CUDA_TRY(cudaMemsetAsync(s->sort_scratch, 0, words * sizeof(unsigned int), st));
-    onesweep_hist_kernel<K, PASSES><<<gb, 256, 0, st>>>(ka, n, hist);
+    // K3 (digit histograms already accumulated by K2)
     K* kin = ka; K* kout = kb;
     uint32_t* vin = nullptr; uint32_t* vout = s->vals_b;
     RT_PROF(ctx, 3);
@@ -395,7 +482,7 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     RT_PROF(ctx, 4);
     RT_CUDA_TRY(cudaMemsetAsync(s->flags, 0xFF, sizeof(int) * (n - 1), st));   // split slots: empty
     RT_PROF(ctx, 5);
-    lbvh_emit_kernel<K><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(kin, vin, s->tris, s->tri_mask, n, s->child,
+    lbvh_emit_kernel<K><<<(unsigned)((n + EMIT_T - 1) / EMIT_T), EMIT_T, 0, st>>>(kin, vin, s->tris, s->tri_mask, n, s->child,
                                                                      s->parent, s->tri_sorted, s->nodes,
                                                                      (int*)s->flags, s->leaf_box);
     RT_PROF(ctx, 6);

@@ -96,7 +96,7 @@ class GpuTlas:
         ms = np.zeros(6, np.float32)
         check(lib().rt_bvh_build_profiled(self.ctx.handle, self.handle, bits, ptr(ms)))
         self.bits = bits
-        return dict(zip(("bounds", "morton", "histogram", "radix_passes", "slot_init", "emit_refit"), map(float, ms)))
+        return dict(zip(("bounds", "morton_hist", "unused", "radix_passes", "slot_init", "emit_refit"), map(float, ms)))
 
     def info(self):
         root = np.empty(6, np.float32)
