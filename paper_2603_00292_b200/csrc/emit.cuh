@@ -1,0 +1,169 @@
+// emit.cuh -- K4+K5: fused Karras emission + bottom-up refit (included by lbvh.cu
+// inside its anonymous namespace; uses load_tri / tri_box / adj_delta from there).
+//
+// One thread per leaf climbs the tree (Apetrei 2014's agglomerative scheme): a
+// node covering keys [l, r] is the LEFT child of its parent iff
+// delta(r, r+1) > delta(l-1, l) (no ties exist for index-augmented keys).
+// Siblings meet at the parent's split slot gamma: the first arrival publishes
+// its box and leaves, the second builds the parent.  Karras's numbering
+// (internal 0..n-2, root 0) is recovered exactly: a left child is numbered by
+// its right end, a right child by its left end, so child / parent arrays equal
+// the split-search construction bit for bit (oracle orc_lbvh_karras/refit).
+//
+// Phase A (per block of EMIT_T leaves [B, E)): pairs whose sibling starts
+// inside the block meet in SHARED memory (ATOMS exchange, delta read from a
+// per-block smem table) -- no global latency on the chain.  A node whose
+// sibling starts outside the block is deferred.  Phase B (after one barrier):
+// deferred nodes and smem slots that saw a single arrival (the sibling
+// extends past the block) climb through the global slots: a release exchange
+// after st.cg of the box, the sibling's box read with ld.cg (no device-scope
+// acquire fence, which would invalidate the whole L1 on every rendezvous).
+//
+// node layout (Aila-Laine): n0 = (L.lo.x, L.hi.x, L.lo.y, L.hi.y)
+//                           n1 = (R.lo.x, R.hi.x, R.lo.y, R.hi.y)
+//                           n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
+//                           n3 = (left id, right id, height, 0)   id < 0: ~leaf
+#pragma once
+
+struct EmitNode {
+    int l, r, h, dl, dr;
+    float lo[3], hi[3];
+};
+
+// Emit the parent of N (N is the left child iff `left`) whose sibling brought
+// `other` (its far endpoint) and box (s0 = lo + height, s1 = hi); pdl / pdr are
+// delta at the parent's boundaries.  N becomes the parent.  Returns true at the root.
+__device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
+                                            float4* __restrict__ nodes, EmitNode& N, bool left, int gamma, int pl,
+                                            int pr, int pdl, int pdr, const float4 s0, const float4 s1) {
+    const int cl = (pl == gamma) ? ~gamma : gamma;
+    const int cr = (pr == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+    float llo[3], lhi[3], rlo[3], rhi[3];
+    const float so[3] = {s0.x, s0.y, s0.z}, sh[3] = {s1.x, s1.y, s1.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        llo[a] = left ? N.lo[a] : so[a]; lhi[a] = left ? N.hi[a] : sh[a];
+        rlo[a] = left ? so[a] : N.lo[a]; rhi[a] = left ? sh[a] : N.hi[a];
+    }
+    const int hs = __float_as_int(s0.w);
+    const bool root = (pl == 0 && pr == n - 1);
+    const int P = root ? 0 : (pdr > pdl ? pr : pl);
+    N.h = 1 + (N.h > hs ? N.h : hs);
+    float4* nd = nodes + 4 * P;
+    nd[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
+    nd[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
+    nd[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
+    nd[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(N.h), 0.0f);
+    child[P] = make_int2(cl, cr);
+    parent[cl < 0 ? (n - 1) + ~cl : cl] = P;
+    parent[cr < 0 ? (n - 1) + ~cr : cr] = P;
+    if (root) parent[0] = -1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) { N.lo[a] = sel_min(llo[a], rlo[a]); N.hi[a] = sel_max(lhi[a], rhi[a]); }
+    N.l = pl; N.r = pr; N.dl = pdl; N.dr = pdr;
+    return root;
+}
+
+template <typename K>
+__device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __restrict__ child,
+                             int32_t* __restrict__ parent, float4* __restrict__ nodes, int* slot_range,
+                             float4* slot_box, EmitNode N) {
+    while (true) {
+        const bool left = N.dr > N.dl;
+        const int gamma = left ? N.r : N.l - 1;
+        const int side = left ? 0 : 1;
+        __stcg(slot_box + 4 * gamma + 2 * side, make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h)));
+        __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(N.hi[0], N.hi[1], N.hi[2], 0.0f));
+        cuda::atomic_ref<int, cuda::thread_scope_device> slot(slot_range[gamma]);
+        const int other = slot.exchange(left ? N.l : N.r, cuda::std::memory_order_release);
+        if (other < 0) return;                       // sibling subtree not finished
+        const float4 s0 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side));
+        const float4 s1 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side) + 1);
+        const int pl = left ? N.l : other, pr = left ? other : N.r;
+        const int pdl = adj_delta(keys, n, pl - 1), pdr = adj_delta(keys, n, pr);
+        if (emit_parent(n, child, parent, nodes, N, left, gamma, pl, pr, pdl, pdr, s0, s1)) return;
+    }
+}
+
+constexpr int EMIT_T = 256;
+
+template <typename K>
+__global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
+                                                           const float* __restrict__ tris, const uint32_t* __restrict__ mask,
+                                                           int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
+                                                           float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
+                                                           int* slot_range, float4* slot_box) {
+    __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
+    __shared__ int s_delta[EMIT_T + 1];         // delta(B - 1 + k)
+    __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, -)]
+    __shared__ EmitNode s_def[EMIT_T];          // deferred (boundary-crossing) nodes
+    __shared__ int s_ndef;
+    const int tid = threadIdx.x;
+    const int64_t B = (int64_t)blockIdx.x * EMIT_T;
+    const int64_t E = (B + EMIT_T < n) ? B + EMIT_T : n;
+    s_range[tid] = -1;
+    s_delta[tid] = adj_delta(keys, n, B - 1 + tid);
+    if (tid == 0) {
+        s_ndef = 0;
+        s_delta[EMIT_T] = adj_delta(keys, n, B - 1 + EMIT_T);
+    }
+    const int64_t i = B + tid;
+    EmitNode N;
+    if (i < E) {
+        const uint32_t id = order[i];
+        float t[9];
+        load_tri(tris, id, t);
+        tri_box(t, N.lo, N.hi);
+        tri_sorted[3 * i + 0] = make_float4(t[0], t[1], t[2], __int_as_float((int)id));
+        tri_sorted[3 * i + 1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask[id]));
+        tri_sorted[3 * i + 2] = make_float4(t[6], t[7], t[8], 0.0f);
+        N.l = N.r = (int)i;
+        N.h = 0;
+    }
+    __syncthreads();
+    if (i < E) {
+        N.dl = s_delta[tid];            // delta(i - 1)
+        N.dr = s_delta[tid + 1];        // delta(i)
+        while (true) {
+            const bool left = N.dr > N.dl;
+            const bool inside = left ? (N.r + 1 < E) : (N.l - 1 >= B);
+            if (!inside) {
+                s_def[atomicAdd(&s_ndef, 1)] = N;
+                break;
+            }
+            const int gamma = left ? N.r : N.l - 1;
+            const int g = gamma - (int)B, side = left ? 0 : 1;
+            s_box[g][side][0] = make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h));
+            s_box[g][side][1] = make_float4(N.hi[0], N.hi[1], N.hi[2], 0.0f);
+            __threadfence_block();
+            const int other = atomicExch(&s_range[g], left ? N.l : N.r);
+            if (other < 0) break;                    // first arrival: pending in smem
+            __threadfence_block();
+            s_range[g] = -2;                         // pair complete
+            const int pl = left ? N.l : other, pr = left ? other : N.r;
+            // the parent lies inside the block, so its boundary deltas are in smem
+            const int pdl = s_delta[pl - (int)B], pdr = s_delta[pr - (int)B + 1];
+            if (emit_parent(n, child, parent, nodes, N, left, gamma, pl, pr, pdl, pdr, s_box[g][1 - side][0],
+                            s_box[g][1 - side][1]))
+                break;                               // root (whole tree inside one block)
+        }
+    }
+    __syncthreads();
+    // phase B: smem slot `tid` left with a single arrival, then deferred node `tid`
+    if (tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0) {
+        const int endpoint = s_range[tid];
+        const int gamma = (int)B + tid;
+        const bool left = endpoint <= gamma;         // left child: [endpoint, gamma]; right: [gamma+1, endpoint]
+        const float4 lo4 = s_box[tid][left ? 0 : 1][0], hi4 = s_box[tid][left ? 0 : 1][1];
+        EmitNode M;
+        M.l = left ? endpoint : gamma + 1;
+        M.r = left ? gamma : endpoint;
+        M.h = __float_as_int(lo4.w);
+        M.lo[0] = lo4.x; M.lo[1] = lo4.y; M.lo[2] = lo4.z;
+        M.hi[0] = hi4.x; M.hi[1] = hi4.y; M.hi[2] = hi4.z;
+        M.dl = s_delta[M.l - (int)B];
+        M.dr = s_delta[M.r - (int)B + 1];
+        climb_global(keys, n, child, parent, nodes, slot_range, slot_box, M);
+    }
+    if (tid < s_ndef) climb_global(keys, n, child, parent, nodes, slot_range, slot_box, s_def[tid]);
+}

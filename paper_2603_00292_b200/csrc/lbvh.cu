@@ -272,155 +272,7 @@ __device__ __forceinline__ int adj_delta(const K* __restrict__ k, int64_t n, int
     return (int)(8 * sizeof(K)) + __clz((unsigned)i ^ (unsigned)(i + 1));
 }
 
-// One climbing node: keys [l, r], its box, subtree height and boundary deltas.
-struct EmitNode {
-    int l, r, h, dl, dr;
-    float lo[3], hi[3];
-};
-
-// Second arrival at split slot gamma: emit the parent (Karras numbering) and
-// make it the current node.  Returns true when the parent is the root.
-template <typename K>
-__device__ __forceinline__ bool emit_parent(const K* __restrict__ keys, int64_t n, int2* __restrict__ child,
-                                            int32_t* __restrict__ parent, float4* __restrict__ nodes, EmitNode& N,
-                                            bool left, int gamma, int other, const float4 s0, const float4 s1) {
-    const int pl = left ? N.l : other, pr = left ? other : N.r;
-    // children in Karras encoding: left = gamma, right = gamma + 1 (leaf if a single key)
-    const int cl = (pl == gamma) ? ~gamma : gamma;
-    const int cr = (pr == gamma + 1) ? ~(gamma + 1) : gamma + 1;
-    float llo[3], lhi[3], rlo[3], rhi[3];
-    const float so[3] = {s0.x, s0.y, s0.z}, sh[3] = {s1.x, s1.y, s1.z};
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-        llo[a] = left ? N.lo[a] : so[a]; lhi[a] = left ? N.hi[a] : sh[a];
-        rlo[a] = left ? so[a] : N.lo[a]; rhi[a] = left ? sh[a] : N.hi[a];
-    }
-    const int hs = __float_as_int(s0.w);
-    // the parent's own number is its side at the next level (root -> 0)
-    const int pdl = adj_delta(keys, n, pl - 1), pdr = adj_delta(keys, n, pr);
-    const bool root = (pl == 0 && pr == n - 1);
-    const int P = root ? 0 : (pdr > pdl ? pr : pl);
-    N.h = 1 + (N.h > hs ? N.h : hs);
-    float4* nd = nodes + 4 * P;
-    nd[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
-    nd[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
-    nd[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
-    nd[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(N.h), 0.0f);
-    child[P] = make_int2(cl, cr);
-    parent[cl < 0 ? (n - 1) + ~cl : cl] = P;
-    parent[cr < 0 ? (n - 1) + ~cr : cr] = P;
-    if (root) parent[0] = -1;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) { N.lo[a] = sel_min(llo[a], rlo[a]); N.hi[a] = sel_max(lhi[a], rhi[a]); }
-    N.l = pl; N.r = pr; N.dl = pdl; N.dr = pdr;
-    return root;
-}
-
-// Global climb (nodes whose rendezvous crosses a block's leaf range)
-template <typename K>
-__device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __restrict__ child,
-                             int32_t* __restrict__ parent, float4* __restrict__ nodes, int* slot_range,
-                             float4* slot_box, EmitNode N) {
-    while (true) {
-        const bool left = N.dr > N.dl;
-        const int gamma = left ? N.r : N.l - 1;
-        const int side = left ? 0 : 1;
-        __stcg(slot_box + 4 * gamma + 2 * side, make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h)));
-        __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(N.hi[0], N.hi[1], N.hi[2], 0.0f));
-        cuda::atomic_ref<int, cuda::thread_scope_device> slot(slot_range[gamma]);
-        const int other = slot.exchange(left ? N.l : N.r, cuda::std::memory_order_acq_rel);
-        if (other < 0) return;                       // sibling subtree not finished
-        const float4 s0 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side));
-        const float4 s1 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side) + 1);
-        if (emit_parent(keys, n, child, parent, nodes, N, left, gamma, other, s0, s1)) return;
-    }
-}
-
-// Phase A: a block owns leaves [B, E).  A pair of siblings that both start in
-// the block meets in a SHARED-memory slot (block-scope acq_rel exchange); a node
-// whose sibling starts outside the block is deferred.  Phase B (after one
-// __syncthreads): deferred nodes and smem slots that saw only one arrival (the
-// sibling extends past the block) move to the global slots and climb there.
-// All subtrees inside a block therefore finish with ~30-cycle smem rendezvous
-// instead of L2 atomics, and only O(log) boundary nodes per block go global.
-constexpr int EMIT_T = 256;
-
-template <typename K>
-__global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
-                                                           const float* __restrict__ tris, const uint32_t* __restrict__ mask,
-                                                           int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
-                                                           float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
-                                                           int* slot_range, float4* slot_box) {
-    __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
-    __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, side)]
-    __shared__ EmitNode s_def[EMIT_T];          // deferred (boundary-crossing) nodes
-    __shared__ int s_ndef;
-    const int tid = threadIdx.x;
-    const int64_t B = (int64_t)blockIdx.x * EMIT_T;
-    const int64_t E = (B + EMIT_T < n) ? B + EMIT_T : n;
-    s_range[tid] = -1;
-    if (tid == 0) s_ndef = 0;
-    __syncthreads();
-    const int64_t i = B + tid;
-    if (i < E) {
-        EmitNode N;
-        {
-            const uint32_t id = order[i];
-            float t[9];
-            load_tri(tris, id, t);
-            tri_box(t, N.lo, N.hi);
-            tri_sorted[3 * i + 0] = make_float4(t[0], t[1], t[2], __int_as_float((int)id));
-            tri_sorted[3 * i + 1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask[id]));
-            tri_sorted[3 * i + 2] = make_float4(t[6], t[7], t[8], 0.0f);
-        }
-        N.l = N.r = (int)i;
-        N.h = 0;
-        N.dl = adj_delta(keys, n, N.l - 1);
-        N.dr = adj_delta(keys, n, N.r);
-        while (true) {
-            const bool left = N.dr > N.dl;
-            const bool inside = left ? (N.r + 1 < E) : (N.l - 1 >= B);
-            if (!inside) {
-                s_def[atomicAdd(&s_ndef, 1)] = N;
-                break;
-            }
-            const int gamma = left ? N.r : N.l - 1;
-            const int g = gamma - (int)B, side = left ? 0 : 1;
-            s_box[g][side][0] = make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h));
-            s_box[g][side][1] = make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(side));
-            cuda::atomic_ref<int, cuda::thread_scope_block> slot(s_range[g]);
-            const int other = slot.exchange(left ? N.l : N.r, cuda::std::memory_order_acq_rel);
-            if (other < 0) break;                    // first arrival: pending in smem
-            s_range[g] = -2;                         // pair complete
-            if (emit_parent(keys, n, child, parent, nodes, N, left, gamma, other, s_box[g][1 - side][0],
-                            s_box[g][1 - side][1]))
-                break;                               // root (whole tree inside one block)
-        }
-    }
-    __syncthreads();
-    // phase B: smem slot `tid` left with a single arrival, then deferred node `tid`
-    if (tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0) {
-        const float4 a = s_box[tid][0][0], b = s_box[tid][0][1], c = s_box[tid][1][0], d = s_box[tid][1][1];
-        // the written side is the one whose hi.w carries its side tag (0 or 1); the slot
-        // data of the empty side is stale, so identify it from the exchanged endpoint
-        EmitNode N;
-        const int endpoint = s_range[tid];
-        const int gamma = (int)B + tid;
-        // left child: [endpoint, gamma]; right child: [gamma + 1, endpoint]
-        const bool left = endpoint <= gamma;
-        const float4 lo4 = left ? a : c, hi4 = left ? b : d;
-        N.l = left ? endpoint : gamma + 1;
-        N.r = left ? gamma : endpoint;
-        N.h = __float_as_int(lo4.w);
-        N.lo[0] = lo4.x; N.lo[1] = lo4.y; N.lo[2] = lo4.z;
-        N.hi[0] = hi4.x; N.hi[1] = hi4.y; N.hi[2] = hi4.z;
-        N.dl = adj_delta(keys, n, N.l - 1);
-        N.dr = adj_delta(keys, n, N.r);
-        climb_global(keys, n, child, parent, nodes, slot_range, slot_box, N);
-    }
-    if (tid < s_ndef) climb_global(keys, n, child, parent, nodes, slot_range, slot_box, s_def[tid]);
-}
-
+#include "emit.cuh"
 
 // n == 1: a root whose left child is leaf 0 and whose right box is empty
 __global__ void single_leaf_root(const float* tris, const uint32_t* mask, float4* nodes, float4* tri_sorted,
