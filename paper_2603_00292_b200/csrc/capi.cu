@@ -154,6 +154,7 @@ int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normal
     ALLOC(s->mat_emissive, sizeof(float4) * n_mat);
     ALLOC(s->nodes, sizeof(float4) * 4 * ni);
     ALLOC(s->tri_sorted, sizeof(float4) * 3 * n);
+    ALLOC(s->bvh4, sizeof(float4) * 8 * ni);
     ALLOC(s->keys_a, sizeof(uint64_t) * n);
     ALLOC(s->keys_b, sizeof(uint64_t) * n);
     ALLOC(s->vals_a, sizeof(uint32_t) * n);
@@ -192,7 +193,7 @@ void rt_scene_destroy(rt_scene* s) {
     if (!s) return;
     rt_render_release(s);
     void* ptrs[] = {s->tris, s->tri_attr, s->tri_inst, s->tri_prim, s->tri_mask, s->mat_color, s->mat_emissive,
-                    s->nodes, s->tri_sorted, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->parent, s->child,
+                    s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->parent, s->child,
                     s->flags, s->cbounds, s->cb_enc, s->sort_scratch, s->leaf_box};
     for (void* p : ptrs)
         if (p) cudaFree(p);

@@ -85,6 +85,59 @@ __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __rest
     }
 }
 
+// BVH4 view for traversal: for EVERY binary internal node p, a 128-B node whose
+// up-to-4 children are p's grandchildren (a leaf child of p stays a leaf).  A
+// traversal from the root only ever reaches even-depth nodes, so the node id of
+// the BVH4 node equals the binary node id (the odd-depth entries are built but
+// unused: one dependency-free thread per node, no depth computation).
+// layout (SoA over the 4 slots): x_lo, x_hi, y_lo, y_hi, z_lo, z_hi (float4 each),
+// then int4 child ids (>= 0 internal, < 0 ~leaf) and (height, 0, 0, 0).
+__global__ void __launch_bounds__(256) bvh4_collapse_kernel(int64_t n, const float4* __restrict__ nodes,
+                                                           float4* __restrict__ bvh4) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= n - 1) return;
+    const float4* nd = nodes + 4 * p;
+    const float4 a0 = __ldg(nd), a1 = __ldg(nd + 1), a2 = __ldg(nd + 2), a3 = __ldg(nd + 3);
+    // a child slot: box (6 floats) + id; an internal child expands into its two children
+    struct Slot { float lx, hx, ly, hy, lz, hz; int id; };
+    const Slot empty = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY, ~0};
+    Slot L0, L1 = empty, R0, R1 = empty;
+    const int cl = __float_as_int(a3.x), cr = __float_as_int(a3.y);
+    if (cl < 0) {
+        L0 = {a0.x, a0.y, a0.z, a0.w, a2.x, a2.y, cl};
+    } else {
+        const float4* cn = nodes + 4 * cl;
+        const float4 b0 = __ldg(cn), b1 = __ldg(cn + 1), b2 = __ldg(cn + 2), b3 = __ldg(cn + 3);
+        L0 = {b0.x, b0.y, b0.z, b0.w, b2.x, b2.y, __float_as_int(b3.x)};
+        L1 = {b1.x, b1.y, b1.z, b1.w, b2.z, b2.w, __float_as_int(b3.y)};
+    }
+    if (cr < 0) {
+        R0 = {a1.x, a1.y, a1.z, a1.w, a2.z, a2.w, cr};
+    } else {
+        const float4* cn = nodes + 4 * cr;
+        const float4 b0 = __ldg(cn), b1 = __ldg(cn + 1), b2 = __ldg(cn + 2), b3 = __ldg(cn + 3);
+        R0 = {b0.x, b0.y, b0.z, b0.w, b2.x, b2.y, __float_as_int(b3.x)};
+        R1 = {b1.x, b1.y, b1.z, b1.w, b2.z, b2.w, __float_as_int(b3.y)};
+    }
+    // pack: L0, (L1), R0, (R1); unused slots stay empty
+    const bool l2 = cl >= 0, r2 = cr >= 0;
+    const Slot s0 = L0, s1 = l2 ? L1 : R0, s2 = l2 ? R0 : (r2 ? R1 : empty), s3 = (l2 && r2) ? R1 : empty;
+    const float lox[4] = {s0.lx, s1.lx, s2.lx, s3.lx}, hix[4] = {s0.hx, s1.hx, s2.hx, s3.hx};
+    const float loy[4] = {s0.ly, s1.ly, s2.ly, s3.ly}, hiy[4] = {s0.hy, s1.hy, s2.hy, s3.hy};
+    const float loz[4] = {s0.lz, s1.lz, s2.lz, s3.lz}, hiz[4] = {s0.hz, s1.hz, s2.hz, s3.hz};
+    const int cid[4] = {s0.id, s1.id, s2.id, s3.id};
+    float4* q = bvh4 + 8 * p;
+    q[0] = make_float4(lox[0], lox[1], lox[2], lox[3]);
+    q[1] = make_float4(hix[0], hix[1], hix[2], hix[3]);
+    q[2] = make_float4(loy[0], loy[1], loy[2], loy[3]);
+    q[3] = make_float4(hiy[0], hiy[1], hiy[2], hiy[3]);
+    q[4] = make_float4(loz[0], loz[1], loz[2], loz[3]);
+    q[5] = make_float4(hiz[0], hiz[1], hiz[2], hiz[3]);
+    q[6] = make_float4(__int_as_float(cid[0]), __int_as_float(cid[1]), __int_as_float(cid[2]),
+                       __int_as_float(cid[3]));
+    q[7] = make_float4(a3.z, 0.0f, 0.0f, 0.0f);     // binary height (stack bound)
+}
+
 constexpr int EMIT_T = 256;
 
 template <typename K>

@@ -337,6 +337,7 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     lbvh_emit_kernel<K><<<(unsigned)((n + EMIT_T - 1) / EMIT_T), EMIT_T, 0, st>>>(kin, vin, s->tris, s->tri_mask, n, s->child,
                                                                      s->parent, s->tri_sorted, s->nodes,
                                                                      (int*)s->flags, s->leaf_box);
+    bvh4_collapse_kernel<<<(unsigned)((n - 1 + 255) / 256), 256, 0, st>>>(n, s->nodes, s->bvh4);
     RT_PROF(ctx, 6);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
@@ -348,6 +349,7 @@ int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits) {
     if (s->n == 1) {
         single_leaf_root<<<1, 1, 0, ctx->stream>>>(s->tris, s->tri_mask, s->nodes, s->tri_sorted, s->leaf_box,
                                                    s->vals_a);
+        bvh4_collapse_kernel<<<1, 1, 0, ctx->stream>>>(2, s->nodes, s->bvh4);   // root node 0 only
         RT_CUDA_TRY(cudaGetLastError());
         return RT_OK;
     }

@@ -14,6 +14,9 @@
 namespace {
 
 constexpr int MEGA_THREADS = 128;
+#ifndef MEGA_MIN_BLOCKS
+#define MEGA_MIN_BLOCKS 7       // 72 registers: the 4-wide walk + PT shading without spills
+#endif
 constexpr int WF_THREADS = 256;
 
 struct FrameConst {
@@ -133,16 +136,17 @@ __device__ __forceinline__ bool shade_bounce(const FrameConst& F, const float4* 
 // ---- K7: megakernel --------------------------------------------------------
 // Persistent warps fetch 32 pixels at a time; each lane renders samples
 // [s0, s1) of its pixel in order and adds the sums to accum once.
-__global__ void __launch_bounds__(MEGA_THREADS, 8) pt_megakernel(
-    const FrameConst F, int s0, int s1, const float4* __restrict__ nodes, const float4* __restrict__ tris,
-    const float4* __restrict__ attr, const float4* __restrict__ mat_color, const float4* __restrict__ mat_emis,
-    float4* __restrict__ accum, unsigned int* counter, unsigned long long* ray_total, int* err) {
+__global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
+    const FrameConst F, int s0, int s1, const float4* __restrict__ nodes, const float4* __restrict__ bvh4,
+    const float4* __restrict__ tris, const float4* __restrict__ attr, const float4* __restrict__ mat_color,
+    const float4* __restrict__ mat_emis, float4* __restrict__ accum, unsigned int* counter,
+    unsigned long long* ray_total, int* err) {
     const int height = __float_as_int(__ldg(nodes + 3).z);
     if (height + 1 > RT_STACK) {
         if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
         return;
     }
-    int stack[RT_STACK];
+    int stack[RT_STACK4];
     const int lane = threadIdx.x & 31;
     unsigned long long rays = 0;
     const int max_depth = F.integ == RT_INTEG_EYE ? 1 : F.max_depth;
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(MEGA_THREADS, 8) pt_megakernel(
                     RayPre R;
                     ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
                     uint32_t nt, nv;
-                    HitRec h = trace_ray<false>(nodes, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+                    HitRec h = trace_ray4<false>(bvh4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
                     ++rays;
                     if (!shade_bounce(F, attr, mat_color, mat_emis, h, P)) break;
                 }
@@ -211,9 +215,15 @@ __global__ void __launch_bounds__(WF_THREADS) wf_raygen(const FrameConst F, cons
 }
 
 // extend: closest hit for every queued path (depth 0: identity queue)
-__global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ nodes, const float4* __restrict__ tris,
-                                                 Wave W, int depth, unsigned int* counter) {
-    int stack[RT_STACK];
+__global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ nodes, const float4* __restrict__ bvh4,
+                                                    const float4* __restrict__ tris, Wave W, int depth,
+                                                    unsigned int* counter, int* err) {
+    const int height = __float_as_int(__ldg(nodes + 3).z);
+    if (height + 1 > RT_STACK) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
+        return;
+    }
+    int stack[RT_STACK4];
     const unsigned n = W.count[depth];
     const int* q = depth == 0 ? nullptr : W.queue[depth & 1];
     const int lane = threadIdx.x & 31;
@@ -230,7 +240,7 @@ __global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ n
             RayPre R;
             ray_setup(R, a.x, a.y, a.z, b.x, b.y, b.z, a.w);
             uint32_t nt, nv;
-            HitRec h = trace_ray<false>(nodes, tris, R, b.w, RT_FULL, stack, nt, nv);
+            HitRec h = trace_ray4<false>(bvh4, tris, R, b.w, RT_FULL, stack, nt, nv);
             W.hit[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
             }
         }
@@ -430,7 +440,8 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         int64_t grid = (int64_t)ctx->num_sms * bps;
         int64_t want = (F.nunits + MEGA_THREADS - 1) / MEGA_THREADS;
         if (grid > want) grid = want;
-        pt_megakernel<<<(unsigned)grid, MEGA_THREADS, 0, st>>>(F, p->s0, p->s1, s->nodes, s->tri_sorted, s->tri_attr,
+        pt_megakernel<<<(unsigned)grid, MEGA_THREADS, 0, st>>>(F, p->s0, p->s1, s->nodes, s->bvh4, s->tri_sorted,
+                                                               s->tri_attr,
                                                                s->mat_color, s->mat_emissive, acc, ctx->d_counter,
                                                                d_rays, ctx->d_error);
         RT_CUDA_TRY(cudaGetLastError());
@@ -455,7 +466,8 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         RT_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         wf_raygen<<<grid_sh, WF_THREADS, 0, cap>>>(F, wb->d_sample, wb->W);
         for (int d = 0; d < md; ++d) {
-            wf_extend<<<grid_ext, 128, 0, cap>>>(s->nodes, s->tri_sorted, wb->W, d, ctx->d_counter);
+            wf_extend<<<grid_ext, 128, 0, cap>>>(s->nodes, s->bvh4, s->tri_sorted, wb->W, d, ctx->d_counter,
+                                                 ctx->d_error);
             wf_shade<<<grid_sh, WF_THREADS, 0, cap>>>(F, s->tri_attr, s->mat_color, s->mat_emissive, wb->W, d);
         }
         wf_accumulate<<<grid_sh, WF_THREADS, 0, cap>>>(F, wb->W, acc, wb->d_sample, ctx->d_counter, d_rays);

@@ -45,6 +45,7 @@ struct rt_scene {
     int bits;
     float4* nodes;        // (max(n-1,1), 4) BVH2 nodes: child boxes + child ids + height
     float4* tri_sorted;   // (n, 3) leaf-ordered vertices; v0.w = flat id, v1.w = mask
+    float4* bvh4;         // (max(n-1,1), 8) 4-wide traversal view (grandchildren of each binary node)
     // build scratch
     void* keys_a; void* keys_b;     // u32 or u64 Morton keys
     uint32_t* vals_a; uint32_t* vals_b;

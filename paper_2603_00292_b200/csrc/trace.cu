@@ -11,15 +11,15 @@ constexpr int TRACE_THREADS = 128;
 // warp), every lane runs the while-while traversal, then the warp fetches again.
 template <bool STATS>
 __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
-    const float4* __restrict__ nodes, const float4* __restrict__ tris, int64_t n, const float* __restrict__ rays,
-    float4* __restrict__ hits, uint32_t ray_mask, uint32_t* __restrict__ stats, unsigned int* counter,
-    int* err) {
+    const float4* __restrict__ nodes, const float4* __restrict__ bvh4, const float4* __restrict__ tris, int64_t n,
+    const float* __restrict__ rays, float4* __restrict__ hits, uint32_t ray_mask, uint32_t* __restrict__ stats,
+    unsigned int* counter, int* err) {
     const int height = __float_as_int(__ldg(nodes + 3).z);   // root height == stack bound
     if (height + 1 > RT_STACK) {
         if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
         return;
     }
-    int stack[RT_STACK];
+    int stack[RT_STACK4];
     const int lane = threadIdx.x & 31;
     while (true) {
         unsigned base = 0;
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
             RayPre R;
             ray_setup(R, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
             uint32_t nt = 0, nv = 0;
-            HitRec h = trace_ray<STATS>(nodes, tris, R, r.tmax, ray_mask, stack, nt, nv);
+            HitRec h = trace_ray4<STATS>(bvh4, tris, R, r.tmax, ray_mask, stack, nt, nv);
             hits[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
             if (STATS) reinterpret_cast<uint2*>(stats)[i] = make_uint2(nt, nv);
         }
@@ -88,10 +88,10 @@ int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4
     if (grid > want) grid = want;
     if (stats)
         trace_closest_kernel<true><<<(unsigned)grid, TRACE_THREADS, 0, st>>>(
-            s->nodes, s->tri_sorted, n, rays, hits, mask, stats, ctx->d_counter, ctx->d_error);
+            s->nodes, s->bvh4, s->tri_sorted, n, rays, hits, mask, stats, ctx->d_counter, ctx->d_error);
     else
         trace_closest_kernel<false><<<(unsigned)grid, TRACE_THREADS, 0, st>>>(
-            s->nodes, s->tri_sorted, n, rays, hits, mask, nullptr, ctx->d_counter, ctx->d_error);
+            s->nodes, s->bvh4, s->tri_sorted, n, rays, hits, mask, nullptr, ctx->d_counter, ctx->d_error);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }

@@ -119,6 +119,64 @@ struct HitRec {
     float u, v;
 };
 
+__device__ __forceinline__ void cswap(float& ta, int& ca, float& tb, int& cb) {
+    if (tb < ta) {
+        float t = ta; ta = tb; tb = t;
+        int c = ca; ca = cb; cb = c;
+    }
+}
+
+// 4-wide traversal over the BVH4 view (emit.cuh bvh4_collapse_kernel): one
+// 112-B node fetch tests 4 child boxes, children visited nearest first, so a
+// ray makes about half the dependent node fetches of the binary walk.  Same
+// triangle test, tie rule and conservative slab test as trace_ray.  The stack
+// holds at most 3 * ceil(height / 2) entries (checked by the caller).
+template <bool STATS>
+__device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, const float4* __restrict__ tris,
+                                             const RayPre& R, float tmax, uint32_t ray_mask, int* stack,
+                                             uint32_t& n_tests, uint32_t& n_visits) {
+    HitRec h;
+    h.t = tmax; h.id = -1; h.u = 0.f; h.v = 0.f;
+    int sp = 0;
+    stack[0] = RT_SENTINEL;
+    int node = 0;
+    while (node != RT_SENTINEL) {
+        if (node >= 0) {
+            const float4* q = bvh4 + 8 * node;
+            const float4 xl = __ldg(q), xh = __ldg(q + 1), yl = __ldg(q + 2), yh = __ldg(q + 3);
+            const float4 zl = __ldg(q + 4), zh = __ldg(q + 5), cc = __ldg(q + 6);
+            if (STATS) ++n_visits;
+            float t0 = box_enter(R, xl.x, xh.x, yl.x, yh.x, zl.x, zh.x, h.t);
+            float t1 = box_enter(R, xl.y, xh.y, yl.y, yh.y, zl.y, zh.y, h.t);
+            float t2 = box_enter(R, xl.z, xh.z, yl.z, yh.z, zl.z, zh.z, h.t);
+            float t3 = box_enter(R, xl.w, xh.w, yl.w, yh.w, zl.w, zh.w, h.t);
+            int c0 = __float_as_int(cc.x), c1 = __float_as_int(cc.y), c2 = __float_as_int(cc.z),
+                c3 = __float_as_int(cc.w);
+            cswap(t0, c0, t1, c1);
+            cswap(t2, c2, t3, c3);
+            cswap(t0, c0, t2, c2);
+            cswap(t1, c1, t3, c3);
+            cswap(t1, c1, t2, c2);
+            if (t3 != INFINITY) stack[++sp] = c3;
+            if (t2 != INFINITY) stack[++sp] = c2;
+            if (t1 != INFINITY) stack[++sp] = c1;
+            node = (t0 != INFINITY) ? c0 : stack[sp--];
+        } else {
+            const float4* tp = tris + 3 * (~node);
+            const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+            if (STATS) ++n_tests;
+            if (__float_as_uint(b.w) & ray_mask) tri_test(R, a, b, c, h.t, h.id, h.u, h.v);
+            node = stack[sp--];
+        }
+    }
+    if (h.id < 0) h.t = -1.0f;
+    return h;
+}
+
+// Stack of the 4-wide walk: at most 3 pushes per BVH4 level and ceil(h/2) levels
+// for a binary tree of height h <= RT_STACK - 1 (the depth limit the build enforces).
+#define RT_STACK4 (3 * (RT_STACK / 2) + 4)
+
 // Persistent-thread while-while traversal (Aila & Laine 2009) for ONE ray per
 // lane; the calling warp may be partially active.  nodes: BVH2 (4 float4 per
 // internal node), tris: leaf-ordered (3 float4 per leaf).  Returns id -1 on miss.
