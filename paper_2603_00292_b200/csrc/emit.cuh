@@ -27,15 +27,47 @@
 
 struct EmitNode {
     int l, r, h, dl, dr;
+    int g;                 // split position this node was created at (BVH4 index); -1 for a leaf
     float lo[3], hi[3];
 };
 
+// BVH4 view, indexed by binary SPLIT position: the BVH4 node of the binary node
+// with split g holds that node's up-to-4 grandchildren (a leaf child stays a
+// leaf).  Each binary node knows its parent's split as soon as it exists (the
+// side test), so it writes its own half -- slots 2*side, 2*side+1 = its two
+// children, or itself if a leaf -- with no cross-thread reads.  SoA layout per
+// node: x_lo, x_hi, y_lo, y_hi, z_lo, z_hi (float4 over the 4 slots), then the 4
+// child ids (split position of an internal grandchild, ~leaf for a leaf).
+__device__ __forceinline__ void bvh4_write_half(float4* __restrict__ bvh4, int pgamma, int side, const float a_lo[3],
+                                                const float a_hi[3], int a_id, const float b_lo[3],
+                                                const float b_hi[3], int b_id) {
+    float* q = reinterpret_cast<float*>(bvh4 + 8 * (int64_t)pgamma) + 2 * side;
+    *reinterpret_cast<float2*>(q + 0) = make_float2(a_lo[0], b_lo[0]);
+    *reinterpret_cast<float2*>(q + 4) = make_float2(a_hi[0], b_hi[0]);
+    *reinterpret_cast<float2*>(q + 8) = make_float2(a_lo[1], b_lo[1]);
+    *reinterpret_cast<float2*>(q + 12) = make_float2(a_hi[1], b_hi[1]);
+    *reinterpret_cast<float2*>(q + 16) = make_float2(a_lo[2], b_lo[2]);
+    *reinterpret_cast<float2*>(q + 20) = make_float2(a_hi[2], b_hi[2]);
+    *reinterpret_cast<int2*>(q + 24) = make_int2(a_id, b_id);
+}
+
+// a leaf writes itself + an empty slot into its parent's BVH4 node
+__device__ __forceinline__ void bvh4_write_leaf(float4* __restrict__ bvh4, const EmitNode& N) {
+    const bool left = N.dr > N.dl;
+    if (N.dr < 0 && N.dl < 0) return;                // n == 1: no parent
+    const float elo[3] = {INFINITY, INFINITY, INFINITY}, ehi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    bvh4_write_half(bvh4, left ? N.r : N.l - 1, left ? 0 : 1, N.lo, N.hi, ~N.l, elo, ehi, ~0);
+}
+
 // Emit the parent of N (N is the left child iff `left`) whose sibling brought
-// `other` (its far endpoint) and box (s0 = lo + height, s1 = hi); pdl / pdr are
-// delta at the parent's boundaries.  N becomes the parent.  Returns true at the root.
+// `other` (its far endpoint), box (s0 = lo + height, s1 = hi + its split g);
+// pdl / pdr are delta at the parent's boundaries.  N becomes the parent, which
+// also writes its half of ITS parent's BVH4 node (or records the BVH4 root).
+// Returns true at the root.
 __device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
-                                            float4* __restrict__ nodes, EmitNode& N, bool left, int gamma, int pl,
-                                            int pr, int pdl, int pdr, const float4 s0, const float4 s1) {
+                                            float4* __restrict__ nodes, float4* __restrict__ bvh4, EmitNode& N,
+                                            bool left, int gamma, int pl, int pr, int pdl, int pdr,
+                                            const float4 s0, const float4 s1) {
     const int cl = (pl == gamma) ? ~gamma : gamma;
     const int cr = (pr == gamma + 1) ? ~(gamma + 1) : gamma + 1;
     float llo[3], lhi[3], rlo[3], rhi[3];
@@ -45,35 +77,42 @@ __device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child,
         llo[a] = left ? N.lo[a] : so[a]; lhi[a] = left ? N.hi[a] : sh[a];
         rlo[a] = left ? so[a] : N.lo[a]; rhi[a] = left ? sh[a] : N.hi[a];
     }
-    const int hs = __float_as_int(s0.w);
+    const int hs = __float_as_int(s0.w), gs = __float_as_int(s1.w);
+    // BVH4 ids of the two children: split position if internal, ~leaf otherwise
+    const int gl = (pl == gamma) ? ~gamma : (left ? N.g : gs);
+    const int gr = (pr == gamma + 1) ? ~(gamma + 1) : (left ? gs : N.g);
     const bool root = (pl == 0 && pr == n - 1);
-    const int P = root ? 0 : (pdr > pdl ? pr : pl);
+    const bool pleft = pdr > pdl;
+    const int P = root ? 0 : (pleft ? pr : pl);
     N.h = 1 + (N.h > hs ? N.h : hs);
     float4* nd = nodes + 4 * P;
     nd[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
     nd[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
     nd[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
-    nd[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(N.h), 0.0f);
+    // binary root: n3.w carries the BVH4 root index (the root's split position)
+    nd[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(N.h),
+                        __int_as_float(root ? gamma : 0));
     child[P] = make_int2(cl, cr);
     parent[cl < 0 ? (n - 1) + ~cl : cl] = P;
     parent[cr < 0 ? (n - 1) + ~cr : cr] = P;
     if (root) parent[0] = -1;
+    else bvh4_write_half(bvh4, pleft ? pr : pl - 1, pleft ? 0 : 1, llo, lhi, gl, rlo, rhi, gr);
 #pragma unroll
     for (int a = 0; a < 3; ++a) { N.lo[a] = sel_min(llo[a], rlo[a]); N.hi[a] = sel_max(lhi[a], rhi[a]); }
-    N.l = pl; N.r = pr; N.dl = pdl; N.dr = pdr;
+    N.l = pl; N.r = pr; N.dl = pdl; N.dr = pdr; N.g = gamma;
     return root;
 }
 
 template <typename K>
 __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __restrict__ child,
-                             int32_t* __restrict__ parent, float4* __restrict__ nodes, int* slot_range,
-                             float4* slot_box, EmitNode N) {
+                             int32_t* __restrict__ parent, float4* __restrict__ nodes, float4* __restrict__ bvh4,
+                             int* slot_range, float4* slot_box, EmitNode N) {
     while (true) {
         const bool left = N.dr > N.dl;
         const int gamma = left ? N.r : N.l - 1;
         const int side = left ? 0 : 1;
         __stcg(slot_box + 4 * gamma + 2 * side, make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h)));
-        __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(N.hi[0], N.hi[1], N.hi[2], 0.0f));
+        __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g)));
         cuda::atomic_ref<int, cuda::thread_scope_device> slot(slot_range[gamma]);
         const int other = slot.exchange(left ? N.l : N.r, cuda::std::memory_order_release);
         if (other < 0) return;                       // sibling subtree not finished
@@ -81,7 +120,7 @@ __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __rest
         const float4 s1 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side) + 1);
         const int pl = left ? N.l : other, pr = left ? other : N.r;
         const int pdl = adj_delta(keys, n, pl - 1), pdr = adj_delta(keys, n, pr);
-        if (emit_parent(n, child, parent, nodes, N, left, gamma, pl, pr, pdl, pdr, s0, s1)) return;
+        if (emit_parent(n, child, parent, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s0, s1)) return;
     }
 }
 
@@ -145,7 +184,8 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
                                                            const float* __restrict__ tris, const uint32_t* __restrict__ mask,
                                                            int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
                                                            float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
-                                                           int* slot_range, float4* slot_box) {
+                                                           float4* __restrict__ bvh4, int* slot_range,
+                                                           float4* slot_box) {
     __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
     __shared__ int s_delta[EMIT_T + 1];         // delta(B - 1 + k)
     __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, -)]
@@ -172,11 +212,13 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         tri_sorted[3 * i + 2] = make_float4(t[6], t[7], t[8], 0.0f);
         N.l = N.r = (int)i;
         N.h = 0;
+        N.g = -1;
     }
     __syncthreads();
     if (i < E) {
         N.dl = s_delta[tid];            // delta(i - 1)
         N.dr = s_delta[tid + 1];        // delta(i)
+        bvh4_write_leaf(bvh4, N);
         while (true) {
             const bool left = N.dr > N.dl;
             const bool inside = left ? (N.r + 1 < E) : (N.l - 1 >= B);
@@ -187,7 +229,7 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
             const int gamma = left ? N.r : N.l - 1;
             const int g = gamma - (int)B, side = left ? 0 : 1;
             s_box[g][side][0] = make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h));
-            s_box[g][side][1] = make_float4(N.hi[0], N.hi[1], N.hi[2], 0.0f);
+            s_box[g][side][1] = make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g));
             __threadfence_block();
             const int other = atomicExch(&s_range[g], left ? N.l : N.r);
             if (other < 0) break;                    // first arrival: pending in smem
@@ -196,7 +238,7 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
             const int pl = left ? N.l : other, pr = left ? other : N.r;
             // the parent lies inside the block, so its boundary deltas are in smem
             const int pdl = s_delta[pl - (int)B], pdr = s_delta[pr - (int)B + 1];
-            if (emit_parent(n, child, parent, nodes, N, left, gamma, pl, pr, pdl, pdr, s_box[g][1 - side][0],
+            if (emit_parent(n, child, parent, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s_box[g][1 - side][0],
                             s_box[g][1 - side][1]))
                 break;                               // root (whole tree inside one block)
         }
@@ -212,11 +254,12 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         M.l = left ? endpoint : gamma + 1;
         M.r = left ? gamma : endpoint;
         M.h = __float_as_int(lo4.w);
+        M.g = __float_as_int(hi4.w);
         M.lo[0] = lo4.x; M.lo[1] = lo4.y; M.lo[2] = lo4.z;
         M.hi[0] = hi4.x; M.hi[1] = hi4.y; M.hi[2] = hi4.z;
         M.dl = s_delta[M.l - (int)B];
         M.dr = s_delta[M.r - (int)B + 1];
-        climb_global(keys, n, child, parent, nodes, slot_range, slot_box, M);
+        climb_global(keys, n, child, parent, nodes, bvh4, slot_range, slot_box, M);
     }
-    if (tid < s_ndef) climb_global(keys, n, child, parent, nodes, slot_range, slot_box, s_def[tid]);
+    if (tid < s_ndef) climb_global(keys, n, child, parent, nodes, bvh4, slot_range, slot_box, s_def[tid]);
 }

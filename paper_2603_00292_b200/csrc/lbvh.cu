@@ -335,9 +335,8 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     RT_CUDA_TRY(cudaMemsetAsync(s->flags, 0xFF, sizeof(int) * (n - 1), st));   // split slots: empty
     RT_PROF(ctx, 5);
     lbvh_emit_kernel<K><<<(unsigned)((n + EMIT_T - 1) / EMIT_T), EMIT_T, 0, st>>>(kin, vin, s->tris, s->tri_mask, n, s->child,
-                                                                     s->parent, s->tri_sorted, s->nodes,
+                                                                     s->parent, s->tri_sorted, s->nodes, s->bvh4,
                                                                      (int*)s->flags, s->leaf_box);
-    bvh4_collapse_kernel<<<(unsigned)((n - 1 + 255) / 256), 256, 0, st>>>(n, s->nodes, s->bvh4);
     RT_PROF(ctx, 6);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;

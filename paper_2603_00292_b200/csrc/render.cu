@@ -142,11 +142,12 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     const float4* __restrict__ mat_emis, float4* __restrict__ accum, unsigned int* counter,
     unsigned long long* ray_total, int* err) {
     const int height = __float_as_int(__ldg(nodes + 3).z);
+    const int root4 = __float_as_int(__ldg(nodes + 3).w);
     if (height + 1 > RT_STACK) {
         if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
         return;
     }
-    int stack[RT_STACK4];
+    int2 stack[RT_STACK4];
     const int lane = threadIdx.x & 31;
     unsigned long long rays = 0;
     const int max_depth = F.integ == RT_INTEG_EYE ? 1 : F.max_depth;
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
                     RayPre R;
                     ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
                     uint32_t nt, nv;
-                    HitRec h = trace_ray4<false>(bvh4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+                    HitRec h = trace_ray4<false>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
                     ++rays;
                     if (!shade_bounce(F, attr, mat_color, mat_emis, h, P)) break;
                 }
@@ -219,11 +220,12 @@ __global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ n
                                                     const float4* __restrict__ tris, Wave W, int depth,
                                                     unsigned int* counter, int* err) {
     const int height = __float_as_int(__ldg(nodes + 3).z);
+    const int root4 = __float_as_int(__ldg(nodes + 3).w);
     if (height + 1 > RT_STACK) {
         if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
         return;
     }
-    int stack[RT_STACK4];
+    int2 stack[RT_STACK4];
     const unsigned n = W.count[depth];
     const int* q = depth == 0 ? nullptr : W.queue[depth & 1];
     const int lane = threadIdx.x & 31;
@@ -240,7 +242,7 @@ __global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ n
             RayPre R;
             ray_setup(R, a.x, a.y, a.z, b.x, b.y, b.z, a.w);
             uint32_t nt, nv;
-            HitRec h = trace_ray4<false>(bvh4, tris, R, b.w, RT_FULL, stack, nt, nv);
+            HitRec h = trace_ray4<false>(bvh4, root4, tris, R, b.w, RT_FULL, stack, nt, nv);
             W.hit[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
             }
         }

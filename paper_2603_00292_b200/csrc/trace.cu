@@ -15,11 +15,12 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
     const float* __restrict__ rays, float4* __restrict__ hits, uint32_t ray_mask, uint32_t* __restrict__ stats,
     unsigned int* counter, int* err) {
     const int height = __float_as_int(__ldg(nodes + 3).z);   // root height == stack bound
+    const int root4 = __float_as_int(__ldg(nodes + 3).w);    // BVH4 root (split position)
     if (height + 1 > RT_STACK) {
         if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
         return;
     }
-    int stack[RT_STACK4];
+    int2 stack[RT_STACK4];
     const int lane = threadIdx.x & 31;
     while (true) {
         unsigned base = 0;
@@ -32,7 +33,7 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
             RayPre R;
             ray_setup(R, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
             uint32_t nt = 0, nv = 0;
-            HitRec h = trace_ray4<STATS>(bvh4, tris, R, r.tmax, ray_mask, stack, nt, nv);
+            HitRec h = trace_ray4<STATS>(bvh4, root4, tris, R, r.tmax, ray_mask, stack, nt, nv);
             hits[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
             if (STATS) reinterpret_cast<uint2*>(stats)[i] = make_uint2(nt, nv);
         }

@@ -132,14 +132,17 @@ __device__ __forceinline__ void cswap(float& ta, int& ca, float& tb, int& cb) {
 // triangle test, tie rule and conservative slab test as trace_ray.  The stack
 // holds at most 3 * ceil(height / 2) entries (checked by the caller).
 template <bool STATS>
-__device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, const float4* __restrict__ tris,
-                                             const RayPre& R, float tmax, uint32_t ray_mask, int* stack,
-                                             uint32_t& n_tests, uint32_t& n_visits) {
+__device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, int root,
+                                             const float4* __restrict__ tris, const RayPre& R, float tmax,
+                                             uint32_t ray_mask, int2* stack, uint32_t& n_tests, uint32_t& n_visits) {
     HitRec h;
     h.t = tmax; h.id = -1; h.u = 0.f; h.v = 0.f;
+    // stack entries carry the child's entry distance: a popped entry that lies
+    // beyond the closest hit found since it was pushed is skipped (leaf children
+    // would otherwise be tested without re-culling)
     int sp = 0;
-    stack[0] = RT_SENTINEL;
-    int node = 0;
+    stack[0] = make_int2(RT_SENTINEL, 0);
+    int node = root;
     while (node != RT_SENTINEL) {
         if (node >= 0) {
             const float4* q = bvh4 + 8 * node;
@@ -157,16 +160,25 @@ __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, co
             cswap(t0, c0, t2, c2);
             cswap(t1, c1, t3, c3);
             cswap(t1, c1, t2, c2);
-            if (t3 != INFINITY) stack[++sp] = c3;
-            if (t2 != INFINITY) stack[++sp] = c2;
-            if (t1 != INFINITY) stack[++sp] = c1;
-            node = (t0 != INFINITY) ? c0 : stack[sp--];
+            if (t3 != INFINITY) stack[++sp] = make_int2(c3, __float_as_int(t3));
+            if (t2 != INFINITY) stack[++sp] = make_int2(c2, __float_as_int(t2));
+            if (t1 != INFINITY) stack[++sp] = make_int2(c1, __float_as_int(t1));
+            if (t0 != INFINITY) {
+                node = c0;
+                continue;
+            }
         } else {
             const float4* tp = tris + 3 * (~node);
             const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
             if (STATS) ++n_tests;
             if (__float_as_uint(b.w) & ray_mask) tri_test(R, a, b, c, h.t, h.id, h.u, h.v);
-            node = stack[sp--];
+        }
+        // pop, dropping entries entered beyond the current closest hit (the box
+        // test is inclusive and widened, so ties at t are kept)
+        while (true) {
+            const int2 e = stack[sp--];
+            node = e.x;
+            if (node == RT_SENTINEL || __int_as_float(e.y) <= h.t * 1.0000008f + 1e-30f) break;
         }
     }
     if (h.id < 0) h.t = -1.0f;
