@@ -376,12 +376,12 @@ def run_ours(args, ws, rank, local):
         return
     # -- roofline: algorithmic bytes / measured device time ---------------------
     render_ms = t_render / K
-    bpr = 112.0 * n_nodes + 48.0 * n_tests + 32.0
+    bpr = 128.0 * n_nodes + 48.0 * n_tests + 32.0
     rays_rank0 = my_rays
     roof_trace = {"kernel": "pt_megakernel (raygen + while-while closest hit + shade, fused)", "bound": "hbm",
                   "achieved": bpr * rays_rank0 / (render_ms * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
                   "traffic": None, "bytes_per_ray": bpr, "peak_source": peak_src,
-                  "bytes_formula": f"112 B x {n_nodes:.2f} BVH4 node fetches (4 child boxes + ids) + 48 B x {n_tests:.2f} triangle "
+                  "bytes_formula": f"128 B x {n_nodes:.2f} BVH4 node fetches (4 child boxes + ids) + 48 B x {n_tests:.2f} triangle "
                                    f"tests + 32 B accumulation RMW per ray (node/test counts: stats build of the "
                                    f"trace kernel on this rank's primary rays{'' if C in (2, 4) else '; bounce rays assumed alike'})",
                   "note": "node/triangle fetches mostly hit L1/L2 (ncu: DRAM 1-2% of peak); the bound that "

@@ -35,27 +35,26 @@ struct EmitNode {
 // with split g holds that node's up-to-4 grandchildren (a leaf child stays a
 // leaf).  Each binary node knows its parent's split as soon as it exists (the
 // side test), so it writes its own half -- slots 2*side, 2*side+1 = its two
-// children, or itself if a leaf -- with no cross-thread reads.  SoA layout per
-// node: x_lo, x_hi, y_lo, y_hi, z_lo, z_hi (float4 over the 4 slots), then the 4
-// child ids (split position of an internal grandchild, ~leaf for a leaf).
+// children, or itself if a leaf -- with no cross-thread reads.  Layout: 4 slots
+// of 2 float4 = (lo.xyz, child id), (hi.xyz, 0); the child id is the split
+// position of an internal grandchild or ~leaf.  A half is 64 contiguous bytes.
 __device__ __forceinline__ void bvh4_write_half(float4* __restrict__ bvh4, int pgamma, int side, const float a_lo[3],
                                                 const float a_hi[3], int a_id, const float b_lo[3],
                                                 const float b_hi[3], int b_id) {
-    float* q = reinterpret_cast<float*>(bvh4 + 8 * (int64_t)pgamma) + 2 * side;
-    *reinterpret_cast<float2*>(q + 0) = make_float2(a_lo[0], b_lo[0]);
-    *reinterpret_cast<float2*>(q + 4) = make_float2(a_hi[0], b_hi[0]);
-    *reinterpret_cast<float2*>(q + 8) = make_float2(a_lo[1], b_lo[1]);
-    *reinterpret_cast<float2*>(q + 12) = make_float2(a_hi[1], b_hi[1]);
-    *reinterpret_cast<float2*>(q + 16) = make_float2(a_lo[2], b_lo[2]);
-    *reinterpret_cast<float2*>(q + 20) = make_float2(a_hi[2], b_hi[2]);
-    *reinterpret_cast<int2*>(q + 24) = make_int2(a_id, b_id);
+    float4* q = bvh4 + 8 * (int64_t)pgamma + 4 * side;
+    q[0] = make_float4(a_lo[0], a_lo[1], a_lo[2], __int_as_float(a_id));
+    q[1] = make_float4(a_hi[0], a_hi[1], a_hi[2], 0.0f);
+    q[2] = make_float4(b_lo[0], b_lo[1], b_lo[2], __int_as_float(b_id));
+    q[3] = make_float4(b_hi[0], b_hi[1], b_hi[2], 0.0f);
 }
 
 // a leaf writes itself + an empty slot into its parent's BVH4 node
 __device__ __forceinline__ void bvh4_write_leaf(float4* __restrict__ bvh4, const EmitNode& N) {
     const bool left = N.dr > N.dl;
     if (N.dr < 0 && N.dl < 0) return;                // n == 1: no parent
-    const float elo[3] = {INFINITY, INFINITY, INFINITY}, ehi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    // empty slot: lo = hi = +inf on every axis.  (lo = +inf, hi = -inf would be an
+    // INFINITE box for the min/max slab test, which orders each slab's ends.)
+    const float elo[3] = {INFINITY, INFINITY, INFINITY}, ehi[3] = {INFINITY, INFINITY, INFINITY};
     bvh4_write_half(bvh4, left ? N.r : N.l - 1, left ? 0 : 1, N.lo, N.hi, ~N.l, elo, ehi, ~0);
 }
 
@@ -124,57 +123,13 @@ __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __rest
     }
 }
 
-// BVH4 view for traversal: for EVERY binary internal node p, a 128-B node whose
-// up-to-4 children are p's grandchildren (a leaf child of p stays a leaf).  A
-// traversal from the root only ever reaches even-depth nodes, so the node id of
-// the BVH4 node equals the binary node id (the odd-depth entries are built but
-// unused: one dependency-free thread per node, no depth computation).
-// layout (SoA over the 4 slots): x_lo, x_hi, y_lo, y_hi, z_lo, z_hi (float4 each),
-// then int4 child ids (>= 0 internal, < 0 ~leaf) and (height, 0, 0, 0).
-__global__ void __launch_bounds__(256) bvh4_collapse_kernel(int64_t n, const float4* __restrict__ nodes,
-                                                           float4* __restrict__ bvh4) {
-    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= n - 1) return;
-    const float4* nd = nodes + 4 * p;
-    const float4 a0 = __ldg(nd), a1 = __ldg(nd + 1), a2 = __ldg(nd + 2), a3 = __ldg(nd + 3);
-    // a child slot: box (6 floats) + id; an internal child expands into its two children
-    struct Slot { float lx, hx, ly, hy, lz, hz; int id; };
-    const Slot empty = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY, ~0};
-    Slot L0, L1 = empty, R0, R1 = empty;
-    const int cl = __float_as_int(a3.x), cr = __float_as_int(a3.y);
-    if (cl < 0) {
-        L0 = {a0.x, a0.y, a0.z, a0.w, a2.x, a2.y, cl};
-    } else {
-        const float4* cn = nodes + 4 * cl;
-        const float4 b0 = __ldg(cn), b1 = __ldg(cn + 1), b2 = __ldg(cn + 2), b3 = __ldg(cn + 3);
-        L0 = {b0.x, b0.y, b0.z, b0.w, b2.x, b2.y, __float_as_int(b3.x)};
-        L1 = {b1.x, b1.y, b1.z, b1.w, b2.z, b2.w, __float_as_int(b3.y)};
-    }
-    if (cr < 0) {
-        R0 = {a1.x, a1.y, a1.z, a1.w, a2.z, a2.w, cr};
-    } else {
-        const float4* cn = nodes + 4 * cr;
-        const float4 b0 = __ldg(cn), b1 = __ldg(cn + 1), b2 = __ldg(cn + 2), b3 = __ldg(cn + 3);
-        R0 = {b0.x, b0.y, b0.z, b0.w, b2.x, b2.y, __float_as_int(b3.x)};
-        R1 = {b1.x, b1.y, b1.z, b1.w, b2.z, b2.w, __float_as_int(b3.y)};
-    }
-    // pack: L0, (L1), R0, (R1); unused slots stay empty
-    const bool l2 = cl >= 0, r2 = cr >= 0;
-    const Slot s0 = L0, s1 = l2 ? L1 : R0, s2 = l2 ? R0 : (r2 ? R1 : empty), s3 = (l2 && r2) ? R1 : empty;
-    const float lox[4] = {s0.lx, s1.lx, s2.lx, s3.lx}, hix[4] = {s0.hx, s1.hx, s2.hx, s3.hx};
-    const float loy[4] = {s0.ly, s1.ly, s2.ly, s3.ly}, hiy[4] = {s0.hy, s1.hy, s2.hy, s3.hy};
-    const float loz[4] = {s0.lz, s1.lz, s2.lz, s3.lz}, hiz[4] = {s0.hz, s1.hz, s2.hz, s3.hz};
-    const int cid[4] = {s0.id, s1.id, s2.id, s3.id};
-    float4* q = bvh4 + 8 * p;
-    q[0] = make_float4(lox[0], lox[1], lox[2], lox[3]);
-    q[1] = make_float4(hix[0], hix[1], hix[2], hix[3]);
-    q[2] = make_float4(loy[0], loy[1], loy[2], loy[3]);
-    q[3] = make_float4(hiy[0], hiy[1], hiy[2], hiy[3]);
-    q[4] = make_float4(loz[0], loz[1], loz[2], loz[3]);
-    q[5] = make_float4(hiz[0], hiz[1], hiz[2], hiz[3]);
-    q[6] = make_float4(__int_as_float(cid[0]), __int_as_float(cid[1]), __int_as_float(cid[2]),
-                       __int_as_float(cid[3]));
-    q[7] = make_float4(a3.z, 0.0f, 0.0f, 0.0f);     // binary height (stack bound)
+// n == 1: the BVH4 root (index 0) holds the single leaf; the other slots are empty
+__global__ void bvh4_single_leaf_kernel(const float4* __restrict__ nodes, float4* __restrict__ bvh4) {
+    const float4 a0 = nodes[0], a2 = nodes[2];
+    const float lo[3] = {a0.x, a0.z, a2.x}, hi[3] = {a0.y, a0.w, a2.y};
+    const float e[3] = {INFINITY, INFINITY, INFINITY};
+    bvh4_write_half(bvh4, 0, 0, lo, hi, ~0, e, e, ~0);
+    bvh4_write_half(bvh4, 0, 1, e, e, ~0, e, e, ~0);
 }
 
 constexpr int EMIT_T = 256;

@@ -287,8 +287,8 @@ __global__ void single_leaf_root(const float* tris, const uint32_t* mask, float4
     leaf_box[0] = make_float4(lo[0], lo[1], lo[2], 0.f);
     leaf_box[1] = make_float4(hi[0], hi[1], hi[2], 0.f);
     nodes[0] = make_float4(lo[0], hi[0], lo[1], hi[1]);
-    nodes[1] = make_float4(INFINITY, -INFINITY, INFINITY, -INFINITY);
-    nodes[2] = make_float4(lo[2], hi[2], INFINITY, -INFINITY);
+    nodes[1] = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);    // empty: never hit
+    nodes[2] = make_float4(lo[2], hi[2], INFINITY, INFINITY);
     nodes[3] = make_float4(__int_as_float(~0), __int_as_float(~0), __int_as_float(1), 0.0f);
 }
 
@@ -348,7 +348,7 @@ int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits) {
     if (s->n == 1) {
         single_leaf_root<<<1, 1, 0, ctx->stream>>>(s->tris, s->tri_mask, s->nodes, s->tri_sorted, s->leaf_box,
                                                    s->vals_a);
-        bvh4_collapse_kernel<<<1, 1, 0, ctx->stream>>>(2, s->nodes, s->bvh4);   // root node 0 only
+        bvh4_single_leaf_kernel<<<1, 1, 0, ctx->stream>>>(s->nodes, s->bvh4);
         RT_CUDA_TRY(cudaGetLastError());
         return RT_OK;
     }

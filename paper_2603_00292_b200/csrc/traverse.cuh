@@ -145,16 +145,17 @@ __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, in
     int node = root;
     while (node != RT_SENTINEL) {
         if (node >= 0) {
+            // 4 slots of (lo.xyz, id), (hi.xyz, -)
             const float4* q = bvh4 + 8 * node;
-            const float4 xl = __ldg(q), xh = __ldg(q + 1), yl = __ldg(q + 2), yh = __ldg(q + 3);
-            const float4 zl = __ldg(q + 4), zh = __ldg(q + 5), cc = __ldg(q + 6);
+            const float4 l0 = __ldg(q), h0 = __ldg(q + 1), l1 = __ldg(q + 2), h1 = __ldg(q + 3);
+            const float4 l2 = __ldg(q + 4), h2 = __ldg(q + 5), l3 = __ldg(q + 6), h3 = __ldg(q + 7);
             if (STATS) ++n_visits;
-            float t0 = box_enter(R, xl.x, xh.x, yl.x, yh.x, zl.x, zh.x, h.t);
-            float t1 = box_enter(R, xl.y, xh.y, yl.y, yh.y, zl.y, zh.y, h.t);
-            float t2 = box_enter(R, xl.z, xh.z, yl.z, yh.z, zl.z, zh.z, h.t);
-            float t3 = box_enter(R, xl.w, xh.w, yl.w, yh.w, zl.w, zh.w, h.t);
-            int c0 = __float_as_int(cc.x), c1 = __float_as_int(cc.y), c2 = __float_as_int(cc.z),
-                c3 = __float_as_int(cc.w);
+            float t0 = box_enter(R, l0.x, h0.x, l0.y, h0.y, l0.z, h0.z, h.t);
+            float t1 = box_enter(R, l1.x, h1.x, l1.y, h1.y, l1.z, h1.z, h.t);
+            float t2 = box_enter(R, l2.x, h2.x, l2.y, h2.y, l2.z, h2.z, h.t);
+            float t3 = box_enter(R, l3.x, h3.x, l3.y, h3.y, l3.z, h3.z, h.t);
+            int c0 = __float_as_int(l0.w), c1 = __float_as_int(l1.w), c2 = __float_as_int(l2.w),
+                c3 = __float_as_int(l3.w);
             cswap(t0, c0, t1, c1);
             cswap(t2, c2, t3, c3);
             cswap(t0, c0, t2, c2);
