@@ -167,6 +167,8 @@ int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normal
     s->sort_scratch_words = rt_sort_scratch_words(n);
     ALLOC(s->sort_scratch, sizeof(unsigned int) * s->sort_scratch_words);
     ALLOC(s->leaf_box, sizeof(float4) * 4 * n);   // per split slot: (lo, h), hi for both sides
+    ALLOC(s->emit_items, 48 * (2 * n + 2));        // EmitNode; every item is a distinct tree node
+    ALLOC(s->emit_count, 16);
 #undef ALLOC
     cudaStream_t st = c->stream;
     RT_CUDA_TRY(cudaMemcpyAsync(s->tris, tris, sizeof(float) * 9 * n, cudaMemcpyHostToDevice, st));
@@ -194,7 +196,8 @@ void rt_scene_destroy(rt_scene* s) {
     rt_render_release(s);
     void* ptrs[] = {s->tris, s->tri_attr, s->tri_inst, s->tri_prim, s->tri_mask, s->mat_color, s->mat_emissive,
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->parent, s->child,
-                    s->flags, s->cbounds, s->cb_enc, s->sort_scratch, s->leaf_box};
+                    s->flags, s->cbounds, s->cb_enc, s->sort_scratch, s->leaf_box, s->emit_items,
+                    s->emit_count};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;

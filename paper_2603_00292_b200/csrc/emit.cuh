@@ -139,8 +139,8 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
                                                            const float* __restrict__ tris, const uint32_t* __restrict__ mask,
                                                            int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
                                                            float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
-                                                           float4* __restrict__ bvh4, int* slot_range,
-                                                           float4* slot_box) {
+                                                           float4* __restrict__ bvh4, EmitNode* __restrict__ items,
+                                                           unsigned int* __restrict__ item_count) {
     __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
     __shared__ int s_delta[EMIT_T + 1];         // delta(B - 1 + k)
     __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, -)]
@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         }
     }
     __syncthreads();
-    // phase B: smem slot `tid` left with a single arrival, then deferred node `tid`
+    // hand-off to phase B: smem slot `tid` left with a single arrival (its sibling
+    // extends past the block), then deferred node `tid`
     if (tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0) {
         const int endpoint = s_range[tid];
         const int gamma = (int)B + tid;
@@ -214,7 +215,23 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         M.hi[0] = hi4.x; M.hi[1] = hi4.y; M.hi[2] = hi4.z;
         M.dl = s_delta[M.l - (int)B];
         M.dr = s_delta[M.r - (int)B + 1];
-        climb_global(keys, n, child, parent, nodes, bvh4, slot_range, slot_box, M);
+        items[atomicAdd(item_count, 1u)] = M;
     }
-    if (tid < s_ndef) climb_global(keys, n, child, parent, nodes, bvh4, slot_range, slot_box, s_def[tid]);
+    if (tid < s_ndef) items[atomicAdd(item_count, 1u)] = s_def[tid];
+}
+
+// Phase B as its own persistent kernel: the few boundary-crossing nodes of all
+// blocks (typically ~n/64) climb through the global split slots.  Keeping these
+// long, mostly single-lane chains out of kernel A lets its blocks retire at once
+// instead of holding an SM slot for the whole chain.
+template <typename K>
+__global__ void __launch_bounds__(128) lbvh_emit_global_kernel(const K* __restrict__ keys, int64_t n,
+                                                              int2* __restrict__ child, int32_t* __restrict__ parent,
+                                                              float4* __restrict__ nodes, float4* __restrict__ bvh4,
+                                                              int* slot_range, float4* slot_box,
+                                                              const EmitNode* __restrict__ items,
+                                                              const unsigned int* __restrict__ item_count) {
+    const unsigned cnt = *item_count;
+    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
+        climb_global(keys, n, child, parent, nodes, bvh4, slot_range, slot_box, items[k]);
 }

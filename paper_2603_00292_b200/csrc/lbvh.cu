@@ -162,6 +162,9 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_pass_kernel(
     __shared__ typename Scan::TempStorage scan_tmp;
     __shared__ unsigned int s_warp[SORT_THREADS / 32][RADIX];
     __shared__ unsigned int s_base[RADIX];
+    __shared__ unsigned int s_texcl[RADIX];
+    __shared__ K s_keys[SORT_TILE];
+    __shared__ uint32_t s_vals[SORT_TILE];
     __shared__ unsigned int s_tile;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) s_tile = atomicAdd(counter, 1u);
@@ -230,20 +233,35 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_pass_kernel(
         }
         atomicExch(st, FLAG_INC | (excl + tile_count));
     }
-    // global digit base = exclusive scan of the digit histogram + look-back prefix
-    unsigned bin_excl;
+    // global digit base = exclusive scan of the digit histogram + look-back prefix;
+    // the tile is first staged in shared memory in digit order (local position =
+    // tile-exclusive digit offset + warp offset + rank), then every digit's run is
+    // written out contiguously (coalesced) instead of a per-key scatter
+    unsigned bin_excl, tile_excl;
     Scan(scan_tmp).ExclusiveSum(hist[tid], bin_excl);
-    s_base[tid] = bin_excl + excl;
+    __syncthreads();
+    Scan(scan_tmp).ExclusiveSum(tile_count, tile_excl);
+    s_base[tid] = bin_excl + excl - tile_excl;        // + local position = global position
+    s_texcl[tid] = tile_excl;
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < SORT_ITEMS; ++i) {
         int64_t idx = seg + i * 32 + lane;
         if (idx < n) {
             unsigned d = (unsigned)(key[i] >> shift) & 0xFFu;
-            unsigned pos = s_base[d] + s_warp[warp][d] + rank[i];
-            keys_out[pos] = key[i];
-            vals_out[pos] = val[i];
+            unsigned lpos = s_texcl[d] + s_warp[warp][d] + rank[i];
+            s_keys[lpos] = key[i];
+            s_vals[lpos] = val[i];
         }
+    }
+    __syncthreads();
+    const int64_t left = n - (int64_t)tile * SORT_TILE;
+    const int cnt = left < SORT_TILE ? (int)left : SORT_TILE;
+    for (int j = tid; j < cnt; j += SORT_THREADS) {
+        const K k = s_keys[j];
+        const unsigned pos = s_base[(unsigned)(k >> shift) & 0xFFu] + (unsigned)j;
+        keys_out[pos] = k;
+        vals_out[pos] = s_vals[j];
     }
 }
 
@@ -333,10 +351,14 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     // K4 + K5
     RT_PROF(ctx, 4);
     RT_CUDA_TRY(cudaMemsetAsync(s->flags, 0xFF, sizeof(int) * (n - 1), st));   // split slots: empty
+    RT_CUDA_TRY(cudaMemsetAsync(s->emit_count, 0, sizeof(unsigned int), st));
     RT_PROF(ctx, 5);
-    lbvh_emit_kernel<K><<<(unsigned)((n + EMIT_T - 1) / EMIT_T), EMIT_T, 0, st>>>(kin, vin, s->tris, s->tri_mask, n, s->child,
-                                                                     s->parent, s->tri_sorted, s->nodes, s->bvh4,
-                                                                     (int*)s->flags, s->leaf_box);
+    EmitNode* items = (EmitNode*)s->emit_items;
+    lbvh_emit_kernel<K><<<(unsigned)((n + EMIT_T - 1) / EMIT_T), EMIT_T, 0, st>>>(
+        kin, vin, s->tris, s->tri_mask, n, s->child, s->parent, s->tri_sorted, s->nodes, s->bvh4, items,
+        s->emit_count);
+    lbvh_emit_global_kernel<K><<<(unsigned)(ctx->num_sms * 4), 128, 0, st>>>(
+        kin, n, s->child, s->parent, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box, items, s->emit_count);
     RT_PROF(ctx, 6);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;

@@ -56,7 +56,9 @@ struct rt_scene {
     unsigned int* cb_enc;           // 6 orderable-uint accumulators
     unsigned int* sort_scratch;     // hist + counters + look-back status
     size_t sort_scratch_words;
-    float4* leaf_box;               // (n, 2) lo, hi
+    float4* leaf_box;               // global split-slot boxes (4 float4 per split)
+    void* emit_items;               // boundary-crossing nodes handed from emit phase A to phase B
+    unsigned int* emit_count;
 };
 
 // --------------------------------------------------------------------------
