@@ -139,6 +139,25 @@ def test_stats_and_culling(native):
     assert stats[:, 1].mean() >= 1
 
 
+def test_near_axis_rays_keep_culling(native, oracle_mod):
+    """Rays with a ~1e-7 direction component (regression: an over-wide slab widening
+    once disabled culling for them -- 54K node fetches per ray on the 10M soup)."""
+    desc = scenes.soup_description(200_000, seed=2)
+    sc = compile_scene(desc)
+    g = np.random.default_rng(3)
+    m = 4096
+    O = np.tile([0.5, 0.5, 2.5], (m, 1))
+    D = np.c_[g.uniform(-0.3, 0.3, m), g.uniform(-0.3, 0.3, m), -np.ones(m)]
+    D[: m // 2, 0] = g.uniform(-3e-7, 3e-7, m // 2)          # near-zero x component
+    D[m // 4: m // 2, 1] = 0.0                                  # and exactly zero y
+    D /= np.linalg.norm(D, axis=1, keepdims=True)
+    res = closest_hit_batch(sc, O, D, with_stats=True)
+    fetches = res[6][:, 1]
+    assert fetches.max() < 20 * np.median(fetches) + 50, (fetches.max(), np.median(fetches))
+    orc = oracle_mod.scene_from_description(desc)
+    _compare(res, orc.closest_hit_batch(O, D, workers=8), m)
+
+
 def test_api_conventions(native):
     sc = compile_scene(scenes.cornell_description())
     O = np.array([[0.5, 0.9, 2.4], [0.5, 0.9, 2.4]])
