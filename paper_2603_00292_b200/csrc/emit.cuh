@@ -134,13 +134,6 @@ __global__ void bvh4_single_leaf_kernel(const float4* __restrict__ nodes, float4
 
 constexpr int EMIT_T = 256;
 
-// compact live node in shared memory (dl / dr are re-read from the block's
-// delta table: a phase-A node lies inside the block)
-struct LiveNode {
-    int l, r, h, g;
-    float lo[3], hi[3];
-};
-
 template <typename K>
 __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
                                                            const float* __restrict__ tris, const uint32_t* __restrict__ mask,
@@ -150,22 +143,21 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
                                                            unsigned int* __restrict__ item_count) {
     __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
     __shared__ int s_delta[EMIT_T + 1];         // delta(B - 1 + k)
-    __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, g)]
-    __shared__ LiveNode s_live[2][EMIT_T / 2];  // nodes created in the previous step (<= EMIT_T/2)
-    __shared__ int s_cnt[2];
-    const int tid = threadIdx.x, lane = tid & 31;
+    __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, -)]
+    __shared__ EmitNode s_def[EMIT_T];          // deferred (boundary-crossing) nodes
+    __shared__ int s_ndef;
+    const int tid = threadIdx.x;
     const int64_t B = (int64_t)blockIdx.x * EMIT_T;
     const int64_t E = (B + EMIT_T < n) ? B + EMIT_T : n;
     s_range[tid] = -1;
     s_delta[tid] = adj_delta(keys, n, B - 1 + tid);
     if (tid == 0) {
-        s_cnt[0] = s_cnt[1] = 0;
+        s_ndef = 0;
         s_delta[EMIT_T] = adj_delta(keys, n, B - 1 + EMIT_T);
     }
     const int64_t i = B + tid;
     EmitNode N;
-    bool have = i < E;
-    if (have) {
+    if (i < E) {
         const uint32_t id = order[i];
         float t[9];
         load_tri(tris, id, t);
@@ -178,69 +170,37 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         N.g = -1;
     }
     __syncthreads();
-    if (have) {
+    if (i < E) {
         N.dl = s_delta[tid];            // delta(i - 1)
         N.dr = s_delta[tid + 1];        // delta(i)
         bvh4_write_leaf(bvh4, N);
-    }
-    // Phase A, level-synchronous: every step, each live node (step 0: the leaves)
-    // meets its sibling in a smem slot; second arrivals create the parent, which is
-    // compacted into the front lanes for the next step so warps stay full.
-    int rb = 0;
-    while (true) {
-        const int wb = rb ^ 1;
-        bool survive = false;
-        if (have) {
+        while (true) {
             const bool left = N.dr > N.dl;
             const bool inside = left ? (N.r + 1 < E) : (N.l - 1 >= B);
             if (!inside) {
-                items[atomicAdd(item_count, 1u)] = N;             // sibling starts outside: phase B
-            } else {
-                const int gamma = left ? N.r : N.l - 1;
-                const int g = gamma - (int)B, side = left ? 0 : 1;
-                s_box[g][side][0] = make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h));
-                s_box[g][side][1] = make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g));
-                __threadfence_block();
-                const int other = atomicExch(&s_range[g], left ? N.l : N.r);
-                if (other >= 0) {                                 // second arrival: build the parent
-                    __threadfence_block();
-                    s_range[g] = -2;
-                    const int pl = left ? N.l : other, pr = left ? other : N.r;
-                    const int pdl = s_delta[pl - (int)B], pdr = s_delta[pr - (int)B + 1];
-                    survive = !emit_parent(n, child, parent, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr,
-                                           s_box[g][1 - side][0], s_box[g][1 - side][1]);
-                }
+                s_def[atomicAdd(&s_ndef, 1)] = N;
+                break;
             }
+            const int gamma = left ? N.r : N.l - 1;
+            const int g = gamma - (int)B, side = left ? 0 : 1;
+            s_box[g][side][0] = make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h));
+            s_box[g][side][1] = make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g));
+            __threadfence_block();
+            const int other = atomicExch(&s_range[g], left ? N.l : N.r);
+            if (other < 0) break;                    // first arrival: pending in smem
+            __threadfence_block();
+            s_range[g] = -2;                         // pair complete
+            const int pl = left ? N.l : other, pr = left ? other : N.r;
+            // the parent lies inside the block, so its boundary deltas are in smem
+            const int pdl = s_delta[pl - (int)B], pdr = s_delta[pr - (int)B + 1];
+            if (emit_parent(n, child, parent, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s_box[g][1 - side][0],
+                            s_box[g][1 - side][1]))
+                break;                               // root (whole tree inside one block)
         }
-        // warp-aggregated append of the survivors
-        const unsigned ballot = __ballot_sync(RT_FULL, survive);
-        int base = 0;
-        if (ballot && lane == 0) base = atomicAdd(&s_cnt[wb], __popc(ballot));
-        base = __shfl_sync(RT_FULL, base, 0);
-        if (survive) {
-            LiveNode& L = s_live[wb][base + __popc(ballot & ((1u << lane) - 1u))];
-            L.l = N.l; L.r = N.r; L.h = N.h; L.g = N.g;
-            L.lo[0] = N.lo[0]; L.lo[1] = N.lo[1]; L.lo[2] = N.lo[2];
-            L.hi[0] = N.hi[0]; L.hi[1] = N.hi[1]; L.hi[2] = N.hi[2];
-        }
-        __syncthreads();
-        const int cnt = s_cnt[wb];
-        have = tid < cnt;
-        if (have) {
-            const LiveNode& L = s_live[wb][tid];
-            N.l = L.l; N.r = L.r; N.h = L.h; N.g = L.g;
-            N.lo[0] = L.lo[0]; N.lo[1] = L.lo[1]; N.lo[2] = L.lo[2];
-            N.hi[0] = L.hi[0]; N.hi[1] = L.hi[1]; N.hi[2] = L.hi[2];
-            N.dl = s_delta[N.l - (int)B];
-            N.dr = s_delta[N.r - (int)B + 1];
-        }
-        __syncthreads();
-        if (tid == 0) s_cnt[wb] = 0;       // written again two steps from now
-        rb = wb;
-        if (cnt == 0) break;
     }
-    // hand-off to phase B: smem slots left with a single arrival (the sibling
-    // extends past the block)
+    __syncthreads();
+    // hand-off to phase B: smem slot `tid` left with a single arrival (its sibling
+    // extends past the block), then deferred node `tid`
     if (tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0) {
         const int endpoint = s_range[tid];
         const int gamma = (int)B + tid;
@@ -257,6 +217,7 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         M.dr = s_delta[M.r - (int)B + 1];
         items[atomicAdd(item_count, 1u)] = M;
     }
+    if (tid < s_ndef) items[atomicAdd(item_count, 1u)] = s_def[tid];
 }
 
 // Phase B as its own persistent kernel: the few boundary-crossing nodes of all
