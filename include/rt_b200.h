@@ -27,8 +27,10 @@ extern "C" {
 #define RT_ENOMEM (-5)        /* device allocation failed     -> MemoryError  */
 #define RT_ESTATE (-6)        /* e.g. trace before build      -> RuntimeError */
 
-#define RT_INTEG_EYE 0        /* integrators.py:129-141 _sample_eye */
-#define RT_INTEG_PT 2         /* integrators.py:182-235 _sample_pt  */
+#define RT_INTEG_EYE 0        /* integrators.py:129-141 _sample_eye   */
+#define RT_INTEG_AO 1         /* integrators.py:144-179 _sample_ao    (megakernel) */
+#define RT_INTEG_PT 2         /* integrators.py:182-235 _sample_pt    */
+#define RT_INTEG_PTNEE 3      /* integrators.py:238-331 _sample_ptnee (megakernel) */
 
 #define RT_KERNEL_MEGA 0      /* one persistent kernel per frame (K7)      */
 #define RT_KERNEL_WAVEFRONT 1 /* raygen / extend / shade / accumulate (K8) */
@@ -59,6 +61,8 @@ typedef struct {
      * into rows of 8x4-pixel tiles; only tile rows r with r % band_stride ==
      * band_offset are rendered (interleaved bands balance the load).  1/0 = all. */
     int32_t band_stride, band_offset;
+    int32_t ao_count;         /* IntegratorConfig.ao_ray_count */
+    float ao_length;          /* IntegratorConfig.ao_max_length */
 } rt_render_params;
 
 /* ---- context --------------------------------------------------------- */
@@ -119,6 +123,17 @@ int rt_closest_hit_host(rt_ctx* ctx, rt_scene* scene, int64_t n, const double* o
                         const double* dirs, const double* t_min, const double* t_max,
                         uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
                         double* v, double* normal, int64_t* stats);
+
+/* ---- any hit (replaces _any_batch / any_hit_batch, accel.py:979-992, 1159-1174) */
+/* device rays (n, 8) -> hit (n) uint8 (1 = some accepted intersection in [tmin, tmax]) */
+int rt_trace_any(rt_ctx* ctx, rt_scene* scene, int64_t n, const float* rays, uint8_t* hit,
+                 uint32_t ray_mask);
+/* host float64 rays -> host uint8 (numpy bool) */
+int rt_any_hit_host(rt_ctx* ctx, rt_scene* scene, int64_t n, const double* origins, const double* dirs,
+                    const double* t_min, const double* t_max, uint32_t ray_mask, uint8_t* hit);
+/* emissive triangles for pt-nee (scene.py:58-76): rows of 16 floats =
+ * v0, v1, v2, unit normal, emission (3 each), area */
+int rt_scene_set_lights(rt_ctx* ctx, rt_scene* scene, int32_t n_lights, const float* rows);
 
 /* ---- render (replaces render_frame / _render_chunk, integrators.py:334-473; K7/K8) */
 /* accum: device (H*W, 4) f32 running (r, g, b, n) sums, row 0 on top, added to in

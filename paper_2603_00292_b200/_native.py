@@ -22,7 +22,9 @@ RT_ENOMEM = -5
 RT_ESTATE = -6
 
 RT_INTEG_EYE = 0
+RT_INTEG_AO = 1
 RT_INTEG_PT = 2
+RT_INTEG_PTNEE = 3
 RT_KERNEL_MEGA = 0
 RT_KERNEL_WAVEFRONT = 1
 
@@ -50,7 +52,8 @@ class RenderParams(ctypes.Structure):
                 ("kernel", ctypes.c_int32), ("cam", ctypes.c_float * 13),
                 ("sky", ctypes.c_float * 3), ("background", ctypes.c_float * 3),
                 ("normal_offset", ctypes.c_float), ("pix_lo", ctypes.c_int64),
-                ("pix_hi", ctypes.c_int64), ("band_stride", ctypes.c_int32), ("band_offset", ctypes.c_int32)]
+                ("pix_hi", ctypes.c_int64), ("band_stride", ctypes.c_int32), ("band_offset", ctypes.c_int32),
+                ("ao_count", ctypes.c_int32), ("ao_length", ctypes.c_float)]
 
 
 def lib():
@@ -80,6 +83,9 @@ def lib():
             "rt_trace_closest": [vp, vp, i64, vp, vp, u32, vp],
             "rt_closest_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp, vp],
             "rt_render": [vp, vp, ctypes.POINTER(RenderParams), vp, vp],
+            "rt_trace_any": [vp, vp, i64, vp, vp, u32],
+            "rt_any_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp],
+            "rt_scene_set_lights": [vp, vp, i32, vp],
             "rt_raygen": [vp, ctypes.POINTER(RenderParams), i32, vp],
         }
         for name, args in sigs.items():

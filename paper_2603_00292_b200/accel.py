@@ -56,6 +56,32 @@ def closest_hit_batch(tlas, origins, dirs, t_min=0.0, t_max=DEFAULT_MAX_T, ray_m
     return res + (stats,) if with_stats else res
 
 
+def any_hit_batch(tlas, origins, dirs, t_min=0.0, t_max=DEFAULT_MAX_T, ray_mask: int = FULL_MASK,
+                  ray_type: int = 0, registry=None) -> np.ndarray:
+    """accel.py:1159-1174: True iff some accepted intersection lies in [t_min, t_max]."""
+    tl = _tlas_of(tlas)
+    if registry is not None:
+        raise RegistryError("custom intersectors are not available on the GPU path")
+    mask = _check_mask(ray_mask)
+    origins = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
+    dirs = np.ascontiguousarray(dirs, dtype=np.float64).reshape(-1, 3)
+    n = origins.shape[0]
+    if dirs.shape[0] != n:
+        raise ValueError("origins and dirs must have the same length")
+    tmin = np.ascontiguousarray(np.broadcast_to(np.asarray(t_min, dtype=np.float64), (n,)))
+    tmax = np.ascontiguousarray(np.broadcast_to(np.asarray(t_max, dtype=np.float64), (n,)))
+    out = np.zeros(n, np.uint8)
+    check(lib().rt_any_hit_host(tl.ctx.handle, tl.handle, n, ptr(origins), ptr(dirs), ptr(tmin), ptr(tmax), mask,
+                                ptr(out)))
+    return out.astype(bool)
+
+
+def trace_any(tlas, rays, hit, ray_mask: int = FULL_MASK):
+    """Device form: rays (n, 8) f32 CUDA tensor -> hit (n,) uint8 CUDA tensor."""
+    tl = _tlas_of(tlas)
+    check(lib().rt_trace_any(tl.ctx.handle, tl.handle, rays.shape[0], ptr(rays), ptr(hit), _check_mask(ray_mask)))
+
+
 def trace_closest(tlas, rays, hits, ray_mask: int = FULL_MASK, stats=None):
     """Device form: rays (n, 8) f32 CUDA tensor [o, tmin, d, tmax] -> hits (n, 4) [t, id, u, v]."""
     tl = _tlas_of(tlas)

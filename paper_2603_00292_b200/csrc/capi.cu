@@ -197,7 +197,7 @@ void rt_scene_destroy(rt_scene* s) {
     void* ptrs[] = {s->tris, s->tri_attr, s->tri_inst, s->tri_prim, s->tri_mask, s->mat_color, s->mat_emissive,
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->parent, s->child,
                     s->flags, s->cbounds, s->cb_enc, s->sort_scratch, s->leaf_box, s->emit_items,
-                    s->emit_count};
+                    s->emit_count, s->lights};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;
@@ -388,12 +388,89 @@ int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, cons
     return check_device_error(c);
 }
 
+int rt_trace_any(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, uint8_t* hit, uint32_t ray_mask) {
+    RT_CHECK_ARG(c && s, "ctx/scene is NULL");
+    RT_CHECK_ARG(n >= 0 && (n == 0 || (rays && hit)), "bad ray/hit buffers");
+    if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    return rt_trace_any_impl(c, s, n, rays, hit, ray_mask);
+}
+
+// accel.py:1159-1174 any_hit_batch with host float64 rays -> host bool (uint8)
+int rt_any_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const double* d, const double* tmin,
+                    const double* tmax, uint32_t ray_mask, uint8_t* out) {
+    RT_CHECK_ARG(c && s, "ctx/scene is NULL");
+    RT_CHECK_ARG(n >= 0, "negative ray count");
+    if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    if (n == 0) return RT_OK;
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    const int64_t CH = std::min<int64_t>(n, 1 << 21);
+    size_t need = (size_t)CH * (64 + 32 + 1) + 256;
+    if (c->d_stage_bytes < need) {
+        if (c->d_stage) cudaFree(c->d_stage);
+        c->d_stage = nullptr;
+        c->d_stage_bytes = 0;
+        RT_CUDA_TRY(cudaMalloc(&c->d_stage, need));
+        c->d_stage_bytes = need;
+    }
+    char* D = (char*)c->d_stage;
+    double* d_o = (double*)D; D += 24 * CH;
+    double* d_d = (double*)D; D += 24 * CH;
+    double* d_tmin = (double*)D; D += 8 * CH;
+    double* d_tmax = (double*)D; D += 8 * CH;
+    float* d_rays = (float*)D; D += 32 * CH;
+    uint8_t* d_out = (uint8_t*)D;
+    cudaStream_t st = c->stream;
+    for (int64_t b = 0; b < n; b += CH) {
+        int64_t m = std::min(CH, n - b);
+        RT_CUDA_TRY(cudaMemcpyAsync(d_o, o + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_d, d + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_tmin, tmin + b, 8 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
+        int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
+        if (rc) return rc;
+        rc = rt_trace_any_impl(c, s, m, d_rays, d_out, ray_mask);
+        if (rc) return rc;
+        RT_CUDA_TRY(cudaMemcpyAsync(out + b, d_out, m, cudaMemcpyDeviceToHost, st));
+    }
+    RT_CUDA_TRY(cudaStreamSynchronize(st));
+    return check_device_error(c);
+}
+
+// world-space emissive triangles for next-event estimation (scene.py:58-76 light rows):
+// rows of 16 floats = v0 (3), v1 (3), v2 (3), unit normal (3), emission (3), area
+int rt_scene_set_lights(rt_ctx* c, rt_scene* s, int32_t n_lights, const float* rows) {
+    RT_CHECK_ARG(c && s && n_lights >= 0 && (n_lights == 0 || rows), "bad light table");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    if (s->lights) cudaFree(s->lights);
+    s->lights = nullptr;
+    s->n_lights = n_lights;
+    if (n_lights == 0) return RT_OK;
+    std::vector<float4> L(5 * (size_t)n_lights);
+    for (int k = 0; k < n_lights; ++k) {
+        const float* r = rows + 16 * k;
+        L[5 * k + 0] = make_float4(r[0], r[1], r[2], r[15]);
+        L[5 * k + 1] = make_float4(r[3], r[4], r[5], 0.f);
+        L[5 * k + 2] = make_float4(r[6], r[7], r[8], 0.f);
+        L[5 * k + 3] = make_float4(r[9], r[10], r[11], 0.f);
+        L[5 * k + 4] = make_float4(r[12], r[13], r[14], 0.f);
+    }
+    RT_CUDA_TRY(cudaMalloc(&s->lights, sizeof(float4) * L.size()));
+    RT_CUDA_TRY(cudaMemcpy(s->lights, L.data(), sizeof(float4) * L.size(), cudaMemcpyHostToDevice));
+    return RT_OK;
+}
+
 int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out) {
     RT_CHECK_ARG(c && s && p && accum, "NULL argument");
     RT_CHECK_ARG(p->width >= 1 && p->height >= 1 && p->s1 > p->s0 && p->s0 >= 0,
                  "width, height, and spp must all be >= 1");
-    RT_CHECK_ARG(p->integrator == RT_INTEG_EYE || p->integrator == RT_INTEG_PT,
-                 "integrator must be eye or pt on the GPU path");
+    RT_CHECK_ARG(p->integrator == RT_INTEG_EYE || p->integrator == RT_INTEG_AO || p->integrator == RT_INTEG_PT ||
+                     p->integrator == RT_INTEG_PTNEE,
+                 "integrator must be eye, ao, pt or pt-nee");
+    RT_CHECK_ARG(p->kernel == RT_KERNEL_MEGA || p->integrator == RT_INTEG_EYE || p->integrator == RT_INTEG_PT,
+                 "ao and pt-nee run in the megakernel (kernel=mega)");
+    RT_CHECK_ARG(p->integrator != RT_INTEG_AO || (p->ao_count >= 1 && p->ao_length > 0.0f), "bad ao parameters");
+    RT_CHECK_ARG(p->integrator != RT_INTEG_PTNEE || s->n_lights > 0, "pt-nee needs a light table");
     RT_CHECK_ARG(p->max_depth >= 1, "max_depth must be >= 1");
     RT_CHECK_ARG(p->kernel == RT_KERNEL_MEGA || p->kernel == RT_KERNEL_WAVEFRONT, "unknown kernel");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }

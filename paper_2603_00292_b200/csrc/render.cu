@@ -26,6 +26,8 @@ struct FrameConst {
     float offset;
     uint64_t seed;
     int width, height, jitter, integ, max_depth;
+    int ao_count;
+    float ao_length;
     int64_t pix_lo, npix;
     // work units: 8x4 pixel tiles (one per warp) when the range is whole rows
     int tiled, tiles_x;
@@ -133,14 +135,132 @@ __device__ __forceinline__ bool shade_bounce(const FrameConst& F, const float4* 
     return true;
 }
 
+// integrators.py:99-115 _geom_term in fp32
+__device__ __forceinline__ float geom_term(float px, float py, float pz, float npx, float npy, float npz, float qx,
+                                           float qy, float qz, float nqx, float nqy, float nqz) {
+    float wx = qx - px, wy = qy - py, wz = qz - pz;
+    const float d2 = wx * wx + wy * wy + wz * wz;
+    if (d2 <= 0.0f) return 0.0f;
+    const float inv = 1.0f / sqrtf(d2);
+    wx *= inv; wy *= inv; wz *= inv;
+    const float cp = npx * wx + npy * wy + npz * wz;
+    const float cq = -(nqx * wx + nqy * wy + nqz * wz);
+    if (cp <= 0.0f || cq <= 0.0f) return 0.0f;
+    return cp * cq / d2;
+}
+
+// integrators.py:144-179 _sample_ao: unoccluded fraction of the cosine lobe
+__device__ __forceinline__ float sample_ao(const FrameConst& F, const float4* __restrict__ bvh4, int root4,
+                                           const float4* __restrict__ tris, const float4* __restrict__ attr,
+                                           PathState& P, int2* stack, unsigned long long& rays) {
+    RayPre R;
+    ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
+    uint32_t nt, nv;
+    const HitRec h = trace_ray4<false>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+    ++rays;
+    if (h.id < 0) return 1.0f;
+    const float4 a = __ldg(attr + h.id);
+    float nx = a.x, ny = a.y, nz = a.z;
+    if (nx * P.dx + ny * P.dy + nz * P.dz > 0.0f) { nx = -nx; ny = -ny; nz = -nz; }
+    const float px = P.ox + P.dx * h.t + nx * F.offset;
+    const float py = P.oy + P.dy * h.t + ny * F.offset;
+    const float pz = P.oz + P.dz * h.t + nz * F.offset;
+    float t[3], b[3];
+    onb(nx, ny, nz, t, b);
+    int occluded = 0;
+    for (int k = 0; k < F.ao_count; ++k) {
+        const float x0 = rt_uniform(P.state, P.inc), x1 = rt_uniform(P.state, P.inc);
+        float sx, sy, sz;
+        cosine_dir(x0, x1, sx, sy, sz);
+        const float wx = t[0] * sx + nx * sy + b[0] * sz;
+        const float wy = t[1] * sx + ny * sy + b[1] * sz;
+        const float wz = t[2] * sx + nz * sy + b[2] * sz;
+        RayPre S;
+        ray_setup(S, px, py, pz, wx, wy, wz, 0.0f);
+        occluded += trace_any4(bvh4, root4, tris, S, F.ao_length, RT_FULL, reinterpret_cast<int*>(stack)) ? 1 : 0;
+        ++rays;
+    }
+    return 1.0f - (float)occluded / (float)F.ao_count;
+}
+
+// integrators.py:238-331 _sample_ptnee: path tracing with one light connection per
+// vertex (3 draws: light, then 2 for the area sample), emission counted only at depth 0
+__device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* __restrict__ bvh4, int root4,
+                                             const float4* __restrict__ tris, const float4* __restrict__ attr,
+                                             const float4* __restrict__ mat_color, const float4* __restrict__ mat_emis,
+                                             const float4* __restrict__ lights, int n_lights, PathState& P,
+                                             int2* stack, unsigned long long& rays) {
+    for (int depth = 0; depth < F.max_depth; ++depth) {
+        RayPre R;
+        ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
+        uint32_t nt, nv;
+        const HitRec h = trace_ray4<false>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+        ++rays;
+        if (h.id < 0) {
+            P.rr += P.tr * F.sky[0]; P.rg += P.tg * F.sky[1]; P.rb += P.tb * F.sky[2];
+            return;
+        }
+        const float4 a = __ldg(attr + h.id);
+        const int m = __float_as_int(a.w);
+        const float4 e = __ldg(mat_emis + m);
+        if (e.x > 0.0f || e.y > 0.0f || e.z > 0.0f) {
+            if (depth == 0) { P.rr += P.tr * e.x; P.rg += P.tg * e.y; P.rb += P.tb * e.z; }
+            return;
+        }
+        float nx = a.x, ny = a.y, nz = a.z;
+        if (nx * P.dx + ny * P.dy + nz * P.dz > 0.0f) { nx = -nx; ny = -ny; nz = -nz; }
+        const float px = P.ox + P.dx * h.t, py = P.oy + P.dy * h.t, pz = P.oz + P.dz * h.t;
+        const float4 c = __ldg(mat_color + m);
+        // explicit light connection
+        const float x0 = rt_uniform(P.state, P.inc), x1 = rt_uniform(P.state, P.inc),
+                    x2 = rt_uniform(P.state, P.inc);
+        int li = (int)(x0 * (float)n_lights);
+        if (li > n_lights - 1) li = n_lights - 1;
+        const float s = sqrtf(x1), w0 = 1.0f - s, w1 = s * (1.0f - x2), w2 = s * x2;
+        const float4 l0 = __ldg(lights + 5 * li), l1 = __ldg(lights + 5 * li + 1), l2 = __ldg(lights + 5 * li + 2);
+        const float4 ln = __ldg(lights + 5 * li + 3), le = __ldg(lights + 5 * li + 4);
+        const float qx = w0 * l0.x + w1 * l1.x + w2 * l2.x;
+        const float qy = w0 * l0.y + w1 * l1.y + w2 * l2.y;
+        const float qz = w0 * l0.z + w1 * l1.z + w2 * l2.z;
+        const float g = geom_term(px, py, pz, nx, ny, nz, qx, qy, qz, ln.x, ln.y, ln.z);
+        if (g > 0.0f) {
+            const float spx = px + nx * F.offset, spy = py + ny * F.offset, spz = pz + nz * F.offset;
+            const float sqx = qx + ln.x * F.offset, sqy = qy + ln.y * F.offset, sqz = qz + ln.z * F.offset;
+            RayPre S;
+            ray_setup(S, spx, spy, spz, sqx - spx, sqy - spy, sqz - spz, 0.0f);
+            const bool occ = trace_any4(bvh4, root4, tris, S, 1.0f - 1e-3f, RT_FULL, reinterpret_cast<int*>(stack));
+            ++rays;
+            if (!occ) {
+                const float pdf = (1.0f / (float)n_lights) * (1.0f / l0.w);
+                const float scale = g / (3.14159265358979323846f * pdf);
+                P.rr += P.tr * c.x * le.x * scale;
+                P.rg += P.tg * c.y * le.y * scale;
+                P.rb += P.tb * c.z * le.z * scale;
+            }
+        }
+        // diffuse bounce, as plain path tracing
+        const float b0 = rt_uniform(P.state, P.inc), b1 = rt_uniform(P.state, P.inc);
+        float sx, sy, sz;
+        cosine_dir(b0, b1, sx, sy, sz);
+        float t[3], b[3];
+        onb(nx, ny, nz, t, b);
+        P.dx = t[0] * sx + nx * sy + b[0] * sz;
+        P.dy = t[1] * sx + ny * sy + b[1] * sz;
+        P.dz = t[2] * sx + nz * sy + b[2] * sz;
+        P.tr *= c.x; P.tg *= c.y; P.tb *= c.z;
+        P.ox = px + nx * F.offset; P.oy = py + ny * F.offset; P.oz = pz + nz * F.offset;
+    }
+}
+
 // ---- K7: megakernel --------------------------------------------------------
 // Persistent warps fetch 32 pixels at a time; each lane renders samples
 // [s0, s1) of its pixel in order and adds the sums to accum once.
+template <int INTEG>
 __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     const FrameConst F, int s0, int s1, const float4* __restrict__ nodes, const float4* __restrict__ bvh4,
     const float4* __restrict__ tris, const float4* __restrict__ attr, const float4* __restrict__ mat_color,
-    const float4* __restrict__ mat_emis, float4* __restrict__ accum, unsigned int* counter,
-    unsigned long long* ray_total, int* err) {
+    const float4* __restrict__ mat_emis, const float4* __restrict__ lights, int n_lights,
+    float4* __restrict__ accum, unsigned int* counter, unsigned long long* ray_total, int* err) {
     const int height = __float_as_int(__ldg(nodes + 3).z);
     const int root4 = __float_as_int(__ldg(nodes + 3).w);
     if (height + 1 > RT_STACK) {
@@ -150,7 +270,7 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     int2 stack[RT_STACK4];
     const int lane = threadIdx.x & 31;
     unsigned long long rays = 0;
-    const int max_depth = F.integ == RT_INTEG_EYE ? 1 : F.max_depth;
+    const int max_depth = INTEG == RT_INTEG_EYE ? 1 : F.max_depth;
     while (true) {
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(counter, 32u);
@@ -165,13 +285,20 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
             for (int s = s0; s < s1; ++s) {
                 PathState P;
                 start_path(F, pix, s, P);
-                for (int depth = 0; depth < max_depth; ++depth) {
-                    RayPre R;
-                    ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
-                    uint32_t nt, nv;
-                    HitRec h = trace_ray4<false>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
-                    ++rays;
-                    if (!shade_bounce(F, attr, mat_color, mat_emis, h, P)) break;
+                if constexpr (INTEG == RT_INTEG_AO) {
+                    const float v = sample_ao(F, bvh4, root4, tris, attr, P, stack, rays);
+                    P.rr = P.rg = P.rb = v;
+                } else if constexpr (INTEG == RT_INTEG_PTNEE) {
+                    sample_ptnee(F, bvh4, root4, tris, attr, mat_color, mat_emis, lights, n_lights, P, stack, rays);
+                } else {
+                    for (int depth = 0; depth < max_depth; ++depth) {
+                        RayPre R;
+                        ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
+                        uint32_t nt, nv;
+                        HitRec h = trace_ray4<false>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+                        ++rays;
+                        if (!shade_bounce(F, attr, mat_color, mat_emis, h, P)) break;
+                    }
                 }
                 a.x += P.rr; a.y += P.rg; a.z += P.rb; a.w += 1.0f;
             }
@@ -336,6 +463,7 @@ FrameConst make_frame(const rt_render_params* p) {
     F.seed = p->seed;
     F.width = p->width; F.height = p->height; F.jitter = p->jitter;
     F.integ = p->integrator; F.max_depth = p->max_depth;
+    F.ao_count = p->ao_count; F.ao_length = p->ao_length;
     int64_t npix_total = (int64_t)p->width * p->height;
     F.pix_lo = p->pix_lo;
     int64_t hi = (p->pix_hi > 0) ? p->pix_hi : npix_total;
@@ -436,17 +564,27 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
     RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, 64 * sizeof(unsigned int), st));
     float4* acc = reinterpret_cast<float4*>(accum);
     if (p->kernel == RT_KERNEL_MEGA) {
-        int bps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pt_megakernel, MEGA_THREADS, 0);
-        if (bps < 1) bps = 1;
-        int64_t grid = (int64_t)ctx->num_sms * bps;
-        int64_t want = (F.nunits + MEGA_THREADS - 1) / MEGA_THREADS;
-        if (grid > want) grid = want;
-        pt_megakernel<<<(unsigned)grid, MEGA_THREADS, 0, st>>>(F, p->s0, p->s1, s->nodes, s->bvh4, s->tri_sorted,
-                                                               s->tri_attr,
-                                                               s->mat_color, s->mat_emissive, acc, ctx->d_counter,
-                                                               d_rays, ctx->d_error);
-        RT_CUDA_TRY(cudaGetLastError());
+        auto launch = [&](auto kern) -> int {
+            int bps = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, MEGA_THREADS, 0);
+            if (bps < 1) bps = 1;
+            int64_t grid = (int64_t)ctx->num_sms * bps;
+            int64_t want = (F.nunits + MEGA_THREADS - 1) / MEGA_THREADS;
+            if (grid > want) grid = want;
+            kern<<<(unsigned)grid, MEGA_THREADS, 0, st>>>(F, p->s0, p->s1, s->nodes, s->bvh4, s->tri_sorted,
+                                                          s->tri_attr, s->mat_color, s->mat_emissive, s->lights,
+                                                          s->n_lights, acc, ctx->d_counter, d_rays, ctx->d_error);
+            RT_CUDA_TRY(cudaGetLastError());
+            return RT_OK;
+        };
+        int rc;
+        switch (F.integ) {
+            case RT_INTEG_EYE: rc = launch(pt_megakernel<RT_INTEG_EYE>); break;
+            case RT_INTEG_AO: rc = launch(pt_megakernel<RT_INTEG_AO>); break;
+            case RT_INTEG_PTNEE: rc = launch(pt_megakernel<RT_INTEG_PTNEE>); break;
+            default: rc = launch(pt_megakernel<RT_INTEG_PT>); break;
+        }
+        if (rc) return rc;
     } else {
         if (F.max_depth > 30) return RT_EINVAL;
         WaveBuffers* wb;

@@ -57,6 +57,8 @@ struct rt_scene {
     unsigned int* sort_scratch;     // hist + counters + look-back status
     size_t sort_scratch_words;
     float4* leaf_box;               // global split-slot boxes (4 float4 per split)
+    float4* lights;                 // (n_lights, 5): (v0, area), v1, v2, normal, emission
+    int n_lights;
     void* emit_items;               // boundary-crossing nodes handed from emit phase A to phase B
     unsigned int* emit_count;
 };
@@ -161,6 +163,7 @@ __device__ __forceinline__ bool rt_primary_dir(const float* cam, float u, float 
 int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits);
 int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4* hits, uint32_t mask,
                   uint32_t* stats);
+int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask);
 int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
                        int64_t* prim, double* u, double* v, double* nrm);
 int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, const double* tmin,

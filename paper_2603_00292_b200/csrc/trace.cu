@@ -40,6 +40,33 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
     }
 }
 
+// any-hit over a ray buffer (same persistent warp fetch as the closest-hit kernel)
+__global__ void __launch_bounds__(TRACE_THREADS, 8) trace_any_kernel(
+    const float4* __restrict__ nodes, const float4* __restrict__ bvh4, const float4* __restrict__ tris, int64_t n,
+    const float* __restrict__ rays, uint8_t* __restrict__ out, uint32_t ray_mask, unsigned int* counter, int* err) {
+    const int height = __float_as_int(__ldg(nodes + 3).z);
+    const int root4 = __float_as_int(__ldg(nodes + 3).w);
+    if (height + 1 > RT_STACK) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(err, RT_EDEPTH);
+        return;
+    }
+    int stack[RT_STACK4];
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(counter, 32u);
+        base = __shfl_sync(RT_FULL, base, 0);
+        if ((int64_t)base >= n) break;
+        int64_t i = (int64_t)base + lane;
+        if (i < n) {
+            TraceRay r = load_ray(rays, i);
+            RayPre R;
+            ray_setup(R, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
+            out[i] = trace_any4(bvh4, root4, tris, R, r.tmax, ray_mask, stack) ? 1 : 0;
+        }
+    }
+}
+
 __global__ void pack_rays_f64(int64_t n, const double* __restrict__ o, const double* __restrict__ d,
                               const double* __restrict__ tmin, const double* __restrict__ tmax,
                               float4* __restrict__ rays) {
@@ -93,6 +120,23 @@ int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4
     else
         trace_closest_kernel<false><<<(unsigned)grid, TRACE_THREADS, 0, st>>>(
             s->nodes, s->bvh4, s->tri_sorted, n, rays, hits, mask, nullptr, ctx->d_counter, ctx->d_error);
+    RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}
+
+int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask) {
+    if (n <= 0) return RT_OK;
+    if ((n + 64) > 0xFFFFFFFFll) return RT_EINVAL;
+    cudaStream_t st = ctx->stream;
+    RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), st));
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, trace_any_kernel, TRACE_THREADS, 0);
+    if (bps < 1) bps = 1;
+    int64_t want = (n + TRACE_THREADS - 1) / TRACE_THREADS;
+    int64_t grid = (int64_t)ctx->num_sms * bps;
+    if (grid > want) grid = want;
+    trace_any_kernel<<<(unsigned)grid, TRACE_THREADS, 0, st>>>(s->nodes, s->bvh4, s->tri_sorted, n, rays, out, mask,
+                                                              ctx->d_counter, ctx->d_error);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }

@@ -189,6 +189,49 @@ __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, in
     return h;
 }
 
+// watertight test for any-hit: t in [tmin, tmax] inclusive, no closest-t logic
+__device__ __forceinline__ bool tri_any(const RayPre& R, const float4 a, const float4 b, const float4 c, float tmax) {
+    float best = tmax;
+    int id = -1;
+    float u, v;
+    // tri_test accepts t <= best with (t < best or lower id); with id = -1 a hit
+    // exactly at tmax is rejected, so test against a slightly larger bound and
+    // re-check inclusively
+    best = nextafterf(tmax, INFINITY);
+    if (!tri_test(R, a, b, c, best, id, u, v)) return false;
+    return best <= tmax;
+}
+
+// Any-hit (accel.py:656-699, 852-895): the first accepted intersection in
+// [tmin, tmax] ends the walk; children are visited in slot order (no sort).
+__device__ __forceinline__ bool trace_any4(const float4* __restrict__ bvh4, int root, const float4* __restrict__ tris,
+                                           const RayPre& R, float tmax, uint32_t ray_mask, int* stack) {
+    int sp = 0;
+    stack[0] = RT_SENTINEL;
+    int node = root;
+    while (node != RT_SENTINEL) {
+        if (node >= 0) {
+            const float4* q = bvh4 + 8 * node;
+            const float4 l0 = __ldg(q), h0 = __ldg(q + 1), l1 = __ldg(q + 2), h1 = __ldg(q + 3);
+            const float4 l2 = __ldg(q + 4), h2 = __ldg(q + 5), l3 = __ldg(q + 6), h3 = __ldg(q + 7);
+            const bool b0 = box_enter(R, l0.x, h0.x, l0.y, h0.y, l0.z, h0.z, tmax) != INFINITY;
+            const bool b1 = box_enter(R, l1.x, h1.x, l1.y, h1.y, l1.z, h1.z, tmax) != INFINITY;
+            const bool b2 = box_enter(R, l2.x, h2.x, l2.y, h2.y, l2.z, h2.z, tmax) != INFINITY;
+            const bool b3 = box_enter(R, l3.x, h3.x, l3.y, h3.y, l3.z, h3.z, tmax) != INFINITY;
+            if (b3) stack[++sp] = __float_as_int(l3.w);
+            if (b2) stack[++sp] = __float_as_int(l2.w);
+            if (b1) stack[++sp] = __float_as_int(l1.w);
+            if (b0) stack[++sp] = __float_as_int(l0.w);
+        } else {
+            const float4* tp = tris + 3 * (~node);
+            const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
+            if ((__float_as_uint(b.w) & ray_mask) && tri_any(R, a, b, c, tmax)) return true;
+        }
+        node = stack[sp--];
+    }
+    return false;
+}
+
 // Stack of the 4-wide walk: at most 3 pushes per BVH4 level and ceil(h/2) levels
 // for a binary tree of height h <= RT_STACK - 1 (the depth limit the build enforces).
 #define RT_STACK4 (3 * (RT_STACK / 2) + 4)

@@ -62,18 +62,21 @@ def make_params(scene, width, height, s0, s1, integrator, seed, cfg, jitter, ker
     if integrator == "pt-nee" and len(scene.lights) == 0:
         warnings.warn("scene has no emissive triangles, falling back to plain path tracing")
         integrator = "pt"
-    if integrator not in ("eye", "pt"):
-        raise ValueError(f"integrator {integrator!r} needs the GPU any-hit kernel (not built yet)")
     if kernel not in KERNELS:
         raise ValueError(f"unknown kernel {kernel!r}, expected one of {tuple(KERNELS)}")
+    if kernel == "wavefront" and integrator not in ("eye", "pt"):
+        raise ValueError(f"integrator {integrator!r} runs in the megakernel only (kernel='mega')")
     cfg, sky, off = resolve_config(scene, cfg)
     scene.camera.validate_distortion()
     p = RenderParams()
     p.width, p.height, p.s0, p.s1 = int(width), int(height), int(s0), int(s1)
     p.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
     p.jitter = 1 if jitter else 0
-    p.integrator = _native.RT_INTEG_EYE if integrator == "eye" else _native.RT_INTEG_PT
+    p.integrator = {"eye": _native.RT_INTEG_EYE, "ao": _native.RT_INTEG_AO, "pt": _native.RT_INTEG_PT,
+                    "pt-nee": _native.RT_INTEG_PTNEE}[integrator]
     p.max_depth = int(cfg.max_depth)
+    p.ao_count = int(cfg.ao_ray_count)
+    p.ao_length = float(min(cfg.ao_max_length, 3.0e38))
     p.kernel = KERNELS[kernel]
     for k, x in enumerate(scene.camera.as_tuple()):
         p.cam[k] = x

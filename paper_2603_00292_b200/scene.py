@@ -260,8 +260,13 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0) -> Scene:
                    np.concatenate(t_prim), np.concatenate(t_mask), np.concatenate(t_mat), mat_color, mat_emissive,
                    bits=QUALITIES[quality], root_lo=root_lo, root_hi=root_hi, instances=len(desc.instances),
                    inverses=np.array(inverses))
+    lights = _light_rows(desc, mat_index, inst_list)
+    if len(lights):
+        rows = np.ascontiguousarray(np.concatenate([lights.v0, lights.v1, lights.v2, lights.normal, lights.emissive,
+                                                    lights.area[:, None]], axis=1), np.float32)
+        check(lib().rt_scene_set_lights(ctx.handle, tlas.handle, rows.shape[0], ptr(rows)))
     return Scene(camera=desc.camera, tlas=tlas, mat_color=mat_color, mat_emissive=mat_emissive,
-                 inst_material=np.array(inst_material, np.int64), lights=_light_rows(desc, mat_index, inst_list),
+                 inst_material=np.array(inst_material, np.int64), lights=lights,
                  sky=np.ascontiguousarray(desc.sky, np.float64), background=np.ascontiguousarray(desc.background,
                                                                                                  np.float64),
                  root_box=(root_lo, root_hi))

@@ -123,11 +123,59 @@ def test_furnace(native):
     assert abs(m - 0.5) <= 0.02, m
 
 
+def _mean_img(acc):
+    return acc[:, :, :3] / acc[:, :, 3:]
+
+
+def test_ao_vs_reference(cornell_gpu, cornell_oracle):
+    """integrators.py:144-179: same-seed AO.  Each sample is a multiple of 1/ao_count;
+    an fp32 occlusion decision can differ from float64 only for rays grazing an edge."""
+    g = golden("cornell_render")
+    w, h, spp, seed, jit, md = (int(x) for x in g["ao16_args"])
+    acc, st = render_frame(cornell_gpu, w, h, spp, "ao", seed=seed, cfg=IntegratorConfig(max_depth=md, ao_ray_count=8),
+                           return_stats=True)
+    assert st["rays"] == int(g["ao16_rays"])
+    d = np.abs(acc.mean() - _mean_img(g["ao16"]))
+    assert np.mean(d < 1e-6) >= 0.98 and d.max() <= 0.125 / spp + 1e-6, (np.mean(d < 1e-6), d.max())
+    a2 = render_frame(cornell_gpu, 96, 64, 4, "ao", seed=2, cfg=IntegratorConfig(ao_ray_count=16))
+    r2, _ = cornell_oracle.render_frame(96, 64, 4, "ao", seed=2, ao_ray_count=16, workers=8)
+    d2 = np.abs(a2.mean() - _mean_img(r2))
+    assert np.mean(d2 < 1e-6) >= 0.98 and float(np.sqrt(np.mean(d2 ** 2))) < 5e-3
+
+
+def test_ptnee_vs_reference(cornell_gpu, cornell_oracle):
+    """integrators.py:238-331: same-seed PT with next-event estimation (shadow rays via any-hit)."""
+    g = golden("cornell_render")
+    w, h, spp, seed, jit, md = (int(x) for x in g["nee16_args"])
+    acc, st = render_frame(cornell_gpu, w, h, spp, "pt-nee", seed=seed, cfg=IntegratorConfig(max_depth=md),
+                           return_stats=True)
+    assert abs(st["rays"] - int(g["nee16_rays"])) <= 2
+    d = acc.mean() - _mean_img(g["nee16"])
+    assert float(np.sqrt(np.mean(d ** 2))) <= 1e-3 and np.abs(d).max() <= 5e-2
+    a2, s2 = render_frame(cornell_gpu, 128, 96, 4, "pt-nee", seed=0, cfg=IntegratorConfig(max_depth=5),
+                          return_stats=True)
+    r2, rays2 = cornell_oracle.render_frame(128, 96, 4, "pt-nee", max_depth=5, workers=8)
+    d2 = a2.mean() - _mean_img(r2)
+    assert float(np.sqrt(np.mean(d2 ** 2))) <= 1e-3, float(np.sqrt(np.mean(d2 ** 2)))
+    assert abs(s2["rays"] - rays2) <= 1e-3 * rays2
+
+
+def test_any_hit_vs_reference(native):
+    from paper_2603_00292_b200 import any_hit_batch
+    sc = compile_scene(scenes.cornell_description())
+    gd = golden("cornell_hits")
+    got = any_hit_batch(sc, gd["RO"], gd["RD"], gd["tmin"], gd["tmax"])
+    assert got.dtype == bool
+    agree = np.mean(got == gd["rany"])
+    assert agree >= 0.999, agree
+    assert not any_hit_batch(sc, gd["RO"], gd["RD"], gd["tmin"], gd["tmax"], ray_mask=0).any()
+
+
 def test_render_errors(cornell_gpu):
     with pytest.raises(ValueError):
         render_frame(cornell_gpu, 0, 8, 1)
     with pytest.raises(ValueError):
-        render_frame(cornell_gpu, 8, 8, 1, "ao")
+        render_frame(cornell_gpu, 8, 8, 1, "ao", kernel="wavefront")
     with pytest.raises(ValueError):
         render_frame(cornell_gpu, 8, 8, 1, "nope")
     with pytest.raises(ValueError):
