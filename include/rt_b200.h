@@ -22,7 +22,7 @@ extern "C" {
 #define RT_OK 0
 #define RT_EINVAL (-1)        /* bad argument                 -> ValueError   */
 #define RT_ECUDA (-2)         /* CUDA runtime failure         -> RuntimeError */
-#define RT_EUNSUPPORTED (-3)  /* custom primitives (no GPU intersector yet) -> RegistryError */
+#define RT_EUNSUPPORTED (-3)  /* a ray reached a custom primitive with no intersector -> RegistryError */
 #define RT_EDEPTH (-4)        /* BVH deeper than the traversal stack -> BuildError (accel.py:148-149) */
 #define RT_ENOMEM (-5)        /* device allocation failed     -> MemoryError  */
 #define RT_ESTATE (-6)        /* e.g. trace before build      -> RuntimeError */
@@ -31,6 +31,11 @@ extern "C" {
 #define RT_INTEG_AO 1         /* integrators.py:144-179 _sample_ao    (megakernel) */
 #define RT_INTEG_PT 2         /* integrators.py:182-235 _sample_pt    */
 #define RT_INTEG_PTNEE 3      /* integrators.py:238-331 _sample_ptnee (megakernel) */
+
+/* trace flags (rt_trace_closest / rt_trace_any / rt_closest_hit_host / rt_any_hit_host) */
+#define RT_TRACE_NO_CUSTOM 1  /* no intersector registered for the scene's custom primitives
+                                 (registry=None, accel.py:1002-1008): a ray that reaches one
+                                 fails with RT_EUNSUPPORTED -> RegistryError (accel.py:800-803) */
 
 #define RT_KERNEL_MEGA 0      /* one persistent kernel per frame (K7)      */
 #define RT_KERNEL_WAVEFRONT 1 /* raygen / extend / shade / accumulate (K8) */
@@ -89,6 +94,13 @@ int rt_scene_create(rt_ctx* ctx, int64_t n, const float* tris, const float* norm
                     const int32_t* tri_material, const float* mat_color, const float* mat_emissive,
                     int32_t n_mat, rt_scene** out);
 void rt_scene_destroy(rt_scene* scene);
+/* custom primitives (compile_scene's sphere instances, scene.py:101-112): the LAST
+ * n_spheres primitives of the scene are spheres, each its own instance.  Their rows
+ * in rt_scene_create's `tris` hold the instance's world AABB as (lo, hi, lo) so the
+ * LBVH bounds them like triangles; `rows` holds 16 doubles per sphere: the instance
+ * inverse 3x4 (row-major, accel.py:311-336), the local center xyz and the radius.
+ * Hits on them are computed in float64 (geometry.py:334-363) with u = v = 0. */
+int rt_scene_set_spheres(rt_ctx* ctx, rt_scene* scene, int32_t n_spheres, const double* rows);
 /* new vertex positions for the same triangles (Blas.refit(vertices), accel.py:263-283);
  * host (n, 9) fp32, copied on the context stream; the BVH must be rebuilt */
 int rt_scene_set_vertices(rt_ctx* ctx, rt_scene* scene, const float* tris);
@@ -115,22 +127,23 @@ int rt_bvh_download(rt_ctx* ctx, rt_scene* scene, uint64_t* sorted_keys, uint32_
  * hits: (n, 4) [t (f32), flat id (i32, -1 miss), u, v]; stats (nullable): (n, 2)
  * u32 [triangle tests, node visits]. */
 int rt_trace_closest(rt_ctx* ctx, rt_scene* scene, int64_t n, const float* rays, float* hits,
-                     uint32_t ray_mask, uint32_t* stats);
+                     uint32_t ray_mask, uint32_t* stats, int32_t flags);
 /* Host buffers with the reference's dtypes (float64 / int64), chunked and
  * pipelined H2D / trace / D2H.  Misses: t = -1, inst = prim = -1 (accel.py:964, 1144).
  * stats nullable (n, 2) int64. */
 int rt_closest_hit_host(rt_ctx* ctx, rt_scene* scene, int64_t n, const double* origins,
                         const double* dirs, const double* t_min, const double* t_max,
                         uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
-                        double* v, double* normal, int64_t* stats);
+                        double* v, double* normal, int64_t* stats, int32_t flags);
 
 /* ---- any hit (replaces _any_batch / any_hit_batch, accel.py:979-992, 1159-1174) */
 /* device rays (n, 8) -> hit (n) uint8 (1 = some accepted intersection in [tmin, tmax]) */
 int rt_trace_any(rt_ctx* ctx, rt_scene* scene, int64_t n, const float* rays, uint8_t* hit,
-                 uint32_t ray_mask);
+                 uint32_t ray_mask, int32_t flags);
 /* host float64 rays -> host uint8 (numpy bool) */
 int rt_any_hit_host(rt_ctx* ctx, rt_scene* scene, int64_t n, const double* origins, const double* dirs,
-                    const double* t_min, const double* t_max, uint32_t ray_mask, uint8_t* hit);
+                    const double* t_min, const double* t_max, uint32_t ray_mask, uint8_t* hit,
+                    int32_t flags);
 /* emissive triangles for pt-nee (scene.py:58-76): rows of 16 floats =
  * v0, v1, v2, unit normal, emission (3 each), area */
 int rt_scene_set_lights(rt_ctx* ctx, rt_scene* scene, int32_t n_lights, const float* rows);

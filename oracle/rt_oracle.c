@@ -10,6 +10,7 @@
  * (pkg/src/pathtrace, a numba CPU library) operation for operation, so that
  * the result is bit-identical to the reference on the same inputs:
  *   - _tri_hit            geometry.py:219-275
+ *   - _sphere_hit / sphere_intersector   geometry.py:334-363, accel.py:396-401
  *   - _aabb_hit           geometry.py:278-330
  *   - _build_bvh (binned SAH / median)   accel.py:68-187
  *   - _blas_closest / _tlas_closest      accel.py:575-653, 762-849
@@ -78,6 +79,33 @@ static inline double tri_hit(double ox, double oy, double oz, double dx, double 
     *ov = ea / s;
     double nlen = sqrt(nx * nx + ny * ny + nz * nz);
     *onx = nx / nlen; *ony = ny / nlen; *onz = nz / nlen;
+    return t;
+}
+
+/* geometry.py:334-363  _sphere_hit: stable quadratic solve; t < 0 on miss */
+static inline double sphere_hit(double ox, double oy, double oz, double dx, double dy, double dz,
+                                double t_min, double t_max, double cx, double cy, double cz, double r,
+                                double* onx, double* ony, double* onz)
+{
+    double lx = ox - cx, ly = oy - cy, lz = oz - cz;
+    double a = dx * dx + dy * dy + dz * dz;
+    double b = 2.0 * (lx * dx + ly * dy + lz * dz);
+    double c = lx * lx + ly * ly + lz * lz - r * r;
+    double disc = b * b - 4.0 * a * c;
+    if (disc < 0.0) return -1.0;
+    double sq = sqrt(disc);
+    double q = -0.5 * (b + copysign(sq, b));
+    double t0, t1;
+    if (q == 0.0) { t0 = 0.0; t1 = 0.0; }
+    else { t0 = q / a; t1 = c / q; }
+    if (t0 > t1) { double tmp = t0; t0 = t1; t1 = tmp; }
+    double t = t0;
+    if (t < t_min || t > t_max) {
+        t = t1;
+        if (t < t_min || t > t_max) return -1.0;
+    }
+    double px = ox + dx * t, py = oy + dy * t, pz = oz + dz * t;
+    *onx = (px - cx) / r; *ony = (py - cy) / r; *onz = (pz - cz) / r;
     return t;
 }
 
@@ -345,7 +373,11 @@ typedef struct {
     const double* n_bounds; const int64_t *n_left, *n_right, *n_count, *n_axis;
     const int64_t* prim_order; const int64_t* tri_vidx; const double* verts;
     int64_t n_inst;
+    /* custom primitives (accel.py:41-43 CUSTOM; sphere_intersector data rows cx cy cz r) */
+    const int64_t* b_data_ofs; const double* custom_data;
 } orc_bundle;
+
+#define KIND_CUSTOM 1
 
 #define PRIM_SENTINEL ((int64_t)1 << 62)
 
@@ -375,14 +407,20 @@ static int blas_closest(const orc_bundle* bd, int64_t b, double ox, double oy, d
             for (int64_t k = 0; k < cnt; ++k) {
                 int64_t prim = bd->prim_order[first + k];
                 *tests += 1;
-                int64_t tri = tri0 + prim;
-                const double* A = bd->verts + 3 * bd->tri_vidx[3 * tri + 0];
-                const double* Bv = bd->verts + 3 * bd->tri_vidx[3 * tri + 1];
-                const double* C = bd->verts + 3 * bd->tri_vidx[3 * tri + 2];
-                double u = 0, v = 0, nx = 0, ny = 0, nz = 0;
-                double t = tri_hit(ox, oy, oz, dx, dy, dz, t_min, cur_t,
-                                   A[0], A[1], A[2], Bv[0], Bv[1], Bv[2], C[0], C[1], C[2],
-                                   &u, &v, &nx, &ny, &nz);
+                double u = 0, v = 0, nx = 0, ny = 0, nz = 0, t;
+                if (bd->b_kind[b] == KIND_CUSTOM) {
+                    /* accel.py:618-623: _custom_hit(table, slot, data0 + prim, ...), u = v = 0 */
+                    const double* S = bd->custom_data + 4 * (bd->b_data_ofs[b] + prim);
+                    t = sphere_hit(ox, oy, oz, dx, dy, dz, t_min, cur_t, S[0], S[1], S[2], S[3], &nx, &ny, &nz);
+                } else {
+                    int64_t tri = tri0 + prim;
+                    const double* A = bd->verts + 3 * bd->tri_vidx[3 * tri + 0];
+                    const double* Bv = bd->verts + 3 * bd->tri_vidx[3 * tri + 1];
+                    const double* C = bd->verts + 3 * bd->tri_vidx[3 * tri + 2];
+                    t = tri_hit(ox, oy, oz, dx, dy, dz, t_min, cur_t,
+                                A[0], A[1], A[2], Bv[0], Bv[1], Bv[2], C[0], C[1], C[2],
+                                &u, &v, &nx, &ny, &nz);
+                }
                 if (t >= 0.0 && (t < cur_t || (t == cur_t && prim < cur_prim))) {
                     found = 1; cur_t = t; cur_prim = prim;
                     hnx = nx; hny = ny; hnz = nz; hu = u; hv = v;
@@ -418,14 +456,19 @@ static int blas_any(const orc_bundle* bd, int64_t b, double ox, double oy, doubl
             int64_t first = prim0 + bd->n_left[row];
             for (int64_t k = 0; k < cnt; ++k) {
                 int64_t prim = bd->prim_order[first + k];
-                int64_t tri = tri0 + prim;
-                const double* A = bd->verts + 3 * bd->tri_vidx[3 * tri + 0];
-                const double* Bv = bd->verts + 3 * bd->tri_vidx[3 * tri + 1];
-                const double* C = bd->verts + 3 * bd->tri_vidx[3 * tri + 2];
-                double u, v, nx, ny, nz;
-                double t = tri_hit(ox, oy, oz, dx, dy, dz, t_min, t_max,
-                                   A[0], A[1], A[2], Bv[0], Bv[1], Bv[2], C[0], C[1], C[2],
-                                   &u, &v, &nx, &ny, &nz);
+                double u, v, nx, ny, nz, t;
+                if (bd->b_kind[b] == KIND_CUSTOM) {
+                    const double* S = bd->custom_data + 4 * (bd->b_data_ofs[b] + prim);
+                    t = sphere_hit(ox, oy, oz, dx, dy, dz, t_min, t_max, S[0], S[1], S[2], S[3], &nx, &ny, &nz);
+                } else {
+                    int64_t tri = tri0 + prim;
+                    const double* A = bd->verts + 3 * bd->tri_vidx[3 * tri + 0];
+                    const double* Bv = bd->verts + 3 * bd->tri_vidx[3 * tri + 1];
+                    const double* C = bd->verts + 3 * bd->tri_vidx[3 * tri + 2];
+                    t = tri_hit(ox, oy, oz, dx, dy, dz, t_min, t_max,
+                                A[0], A[1], A[2], Bv[0], Bv[1], Bv[2], C[0], C[1], C[2],
+                                &u, &v, &nx, &ny, &nz);
+                }
                 if (t >= 0.0) return 1;
             }
         } else {

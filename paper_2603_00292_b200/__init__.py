@@ -12,7 +12,8 @@ from .scene_io import (AccumBuffer, InstanceDecl, Material, ParseError, SceneDes
                        load_obj, load_scene, parse_obj, parse_scene, ppm_bytes, resolve, write_ppm)
 from ._native import BuildError, RegistryError
 from .scene import Scene, compile_scene
-from .accel import any_hit_batch, closest_hit_batch, trace_any, trace_closest
+from .accel import (CUSTOM, SPHERE_GEOM_TYPE, TRIANGLES, IntersectorRegistry, any_hit_batch, closest_hit_batch,
+                    make_sphere_registry, sphere_aabbs, sphere_data, sphere_intersector, trace_any, trace_closest)
 from .integrators import INTEGRATORS, IntegratorConfig, render_frame, render_into
 
 __version__ = "0.1.0"

@@ -80,12 +80,13 @@ def lib():
             "rt_scene_set_vertices": [vp, vp, vp],
             "rt_bvh_info": [vp, vp, vp, vp, vp],
             "rt_bvh_download": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
-            "rt_trace_closest": [vp, vp, i64, vp, vp, u32, vp],
-            "rt_closest_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp, vp],
+            "rt_trace_closest": [vp, vp, i64, vp, vp, u32, vp, i32],
+            "rt_closest_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp, vp, i32],
             "rt_render": [vp, vp, ctypes.POINTER(RenderParams), vp, vp],
-            "rt_trace_any": [vp, vp, i64, vp, vp, u32],
-            "rt_any_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp],
+            "rt_trace_any": [vp, vp, i64, vp, vp, u32, i32],
+            "rt_any_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, i32],
             "rt_scene_set_lights": [vp, vp, i32, vp],
+            "rt_scene_set_spheres": [vp, vp, i32, vp],
             "rt_raygen": [vp, ctypes.POINTER(RenderParams), i32, vp],
         }
         for name, args in sigs.items():

@@ -32,13 +32,19 @@ static int check_device_error(rt_ctx* ctx) {
     int e = 0;
     RT_CUDA_TRY(cudaMemcpyAsync(&e, ctx->d_error, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
     RT_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (e == 0) return RT_OK;
+    int z = 0;
+    cudaMemcpy(ctx->d_error, &z, sizeof z, cudaMemcpyHostToDevice);
     if (e == RT_EDEPTH) {
         rt_set_error("BVH height exceeds the %d-entry traversal stack", RT_STACK - 1);
-        int z = 0;
-        cudaMemcpy(ctx->d_error, &z, sizeof z, cudaMemcpyHostToDevice);
         return RT_EDEPTH;
     }
-    return RT_OK;
+    if (e == RT_EUNSUPPORTED) {
+        rt_set_error("a ray reached a custom primitive with no intersection function registered");
+        return RT_EUNSUPPORTED;
+    }
+    rt_set_error("device error %d", e);
+    return RT_ECUDA;
 }
 
 extern "C" {
@@ -197,7 +203,7 @@ void rt_scene_destroy(rt_scene* s) {
     void* ptrs[] = {s->tris, s->tri_attr, s->tri_inst, s->tri_prim, s->tri_mask, s->mat_color, s->mat_emissive,
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->parent, s->child,
                     s->flags, s->cbounds, s->cb_enc, s->sort_scratch, s->leaf_box, s->emit_items,
-                    s->emit_count, s->lights};
+                    s->emit_count, s->lights, s->spheres};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;
@@ -311,19 +317,19 @@ int rt_bvh_download(rt_ctx* c, rt_scene* s, uint64_t* sorted_keys, uint32_t* ord
 }
 
 int rt_trace_closest(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, float* hits, uint32_t ray_mask,
-                     uint32_t* stats) {
+                     uint32_t* stats, int32_t flags) {
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0 && (n == 0 || (rays && hits)), "bad ray/hit buffers");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    return rt_trace_impl(c, s, n, rays, reinterpret_cast<float4*>(hits), ray_mask, stats);
+    return rt_trace_impl(c, s, n, rays, reinterpret_cast<float4*>(hits), ray_mask, stats, flags & RT_TRACE_NO_CUSTOM);
 }
 
 // accel.py:1128-1156 with the reference's host dtypes; rays are processed in
 // chunks through pinned staging: H2D(f64) -> pack -> trace -> expand -> D2H(f64)
 int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const double* d, const double* tmin,
                         const double* tmax, uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
-                        double* v, double* nrm, int64_t* stats) {
+                        double* v, double* nrm, int64_t* stats, int32_t flags) {
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0, "negative ray count");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
@@ -365,9 +371,9 @@ int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, cons
         RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
         int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
         if (rc) return rc;
-        rc = rt_trace_impl(c, s, m, d_rays, d_hits, ray_mask, stats ? d_stats : nullptr);
+        rc = rt_trace_impl(c, s, m, d_rays, d_hits, ray_mask, stats ? d_stats : nullptr, flags & RT_TRACE_NO_CUSTOM);
         if (rc) return rc;
-        rc = rt_expand_hits_f64(c, s, m, d_hits, d_t, d_inst, d_prim, d_u, d_v, d_n);
+        rc = rt_expand_hits_f64(c, s, m, d_hits, d_t, d_inst, d_prim, d_u, d_v, d_n, d_rays);
         if (rc) return rc;
         RT_CUDA_TRY(cudaMemcpyAsync(t + b, d_t, 8 * m, cudaMemcpyDeviceToHost, st));
         RT_CUDA_TRY(cudaMemcpyAsync(inst + b, d_inst, 8 * m, cudaMemcpyDeviceToHost, st));
@@ -388,17 +394,18 @@ int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, cons
     return check_device_error(c);
 }
 
-int rt_trace_any(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, uint8_t* hit, uint32_t ray_mask) {
+int rt_trace_any(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, uint8_t* hit, uint32_t ray_mask,
+                 int32_t flags) {
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0 && (n == 0 || (rays && hit)), "bad ray/hit buffers");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    return rt_trace_any_impl(c, s, n, rays, hit, ray_mask);
+    return rt_trace_any_impl(c, s, n, rays, hit, ray_mask, flags & RT_TRACE_NO_CUSTOM);
 }
 
 // accel.py:1159-1174 any_hit_batch with host float64 rays -> host bool (uint8)
 int rt_any_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const double* d, const double* tmin,
-                    const double* tmax, uint32_t ray_mask, uint8_t* out) {
+                    const double* tmax, uint32_t ray_mask, uint8_t* out, int32_t flags) {
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0, "negative ray count");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
@@ -429,7 +436,7 @@ int rt_any_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const do
         RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
         int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
         if (rc) return rc;
-        rc = rt_trace_any_impl(c, s, m, d_rays, d_out, ray_mask);
+        rc = rt_trace_any_impl(c, s, m, d_rays, d_out, ray_mask, flags & RT_TRACE_NO_CUSTOM);
         if (rc) return rc;
         RT_CUDA_TRY(cudaMemcpyAsync(out + b, d_out, m, cudaMemcpyDeviceToHost, st));
     }
@@ -457,6 +464,21 @@ int rt_scene_set_lights(rt_ctx* c, rt_scene* s, int32_t n_lights, const float* r
     }
     RT_CUDA_TRY(cudaMalloc(&s->lights, sizeof(float4) * L.size()));
     RT_CUDA_TRY(cudaMemcpy(s->lights, L.data(), sizeof(float4) * L.size(), cudaMemcpyHostToDevice));
+    return RT_OK;
+}
+
+int rt_scene_set_spheres(rt_ctx* c, rt_scene* s, int32_t n_spheres, const double* rows) {
+    RT_CHECK_ARG(c && s && n_spheres >= 0 && (n_spheres == 0 || rows), "bad sphere table");
+    RT_CHECK_ARG(n_spheres <= s->n, "more spheres than primitives");
+    for (int k = 0; k < n_spheres; ++k)
+        RT_CHECK_ARG(rows[16 * k + 15] > 0.0, "sphere radius must be > 0");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    if (s->spheres) cudaFree(s->spheres);
+    s->spheres = nullptr;
+    s->n_spheres = n_spheres;
+    if (n_spheres == 0) return RT_OK;
+    RT_CUDA_TRY(cudaMalloc(&s->spheres, sizeof(double) * 16 * (size_t)n_spheres));
+    RT_CUDA_TRY(cudaMemcpy(s->spheres, rows, sizeof(double) * 16 * (size_t)n_spheres, cudaMemcpyHostToDevice));
     return RT_OK;
 }
 

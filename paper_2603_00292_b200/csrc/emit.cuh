@@ -200,8 +200,18 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
     }
     __syncthreads();
     // hand-off to phase B: smem slot `tid` left with a single arrival (its sibling
-    // extends past the block), then deferred node `tid`
-    if (tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0) {
+    // extends past the block), then deferred node `tid`.  One global atomic per
+    // block reserves the block's items (per-item atomics on the one counter
+    // serialise in L2: ~20% of this kernel's stall samples)
+    __shared__ unsigned s_base, s_next;
+    const bool single = tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0;
+    const int n_single = __syncthreads_count(single);
+    if (tid == 0) {
+        s_base = atomicAdd(item_count, (unsigned)(n_single + s_ndef));
+        s_next = 0;
+    }
+    __syncthreads();
+    if (single) {
         const int endpoint = s_range[tid];
         const int gamma = (int)B + tid;
         const bool left = endpoint <= gamma;         // left child: [endpoint, gamma]; right: [gamma+1, endpoint]
@@ -215,9 +225,9 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         M.hi[0] = hi4.x; M.hi[1] = hi4.y; M.hi[2] = hi4.z;
         M.dl = s_delta[M.l - (int)B];
         M.dr = s_delta[M.r - (int)B + 1];
-        items[atomicAdd(item_count, 1u)] = M;
+        items[s_base + atomicAdd(&s_next, 1u)] = M;
     }
-    if (tid < s_ndef) items[atomicAdd(item_count, 1u)] = s_def[tid];
+    if (tid < s_ndef) items[s_base + n_single + tid] = s_def[tid];
 }
 
 // Phase B as its own persistent kernel: the few boundary-crossing nodes of all

@@ -43,20 +43,41 @@ __device__ __forceinline__ void load_tri(const float* tris, int64_t i, float t[9
     for (int k = 0; k < 9; ++k) t[k] = __ldg(p + k);
 }
 
+// Block-cooperative staging of TRI_CHUNK consecutive triangles (36 B each) into
+// shared memory with 16-B coalesced loads; the per-triangle loads of a direct
+// (n, 9) walk are 36-B strided and waste most of each sector request.
+constexpr int TRI_CHUNK = 256;
+__device__ __forceinline__ int stage_tris(const float* __restrict__ tris, int64_t base, int64_t n, float* s) {
+    const int64_t left = n - base;
+    const int cnt = left < TRI_CHUNK ? (int)left : TRI_CHUNK;
+    const int nf = 9 * cnt, nv = nf >> 2;
+    const float4* src = reinterpret_cast<const float4*>(tris + 9 * base);   // 9216-B aligned chunks
+    for (int k = threadIdx.x; k < nv; k += blockDim.x) reinterpret_cast<float4*>(s)[k] = __ldg(src + k);
+    for (int k = 4 * nv + threadIdx.x; k < nf; k += blockDim.x) s[k] = __ldg(tris + 9 * base + k);
+    return cnt;
+}
+
 // ---- K1 -------------------------------------------------------------------
-__global__ void __launch_bounds__(256) lbvh_bounds_kernel(const float* __restrict__ tris, int64_t n,
-                                                         unsigned int* __restrict__ cb_enc) {
+__global__ void __launch_bounds__(TRI_CHUNK) lbvh_bounds_kernel(const float* __restrict__ tris, int64_t n,
+                                                               unsigned int* __restrict__ cb_enc) {
+    __shared__ __align__(16) float s_tri[9 * TRI_CHUNK];
     float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        float t[9], blo[3], bhi[3];
-        load_tri(tris, i, t);
-        tri_box(t, blo, bhi);
+    for (int64_t base = blockIdx.x * (int64_t)TRI_CHUNK; base < n; base += (int64_t)gridDim.x * TRI_CHUNK) {
+        const int cnt = stage_tris(tris, base, n, s_tri);
+        __syncthreads();
+        if ((int)threadIdx.x < cnt) {
+            float t[9], blo[3], bhi[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            float c = __fmul_rn(0.5f, __fadd_rn(blo[a], bhi[a]));
-            lo[a] = sel_min(lo[a], c);
-            hi[a] = sel_max(hi[a], c);
+            for (int k = 0; k < 9; ++k) t[k] = s_tri[9 * threadIdx.x + k];
+            tri_box(t, blo, bhi);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                float c = __fmul_rn(0.5f, __fadd_rn(blo[a], bhi[a]));
+                lo[a] = sel_min(lo[a], c);
+                hi[a] = sel_max(hi[a], c);
+            }
         }
+        __syncthreads();
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
@@ -115,38 +136,43 @@ __device__ __forceinline__ uint64_t expand21(uint64_t v) {
 // K2 fused with the onesweep digit histogram of every pass (the keys are in
 // registers here, so the histogram costs no extra read of the key array)
 template <typename K, int B, int PASSES>
-__global__ void __launch_bounds__(256) lbvh_morton_kernel(const float* __restrict__ tris, int64_t n,
-                                                         const float* __restrict__ cb, K* __restrict__ keys,
-                                                         unsigned int* __restrict__ hist) {
+__global__ void __launch_bounds__(TRI_CHUNK) lbvh_morton_kernel(const float* __restrict__ tris, int64_t n,
+                                                               const float* __restrict__ cb, K* __restrict__ keys,
+                                                               unsigned int* __restrict__ hist) {
     __shared__ unsigned int s_hist[PASSES][256];
+    __shared__ __align__(16) float s_tri[9 * TRI_CHUNK];
     for (int i = threadIdx.x; i < PASSES * 256; i += blockDim.x) (&s_hist[0][0])[i] = 0;
-    __syncthreads();
     const float scale = (float)(1u << B), qmax = (float)((1u << B) - 1u);
     float lo[3], inv[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) { lo[a] = __ldg(cb + a); inv[a] = __ldg(cb + 6 + a); }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        float t[9], blo[3], bhi[3];
-        load_tri(tris, i, t);
-        tri_box(t, blo, bhi);
-        uint32_t q[3];
+    for (int64_t base = blockIdx.x * (int64_t)TRI_CHUNK; base < n; base += (int64_t)gridDim.x * TRI_CHUNK) {
+        const int cnt = stage_tris(tris, base, n, s_tri);
+        __syncthreads();
+        if ((int)threadIdx.x < cnt) {
+            float t[9], blo[3], bhi[3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            float c = __fmul_rn(0.5f, __fadd_rn(blo[a], bhi[a]));
-            float x = __fmul_rn(__fmul_rn(__fsub_rn(c, lo[a]), inv[a]), scale);
-            x = sel_min(sel_max(x, 0.0f), qmax);
-            q[a] = (uint32_t)x;
+            for (int k = 0; k < 9; ++k) t[k] = s_tri[9 * threadIdx.x + k];
+            tri_box(t, blo, bhi);
+            uint32_t q[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                float c = __fmul_rn(0.5f, __fadd_rn(blo[a], bhi[a]));
+                float x = __fmul_rn(__fmul_rn(__fsub_rn(c, lo[a]), inv[a]), scale);
+                x = sel_min(sel_max(x, 0.0f), qmax);
+                q[a] = (uint32_t)x;
+            }
+            K k;
+            if (B == 10)
+                k = (K)((expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]));
+            else
+                k = (K)((expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]));
+            keys[base + threadIdx.x] = k;
+#pragma unroll
+            for (int p = 0; p < PASSES; ++p) atomicAdd(&s_hist[p][(unsigned)(k >> (8 * p)) & 0xFFu], 1u);
         }
-        K k;
-        if (B == 10)
-            k = (K)((expand10(q[0]) << 2) | (expand10(q[1]) << 1) | expand10(q[2]));
-        else
-            k = (K)((expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]));
-        keys[i] = k;
-#pragma unroll
-        for (int p = 0; p < PASSES; ++p) atomicAdd(&s_hist[p][(unsigned)(k >> (8 * p)) & 0xFFu], 1u);
+        __syncthreads();
     }
-    __syncthreads();
     for (int i = threadIdx.x; i < PASSES * RADIX; i += blockDim.x) {
         unsigned v = (&s_hist[0][0])[i];
         if (v) atomicAdd(hist + i, v);

@@ -96,9 +96,11 @@ __device__ __forceinline__ void start_path(const FrameConst& F, int64_t pix, int
 
 // One closest-hit result applied to the path (integrators.py:129-141 eye,
 // 198-235 pt).  Returns true if the path continues with a new ray.
+template <bool SPH>
 __device__ __forceinline__ bool shade_bounce(const FrameConst& F, const float4* __restrict__ attr,
                                              const float4* __restrict__ mat_color,
-                                             const float4* __restrict__ mat_emis, const HitRec& h, PathState& P) {
+                                             const float4* __restrict__ mat_emis, const HitRec& h, PathState& P,
+                                             const SphereView& sv) {
     if (F.integ == RT_INTEG_EYE) {
         if (h.id < 0) { P.rr = F.bg[0]; P.rg = F.bg[1]; P.rb = F.bg[2]; return false; }
         int m = __float_as_int(__ldg(attr + h.id).w);
@@ -117,7 +119,8 @@ __device__ __forceinline__ bool shade_bounce(const FrameConst& F, const float4* 
         P.rr += P.tr * e.x; P.rg += P.tg * e.y; P.rb += P.tb * e.z;
         return false;
     }
-    float nx = a.x, ny = a.y, nz = a.z;
+    float nx, ny, nz;
+    hit_normal<SPH>(sv, h.id, a, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, h.t, nx, ny, nz);
     if (nx * P.dx + ny * P.dy + nz * P.dz > 0.0f) { nx = -nx; ny = -ny; nz = -nz; }
     float px = P.ox + P.dx * h.t, py = P.oy + P.dy * h.t, pz = P.oz + P.dz * h.t;
     float x0 = rt_uniform(P.state, P.inc);
@@ -150,17 +153,19 @@ __device__ __forceinline__ float geom_term(float px, float py, float pz, float n
 }
 
 // integrators.py:144-179 _sample_ao: unoccluded fraction of the cosine lobe
+template <bool SPH>
 __device__ __forceinline__ float sample_ao(const FrameConst& F, const float4* __restrict__ bvh4, int root4,
                                            const float4* __restrict__ tris, const float4* __restrict__ attr,
-                                           PathState& P, int2* stack, unsigned long long& rays) {
+                                           PathState& P, int2* stack, unsigned long long& rays, const SphereView& sv) {
     RayPre R;
     ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
     uint32_t nt, nv;
-    const HitRec h = trace_ray4<false>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+    const HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv, sv);
     ++rays;
     if (h.id < 0) return 1.0f;
     const float4 a = __ldg(attr + h.id);
-    float nx = a.x, ny = a.y, nz = a.z;
+    float nx, ny, nz;
+    hit_normal<SPH>(sv, h.id, a, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, h.t, nx, ny, nz);
     if (nx * P.dx + ny * P.dy + nz * P.dz > 0.0f) { nx = -nx; ny = -ny; nz = -nz; }
     const float px = P.ox + P.dx * h.t + nx * F.offset;
     const float py = P.oy + P.dy * h.t + ny * F.offset;
@@ -177,7 +182,7 @@ __device__ __forceinline__ float sample_ao(const FrameConst& F, const float4* __
         const float wz = t[2] * sx + nz * sy + b[2] * sz;
         RayPre S;
         ray_setup(S, px, py, pz, wx, wy, wz, 0.0f);
-        occluded += trace_any4(bvh4, root4, tris, S, F.ao_length, RT_FULL, reinterpret_cast<int*>(stack)) ? 1 : 0;
+        occluded += trace_any4<SPH>(bvh4, root4, tris, S, F.ao_length, RT_FULL, reinterpret_cast<int*>(stack), sv) ? 1 : 0;
         ++rays;
     }
     return 1.0f - (float)occluded / (float)F.ao_count;
@@ -185,16 +190,17 @@ __device__ __forceinline__ float sample_ao(const FrameConst& F, const float4* __
 
 // integrators.py:238-331 _sample_ptnee: path tracing with one light connection per
 // vertex (3 draws: light, then 2 for the area sample), emission counted only at depth 0
+template <bool SPH>
 __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* __restrict__ bvh4, int root4,
                                              const float4* __restrict__ tris, const float4* __restrict__ attr,
                                              const float4* __restrict__ mat_color, const float4* __restrict__ mat_emis,
                                              const float4* __restrict__ lights, int n_lights, PathState& P,
-                                             int2* stack, unsigned long long& rays) {
+                                             int2* stack, unsigned long long& rays, const SphereView& sv) {
     for (int depth = 0; depth < F.max_depth; ++depth) {
         RayPre R;
         ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
         uint32_t nt, nv;
-        const HitRec h = trace_ray4<false>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+        const HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv, sv);
         ++rays;
         if (h.id < 0) {
             P.rr += P.tr * F.sky[0]; P.rg += P.tg * F.sky[1]; P.rb += P.tb * F.sky[2];
@@ -207,7 +213,8 @@ __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* 
             if (depth == 0) { P.rr += P.tr * e.x; P.rg += P.tg * e.y; P.rb += P.tb * e.z; }
             return;
         }
-        float nx = a.x, ny = a.y, nz = a.z;
+        float nx, ny, nz;
+        hit_normal<SPH>(sv, h.id, a, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, h.t, nx, ny, nz);
         if (nx * P.dx + ny * P.dy + nz * P.dz > 0.0f) { nx = -nx; ny = -ny; nz = -nz; }
         const float px = P.ox + P.dx * h.t, py = P.oy + P.dy * h.t, pz = P.oz + P.dz * h.t;
         const float4 c = __ldg(mat_color + m);
@@ -228,7 +235,7 @@ __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* 
             const float sqx = qx + ln.x * F.offset, sqy = qy + ln.y * F.offset, sqz = qz + ln.z * F.offset;
             RayPre S;
             ray_setup(S, spx, spy, spz, sqx - spx, sqy - spy, sqz - spz, 0.0f);
-            const bool occ = trace_any4(bvh4, root4, tris, S, 1.0f - 1e-3f, RT_FULL, reinterpret_cast<int*>(stack));
+            const bool occ = trace_any4<SPH>(bvh4, root4, tris, S, 1.0f - 1e-3f, RT_FULL, reinterpret_cast<int*>(stack), sv);
             ++rays;
             if (!occ) {
                 const float pdf = (1.0f / (float)n_lights) * (1.0f / l0.w);
@@ -255,12 +262,13 @@ __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* 
 // ---- K7: megakernel --------------------------------------------------------
 // Persistent warps fetch 32 pixels at a time; each lane renders samples
 // [s0, s1) of its pixel in order and adds the sums to accum once.
-template <int INTEG>
+template <int INTEG, bool SPH>
 __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     const FrameConst F, int s0, int s1, const float4* __restrict__ nodes, const float4* __restrict__ bvh4,
     const float4* __restrict__ tris, const float4* __restrict__ attr, const float4* __restrict__ mat_color,
     const float4* __restrict__ mat_emis, const float4* __restrict__ lights, int n_lights,
-    float4* __restrict__ accum, unsigned int* counter, unsigned long long* ray_total, int* err) {
+    float4* __restrict__ accum, unsigned int* counter, unsigned long long* ray_total, int* err,
+    const SphereView sv) {
     const int height = __float_as_int(__ldg(nodes + 3).z);
     const int root4 = __float_as_int(__ldg(nodes + 3).w);
     if (height + 1 > RT_STACK) {
@@ -286,18 +294,18 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
                 PathState P;
                 start_path(F, pix, s, P);
                 if constexpr (INTEG == RT_INTEG_AO) {
-                    const float v = sample_ao(F, bvh4, root4, tris, attr, P, stack, rays);
+                    const float v = sample_ao<SPH>(F, bvh4, root4, tris, attr, P, stack, rays, sv);
                     P.rr = P.rg = P.rb = v;
                 } else if constexpr (INTEG == RT_INTEG_PTNEE) {
-                    sample_ptnee(F, bvh4, root4, tris, attr, mat_color, mat_emis, lights, n_lights, P, stack, rays);
+                    sample_ptnee<SPH>(F, bvh4, root4, tris, attr, mat_color, mat_emis, lights, n_lights, P, stack, rays, sv);
                 } else {
                     for (int depth = 0; depth < max_depth; ++depth) {
                         RayPre R;
                         ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
                         uint32_t nt, nv;
-                        HitRec h = trace_ray4<false>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv);
+                        HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv, sv);
                         ++rays;
-                        if (!shade_bounce(F, attr, mat_color, mat_emis, h, P)) break;
+                        if (!shade_bounce<SPH>(F, attr, mat_color, mat_emis, h, P, sv)) break;
                     }
                 }
                 a.x += P.rr; a.y += P.rg; a.z += P.rb; a.w += 1.0f;
@@ -343,9 +351,10 @@ __global__ void __launch_bounds__(WF_THREADS) wf_raygen(const FrameConst F, cons
 }
 
 // extend: closest hit for every queued path (depth 0: identity queue)
+template <bool SPH>
 __global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ nodes, const float4* __restrict__ bvh4,
                                                     const float4* __restrict__ tris, Wave W, int depth,
-                                                    unsigned int* counter, int* err) {
+                                                    unsigned int* counter, int* err, const SphereView sv) {
     const int height = __float_as_int(__ldg(nodes + 3).z);
     const int root4 = __float_as_int(__ldg(nodes + 3).w);
     if (height + 1 > RT_STACK) {
@@ -369,7 +378,7 @@ __global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ n
             RayPre R;
             ray_setup(R, a.x, a.y, a.z, b.x, b.y, b.z, a.w);
             uint32_t nt, nv;
-            HitRec h = trace_ray4<false>(bvh4, root4, tris, R, b.w, RT_FULL, stack, nt, nv);
+            HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, b.w, RT_FULL, stack, nt, nv, sv);
             W.hit[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
             }
         }
@@ -378,9 +387,11 @@ __global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ n
 
 // shade: apply the hit, bounce, append survivors to the next queue with one
 // atomicAdd per warp (ballot + popc)
+template <bool SPH>
 __global__ void __launch_bounds__(WF_THREADS) wf_shade(const FrameConst F, const float4* __restrict__ attr,
                                                         const float4* __restrict__ mat_color,
-                                                        const float4* __restrict__ mat_emis, Wave W, int depth) {
+                                                        const float4* __restrict__ mat_emis, Wave W, int depth,
+                                                        const SphereView sv) {
     const unsigned n = W.count[depth];
     const int* q = depth == 0 ? nullptr : W.queue[depth & 1];
     int* qn = W.queue[(depth + 1) & 1];
@@ -403,7 +414,7 @@ __global__ void __launch_bounds__(WF_THREADS) wf_shade(const FrameConst F, const
             P.tr = tp.x; P.tg = tp.y; P.tb = tp.z; P.rr = rd.x; P.rg = rd.y; P.rb = rd.z;
             P.state = ((uint64_t)s0.y << 32) | s0.x;
             P.inc = ((uint64_t)s1.y << 32) | s1.x;
-            bool cont = shade_bounce(F, attr, mat_color, mat_emis, h, P);
+            bool cont = shade_bounce<SPH>(F, attr, mat_color, mat_emis, h, P, sv);
             W.rad[i] = make_float4(P.rr, P.rg, P.rb, 0.f);
             if (cont && !last) {
                 alive = true;
@@ -573,16 +584,26 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             if (grid > want) grid = want;
             kern<<<(unsigned)grid, MEGA_THREADS, 0, st>>>(F, p->s0, p->s1, s->nodes, s->bvh4, s->tri_sorted,
                                                           s->tri_attr, s->mat_color, s->mat_emissive, s->lights,
-                                                          s->n_lights, acc, ctx->d_counter, d_rays, ctx->d_error);
+                                                          s->n_lights, acc, ctx->d_counter, d_rays, ctx->d_error,
+                                                          rt_sphere_view(ctx, s, 0));
             RT_CUDA_TRY(cudaGetLastError());
             return RT_OK;
         };
         int rc;
+        const bool sph = s->n_spheres > 0;   // triangle-only scenes run the walk without the sphere branch
         switch (F.integ) {
-            case RT_INTEG_EYE: rc = launch(pt_megakernel<RT_INTEG_EYE>); break;
-            case RT_INTEG_AO: rc = launch(pt_megakernel<RT_INTEG_AO>); break;
-            case RT_INTEG_PTNEE: rc = launch(pt_megakernel<RT_INTEG_PTNEE>); break;
-            default: rc = launch(pt_megakernel<RT_INTEG_PT>); break;
+            case RT_INTEG_EYE:
+                rc = sph ? launch(pt_megakernel<RT_INTEG_EYE, true>) : launch(pt_megakernel<RT_INTEG_EYE, false>);
+                break;
+            case RT_INTEG_AO:
+                rc = sph ? launch(pt_megakernel<RT_INTEG_AO, true>) : launch(pt_megakernel<RT_INTEG_AO, false>);
+                break;
+            case RT_INTEG_PTNEE:
+                rc = sph ? launch(pt_megakernel<RT_INTEG_PTNEE, true>) : launch(pt_megakernel<RT_INTEG_PTNEE, false>);
+                break;
+            default:
+                rc = sph ? launch(pt_megakernel<RT_INTEG_PT, true>) : launch(pt_megakernel<RT_INTEG_PT, false>);
+                break;
         }
         if (rc) return rc;
     } else {
@@ -592,8 +613,10 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         if (rc) return rc;
         RT_CUDA_TRY(cudaMemsetAsync(wb->d_sample, 0, 32, st));
         RT_CUDA_TRY(cudaMemcpyAsync(wb->d_sample, &p->s0, sizeof(int), cudaMemcpyHostToDevice, st));
+        const bool sph = s->n_spheres > 0;
         int bps = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, wf_extend, 128, 0);
+        if (sph) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, wf_extend<true>, 128, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, wf_extend<false>, 128, 0);
         if (bps < 1) bps = 1;
         unsigned grid_ext = (unsigned)(ctx->num_sms * bps);
         unsigned grid_sh = (unsigned)ctx->num_sms * 8;
@@ -606,9 +629,18 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         RT_CUDA_TRY(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
         wf_raygen<<<grid_sh, WF_THREADS, 0, cap>>>(F, wb->d_sample, wb->W);
         for (int d = 0; d < md; ++d) {
-            wf_extend<<<grid_ext, 128, 0, cap>>>(s->nodes, s->bvh4, s->tri_sorted, wb->W, d, ctx->d_counter,
-                                                 ctx->d_error);
-            wf_shade<<<grid_sh, WF_THREADS, 0, cap>>>(F, s->tri_attr, s->mat_color, s->mat_emissive, wb->W, d);
+            const SphereView sv = rt_sphere_view(ctx, s, 0);
+            if (sph) {
+                wf_extend<true><<<grid_ext, 128, 0, cap>>>(s->nodes, s->bvh4, s->tri_sorted, wb->W, d, ctx->d_counter,
+                                                           ctx->d_error, sv);
+                wf_shade<true><<<grid_sh, WF_THREADS, 0, cap>>>(F, s->tri_attr, s->mat_color, s->mat_emissive, wb->W,
+                                                                d, sv);
+            } else {
+                wf_extend<false><<<grid_ext, 128, 0, cap>>>(s->nodes, s->bvh4, s->tri_sorted, wb->W, d,
+                                                            ctx->d_counter, ctx->d_error, sv);
+                wf_shade<false><<<grid_sh, WF_THREADS, 0, cap>>>(F, s->tri_attr, s->mat_color, s->mat_emissive,
+                                                                 wb->W, d, sv);
+            }
         }
         wf_accumulate<<<grid_sh, WF_THREADS, 0, cap>>>(F, wb->W, acc, wb->d_sample, ctx->d_counter, d_rays);
         cudaError_t ce = cudaStreamEndCapture(cap, &graph);

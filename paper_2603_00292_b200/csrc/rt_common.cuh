@@ -61,6 +61,9 @@ struct rt_scene {
     int n_lights;
     void* emit_items;               // boundary-crossing nodes handed from emit phase A to phase B
     unsigned int* emit_count;
+    // custom primitives: the last n_spheres flat primitives are spheres
+    double* spheres;                // (n_spheres, 16): inverse 3x4, center, radius
+    int n_spheres;
 };
 
 // --------------------------------------------------------------------------
@@ -161,11 +164,13 @@ __device__ __forceinline__ bool rt_primary_dir(const float* cam, float u, float 
 
 // host-side launch helpers (defined in capi.cu / lbvh.cu / trace.cu / render.cu)
 int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits);
+// custom_mode: 0 = spheres intersected, 1 = reaching one is RT_EUNSUPPORTED (no intersector registered)
 int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4* hits, uint32_t mask,
-                  uint32_t* stats);
-int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask);
+                  uint32_t* stats, int custom_mode);
+int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask,
+                      int custom_mode);
 int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
-                       int64_t* prim, double* u, double* v, double* nrm);
+                       int64_t* prim, double* u, double* v, double* nrm, const float* rays);
 int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, const double* tmin,
                      const double* tmax, float* rays);
 int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out);

@@ -9,11 +9,11 @@ constexpr int TRACE_THREADS = 128;
 
 // One warp fetches 32 rays at a time from a global counter (one atomicAdd per
 // warp), every lane runs the while-while traversal, then the warp fetches again.
-template <bool STATS>
+template <bool STATS, bool SPH>
 __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
     const float4* __restrict__ nodes, const float4* __restrict__ bvh4, const float4* __restrict__ tris, int64_t n,
     const float* __restrict__ rays, float4* __restrict__ hits, uint32_t ray_mask, uint32_t* __restrict__ stats,
-    unsigned int* counter, int* err) {
+    unsigned int* counter, int* err, const SphereView sv) {
     const int height = __float_as_int(__ldg(nodes + 3).z);   // root height == stack bound
     const int root4 = __float_as_int(__ldg(nodes + 3).w);    // BVH4 root (split position)
     if (height + 1 > RT_STACK) {
@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
             RayPre R;
             ray_setup(R, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
             uint32_t nt = 0, nv = 0;
-            HitRec h = trace_ray4<STATS>(bvh4, root4, tris, R, r.tmax, ray_mask, stack, nt, nv);
+            HitRec h = trace_ray4<STATS, SPH>(bvh4, root4, tris, R, r.tmax, ray_mask, stack, nt, nv, sv);
             hits[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
             if (STATS) reinterpret_cast<uint2*>(stats)[i] = make_uint2(nt, nv);
         }
@@ -41,9 +41,11 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
 }
 
 // any-hit over a ray buffer (same persistent warp fetch as the closest-hit kernel)
+template <bool SPH>
 __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_any_kernel(
     const float4* __restrict__ nodes, const float4* __restrict__ bvh4, const float4* __restrict__ tris, int64_t n,
-    const float* __restrict__ rays, uint8_t* __restrict__ out, uint32_t ray_mask, unsigned int* counter, int* err) {
+    const float* __restrict__ rays, uint8_t* __restrict__ out, uint32_t ray_mask, unsigned int* counter, int* err,
+    const SphereView sv) {
     const int height = __float_as_int(__ldg(nodes + 3).z);
     const int root4 = __float_as_int(__ldg(nodes + 3).w);
     if (height + 1 > RT_STACK) {
@@ -62,7 +64,7 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_any_kernel(
             TraceRay r = load_ray(rays, i);
             RayPre R;
             ray_setup(R, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
-            out[i] = trace_any4(bvh4, root4, tris, R, r.tmax, ray_mask, stack) ? 1 : 0;
+            out[i] = trace_any4<SPH>(bvh4, root4, tris, R, r.tmax, ray_mask, stack, sv) ? 1 : 0;
         }
     }
 }
@@ -79,10 +81,12 @@ __global__ void pack_rays_f64(int64_t n, const double* __restrict__ o, const dou
 }
 
 // hit (t, id, u, v) -> the reference's per-ray outputs (float64 / int64),
-// world normal from the per-triangle reference-style normal
+// world normal from the per-triangle reference-style normal, or
+// the sphere's at the hit point (rays needed only then)
 __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, const float4* __restrict__ attr,
                                 const int32_t* __restrict__ tri_inst, const int32_t* __restrict__ tri_prim,
-                                double* t, int64_t* inst, int64_t* prim, double* u, double* v, double* nrm) {
+                                double* t, int64_t* inst, int64_t* prim, double* u, double* v, double* nrm,
+                                const float* __restrict__ rays, const SphereView sv) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float4 h = hits[i];
         int id = __float_as_int(h.y);
@@ -92,6 +96,12 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
         } else {
             float4 a = attr[id];
             t[i] = h.x; inst[i] = tri_inst[id]; prim[i] = tri_prim[id]; u[i] = h.z; v[i] = h.w;
+            if (id >= sv.base) {
+                const TraceRay r = load_ray(rays, i);
+                const float3 w = sphere_normal(sv.rows + 16 * (int64_t)(id - sv.base), r.ox, r.oy, r.oz, r.dx, r.dy,
+                                               r.dz, h.x);
+                a.x = w.x; a.y = w.y; a.z = w.z;
+            }
             nrm[3 * i] = a.x; nrm[3 * i + 1] = a.y; nrm[3 * i + 2] = a.z;
         }
     }
@@ -100,43 +110,53 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
 }  // namespace
 
 int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4* hits, uint32_t mask,
-                  uint32_t* stats) {
+                  uint32_t* stats, int custom_mode) {
     if (n <= 0) return RT_OK;
     if ((n + 64) > 0xFFFFFFFFll) return RT_EINVAL;
     cudaStream_t st = ctx->stream;
     RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), st));
-    int blocks_per_sm = 0;
-    if (stats)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, trace_closest_kernel<true>, TRACE_THREADS, 0);
-    else
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, trace_closest_kernel<false>, TRACE_THREADS, 0);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-    int64_t want = (n + TRACE_THREADS - 1) / TRACE_THREADS;
-    int64_t grid = (int64_t)ctx->num_sms * blocks_per_sm;
-    if (grid > want) grid = want;
-    if (stats)
-        trace_closest_kernel<true><<<(unsigned)grid, TRACE_THREADS, 0, st>>>(
-            s->nodes, s->bvh4, s->tri_sorted, n, rays, hits, mask, stats, ctx->d_counter, ctx->d_error);
-    else
-        trace_closest_kernel<false><<<(unsigned)grid, TRACE_THREADS, 0, st>>>(
-            s->nodes, s->bvh4, s->tri_sorted, n, rays, hits, mask, nullptr, ctx->d_counter, ctx->d_error);
+    const SphereView sv = rt_sphere_view(ctx, s, custom_mode);
+    auto launch = [&](auto kern, uint32_t* st_ptr) {
+        int blocks_per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, TRACE_THREADS, 0);
+        if (blocks_per_sm < 1) blocks_per_sm = 1;
+        int64_t want = (n + TRACE_THREADS - 1) / TRACE_THREADS;
+        int64_t grid = (int64_t)ctx->num_sms * blocks_per_sm;
+        if (grid > want) grid = want;
+        kern<<<(unsigned)grid, TRACE_THREADS, 0, st>>>(s->nodes, s->bvh4, s->tri_sorted, n, rays, hits, mask, st_ptr,
+                                                       ctx->d_counter, ctx->d_error, sv);
+    };
+    const bool sph = s->n_spheres > 0;
+    if (stats) {
+        if (sph) launch(trace_closest_kernel<true, true>, stats);
+        else launch(trace_closest_kernel<true, false>, stats);
+    } else {
+        if (sph) launch(trace_closest_kernel<false, true>, nullptr);
+        else launch(trace_closest_kernel<false, false>, nullptr);
+    }
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }
 
-int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask) {
+int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask,
+                      int custom_mode) {
     if (n <= 0) return RT_OK;
     if ((n + 64) > 0xFFFFFFFFll) return RT_EINVAL;
     cudaStream_t st = ctx->stream;
     RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), st));
-    int bps = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, trace_any_kernel, TRACE_THREADS, 0);
-    if (bps < 1) bps = 1;
-    int64_t want = (n + TRACE_THREADS - 1) / TRACE_THREADS;
-    int64_t grid = (int64_t)ctx->num_sms * bps;
-    if (grid > want) grid = want;
-    trace_any_kernel<<<(unsigned)grid, TRACE_THREADS, 0, st>>>(s->nodes, s->bvh4, s->tri_sorted, n, rays, out, mask,
-                                                              ctx->d_counter, ctx->d_error);
+    const SphereView sv = rt_sphere_view(ctx, s, custom_mode);
+    auto launch = [&](auto kern) {
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, TRACE_THREADS, 0);
+        if (bps < 1) bps = 1;
+        int64_t want = (n + TRACE_THREADS - 1) / TRACE_THREADS;
+        int64_t grid = (int64_t)ctx->num_sms * bps;
+        if (grid > want) grid = want;
+        kern<<<(unsigned)grid, TRACE_THREADS, 0, st>>>(s->nodes, s->bvh4, s->tri_sorted, n, rays, out, mask,
+                                                       ctx->d_counter, ctx->d_error, sv);
+    };
+    if (s->n_spheres > 0) launch(trace_any_kernel<true>);
+    else launch(trace_any_kernel<false>);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }
@@ -150,10 +170,10 @@ int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, c
 }
 
 int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
-                       int64_t* prim, double* u, double* v, double* nrm) {
+                       int64_t* prim, double* u, double* v, double* nrm, const float* rays) {
     int grid = ctx->num_sms * 8;
     expand_hits_f64<<<grid, 256, 0, ctx->stream>>>(n, hits, s->tri_attr, s->tri_inst, s->tri_prim, t, inst, prim,
-                                                    u, v, nrm);
+                                                    u, v, nrm, rays, rt_sphere_view(ctx, s, 0));
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }

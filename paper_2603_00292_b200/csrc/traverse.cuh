@@ -14,6 +14,7 @@
 
 struct RayPre {
     float ox, oy, oz, tmin;
+    float dx, dy, dz;          // only the sphere test reads these (dead code for triangle walks)
     float ix, iy, iz;          // safe 1/d
     // watertight shear: A' = M (v - o); rows of M
     float m00, m01, m02, m10, m11, m12, m20, m21, m22;
@@ -27,6 +28,7 @@ __device__ __forceinline__ float safe_rcp(float d) {
 __device__ __forceinline__ void ray_setup(RayPre& R, float ox, float oy, float oz, float dx, float dy, float dz,
                                           float tmin) {
     R.ox = ox; R.oy = oy; R.oz = oz; R.tmin = tmin;
+    R.dx = dx; R.dy = dy; R.dz = dz;
     R.ix = safe_rcp(dx); R.iy = safe_rcp(dy); R.iz = safe_rcp(dz);
     // kz = argmax |d|, kx = (kz+1)%3, ky = (kx+1)%3; swap kx,ky if d[kz] < 0
     float ax = fabsf(dx), ay = fabsf(dy), az = fabsf(dz);
@@ -116,6 +118,125 @@ __device__ __forceinline__ bool tri_test(const RayPre& R, const float4 a, const 
     return true;
 }
 
+// ---- custom primitives: spheres (accel.py:366-423 sphere_intersector; geometry.py:334-363) ----
+// A sphere is its own instance (scene.py:101-112) whose single primitive sits in the
+// flat primitive list after every triangle: flat ids >= base are spheres, and the
+// leaf record holds the instance's world AABB.  rows: 16 doubles per sphere =
+// the instance inverse 3x4 (row-major), local center xyz, radius.  The test runs
+// in float64 exactly as the reference: ray to local space (accel.py:804-809, the
+// direction keeps its length so t is the world t), stable quadratic solve.
+// mode 1 = no intersector registered for (sphere, ray type): reaching a sphere
+// leaf raises the reference's RegistryError (accel.py:800-803) via *err.
+struct SphereView {
+    const double* rows;
+    int base;          // first sphere flat id (== n: no spheres)
+    int mode;          // 0 intersect, 1 error on reach
+    int* err;
+};
+
+__device__ __forceinline__ void sphere_local(const double* m, double ox, double oy, double oz, double dx, double dy,
+                                             double dz, double lo[3], double ld[3]) {
+    lo[0] = m[0] * ox + m[1] * oy + m[2] * oz + m[3];
+    lo[1] = m[4] * ox + m[5] * oy + m[6] * oz + m[7];
+    lo[2] = m[8] * ox + m[9] * oy + m[10] * oz + m[11];
+    ld[0] = m[0] * dx + m[1] * dy + m[2] * dz;
+    ld[1] = m[4] * dx + m[5] * dy + m[6] * dz;
+    ld[2] = m[8] * dx + m[9] * dy + m[10] * dz;
+}
+
+// geometry.py:334-363 _sphere_hit in float64 (no FMA contraction: explicit _rn ops)
+static __device__ __noinline__ double sphere_hit_f64(const double* __restrict__ row, float fox, float foy, float foz,
+                                                     float fdx, float fdy, float fdz, double t_min, double t_max) {
+    double m[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) m[k] = __ldg(row + k);
+    double o[3], d[3];
+    const double ox = fox, oy = foy, oz = foz, dx = fdx, dy = fdy, dz = fdz;
+    o[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[0], ox), __dmul_rn(m[1], oy)), __dmul_rn(m[2], oz)), m[3]);
+    o[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[4], ox), __dmul_rn(m[5], oy)), __dmul_rn(m[6], oz)), m[7]);
+    o[2] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[8], ox), __dmul_rn(m[9], oy)), __dmul_rn(m[10], oz)), m[11]);
+    d[0] = __dadd_rn(__dadd_rn(__dmul_rn(m[0], dx), __dmul_rn(m[1], dy)), __dmul_rn(m[2], dz));
+    d[1] = __dadd_rn(__dadd_rn(__dmul_rn(m[4], dx), __dmul_rn(m[5], dy)), __dmul_rn(m[6], dz));
+    d[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[8], dx), __dmul_rn(m[9], dy)), __dmul_rn(m[10], dz));
+    const double cx = __ldg(row + 12), cy = __ldg(row + 13), cz = __ldg(row + 14), r = __ldg(row + 15);
+    const double lx = __dsub_rn(o[0], cx), ly = __dsub_rn(o[1], cy), lz = __dsub_rn(o[2], cz);
+    const double a = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
+    const double b = __dmul_rn(2.0, __dadd_rn(__dadd_rn(__dmul_rn(lx, d[0]), __dmul_rn(ly, d[1])), __dmul_rn(lz, d[2])));
+    const double c = __dsub_rn(__dadd_rn(__dadd_rn(__dmul_rn(lx, lx), __dmul_rn(ly, ly)), __dmul_rn(lz, lz)),
+                               __dmul_rn(r, r));
+    const double disc = __dsub_rn(__dmul_rn(b, b), __dmul_rn(__dmul_rn(4.0, a), c));
+    if (disc < 0.0) return -1.0;
+    const double sq = sqrt(disc);
+    const double q = __dmul_rn(-0.5, __dadd_rn(b, copysign(sq, b)));
+    double t0, t1;
+    if (q == 0.0) { t0 = 0.0; t1 = 0.0; }
+    else { t0 = __ddiv_rn(q, a); t1 = __ddiv_rn(c, q); }
+    if (t0 > t1) { const double tt = t0; t0 = t1; t1 = tt; }
+    double t = t0;
+    if (t < t_min || t > t_max) {
+        t = t1;
+        if (t < t_min || t > t_max) return -1.0;
+    }
+    return t;
+}
+
+// world normal of a sphere hit: local (p - c) / r through the inverse transpose,
+// renormalised (geometry.py:360-363, accel.py:843-847), float64
+static __device__ __noinline__ float3 sphere_normal(const double* __restrict__ row, float fox, float foy, float foz,
+                                                    float fdx, float fdy, float fdz, float t) {
+    double m[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) m[k] = __ldg(row + k);
+    double o[3], d[3];
+    sphere_local(m, fox, foy, foz, fdx, fdy, fdz, o, d);
+    const double cx = __ldg(row + 12), cy = __ldg(row + 13), cz = __ldg(row + 14), r = __ldg(row + 15);
+    const double px = o[0] + d[0] * (double)t, py = o[1] + d[1] * (double)t, pz = o[2] + d[2] * (double)t;
+    const double lnx = (px - cx) / r, lny = (py - cy) / r, lnz = (pz - cz) / r;
+    const double wx = m[0] * lnx + m[4] * lny + m[8] * lnz;
+    const double wy = m[1] * lnx + m[5] * lny + m[9] * lnz;
+    const double wz = m[2] * lnx + m[6] * lny + m[10] * lnz;
+    const double il = 1.0 / sqrt(wx * wx + wy * wy + wz * wz);
+    return make_float3((float)(wx * il), (float)(wy * il), (float)(wz * il));
+}
+
+inline SphereView rt_sphere_view(rt_ctx* ctx, rt_scene* s, int mode) {
+    SphereView v;
+    v.rows = s->spheres;
+    v.base = (int)(s->n - s->n_spheres);
+    v.mode = mode;
+    v.err = ctx->d_error;
+    return v;
+}
+
+// closest-hit update for a sphere leaf (u = v = 0 for custom primitives, accel.py:621-623)
+static __device__ __noinline__ void sphere_closest(const RayPre& R, const SphereView& sv, int id, float& best_t,
+                                                   int& best_id, float& bu, float& bv) {
+    if (sv.mode) { atomicExch(sv.err, RT_EUNSUPPORTED); return; }
+    const double t = sphere_hit_f64(sv.rows + 16 * (int64_t)(id - sv.base), R.ox, R.oy, R.oz, R.dx, R.dy, R.dz,
+                                    (double)R.tmin, (double)best_t);
+    if (t < 0.0) return;
+    const float tf = (float)t;
+    if (tf > best_t || (tf == best_t && id >= best_id)) return;
+    best_t = tf; best_id = id; bu = 0.0f; bv = 0.0f;
+}
+
+static __device__ __noinline__ bool sphere_any(const RayPre& R, const SphereView& sv, int id, float tmax) {
+    if (sv.mode) { atomicExch(sv.err, RT_EUNSUPPORTED); return false; }
+    return sphere_hit_f64(sv.rows + 16 * (int64_t)(id - sv.base), R.ox, R.oy, R.oz, R.dx, R.dy, R.dz,
+                          (double)R.tmin, (double)tmax) >= 0.0;
+}
+
+// shading normal of hit `id` (per-triangle reference normal, or the sphere's at t)
+template <bool SPH>
+__device__ __forceinline__ void hit_normal(const SphereView& sv, int id, const float4 attr, float ox, float oy, float oz,
+                                           float dx, float dy, float dz, float t, float& nx, float& ny, float& nz) {
+    nx = attr.x; ny = attr.y; nz = attr.z;
+    if (SPH && id >= sv.base) {
+        const float3 w = sphere_normal(sv.rows + 16 * (int64_t)(id - sv.base), ox, oy, oz, dx, dy, dz, t);
+        nx = w.x; ny = w.y; nz = w.z;
+    }
+}
+
 struct HitRec {
     float t;
     int id;
@@ -134,10 +255,11 @@ __device__ __forceinline__ void cswap(float& ta, int& ca, float& tb, int& cb) {
 // ray makes about half the dependent node fetches of the binary walk.  Same
 // triangle test, tie rule and conservative slab test as trace_ray.  The stack
 // holds at most 3 * ceil(height / 2) entries (checked by the caller).
-template <bool STATS>
+template <bool STATS, bool SPH>
 __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, int root,
                                              const float4* __restrict__ tris, const RayPre& R, float tmax,
-                                             uint32_t ray_mask, int2* stack, uint32_t& n_tests, uint32_t& n_visits) {
+                                             uint32_t ray_mask, int2* stack, uint32_t& n_tests, uint32_t& n_visits,
+                                             const SphereView& sv) {
     HitRec h;
     h.t = tmax; h.id = -1; h.u = 0.f; h.v = 0.f;
     // stack entries carry the child's entry distance: a popped entry that lies
@@ -175,7 +297,10 @@ __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, in
             const float4* tp = tris + 3 * (~node);
             const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
             if (STATS) ++n_tests;
-            if (__float_as_uint(b.w) & ray_mask) tri_test(R, a, b, c, h.t, h.id, h.u, h.v);
+            if (__float_as_uint(b.w) & ray_mask) {
+                if (!SPH || __float_as_int(a.w) < sv.base) tri_test(R, a, b, c, h.t, h.id, h.u, h.v);
+                else sphere_closest(R, sv, __float_as_int(a.w), h.t, h.id, h.u, h.v);
+            }
         }
         // pop, dropping entries entered beyond the current closest hit (the box
         // test is inclusive and widened, so ties at t are kept)
@@ -204,8 +329,10 @@ __device__ __forceinline__ bool tri_any(const RayPre& R, const float4 a, const f
 
 // Any-hit (accel.py:656-699, 852-895): the first accepted intersection in
 // [tmin, tmax] ends the walk; children are visited in slot order (no sort).
+template <bool SPH>
 __device__ __forceinline__ bool trace_any4(const float4* __restrict__ bvh4, int root, const float4* __restrict__ tris,
-                                           const RayPre& R, float tmax, uint32_t ray_mask, int* stack) {
+                                           const RayPre& R, float tmax, uint32_t ray_mask, int* stack,
+                                           const SphereView& sv) {
     int sp = 0;
     stack[0] = RT_SENTINEL;
     int node = root;
@@ -225,7 +352,11 @@ __device__ __forceinline__ bool trace_any4(const float4* __restrict__ bvh4, int 
         } else {
             const float4* tp = tris + 3 * (~node);
             const float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
-            if ((__float_as_uint(b.w) & ray_mask) && tri_any(R, a, b, c, tmax)) return true;
+            if (__float_as_uint(b.w) & ray_mask) {
+                if ((!SPH || __float_as_int(a.w) < sv.base) ? tri_any(R, a, b, c, tmax)
+                                                            : sphere_any(R, sv, __float_as_int(a.w), tmax))
+                    return true;
+            }
         }
         node = stack[sp--];
     }

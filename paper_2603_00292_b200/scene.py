@@ -19,7 +19,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from ._native import BuildError, RegistryError, check, lib, ptr
+from ._native import BuildError, check, lib, ptr
+from .accel import IntersectorRegistry, SPHERE_GEOM_TYPE, sphere_data, sphere_intersector
 from .camera import Camera
 from .frames import frame_to_matrix, invert_affine
 
@@ -47,7 +48,7 @@ class GpuTlas:
     """Device-resident flattened scene + LBVH (replaces Tlas/TlasBundle, accel.py:439-549)."""
 
     def __init__(self, ctx, tris, normals, tri_inst, tri_prim, tri_mask, tri_material, mat_color,
-                 mat_emissive, bits=30, root_lo=None, root_hi=None, instances=None, inverses=None):
+                 mat_emissive, bits=30, root_lo=None, root_hi=None, instances=None, inverses=None, spheres=None):
         self.ctx = ctx
         self.n = int(tris.shape[0])
         self.bits = bits
@@ -68,7 +69,16 @@ class GpuTlas:
                                     ptr(me), mc.shape[0], ctypes.byref(h)))
         self.handle = h
         self.build_ms = None
+        # custom primitives: the last rows of `tris` are sphere instance boxes
+        self.sphere_rows = np.zeros((0, 16)) if spheres is None else np.ascontiguousarray(spheres, np.float64)
+        self.n_spheres = int(self.sphere_rows.shape[0])
+        if self.n_spheres:
+            check(lib().rt_scene_set_spheres(ctx.handle, h, self.n_spheres, ptr(self.sphere_rows)))
         self.build(bits)
+
+    def custom_geom_types(self):
+        """accel.py Tlas.custom_geom_types: geometry types of the custom BLASes present."""
+        return [SPHERE_GEOM_TYPE] if self.n_spheres else []
 
     def build(self, bits=None, timed=False):
         """(Re)build the LBVH from the resident triangles; returns device ms if timed."""
@@ -132,6 +142,7 @@ class Scene:
 
     camera: Camera
     tlas: GpuTlas
+    registry: IntersectorRegistry
     mat_color: np.ndarray
     mat_emissive: np.ndarray
     inst_material: np.ndarray
@@ -196,14 +207,11 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0) -> Scene:
     """Flatten + upload + LBVH build (scene.py:79-141 semantics, GPU backend)."""
     if quality not in QUALITIES:
         raise ValueError(f"unknown build quality {quality!r}, expected one of {tuple(QUALITIES)}")
-    if desc.spheres:
-        raise RegistryError("custom primitives (spheres) have no GPU intersector yet; "
-                            "the GPU path has no CPU fallback")
     mat_names = list(desc.materials)
     mat_index = {n: i for i, n in enumerate(mat_names)}
     mat_color = np.array([desc.materials[n].color for n in mat_names]).reshape(-1, 3)
     mat_emissive = np.array([desc.materials[n].emissive for n in mat_names]).reshape(-1, 3)
-    if not desc.instances:
+    if not desc.instances and not desc.spheres:
         raise BuildError("a scene needs at least one instance")
 
     # per-mesh validation and local data (Blas.from_mesh, accel.py:223-236)
@@ -253,19 +261,60 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0) -> Scene:
         mi = mat_index[decl.material]
         inst_material.append(mi)
         t_mat.append(np.full(nt, mi, np.int32))
+    # sphere instances after the mesh instances (scene.py:101-112): one custom
+    # primitive each, flat ids after every triangle; its leaf box is the world AABB
+    # of the transformed local box (accel.py:459-469), rounded outward to fp32
+    sph_rows = []
+    if desc.spheres:
+        rows = np.array([[*sph.center, sph.radius] for sph in desc.spheres], dtype=np.float64)
+        sphere_data(rows)                               # radius > 0 (accel.py:403-408)
+        for k, sph in enumerate(desc.spheres):
+            m = frame_to_matrix(sph.frame)
+            try:
+                inv = invert_affine(m)
+            except ValueError as exc:
+                raise BuildError(f"sphere {k} frame is not invertible") from exc
+            c, r = rows[k, :3], rows[k, 3]
+            blo, bhi = c - r, c + r
+            corners = np.array([[(blo, bhi)[s & 1][0], (blo, bhi)[(s >> 1) & 1][1], (blo, bhi)[(s >> 2) & 1][2]]
+                                for s in range(8)])
+            pts = corners @ m[:, :3].T + m[:, 3]
+            lo, hi = pts.min(axis=0), pts.max(axis=0)
+            wlo.append(lo)
+            whi.append(hi)
+            lo32 = lo.astype(np.float32)
+            hi32 = hi.astype(np.float32)
+            lo32 = np.where(lo32.astype(np.float64) > lo, np.nextafter(lo32, np.float32(-np.inf)), lo32)
+            hi32 = np.where(hi32.astype(np.float64) < hi, np.nextafter(hi32, np.float32(np.inf)), hi32)
+            tris.append(np.concatenate([lo32, hi32, lo32]).reshape(1, 9).astype(np.float32))
+            normals.append(np.zeros((1, 3), np.float32))
+            inst_idx = len(desc.instances) + k
+            t_inst.append(np.array([inst_idx], np.int32))
+            t_prim.append(np.zeros(1, np.int32))
+            t_mask.append(np.array([sph.mask], np.uint32))
+            mi = mat_index[sph.material]
+            inst_material.append(mi)
+            t_mat.append(np.array([mi], np.int32))
+            inverses.append(inv)
+            sph_rows.append(np.concatenate([inv.reshape(12), c, [r]]))
     root_lo = np.min(np.array(wlo), axis=0)
     root_hi = np.max(np.array(whi), axis=0)
     ctx = _native.Context.get(device)
     tlas = GpuTlas(ctx, np.concatenate(tris), np.concatenate(normals), np.concatenate(t_inst),
                    np.concatenate(t_prim), np.concatenate(t_mask), np.concatenate(t_mat), mat_color, mat_emissive,
-                   bits=QUALITIES[quality], root_lo=root_lo, root_hi=root_hi, instances=len(desc.instances),
-                   inverses=np.array(inverses))
+                   bits=QUALITIES[quality], root_lo=root_lo, root_hi=root_hi,
+                   instances=len(desc.instances) + len(desc.spheres), inverses=np.array(inverses),
+                   spheres=np.array(sph_rows) if sph_rows else None)
+    registry = IntersectorRegistry()
+    if desc.spheres:
+        registry.register(SPHERE_GEOM_TYPE, 0, sphere_intersector,
+                          np.array([[*sph.center, sph.radius] for sph in desc.spheres]))
     lights = _light_rows(desc, mat_index, inst_list)
     if len(lights):
         rows = np.ascontiguousarray(np.concatenate([lights.v0, lights.v1, lights.v2, lights.normal, lights.emissive,
                                                     lights.area[:, None]], axis=1), np.float32)
         check(lib().rt_scene_set_lights(ctx.handle, tlas.handle, rows.shape[0], ptr(rows)))
-    return Scene(camera=desc.camera, tlas=tlas, mat_color=mat_color, mat_emissive=mat_emissive,
+    return Scene(camera=desc.camera, tlas=tlas, registry=registry, mat_color=mat_color, mat_emissive=mat_emissive,
                  inst_material=np.array(inst_material, np.int64), lights=lights,
                  sky=np.ascontiguousarray(desc.sky, np.float64), background=np.ascontiguousarray(desc.background,
                                                                                                  np.float64),

@@ -14,7 +14,7 @@ import numpy as np
 
 from .camera import Camera
 from .frames import SrtFrame
-from .scene_io import InstanceDecl, Material, SceneDescription, TriangleMesh
+from .scene_io import InstanceDecl, Material, SceneDescription, SphereDecl, TriangleMesh
 
 
 def _quads(verts, quads):
@@ -83,6 +83,33 @@ def furnace_description() -> SceneDescription:
     return SceneDescription(cam, {"ground": quad}, {"ground": "quad.obj"}, {"gray": Material([0.5] * 3)},
                             [InstanceDecl("ground", "gray", SrtFrame(scale=np.array([100.0, 1.0, 100.0])))],
                             [], np.ones(3), np.zeros(3))
+
+
+def spheres_description() -> SceneDescription:
+    """spheres.scn: three custom-primitive spheres on a ground quad under an emissive
+    panel (spheres.scn:1-17; quad.obj = unit quad in y = 0, face 1 4 3 2)."""
+    quad = _quads([(-0.5, 0, -0.5), (0.5, 0, -0.5), (0.5, 0, 0.5), (-0.5, 0, 0.5)], [(1, 4, 3, 2)])
+    mats = {
+        "floor": Material([0.6, 0.6, 0.6]),
+        "orange": Material([0.85, 0.45, 0.15]),
+        "blue": Material([0.2, 0.35, 0.8]),
+        "gray": Material([0.75, 0.75, 0.75]),
+        "lamp": Material([0, 0, 0], [10, 10, 9]),
+    }
+    inst = [
+        InstanceDecl("ground", "floor", SrtFrame(scale=np.array([40.0, 1.0, 40.0]))),
+        InstanceDecl("panel", "lamp", SrtFrame(np.array([3.0, 1.0, 3.0]), np.array([1.0, 0.0, 0.0]),
+                                               math.radians(180.0), np.array([0.0, 4.0, 0.0]))),
+    ]
+    sph = [
+        SphereDecl("orange", np.zeros(3), 0.6, SrtFrame(translation=np.array([-1.3, 0.6, 0.0]))),
+        SphereDecl("blue", np.zeros(3), 0.6, SrtFrame(translation=np.array([1.3, 0.6, 0.0]))),
+        SphereDecl("gray", np.zeros(3), 0.9, SrtFrame(translation=np.array([0.0, 0.9, -1.6]))),
+    ]
+    cam = Camera(np.array([0.0, 1.2, 4.0]), np.array([0.45, 0.0, 0.0]), np.array([0.0, 0.45, 0.0]))
+    sky = np.array([0.05, 0.07, 0.1])
+    return SceneDescription(cam, {"ground": quad, "panel": quad}, {"ground": "quad.obj", "panel": "quad.obj"}, mats,
+                            inst, sph, sky, sky.copy())
 
 
 def uv_sphere(stacks=500, slices=1000):

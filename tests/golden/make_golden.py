@@ -2,7 +2,8 @@
 
 Run in the build container (where /root/reference exists):
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py            # all fixtures
+    python tests/golden/make_golden.py spheres    # only spheres.npz
 
 It imports the reference ``pathtrace`` package from /root/reference/pkg/src
 (numba CPU library) and records its outputs on small, seeded inputs.  The
@@ -59,8 +60,61 @@ def primary_rays(pt, scene, W, H, seed=0, s=0, jitter=True):
     return O, D
 
 
+def make_spheres(pt):
+    """7. spheres.scn (custom-primitive sphere instances, scene.py:101-112): hits, any-hit,
+    the registry error and render_frame accumulations, all from the reference."""
+    from pathtrace.integrators import IntegratorConfig
+    desc = pt.load_scene("/root/reference/pkg/scenes/spheres.scn")
+    sc = ref_scene(pt, desc)
+    out = {}
+    O, D = primary_rays(pt, sc, 48, 36)
+    r = pt.closest_hit_batch(sc.tlas, O, D, registry=sc.registry, with_stats=True)
+    for k, val in zip(("t", "inst", "prim", "u", "v", "n", "stats"), r):
+        out["p_" + k] = val
+    out["O"], out["D"] = O, D
+    rng = np.random.default_rng(7)
+    m = 4000
+    # rays from points around the spheres toward random directions (many start inside
+    # or graze a sphere), plus rays aimed at sphere centers from outside
+    RO = rng.uniform((-2.5, 0.01, -2.8), (2.5, 2.2, 1.2), (m, 3))
+    RD = rng.normal(size=(m, 3))
+    ctr = np.array([[-1.3, 0.6, 0.0], [1.3, 0.6, 0.0], [0.0, 0.9, -1.6]])
+    aim = ctr[np.arange(m) % 3] + rng.normal(scale=0.5, size=(m, 3))
+    RD[m // 2:] = aim[m // 2:] - RO[m // 2:]
+    RD /= np.linalg.norm(RD, axis=1, keepdims=True)
+    RD[m // 2:] *= rng.uniform(0.5, 2.0, (m - m // 2, 1))     # unnormalised directions too
+    tmin = np.where(np.arange(m) % 7 == 0, 0.05, 0.0)
+    tmax = np.where(np.arange(m) % 5 == 0, 1.5, 1e30)
+    r = pt.closest_hit_batch(sc.tlas, RO, RD, tmin, tmax, registry=sc.registry, with_stats=True)
+    for k, val in zip(("t", "inst", "prim", "u", "v", "n", "stats"), r):
+        out["r_" + k] = val
+    out["RO"], out["RD"], out["tmin"], out["tmax"] = RO, RD, tmin, tmax
+    out["r_any"] = pt.any_hit_batch(sc.tlas, RO, RD, tmin, tmax, registry=sc.registry)
+    # ray_mask selecting only the mesh instances would need masks; the scene uses
+    # full masks, so the masked case is all misses -- keep the registry=None error
+    try:
+        pt.closest_hit_batch(sc.tlas, O, D)
+        out["noreg_error"] = np.array("")
+    except Exception as exc:                       # RegistryError
+        out["noreg_error"] = np.array(f"{type(exc).__name__}: {exc}")
+    meta = dict(inverses=sc.tlas.inverses, diag=np.array(sc.diagonal()), inst_material=sc.inst_material,
+                root_box=sc.tlas.nodes["bounds"][0])
+    out.update({"meta_" + k: v for k, v in meta.items()})
+    for name, integ, w, h, spp, md in (("eye", "eye", 32, 24, 2, 8), ("pt", "pt", 24, 18, 4, 5),
+                                       ("ao", "ao", 16, 12, 2, 8), ("nee", "pt-nee", 16, 12, 4, 5)):
+        cfg = IntegratorConfig(max_depth=md, ao_ray_count=8)
+        acc, st = pt.render_frame(sc, w, h, spp, integ, seed=0, workers=2, cfg=cfg, return_stats=True)
+        out["render_" + name] = acc.data
+        out["render_" + name + "_rays"] = np.array(st["rays"])
+        out["render_" + name + "_args"] = np.array([w, h, spp, md])
+    np.savez_compressed(os.path.join(HERE, "spheres.npz"), **out)
+
+
 def main():
     pt = import_reference()
+    if sys.argv[1:] == ["spheres"]:
+        make_spheres(pt)
+        return
     from pathtrace.accel import _build_bvh
     from pathtrace.integrators import IntegratorConfig
     sys.path.insert(0, ROOT)
@@ -169,6 +223,7 @@ def main():
     o[1], d[1] = (0.25, 0.25, -1), (1, 0, 0)
     res = intersect_ray_triangle_batch(o, d, tmn, tmx, v0, v1, v2)
     np.savez_compressed(os.path.join(HERE, "tri_hit.npz"), o=o, d=d, v0=v0, v1=v1, v2=v2, out=res)
+    make_spheres(pt)
     print("golden fixtures written to", HERE)
 
 

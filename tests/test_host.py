@@ -32,6 +32,42 @@ def test_builtin_cornell_matches_reference_file(reference):
     assert np.array_equal(ref.camera.forward, mine.camera.forward)
 
 
+def test_builtin_spheres_matches_reference_file(reference):
+    ref = reference.load_scene("/root/reference/pkg/scenes/spheres.scn")
+    mine = scenes.spheres_description()
+    for k in ref.meshes:
+        assert np.array_equal(ref.meshes[k].vertices, mine.meshes[k].vertices), k
+        assert np.array_equal(ref.meshes[k].faces, mine.meshes[k].faces), k
+    for a, b in zip(ref.instances, mine.instances):
+        assert (a.mesh, a.material, a.mask) == (b.mesh, b.material, b.mask)
+        assert np.array_equal(frame_to_matrix(b.frame), reference.accel.frame_to_matrix(a.frame))
+    assert len(ref.spheres) == len(mine.spheres) == 3
+    for a, b in zip(ref.spheres, mine.spheres):
+        assert (a.material, a.radius, a.mask) == (b.material, b.radius, b.mask)
+        assert np.array_equal(a.center, b.center)
+        assert np.array_equal(frame_to_matrix(b.frame), reference.accel.frame_to_matrix(a.frame))
+    for k in ref.materials:
+        assert np.array_equal(ref.materials[k].color, mine.materials[k].color)
+        assert np.array_equal(ref.materials[k].emissive, mine.materials[k].emissive)
+    assert np.array_equal(ref.sky, mine.sky) and np.array_equal(ref.background, mine.background)
+
+
+def test_sphere_registry_api():
+    from paper_2603_00292_b200 import accel
+    data = accel.sphere_data([[0, 0, 0, 1.0]])
+    reg = accel.make_sphere_registry(data, ray_types=(0, 1))
+    assert reg.entry(accel.SPHERE_GEOM_TYPE, 1)[0] is accel.sphere_intersector
+    table, slots = reg.resolve([0], 0)
+    assert len(table) == 1 and slots.tolist() == [0]
+    # o = (0,0,-3), d = (0,0,1), unit sphere -> t = 2, normal (0,0,-1); o = (0,2,-3) misses
+    t, nx, ny, nz = accel.sphere_intersector(data, 0, 0.0, 0.0, -3.0, 0.0, 0.0, 1.0, 0.0, 1e30)
+    assert t == 2.0 and (nx, ny, nz) == (0.0, 0.0, -1.0)
+    assert accel.sphere_intersector(data, 0, 0.0, 2.0, -3.0, 0.0, 0.0, 1.0, 0.0, 1e30)[0] < 0.0
+    with pytest.raises(ValueError):
+        accel.sphere_data([[0, 0, 0, 0.0]])
+    assert accel.sphere_aabbs([[1, 2, 3, 0.5]]).tolist() == [[0.5, 1.5, 2.5, 1.5, 2.5, 3.5]]
+
+
 def test_parse_scene_text_matches_reference(reference, tmp_path):
     text = open("/root/reference/pkg/scenes/cornell.scn").read()
     mine = parse_scene(text, "/root/reference/pkg/scenes")

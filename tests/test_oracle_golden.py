@@ -125,3 +125,42 @@ def test_lbvh_through_reference_traversal(oracle_mod, reference):
         b = pt.closest_hit_batch(tl_ref, O, D)
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
+
+
+# ---- spheres.scn: custom-primitive sphere instances (accel.py:366-423, scene.py:101-112) ----
+
+@pytest.fixture(scope="module")
+def spheres_oracle(oracle_mod):
+    from paper_2603_00292_b200 import scenes
+    return oracle_mod.scene_from_description(scenes.spheres_description())
+
+
+def test_spheres_scene_assembly(spheres_oracle):
+    g = golden("spheres")
+    assert np.array_equal(spheres_oracle.inverses, g["meta_inverses"])
+    assert np.array_equal(spheres_oracle.inst_material, g["meta_inst_material"])
+    assert spheres_oracle.diagonal() == float(g["meta_diag"])
+    assert np.array_equal(spheres_oracle.tlas_nodes["bounds"][0], g["meta_root_box"])
+
+
+def test_spheres_closest_any_bit_exact(spheres_oracle):
+    g = golden("spheres")
+    r = spheres_oracle.closest_hit_batch(g["O"], g["D"], with_stats=True)
+    for a, k in zip(r, ("t", "inst", "prim", "u", "v", "n", "stats")):
+        assert np.array_equal(a, g["p_" + k]), k
+    r = spheres_oracle.closest_hit_batch(g["RO"], g["RD"], g["tmin"], g["tmax"], with_stats=True, workers=3)
+    for a, k in zip(r, ("t", "inst", "prim", "u", "v", "n", "stats")):
+        assert np.array_equal(a, g["r_" + k]), k
+    assert np.array_equal(spheres_oracle.any_hit_batch(g["RO"], g["RD"], g["tmin"], g["tmax"]), g["r_any"])
+    # the fixture exercises the sphere instances (2, 3, 4) and the ground/panel meshes
+    assert set(np.unique(g["r_inst"])) >= {-1, 0, 1, 2, 3, 4}
+
+
+@pytest.mark.parametrize("name", ["eye", "pt", "ao", "nee"])
+def test_spheres_render_frame_bit_exact(spheres_oracle, name):
+    g = golden("spheres")
+    w, h, spp, md = (int(x) for x in g["render_" + name + "_args"])
+    integ = {"eye": "eye", "pt": "pt", "ao": "ao", "nee": "pt-nee"}[name]
+    acc, rays = spheres_oracle.render_frame(w, h, spp, integ, seed=0, workers=3, max_depth=md, ao_ray_count=8)
+    assert rays == int(g["render_" + name + "_rays"])
+    assert np.array_equal(acc, g["render_" + name])
