@@ -153,6 +153,10 @@ int rt_scene_set_lights(rt_ctx* ctx, rt_scene* scene, int32_t n_lights, const fl
  * place (sample order per pixel).  rays_out (nullable): closest-hit queries issued. */
 int rt_render(rt_ctx* ctx, rt_scene* scene, const rt_render_params* p, float* accum,
               uint64_t* rays_out);
+/* device resolve (scene_io.py:349-355): accum (npix, 4) f32 running sums -> rgb (npix, 3)
+ * uint8, mean clamped to [0, 1], ^(1/2.2) when gamma != 0, round-half-even of 255 v;
+ * both device buffers.  RT_EINVAL if a pixel has zero samples (AccumBuffer.mean). */
+int rt_resolve(rt_ctx* ctx, const float* accum, int64_t npix, int32_t gamma, uint8_t* rgb);
 /* primary rays of sample s for every pixel of the frame (parity tests): (W*H, 8) like rt_trace_closest */
 int rt_raygen(rt_ctx* ctx, const rt_render_params* p, int32_t sample, float* rays);
 

@@ -88,6 +88,7 @@ def lib():
             "rt_scene_set_lights": [vp, vp, i32, vp],
             "rt_scene_set_spheres": [vp, vp, i32, vp],
             "rt_raygen": [vp, ctypes.POINTER(RenderParams), i32, vp],
+            "rt_resolve": [vp, vp, i64, i32, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)

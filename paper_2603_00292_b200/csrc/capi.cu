@@ -503,6 +503,23 @@ int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, u
     return RT_OK;
 }
 
+int rt_resolve(rt_ctx* c, const float* accum, int64_t npix, int32_t gamma, uint8_t* rgb) {
+    RT_CHECK_ARG(c && accum && rgb && npix >= 0, "NULL argument");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    int rc = rt_resolve_impl(c, accum, npix, gamma, rgb);
+    if (rc) return rc;
+    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    int e = 0;
+    RT_CUDA_TRY(cudaMemcpy(&e, c->d_error, sizeof e, cudaMemcpyDeviceToHost));
+    if (e == RT_EINVAL) {
+        int z = 0;
+        cudaMemcpy(c->d_error, &z, sizeof z, cudaMemcpyHostToDevice);
+        rt_set_error("accumulation buffer has pixels with zero samples");
+        return RT_EINVAL;
+    }
+    return check_device_error(c);
+}
+
 int rt_raygen(rt_ctx* c, const rt_render_params* p, int32_t sample, float* rays) {
     RT_CHECK_ARG(c && p && rays, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));

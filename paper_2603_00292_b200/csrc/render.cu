@@ -457,6 +457,27 @@ __global__ void __launch_bounds__(WF_THREADS) wf_accumulate(const FrameConst F, 
     }
 }
 
+// scene_io.py:349-355 resolve: mean = sum / n, clamp to [0, 1], optional ^(1/2.2),
+// round(255 v) half-to-even (np.round), in float64 from the fp32 running sums
+__global__ void resolve_kernel(const float4* __restrict__ accum, int64_t npix, int gamma, uint8_t* __restrict__ rgb,
+                               int* err) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < npix; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 a = accum[i];
+        if (!(a.w > 0.0f)) {
+            atomicExch(err, RT_EINVAL);
+            continue;
+        }
+        const double n = a.w;
+        const double c[3] = {a.x / n, a.y / n, a.z / n};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double v = c[k] < 0.0 ? 0.0 : (c[k] > 1.0 ? 1.0 : c[k]);
+            if (gamma) v = pow(v, 1.0 / 2.2);
+            rgb[3 * i + k] = (uint8_t)rint(255.0 * v);
+        }
+    }
+}
+
 __global__ void raygen_kernel(const FrameConst F, int s, float4* __restrict__ rays) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F.npix; i += (int64_t)gridDim.x * blockDim.x) {
         PathState P;
@@ -661,6 +682,13 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         RT_CUDA_TRY(cudaMemcpyAsync(rays_out, d_rays, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
         RT_CUDA_TRY(cudaStreamSynchronize(st));
     }
+    return RT_OK;
+}
+
+int rt_resolve_impl(rt_ctx* ctx, const float* accum, int64_t npix, int gamma, uint8_t* rgb) {
+    resolve_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(reinterpret_cast<const float4*>(accum), npix, gamma,
+                                                             rgb, ctx->d_error);
+    RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }
 

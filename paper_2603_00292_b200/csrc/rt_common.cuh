@@ -175,3 +175,4 @@ int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, c
                      const double* tmax, float* rays);
 int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out);
 int rt_raygen_impl(rt_ctx* ctx, const rt_render_params* p, int sample, float* rays);
+int rt_resolve_impl(rt_ctx* ctx, const float* accum, int64_t npix, int gamma, uint8_t* rgb);

@@ -89,3 +89,45 @@ def render_frame_distributed(scene, width, height, spp, integrator="pt", seed=0,
     if rank != 0:
         return None, rays
     return AccumBuffer(width, height, acc.cpu().numpy().astype(np.float64).reshape(height, width, 4)), rays
+
+
+def render_frame_multi(scenes, width, height, spp, integrator="pt", seed=0, cfg=None, jitter=True, kernel="mega",
+                       return_device=False):
+    """One process, several GPUs: ``scenes[g]`` is the replica compiled on device g.
+
+    Sample split (global sample indices, so the random numbers are those of a
+    1-GPU run), one host thread per GPU (the ctypes calls release the GIL),
+    then the partial (H*W, 4) sums are added on GPU 0 (peer copies over
+    NVLink).  Returns (accum on GPU 0, rays) with return_device, else
+    (AccumBuffer, rays)."""
+    import torch
+    from concurrent.futures import ThreadPoolExecutor
+    from .integrators import render_into
+    from .scene_io import AccumBuffer
+    G = len(scenes)
+    if G < 1:
+        raise ValueError("need at least one scene replica")
+    if width < 1 or height < 1 or spp < 1:
+        raise ValueError("width, height, and spp must all be >= 1")
+    accs = [torch.zeros((width * height, 4), dtype=torch.float32, device=torch.device("cuda", sc.tlas.ctx.device))
+            for sc in scenes]
+
+    def job(g):
+        s0, s1 = sample_slice(g, G, spp)
+        if s1 <= s0:
+            return 0
+        with torch.cuda.device(scenes[g].tlas.ctx.device):
+            return render_into(scenes[g], accs[g], width, height, spp, integrator, seed, cfg, jitter, kernel,
+                               samples=(s0, s1))
+
+    if G == 1:
+        rays = job(0)
+    else:
+        with ThreadPoolExecutor(max_workers=G) as pool:
+            rays = sum(pool.map(job, range(G)))
+    acc = accs[0]
+    for g in range(1, G):
+        acc.add_(accs[g].to(acc.device))
+    if return_device:
+        return acc, rays
+    return AccumBuffer(width, height, acc.cpu().numpy().astype(np.float64).reshape(height, width, 4)), rays

@@ -1,11 +1,11 @@
 """render_frame on the GPU (drop-in for integrators.py:426-473 of the reference).
 
-Same signature and validation as the reference plus three GPU knobs:
-``kernel`` ("mega" | "wavefront"), ``samples`` (a [s0, s1) window of GLOBAL
-sample indices, for the sample split across GPUs) and ``accum`` (a CUDA
-(H*W, 4) float32 tensor to accumulate into and keep on the device).  Eye and
-path tracing run on the GPU; "ao" and "pt-nee" need the any-hit kernel, a
-"next" item, and raise ValueError rather than falling back.
+Same signature and validation as the reference plus GPU knobs: ``kernel``
+("mega" | "wavefront"; ao and pt-nee run in the megakernel) and ``samples``
+(a [s0, s1) window of GLOBAL sample indices, for the sample split across
+GPUs).  ``render_into`` accumulates into a caller-owned CUDA (H*W, 4) float32
+tensor and keeps it on the device; ``resolve_device`` turns such a buffer
+into display bytes on the GPU (scene_io.py:349-355).
 """
 
 import warnings
@@ -122,6 +122,17 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
     if return_stats:
         return buf, {"rays": rays}
     return buf
+
+
+def resolve_device(ctx_or_scene, accum, width, height, gamma_encode=True) -> np.ndarray:
+    """scene_io.py:349-355 on the GPU: (H*W, 4) f32 CUDA sums -> (H, W, 3) uint8 host image."""
+    import torch
+    ctx = ctx_or_scene.tlas.ctx if hasattr(ctx_or_scene, "tlas") else ctx_or_scene
+    if accum.shape[0] != width * height:
+        raise ValueError("accumulation buffer does not match the frame size")
+    rgb = torch.empty((height * width * 3,), dtype=torch.uint8, device=accum.device)
+    check(lib().rt_resolve(ctx.handle, ptr(accum), width * height, 1 if gamma_encode else 0, ptr(rgb)))
+    return rgb.cpu().numpy().reshape(height, width, 3)
 
 
 def raygen(scene, width, height, sample=0, seed=0, jitter=True):

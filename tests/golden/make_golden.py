@@ -4,6 +4,7 @@ Run in the build container (where /root/reference exists):
 
     python tests/golden/make_golden.py            # all fixtures
     python tests/golden/make_golden.py spheres    # only spheres.npz
+    python tests/golden/make_golden.py cli        # only cli_ppm.npz (reference CLI PPM bytes)
 
 It imports the reference ``pathtrace`` package from /root/reference/pkg/src
 (numba CPU library) and records its outputs on small, seeded inputs.  The
@@ -110,10 +111,44 @@ def make_spheres(pt):
     np.savez_compressed(os.path.join(HERE, "spheres.npz"), **out)
 
 
+CLI_JOBS = (
+    ("cornell_eye", "cornell", ["--width", "64", "--height", "48", "--spp", "2", "--integrator", "eye"]),
+    ("cornell_pt", "cornell", ["--width", "32", "--height", "24", "--spp", "4", "--integrator", "pt",
+                               "--max-depth", "5"]),
+    ("cornell_ao", "cornell", ["--width", "24", "--height", "16", "--spp", "2", "--integrator", "ao",
+                               "--ao-rays", "4", "--no-gamma"]),
+    ("spheres_eye", "spheres", ["--width", "48", "--height", "36", "--spp", "1", "--integrator", "eye"]),
+    ("spheres_nee", "spheres", ["--width", "24", "--height", "18", "--spp", "2", "--integrator", "pt-nee",
+                                "--max-depth", "4", "--seed", "3"]),
+)
+
+
+def make_cli(pt):
+    """8. the reference CLI (cli.py:45-101) end to end: PPM bytes for scene files written
+    from the package's built-in descriptions (scene_io.write_scene_files)."""
+    from pathtrace.cli import run
+    sys.path.insert(0, ROOT)
+    from paper_2603_00292_b200 import scenes
+    from paper_2603_00292_b200.scene_io import write_scene_files
+    out = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        paths = {"cornell": write_scene_files(scenes.cornell_description(), os.path.join(tmp, "c")),
+                 "spheres": write_scene_files(scenes.spheres_description(), os.path.join(tmp, "s"))}
+        for name, scn, args in CLI_JOBS:
+            ppm = os.path.join(tmp, name + ".ppm")
+            rc = run(["--scene", paths[scn], "--out", ppm] + args)
+            assert rc == 0, (name, rc)
+            out[name] = np.frombuffer(open(ppm, "rb").read(), dtype=np.uint8)
+    np.savez_compressed(os.path.join(HERE, "cli_ppm.npz"), **out)
+
+
 def main():
     pt = import_reference()
     if sys.argv[1:] == ["spheres"]:
         make_spheres(pt)
+        return
+    if sys.argv[1:] == ["cli"]:
+        make_cli(pt)
         return
     from pathtrace.accel import _build_bvh
     from pathtrace.integrators import IntegratorConfig
@@ -224,6 +259,7 @@ def main():
     res = intersect_ray_triangle_batch(o, d, tmn, tmx, v0, v1, v2)
     np.savez_compressed(os.path.join(HERE, "tri_hit.npz"), o=o, d=d, v0=v0, v1=v1, v2=v2, out=res)
     make_spheres(pt)
+    make_cli(pt)
     print("golden fixtures written to", HERE)
 
 
