@@ -42,6 +42,7 @@ extern "C" {
 
 typedef struct rt_ctx rt_ctx;
 typedef struct rt_scene rt_scene;
+typedef struct rt_tlas rt_tlas;
 
 /* Frame parameters: render_frame(scene, width, height, spp, integrator, seed,
  * workers, cfg, jitter) -- integrators.py:426-473.  Samples [s0, s1) are
@@ -159,6 +160,40 @@ int rt_render(rt_ctx* ctx, rt_scene* scene, const rt_render_params* p, float* ac
 int rt_resolve(rt_ctx* ctx, const float* accum, int64_t npix, int32_t gamma, uint8_t* rgb);
 /* primary rays of sample s for every pixel of the frame (parity tests): (W*H, 8) like rt_trace_closest */
 int rt_raygen(rt_ctx* ctx, const rt_render_params* p, int32_t sample, float* rays);
+
+/* ---- two-level structure (replaces Blas / Instance / Tlas, accel.py:211-283, 339-346,
+ *      439-549, and their traversal kernels accel.py:575-699, 762-895) ---------------
+ * A BLAS is an rt_scene over one mesh in LOCAL space (rt_scene_create with the mesh's
+ * local vertices, ids = prim, full masks) plus its float64 local normals; a custom-
+ * primitive BLAS is an rt_scene over the primitives' local AABBs given as (lo, hi, lo)
+ * rows, marked with rt_scene_set_custom (Blas.from_aabbs).  Both need rt_bvh_build. */
+/* (n, 3) float64 local triangle normals in the reference's order (geometry.py:229-237, 274-275) */
+int rt_scene_set_local_normals(rt_ctx* ctx, rt_scene* blas, const double* normals);
+/* custom-primitive BLAS: geometry type and the offset of its first row in the registry data */
+int rt_scene_set_custom(rt_ctx* ctx, rt_scene* blas, int32_t geom_type, int64_t data_offset);
+/* TLAS over n_inst instances: inst_blas[i] = the instance's BLAS, inv12 (n, 12) float64
+ * instance inverses (invert_affine, accel.py:328-336), boxes6 (n, 6) fp32 world AABBs
+ * (lo, hi) of the BLAS root box corners through the instance matrix (accel.py:459-469,
+ * rounded outward), masks (n).  Builds the top-level LBVH.  BLAS handles are borrowed. */
+int rt_tlas_create(rt_ctx* ctx, int32_t n_inst, rt_scene* const* inst_blas, const double* inv12,
+                   const float* boxes6, const uint32_t* masks, rt_tlas** out);
+/* Tlas.refresh_instance_bounds (accel.py:477-497): new inverses / world boxes, rebuilt
+ * top level; also picks up BLASes rebuilt after a refit */
+int rt_tlas_update(rt_ctx* ctx, rt_tlas* tlas, const double* inv12, const float* boxes6);
+/* registry data of one custom geometry type (IntersectorRegistry, accel.py:366-392):
+ * rows (n_rows, 4) float64 = sphere (cx, cy, cz, r); n_rows = 0 unregisters (a ray that
+ * then reaches such a primitive fails with RT_EUNSUPPORTED) */
+int rt_tlas_set_custom_data(rt_ctx* ctx, rt_tlas* tlas, int32_t geom_type, int64_t n_rows, const double* rows4);
+int rt_tlas_info(rt_ctx* ctx, rt_tlas* tlas, float* root6, int32_t* height);
+void rt_tlas_destroy(rt_tlas* tlas);
+/* closest_hit_batch / any_hit_batch over the two-level structure, host float64 rays,
+ * outputs and conventions as rt_closest_hit_host / rt_any_hit_host (inst = instance
+ * index, prim = primitive index in its BLAS) */
+int rt_tlas_closest_host(rt_ctx* ctx, rt_tlas* tlas, int64_t n, const double* origins, const double* dirs,
+                         const double* t_min, const double* t_max, uint32_t ray_mask, double* t, int64_t* inst,
+                         int64_t* prim, double* u, double* v, double* normal, int64_t* stats);
+int rt_tlas_any_host(rt_ctx* ctx, rt_tlas* tlas, int64_t n, const double* origins, const double* dirs,
+                     const double* t_min, const double* t_max, uint32_t ray_mask, uint8_t* hit);
 
 #ifdef __cplusplus
 }

@@ -15,5 +15,6 @@ from .scene import Scene, compile_scene
 from .accel import (CUSTOM, SPHERE_GEOM_TYPE, TRIANGLES, IntersectorRegistry, any_hit_batch, closest_hit_batch,
                     make_sphere_registry, sphere_aabbs, sphere_data, sphere_intersector, trace_any, trace_closest)
 from .integrators import INTEGRATORS, IntegratorConfig, render_frame, render_into
+from .twolevel import Blas, Instance, Tlas, build_tlas, transform_ray_to_local
 
 __version__ = "0.1.0"

@@ -89,6 +89,14 @@ def lib():
             "rt_scene_set_spheres": [vp, vp, i32, vp],
             "rt_raygen": [vp, ctypes.POINTER(RenderParams), i32, vp],
             "rt_resolve": [vp, vp, i64, i32, vp],
+            "rt_scene_set_local_normals": [vp, vp, vp],
+            "rt_scene_set_custom": [vp, vp, i32, i64],
+            "rt_tlas_create": [vp, i32, vp, vp, vp, vp, vp],
+            "rt_tlas_update": [vp, vp, vp, vp],
+            "rt_tlas_set_custom_data": [vp, vp, i32, i64, vp],
+            "rt_tlas_info": [vp, vp, vp, vp],
+            "rt_tlas_closest_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp, vp],
+            "rt_tlas_any_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -98,6 +106,8 @@ def lib():
         L.rt_ctx_destroy.restype = None
         L.rt_scene_destroy.argtypes = [vp]
         L.rt_scene_destroy.restype = None
+        L.rt_tlas_destroy.argtypes = [vp]
+        L.rt_tlas_destroy.restype = None
         _lib = L
         return L
 

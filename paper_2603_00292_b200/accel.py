@@ -160,6 +160,8 @@ def closest_hit_batch(tlas, origins, dirs, t_min=0.0, t_max=DEFAULT_MAX_T, ray_m
                       ray_type: int = 0, registry=None, with_stats: bool = False):
     """Array-of-rays closest hit: (t, inst, prim, u, v, normal[, stats])."""
     tl = _tlas_of(tlas)
+    if getattr(tl, "two_level", False):
+        return tl.closest_hit_batch(origins, dirs, t_min, t_max, ray_mask, ray_type, registry, with_stats)
     flags = _trace_flags(tl, registry, ray_type)
     mask = _check_mask(ray_mask)
     origins = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)
@@ -186,6 +188,8 @@ def any_hit_batch(tlas, origins, dirs, t_min=0.0, t_max=DEFAULT_MAX_T, ray_mask:
                   ray_type: int = 0, registry=None) -> np.ndarray:
     """accel.py:1159-1174: True iff some accepted intersection lies in [t_min, t_max]."""
     tl = _tlas_of(tlas)
+    if getattr(tl, "two_level", False):
+        return tl.any_hit_batch(origins, dirs, t_min, t_max, ray_mask, ray_type, registry)
     flags = _trace_flags(tl, registry, ray_type)
     mask = _check_mask(ray_mask)
     origins = np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)

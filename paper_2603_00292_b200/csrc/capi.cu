@@ -20,15 +20,9 @@ void rt_set_error(const char* fmt, ...) {
 size_t rt_sort_scratch_words(int64_t n);
 void rt_render_release(rt_scene* s);
 
-#define RT_CHECK_ARG(cond, msg)              \
-    do {                                     \
-        if (!(cond)) {                       \
-            rt_set_error("%s", msg);         \
-            return RT_EINVAL;                \
-        }                                    \
-    } while (0)
 
-static int check_device_error(rt_ctx* ctx) {
+
+int rt_check_device_error(rt_ctx* ctx) {
     int e = 0;
     RT_CUDA_TRY(cudaMemcpyAsync(&e, ctx->d_error, sizeof e, cudaMemcpyDeviceToHost, ctx->stream));
     RT_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
@@ -108,7 +102,7 @@ int rt_ctx_sync(rt_ctx* c) {
     RT_CHECK_ARG(c, "ctx is NULL");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-    return check_device_error(c);
+    return rt_check_device_error(c);
 }
 
 int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normals, const int32_t* tri_inst,
@@ -203,7 +197,7 @@ void rt_scene_destroy(rt_scene* s) {
     void* ptrs[] = {s->tris, s->tri_attr, s->tri_inst, s->tri_prim, s->tri_mask, s->mat_color, s->mat_emissive,
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->parent, s->child,
                     s->flags, s->cbounds, s->cb_enc, s->sort_scratch, s->leaf_box, s->emit_items,
-                    s->emit_count, s->lights, s->spheres};
+                    s->emit_count, s->lights, s->spheres, s->lnormal64};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;
@@ -391,7 +385,7 @@ int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, cons
         }
     }
     RT_CUDA_TRY(cudaStreamSynchronize(st));
-    return check_device_error(c);
+    return rt_check_device_error(c);
 }
 
 int rt_trace_any(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, uint8_t* hit, uint32_t ray_mask,
@@ -441,7 +435,7 @@ int rt_any_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const do
         RT_CUDA_TRY(cudaMemcpyAsync(out + b, d_out, m, cudaMemcpyDeviceToHost, st));
     }
     RT_CUDA_TRY(cudaStreamSynchronize(st));
-    return check_device_error(c);
+    return rt_check_device_error(c);
 }
 
 // world-space emissive triangles for next-event estimation (scene.py:58-76 light rows):
@@ -499,7 +493,7 @@ int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, u
     RT_CUDA_TRY(cudaSetDevice(c->device));
     int rc = rt_render_impl(c, s, p, accum, rays_out);
     if (rc) return rc;
-    if (rays_out) return check_device_error(c);
+    if (rays_out) return rt_check_device_error(c);
     return RT_OK;
 }
 
@@ -517,7 +511,7 @@ int rt_resolve(rt_ctx* c, const float* accum, int64_t npix, int32_t gamma, uint8
         rt_set_error("accumulation buffer has pixels with zero samples");
         return RT_EINVAL;
     }
-    return check_device_error(c);
+    return rt_check_device_error(c);
 }
 
 int rt_raygen(rt_ctx* c, const rt_render_params* p, int32_t sample, float* rays) {

@@ -64,6 +64,11 @@ struct rt_scene {
     // custom primitives: the last n_spheres flat primitives are spheres
     double* spheres;                // (n_spheres, 16): inverse 3x4, center, radius
     int n_spheres;
+    // as a bottom-level structure of a two-level rt_tlas (tlas.cu)
+    double* lnormal64;              // (n, 3) float64 local normals (reference order), triangles
+    int custom;                     // 1: prims are AABBs of custom primitives (geom_type, data_offset)
+    int geom_type;
+    int64_t data_offset;
 };
 
 // --------------------------------------------------------------------------
@@ -79,6 +84,17 @@ void rt_set_error(const char* fmt, ...);
             return RT_ECUDA;                                                      \
         }                                                                         \
     } while (0)
+
+#define RT_CHECK_ARG(cond, msg)              \
+    do {                                     \
+        if (!(cond)) {                       \
+            rt_set_error("%s", msg);         \
+            return RT_EINVAL;                \
+        }                                    \
+    } while (0)
+
+// reads and clears the device error flag (synchronises the context stream)
+int rt_check_device_error(rt_ctx* ctx);
 
 // --------------------------------------------------------------------------
 // exact fp32 helpers (parity-critical paths use explicit selects, no FMNMX

@@ -1,0 +1,610 @@
+// tlas.cu -- two-level (TLAS / BLAS) closest- and any-hit traversal on the GPU
+// (replaces the reference's Tlas / Blas / Instance kernels, accel.py:211-283,
+// 439-549, 575-699, 762-895).
+//
+// A BLAS is an rt_scene in LOCAL space (its own LBVH; triangle prims, or the
+// AABBs of custom primitives).  The TLAS is an rt_scene whose primitives are
+// the instances' world AABBs (the corners of the BLAS root box through the
+// instance matrix, accel.py:459-469), so it reuses the same LBVH builder.
+// One thread per ray walks the TLAS 4-wide; at an instance leaf (mask AND,
+// accel.py:796) the ray goes to local space (accel.py:804-809; the direction
+// keeps its length so local t == world t) and walks that BLAS with a second
+// stack.  The tie rule is the reference's: lowest instance, then lowest prim
+// (accel.py:629, 815-817).  Normals leave the kernel as (inst, prim) and are
+// produced in float64 by the expand kernel: the BLAS's float64 local normal
+// (or the sphere's at the hit) through the instance inverse transpose,
+// renormalised (accel.py:843-847).  Custom primitives are spheres behind the
+// registry: with no registered data, reaching one is RT_EUNSUPPORTED.
+#include <map>
+#include <vector>
+
+#include "traverse.cuh"
+
+struct BlasDev {
+    const float4* bvh4;
+    const float4* tris;       // leaf-ordered: v0.w = prim, v1.w = mask (full)
+    const double* lnormal;    // (n, 3) float64 local normals (triangles)
+    const double* data;       // custom: rows (cx, cy, cz, r) of this BLAS's prims (nullptr: not registered)
+    int root4, height, kind, geom_type;
+};
+
+struct InstDev {
+    float inv[12];            // fp32 inverse for the local ray of the walk
+    double inv64[12];         // float64 inverse (custom tests, normals)
+    uint32_t mask;
+    int blas;
+    int pad0, pad1;
+};
+
+struct rt_tlas {
+    int n_inst = 0;
+    rt_scene* top = nullptr;            // owned: LBVH over instance world boxes
+    std::vector<rt_scene*> blas;        // unique BLAS handles (not owned)
+    std::vector<int> inst_blas;
+    std::vector<BlasDev> hblas;
+    std::vector<InstDev> hinst;
+    BlasDev* d_blas = nullptr;
+    InstDev* d_inst = nullptr;
+    std::vector<double*> d_data;        // per BLAS registered custom rows (owned)
+    int top_root4 = 0, top_height = 0, max_height = 0;
+};
+
+namespace {
+
+constexpr int TL_THREADS = 128;
+
+struct TlasView {
+    const float4* tbvh4;
+    const float4* ttris;
+    int troot;
+    const InstDev* inst;
+    const BlasDev* blas;
+    int* err;
+};
+
+struct Hit2 {
+    float t;
+    int inst, prim;
+    float u, v;
+};
+
+// tie bound for the BLAS walk of instance i given the best hit so far: a hit at
+// exactly best_t wins iff i < best_inst (each instance is one TLAS leaf, so
+// i != best_inst); tri_test rejects a tie when prim >= bound
+__device__ __forceinline__ int tie_bound(int i, int best_inst) {
+    return (best_inst >= 0 && i < best_inst) ? INT_MAX : INT_MIN;
+}
+
+__device__ __forceinline__ void inst_local(const InstDev* __restrict__ I, const RayPre& W, float lo[3], float ld[3]) {
+    float m[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) m[k] = __ldg(I->inv + k);
+    lo[0] = fmaf(m[0], W.ox, fmaf(m[1], W.oy, fmaf(m[2], W.oz, m[3])));
+    lo[1] = fmaf(m[4], W.ox, fmaf(m[5], W.oy, fmaf(m[6], W.oz, m[7])));
+    lo[2] = fmaf(m[8], W.ox, fmaf(m[9], W.oy, fmaf(m[10], W.oz, m[11])));
+    ld[0] = fmaf(m[0], W.dx, fmaf(m[1], W.dy, m[2] * W.dz));
+    ld[1] = fmaf(m[4], W.dx, fmaf(m[5], W.dy, m[6] * W.dz));
+    ld[2] = fmaf(m[8], W.dx, fmaf(m[9], W.dy, m[10] * W.dz));
+}
+
+// custom primitive (sphere) k of a custom BLAS: float64 test on the float64 local ray
+static __device__ __noinline__ double custom_hit(const InstDev* __restrict__ I, const double* __restrict__ row,
+                                                 const RayPre& W, double t_min, double t_max) {
+    double m[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) m[k] = __ldg(I->inv64 + k);
+    double o[3], d[3];
+    to_local_f64(m, W.ox, W.oy, W.oz, W.dx, W.dy, W.dz, o, d);
+    return sphere_solve_f64(o, d, __ldg(row), __ldg(row + 1), __ldg(row + 2), __ldg(row + 3), t_min, t_max);
+}
+
+template <bool STATS>
+__device__ __forceinline__ Hit2 tlas_closest(const TlasView& T, const RayPre& W, float tmax, uint32_t ray_mask,
+                                             int2* st_top, int2* st_bot, uint32_t& n_tests, uint32_t& n_visits) {
+    Hit2 best;
+    best.t = tmax; best.inst = -1; best.prim = -1; best.u = 0.f; best.v = 0.f;
+    walk4<STATS>(T.tbvh4, T.troot, W, best.t, st_top, n_visits, [&](int k) {
+        const float4* tp = T.ttris + 3 * k;
+        const int i = __float_as_int(__ldg(tp).w);
+        const uint32_t m = __float_as_uint(__ldg(tp + 1).w);
+        if (!(m & ray_mask)) return;                          // accel.py:796
+        const InstDev* I = T.inst + i;
+        const BlasDev B = T.blas[__ldg(&I->blas)];
+        float t = best.t, u = best.u, v = best.v;
+        int id = tie_bound(i, best.inst);
+        const int id0 = id;
+        float lo[3], ld[3];
+        inst_local(I, W, lo, ld);
+        RayPre L;
+        ray_setup(L, lo[0], lo[1], lo[2], ld[0], ld[1], ld[2], W.tmin);
+        if (B.kind == 0) {
+            walk4<STATS>(B.bvh4, B.root4, L, t, st_bot, n_visits, [&](int kk) {
+                const float4* q = B.tris + 3 * kk;
+                const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+                if (STATS) ++n_tests;
+                tri_test(L, a, b, c, t, id, u, v);
+            });
+        } else {
+            if (!B.data) {                                    // accel.py:800-803
+                atomicExch(T.err, RT_EUNSUPPORTED);
+                return;
+            }
+            walk4<STATS>(B.bvh4, B.root4, L, t, st_bot, n_visits, [&](int kk) {
+                const int prim = __float_as_int(__ldg(B.tris + 3 * kk).w);
+                if (STATS) ++n_tests;
+                const double th = custom_hit(I, B.data + 4 * (int64_t)prim, W, (double)W.tmin, (double)t);
+                if (th < 0.0) return;
+                const float tf = (float)th;
+                if (tf > t || (tf == t && prim >= id)) return;
+                t = tf; id = prim; u = 0.f; v = 0.f;
+            });
+        }
+        if (id != id0) {
+            best.t = t; best.inst = i; best.prim = id; best.u = u; best.v = v;
+        }
+    });
+    if (best.inst < 0) best.t = -1.0f;
+    return best;
+}
+
+__device__ __forceinline__ bool tlas_any(const TlasView& T, const RayPre& W, float tmax, uint32_t ray_mask,
+                                         int* st_top, int* st_bot) {
+    return walk_any4(T.tbvh4, T.troot, W, tmax, st_top, [&](int k) -> bool {
+        const float4* tp = T.ttris + 3 * k;
+        const int i = __float_as_int(__ldg(tp).w);
+        const uint32_t m = __float_as_uint(__ldg(tp + 1).w);
+        if (!(m & ray_mask)) return false;
+        const InstDev* I = T.inst + i;
+        const BlasDev B = T.blas[__ldg(&I->blas)];
+        float lo[3], ld[3];
+        inst_local(I, W, lo, ld);
+        RayPre L;
+        ray_setup(L, lo[0], lo[1], lo[2], ld[0], ld[1], ld[2], W.tmin);
+        if (B.kind == 0)
+            return walk_any4(B.bvh4, B.root4, L, tmax, st_bot, [&](int kk) -> bool {
+                const float4* q = B.tris + 3 * kk;
+                return tri_any(L, __ldg(q), __ldg(q + 1), __ldg(q + 2), tmax);
+            });
+        if (!B.data) {
+            atomicExch(T.err, RT_EUNSUPPORTED);
+            return false;
+        }
+        return walk_any4(B.bvh4, B.root4, L, tmax, st_bot, [&](int kk) -> bool {
+            const int prim = __float_as_int(__ldg(B.tris + 3 * kk).w);
+            return custom_hit(I, B.data + 4 * (int64_t)prim, W, (double)W.tmin, (double)tmax) >= 0.0;
+        });
+    });
+}
+
+template <bool STATS>
+__global__ void __launch_bounds__(TL_THREADS) tlas_closest_kernel(const TlasView T, int max_height, int64_t n,
+                                                                  const float* __restrict__ rays,
+                                                                  float4* __restrict__ hits, uint32_t ray_mask,
+                                                                  uint32_t* __restrict__ stats, unsigned int* counter) {
+    if (max_height + 1 > RT_STACK) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(T.err, RT_EDEPTH);
+        return;
+    }
+    int2 st_top[RT_STACK4], st_bot[RT_STACK4];
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(counter, 32u);
+        base = __shfl_sync(RT_FULL, base, 0);
+        if ((int64_t)base >= n) break;
+        const int64_t i = (int64_t)base + lane;
+        if (i < n) {
+            const TraceRay r = load_ray(rays, i);
+            RayPre W;
+            ray_setup(W, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
+            uint32_t nt = 0, nv = 0;
+            const Hit2 h = tlas_closest<STATS>(T, W, r.tmax, ray_mask, st_top, st_bot, nt, nv);
+            hits[2 * i] = make_float4(h.t, __int_as_float(h.inst), __int_as_float(h.prim), h.u);
+            hits[2 * i + 1] = make_float4(h.v, 0.f, 0.f, 0.f);
+            if (STATS) reinterpret_cast<uint2*>(stats)[i] = make_uint2(nt, nv);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(TL_THREADS) tlas_any_kernel(const TlasView T, int max_height, int64_t n,
+                                                              const float* __restrict__ rays, uint8_t* __restrict__ out,
+                                                              uint32_t ray_mask, unsigned int* counter) {
+    if (max_height + 1 > RT_STACK) {
+        if (threadIdx.x == 0 && blockIdx.x == 0) atomicExch(T.err, RT_EDEPTH);
+        return;
+    }
+    int st_top[RT_STACK4], st_bot[RT_STACK4];
+    const int lane = threadIdx.x & 31;
+    while (true) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(counter, 32u);
+        base = __shfl_sync(RT_FULL, base, 0);
+        if ((int64_t)base >= n) break;
+        const int64_t i = (int64_t)base + lane;
+        if (i < n) {
+            const TraceRay r = load_ray(rays, i);
+            RayPre W;
+            ray_setup(W, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
+            out[i] = tlas_any(T, W, r.tmax, ray_mask, st_top, st_bot) ? 1 : 0;
+        }
+    }
+}
+
+// accel.py:843-847 in the reference's operation order (float64, no contraction)
+__device__ __forceinline__ void world_normal_f64(const double* m, double lx, double ly, double lz, double* out) {
+    const double wx = __dadd_rn(__dadd_rn(__dmul_rn(m[0], lx), __dmul_rn(m[4], ly)), __dmul_rn(m[8], lz));
+    const double wy = __dadd_rn(__dadd_rn(__dmul_rn(m[1], lx), __dmul_rn(m[5], ly)), __dmul_rn(m[9], lz));
+    const double wz = __dadd_rn(__dadd_rn(__dmul_rn(m[2], lx), __dmul_rn(m[6], ly)), __dmul_rn(m[10], lz));
+    const double il = __ddiv_rn(1.0, sqrt(__dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)),
+                                                   __dmul_rn(wz, wz))));
+    out[0] = __dmul_rn(wx, il); out[1] = __dmul_rn(wy, il); out[2] = __dmul_rn(wz, il);
+}
+
+__global__ void tlas_expand_f64(int64_t n, const float4* __restrict__ hits, const float* __restrict__ rays,
+                                const InstDev* __restrict__ inst, const BlasDev* __restrict__ blas, double* t,
+                                int64_t* oinst, int64_t* oprim, double* u, double* v, double* nrm) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 h0 = hits[2 * i], h1 = hits[2 * i + 1];
+        const int ii = __float_as_int(h0.y), p = __float_as_int(h0.z);
+        if (ii < 0) {
+            t[i] = -1.0; oinst[i] = -1; oprim[i] = -1; u[i] = -1.0; v[i] = -1.0;
+            nrm[3 * i] = nrm[3 * i + 1] = nrm[3 * i + 2] = 0.0;
+            continue;
+        }
+        const InstDev* I = inst + ii;
+        const BlasDev B = blas[I->blas];
+        double m[12];
+        for (int k = 0; k < 12; ++k) m[k] = I->inv64[k];
+        double ln[3];
+        if (B.kind == 0) {
+            ln[0] = B.lnormal[3 * p]; ln[1] = B.lnormal[3 * p + 1]; ln[2] = B.lnormal[3 * p + 2];
+        } else {                                   // geometry.py:360-363 at the hit, local space
+            const TraceRay r = load_ray(rays, i);
+            double o[3], d[3];
+            to_local_f64(m, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, o, d);
+            const double* row = B.data + 4 * (int64_t)p;
+            const double th = h0.x;
+            for (int k = 0; k < 3; ++k) ln[k] = (o[k] + d[k] * th - row[k]) / row[3];
+        }
+        world_normal_f64(m, ln[0], ln[1], ln[2], nrm + 3 * i);
+        t[i] = h0.x; oinst[i] = ii; oprim[i] = p; u[i] = h0.w; v[i] = h1.x;
+    }
+}
+
+int tlas_view(rt_ctx* c, rt_tlas* T, TlasView& V) {
+    V.tbvh4 = T->top->bvh4;
+    V.ttris = T->top->tri_sorted;
+    V.troot = T->top_root4;
+    V.inst = T->d_inst;
+    V.blas = T->d_blas;
+    V.err = c->d_error;
+    return RT_OK;
+}
+
+int read_root(rt_ctx* c, rt_scene* s, int& root4, int& height) {
+    float4 n3;
+    RT_CUDA_TRY(cudaMemcpyAsync(&n3, s->nodes + 3, sizeof n3, cudaMemcpyDeviceToHost, c->stream));
+    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    memcpy(&height, &n3.z, 4);
+    memcpy(&root4, &n3.w, 4);
+    return RT_OK;
+}
+
+int upload_inst(rt_ctx* c, rt_tlas* T, const double* inv12) {
+    for (int i = 0; i < T->n_inst; ++i) {
+        InstDev& I = T->hinst[i];
+        for (int k = 0; k < 12; ++k) {
+            I.inv64[k] = inv12[12 * i + k];
+            I.inv[k] = (float)inv12[12 * i + k];
+        }
+    }
+    RT_CUDA_TRY(cudaMemcpyAsync(T->d_inst, T->hinst.data(), sizeof(InstDev) * T->n_inst, cudaMemcpyHostToDevice,
+                                c->stream));
+    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return RT_OK;
+}
+
+int build_top(rt_ctx* c, rt_tlas* T, const float* boxes6) {
+    std::vector<float> tris(9 * (size_t)T->n_inst);
+    for (int i = 0; i < T->n_inst; ++i) {
+        const float* b = boxes6 + 6 * i;
+        float* q = tris.data() + 9 * (size_t)i;
+        q[0] = b[0]; q[1] = b[1]; q[2] = b[2];
+        q[3] = b[3]; q[4] = b[4]; q[5] = b[5];
+        q[6] = b[0]; q[7] = b[1]; q[8] = b[2];
+    }
+    int rc = rt_scene_set_vertices(c, T->top, tris.data());
+    if (rc) return rc;
+    rc = rt_bvh_build(c, T->top, 30, nullptr);
+    if (rc) return rc;
+    return read_root(c, T->top, T->top_root4, T->top_height);
+}
+
+}  // namespace
+
+extern "C" {
+
+int rt_scene_set_local_normals(rt_ctx* c, rt_scene* s, const double* n3) {
+    RT_CHECK_ARG(c && s && n3, "NULL argument");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    if (!s->lnormal64) RT_CUDA_TRY(cudaMalloc(&s->lnormal64, sizeof(double) * 3 * (size_t)s->n));
+    RT_CUDA_TRY(cudaMemcpy(s->lnormal64, n3, sizeof(double) * 3 * (size_t)s->n, cudaMemcpyHostToDevice));
+    return RT_OK;
+}
+
+int rt_scene_set_custom(rt_ctx* c, rt_scene* s, int32_t geom_type, int64_t data_offset) {
+    RT_CHECK_ARG(c && s && geom_type >= 0 && data_offset >= 0, "bad custom primitive description");
+    s->custom = 1;
+    s->geom_type = geom_type;
+    s->data_offset = data_offset;
+    return RT_OK;
+}
+
+int rt_tlas_create(rt_ctx* c, int32_t n_inst, rt_scene* const* inst_blas, const double* inv12, const float* boxes6,
+                   const uint32_t* masks, rt_tlas** out) {
+    RT_CHECK_ARG(c && out && n_inst >= 1 && inst_blas && inv12 && boxes6 && masks, "bad tlas arguments");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    rt_tlas* T = new rt_tlas();
+    T->n_inst = n_inst;
+    std::map<rt_scene*, int> idx;
+    for (int i = 0; i < n_inst; ++i) {
+        rt_scene* b = inst_blas[i];
+        if (!b || !b->built) {
+            delete T;
+            rt_set_error("instance %d references an unbuilt blas", i);
+            return RT_EINVAL;
+        }
+        auto it = idx.find(b);
+        if (it == idx.end()) {
+            it = idx.emplace(b, (int)T->blas.size()).first;
+            T->blas.push_back(b);
+        }
+        T->inst_blas.push_back(it->second);
+    }
+    // top level: an rt_scene over the instance boxes; flat id == instance, mask per prim
+    std::vector<float> zeros(9 * (size_t)n_inst, 0.f), nz(3 * (size_t)n_inst, 0.f), mat(3, 0.f);
+    std::vector<int32_t> ids(n_inst), prim(n_inst, 0), tmat(n_inst, 0);
+    for (int i = 0; i < n_inst; ++i) ids[i] = i;
+    int rc = rt_scene_create(c, n_inst, zeros.data(), nz.data(), ids.data(), prim.data(), masks, tmat.data(),
+                             mat.data(), mat.data(), 1, &T->top);
+    if (rc) { delete T; return rc; }
+    T->hblas.resize(T->blas.size());
+    T->d_data.assign(T->blas.size(), nullptr);
+    T->max_height = 0;
+    for (size_t b = 0; b < T->blas.size(); ++b) {
+        rt_scene* s = T->blas[b];
+        BlasDev& B = T->hblas[b];
+        B.bvh4 = s->bvh4;
+        B.tris = s->tri_sorted;
+        B.lnormal = s->lnormal64;
+        B.data = nullptr;
+        B.kind = s->custom ? 1 : 0;
+        B.geom_type = s->custom ? s->geom_type : -1;
+        if (!s->custom && !s->lnormal64) {
+            rt_tlas_destroy(T);
+            rt_set_error("triangle blas without local normals (rt_scene_set_local_normals)");
+            return RT_EINVAL;
+        }
+        rc = read_root(c, s, B.root4, B.height);
+        if (rc) { rt_tlas_destroy(T); return rc; }
+        T->max_height = std::max(T->max_height, B.height);
+    }
+    T->hinst.resize(n_inst);
+    for (int i = 0; i < n_inst; ++i) {
+        T->hinst[i].mask = masks[i];
+        T->hinst[i].blas = T->inst_blas[i];
+        T->hinst[i].pad0 = T->hinst[i].pad1 = 0;
+    }
+    cudaError_t e1 = cudaMalloc(&T->d_blas, sizeof(BlasDev) * T->hblas.size());
+    cudaError_t e2 = cudaMalloc(&T->d_inst, sizeof(InstDev) * n_inst);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+        rt_tlas_destroy(T);
+        rt_set_error("cudaMalloc failed for the tlas tables");
+        return RT_ENOMEM;
+    }
+    RT_CUDA_TRY(cudaMemcpy(T->d_blas, T->hblas.data(), sizeof(BlasDev) * T->hblas.size(), cudaMemcpyHostToDevice));
+    rc = upload_inst(c, T, inv12);
+    if (!rc) rc = build_top(c, T, boxes6);
+    if (rc) { rt_tlas_destroy(T); return rc; }
+    T->max_height = std::max(T->max_height, T->top_height);
+    *out = T;
+    return RT_OK;
+}
+
+int rt_tlas_update(rt_ctx* c, rt_tlas* T, const double* inv12, const float* boxes6) {
+    RT_CHECK_ARG(c && T && inv12 && boxes6, "NULL argument");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    // BLAS refits may have changed their roots / heights (rebuilt LBVH)
+    T->max_height = 0;
+    for (size_t b = 0; b < T->blas.size(); ++b) {
+        int rc = read_root(c, T->blas[b], T->hblas[b].root4, T->hblas[b].height);
+        if (rc) return rc;
+        T->hblas[b].bvh4 = T->blas[b]->bvh4;
+        T->hblas[b].tris = T->blas[b]->tri_sorted;
+        T->max_height = std::max(T->max_height, T->hblas[b].height);
+    }
+    RT_CUDA_TRY(cudaMemcpy(T->d_blas, T->hblas.data(), sizeof(BlasDev) * T->hblas.size(), cudaMemcpyHostToDevice));
+    int rc = upload_inst(c, T, inv12);
+    if (rc) return rc;
+    rc = build_top(c, T, boxes6);
+    if (rc) return rc;
+    T->max_height = std::max(T->max_height, T->top_height);
+    return RT_OK;
+}
+
+int rt_tlas_set_custom_data(rt_ctx* c, rt_tlas* T, int32_t geom_type, int64_t n_rows, const double* rows4) {
+    RT_CHECK_ARG(c && T && n_rows >= 0 && (n_rows == 0 || rows4), "bad custom data");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    bool changed = false;
+    for (size_t b = 0; b < T->blas.size(); ++b) {
+        rt_scene* s = T->blas[b];
+        if (!s->custom || s->geom_type != geom_type) continue;
+        if (T->d_data[b]) cudaFree(T->d_data[b]);
+        T->d_data[b] = nullptr;
+        T->hblas[b].data = nullptr;
+        changed = true;
+        if (n_rows == 0) continue;                       // unregister
+        if (s->data_offset + s->n > n_rows) {
+            rt_set_error("custom data has %lld rows, blas needs rows [%lld, %lld)", (long long)n_rows,
+                         (long long)s->data_offset, (long long)(s->data_offset + s->n));
+            return RT_EINVAL;
+        }
+        RT_CUDA_TRY(cudaMalloc(&T->d_data[b], sizeof(double) * 4 * (size_t)s->n));
+        RT_CUDA_TRY(cudaMemcpy(T->d_data[b], rows4 + 4 * s->data_offset, sizeof(double) * 4 * (size_t)s->n,
+                               cudaMemcpyHostToDevice));
+        T->hblas[b].data = T->d_data[b];
+    }
+    if (changed)
+        RT_CUDA_TRY(cudaMemcpy(T->d_blas, T->hblas.data(), sizeof(BlasDev) * T->hblas.size(),
+                               cudaMemcpyHostToDevice));
+    return RT_OK;
+}
+
+void rt_tlas_destroy(rt_tlas* T) {
+    if (!T) return;
+    if (T->top) rt_scene_destroy(T->top);
+    if (T->d_blas) cudaFree(T->d_blas);
+    if (T->d_inst) cudaFree(T->d_inst);
+    for (double* p : T->d_data)
+        if (p) cudaFree(p);
+    delete T;
+}
+
+int rt_tlas_info(rt_ctx* c, rt_tlas* T, float* root6, int32_t* height) {
+    RT_CHECK_ARG(c && T, "NULL argument");
+    return rt_bvh_info(c, T->top, root6, height, nullptr);
+}
+
+// accel.py:1128-1156 closest_hit_batch over a two-level structure (host float64 rays)
+int rt_tlas_closest_host(rt_ctx* c, rt_tlas* T, int64_t n, const double* o, const double* d, const double* tmin,
+                         const double* tmax, uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
+                         double* v, double* nrm, int64_t* stats) {
+    RT_CHECK_ARG(c && T, "NULL argument");
+    RT_CHECK_ARG(n >= 0, "negative ray count");
+    if (n == 0) return RT_OK;
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    const int64_t CH = std::min<int64_t>(n, 1 << 20);
+    double *d_o, *d_d, *d_tmin, *d_tmax, *d_t, *d_u, *d_v, *d_n;
+    int64_t *d_inst, *d_prim;
+    float* d_rays;
+    float4* d_hits;
+    uint32_t* d_stats;
+    size_t need = (size_t)CH * (24 + 24 + 8 + 8 + 32 + 32 + 8 + 8 + 8 + 8 + 8 + 8 + 24) + 1024;
+    if (c->d_stage_bytes < need) {
+        if (c->d_stage) cudaFree(c->d_stage);
+        c->d_stage = nullptr;
+        c->d_stage_bytes = 0;
+        RT_CUDA_TRY(cudaMalloc(&c->d_stage, need));
+        c->d_stage_bytes = need;
+    }
+    char* D = (char*)c->d_stage;
+    d_o = (double*)D; D += 24 * CH;
+    d_d = (double*)D; D += 24 * CH;
+    d_tmin = (double*)D; D += 8 * CH;
+    d_tmax = (double*)D; D += 8 * CH;
+    d_rays = (float*)D; D += 32 * CH;
+    d_hits = (float4*)D; D += 32 * CH;
+    d_stats = (uint32_t*)D; D += 8 * CH;
+    d_t = (double*)D; D += 8 * CH;
+    d_inst = (int64_t*)D; D += 8 * CH;
+    d_prim = (int64_t*)D; D += 8 * CH;
+    d_u = (double*)D; D += 8 * CH;
+    d_v = (double*)D; D += 8 * CH;
+    d_n = (double*)D; D += 24 * CH;
+    TlasView V;
+    tlas_view(c, T, V);
+    cudaStream_t st = c->stream;
+    std::vector<uint32_t> hs;
+    if (stats) hs.resize(2 * CH);
+    for (int64_t b = 0; b < n; b += CH) {
+        const int64_t m = std::min(CH, n - b);
+        RT_CUDA_TRY(cudaMemcpyAsync(d_o, o + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_d, d + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_tmin, tmin + b, 8 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
+        int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
+        if (rc) return rc;
+        RT_CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), st));
+        int bps = 0;
+        if (stats) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, tlas_closest_kernel<true>, TL_THREADS, 0);
+        else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, tlas_closest_kernel<false>, TL_THREADS, 0);
+        if (bps < 1) bps = 1;
+        const int64_t grid = std::min<int64_t>((int64_t)c->num_sms * bps, (m + TL_THREADS - 1) / TL_THREADS);
+        if (stats)
+            tlas_closest_kernel<true><<<(unsigned)grid, TL_THREADS, 0, st>>>(V, T->max_height, m, d_rays, d_hits,
+                                                                            ray_mask, d_stats, c->d_counter);
+        else
+            tlas_closest_kernel<false><<<(unsigned)grid, TL_THREADS, 0, st>>>(V, T->max_height, m, d_rays, d_hits,
+                                                                             ray_mask, nullptr, c->d_counter);
+        RT_CUDA_TRY(cudaGetLastError());
+        tlas_expand_f64<<<c->num_sms * 4, 256, 0, st>>>(m, d_hits, d_rays, T->d_inst, T->d_blas, d_t, d_inst, d_prim,
+                                                        d_u, d_v, d_n);
+        RT_CUDA_TRY(cudaGetLastError());
+        RT_CUDA_TRY(cudaMemcpyAsync(t + b, d_t, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(inst + b, d_inst, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(prim + b, d_prim, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(u + b, d_u, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(v + b, d_v, 8 * m, cudaMemcpyDeviceToHost, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(nrm + 3 * b, d_n, 24 * m, cudaMemcpyDeviceToHost, st));
+        if (stats) {
+            RT_CUDA_TRY(cudaMemcpyAsync(hs.data(), d_stats, 8 * m, cudaMemcpyDeviceToHost, st));
+            RT_CUDA_TRY(cudaStreamSynchronize(st));
+            for (int64_t k = 0; k < m; ++k) {
+                stats[2 * (b + k)] = hs[2 * k];
+                stats[2 * (b + k) + 1] = hs[2 * k + 1];
+            }
+        }
+    }
+    RT_CUDA_TRY(cudaStreamSynchronize(st));
+    return rt_check_device_error(c);
+}
+
+// accel.py:1159-1174 any_hit_batch over a two-level structure
+int rt_tlas_any_host(rt_ctx* c, rt_tlas* T, int64_t n, const double* o, const double* d, const double* tmin,
+                     const double* tmax, uint32_t ray_mask, uint8_t* out) {
+    RT_CHECK_ARG(c && T, "NULL argument");
+    RT_CHECK_ARG(n >= 0, "negative ray count");
+    if (n == 0) return RT_OK;
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    const int64_t CH = std::min<int64_t>(n, 1 << 20);
+    size_t need = (size_t)CH * (24 + 24 + 8 + 8 + 32 + 1) + 1024;
+    if (c->d_stage_bytes < need) {
+        if (c->d_stage) cudaFree(c->d_stage);
+        c->d_stage = nullptr;
+        c->d_stage_bytes = 0;
+        RT_CUDA_TRY(cudaMalloc(&c->d_stage, need));
+        c->d_stage_bytes = need;
+    }
+    char* D = (char*)c->d_stage;
+    double* d_o = (double*)D; D += 24 * CH;
+    double* d_d = (double*)D; D += 24 * CH;
+    double* d_tmin = (double*)D; D += 8 * CH;
+    double* d_tmax = (double*)D; D += 8 * CH;
+    float* d_rays = (float*)D; D += 32 * CH;
+    uint8_t* d_out = (uint8_t*)D;
+    TlasView V;
+    tlas_view(c, T, V);
+    cudaStream_t st = c->stream;
+    for (int64_t b = 0; b < n; b += CH) {
+        const int64_t m = std::min(CH, n - b);
+        RT_CUDA_TRY(cudaMemcpyAsync(d_o, o + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_d, d + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_tmin, tmin + b, 8 * m, cudaMemcpyHostToDevice, st));
+        RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
+        int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
+        if (rc) return rc;
+        RT_CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), st));
+        int bps = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, tlas_any_kernel, TL_THREADS, 0);
+        if (bps < 1) bps = 1;
+        const int64_t grid = std::min<int64_t>((int64_t)c->num_sms * bps, (m + TL_THREADS - 1) / TL_THREADS);
+        tlas_any_kernel<<<(unsigned)grid, TL_THREADS, 0, st>>>(V, T->max_height, m, d_rays, d_out, ray_mask,
+                                                               c->d_counter);
+        RT_CUDA_TRY(cudaGetLastError());
+        RT_CUDA_TRY(cudaMemcpyAsync(out + b, d_out, m, cudaMemcpyDeviceToHost, st));
+    }
+    RT_CUDA_TRY(cudaStreamSynchronize(st));
+    return rt_check_device_error(c);
+}
+
+}  // extern "C"

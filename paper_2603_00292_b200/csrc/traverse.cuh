@@ -144,21 +144,10 @@ __device__ __forceinline__ void sphere_local(const double* m, double ox, double 
     ld[2] = m[8] * dx + m[9] * dy + m[10] * dz;
 }
 
-// geometry.py:334-363 _sphere_hit in float64 (no FMA contraction: explicit _rn ops)
-static __device__ __noinline__ double sphere_hit_f64(const double* __restrict__ row, float fox, float foy, float foz,
-                                                     float fdx, float fdy, float fdz, double t_min, double t_max) {
-    double m[12];
-#pragma unroll
-    for (int k = 0; k < 12; ++k) m[k] = __ldg(row + k);
-    double o[3], d[3];
-    const double ox = fox, oy = foy, oz = foz, dx = fdx, dy = fdy, dz = fdz;
-    o[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[0], ox), __dmul_rn(m[1], oy)), __dmul_rn(m[2], oz)), m[3]);
-    o[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[4], ox), __dmul_rn(m[5], oy)), __dmul_rn(m[6], oz)), m[7]);
-    o[2] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[8], ox), __dmul_rn(m[9], oy)), __dmul_rn(m[10], oz)), m[11]);
-    d[0] = __dadd_rn(__dadd_rn(__dmul_rn(m[0], dx), __dmul_rn(m[1], dy)), __dmul_rn(m[2], dz));
-    d[1] = __dadd_rn(__dadd_rn(__dmul_rn(m[4], dx), __dmul_rn(m[5], dy)), __dmul_rn(m[6], dz));
-    d[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[8], dx), __dmul_rn(m[9], dy)), __dmul_rn(m[10], dz));
-    const double cx = __ldg(row + 12), cy = __ldg(row + 13), cz = __ldg(row + 14), r = __ldg(row + 15);
+// geometry.py:334-363 _sphere_hit in float64 on a local ray (no FMA contraction:
+// explicit _rn ops); returns t or -1
+__device__ __forceinline__ double sphere_solve_f64(const double o[3], const double d[3], double cx, double cy,
+                                                   double cz, double r, double t_min, double t_max) {
     const double lx = __dsub_rn(o[0], cx), ly = __dsub_rn(o[1], cy), lz = __dsub_rn(o[2], cz);
     const double a = __dadd_rn(__dadd_rn(__dmul_rn(d[0], d[0]), __dmul_rn(d[1], d[1])), __dmul_rn(d[2], d[2]));
     const double b = __dmul_rn(2.0, __dadd_rn(__dadd_rn(__dmul_rn(lx, d[0]), __dmul_rn(ly, d[1])), __dmul_rn(lz, d[2])));
@@ -178,6 +167,28 @@ static __device__ __noinline__ double sphere_hit_f64(const double* __restrict__ 
         if (t < t_min || t > t_max) return -1.0;
     }
     return t;
+}
+
+// accel.py:804-809 world -> local in float64, the reference's operation order
+__device__ __forceinline__ void to_local_f64(const double* m, double ox, double oy, double oz, double dx, double dy,
+                                             double dz, double o[3], double d[3]) {
+    o[0] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[0], ox), __dmul_rn(m[1], oy)), __dmul_rn(m[2], oz)), m[3]);
+    o[1] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[4], ox), __dmul_rn(m[5], oy)), __dmul_rn(m[6], oz)), m[7]);
+    o[2] = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[8], ox), __dmul_rn(m[9], oy)), __dmul_rn(m[10], oz)), m[11]);
+    d[0] = __dadd_rn(__dadd_rn(__dmul_rn(m[0], dx), __dmul_rn(m[1], dy)), __dmul_rn(m[2], dz));
+    d[1] = __dadd_rn(__dadd_rn(__dmul_rn(m[4], dx), __dmul_rn(m[5], dy)), __dmul_rn(m[6], dz));
+    d[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[8], dx), __dmul_rn(m[9], dy)), __dmul_rn(m[10], dz));
+}
+
+// geometry.py:334-363 _sphere_hit in float64 on the world ray of a sphere instance
+static __device__ __noinline__ double sphere_hit_f64(const double* __restrict__ row, float fox, float foy, float foz,
+                                                     float fdx, float fdy, float fdz, double t_min, double t_max) {
+    double m[12];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) m[k] = __ldg(row + k);
+    double o[3], d[3];
+    to_local_f64(m, fox, foy, foz, fdx, fdy, fdz, o, d);
+    return sphere_solve_f64(o, d, __ldg(row + 12), __ldg(row + 13), __ldg(row + 14), __ldg(row + 15), t_min, t_max);
 }
 
 // world normal of a sphere hit: local (p - c) / r through the inverse transpose,
@@ -421,4 +432,72 @@ __device__ __forceinline__ HitRec trace_ray(const float4* __restrict__ nodes, co
     }
     if (h.id < 0) h.t = -1.0f;
     return h;
+}
+
+// ---- generic 4-wide walks with a leaf callback (two-level traversal, tlas.cu) ----
+// Same node layout, slab test, nearest-first order and pop culling as
+// trace_ray4; leaf(k) handles leaf k and may lower best_t.
+template <bool STATS, typename Leaf>
+__device__ __forceinline__ void walk4(const float4* __restrict__ bvh4, int root, const RayPre& R, float& best_t,
+                                      int2* stack, uint32_t& n_visits, Leaf&& leaf) {
+    int sp = 0;
+    stack[0] = make_int2(RT_SENTINEL, 0);
+    int node = root;
+    while (node != RT_SENTINEL) {
+        if (node >= 0) {
+            const float4* q = bvh4 + 8 * node;
+            const float4 l0 = __ldg(q), h0 = __ldg(q + 1), l1 = __ldg(q + 2), h1 = __ldg(q + 3);
+            const float4 l2 = __ldg(q + 4), h2 = __ldg(q + 5), l3 = __ldg(q + 6), h3 = __ldg(q + 7);
+            if (STATS) ++n_visits;
+            float t0 = box_enter(R, l0.x, h0.x, l0.y, h0.y, l0.z, h0.z, best_t);
+            float t1 = box_enter(R, l1.x, h1.x, l1.y, h1.y, l1.z, h1.z, best_t);
+            float t2 = box_enter(R, l2.x, h2.x, l2.y, h2.y, l2.z, h2.z, best_t);
+            float t3 = box_enter(R, l3.x, h3.x, l3.y, h3.y, l3.z, h3.z, best_t);
+            int c0 = __float_as_int(l0.w), c1 = __float_as_int(l1.w), c2 = __float_as_int(l2.w),
+                c3 = __float_as_int(l3.w);
+            cswap(t0, c0, t1, c1);
+            cswap(t2, c2, t3, c3);
+            cswap(t0, c0, t2, c2);
+            cswap(t1, c1, t3, c3);
+            cswap(t1, c1, t2, c2);
+            if (t3 != INFINITY) stack[++sp] = make_int2(c3, __float_as_int(t3));
+            if (t2 != INFINITY) stack[++sp] = make_int2(c2, __float_as_int(t2));
+            if (t1 != INFINITY) stack[++sp] = make_int2(c1, __float_as_int(t1));
+            if (t0 != INFINITY) {
+                node = c0;
+                continue;
+            }
+        } else {
+            leaf(~node);
+        }
+        while (true) {
+            const int2 e = stack[sp--];
+            node = e.x;
+            if (node == RT_SENTINEL || __int_as_float(e.y) <= fmaf(best_t, 1.0000008f, 1e-30f)) break;
+        }
+    }
+}
+
+// any-hit walk: leaf(k) returns true to stop
+template <typename Leaf>
+__device__ __forceinline__ bool walk_any4(const float4* __restrict__ bvh4, int root, const RayPre& R, float tmax,
+                                          int* stack, Leaf&& leaf) {
+    int sp = 0;
+    stack[0] = RT_SENTINEL;
+    int node = root;
+    while (node != RT_SENTINEL) {
+        if (node >= 0) {
+            const float4* q = bvh4 + 8 * node;
+            const float4 l0 = __ldg(q), h0 = __ldg(q + 1), l1 = __ldg(q + 2), h1 = __ldg(q + 3);
+            const float4 l2 = __ldg(q + 4), h2 = __ldg(q + 5), l3 = __ldg(q + 6), h3 = __ldg(q + 7);
+            if (box_enter(R, l3.x, h3.x, l3.y, h3.y, l3.z, h3.z, tmax) != INFINITY) stack[++sp] = __float_as_int(l3.w);
+            if (box_enter(R, l2.x, h2.x, l2.y, h2.y, l2.z, h2.z, tmax) != INFINITY) stack[++sp] = __float_as_int(l2.w);
+            if (box_enter(R, l1.x, h1.x, l1.y, h1.y, l1.z, h1.z, tmax) != INFINITY) stack[++sp] = __float_as_int(l1.w);
+            if (box_enter(R, l0.x, h0.x, l0.y, h0.y, l0.z, h0.z, tmax) != INFINITY) stack[++sp] = __float_as_int(l0.w);
+        } else if (leaf(~node)) {
+            return true;
+        }
+        node = stack[sp--];
+    }
+    return false;
 }
