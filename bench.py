@@ -307,8 +307,10 @@ def run_ours(args, ws, rank, local):
                 rows = np.array(distributed.band_rows(H, rank, ws))
                 sel = (rows[:, None] * W + np.arange(W)[None, :]).ravel()
                 r = r[sel]
-            O, D = np.ascontiguousarray(r[:, 0:3]), np.ascontiguousarray(r[:, 4:7])
-            host_tris = tl.tris.copy()
+            # the step's inputs live in pinned host memory (H2D runs as full-rate DMA)
+            from paper_2603_00292_b200._native import host_pinned_copy
+            O, D = host_pinned_copy(np.ascontiguousarray(r[:, 0:3])), host_pinned_copy(np.ascontiguousarray(r[:, 4:7]))
+            host_tris = host_pinned_copy(tl.tris)
             closest_hit_batch(sc, O, D)
             ke = max(1, min(K, 5))
             if ws > 1:
@@ -321,7 +323,7 @@ def run_ours(args, ws, rank, local):
             torch.cuda.synchronize()
             te = time.perf_counter() - t0
             nr = O.shape[0]
-            h2d = int(host_tris.nbytes + nr * (24 + 24 + 8 + 8))
+            h2d = int(host_tris.nbytes + nr * (24 + 24))        # t_min / t_max are broadcast scalars
             d2h = int(nr * (8 + 8 + 8 + 8 + 8 + 24))
             path = ("GpuTlas.refit(host fp32 vertices, H2D + LBVH rebuild) + closest_hit_batch(host float64 rays) "
                     "-> host float64/int64 (t, inst, prim, u, v, normal)")

@@ -129,22 +129,24 @@ int rt_bvh_download(rt_ctx* ctx, rt_scene* scene, uint64_t* sorted_keys, uint32_
  * u32 [triangle tests, node visits]. */
 int rt_trace_closest(rt_ctx* ctx, rt_scene* scene, int64_t n, const float* rays, float* hits,
                      uint32_t ray_mask, uint32_t* stats, int32_t flags);
-/* Host buffers with the reference's dtypes (float64 / int64), chunked and
- * pipelined H2D / trace / D2H.  Misses: t = -1, inst = prim = -1 (accel.py:964, 1144).
- * stats nullable (n, 2) int64. */
+/* Host buffers with the reference's dtypes (float64 / int64), in chunks through a
+ * three-stream pipeline (H2D of chunk k+1 || kernels of chunk k || D2H of chunk k-1;
+ * full-rate DMA when the host buffers are pinned).  t_min / t_max: per-ray arrays, or
+ * NULL to broadcast the scalars t_min_s / t_max_s (the reference's defaults 0, 1e30).
+ * Misses: t = -1, inst = prim = -1 (accel.py:964, 1144).  stats nullable (n, 2) int64. */
 int rt_closest_hit_host(rt_ctx* ctx, rt_scene* scene, int64_t n, const double* origins,
-                        const double* dirs, const double* t_min, const double* t_max,
-                        uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
-                        double* v, double* normal, int64_t* stats, int32_t flags);
+                        const double* dirs, const double* t_min, const double* t_max, double t_min_s,
+                        double t_max_s, uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim,
+                        double* u, double* v, double* normal, int64_t* stats, int32_t flags);
 
 /* ---- any hit (replaces _any_batch / any_hit_batch, accel.py:979-992, 1159-1174) */
 /* device rays (n, 8) -> hit (n) uint8 (1 = some accepted intersection in [tmin, tmax]) */
 int rt_trace_any(rt_ctx* ctx, rt_scene* scene, int64_t n, const float* rays, uint8_t* hit,
                  uint32_t ray_mask, int32_t flags);
-/* host float64 rays -> host uint8 (numpy bool) */
+/* host float64 rays -> host uint8 (numpy bool); same pipeline and t-range convention */
 int rt_any_hit_host(rt_ctx* ctx, rt_scene* scene, int64_t n, const double* origins, const double* dirs,
-                    const double* t_min, const double* t_max, uint32_t ray_mask, uint8_t* hit,
-                    int32_t flags);
+                    const double* t_min, const double* t_max, double t_min_s, double t_max_s,
+                    uint32_t ray_mask, uint8_t* hit, int32_t flags);
 /* emissive triangles for pt-nee (scene.py:58-76): rows of 16 floats =
  * v0, v1, v2, unit normal, emission (3 each), area */
 int rt_scene_set_lights(rt_ctx* ctx, rt_scene* scene, int32_t n_lights, const float* rows);
@@ -190,10 +192,12 @@ void rt_tlas_destroy(rt_tlas* tlas);
  * outputs and conventions as rt_closest_hit_host / rt_any_hit_host (inst = instance
  * index, prim = primitive index in its BLAS) */
 int rt_tlas_closest_host(rt_ctx* ctx, rt_tlas* tlas, int64_t n, const double* origins, const double* dirs,
-                         const double* t_min, const double* t_max, uint32_t ray_mask, double* t, int64_t* inst,
-                         int64_t* prim, double* u, double* v, double* normal, int64_t* stats);
+                         const double* t_min, const double* t_max, double t_min_s, double t_max_s,
+                         uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u, double* v,
+                         double* normal, int64_t* stats);
 int rt_tlas_any_host(rt_ctx* ctx, rt_tlas* tlas, int64_t n, const double* origins, const double* dirs,
-                     const double* t_min, const double* t_max, uint32_t ray_mask, uint8_t* hit);
+                     const double* t_min, const double* t_max, double t_min_s, double t_max_s,
+                     uint32_t ray_mask, uint8_t* hit);
 
 #ifdef __cplusplus
 }

@@ -10,8 +10,11 @@ import ctypes
 import os
 import threading
 
+import numpy as np
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librt_b200.so")
+# RT_B200_LIB: an alternative build of the same library (tools/ variant sweeps only)
+LIB_PATH = os.environ.get("RT_B200_LIB") or os.path.join(_HERE, "librt_b200.so")
 
 RT_OK = 0
 RT_EINVAL = -1
@@ -67,6 +70,7 @@ def lib():
                               "(this package has no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         vp, i32, i64, u32, ci = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_int
+        f64 = ctypes.c_double
         L.rt_last_error.restype = ctypes.c_char_p
         L.rt_version.restype = ctypes.c_char_p
         sigs = {
@@ -81,10 +85,10 @@ def lib():
             "rt_bvh_info": [vp, vp, vp, vp, vp],
             "rt_bvh_download": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp],
             "rt_trace_closest": [vp, vp, i64, vp, vp, u32, vp, i32],
-            "rt_closest_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp, vp, i32],
+            "rt_closest_hit_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp, vp, vp, vp, vp, vp, vp, i32],
             "rt_render": [vp, vp, ctypes.POINTER(RenderParams), vp, vp],
             "rt_trace_any": [vp, vp, i64, vp, vp, u32, i32],
-            "rt_any_hit_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, i32],
+            "rt_any_hit_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp, i32],
             "rt_scene_set_lights": [vp, vp, i32, vp],
             "rt_scene_set_spheres": [vp, vp, i32, vp],
             "rt_raygen": [vp, ctypes.POINTER(RenderParams), i32, vp],
@@ -95,8 +99,8 @@ def lib():
             "rt_tlas_update": [vp, vp, vp, vp],
             "rt_tlas_set_custom_data": [vp, vp, i32, i64, vp],
             "rt_tlas_info": [vp, vp, vp, vp],
-            "rt_tlas_closest_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp, vp, vp, vp, vp, vp, vp],
-            "rt_tlas_any_host": [vp, vp, i64, vp, vp, vp, vp, u32, vp],
+            "rt_tlas_closest_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp, vp, vp, vp, vp, vp, vp],
+            "rt_tlas_any_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -125,6 +129,34 @@ def check(rc):
     if rc == RT_ENOMEM:
         raise MemoryError(msg)
     raise NativeError(f"librt_b200 error {rc}: {msg}")
+
+
+def host_empty(shape, dtype):
+    """Output array in PINNED host memory (PyTorch's caching host allocator reuses freed
+    blocks), so device->host copies into it run as full-rate async DMA."""
+    import torch
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64,
+           np.dtype(np.uint8): torch.uint8, np.dtype(np.float32): torch.float32,
+           np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+    if not torch.cuda.is_available():
+        return np.empty(shape, dtype)
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
+
+def host_pinned_copy(a):
+    """A pinned copy of a host array (for callers that reuse inputs across calls)."""
+    out = host_empty(a.shape, a.dtype)
+    np.copyto(out, a)
+    return out
+
+
+def t_range(t, n):
+    """(array pointer source or None, scalar) for a t_min / t_max argument: a scalar is
+    broadcast on the device instead of materialising an (n,) host array."""
+    a = np.asarray(t, dtype=np.float64)
+    if a.ndim == 0:
+        return None, float(a)
+    return np.ascontiguousarray(np.broadcast_to(a, (n,))), 0.0
 
 
 def ptr(x):

@@ -21,7 +21,7 @@ import math
 
 import numpy as np
 
-from ._native import RegistryError, check, lib, ptr
+from ._native import RegistryError, check, host_empty, lib, ptr, t_range
 
 FULL_MASK = 0xFFFFFFFF
 DEFAULT_MAX_T = 1e30
@@ -169,17 +169,18 @@ def closest_hit_batch(tlas, origins, dirs, t_min=0.0, t_max=DEFAULT_MAX_T, ray_m
     n = origins.shape[0]
     if dirs.shape[0] != n:
         raise ValueError("origins and dirs must have the same length")
-    tmin = np.ascontiguousarray(np.broadcast_to(np.asarray(t_min, dtype=np.float64), (n,)))
-    tmax = np.ascontiguousarray(np.broadcast_to(np.asarray(t_max, dtype=np.float64), (n,)))
-    t = np.empty(n)
-    inst = np.empty(n, np.int64)
-    prim = np.empty(n, np.int64)
-    u = np.empty(n)
-    v = np.empty(n)
-    nrm = np.empty((n, 3))
-    stats = np.empty((n, 2), np.int64) if with_stats else None
+    tmin, tmin_s = t_range(t_min, n)
+    tmax, tmax_s = t_range(t_max, n)
+    # outputs in pinned memory: the device->host copies are full-rate async DMA
+    t = host_empty(n, np.float64)
+    inst = host_empty(n, np.int64)
+    prim = host_empty(n, np.int64)
+    u = host_empty(n, np.float64)
+    v = host_empty(n, np.float64)
+    nrm = host_empty((n, 3), np.float64)
+    stats = host_empty((n, 2), np.int64) if with_stats else None
     _call(lib().rt_closest_hit_host, ray_type, tl.ctx.handle, tl.handle, n, ptr(origins), ptr(dirs), ptr(tmin),
-          ptr(tmax), mask, ptr(t), ptr(inst), ptr(prim), ptr(u), ptr(v), ptr(nrm), ptr(stats), flags)
+          ptr(tmax), tmin_s, tmax_s, mask, ptr(t), ptr(inst), ptr(prim), ptr(u), ptr(v), ptr(nrm), ptr(stats), flags)
     res = (t, inst, prim, u, v, nrm)
     return res + (stats,) if with_stats else res
 
@@ -197,12 +198,12 @@ def any_hit_batch(tlas, origins, dirs, t_min=0.0, t_max=DEFAULT_MAX_T, ray_mask:
     n = origins.shape[0]
     if dirs.shape[0] != n:
         raise ValueError("origins and dirs must have the same length")
-    tmin = np.ascontiguousarray(np.broadcast_to(np.asarray(t_min, dtype=np.float64), (n,)))
-    tmax = np.ascontiguousarray(np.broadcast_to(np.asarray(t_max, dtype=np.float64), (n,)))
-    out = np.zeros(n, np.uint8)
+    tmin, tmin_s = t_range(t_min, n)
+    tmax, tmax_s = t_range(t_max, n)
+    out = host_empty(n, np.uint8)
     _call(lib().rt_any_hit_host, ray_type, tl.ctx.handle, tl.handle, n, ptr(origins), ptr(dirs), ptr(tmin),
-          ptr(tmax), mask, ptr(out), flags)
-    return out.astype(bool)
+          ptr(tmax), tmin_s, tmax_s, mask, ptr(out), flags)
+    return out.view(bool)
 
 
 def trace_any(tlas, rays, hit, ray_mask: int = FULL_MASK, ray_type: int = 0, registry=None):

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "hostio.cuh"
 #include "rt_common.cuh"
 
 static thread_local char g_err[1024] = "";
@@ -84,6 +85,14 @@ void rt_ctx_destroy(rt_ctx* c) {
     cudaStreamSynchronize(c->stream);
     if (c->h_stage) cudaFreeHost(c->h_stage);
     if (c->d_stage) cudaFree(c->d_stage);
+    if (c->d_io) cudaFree(c->d_io);
+    if (c->io_in) {
+        cudaStreamSynchronize(c->io_in);
+        cudaStreamSynchronize(c->io_out);
+        cudaStreamDestroy(c->io_in);
+        cudaStreamDestroy(c->io_out);
+        for (int k = 0; k < 9; ++k) cudaEventDestroy(c->io_ev[k]);
+    }
     cudaFree(c->d_counter);
     cudaFree(c->d_error);
     cudaEventDestroy(c->ev0);
@@ -319,72 +328,43 @@ int rt_trace_closest(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, float
     return rt_trace_impl(c, s, n, rays, reinterpret_cast<float4*>(hits), ray_mask, stats, flags & RT_TRACE_NO_CUSTOM);
 }
 
-// accel.py:1128-1156 with the reference's host dtypes; rays are processed in
-// chunks through pinned staging: H2D(f64) -> pack -> trace -> expand -> D2H(f64)
+// accel.py:1128-1156 with the reference's host dtypes through the chunked
+// three-stream pipeline of hostio.cuh: H2D(f64) -> pack -> trace -> expand -> D2H(f64)
 int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const double* d, const double* tmin,
-                        const double* tmax, uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
-                        double* v, double* nrm, int64_t* stats, int32_t flags) {
+                        const double* tmax, double tmin_s, double tmax_s, uint32_t ray_mask, double* t,
+                        int64_t* inst, int64_t* prim, double* u, double* v, double* nrm, int64_t* stats,
+                        int32_t flags) {
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0, "negative ray count");
+    RT_CHECK_ARG(n == 0 || (o && d && t && inst && prim && u && v && nrm), "NULL ray or output buffer");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
     if (n == 0) return RT_OK;
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    const int64_t CH = std::min<int64_t>(n, 1 << 21);
-    // per ray: in 8*8 = 64 B (o, d, tmin, tmax), packed 32 B, hit 16 B, stats 8 B, out 64 B (+16 stats)
-    const size_t in_b = 64, out_b = 64 + 16;
-    size_t dev_need = (size_t)CH * (in_b + 32 + 16 + 8 + out_b);
-    if (c->d_stage_bytes < dev_need) {
-        if (c->d_stage) cudaFree(c->d_stage);
-        c->d_stage = nullptr;
-        c->d_stage_bytes = 0;
-        RT_CUDA_TRY(cudaMalloc(&c->d_stage, dev_need));
-        c->d_stage_bytes = dev_need;
-    }
-    char* D = (char*)c->d_stage;
-    double* d_o = (double*)D; D += 24 * CH;
-    double* d_d = (double*)D; D += 24 * CH;
-    double* d_tmin = (double*)D; D += 8 * CH;
-    double* d_tmax = (double*)D; D += 8 * CH;
-    float* d_rays = (float*)D; D += 32 * CH;
-    float4* d_hits = (float4*)D; D += 16 * CH;
-    uint32_t* d_stats = (uint32_t*)D; D += 8 * CH;
-    double* d_t = (double*)D; D += 8 * CH;
-    int64_t* d_inst = (int64_t*)D; D += 8 * CH;
-    int64_t* d_prim = (int64_t*)D; D += 8 * CH;
-    double* d_u = (double*)D; D += 8 * CH;
-    double* d_v = (double*)D; D += 8 * CH;
-    double* d_n = (double*)D; D += 24 * CH;
-    cudaStream_t st = c->stream;
-    std::vector<uint32_t> hstats;
-    if (stats) hstats.resize(2 * CH);
-    for (int64_t b = 0; b < n; b += CH) {
-        int64_t m = std::min(CH, n - b);
-        RT_CUDA_TRY(cudaMemcpyAsync(d_o, o + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_d, d + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_tmin, tmin + b, 8 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
-        int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
+    const HostIo in{o, d, tmin, tmax, tmin_s, tmax_s};
+    // hits: (t, id, u, v) 16 B + stats 8 B; out: t, inst, prim, u, v (8 B each), normal 24 B, stats 16 B
+    auto kernels = [&](const IoSlot& S, int64_t m) -> int {
+        float4* hits = (float4*)S.hits;
+        uint32_t* st = stats ? (uint32_t*)((char*)S.hits + 16 * m) : nullptr;
+        int rc = rt_trace_impl(c, s, m, S.rays, hits, ray_mask, st, flags & RT_TRACE_NO_CUSTOM);
         if (rc) return rc;
-        rc = rt_trace_impl(c, s, m, d_rays, d_hits, ray_mask, stats ? d_stats : nullptr, flags & RT_TRACE_NO_CUSTOM);
-        if (rc) return rc;
-        rc = rt_expand_hits_f64(c, s, m, d_hits, d_t, d_inst, d_prim, d_u, d_v, d_n, d_rays);
-        if (rc) return rc;
-        RT_CUDA_TRY(cudaMemcpyAsync(t + b, d_t, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(inst + b, d_inst, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(prim + b, d_prim, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(u + b, d_u, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(v + b, d_v, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(nrm + 3 * b, d_n, 24 * m, cudaMemcpyDeviceToHost, st));
-        if (stats) {
-            RT_CUDA_TRY(cudaMemcpyAsync(hstats.data(), d_stats, 8 * m, cudaMemcpyDeviceToHost, st));
-            RT_CUDA_TRY(cudaStreamSynchronize(st));
-            for (int64_t i = 0; i < m; ++i) {
-                stats[2 * (b + i)] = hstats[2 * i];
-                stats[2 * (b + i) + 1] = hstats[2 * i + 1];
-            }
-        }
-    }
-    RT_CUDA_TRY(cudaStreamSynchronize(st));
+        char* O = (char*)S.out;
+        return rt_expand_hits_f64(c, s, m, hits, (double*)O, (int64_t*)(O + 8 * m), (int64_t*)(O + 16 * m),
+                                  (double*)(O + 24 * m), (double*)(O + 32 * m), (double*)(O + 40 * m), S.rays, st,
+                                  (int64_t*)(O + 64 * m));
+    };
+    auto download = [&](const IoSlot& S, int64_t b, int64_t m, cudaStream_t so) -> int {
+        const char* O = (const char*)S.out;
+        RT_CUDA_TRY(cudaMemcpyAsync(t + b, O, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(inst + b, O + 8 * m, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(prim + b, O + 16 * m, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(u + b, O + 24 * m, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(v + b, O + 32 * m, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(nrm + 3 * b, O + 40 * m, 24 * m, cudaMemcpyDeviceToHost, so));
+        if (stats) RT_CUDA_TRY(cudaMemcpyAsync(stats + 2 * b, O + 64 * m, 16 * m, cudaMemcpyDeviceToHost, so));
+        return RT_OK;
+    };
+    int rc = rt_io_run(c, n, in, 24, 80, kernels, download);
+    if (rc) return rc;
     return rt_check_device_error(c);
 }
 
@@ -397,44 +377,26 @@ int rt_trace_any(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, uint8_t* 
     return rt_trace_any_impl(c, s, n, rays, hit, ray_mask, flags & RT_TRACE_NO_CUSTOM);
 }
 
-// accel.py:1159-1174 any_hit_batch with host float64 rays -> host bool (uint8)
+// accel.py:1159-1174 any_hit_batch with host float64 rays -> host bool (uint8), same pipeline
 int rt_any_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const double* d, const double* tmin,
-                    const double* tmax, uint32_t ray_mask, uint8_t* out, int32_t flags) {
+                    const double* tmax, double tmin_s, double tmax_s, uint32_t ray_mask, uint8_t* out,
+                    int32_t flags) {
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0, "negative ray count");
+    RT_CHECK_ARG(n == 0 || (o && d && out), "NULL ray or output buffer");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
     if (n == 0) return RT_OK;
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    const int64_t CH = std::min<int64_t>(n, 1 << 21);
-    size_t need = (size_t)CH * (64 + 32 + 1) + 256;
-    if (c->d_stage_bytes < need) {
-        if (c->d_stage) cudaFree(c->d_stage);
-        c->d_stage = nullptr;
-        c->d_stage_bytes = 0;
-        RT_CUDA_TRY(cudaMalloc(&c->d_stage, need));
-        c->d_stage_bytes = need;
-    }
-    char* D = (char*)c->d_stage;
-    double* d_o = (double*)D; D += 24 * CH;
-    double* d_d = (double*)D; D += 24 * CH;
-    double* d_tmin = (double*)D; D += 8 * CH;
-    double* d_tmax = (double*)D; D += 8 * CH;
-    float* d_rays = (float*)D; D += 32 * CH;
-    uint8_t* d_out = (uint8_t*)D;
-    cudaStream_t st = c->stream;
-    for (int64_t b = 0; b < n; b += CH) {
-        int64_t m = std::min(CH, n - b);
-        RT_CUDA_TRY(cudaMemcpyAsync(d_o, o + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_d, d + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_tmin, tmin + b, 8 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
-        int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
-        if (rc) return rc;
-        rc = rt_trace_any_impl(c, s, m, d_rays, d_out, ray_mask, flags & RT_TRACE_NO_CUSTOM);
-        if (rc) return rc;
-        RT_CUDA_TRY(cudaMemcpyAsync(out + b, d_out, m, cudaMemcpyDeviceToHost, st));
-    }
-    RT_CUDA_TRY(cudaStreamSynchronize(st));
+    const HostIo in{o, d, tmin, tmax, tmin_s, tmax_s};
+    auto kernels = [&](const IoSlot& S, int64_t m) -> int {
+        return rt_trace_any_impl(c, s, m, S.rays, (uint8_t*)S.out, ray_mask, flags & RT_TRACE_NO_CUSTOM);
+    };
+    auto download = [&](const IoSlot& S, int64_t b, int64_t m, cudaStream_t so) -> int {
+        RT_CUDA_TRY(cudaMemcpyAsync(out + b, S.out, m, cudaMemcpyDeviceToHost, so));
+        return RT_OK;
+    };
+    int rc = rt_io_run(c, n, in, 0, 1, kernels, download);
+    if (rc) return rc;
     return rt_check_device_error(c);
 }
 

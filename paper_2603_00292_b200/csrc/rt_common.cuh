@@ -27,6 +27,11 @@ struct rt_ctx {
     size_t d_stage_bytes;
     unsigned int* d_counter;       // persistent-kernel work counters (64 slots)
     int* d_error;                  // device-side error flag
+    // host-buffer transfer pipeline (hostio.cuh): copy-in / copy-out streams + events
+    cudaStream_t io_in, io_out;
+    cudaEvent_t io_ev[9];
+    void* d_io;
+    size_t d_io_bytes;
 };
 
 struct rt_scene {
@@ -186,7 +191,8 @@ int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4
 int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask,
                       int custom_mode);
 int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
-                       int64_t* prim, double* u, double* v, double* nrm, const float* rays);
+                       int64_t* prim, double* u, double* v, double* nrm, const float* rays,
+                       const uint32_t* st32 = nullptr, int64_t* st64 = nullptr);
 int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, const double* tmin,
                      const double* tmax, float* rays);
 int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out);

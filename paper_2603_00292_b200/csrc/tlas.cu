@@ -18,6 +18,7 @@
 #include <map>
 #include <vector>
 
+#include "hostio.cuh"
 #include "traverse.cuh"
 
 struct BlasDev {
@@ -242,10 +243,12 @@ __device__ __forceinline__ void world_normal_f64(const double* m, double lx, dou
 
 __global__ void tlas_expand_f64(int64_t n, const float4* __restrict__ hits, const float* __restrict__ rays,
                                 const InstDev* __restrict__ inst, const BlasDev* __restrict__ blas, double* t,
-                                int64_t* oinst, int64_t* oprim, double* u, double* v, double* nrm) {
+                                int64_t* oinst, int64_t* oprim, double* u, double* v, double* nrm,
+                                const uint32_t* __restrict__ st32, int64_t* __restrict__ st64) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float4 h0 = hits[2 * i], h1 = hits[2 * i + 1];
         const int ii = __float_as_int(h0.y), p = __float_as_int(h0.z);
+        if (st32) { st64[2 * i] = st32[2 * i]; st64[2 * i + 1] = st32[2 * i + 1]; }
         if (ii < 0) {
             t[i] = -1.0; oinst[i] = -1; oprim[i] = -1; u[i] = -1.0; v[i] = -1.0;
             nrm[3 * i] = nrm[3 * i + 1] = nrm[3 * i + 2] = 0.0;
@@ -475,135 +478,87 @@ int rt_tlas_info(rt_ctx* c, rt_tlas* T, float* root6, int32_t* height) {
     return rt_bvh_info(c, T->top, root6, height, nullptr);
 }
 
-// accel.py:1128-1156 closest_hit_batch over a two-level structure (host float64 rays)
+// accel.py:1128-1156 closest_hit_batch over a two-level structure (host float64 rays,
+// hostio.cuh pipeline)
 int rt_tlas_closest_host(rt_ctx* c, rt_tlas* T, int64_t n, const double* o, const double* d, const double* tmin,
-                         const double* tmax, uint32_t ray_mask, double* t, int64_t* inst, int64_t* prim, double* u,
-                         double* v, double* nrm, int64_t* stats) {
+                         const double* tmax, double tmin_s, double tmax_s, uint32_t ray_mask, double* t,
+                         int64_t* inst, int64_t* prim, double* u, double* v, double* nrm, int64_t* stats) {
     RT_CHECK_ARG(c && T, "NULL argument");
     RT_CHECK_ARG(n >= 0, "negative ray count");
+    RT_CHECK_ARG(n == 0 || (o && d && t && inst && prim && u && v && nrm), "NULL ray or output buffer");
     if (n == 0) return RT_OK;
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    const int64_t CH = std::min<int64_t>(n, 1 << 20);
-    double *d_o, *d_d, *d_tmin, *d_tmax, *d_t, *d_u, *d_v, *d_n;
-    int64_t *d_inst, *d_prim;
-    float* d_rays;
-    float4* d_hits;
-    uint32_t* d_stats;
-    size_t need = (size_t)CH * (24 + 24 + 8 + 8 + 32 + 32 + 8 + 8 + 8 + 8 + 8 + 8 + 24) + 1024;
-    if (c->d_stage_bytes < need) {
-        if (c->d_stage) cudaFree(c->d_stage);
-        c->d_stage = nullptr;
-        c->d_stage_bytes = 0;
-        RT_CUDA_TRY(cudaMalloc(&c->d_stage, need));
-        c->d_stage_bytes = need;
-    }
-    char* D = (char*)c->d_stage;
-    d_o = (double*)D; D += 24 * CH;
-    d_d = (double*)D; D += 24 * CH;
-    d_tmin = (double*)D; D += 8 * CH;
-    d_tmax = (double*)D; D += 8 * CH;
-    d_rays = (float*)D; D += 32 * CH;
-    d_hits = (float4*)D; D += 32 * CH;
-    d_stats = (uint32_t*)D; D += 8 * CH;
-    d_t = (double*)D; D += 8 * CH;
-    d_inst = (int64_t*)D; D += 8 * CH;
-    d_prim = (int64_t*)D; D += 8 * CH;
-    d_u = (double*)D; D += 8 * CH;
-    d_v = (double*)D; D += 8 * CH;
-    d_n = (double*)D; D += 24 * CH;
     TlasView V;
     tlas_view(c, T, V);
-    cudaStream_t st = c->stream;
-    std::vector<uint32_t> hs;
-    if (stats) hs.resize(2 * CH);
-    for (int64_t b = 0; b < n; b += CH) {
-        const int64_t m = std::min(CH, n - b);
-        RT_CUDA_TRY(cudaMemcpyAsync(d_o, o + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_d, d + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_tmin, tmin + b, 8 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
-        int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
-        if (rc) return rc;
-        RT_CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), st));
+    const HostIo in{o, d, tmin, tmax, tmin_s, tmax_s};
+    // hits: 2 float4 + stats u32 pair; out: t, inst, prim, u, v, normal, stats i64 pair
+    auto kernels = [&](const IoSlot& S, int64_t m) -> int {
+        float4* hits = (float4*)S.hits;
+        uint32_t* st = stats ? (uint32_t*)((char*)S.hits + 32 * m) : nullptr;
+        RT_CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), c->stream));
         int bps = 0;
         if (stats) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, tlas_closest_kernel<true>, TL_THREADS, 0);
         else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, tlas_closest_kernel<false>, TL_THREADS, 0);
         if (bps < 1) bps = 1;
         const int64_t grid = std::min<int64_t>((int64_t)c->num_sms * bps, (m + TL_THREADS - 1) / TL_THREADS);
         if (stats)
-            tlas_closest_kernel<true><<<(unsigned)grid, TL_THREADS, 0, st>>>(V, T->max_height, m, d_rays, d_hits,
-                                                                            ray_mask, d_stats, c->d_counter);
+            tlas_closest_kernel<true><<<(unsigned)grid, TL_THREADS, 0, c->stream>>>(
+                V, T->max_height, m, S.rays, hits, ray_mask, st, c->d_counter);
         else
-            tlas_closest_kernel<false><<<(unsigned)grid, TL_THREADS, 0, st>>>(V, T->max_height, m, d_rays, d_hits,
-                                                                             ray_mask, nullptr, c->d_counter);
+            tlas_closest_kernel<false><<<(unsigned)grid, TL_THREADS, 0, c->stream>>>(
+                V, T->max_height, m, S.rays, hits, ray_mask, nullptr, c->d_counter);
         RT_CUDA_TRY(cudaGetLastError());
-        tlas_expand_f64<<<c->num_sms * 4, 256, 0, st>>>(m, d_hits, d_rays, T->d_inst, T->d_blas, d_t, d_inst, d_prim,
-                                                        d_u, d_v, d_n);
+        char* O = (char*)S.out;
+        tlas_expand_f64<<<c->num_sms * 4, 256, 0, c->stream>>>(
+            m, hits, S.rays, T->d_inst, T->d_blas, (double*)O, (int64_t*)(O + 8 * m), (int64_t*)(O + 16 * m),
+            (double*)(O + 24 * m), (double*)(O + 32 * m), (double*)(O + 40 * m), st, (int64_t*)(O + 64 * m));
         RT_CUDA_TRY(cudaGetLastError());
-        RT_CUDA_TRY(cudaMemcpyAsync(t + b, d_t, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(inst + b, d_inst, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(prim + b, d_prim, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(u + b, d_u, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(v + b, d_v, 8 * m, cudaMemcpyDeviceToHost, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(nrm + 3 * b, d_n, 24 * m, cudaMemcpyDeviceToHost, st));
-        if (stats) {
-            RT_CUDA_TRY(cudaMemcpyAsync(hs.data(), d_stats, 8 * m, cudaMemcpyDeviceToHost, st));
-            RT_CUDA_TRY(cudaStreamSynchronize(st));
-            for (int64_t k = 0; k < m; ++k) {
-                stats[2 * (b + k)] = hs[2 * k];
-                stats[2 * (b + k) + 1] = hs[2 * k + 1];
-            }
-        }
-    }
-    RT_CUDA_TRY(cudaStreamSynchronize(st));
+        return RT_OK;
+    };
+    auto download = [&](const IoSlot& S, int64_t b, int64_t m, cudaStream_t so) -> int {
+        const char* O = (const char*)S.out;
+        RT_CUDA_TRY(cudaMemcpyAsync(t + b, O, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(inst + b, O + 8 * m, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(prim + b, O + 16 * m, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(u + b, O + 24 * m, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(v + b, O + 32 * m, 8 * m, cudaMemcpyDeviceToHost, so));
+        RT_CUDA_TRY(cudaMemcpyAsync(nrm + 3 * b, O + 40 * m, 24 * m, cudaMemcpyDeviceToHost, so));
+        if (stats) RT_CUDA_TRY(cudaMemcpyAsync(stats + 2 * b, O + 64 * m, 16 * m, cudaMemcpyDeviceToHost, so));
+        return RT_OK;
+    };
+    int rc = rt_io_run(c, n, in, 40, 80, kernels, download);
+    if (rc) return rc;
     return rt_check_device_error(c);
 }
 
 // accel.py:1159-1174 any_hit_batch over a two-level structure
 int rt_tlas_any_host(rt_ctx* c, rt_tlas* T, int64_t n, const double* o, const double* d, const double* tmin,
-                     const double* tmax, uint32_t ray_mask, uint8_t* out) {
+                     const double* tmax, double tmin_s, double tmax_s, uint32_t ray_mask, uint8_t* out) {
     RT_CHECK_ARG(c && T, "NULL argument");
     RT_CHECK_ARG(n >= 0, "negative ray count");
+    RT_CHECK_ARG(n == 0 || (o && d && out), "NULL ray or output buffer");
     if (n == 0) return RT_OK;
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    const int64_t CH = std::min<int64_t>(n, 1 << 20);
-    size_t need = (size_t)CH * (24 + 24 + 8 + 8 + 32 + 1) + 1024;
-    if (c->d_stage_bytes < need) {
-        if (c->d_stage) cudaFree(c->d_stage);
-        c->d_stage = nullptr;
-        c->d_stage_bytes = 0;
-        RT_CUDA_TRY(cudaMalloc(&c->d_stage, need));
-        c->d_stage_bytes = need;
-    }
-    char* D = (char*)c->d_stage;
-    double* d_o = (double*)D; D += 24 * CH;
-    double* d_d = (double*)D; D += 24 * CH;
-    double* d_tmin = (double*)D; D += 8 * CH;
-    double* d_tmax = (double*)D; D += 8 * CH;
-    float* d_rays = (float*)D; D += 32 * CH;
-    uint8_t* d_out = (uint8_t*)D;
     TlasView V;
     tlas_view(c, T, V);
-    cudaStream_t st = c->stream;
-    for (int64_t b = 0; b < n; b += CH) {
-        const int64_t m = std::min(CH, n - b);
-        RT_CUDA_TRY(cudaMemcpyAsync(d_o, o + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_d, d + 3 * b, 24 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_tmin, tmin + b, 8 * m, cudaMemcpyHostToDevice, st));
-        RT_CUDA_TRY(cudaMemcpyAsync(d_tmax, tmax + b, 8 * m, cudaMemcpyHostToDevice, st));
-        int rc = rt_pack_rays_f64(c, m, d_o, d_d, d_tmin, d_tmax, d_rays);
-        if (rc) return rc;
-        RT_CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), st));
+    const HostIo in{o, d, tmin, tmax, tmin_s, tmax_s};
+    auto kernels = [&](const IoSlot& S, int64_t m) -> int {
+        RT_CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned), c->stream));
         int bps = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, tlas_any_kernel, TL_THREADS, 0);
         if (bps < 1) bps = 1;
         const int64_t grid = std::min<int64_t>((int64_t)c->num_sms * bps, (m + TL_THREADS - 1) / TL_THREADS);
-        tlas_any_kernel<<<(unsigned)grid, TL_THREADS, 0, st>>>(V, T->max_height, m, d_rays, d_out, ray_mask,
-                                                               c->d_counter);
+        tlas_any_kernel<<<(unsigned)grid, TL_THREADS, 0, c->stream>>>(V, T->max_height, m, S.rays,
+                                                                      (uint8_t*)S.out, ray_mask, c->d_counter);
         RT_CUDA_TRY(cudaGetLastError());
-        RT_CUDA_TRY(cudaMemcpyAsync(out + b, d_out, m, cudaMemcpyDeviceToHost, st));
-    }
-    RT_CUDA_TRY(cudaStreamSynchronize(st));
+        return RT_OK;
+    };
+    auto download = [&](const IoSlot& S, int64_t b, int64_t m, cudaStream_t so) -> int {
+        RT_CUDA_TRY(cudaMemcpyAsync(out + b, S.out, m, cudaMemcpyDeviceToHost, so));
+        return RT_OK;
+    };
+    int rc = rt_io_run(c, n, in, 0, 1, kernels, download);
+    if (rc) return rc;
     return rt_check_device_error(c);
 }
 

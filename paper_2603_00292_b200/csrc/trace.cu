@@ -1,6 +1,7 @@
 // trace.cu -- K6: persistent-thread closest-hit kernel over a ray buffer, plus
 // the f64 <-> f32 packing kernels behind rt_closest_hit_host (the reference's
 // closest_hit_batch dtypes, accel.py:1128-1156).
+#include "hostio.cuh"
 #include "traverse.cuh"
 
 namespace {
@@ -69,12 +70,14 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_any_kernel(
     }
 }
 
+// float64 rays -> the fp32 trace layout; t ranges per ray (arrays) or broadcast (scalars)
 __global__ void pack_rays_f64(int64_t n, const double* __restrict__ o, const double* __restrict__ d,
-                              const double* __restrict__ tmin, const double* __restrict__ tmax,
-                              float4* __restrict__ rays) {
+                              const double* __restrict__ tmin, const double* __restrict__ tmax, double tmin_s,
+                              double tmax_s, float4* __restrict__ rays) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        rays[2 * i] = make_float4((float)o[3 * i], (float)o[3 * i + 1], (float)o[3 * i + 2], (float)tmin[i]);
-        double tm = tmax[i];
+        const double tn = tmin ? tmin[i] : tmin_s;
+        const double tm = tmax ? tmax[i] : tmax_s;
+        rays[2 * i] = make_float4((float)o[3 * i], (float)o[3 * i + 1], (float)o[3 * i + 2], (float)tn);
         rays[2 * i + 1] = make_float4((float)d[3 * i], (float)d[3 * i + 1], (float)d[3 * i + 2],
                                       tm > 3.0e38 ? INFINITY : (float)tm);
     }
@@ -86,7 +89,8 @@ __global__ void pack_rays_f64(int64_t n, const double* __restrict__ o, const dou
 __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, const float4* __restrict__ attr,
                                 const int32_t* __restrict__ tri_inst, const int32_t* __restrict__ tri_prim,
                                 double* t, int64_t* inst, int64_t* prim, double* u, double* v, double* nrm,
-                                const float* __restrict__ rays, const SphereView sv) {
+                                const float* __restrict__ rays, const SphereView sv,
+                                const uint32_t* __restrict__ st32, int64_t* __restrict__ st64) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float4 h = hits[i];
         int id = __float_as_int(h.y);
@@ -104,6 +108,7 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
             }
             nrm[3 * i] = a.x; nrm[3 * i + 1] = a.y; nrm[3 * i + 2] = a.z;
         }
+        if (st64) { st64[2 * i] = st32[2 * i]; st64[2 * i + 1] = st32[2 * i + 1]; }
     }
 }
 
@@ -164,16 +169,62 @@ int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, ui
 int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, const double* tmin,
                      const double* tmax, float* rays) {
     int grid = ctx->num_sms * 8;
-    pack_rays_f64<<<grid, 256, 0, ctx->stream>>>(n, o, d, tmin, tmax, reinterpret_cast<float4*>(rays));
+    pack_rays_f64<<<grid, 256, 0, ctx->stream>>>(n, o, d, tmin, tmax, 0.0, 0.0, reinterpret_cast<float4*>(rays));
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }
 
+int rt_pack_rays_io(rt_ctx* ctx, int64_t n, const IoSlot& s, bool per_ray_tmin, bool per_ray_tmax, double tmin_s,
+                    double tmax_s) {
+    int grid = ctx->num_sms * 8;
+    pack_rays_f64<<<grid, 256, 0, ctx->stream>>>(n, s.o, s.d, per_ray_tmin ? s.tmin : nullptr,
+                                                 per_ray_tmax ? s.tmax : nullptr, tmin_s, tmax_s,
+                                                 reinterpret_cast<float4*>(s.rays));
+    RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}
+
+int rt_io_streams(rt_ctx* c) {
+    if (c->io_in) return RT_OK;
+    RT_CUDA_TRY(cudaStreamCreateWithFlags(&c->io_in, cudaStreamNonBlocking));
+    RT_CUDA_TRY(cudaStreamCreateWithFlags(&c->io_out, cudaStreamNonBlocking));
+    for (int k = 0; k < 9; ++k) RT_CUDA_TRY(cudaEventCreateWithFlags(&c->io_ev[k], cudaEventDisableTiming));
+    return RT_OK;
+}
+
+int rt_io_ensure(rt_ctx* c, int64_t chunk, size_t hit_bytes, size_t out_bytes, IoSlot slots[2]) {
+    // per ray and slot: o 24, d 24, tmin 8, tmax 8, rays 32, hits, out (each region 256-B aligned)
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t m = (size_t)chunk;
+    const size_t per_slot = al(24 * m) * 2 + al(8 * m) * 2 + al(32 * m) + al(hit_bytes * m + 16) + al(out_bytes * m);
+    const size_t need = 2 * per_slot;
+    if (c->d_io_bytes < need) {
+        if (c->d_io) cudaFree(c->d_io);
+        c->d_io = nullptr;
+        c->d_io_bytes = 0;
+        RT_CUDA_TRY(cudaMalloc(&c->d_io, need));
+        c->d_io_bytes = need;
+    }
+    char* p = (char*)c->d_io;
+    for (int k = 0; k < 2; ++k) {
+        slots[k].o = (double*)p; p += al(24 * m);
+        slots[k].d = (double*)p; p += al(24 * m);
+        slots[k].tmin = (double*)p; p += al(8 * m);
+        slots[k].tmax = (double*)p; p += al(8 * m);
+        slots[k].rays = (float*)p; p += al(32 * m);
+        slots[k].hits = p; p += al(hit_bytes * m + 16);
+        slots[k].out = p; p += al(out_bytes * m);
+    }
+    return RT_OK;
+}
+
 int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
-                       int64_t* prim, double* u, double* v, double* nrm, const float* rays) {
+                       int64_t* prim, double* u, double* v, double* nrm, const float* rays, const uint32_t* st32,
+                       int64_t* st64) {
     int grid = ctx->num_sms * 8;
     expand_hits_f64<<<grid, 256, 0, ctx->stream>>>(n, hits, s->tri_attr, s->tri_inst, s->tri_prim, t, inst, prim,
-                                                    u, v, nrm, rays, rt_sphere_view(ctx, s, 0));
+                                                    u, v, nrm, rays, rt_sphere_view(ctx, s, 0), st32,
+                                                    st32 ? st64 : nullptr);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }

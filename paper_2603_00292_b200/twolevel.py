@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from ._native import BuildError, RegistryError, check, lib, ptr
+from ._native import BuildError, RegistryError, check, host_empty, lib, ptr, t_range
 from .accel import CUSTOM, SPHERE_GEOM_TYPE, TRIANGLES, _check_mask, registry_error, sphere_intersector
 from .frames import FULL_MASK, SrtFrame, frame_to_matrix, invert_affine
 
@@ -302,14 +302,14 @@ class Tlas:
         n = origins.shape[0]
         if dirs.shape[0] != n:
             raise ValueError("origins and dirs must have the same length")
-        tmin = np.ascontiguousarray(np.broadcast_to(np.asarray(t_min, dtype=np.float64), (n,)))
-        tmax = np.ascontiguousarray(np.broadcast_to(np.asarray(t_max, dtype=np.float64), (n,)))
-        t, u, v = np.empty(n), np.empty(n), np.empty(n)
-        inst, prim = np.empty(n, np.int64), np.empty(n, np.int64)
-        nrm = np.empty((n, 3))
-        stats = np.empty((n, 2), np.int64) if with_stats else None
-        self._query(lib().rt_tlas_closest_host, ray_type, n, ptr(origins), ptr(dirs), ptr(tmin), ptr(tmax), mask,
-                    ptr(t), ptr(inst), ptr(prim), ptr(u), ptr(v), ptr(nrm), ptr(stats))
+        tmin, tmin_s = t_range(t_min, n)
+        tmax, tmax_s = t_range(t_max, n)
+        t, u, v = host_empty(n, np.float64), host_empty(n, np.float64), host_empty(n, np.float64)
+        inst, prim = host_empty(n, np.int64), host_empty(n, np.int64)
+        nrm = host_empty((n, 3), np.float64)
+        stats = host_empty((n, 2), np.int64) if with_stats else None
+        self._query(lib().rt_tlas_closest_host, ray_type, n, ptr(origins), ptr(dirs), ptr(tmin), ptr(tmax), tmin_s,
+                    tmax_s, mask, ptr(t), ptr(inst), ptr(prim), ptr(u), ptr(v), ptr(nrm), ptr(stats))
         res = (t, inst, prim, u, v, nrm)
         return res + (stats,) if with_stats else res
 
@@ -321,12 +321,12 @@ class Tlas:
         n = origins.shape[0]
         if dirs.shape[0] != n:
             raise ValueError("origins and dirs must have the same length")
-        tmin = np.ascontiguousarray(np.broadcast_to(np.asarray(t_min, dtype=np.float64), (n,)))
-        tmax = np.ascontiguousarray(np.broadcast_to(np.asarray(t_max, dtype=np.float64), (n,)))
-        out = np.zeros(n, np.uint8)
-        self._query(lib().rt_tlas_any_host, ray_type, n, ptr(origins), ptr(dirs), ptr(tmin), ptr(tmax), mask,
-                    ptr(out))
-        return out.astype(bool)
+        tmin, tmin_s = t_range(t_min, n)
+        tmax, tmax_s = t_range(t_max, n)
+        out = host_empty(n, np.uint8)
+        self._query(lib().rt_tlas_any_host, ray_type, n, ptr(origins), ptr(dirs), ptr(tmin), ptr(tmax), tmin_s,
+                    tmax_s, mask, ptr(out))
+        return out.view(bool)
 
     def __del__(self):
         try:

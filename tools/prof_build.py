@@ -60,6 +60,21 @@ def main():
                 ts.append(e0.elapsed_time(e1))
             out["eye1080_ms_median"] = round(float(np.median(ts)), 4)
         del sc
+    if a.trace:
+        from paper_2603_00292_b200 import IntegratorConfig
+        cs = compile_scene(scenes.cornell_description(), "lbvh30", device=0)
+        W, H = 1920, 1080
+        accb = torch.zeros((H * W, 4), dtype=torch.float32, device="cuda")
+        cfg = IntegratorConfig(max_depth=5)
+        for kern in ("mega", "wavefront"):
+            render_into(cs, accb, W, H, 2, "pt", cfg=cfg, kernel=kern, count_rays=False)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            render_into(cs, accb, W, H, 8, "pt", cfg=cfg, kernel=kern, count_rays=False)
+            e1.record()
+            torch.cuda.synchronize()
+            out[f"pt1080x8spp_{kern}_ms"] = round(e0.elapsed_time(e1), 3)
     print(json.dumps(out, indent=1))
 
 
