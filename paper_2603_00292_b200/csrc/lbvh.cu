@@ -22,8 +22,21 @@
 namespace {
 
 constexpr int SORT_THREADS = 256;   // == RADIX
-constexpr int SORT_ITEMS = 8;
-constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;   // 4096 keys per tile
+#ifndef SORT_ITEMS32
+#define SORT_ITEMS32 8
+#endif
+#ifndef SORT_ITEMS64
+#define SORT_ITEMS64 8
+#endif
+#ifndef SORT_LB_WIN
+#define SORT_LB_WIN 16
+#endif
+// keys per thread / per tile of one onesweep pass (u32: 30-bit keys, u64: 63-bit keys)
+template <typename K> struct SortCfg {
+    static constexpr int ITEMS = sizeof(K) == 4 ? SORT_ITEMS32 : SORT_ITEMS64;
+    static constexpr int TILE = 256 * ITEMS;
+};
+constexpr int SORT_TILE_MIN = 256 * (SORT_ITEMS32 < SORT_ITEMS64 ? SORT_ITEMS32 : SORT_ITEMS64);
 constexpr int RADIX = 256;
 constexpr unsigned FLAG_AGG = 1u << 30;
 constexpr unsigned FLAG_INC = 2u << 30;
@@ -189,6 +202,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_pass_kernel(
     __shared__ unsigned int s_warp[SORT_THREADS / 32][RADIX];
     __shared__ unsigned int s_base[RADIX];
     __shared__ unsigned int s_texcl[RADIX];
+    constexpr int SORT_ITEMS = SortCfg<K>::ITEMS, SORT_TILE = SortCfg<K>::TILE;
     __shared__ K s_keys[SORT_TILE];
     __shared__ uint32_t s_vals[SORT_TILE];
     __shared__ unsigned int s_tile;
@@ -238,7 +252,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_pass_kernel(
         atomicExch(st, FLAG_AGG | tile_count);
         // windowed look-back: LB_WIN independent status loads per round instead of
         // one dependent L2 round trip per predecessor tile
-        constexpr int LB_WIN = 16;
+        constexpr int LB_WIN = SORT_LB_WIN;
         int j = (int)tile - 1;
         bool done = false;
         while (!done) {
@@ -347,7 +361,7 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     RT_CUDA_TRY(cudaMemsetAsync(s->cb_enc + 3, 0, 3 * sizeof(unsigned int), st));
     int gb = (int)((n + 255) / 256);
     if (gb > grid_stream) gb = grid_stream;
-    const int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+    const int64_t tiles = (n + SortCfg<K>::TILE - 1) / SortCfg<K>::TILE;
     unsigned int* hist = s->sort_scratch;                    // PASSES * 256
     unsigned int* counters = hist + PASSES * RADIX;          // PASSES
     unsigned int* status = counters + 32;                    // PASSES * tiles * 256
@@ -405,6 +419,6 @@ int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits) {
 }
 
 size_t rt_sort_scratch_words(int64_t n) {
-    int64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+    int64_t tiles = (n + SORT_TILE_MIN - 1) / SORT_TILE_MIN;
     return (size_t)8 * RADIX + 32 + (size_t)8 * tiles * RADIX;
 }

@@ -12,10 +12,18 @@
 #pragma once
 #include "rt_common.cuh"
 
+#ifndef RT_FMA_SLABS
+#define RT_FMA_SLABS 1
+#endif
+
 struct RayPre {
     float ox, oy, oz, tmin;
     float dx, dy, dz;          // only the sphere test reads these (dead code for triangle walks)
     float ix, iy, iz;          // safe 1/d
+#if RT_FMA_SLABS
+    float blx, bly, blz;       // slab plane bias of the lo / hi plane per axis: -o/d -+ e
+    float bhx, bhy, bhz;
+#endif
     // watertight shear: A' = M (v - o); rows of M
     float m00, m01, m02, m10, m11, m12, m20, m21, m22;
 };
@@ -30,6 +38,21 @@ __device__ __forceinline__ void ray_setup(RayPre& R, float ox, float oy, float o
     R.ox = ox; R.oy = oy; R.oz = oz; R.tmin = tmin;
     R.dx = dx; R.dy = dy; R.dz = dz;
     R.ix = safe_rcp(dx); R.iy = safe_rcp(dy); R.iz = safe_rcp(dz);
+#if RT_FMA_SLABS
+    {
+        // plane distance t = c * (1/d) + (-o/d): one FFMA per plane.  Its error is
+        // ~ulp(|o/d|) absolute (the rounded -o/d) + ~ulp(|t|) relative (the FFMA);
+        // the absolute part is absorbed PER AXIS by moving the near plane down and
+        // the far plane up by e = |o/d| * 2^-21 (a per-ray bound would disable all
+        // culling for near-axis rays), the relative part by the tfar widening below
+        const float ax = __fmul_rn(ox, R.ix), ay = __fmul_rn(oy, R.iy), az = __fmul_rn(oz, R.iz);
+        const float ex = fabsf(ax) * 0x1p-21f, ey = fabsf(ay) * 0x1p-21f, ez = fabsf(az) * 0x1p-21f;
+        // for 1/d > 0 the lo plane is the near one
+        R.blx = R.ix >= 0.f ? -ax - ex : -ax + ex;  R.bhx = R.ix >= 0.f ? -ax + ex : -ax - ex;
+        R.bly = R.iy >= 0.f ? -ay - ey : -ay + ey;  R.bhy = R.iy >= 0.f ? -ay + ey : -ay - ey;
+        R.blz = R.iz >= 0.f ? -az - ez : -az + ez;  R.bhz = R.iz >= 0.f ? -az + ez : -az - ez;
+    }
+#endif
     // kz = argmax |d|, kx = (kz+1)%3, ky = (kx+1)%3; swap kx,ky if d[kz] < 0
     float ax = fabsf(dx), ay = fabsf(dy), az = fabsf(dz);
     int kz = (ax > ay) ? (ax > az ? 0 : 2) : (ay > az ? 1 : 2);
@@ -62,9 +85,15 @@ __device__ __forceinline__ float box_enter(const RayPre& R, float lox, float hix
     // all culling for rays with a near-zero direction component -- measured:
     // 54K node fetches for such a ray on the 10M soup -- and bounding it per axis
     // costs as many instructions as this form.)
+#if RT_FMA_SLABS
+    float tx0 = __fmaf_rn(lox, R.ix, R.blx), tx1 = __fmaf_rn(hix, R.ix, R.bhx);
+    float ty0 = __fmaf_rn(loy, R.iy, R.bly), ty1 = __fmaf_rn(hiy, R.iy, R.bhy);
+    float tz0 = __fmaf_rn(loz, R.iz, R.blz), tz1 = __fmaf_rn(hiz, R.iz, R.bhz);
+#else
     float tx0 = __fmul_rn(__fsub_rn(lox, R.ox), R.ix), tx1 = __fmul_rn(__fsub_rn(hix, R.ox), R.ix);
     float ty0 = __fmul_rn(__fsub_rn(loy, R.oy), R.iy), ty1 = __fmul_rn(__fsub_rn(hiy, R.oy), R.iy);
     float tz0 = __fmul_rn(__fsub_rn(loz, R.oz), R.iz), tz1 = __fmul_rn(__fsub_rn(hiz, R.oz), R.iz);
+#endif
     float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), R.tmin));
     float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), tmax));
     tf = fmaf(tf, 1.0000008f, 1e-30f);
