@@ -50,6 +50,16 @@ WORKLOADS = {
 }
 
 
+def load_traffic(key, per=1.0):
+    """DRAM bytes per launch of a kernel from a committed ncu --set full capture
+    (profiles/ncu_traffic.json, written by tools/ncu_traffic.py), scaled to this launch."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)[key]["bytes"] * per
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -380,9 +390,14 @@ def run_ours(args, ws, rank, local):
     render_ms = t_render / K
     bpr = 128.0 * n_nodes + 48.0 * n_tests + 32.0
     rays_rank0 = my_rays
-    roof_trace = {"kernel": "pt_megakernel (raygen + while-while closest hit + shade, fused)", "bound": "hbm",
+    traffic_key = {2: ("config2_trace", 1.0), 3: ("config3_trace_1spp", samples[1] - samples[0]),
+                   5: ("config3_trace_1spp", samples[1] - samples[0]), 4: ("config4_trace", 1.0)}[C]
+    trace_traffic = load_traffic(traffic_key[0], traffic_key[1]) if traffic_key[1] else None
+    roof_trace = {"kernel": "pt_megakernel (raygen + persistent 4-wide BVH walk + shade, fused)", "bound": "hbm",
                   "achieved": bpr * rays_rank0 / (render_ms * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
-                  "traffic": None, "bytes_per_ray": bpr, "peak_source": peak_src,
+                  "traffic": trace_traffic, "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch, "
+                                                              "cold caches)",
+                  "bytes_per_ray": bpr, "peak_source": peak_src,
                   "bytes_formula": f"128 B x {n_nodes:.2f} BVH4 node fetches (4 child boxes + ids) + 48 B x {n_tests:.2f} triangle "
                                    f"tests + 32 B accumulation RMW per ray (node/test counts: stats build of the "
                                    f"trace kernel on this rank's primary rays{'' if C in (2, 4) else '; bounce rays assumed alike'})",
@@ -396,7 +411,10 @@ def run_ours(args, ws, rank, local):
         build_bytes = 328.0 * tl.n
         roof_build = {"kernel": "LBVH build (K1-K5: bounds, morton, onesweep x4, fused emit+refit)", "bound": "hbm",
                       "achieved": build_bytes / (build_ms * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
-                      "traffic": None, "bytes_formula": f"328 B/tri x {tl.n} tris (SURVEY 8(d), 30-bit keys)",
+                      "traffic": load_traffic("config2_build") if C == 2 else load_traffic("config4_build"),
+                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full of one build, each kernel "
+                                        "with cold caches)",
+                      "bytes_formula": f"328 B/tri x {tl.n} tris (SURVEY 8(d), 30-bit keys)",
                       "stage_ms": stages, "peak_source": peak_src}
         roof_build["frac"] = roof_build["achieved"] / peak_gbs
         if t_build > t_render:

@@ -161,7 +161,7 @@ int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normal
     ALLOC(s->tri_mask, sizeof(uint32_t) * n);
     ALLOC(s->mat_color, sizeof(float4) * n_mat);
     ALLOC(s->mat_emissive, sizeof(float4) * n_mat);
-    ALLOC(s->nodes, sizeof(float4) * 4 * ni);
+    ALLOC(s->nodes, sizeof(float4) * 4);          // root record (the binary view is derived on download)
     ALLOC(s->tri_sorted, sizeof(float4) * 3 * n);
     ALLOC(s->bvh4, sizeof(float4) * 8 * ni);
     ALLOC(s->keys_a, sizeof(uint64_t) * n);
@@ -290,19 +290,60 @@ int rt_bvh_download(rt_ctx* c, rt_scene* s, uint64_t* sorted_keys, uint32_t* ord
     int rc;
     if (sorted_keys && (rc = keys_to_u64(s->keys_a, sorted_keys))) return rc;
     if (order) RT_CUDA_TRY(cudaMemcpy(order, s->vals_a, 4 * n, cudaMemcpyDeviceToHost));
-    if (child) RT_CUDA_TRY(cudaMemcpy(child, s->child, 8 * (n - 1), cudaMemcpyDeviceToHost));
-    if (parent) RT_CUDA_TRY(cudaMemcpy(parent, s->parent, 4 * (2 * n - 1), cudaMemcpyDeviceToHost));
-    if (boxes || heights) {
-        std::vector<float4> nd(4 * (n - 1));
-        RT_CUDA_TRY(cudaMemcpy(nd.data(), s->nodes, sizeof(float4) * 4 * (n - 1), cudaMemcpyDeviceToHost));
-        for (int64_t i = 0; i < n - 1; ++i) {
-            const float4 *q = &nd[4 * i];
-            if (boxes) {
-                float* b = boxes + 12 * i;
-                b[0] = q[0].x; b[1] = q[0].z; b[2] = q[2].x; b[3] = q[0].y; b[4] = q[0].w; b[5] = q[2].y;
-                b[6] = q[1].x; b[7] = q[1].z; b[8] = q[2].z; b[9] = q[1].y; b[10] = q[1].w; b[11] = q[2].w;
+    if (child || parent || boxes || heights) {
+        // the build writes only child ids + the BVH4 halves + the root record; the
+        // binary view is derived here: node P's child boxes are the half its parent Q
+        // wrote into BVH4[split of Q] (side = P is Q's right child), the root's are in
+        // the root record; heights bottom-up; parents by inverting child
+        const int64_t m = n - 1;
+        std::vector<int2> ch(m);
+        RT_CUDA_TRY(cudaMemcpy(ch.data(), s->child, 8 * m, cudaMemcpyDeviceToHost));
+        if (child) memcpy(child, ch.data(), 8 * m);
+        std::vector<int32_t> par(2 * n - 1, -1);
+        for (int64_t p = 0; p < m; ++p) {
+            const int cl = ch[p].x, cr = ch[p].y;
+            par[cl < 0 ? m + ~cl : cl] = (int32_t)p;
+            par[cr < 0 ? m + ~cr : cr] = (int32_t)p;
+        }
+        if (parent) memcpy(parent, par.data(), 4 * (2 * n - 1));
+        if (boxes) {
+            std::vector<float4> b4(8 * m), root(4);
+            RT_CUDA_TRY(cudaMemcpy(b4.data(), s->bvh4, sizeof(float4) * 8 * m, cudaMemcpyDeviceToHost));
+            RT_CUDA_TRY(cudaMemcpy(root.data(), s->nodes, sizeof(float4) * 4, cudaMemcpyDeviceToHost));
+            for (int64_t p = 0; p < m; ++p) {
+                float* b = boxes + 12 * p;
+                if (p == 0) {
+                    const float4* q = root.data();
+                    b[0] = q[0].x; b[1] = q[0].z; b[2] = q[2].x; b[3] = q[0].y; b[4] = q[0].w; b[5] = q[2].y;
+                    b[6] = q[1].x; b[7] = q[1].z; b[8] = q[2].z; b[9] = q[1].y; b[10] = q[1].w; b[11] = q[2].w;
+                    continue;
+                }
+                const int q = par[p];
+                const int side = ch[q].y == (int)p ? 1 : 0;
+                const int gq = ch[q].x < 0 ? ~ch[q].x : ch[q].x;       // split of Q = right end of its left child
+                const float4* h = &b4[8 * (int64_t)gq + 4 * side];
+                b[0] = h[0].x; b[1] = h[0].y; b[2] = h[0].z; b[3] = h[1].x; b[4] = h[1].y; b[5] = h[1].z;
+                b[6] = h[2].x; b[7] = h[2].y; b[8] = h[2].z; b[9] = h[3].x; b[10] = h[3].y; b[11] = h[3].z;
             }
-            if (heights) memcpy(heights + i, &q[3].z, 4);
+        }
+        if (heights) {
+            // subtree heights in reverse breadth-first order (children before parents)
+            std::vector<int64_t> bfs;
+            bfs.reserve(m);
+            bfs.push_back(0);
+            for (size_t k = 0; k < bfs.size(); ++k) {
+                const int2 c2 = ch[bfs[k]];
+                if (c2.x >= 0) bfs.push_back(c2.x);
+                if (c2.y >= 0) bfs.push_back(c2.y);
+            }
+            std::vector<int32_t> hh(m, 0);
+            for (size_t k = bfs.size(); k-- > 0;) {
+                const int64_t p = bfs[k];
+                const int2 c2 = ch[p];
+                const int a = c2.x >= 0 ? hh[c2.x] : 0, bb = c2.y >= 0 ? hh[c2.y] : 0;
+                hh[p] = 1 + (a > bb ? a : bb);
+            }
+            memcpy(heights, hh.data(), 4 * m);
         }
     }
     if (cbounds || inv_ext) {

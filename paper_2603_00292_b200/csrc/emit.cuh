@@ -84,18 +84,19 @@ __device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child,
     const bool pleft = pdr > pdl;
     const int P = root ? 0 : (pleft ? pr : pl);
     N.h = 1 + (N.h > hs ? N.h : hs);
-    float4* nd = nodes + 4 * P;
-    nd[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
-    nd[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
-    nd[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
-    // binary root: n3.w carries the BVH4 root index (the root's split position)
-    nd[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(N.h),
-                        __int_as_float(root ? gamma : 0));
+    // Only the topology (child ids, 8 B) and the BVH4 half are written per node: the
+    // binary node's child boxes ARE that half, so parent pointers, per-node boxes and
+    // heights are derived from child + bvh4 by rt_bvh_download (parity only).  The
+    // root alone writes its 64-B record (child boxes, ids, tree height, BVH4 root).
     child[P] = make_int2(cl, cr);
-    parent[cl < 0 ? (n - 1) + ~cl : cl] = P;
-    parent[cr < 0 ? (n - 1) + ~cr : cr] = P;
-    if (root) parent[0] = -1;
-    else bvh4_write_half(bvh4, pleft ? pr : pl - 1, pleft ? 0 : 1, llo, lhi, gl, rlo, rhi, gr);
+    if (root) {
+        nodes[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
+        nodes[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
+        nodes[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
+        nodes[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(N.h), __int_as_float(gamma));
+    } else {
+        bvh4_write_half(bvh4, pleft ? pr : pl - 1, pleft ? 0 : 1, llo, lhi, gl, rlo, rhi, gr);
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) { N.lo[a] = sel_min(llo[a], rlo[a]); N.hi[a] = sel_max(lhi[a], rhi[a]); }
     N.l = pl; N.r = pr; N.dl = pdl; N.dr = pdr; N.g = gamma;
