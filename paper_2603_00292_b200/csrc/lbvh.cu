@@ -217,19 +217,30 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_pass_kernel(
     uint32_t val[SORT_ITEMS];
     unsigned rank[SORT_ITEMS];
     const unsigned lt_mask = (1u << lane) - 1u;
+    // all loads, then all warp matches (independent, so their latencies overlap),
+    // then the per-digit warp counters in item order (stable ranks)
+    unsigned dig[SORT_ITEMS], peers[SORT_ITEMS];
 #pragma unroll
     for (int i = 0; i < SORT_ITEMS; ++i) {
         int64_t idx = seg + i * 32 + lane;
         bool ok = idx < n;
         key[i] = ok ? keys_in[idx] : (K)0;
         val[i] = ok ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;
-        unsigned d = ok ? ((unsigned)(key[i] >> shift) & 0xFFu) : 0x100u;
-        unsigned peers = __match_any_sync(RT_FULL, d);
-        unsigned below = __popc(peers & lt_mask);
+    }
+#pragma unroll
+    for (int i = 0; i < SORT_ITEMS; ++i) {
+        const bool ok = seg + i * 32 + lane < n;
+        dig[i] = ok ? ((unsigned)(key[i] >> shift) & 0xFFu) : 0x100u;
+        peers[i] = __match_any_sync(RT_FULL, dig[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < SORT_ITEMS; ++i) {
+        const bool ok = dig[i] < 0x100u;
+        const unsigned below = __popc(peers[i] & lt_mask);
         unsigned base = 0;
-        if (ok) base = s_warp[warp][d];
+        if (ok) base = s_warp[warp][dig[i]];
         __syncwarp();
-        if (ok && below == 0) s_warp[warp][d] = base + __popc(peers);
+        if (ok && below == 0) s_warp[warp][dig[i]] = base + __popc(peers[i]);
         __syncwarp();
         rank[i] = base + below;
     }

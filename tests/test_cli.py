@@ -104,3 +104,19 @@ def test_resolve_device_matches_host(native):
         assert np.array_equal(resolve_device(sc, acc, 40, 30, gamma), resolve(host, gamma))
     with pytest.raises(ValueError, match="zero samples"):
         resolve_device(sc, torch.zeros((4, 4), device="cuda"), 2, 2)
+
+
+@pytest.mark.gpu
+def test_render_frame_multi_replicas_sum(native):
+    """--gpus N logic on one device: two replicas split the samples, partial sums add up
+    to the single-replica frame (fp32 addition order differs only at rounding level)."""
+    from paper_2603_00292_b200 import IntegratorConfig, compile_scene, render_frame
+    from paper_2603_00292_b200.distributed import render_frame_multi
+    desc = scenes.cornell_description()
+    reps = [compile_scene(desc), compile_scene(desc)]
+    cfg = IntegratorConfig(max_depth=5)
+    acc2, rays2 = render_frame_multi(reps, 40, 30, 6, "pt", cfg=cfg)
+    acc1, st = render_frame(reps[0], 40, 30, 6, "pt", cfg=cfg, return_stats=True)
+    assert rays2 == st["rays"]
+    assert np.array_equal(acc2.data[:, :, 3], acc1.data[:, :, 3])
+    assert np.allclose(acc2.data, acc1.data, rtol=1e-5, atol=1e-5)

@@ -7,7 +7,8 @@ from paper_2603_00292_b200 import compile_scene, scenes  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 bits = int(sys.argv[2]) if len(sys.argv) > 2 else 30
-sc = compile_scene(scenes.sphere_description(), "lbvh30", device=0)
+desc = scenes.soup_description() if len(sys.argv) > 3 and sys.argv[3] == "soup" else scenes.sphere_description()
+sc = compile_scene(desc, "lbvh30", device=0)
 for _ in range(reps):
     sc.tlas.build(bits)
 sc.tlas.ctx.sync()
