@@ -141,7 +141,8 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
                                                            int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
                                                            float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
                                                            float4* __restrict__ bvh4, EmitNode* __restrict__ items,
-                                                           unsigned int* __restrict__ item_count) {
+                                                           unsigned int* __restrict__ item_count,
+                                                           int* __restrict__ slot_range) {
     __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
     __shared__ int s_delta[EMIT_T + 1];         // delta(B - 1 + k)
     __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, -)]
@@ -227,8 +228,12 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         M.dl = s_delta[M.l - (int)B];
         M.dr = s_delta[M.r - (int)B + 1];
         items[s_base + atomicAdd(&s_next, 1u)] = M;
+        if (M.r < n - 1) slot_range[M.r] = -1;       // the global climb's slots: item right ends
     }
-    if (tid < s_ndef) items[s_base + n_single + tid] = s_def[tid];
+    if (tid < s_ndef) {
+        items[s_base + n_single + tid] = s_def[tid];
+        if (s_def[tid].r < n - 1) slot_range[s_def[tid].r] = -1;
+    }
 }
 
 // Phase B as its own persistent kernel: the few boundary-crossing nodes of all

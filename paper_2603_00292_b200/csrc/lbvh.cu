@@ -111,19 +111,28 @@ __global__ void __launch_bounds__(TRI_CHUNK) lbvh_bounds_kernel(const float* __r
         int a = threadIdx.x;
         float v = s[0][a];
         for (int k = 1; k < (int)(blockDim.x >> 5); ++k) v = (a < 3) ? sel_min(v, s[k][a]) : sel_max(v, s[k][a]);
-        if (a < 3) atomicMin(cb_enc + a, f2ord(v));
+        // both accumulators start at 0 (one memset with the sort scratch): the min
+        // slots hold max(~ord(v)), since ~ord is order-reversing
+        if (a < 3) atomicMax(cb_enc + a, ~f2ord(v));
         else atomicMax(cb_enc + a, f2ord(v));
     }
 }
 
-__global__ void lbvh_bounds_finish(const unsigned int* __restrict__ cb_enc, float* __restrict__ cb) {
-    int a = threadIdx.x;
-    if (a < 3) {
-        float lo = ord2f(cb_enc[a]), hi = ord2f(cb_enc[3 + a]);
-        cb[a] = lo;
-        cb[3 + a] = hi;
-        float ext = __fsub_rn(hi, lo);
-        cb[6 + a] = ext > 0.0f ? __fdiv_rn(1.0f, ext) : 0.0f;
+// centroid bounds and inverse extents from the accumulators (each Morton block
+// computes them; block 0 also stores them for rt_bvh_download)
+__device__ __forceinline__ void bounds_from_enc(const unsigned int* __restrict__ cb_enc, float lo[3], float inv[3],
+                                                float* __restrict__ cb) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float l = ord2f(~__ldg(cb_enc + a)), h = ord2f(__ldg(cb_enc + 3 + a));
+        const float ext = __fsub_rn(h, l);
+        lo[a] = l;
+        inv[a] = ext > 0.0f ? __fdiv_rn(1.0f, ext) : 0.0f;
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            cb[a] = l;
+            cb[3 + a] = h;
+            cb[6 + a] = inv[a];
+        }
     }
 }
 
@@ -150,15 +159,15 @@ __device__ __forceinline__ uint64_t expand21(uint64_t v) {
 // registers here, so the histogram costs no extra read of the key array)
 template <typename K, int B, int PASSES>
 __global__ void __launch_bounds__(TRI_CHUNK) lbvh_morton_kernel(const float* __restrict__ tris, int64_t n,
-                                                               const float* __restrict__ cb, K* __restrict__ keys,
+                                                               const unsigned int* __restrict__ cb_enc,
+                                                               float* __restrict__ cb, K* __restrict__ keys,
                                                                unsigned int* __restrict__ hist) {
     __shared__ unsigned int s_hist[PASSES][256];
     __shared__ __align__(16) float s_tri[9 * TRI_CHUNK];
     for (int i = threadIdx.x; i < PASSES * 256; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     const float scale = (float)(1u << B), qmax = (float)((1u << B) - 1u);
     float lo[3], inv[3];
-#pragma unroll
-    for (int a = 0; a < 3; ++a) { lo[a] = __ldg(cb + a); inv[a] = __ldg(cb + 6 + a); }
+    bounds_from_enc(cb_enc, lo, inv, cb);
     for (int64_t base = blockIdx.x * (int64_t)TRI_CHUNK; base < n; base += (int64_t)gridDim.x * TRI_CHUNK) {
         const int cnt = stage_tris(tris, base, n, s_tri);
         __syncthreads();
@@ -366,26 +375,26 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     const int64_t n = s->n;
     cudaStream_t st = ctx->stream;
     const int grid_stream = ctx->num_sms * 8;
-    // K1
-    // orderable-uint accumulators: min slots start at 0xFFFFFFFF, max slots at 0
-    RT_CUDA_TRY(cudaMemsetAsync(s->cb_enc, 0xFF, 3 * sizeof(unsigned int), st));
-    RT_CUDA_TRY(cudaMemsetAsync(s->cb_enc + 3, 0, 3 * sizeof(unsigned int), st));
+    // one memset zeroes the sort scratch: digit histograms, tile counters, the
+    // centroid-bound accumulators, the emit item count and the look-back status
     int gb = (int)((n + 255) / 256);
     if (gb > grid_stream) gb = grid_stream;
     const int64_t tiles = (n + SortCfg<K>::TILE - 1) / SortCfg<K>::TILE;
     unsigned int* hist = s->sort_scratch;                    // PASSES * 256
-    unsigned int* counters = hist + PASSES * RADIX;          // PASSES
+    unsigned int* counters = hist + PASSES * RADIX;          // [0, 8) tile counters, [8, 14) cb_enc, [16] emit count
+    unsigned int* cb_enc = counters + 8;
+    unsigned int* emit_count = counters + 16;
     unsigned int* status = counters + 32;                    // PASSES * tiles * 256
     size_t words = (size_t)PASSES * RADIX + 32 + (size_t)PASSES * tiles * RADIX;
     RT_PROF(ctx, 0);
     RT_CUDA_TRY(cudaMemsetAsync(s->sort_scratch, 0, words * sizeof(unsigned int), st));
-    lbvh_bounds_kernel<<<gb, 256, 0, st>>>(s->tris, n, s->cb_enc);
-    lbvh_bounds_finish<<<1, 32, 0, st>>>(s->cb_enc, s->cbounds);
+    // K1
+    lbvh_bounds_kernel<<<gb, 256, 0, st>>>(s->tris, n, cb_enc);
     // K2
     K* ka = (K*)s->keys_a;
     K* kb = (K*)s->keys_b;
     RT_PROF(ctx, 1);
-    lbvh_morton_kernel<K, B, PASSES><<<gb, 256, 0, st>>>(s->tris, n, s->cbounds, ka, hist);
+    lbvh_morton_kernel<K, B, PASSES><<<gb, 256, 0, st>>>(s->tris, n, cb_enc, s->cbounds, ka, hist);
     RT_PROF(ctx, 2);
     // K3 (digit histograms already accumulated by K2)
     K* kin = ka; K* kout = kb;
@@ -401,15 +410,14 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     // PASSES is even: sorted keys in keys_a, values in vals_a
     // K4 + K5
     RT_PROF(ctx, 4);
-    RT_CUDA_TRY(cudaMemsetAsync(s->flags, 0xFF, sizeof(int) * (n - 1), st));   // split slots: empty
-    RT_CUDA_TRY(cudaMemsetAsync(s->emit_count, 0, sizeof(unsigned int), st));
+    // (the global split slots are reset by the emit kernel at its hand-off boundaries)
     RT_PROF(ctx, 5);
     EmitNode* items = (EmitNode*)s->emit_items;
     lbvh_emit_kernel<K><<<(unsigned)((n + EMIT_T - 1) / EMIT_T), EMIT_T, 0, st>>>(
         kin, vin, s->tris, s->tri_mask, n, s->child, s->parent, s->tri_sorted, s->nodes, s->bvh4, items,
-        s->emit_count);
+        emit_count, (int*)s->flags);
     lbvh_emit_global_kernel<K><<<(unsigned)(ctx->num_sms * 4), 128, 0, st>>>(
-        kin, n, s->child, s->parent, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box, items, s->emit_count);
+        kin, n, s->child, s->parent, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box, items, emit_count);
     RT_PROF(ctx, 6);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
