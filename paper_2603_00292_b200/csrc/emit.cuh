@@ -103,6 +103,20 @@ __device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child,
     return root;
 }
 
+// Global rendezvous without a release fence: a fence.gpu before the exchange would wait
+// for every earlier store of the thread (the previous level's node writes) to reach L2,
+// on each level of the chain.  Instead the box halves carry validity tags in .w
+// (height >= 0, split g >= -1; both sides' tags are invalidated by the emit kernel's
+// hand-off before this kernel runs), the exchange is relaxed, and the second arrival
+// spins on the L2 copy of its sibling's box until both tags are valid.
+constexpr int SLOT_INVALID = (int)0x80000000;
+
+__device__ __forceinline__ float4 ld_box_valid(const float4* p) {
+    float4 v;
+    do { v = __ldcg(p); } while (__float_as_int(v.w) == SLOT_INVALID);
+    return v;
+}
+
 template <typename K>
 __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __restrict__ child,
                              int32_t* __restrict__ parent, float4* __restrict__ nodes, float4* __restrict__ bvh4,
@@ -113,15 +127,23 @@ __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __rest
         const int side = left ? 0 : 1;
         __stcg(slot_box + 4 * gamma + 2 * side, make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h)));
         __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g)));
-        cuda::atomic_ref<int, cuda::thread_scope_device> slot(slot_range[gamma]);
-        const int other = slot.exchange(left ? N.l : N.r, cuda::std::memory_order_release);
+        const int other = atomicExch(slot_range + gamma, left ? N.l : N.r);
         if (other < 0) return;                       // sibling subtree not finished
-        const float4 s0 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side));
-        const float4 s1 = __ldcg(slot_box + 4 * gamma + 2 * (1 - side) + 1);
         const int pl = left ? N.l : other, pr = left ? other : N.r;
-        const int pdl = adj_delta(keys, n, pl - 1), pdr = adj_delta(keys, n, pr);
+        // one boundary delta of the parent is this node's own
+        const int pdl = left ? N.dl : adj_delta(keys, n, pl - 1);
+        const int pdr = left ? adj_delta(keys, n, pr) : N.dr;
+        const float4 s0 = ld_box_valid(slot_box + 4 * gamma + 2 * (1 - side));
+        const float4 s1 = ld_box_valid(slot_box + 4 * gamma + 2 * (1 - side) + 1);
         if (emit_parent(n, child, parent, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s0, s1)) return;
     }
+}
+
+// invalidate both sides' box tags of a global split slot (emit hand-off)
+__device__ __forceinline__ void slot_reset(int* slot_range, float4* slot_box, int gamma) {
+    slot_range[gamma] = -1;
+    int* b = reinterpret_cast<int*>(slot_box + 4 * (int64_t)gamma);
+    b[3] = SLOT_INVALID; b[7] = SLOT_INVALID; b[11] = SLOT_INVALID; b[15] = SLOT_INVALID;
 }
 
 // n == 1: the BVH4 root (index 0) holds the single leaf; the other slots are empty
@@ -142,7 +164,7 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
                                                            float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
                                                            float4* __restrict__ bvh4, EmitNode* __restrict__ items,
                                                            unsigned int* __restrict__ item_count,
-                                                           int* __restrict__ slot_range) {
+                                                           int* __restrict__ slot_range, float4* __restrict__ slot_box) {
     __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
     __shared__ int s_delta[EMIT_T + 1];         // delta(B - 1 + k)
     __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, -)]
@@ -228,11 +250,11 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         M.dl = s_delta[M.l - (int)B];
         M.dr = s_delta[M.r - (int)B + 1];
         items[s_base + atomicAdd(&s_next, 1u)] = M;
-        if (M.r < n - 1) slot_range[M.r] = -1;       // the global climb's slots: item right ends
+        if (M.r < n - 1) slot_reset(slot_range, slot_box, M.r);   // the global climb's slots: item right ends
     }
     if (tid < s_ndef) {
         items[s_base + n_single + tid] = s_def[tid];
-        if (s_def[tid].r < n - 1) slot_range[s_def[tid].r] = -1;
+        if (s_def[tid].r < n - 1) slot_reset(slot_range, slot_box, s_def[tid].r);
     }
 }
 
