@@ -187,6 +187,18 @@ int rt_tlas_update(rt_ctx* ctx, rt_tlas* tlas, const double* inv12, const float*
  * then reaches such a primitive fails with RT_EUNSUPPORTED) */
 int rt_tlas_set_custom_data(rt_ctx* ctx, rt_tlas* tlas, int32_t geom_type, int64_t n_rows, const double* rows4);
 int rt_tlas_info(rt_ctx* ctx, rt_tlas* tlas, float* root6, int32_t* height);
+/* Flatten on the device into a single-level scene for rendering (the flat LBVH path of
+ * rt_render): triangle instances are transformed by a kernel (float64, the host
+ * flatten's order; reference-style normals from the BLAS float64 local normals), in
+ * (instance, prim) order, so every triangle instance must precede the custom ones; the
+ * n_custom custom primitives (spheres) are appended from host rows: world boxes as
+ * (lo, hi, lo) (n_custom, 9) fp32, rt_scene_set_spheres rows, instance and prim ids.
+ * mat12 (n_inst, 12) float64 instance matrices; inst_material (n_inst).  *io == NULL
+ * creates the scene; otherwise a scene of the same size is refilled and rebuilt. */
+int rt_tlas_flatten(rt_ctx* ctx, rt_tlas* tlas, const double* mat12, const int32_t* inst_material,
+                    const float* mat_color, const float* mat_emissive, int32_t n_mat, int32_t n_custom,
+                    const float* custom_boxes9, const double* custom_rows16, const int32_t* custom_inst,
+                    const int32_t* custom_prim, int32_t bits, rt_scene** io);
 void rt_tlas_destroy(rt_tlas* tlas);
 /* closest_hit_batch / any_hit_batch over the two-level structure, host float64 rays,
  * outputs and conventions as rt_closest_hit_host / rt_any_hit_host (inst = instance

@@ -99,6 +99,7 @@ def lib():
             "rt_tlas_update": [vp, vp, vp, vp],
             "rt_tlas_set_custom_data": [vp, vp, i32, i64, vp],
             "rt_tlas_info": [vp, vp, vp, vp],
+            "rt_tlas_flatten": [vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, i32, vp],
             "rt_tlas_closest_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp, vp, vp, vp, vp, vp, vp],
             "rt_tlas_any_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp],
         }

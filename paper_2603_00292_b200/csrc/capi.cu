@@ -114,37 +114,18 @@ int rt_ctx_sync(rt_ctx* c) {
     return rt_check_device_error(c);
 }
 
-int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normals, const int32_t* tri_inst,
-                    const int32_t* tri_prim, const uint32_t* tri_mask, const int32_t* tri_material,
-                    const float* mat_color, const float* mat_emissive, int32_t n_mat, rt_scene** out) {
+// device allocations of a scene of n primitives and n_mat materials (contents unset)
+int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
     RT_CHECK_ARG(c && out, "ctx/out is NULL");
     RT_CHECK_ARG(n >= 1, "cannot build over zero primitives");
     RT_CHECK_ARG(n < (1ll << 30), "at most 2^30 - 1 triangles per scene");
-    RT_CHECK_ARG(tris && normals && tri_inst && tri_prim && tri_mask && tri_material, "NULL triangle array");
-    RT_CHECK_ARG(n_mat >= 1 && mat_color && mat_emissive, "materials missing");
-    for (int64_t i = 0; i < n; ++i)
-        if (tri_material[i] < 0 || tri_material[i] >= n_mat) {
-            rt_set_error("triangle %lld references material %d of %d", (long long)i, tri_material[i], n_mat);
-            return RT_EINVAL;
-        }
+    RT_CHECK_ARG(n_mat >= 1, "materials missing");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     rt_scene* s = new rt_scene();
     memset(s, 0, sizeof *s);
     s->n = n;
     s->n_mat = n_mat;
     const int64_t ni = n > 1 ? n - 1 : 1;
-    std::vector<float4> attr(n), mc(n_mat), me(n_mat);
-    for (int64_t i = 0; i < n; ++i) {
-        float4 a;
-        a.x = normals[3 * i]; a.y = normals[3 * i + 1]; a.z = normals[3 * i + 2];
-        int m = tri_material[i];
-        memcpy(&a.w, &m, 4);
-        attr[i] = a;
-    }
-    for (int k = 0; k < n_mat; ++k) {
-        mc[k] = make_float4(mat_color[3 * k], mat_color[3 * k + 1], mat_color[3 * k + 2], 0.f);
-        me[k] = make_float4(mat_emissive[3 * k], mat_emissive[3 * k + 1], mat_emissive[3 * k + 2], 0.f);
-    }
 #define ALLOC(ptr, bytes)                                                       \
     do {                                                                        \
         cudaError_t _e = cudaMalloc((void**)&(ptr), (bytes));                   \
@@ -168,26 +149,68 @@ int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normal
     ALLOC(s->keys_b, sizeof(uint64_t) * n);
     ALLOC(s->vals_a, sizeof(uint32_t) * n);
     ALLOC(s->vals_b, sizeof(uint32_t) * n);
-    ALLOC(s->parent, sizeof(int32_t) * (2 * n - 1));
     ALLOC(s->child, sizeof(int2) * ni);
     ALLOC(s->flags, sizeof(unsigned int) * ni);
     ALLOC(s->cbounds, sizeof(float) * 16);
-    ALLOC(s->cb_enc, sizeof(unsigned int) * 8);
     s->sort_scratch_words = rt_sort_scratch_words(n);
     ALLOC(s->sort_scratch, sizeof(unsigned int) * s->sort_scratch_words);
     ALLOC(s->leaf_box, sizeof(float4) * 4 * n);   // per split slot: (lo, h), hi for both sides
     ALLOC(s->emit_items, 48 * (2 * n + 2));        // EmitNode; every item is a distinct tree node
-    ALLOC(s->emit_count, 16);
 #undef ALLOC
+    *out = s;
+    return RT_OK;
+}
+
+int rt_scene_set_materials(rt_ctx* c, rt_scene* s, const float* mat_color, const float* mat_emissive) {
+    std::vector<float4> mc(s->n_mat), me(s->n_mat);
+    for (int k = 0; k < s->n_mat; ++k) {
+        mc[k] = make_float4(mat_color[3 * k], mat_color[3 * k + 1], mat_color[3 * k + 2], 0.f);
+        me[k] = make_float4(mat_emissive[3 * k], mat_emissive[3 * k + 1], mat_emissive[3 * k + 2], 0.f);
+    }
+    RT_CUDA_TRY(cudaMemcpy(s->mat_color, mc.data(), sizeof(float4) * s->n_mat, cudaMemcpyHostToDevice));
+    RT_CUDA_TRY(cudaMemcpy(s->mat_emissive, me.data(), sizeof(float4) * s->n_mat, cudaMemcpyHostToDevice));
+    return RT_OK;
+}
+
+int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normals, const int32_t* tri_inst,
+                    const int32_t* tri_prim, const uint32_t* tri_mask, const int32_t* tri_material,
+                    const float* mat_color, const float* mat_emissive, int32_t n_mat, rt_scene** out) {
+    RT_CHECK_ARG(c && out, "ctx/out is NULL");
+    RT_CHECK_ARG(n >= 1, "cannot build over zero primitives");
+    RT_CHECK_ARG(tris && normals && tri_inst && tri_prim && tri_mask && tri_material, "NULL triangle array");
+    RT_CHECK_ARG(n_mat >= 1 && mat_color && mat_emissive, "materials missing");
+    for (int64_t i = 0; i < n; ++i)
+        if (tri_material[i] < 0 || tri_material[i] >= n_mat) {
+            rt_set_error("triangle %lld references material %d of %d", (long long)i, tri_material[i], n_mat);
+            return RT_EINVAL;
+        }
+    rt_scene* s = nullptr;
+    int rc = rt_scene_alloc(c, n, n_mat, &s);
+    if (rc) return rc;
+    std::vector<float4> attr(n);
+    for (int64_t i = 0; i < n; ++i) {
+        float4 a;
+        a.x = normals[3 * i]; a.y = normals[3 * i + 1]; a.z = normals[3 * i + 2];
+        int m = tri_material[i];
+        memcpy(&a.w, &m, 4);
+        attr[i] = a;
+    }
     cudaStream_t st = c->stream;
-    RT_CUDA_TRY(cudaMemcpyAsync(s->tris, tris, sizeof(float) * 9 * n, cudaMemcpyHostToDevice, st));
-    RT_CUDA_TRY(cudaMemcpyAsync(s->tri_attr, attr.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, st));
-    RT_CUDA_TRY(cudaMemcpyAsync(s->tri_inst, tri_inst, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
-    RT_CUDA_TRY(cudaMemcpyAsync(s->tri_prim, tri_prim, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st));
-    RT_CUDA_TRY(cudaMemcpyAsync(s->tri_mask, tri_mask, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
-    RT_CUDA_TRY(cudaMemcpyAsync(s->mat_color, mc.data(), sizeof(float4) * n_mat, cudaMemcpyHostToDevice, st));
-    RT_CUDA_TRY(cudaMemcpyAsync(s->mat_emissive, me.data(), sizeof(float4) * n_mat, cudaMemcpyHostToDevice, st));
-    RT_CUDA_TRY(cudaStreamSynchronize(st));   // host vectors go out of scope
+    auto fail = [&](cudaError_t e) {
+        rt_set_error("upload failed: %s", cudaGetErrorString(e));
+        rt_scene_destroy(s);
+        return RT_ECUDA;
+    };
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(s->tris, tris, sizeof(float) * 9 * n, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(s->tri_attr, attr.data(), sizeof(float4) * n, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(s->tri_inst, tri_inst, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(s->tri_prim, tri_prim, sizeof(int32_t) * n, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaMemcpyAsync(s->tri_mask, tri_mask, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st)) ||
+        (e = cudaStreamSynchronize(st)))   // host vectors go out of scope
+        return fail(e);
+    rc = rt_scene_set_materials(c, s, mat_color, mat_emissive);
+    if (rc) { rt_scene_destroy(s); return rc; }
     *out = s;
     return RT_OK;
 }
@@ -204,9 +227,9 @@ void rt_scene_destroy(rt_scene* s) {
     if (!s) return;
     rt_render_release(s);
     void* ptrs[] = {s->tris, s->tri_attr, s->tri_inst, s->tri_prim, s->tri_mask, s->mat_color, s->mat_emissive,
-                    s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->parent, s->child,
-                    s->flags, s->cbounds, s->cb_enc, s->sort_scratch, s->leaf_box, s->emit_items,
-                    s->emit_count, s->lights, s->spheres, s->lnormal64};
+                    s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->child,
+                    s->flags, s->cbounds, s->sort_scratch, s->leaf_box, s->emit_items, s->lights, s->spheres,
+                    s->lnormal64};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;

@@ -54,18 +54,18 @@ struct rt_scene {
     // build scratch
     void* keys_a; void* keys_b;     // u32 or u64 Morton keys
     uint32_t* vals_a; uint32_t* vals_b;
-    int32_t* parent;                // (2n-1)
+    int32_t* parent;                // unused (parents are derived on download)
     int2* child;                    // (n-1)
     unsigned int* flags;            // (n-1) refit arrival counters
     float* cbounds;                 // 6 floats + 3 inv_ext (+pad)
-    unsigned int* cb_enc;           // 6 orderable-uint accumulators
+    unsigned int* cb_enc;           // unused (the accumulators live in sort_scratch)
     unsigned int* sort_scratch;     // hist + counters + look-back status
     size_t sort_scratch_words;
     float4* leaf_box;               // global split-slot boxes (4 float4 per split)
     float4* lights;                 // (n_lights, 5): (v0, area), v1, v2, normal, emission
     int n_lights;
     void* emit_items;               // boundary-crossing nodes handed from emit phase A to phase B
-    unsigned int* emit_count;
+    unsigned int* emit_count;       // unused (in sort_scratch)
     // custom primitives: the last n_spheres flat primitives are spheres
     double* spheres;                // (n_spheres, 16): inverse 3x4, center, radius
     int n_spheres;
@@ -100,6 +100,9 @@ void rt_set_error(const char* fmt, ...);
 
 // reads and clears the device error flag (synchronises the context stream)
 int rt_check_device_error(rt_ctx* ctx);
+// scene storage for n primitives (contents unset) / material table upload
+extern "C" int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out);
+extern "C" int rt_scene_set_materials(rt_ctx* c, rt_scene* s, const float* mat_color, const float* mat_emissive);
 
 // --------------------------------------------------------------------------
 // exact fp32 helpers (parity-critical paths use explicit selects, no FMNMX

@@ -274,6 +274,53 @@ __global__ void tlas_expand_f64(int64_t n, const float4* __restrict__ hits, cons
     }
 }
 
+// ---- device flatten (render a two-level scene through the flat LBVH path) ----
+struct FlatInst {
+    double m[12];             // instance matrix (world <- local), frame_to_matrix
+    double inv[12];           // its inverse (normals, accel.py:843-847)
+    const float* ltris;       // BLAS local vertices in prim order, (n_b, 9) fp32
+    const double* lnormal;    // BLAS float64 local normals
+    int64_t off;              // first flat id
+    int inst;                 // instance index
+    uint32_t mask;
+    int material;
+    int pad;
+};
+
+__device__ __forceinline__ double madd3(const double* r, double x, double y, double z, double t) {
+    return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(r[0], x), __dmul_rn(r[1], y)), __dmul_rn(r[2], z)), t);
+}
+
+// one thread per flat triangle: world vertices (float64 in the host flatten's order,
+// rounded to fp32), the reference-style world normal, ids, mask, material
+__global__ void flatten_tris_kernel(const FlatInst* __restrict__ fi, int n_fi, int64_t n_tri, float* __restrict__ tris,
+                                    float4* __restrict__ attr, int32_t* __restrict__ tinst,
+                                    int32_t* __restrict__ tprim, uint32_t* __restrict__ tmask) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n_tri; k += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = n_fi - 1;                    // last instance with off <= k
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (fi[mid].off <= k) lo = mid; else hi = mid - 1;
+        }
+        const FlatInst& F = fi[lo];
+        const int64_t p = k - F.off;
+        const float* v = F.ltris + 9 * p;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double x = v[3 * j], y = v[3 * j + 1], z = v[3 * j + 2];
+            tris[9 * k + 3 * j + 0] = (float)madd3(F.m + 0, x, y, z, F.m[3]);
+            tris[9 * k + 3 * j + 1] = (float)madd3(F.m + 4, x, y, z, F.m[7]);
+            tris[9 * k + 3 * j + 2] = (float)madd3(F.m + 8, x, y, z, F.m[11]);
+        }
+        double wn[3];
+        world_normal_f64(F.inv, F.lnormal[3 * p], F.lnormal[3 * p + 1], F.lnormal[3 * p + 2], wn);
+        attr[k] = make_float4((float)wn[0], (float)wn[1], (float)wn[2], __int_as_float(F.material));
+        tinst[k] = F.inst;
+        tprim[k] = (int32_t)p;
+        tmask[k] = F.mask;
+    }
+}
+
 int tlas_view(rt_ctx* c, rt_tlas* T, TlasView& V) {
     V.tbvh4 = T->top->bvh4;
     V.ttris = T->top->tri_sorted;
@@ -471,6 +518,106 @@ void rt_tlas_destroy(rt_tlas* T) {
     for (double* p : T->d_data)
         if (p) cudaFree(p);
     delete T;
+}
+
+// Flat single-level scene from a two-level one, built on the device: the triangle
+// instances (all before any custom instance, so flat ids stay in (instance, prim)
+// order) are transformed by flatten_tris_kernel; custom primitives are appended from
+// host rows like compile_scene's spheres.  *io: NULL -> a new scene; else a scene of
+// the same size is refilled in place (after refits / frame edits).  Built with LBVH-bits.
+int rt_tlas_flatten(rt_ctx* c, rt_tlas* T, const double* mat12, const int32_t* inst_material, const float* mat_color,
+                    const float* mat_emissive, int32_t n_mat, int32_t n_custom, const float* custom_boxes9,
+                    const double* custom_rows16, const int32_t* custom_inst, const int32_t* custom_prim,
+                    int32_t bits, rt_scene** io) {
+    RT_CHECK_ARG(c && T && mat12 && inst_material && mat_color && mat_emissive && io, "NULL argument");
+    RT_CHECK_ARG(n_custom >= 0 && (n_custom == 0 || (custom_boxes9 && custom_rows16 && custom_inst && custom_prim)),
+                 "bad custom primitive rows");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    std::vector<FlatInst> fi;
+    int64_t n_tri = 0;
+    bool seen_custom = false;
+    for (int i = 0; i < T->n_inst; ++i) {
+        rt_scene* b = T->blas[T->inst_blas[i]];
+        if (b->custom) { seen_custom = true; continue; }
+        if (seen_custom) {
+            rt_set_error("flatten needs every triangle instance before the custom-primitive instances");
+            return RT_EINVAL;
+        }
+        RT_CHECK_ARG(inst_material[i] >= 0 && inst_material[i] < n_mat, "instance material out of range");
+        FlatInst f;
+        for (int k = 0; k < 12; ++k) { f.m[k] = mat12[12 * i + k]; f.inv[k] = T->hinst[i].inv64[k]; }
+        f.ltris = b->tris;
+        f.lnormal = b->lnormal64;
+        f.off = n_tri;
+        f.inst = i;
+        f.mask = T->hinst[i].mask;
+        f.material = inst_material[i];
+        f.pad = 0;
+        fi.push_back(f);
+        n_tri += b->n;
+    }
+    const int64_t n = n_tri + n_custom;
+    RT_CHECK_ARG(n >= 1, "cannot build over zero primitives");
+    rt_scene* s = *io;
+    if (s && (s->n != n || s->n_mat != n_mat)) {
+        rt_set_error("flatten target has %lld primitives / %d materials, need %lld / %d", (long long)s->n, s->n_mat,
+                     (long long)n, n_mat);
+        return RT_EINVAL;
+    }
+    const bool fresh = s == nullptr;
+    if (fresh) {
+        int rc = rt_scene_alloc(c, n, n_mat, &s);
+        if (rc) return rc;
+    }
+    auto bail = [&](int rc) { if (fresh) rt_scene_destroy(s); return rc; };
+    FlatInst* d_fi = nullptr;
+    cudaError_t e = cudaSuccess;
+    if (!fi.empty()) {
+        if ((e = cudaMalloc(&d_fi, sizeof(FlatInst) * fi.size())) ||
+            (e = cudaMemcpy(d_fi, fi.data(), sizeof(FlatInst) * fi.size(), cudaMemcpyHostToDevice))) {
+            if (d_fi) cudaFree(d_fi);
+            rt_set_error("flatten upload: %s", cudaGetErrorString(e));
+            return bail(RT_ECUDA);
+        }
+        flatten_tris_kernel<<<c->num_sms * 8, 256, 0, c->stream>>>(d_fi, (int)fi.size(), n_tri, s->tris, s->tri_attr,
+                                                                    s->tri_inst, s->tri_prim, s->tri_mask);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess && n_custom) {
+        std::vector<float4> attr(n_custom);
+        std::vector<uint32_t> mk(n_custom);
+        for (int k = 0; k < n_custom; ++k) {
+            const int i = custom_inst[k];
+            float mf;
+            memcpy(&mf, &inst_material[i], 4);
+            attr[k] = make_float4(0.f, 0.f, 0.f, mf);
+            mk[k] = T->hinst[i].mask;
+        }
+        cudaStream_t st = c->stream;
+        if (!(e = cudaMemcpyAsync(s->tris + 9 * n_tri, custom_boxes9, sizeof(float) * 9 * n_custom,
+                                  cudaMemcpyHostToDevice, st)) &&
+            !(e = cudaMemcpyAsync(s->tri_attr + n_tri, attr.data(), sizeof(float4) * n_custom, cudaMemcpyHostToDevice,
+                                  st)) &&
+            !(e = cudaMemcpyAsync(s->tri_inst + n_tri, custom_inst, 4 * n_custom, cudaMemcpyHostToDevice, st)) &&
+            !(e = cudaMemcpyAsync(s->tri_prim + n_tri, custom_prim, 4 * n_custom, cudaMemcpyHostToDevice, st)) &&
+            !(e = cudaMemcpyAsync(s->tri_mask + n_tri, mk.data(), 4 * n_custom, cudaMemcpyHostToDevice, st)))
+            e = cudaStreamSynchronize(st);
+    }
+    if (d_fi) {
+        cudaError_t e2 = cudaStreamSynchronize(c->stream);
+        cudaFree(d_fi);
+        if (e == cudaSuccess) e = e2;
+    }
+    if (e != cudaSuccess) {
+        rt_set_error("flatten: %s", cudaGetErrorString(e));
+        return bail(RT_ECUDA);
+    }
+    int rc = rt_scene_set_materials(c, s, mat_color, mat_emissive);
+    if (!rc) rc = rt_scene_set_spheres(c, s, n_custom, n_custom ? custom_rows16 : nullptr);
+    if (!rc) rc = rt_bvh_build(c, s, bits, nullptr);
+    if (rc) return bail(rc);
+    *io = s;
+    return RT_OK;
 }
 
 int rt_tlas_info(rt_ctx* c, rt_tlas* T, float* root6, int32_t* height) {

@@ -101,8 +101,8 @@ def render_into(scene, accum, width, height, spp=1, integrator="pt", seed=0, cfg
     if bands is not None:
         p.band_stride, p.band_offset = int(bands[0]), int(bands[1])
     rays = np.zeros(1, np.uint64)
-    check(lib().rt_render(scene.tlas.ctx.handle, scene.tlas.handle, p, ptr(accum),
-                          ptr(rays) if count_rays else None))
+    flat = getattr(scene, "render_tlas", None) or scene.tlas   # two-level scenes render their device flatten
+    check(lib().rt_render(flat.ctx.handle, flat.handle, p, ptr(accum), ptr(rays) if count_rays else None))
     return int(rays[0]) if count_rays else None
 
 

@@ -100,6 +100,19 @@ class GpuTlas:
         self.tris = tris
         self.build(bits)
 
+    @classmethod
+    def from_handle(cls, ctx, handle, n, bits, sphere_rows=None):
+        """Wrap a scene built on the device (rt_tlas_flatten); host geometry copies absent."""
+        self = cls.__new__(cls)
+        self.ctx, self.handle, self.n, self.bits = ctx, handle, int(n), bits
+        self.tris = self.normals = self.tri_inst = self.tri_prim = self.tri_mask = self.tri_material = None
+        self.inverses = self.n_instances = None
+        self.world_root = (None, None)
+        self.build_ms = None
+        self.sphere_rows = np.zeros((0, 16)) if sphere_rows is None else sphere_rows
+        self.n_spheres = int(self.sphere_rows.shape[0])
+        return self
+
     def build_profiled(self, bits=None):
         """Rebuild with stage events; returns dict of device ms per stage."""
         bits = self.bits if bits is None else bits
@@ -150,6 +163,7 @@ class Scene:
     sky: np.ndarray
     background: np.ndarray
     root_box: tuple
+    render_tlas: object = None   # two-level scenes: the device-flattened structure rt_render walks
 
     def diagonal(self) -> float:
         d = self.root_box[1] - self.root_box[0]
@@ -203,8 +217,16 @@ def _light_rows(desc, mats_index, inst_list):
                       col(4).reshape(-1, 3), col(5), col(6).astype(np.int64), col(7).astype(np.int64))
 
 
-def compile_scene(desc, quality: str = "lbvh30", device: int = 0) -> Scene:
-    """Flatten + upload + LBVH build (scene.py:79-141 semantics, GPU backend)."""
+def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: bool = False) -> Scene:
+    """Flatten + upload + LBVH build (scene.py:79-141 semantics, GPU backend).
+
+    two_level=True builds the reference's structure instead -- one device Blas per mesh
+    (and per sphere), a Tlas over the instances -- so queries run the two-level kernels;
+    rendering walks a flattened copy made on the device from that Tlas."""
+    if quality not in QUALITIES:
+        raise ValueError(f"unknown build quality {quality!r}, expected one of {tuple(QUALITIES)}")
+    if two_level:
+        return _compile_two_level(desc, quality, device)
     if quality not in QUALITIES:
         raise ValueError(f"unknown build quality {quality!r}, expected one of {tuple(QUALITIES)}")
     mat_names = list(desc.materials)
@@ -319,3 +341,44 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0) -> Scene:
                  sky=np.ascontiguousarray(desc.sky, np.float64), background=np.ascontiguousarray(desc.background,
                                                                                                  np.float64),
                  root_box=(root_lo, root_hi))
+
+
+def _compile_two_level(desc, quality, device):
+    """compile_scene through Blas / Instance / Tlas (scene.py:85-117), plus the device flatten."""
+    from .twolevel import Blas, Instance, Tlas
+    from .accel import sphere_aabbs
+    if not desc.instances and not desc.spheres:
+        raise BuildError("a scene needs at least one instance")
+    mat_names = list(desc.materials)
+    mat_index = {n: i for i, n in enumerate(mat_names)}
+    mat_color = np.array([desc.materials[n].color for n in mat_names]).reshape(-1, 3)
+    mat_emissive = np.array([desc.materials[n].emissive for n in mat_names]).reshape(-1, 3)
+    blases, blas_of_mesh, instances, inst_material, inst_list = [], {}, [], [], []
+    for name, mesh in desc.meshes.items():
+        blas_of_mesh[name] = len(blases)
+        blases.append(Blas.from_mesh(mesh.vertices, mesh.faces, quality, device=device))
+    for decl in desc.instances:
+        instances.append(Instance(blas_of_mesh[decl.mesh], decl.frame, decl.mask))
+        inst_material.append(mat_index[decl.material])
+        inst_list.append((decl, frame_to_matrix(decl.frame)))
+    registry = IntersectorRegistry()
+    if desc.spheres:
+        rows = np.array([[*sph.center, sph.radius] for sph in desc.spheres], dtype=np.float64)
+        registry.register(SPHERE_GEOM_TYPE, 0, sphere_intersector, sphere_data(rows))
+        for i, sph in enumerate(desc.spheres):
+            instances.append(Instance(len(blases), sph.frame, sph.mask))
+            blases.append(Blas.from_aabbs(sphere_aabbs(rows[i:i + 1]), SPHERE_GEOM_TYPE, quality, data_offset=i,
+                                          device=device))
+            inst_material.append(mat_index[sph.material])
+    tlas = Tlas(instances, blases, quality)
+    flat = tlas.flatten(np.array(inst_material, np.int32), mat_color, mat_emissive, registry, QUALITIES[quality])
+    lights = _light_rows(desc, mat_index, inst_list)
+    if len(lights):
+        rows = np.ascontiguousarray(np.concatenate([lights.v0, lights.v1, lights.v2, lights.normal, lights.emissive,
+                                                    lights.area[:, None]], axis=1), np.float32)
+        check(lib().rt_scene_set_lights(flat.ctx.handle, flat.handle, rows.shape[0], ptr(rows)))
+    return Scene(camera=desc.camera, tlas=tlas, registry=registry, mat_color=mat_color, mat_emissive=mat_emissive,
+                 inst_material=np.array(inst_material, np.int64), lights=lights,
+                 sky=np.ascontiguousarray(desc.sky, np.float64),
+                 background=np.ascontiguousarray(desc.background, np.float64), root_box=tlas.root_box,
+                 render_tlas=flat)

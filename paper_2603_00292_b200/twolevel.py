@@ -287,6 +287,51 @@ class Tlas:
                                                 ptr(data)))
             self._bound[g] = key
 
+    def flatten(self, inst_material, mat_color, mat_emissive, registry=None, bits=30, into=None):
+        """Single-level copy of this scene made on the device, for rendering (rt_render walks
+        the flat LBVH): triangle instances transformed by a kernel, custom primitives
+        (spheres of the registry's data) appended.  ``into``: a previous flatten to refill."""
+        from .scene import GpuTlas
+        if [b.version for b in self.blases] != self._versions:
+            raise RuntimeError("a blas was refit since the last Tlas.refresh_instance_bounds()")
+        n_inst = len(self.instances)
+        inst_material = np.ascontiguousarray(inst_material, np.int32).reshape(n_inst)
+        mc = np.ascontiguousarray(mat_color, np.float32).reshape(-1, 3)
+        me = np.ascontiguousarray(mat_emissive, np.float32).reshape(-1, 3)
+        boxes, rows, cinst, cprim = [], [], [], []
+        for i, inst in enumerate(self.instances):
+            b = self.blases[inst.blas_id]
+            if b.kind != CUSTOM:
+                continue
+            e = registry.entry(b.geom_type, 0) if registry is not None else None
+            if e is None or e[0] is not sphere_intersector:
+                raise RegistryError(f"no GPU intersector registered for geometry type {b.geom_type} (ray type 0)")
+            data = np.asarray(e[1], np.float64).reshape(-1, 4)
+            m = self.matrices[i]
+            for p in range(b.prim_count):
+                lo, hi = b.aabbs[p, :3], b.aabbs[p, 3:]
+                corners = np.array([[(lo, hi)[s & 1][0], (lo, hi)[(s >> 1) & 1][1], (lo, hi)[(s >> 2) & 1][2]]
+                                    for s in range(8)])
+                pts = corners @ m[:, :3].T + m[:, 3]
+                w_lo, w_hi = _outward_f32(pts.min(axis=0), pts.max(axis=0))
+                boxes.append(np.concatenate([w_lo, w_hi, w_lo]))
+                rows.append(np.concatenate([self.inverses[i].reshape(12), data[b.data_offset + p]]))
+                cinst.append(i)
+                cprim.append(p)
+        nc = len(rows)
+        boxes = np.ascontiguousarray(np.array(boxes, np.float32).reshape(nc, 9)) if nc else None
+        rows = np.ascontiguousarray(np.array(rows, np.float64).reshape(nc, 16)) if nc else None
+        cinst = np.ascontiguousarray(np.array(cinst, np.int32)) if nc else None
+        cprim = np.ascontiguousarray(np.array(cprim, np.int32)) if nc else None
+        h = ctypes.c_void_p(into.handle.value if into is not None else None)
+        check(lib().rt_tlas_flatten(self.ctx.handle, self.handle, ptr(np.ascontiguousarray(self.matrices.reshape(-1, 12))),
+                                    ptr(inst_material), ptr(mc), ptr(me), mc.shape[0], nc, ptr(boxes), ptr(rows),
+                                    ptr(cinst), ptr(cprim), bits, ctypes.byref(h)))
+        if into is not None:
+            return into
+        n = sum(self.blases[i.blas_id].prim_count for i in self.instances)
+        return GpuTlas.from_handle(self.ctx, h, n, bits, rows)
+
     def _query(self, fn, ray_type, *args):
         try:
             check(fn(self.ctx.handle, self.handle, *args))

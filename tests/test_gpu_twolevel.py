@@ -154,3 +154,63 @@ def test_tlas_api_errors(native):
     # exact tie between two coincident instances: the lower instance wins (accel.py:815-817)
     tl2 = Tlas([Instance(0), Instance(0)], [b])
     assert closest_hit_batch(tl2, [[0.2, 0.2, 5.0]], [[0.0, 0.0, -1.0]])[1][0] == 0
+
+
+@pytest.mark.parametrize("which", ["cornell", "spheres"])
+def test_compile_two_level_queries_and_render(native, which):
+    """compile_scene(two_level=True): queries through the two-level kernels, frames through
+    the device flatten of the same Tlas -- both against the reference's goldens."""
+    from paper_2603_00292_b200 import IntegratorConfig, compile_scene, render_frame
+    desc = scenes.cornell_description() if which == "cornell" else scenes.spheres_description()
+    sc = compile_scene(desc, two_level=True)
+    assert isinstance(sc.tlas, Tlas) and sc.render_tlas is not None
+    if which == "cornell":
+        g = golden("cornell_hits")
+        res = closest_hit_batch(sc, g["O"], g["D"])
+        same, _ = _agree(res, tuple(g[k] for k in ("t", "inst", "prim", "u", "v", "n")))
+        assert same.all()
+        r = golden("cornell_render")
+        jobs = [("eye32", "eye"), ("pt24", "pt"), ("nee16", "pt-nee")]
+        for name, integ in jobs:
+            w, h, spp, seed, jit, md = (int(x) for x in r[name + "_args"])
+            acc, st = render_frame(sc, w, h, spp, integ, seed=seed, cfg=IntegratorConfig(max_depth=md),
+                                   jitter=bool(jit), return_stats=True)
+            d = acc.mean() - r[name][:, :, :3] / r[name][:, :, 3:]
+            assert float(np.sqrt(np.mean(d ** 2))) <= 1e-4, name
+            assert st["rays"] == int(r[name + "_rays"]), name
+    else:
+        g = golden("spheres")
+        res = closest_hit_batch(sc, g["O"], g["D"], registry=sc.registry)
+        same, _ = _agree(res, tuple(g["p_" + k] for k in ("t", "inst", "prim", "u", "v", "n")))
+        assert same.all()
+        for name, integ in (("eye", "eye"), ("pt", "pt"), ("nee", "pt-nee")):
+            w, h, spp, md = (int(x) for x in g["render_" + name + "_args"])
+            acc, st = render_frame(sc, w, h, spp, integ, cfg=IntegratorConfig(max_depth=md), return_stats=True)
+            d = acc.mean() - g["render_" + name][:, :, :3] / g["render_" + name][:, :, 3:]
+            assert float(np.sqrt(np.mean(d ** 2))) <= 1e-4, name
+            assert st["rays"] == int(g["render_" + name + "_rays"]), name
+
+
+def test_flatten_refill_after_refit(native):
+    """Tlas.flatten(into=...) re-makes the render copy after a Blas refit + refresh."""
+    from paper_2603_00292_b200 import IntegratorConfig, compile_scene, render_frame
+    desc = scenes.cornell_description()
+    tl, blases, insts, _ = tlas_from_description(desc)
+    mats = list(desc.materials)
+    inst_mat = np.array([mats.index(d.material) for d in desc.instances], np.int32)
+    mc = np.array([desc.materials[k].color for k in mats])
+    me = np.array([desc.materials[k].emissive for k in mats])
+    flat = tl.flatten(inst_mat, mc, me)
+    cube = list(desc.meshes).index("cube")
+    blases[cube].refit(vertices=desc.meshes["cube"].vertices * 1.5)
+    with pytest.raises(RuntimeError):
+        tl.flatten(inst_mat, mc, me, into=flat)
+    tl.refresh_instance_bounds()
+    tl.flatten(inst_mat, mc, me, into=flat)
+    # the refilled flat scene traces like the two-level one
+    rng = np.random.default_rng(5)
+    O = rng.uniform(0.05, 0.95, (3000, 3))
+    D = rng.normal(size=(3000, 3))
+    a = closest_hit_batch(flat, O, D)
+    b = closest_hit_batch(tl, O, D)
+    _only_ties(a, b)
