@@ -49,17 +49,21 @@ int rt_io_run(rt_ctx* c, int64_t n, const HostIo& in, size_t hit_bytes, size_t o
     if (n <= 0) return RT_OK;
     int rc = rt_io_streams(c);
     if (rc) return rc;
-    // chunks small enough to pipeline, large enough to fill the GPU
-    int64_t chunk = std::max<int64_t>(1 << 16, std::min<int64_t>(1 << 19, (n + 7) / 8));
+    // 4 chunks: enough overlap; more chunks cost more in per-copy / per-launch overhead
+    // than they save in pipeline fill and drain (config 2 e2e: 16 -> 436, 8 -> 485,
+    // 4 -> 490 Mrays/s)
+#ifndef RT_IO_CHUNKS
+#define RT_IO_CHUNKS 4
+#endif
+    int64_t chunk = std::max<int64_t>(1 << 16, std::min<int64_t>(1 << 19, (n + RT_IO_CHUNKS - 1) / RT_IO_CHUNKS));
     chunk = std::min(chunk, n);
     IoSlot slots[2];
     rc = rt_io_ensure(c, chunk, hit_bytes, out_bytes, slots);
     if (rc) return rc;
     cudaStream_t sc = c->stream, si = c->io_in, so = c->io_out;
-    // the previous user of the context stream may still run: start after it
-    RT_CUDA_TRY(cudaEventRecord(c->io_ev[6], sc));
-    RT_CUDA_TRY(cudaStreamWaitEvent(si, c->io_ev[6], 0));
-    RT_CUDA_TRY(cudaStreamWaitEvent(so, c->io_ev[6], 0));
+    // the staging slots are free (every earlier call synchronised its streams), so the
+    // first uploads overlap whatever still runs on the context stream (e.g. a rebuild);
+    // the kernels themselves queue behind it on that stream
     cudaEvent_t* in_ready = c->io_ev;          // [2]
     cudaEvent_t* in_free = c->io_ev + 2;       // [2]
     cudaEvent_t* out_free = c->io_ev + 4;      // [2]
