@@ -63,8 +63,7 @@ __device__ __forceinline__ void bvh4_write_leaf(float4* __restrict__ bvh4, const
 // pdl / pdr are delta at the parent's boundaries.  N becomes the parent, which
 // also writes its half of ITS parent's BVH4 node (or records the BVH4 root).
 // Returns true at the root.
-__device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
-                                            float4* __restrict__ nodes, float4* __restrict__ bvh4, EmitNode& N,
+__device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child, float4* __restrict__ nodes, float4* __restrict__ bvh4, EmitNode& N,
                                             bool left, int gamma, int pl, int pr, int pdl, int pdr,
                                             const float4 s0, const float4 s1) {
     const int cl = (pl == gamma) ? ~gamma : gamma;
@@ -119,8 +118,8 @@ __device__ __forceinline__ float4 ld_box_valid(const float4* p) {
 
 template <typename K>
 __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __restrict__ child,
-                             int32_t* __restrict__ parent, float4* __restrict__ nodes, float4* __restrict__ bvh4,
-                             int* slot_range, float4* slot_box, EmitNode N) {
+                             float4* __restrict__ nodes, float4* __restrict__ bvh4, int* slot_range,
+                             float4* slot_box, EmitNode N) {
     while (true) {
         const bool left = N.dr > N.dl;
         const int gamma = left ? N.r : N.l - 1;
@@ -135,7 +134,7 @@ __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __rest
         const int pdr = left ? adj_delta(keys, n, pr) : N.dr;
         const float4 s0 = ld_box_valid(slot_box + 4 * gamma + 2 * (1 - side));
         const float4 s1 = ld_box_valid(slot_box + 4 * gamma + 2 * (1 - side) + 1);
-        if (emit_parent(n, child, parent, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s0, s1)) return;
+        if (emit_parent(n, child, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s0, s1)) return;
     }
 }
 
@@ -160,7 +159,7 @@ constexpr int EMIT_T = 256;
 template <typename K>
 __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
                                                            const float* __restrict__ tris, const uint32_t* __restrict__ mask,
-                                                           int64_t n, int2* __restrict__ child, int32_t* __restrict__ parent,
+                                                           int64_t n, int2* __restrict__ child,
                                                            float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
                                                            float4* __restrict__ bvh4, EmitNode* __restrict__ items,
                                                            unsigned int* __restrict__ item_count,
@@ -217,7 +216,7 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
             const int pl = left ? N.l : other, pr = left ? other : N.r;
             // the parent lies inside the block, so its boundary deltas are in smem
             const int pdl = s_delta[pl - (int)B], pdr = s_delta[pr - (int)B + 1];
-            if (emit_parent(n, child, parent, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s_box[g][1 - side][0],
+            if (emit_parent(n, child, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s_box[g][1 - side][0],
                             s_box[g][1 - side][1]))
                 break;                               // root (whole tree inside one block)
         }
@@ -264,12 +263,12 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
 // instead of holding an SM slot for the whole chain.
 template <typename K>
 __global__ void __launch_bounds__(128) lbvh_emit_global_kernel(const K* __restrict__ keys, int64_t n,
-                                                              int2* __restrict__ child, int32_t* __restrict__ parent,
+                                                              int2* __restrict__ child,
                                                               float4* __restrict__ nodes, float4* __restrict__ bvh4,
                                                               int* slot_range, float4* slot_box,
                                                               const EmitNode* __restrict__ items,
                                                               const unsigned int* __restrict__ item_count) {
     const unsigned cnt = *item_count;
     for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
-        climb_global(keys, n, child, parent, nodes, bvh4, slot_range, slot_box, items[k]);
+        climb_global(keys, n, child, nodes, bvh4, slot_range, slot_box, items[k]);
 }

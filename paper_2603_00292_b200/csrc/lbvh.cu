@@ -414,10 +414,10 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     RT_PROF(ctx, 5);
     EmitNode* items = (EmitNode*)s->emit_items;
     lbvh_emit_kernel<K><<<(unsigned)((n + EMIT_T - 1) / EMIT_T), EMIT_T, 0, st>>>(
-        kin, vin, s->tris, s->tri_mask, n, s->child, s->parent, s->tri_sorted, s->nodes, s->bvh4, items,
+        kin, vin, s->tris, s->tri_mask, n, s->child, s->tri_sorted, s->nodes, s->bvh4, items,
         emit_count, (int*)s->flags, s->leaf_box);
     lbvh_emit_global_kernel<K><<<(unsigned)(ctx->num_sms * 4), 128, 0, st>>>(
-        kin, n, s->child, s->parent, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box, items, emit_count);
+        kin, n, s->child, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box, items, emit_count);
     RT_PROF(ctx, 6);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;

@@ -48,24 +48,21 @@ struct rt_scene {
     // LBVH
     int built;
     int bits;
-    float4* nodes;        // (max(n-1,1), 4) BVH2 nodes: child boxes + child ids + height
+    float4* nodes;        // root record, 4 float4: root child boxes, child ids, tree height, BVH4 root
     float4* tri_sorted;   // (n, 3) leaf-ordered vertices; v0.w = flat id, v1.w = mask
     float4* bvh4;         // (max(n-1,1), 8) 4-wide traversal view (grandchildren of each binary node)
     // build scratch
     void* keys_a; void* keys_b;     // u32 or u64 Morton keys
     uint32_t* vals_a; uint32_t* vals_b;
-    int32_t* parent;                // unused (parents are derived on download)
-    int2* child;                    // (n-1)
-    unsigned int* flags;            // (n-1) refit arrival counters
+    int2* child;                    // (n-1) Karras child ids (parents, boxes, heights derived on download)
+    unsigned int* flags;            // (n-1) global split slots of the emit climb
     float* cbounds;                 // 6 floats + 3 inv_ext (+pad)
-    unsigned int* cb_enc;           // unused (the accumulators live in sort_scratch)
     unsigned int* sort_scratch;     // hist + counters + look-back status
     size_t sort_scratch_words;
     float4* leaf_box;               // global split-slot boxes (4 float4 per split)
     float4* lights;                 // (n_lights, 5): (v0, area), v1, v2, normal, emission
     int n_lights;
     void* emit_items;               // boundary-crossing nodes handed from emit phase A to phase B
-    unsigned int* emit_count;       // unused (in sort_scratch)
     // custom primitives: the last n_spheres flat primitives are spheres
     double* spheres;                // (n_spheres, 16): inverse 3x4, center, radius
     int n_spheres;

@@ -1,5 +1,5 @@
-// traverse.cuh -- closest-hit BVH2 traversal, shared by the trace kernel (K6)
-// and the path-tracing kernels (K7/K8).
+// traverse.cuh -- the 4-wide closest-hit / any-hit BVH walks, shared by the trace
+// kernels (K6), the path-tracing kernels (K7/K8) and the two-level kernels.
 //
 // Semantics kept from the reference (accel.py:575-653, 762-849; geometry.py:219-330):
 //   two-sided triangles, inclusive edges, t in [tmin, tmax] inclusive,
@@ -407,61 +407,6 @@ __device__ __forceinline__ bool trace_any4(const float4* __restrict__ bvh4, int 
 // for a binary tree of height h <= RT_STACK - 1 (the depth limit the build enforces).
 #define RT_STACK4 (3 * (RT_STACK / 2) + 4)
 
-// Persistent-thread while-while traversal (Aila & Laine 2009) for ONE ray per
-// lane; the calling warp may be partially active.  nodes: BVH2 (4 float4 per
-// internal node), tris: leaf-ordered (3 float4 per leaf).  Returns id -1 on miss.
-template <bool STATS>
-__device__ __forceinline__ HitRec trace_ray(const float4* __restrict__ nodes, const float4* __restrict__ tris,
-                                            const RayPre& R, float tmax, uint32_t ray_mask, int* stack,
-                                            uint32_t& n_tests, uint32_t& n_visits) {
-    HitRec h;
-    // id -1 = no hit yet: a hit at exactly t == tmax is rejected, as the
-    // reference's TLAS test (best_inst = -1, accel.py:815-817) rejects it
-    h.t = tmax; h.id = -1; h.u = 0.f; h.v = 0.f;
-    int sp = 0;
-    stack[0] = RT_SENTINEL;
-    int node = 0;        // root
-    int leaf = 0;        // pending leaf (< 0) or none (>= 0)
-    while (node != RT_SENTINEL) {
-        // inner loop 1: internal nodes, postponing the first leaf found
-        while ((unsigned)node < (unsigned)RT_SENTINEL) {
-            const float4* nd = nodes + 4 * node;
-            float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2), n3 = __ldg(nd + 3);
-            if (STATS) ++n_visits;
-            float tl = box_enter(R, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, h.t);
-            float tr = box_enter(R, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, h.t);
-            bool hl = tl != INFINITY, hr = tr != INFINITY;
-            int cl = __float_as_int(n3.x), cr = __float_as_int(n3.y);
-            if (!hl && !hr) {
-                node = stack[sp--];
-            } else {
-                node = hl ? cl : cr;
-                if (hl && hr) {
-                    int far = cr;
-                    if (tr < tl) { far = cl; node = cr; }
-                    stack[++sp] = far;
-                }
-            }
-            if (node < 0 && leaf >= 0) {
-                leaf = node;
-                node = stack[sp--];
-            }
-            if (!__any_sync(__activemask(), leaf >= 0)) break;
-        }
-        // inner loop 2: leaves (one triangle each)
-        while (leaf < 0) {
-            int k = ~leaf;
-            const float4* tp = tris + 3 * k;
-            float4 a = __ldg(tp), b = __ldg(tp + 1), c = __ldg(tp + 2);
-            if (STATS) ++n_tests;
-            if (__float_as_uint(b.w) & ray_mask) tri_test(R, a, b, c, h.t, h.id, h.u, h.v);
-            leaf = node;
-            if (node < 0) node = stack[sp--];
-        }
-    }
-    if (h.id < 0) h.t = -1.0f;
-    return h;
-}
 
 // ---- generic 4-wide walks with a leaf callback (two-level traversal, tlas.cu) ----
 // Same node layout, slab test, nearest-first order and pop culling as
