@@ -155,7 +155,8 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
     s->sort_scratch_words = rt_sort_scratch_words(n);
     ALLOC(s->sort_scratch, sizeof(unsigned int) * s->sort_scratch_words);
     ALLOC(s->leaf_box, sizeof(float4) * 4 * n);   // per split slot: (lo, h), hi for both sides
-    ALLOC(s->emit_items, 48 * (2 * n + 2));        // EmitNode; every item is a distinct tree node
+    ALLOC(s->emit_items, 48 * (2 * n + 512));      // EmitNode segments of EMIT_T per emit block
+    ALLOC(s->seg_count, sizeof(unsigned int) * (n / 256 + 2));
 #undef ALLOC
     *out = s;
     return RT_OK;
@@ -228,7 +229,8 @@ void rt_scene_destroy(rt_scene* s) {
     rt_render_release(s);
     void* ptrs[] = {s->tris, s->tri_attr, s->tri_inst, s->tri_prim, s->tri_mask, s->mat_color, s->mat_emissive,
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->child,
-                    s->flags, s->cbounds, s->sort_scratch, s->leaf_box, s->emit_items, s->lights, s->spheres,
+                    s->flags, s->cbounds, s->sort_scratch, s->leaf_box, s->emit_items, s->seg_count, s->lights,
+                    s->spheres,
                     s->lnormal64};
     for (void* p : ptrs)
         if (p) cudaFree(p);

@@ -156,26 +156,28 @@ __global__ void bvh4_single_leaf_kernel(const float4* __restrict__ nodes, float4
 
 constexpr int EMIT_T = 256;
 
+#ifndef EMIT_MINB
+#define EMIT_MINB 1
+#endif
 template <typename K>
-__global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
+__global__ void __launch_bounds__(EMIT_T, EMIT_MINB) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
                                                            const float* __restrict__ tris, const uint32_t* __restrict__ mask,
                                                            int64_t n, int2* __restrict__ child,
                                                            float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
                                                            float4* __restrict__ bvh4, EmitNode* __restrict__ items,
-                                                           unsigned int* __restrict__ item_count,
+                                                           unsigned int* __restrict__ seg_count,
                                                            int* __restrict__ slot_range, float4* __restrict__ slot_box) {
     __shared__ int s_range[EMIT_T];             // smem split slots (gamma - B); -1 empty, -2 done
     __shared__ int s_delta[EMIT_T + 1];         // delta(B - 1 + k)
     __shared__ float4 s_box[EMIT_T][2][2];      // [slot][side][(lo, h) | (hi, -)]
-    __shared__ EmitNode s_def[EMIT_T];          // deferred (boundary-crossing) nodes
-    __shared__ int s_ndef;
+    __shared__ unsigned s_cnt;                  // finished subtrees handed to the global climb
     const int tid = threadIdx.x;
     const int64_t B = (int64_t)blockIdx.x * EMIT_T;
     const int64_t E = (B + EMIT_T < n) ? B + EMIT_T : n;
     s_range[tid] = -1;
     s_delta[tid] = adj_delta(keys, n, B - 1 + tid);
     if (tid == 0) {
-        s_ndef = 0;
+        s_cnt = 0;
         s_delta[EMIT_T] = adj_delta(keys, n, B - 1 + EMIT_T);
     }
     const int64_t i = B + tid;
@@ -201,7 +203,9 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
             const bool left = N.dr > N.dl;
             const bool inside = left ? (N.r + 1 < E) : (N.l - 1 >= B);
             if (!inside) {
-                s_def[atomicAdd(&s_ndef, 1)] = N;
+                // the block's segment of the hand-off list (no global counter)
+                items[B + atomicAdd(&s_cnt, 1u)] = N;
+                if (N.r < n - 1) slot_reset(slot_range, slot_box, N.r);
                 break;
             }
             const int gamma = left ? N.r : N.l - 1;
@@ -223,18 +227,8 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
     }
     __syncthreads();
     // hand-off to phase B: smem slot `tid` left with a single arrival (its sibling
-    // extends past the block), then deferred node `tid`.  One global atomic per
-    // block reserves the block's items (per-item atomics on the one counter
-    // serialise in L2: ~20% of this kernel's stall samples)
-    __shared__ unsigned s_base, s_next;
-    const bool single = tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0;
-    const int n_single = __syncthreads_count(single);
-    if (tid == 0) {
-        s_base = atomicAdd(item_count, (unsigned)(n_single + s_ndef));
-        s_next = 0;
-    }
-    __syncthreads();
-    if (single) {
+    // extends past the block) -> this block's segment items[B, B + count)
+    if (tid < EMIT_T - 1 && B + tid + 1 < E && s_range[tid] >= 0) {
         const int endpoint = s_range[tid];
         const int gamma = (int)B + tid;
         const bool left = endpoint <= gamma;         // left child: [endpoint, gamma]; right: [gamma+1, endpoint]
@@ -248,27 +242,30 @@ __global__ void __launch_bounds__(EMIT_T) lbvh_emit_kernel(const K* __restrict__
         M.hi[0] = hi4.x; M.hi[1] = hi4.y; M.hi[2] = hi4.z;
         M.dl = s_delta[M.l - (int)B];
         M.dr = s_delta[M.r - (int)B + 1];
-        items[s_base + atomicAdd(&s_next, 1u)] = M;
+        items[B + atomicAdd(&s_cnt, 1u)] = M;
         if (M.r < n - 1) slot_reset(slot_range, slot_box, M.r);   // the global climb's slots: item right ends
     }
-    if (tid < s_ndef) {
-        items[s_base + n_single + tid] = s_def[tid];
-        if (s_def[tid].r < n - 1) slot_reset(slot_range, slot_box, s_def[tid].r);
-    }
+    __syncthreads();
+    if (tid == 0) seg_count[blockIdx.x] = s_cnt;
 }
 
-// Phase B as its own persistent kernel: the few boundary-crossing nodes of all
-// blocks (typically ~n/64) climb through the global split slots.  Keeping these
+// Phase B as its own kernel: the few boundary-crossing nodes of all
+// blocks (typically ~n/30) climb through the global split slots.  Keeping these
 // long, mostly single-lane chains out of kernel A lets its blocks retire at once
-// instead of holding an SM slot for the whole chain.
+// instead of holding an SM slot for the whole chain.  Items come in per-block
+// segments items[b * EMIT_T, b * EMIT_T + seg_count[b]), one warp per segment.
 template <typename K>
 __global__ void __launch_bounds__(128) lbvh_emit_global_kernel(const K* __restrict__ keys, int64_t n,
                                                               int2* __restrict__ child,
                                                               float4* __restrict__ nodes, float4* __restrict__ bvh4,
                                                               int* slot_range, float4* slot_box,
                                                               const EmitNode* __restrict__ items,
-                                                              const unsigned int* __restrict__ item_count) {
-    const unsigned cnt = *item_count;
-    for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < cnt; k += gridDim.x * blockDim.x)
-        climb_global(keys, n, child, nodes, bvh4, slot_range, slot_box, items[k]);
+                                                              const unsigned int* __restrict__ seg_count,
+                                                              int64_t n_blocks) {
+    // one warp per segment, so every item climbs concurrently (no thread takes two)
+    const int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (seg >= n_blocks) return;
+    const unsigned cnt = __ldg(seg_count + seg);
+    for (unsigned j = threadIdx.x & 31; j < cnt; j += 32)
+        climb_global(keys, n, child, nodes, bvh4, slot_range, slot_box, items[seg * EMIT_T + j]);
 }

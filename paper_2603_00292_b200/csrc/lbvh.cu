@@ -383,7 +383,6 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     unsigned int* hist = s->sort_scratch;                    // PASSES * 256
     unsigned int* counters = hist + PASSES * RADIX;          // [0, 8) tile counters, [8, 14) cb_enc, [16] emit count
     unsigned int* cb_enc = counters + 8;
-    unsigned int* emit_count = counters + 16;
     unsigned int* status = counters + 32;                    // PASSES * tiles * 256
     size_t words = (size_t)PASSES * RADIX + 32 + (size_t)PASSES * tiles * RADIX;
     RT_PROF(ctx, 0);
@@ -413,11 +412,12 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     // (the global split slots are reset by the emit kernel at its hand-off boundaries)
     RT_PROF(ctx, 5);
     EmitNode* items = (EmitNode*)s->emit_items;
-    lbvh_emit_kernel<K><<<(unsigned)((n + EMIT_T - 1) / EMIT_T), EMIT_T, 0, st>>>(
+    const int64_t n_blocks = (n + EMIT_T - 1) / EMIT_T;
+    lbvh_emit_kernel<K><<<(unsigned)n_blocks, EMIT_T, 0, st>>>(
         kin, vin, s->tris, s->tri_mask, n, s->child, s->tri_sorted, s->nodes, s->bvh4, items,
-        emit_count, (int*)s->flags, s->leaf_box);
-    lbvh_emit_global_kernel<K><<<(unsigned)(ctx->num_sms * 4), 128, 0, st>>>(
-        kin, n, s->child, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box, items, emit_count);
+        s->seg_count, (int*)s->flags, s->leaf_box);
+    lbvh_emit_global_kernel<K><<<(unsigned)((n_blocks * 32 + 127) / 128), 128, 0, st>>>(
+        kin, n, s->child, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box, items, s->seg_count, n_blocks);
     RT_PROF(ctx, 6);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;

@@ -63,6 +63,7 @@ struct rt_scene {
     float4* lights;                 // (n_lights, 5): (v0, area), v1, v2, normal, emission
     int n_lights;
     void* emit_items;               // boundary-crossing nodes handed from emit phase A to phase B
+    unsigned int* seg_count;        // per emit block: items in its segment
     // custom primitives: the last n_spheres flat primitives are spheres
     double* spheres;                // (n_spheres, 16): inverse 3x4, center, radius
     int n_spheres;
