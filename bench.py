@@ -423,9 +423,9 @@ def run_ours(args, ws, rank, local):
             other = roof_build
         line_extra = {"lbvh_build_ms": build_ms, "trace_mrays_s": rays_step * K / (t_render * 1e-3) / 1e6,
                       "roofline_other": other}
-        launches = 9 + 1
-        detail = "per step: 9 LBVH kernels (bounds, bounds_finish, morton, histogram, 4 onesweep passes, fused " \
-                 "emit+refit) + 1 megakernel"
+        launches = 8 + 1      # the bench builds with 30-bit keys
+        detail = "per step: 8 LBVH kernels (bounds, Morton + digit histograms, 4 onesweep passes, emit+refit, " \
+                 "global emit climb) + 1 megakernel (plus one memset)"
     else:
         launches = 1 if kernel == "mega" else (samples[1] - samples[0]) * (2 + 2 * cfg.max_depth)
         detail = "per step: 1 megakernel" if kernel == "mega" else \
