@@ -157,7 +157,7 @@ __global__ void bvh4_single_leaf_kernel(const float4* __restrict__ nodes, float4
 constexpr int EMIT_T = 256;
 
 #ifndef EMIT_MINB
-#define EMIT_MINB 1
+#define EMIT_MINB 5   // 48 registers: 5 blocks per SM (10M emit 1.14 -> 1.09 ms)
 #endif
 template <typename K>
 __global__ void __launch_bounds__(EMIT_T, EMIT_MINB) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
