@@ -26,6 +26,7 @@ extern "C" {
 #define RT_EDEPTH (-4)        /* BVH deeper than the traversal stack -> BuildError (accel.py:148-149) */
 #define RT_ENOMEM (-5)        /* device allocation failed     -> MemoryError  */
 #define RT_ESTATE (-6)        /* e.g. trace before build      -> RuntimeError */
+#define RT_ENCCL (-7)         /* NCCL failure (rt_multi_render) -> RuntimeError */
 
 #define RT_INTEG_EYE 0        /* integrators.py:129-141 _sample_eye   */
 #define RT_INTEG_AO 1         /* integrators.py:144-179 _sample_ao    (megakernel) */
@@ -160,6 +161,18 @@ int rt_render(rt_ctx* ctx, rt_scene* scene, const rt_render_params* p, float* ac
  * uint8, mean clamped to [0, 1], ^(1/2.2) when gamma != 0, round-half-even of 255 v;
  * both device buffers.  RT_EINVAL if a pixel has zero samples (AccumBuffer.mean). */
 int rt_resolve(rt_ctx* ctx, const float* accum, int64_t npix, int32_t gamma, uint8_t* rgb);
+/* ---- multi-GPU: one process, n devices of a node ------------------
+ * Each device g has its own context, scene replica (identical deterministic LBVH) and
+ * ZERO-initialised (H*W, 4) fp32 accumulation buffer accums[g].  split RT_SPLIT_SAMPLES:
+ * device g renders global samples [s0 + g*S/n, s0 + (g+1)*S/n) (the same random numbers as
+ * one GPU); RT_SPLIT_TILES: device g renders the 4-row tile bands r % n == g.  All renders
+ * run concurrently, then ONE grouped ncclReduce(sum, fp32) leaves the frame in accums[0]
+ * (NCCL is dlopen'ed: the process's libnccl.so.2).  rays_out (nullable): all devices'
+ * closest-hit queries.  Replaces render_frame's worker split (integrators.py:426-473). */
+#define RT_SPLIT_SAMPLES 0
+#define RT_SPLIT_TILES 1
+int rt_multi_render(int32_t n_gpus, rt_ctx* const* ctxs, rt_scene* const* scenes, const rt_render_params* p,
+                    float* const* accums, int32_t split, uint64_t* rays_out);
 /* primary rays of sample s for every pixel of the frame (parity tests): (W*H, 8) like rt_trace_closest */
 int rt_raygen(rt_ctx* ctx, const rt_render_params* p, int32_t sample, float* rays);
 

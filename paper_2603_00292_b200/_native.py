@@ -23,6 +23,9 @@ RT_EUNSUPPORTED = -3
 RT_EDEPTH = -4
 RT_ENOMEM = -5
 RT_ESTATE = -6
+RT_ENCCL = -7
+RT_SPLIT_SAMPLES = 0
+RT_SPLIT_TILES = 1
 
 RT_INTEG_EYE = 0
 RT_INTEG_AO = 1
@@ -93,6 +96,7 @@ def lib():
             "rt_scene_set_spheres": [vp, vp, i32, vp],
             "rt_raygen": [vp, ctypes.POINTER(RenderParams), i32, vp],
             "rt_resolve": [vp, vp, i64, i32, vp],
+            "rt_multi_render": [i32, vp, vp, ctypes.POINTER(RenderParams), vp, i32, vp],
             "rt_scene_set_local_normals": [vp, vp, vp],
             "rt_scene_set_custom": [vp, vp, i32, i64],
             "rt_tlas_create": [vp, i32, vp, vp, vp, vp, vp],

@@ -92,42 +92,37 @@ def render_frame_distributed(scene, width, height, spp, integrator="pt", seed=0,
 
 
 def render_frame_multi(scenes, width, height, spp, integrator="pt", seed=0, cfg=None, jitter=True, kernel="mega",
-                       return_device=False):
+                       return_device=False, mode="samples"):
     """One process, several GPUs: ``scenes[g]`` is the replica compiled on device g.
 
-    Sample split (global sample indices, so the random numbers are those of a
-    1-GPU run), one host thread per GPU (the ctypes calls release the GIL),
-    then the partial (H*W, 4) sums are added on GPU 0 (peer copies over
-    NVLink).  Returns (accum on GPU 0, rays) with return_device, else
-    (AccumBuffer, rays)."""
+    ``rt_multi_render`` (csrc/multi.cu) enqueues every device's share concurrently --
+    the sample split (global sample indices, so the random numbers are those of a
+    1-GPU run) or the tile-band split -- then ONE grouped NCCL reduce of the fp32
+    accumulation buffers into GPU 0.  Returns (accum on GPU 0, rays) with
+    return_device, else (AccumBuffer, rays)."""
+    import ctypes
     import torch
-    from concurrent.futures import ThreadPoolExecutor
-    from .integrators import render_into
+    from ._native import RT_SPLIT_SAMPLES, RT_SPLIT_TILES, check, lib
+    from .integrators import make_params
     from .scene_io import AccumBuffer
     G = len(scenes)
     if G < 1:
         raise ValueError("need at least one scene replica")
     if width < 1 or height < 1 or spp < 1:
         raise ValueError("width, height, and spp must all be >= 1")
-    accs = [torch.zeros((width * height, 4), dtype=torch.float32, device=torch.device("cuda", sc.tlas.ctx.device))
-            for sc in scenes]
-
-    def job(g):
-        s0, s1 = sample_slice(g, G, spp)
-        if s1 <= s0:
-            return 0
-        with torch.cuda.device(scenes[g].tlas.ctx.device):
-            return render_into(scenes[g], accs[g], width, height, spp, integrator, seed, cfg, jitter, kernel,
-                               samples=(s0, s1))
-
-    if G == 1:
-        rays = job(0)
-    else:
-        with ThreadPoolExecutor(max_workers=G) as pool:
-            rays = sum(pool.map(job, range(G)))
+    if mode not in ("samples", "tiles"):
+        raise ValueError(f"unknown split {mode!r}")
+    flats = [getattr(sc, "render_tlas", None) or sc.tlas for sc in scenes]
+    accs = [torch.zeros((width * height, 4), dtype=torch.float32, device=torch.device("cuda", f.ctx.device))
+            for f in flats]
+    p = make_params(scenes[0], width, height, 0, spp, integrator, seed, cfg, jitter, kernel)
+    ctxs = (ctypes.c_void_p * G)(*[f.ctx.handle.value for f in flats])
+    hs = (ctypes.c_void_p * G)(*[f.handle.value for f in flats])
+    ptrs = (ctypes.c_void_p * G)(*[a.data_ptr() for a in accs])
+    rays = np.zeros(1, np.uint64)
+    check(lib().rt_multi_render(G, ctxs, hs, p, ptrs, RT_SPLIT_SAMPLES if mode == "samples" else RT_SPLIT_TILES,
+                                rays.ctypes.data_as(ctypes.c_void_p)))
     acc = accs[0]
-    for g in range(1, G):
-        acc.add_(accs[g].to(acc.device))
     if return_device:
-        return acc, rays
-    return AccumBuffer(width, height, acc.cpu().numpy().astype(np.float64).reshape(height, width, 4)), rays
+        return acc, int(rays[0])
+    return AccumBuffer(width, height, acc.cpu().numpy().astype(np.float64).reshape(height, width, 4)), int(rays[0])

@@ -107,16 +107,43 @@ def test_resolve_device_matches_host(native):
 
 
 @pytest.mark.gpu
-def test_render_frame_multi_replicas_sum(native):
-    """--gpus N logic on one device: two replicas split the samples, partial sums add up
-    to the single-replica frame (fp32 addition order differs only at rounding level)."""
+@pytest.mark.parametrize("mode", ["samples", "tiles"])
+def test_multi_render_native(native, mode):
+    """rt_multi_render (the --gpus path) on the devices present: the split frame equals
+    the single-device frame (one device: bit-identical; more: fp32 reduce order only)."""
+    import torch
     from paper_2603_00292_b200 import IntegratorConfig, compile_scene, render_frame
     from paper_2603_00292_b200.distributed import render_frame_multi
     desc = scenes.cornell_description()
-    reps = [compile_scene(desc), compile_scene(desc)]
+    n = torch.cuda.device_count()
+    reps = [compile_scene(desc, device=g) for g in range(n)]
     cfg = IntegratorConfig(max_depth=5)
-    acc2, rays2 = render_frame_multi(reps, 40, 30, 6, "pt", cfg=cfg)
-    acc1, st = render_frame(reps[0], 40, 30, 6, "pt", cfg=cfg, return_stats=True)
+    spp = 6 if mode == "samples" else 1
+    integ = "pt" if mode == "samples" else "eye"
+    acc2, rays2 = render_frame_multi(reps, 40, 30, spp, integ, cfg=cfg, mode=mode)
+    acc1, st = render_frame(reps[0], 40, 30, spp, integ, cfg=cfg, return_stats=True)
     assert rays2 == st["rays"]
     assert np.array_equal(acc2.data[:, :, 3], acc1.data[:, :, 3])
-    assert np.allclose(acc2.data, acc1.data, rtol=1e-5, atol=1e-5)
+    if n == 1:
+        assert np.array_equal(acc2.data, acc1.data)
+    else:
+        assert np.allclose(acc2.data, acc1.data, rtol=1e-5, atol=1e-5)
+    with pytest.raises(ValueError, match="distinct device"):
+        render_frame_multi([reps[0], reps[0]], 8, 8, 2, "pt", cfg=cfg)
+
+
+@pytest.mark.gpu
+def test_multi_render_nccl_plumbing(native):
+    """The dlopen'ed NCCL reduce path of rt_multi_render, forced on one device."""
+    import subprocess
+    import sys
+    code = ("import numpy as np; from paper_2603_00292_b200 import compile_scene, render_frame, scenes; "
+            "from paper_2603_00292_b200.distributed import render_frame_multi; "
+            "sc = compile_scene(scenes.cornell_description()); "
+            "a, r = render_frame_multi([sc], 16, 12, 4, 'pt'); b = render_frame(sc, 16, 12, 4, 'pt'); "
+            "assert np.array_equal(a.data, b.data); print('nccl ok', r)")
+    env = dict(os.environ, RT_MULTI_FORCE_NCCL="1")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))), timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "nccl ok" in out.stdout

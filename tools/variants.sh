@@ -10,11 +10,11 @@ while [ $# -ge 2 ]; do
   name=$1; defs=$2; shift 2
   out=variants/$name; mkdir -p $out
   pids=()
-  for f in capi lbvh trace render tlas; do
+  for f in capi lbvh trace render tlas multi; do
     /usr/local/cuda/bin/nvcc $FLAGS $defs -c $CS/$f.cu -o $out/$f.o & pids+=($!)
   done
   for p in "${pids[@]}"; do wait $p; done
-  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/librt_b200.so $out/*.o -lcudart
+  /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $out/librt_b200.so $out/*.o -lcudart -ldl
   rm -f $out/*.o
   echo "built $out"
 done
