@@ -105,14 +105,22 @@ __device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child,
 // Global rendezvous without a release fence: a fence.gpu before the exchange would wait
 // for every earlier store of the thread (the previous level's node writes) to reach L2,
 // on each level of the chain.  Instead the box halves carry validity tags in .w
-// (height >= 0, split g >= -1; both sides' tags are invalidated by the emit kernel's
-// hand-off before this kernel runs), the exchange is relaxed, and the second arrival
-// spins on the L2 copy of its sibling's box until both tags are valid.
+// (height | (outer delta + 1) << 8 >= 0, split g >= -1; both sides' tags are invalidated
+// by the emit kernel's hand-off before this kernel runs), the exchange is relaxed, and
+// the second arrival spins on the L2 copy of its sibling's box until both tags are
+// valid.  (This relies on a 16-B aligned st.v4 landing in L2 as one access, which
+// holds on the hardware; the tag word and the box share a 32-B sector.)
 constexpr int SLOT_INVALID = (int)0x80000000;
 
-__device__ __forceinline__ float4 ld_box_valid(const float4* p) {
+// A spin on a plain (even asm-volatile ld.global.cg) load is NOT a loop to ptxas: it
+// assumes the location cannot change and keeps at most one reload.  The re-reads must be
+// strong relaxed loads at GPU scope, which ptxas must re-issue on every iteration.
+__device__ __forceinline__ float4 ld_relaxed_gpu(const float4* p) {
     float4 v;
-    do { v = __ldcg(p); } while (__float_as_int(v.w) == SLOT_INVALID);
+    asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p)
+                 : "memory");
     return v;
 }
 
@@ -124,16 +132,24 @@ __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __rest
         const bool left = N.dr > N.dl;
         const int gamma = left ? N.r : N.l - 1;
         const int side = left ? 0 : 1;
-        __stcg(slot_box + 4 * gamma + 2 * side, make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h)));
+        // the box record also carries this node's OUTER boundary delta (the parent's
+        // boundary on this side: dl for a left child, dr for a right child), so the
+        // second arrival needs no key loads: one L2 round trip per level (the sibling's
+        // record is read speculatively alongside the exchange)
+        const int outer = (left ? N.dl : N.dr) + 1;
+        __stcg(slot_box + 4 * gamma + 2 * side, make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h | (outer << 8))));
         __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g)));
+        const float4* sib = slot_box + 4 * gamma + 2 * (1 - side);
+        float4 s0 = __ldcg(sib), s1 = __ldcg(sib + 1);
         const int other = atomicExch(slot_range + gamma, left ? N.l : N.r);
         if (other < 0) return;                       // sibling subtree not finished
+        while (__float_as_int(s0.w) == SLOT_INVALID) s0 = ld_relaxed_gpu(sib);
+        while (__float_as_int(s1.w) == SLOT_INVALID) s1 = ld_relaxed_gpu(sib + 1);
         const int pl = left ? N.l : other, pr = left ? other : N.r;
-        // one boundary delta of the parent is this node's own
-        const int pdl = left ? N.dl : adj_delta(keys, n, pl - 1);
-        const int pdr = left ? adj_delta(keys, n, pr) : N.dr;
-        const float4 s0 = ld_box_valid(slot_box + 4 * gamma + 2 * (1 - side));
-        const float4 s1 = ld_box_valid(slot_box + 4 * gamma + 2 * (1 - side) + 1);
+        const int sd = (__float_as_int(s0.w) >> 8) - 1;
+        s0.w = __int_as_float(__float_as_int(s0.w) & 0xFF);
+        const int pdl = left ? N.dl : sd;
+        const int pdr = left ? sd : N.dr;
         if (emit_parent(n, child, nodes, bvh4, N, left, gamma, pl, pr, pdl, pdr, s0, s1)) return;
     }
 }

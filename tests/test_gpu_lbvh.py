@@ -74,6 +74,21 @@ def test_rebuild_is_deterministic(native):
     assert sc.tlas.build_ms > 0
 
 
+def test_rebuild_alternating_widths_1m(native):
+    """Config-2 size, rebuilt in place with alternating Morton widths: every rebuild equals a
+    fresh build (the global climb's slot records from the previous build, or a sibling's
+    record that has not landed yet, must never be consumed; this caught a spin loop that
+    ptxas had reduced to a single reload)."""
+    desc = scenes.sphere_description()
+    fresh = {b: compile_scene(desc, f"lbvh{b}").tlas.download() for b in (30, 63)}
+    sc = compile_scene(desc, "lbvh30")
+    for bits in (63, 30, 63, 63, 30, 30, 63, 30):
+        sc.tlas.build(bits)
+        got = sc.tlas.download()
+        for k in fresh[bits]:
+            assert np.array_equal(got[k], fresh[bits][k]), (bits, k)
+
+
 def test_lbvh_cost_through_reference_traversal(native, oracle_mod):
     """the GPU BVH, traversed by the (restated) reference kernels,
     gives the SAH tree's exact hits; also reports its per-ray node/tri cost."""
