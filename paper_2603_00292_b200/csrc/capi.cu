@@ -156,7 +156,7 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
     ALLOC(s->sort_scratch, sizeof(unsigned int) * s->sort_scratch_words);
     ALLOC(s->leaf_box, sizeof(float4) * 4 * n);   // per split slot: (lo, h), hi for both sides
     ALLOC(s->emit_items, 48 * (2 * n + 512));      // EmitNode segments of EMIT_T per emit block
-    ALLOC(s->seg_count, sizeof(unsigned int) * (n / 256 + 2));
+    ALLOC(s->seg_count, sizeof(unsigned int) * (n / 64 + 2));   // one count per emit block (EMIT_T >= 64)
 #undef ALLOC
     *out = s;
     return RT_OK;

@@ -170,7 +170,10 @@ __global__ void bvh4_single_leaf_kernel(const float4* __restrict__ nodes, float4
     bvh4_write_half(bvh4, 0, 1, e, e, ~0, e, e, ~0);
 }
 
-constexpr int EMIT_T = 256;
+#ifndef EMIT_TILE
+#define EMIT_TILE 256   // 128 / 512 measured slower (1M emit 0.125 -> 0.134 / 0.136 ms)
+#endif
+constexpr int EMIT_T = EMIT_TILE;
 
 #ifndef EMIT_MINB
 #define EMIT_MINB 5   // 48 registers: 5 blocks per SM (10M emit 1.14 -> 1.09 ms)

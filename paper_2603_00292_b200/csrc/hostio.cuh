@@ -55,8 +55,19 @@ int rt_io_run(rt_ctx* c, int64_t n, const HostIo& in, size_t hit_bytes, size_t o
 #ifndef RT_IO_CHUNKS
 #define RT_IO_CHUNKS 4
 #endif
+#ifndef RT_IO_GEOMETRIC
+#define RT_IO_GEOMETRIC 1      // config-2 closest_hit_batch 3.63 -> 3.45 ms (first chunk 64k: 3.49)
+#endif
+#ifndef RT_IO_FIRST
+#define RT_IO_FIRST (1 << 17)
+#endif
     int64_t chunk = std::max<int64_t>(1 << 16, std::min<int64_t>(1 << 19, (n + RT_IO_CHUNKS - 1) / RT_IO_CHUNKS));
     chunk = std::min(chunk, n);
+#if RT_IO_GEOMETRIC
+    // chunk sizes grow from RT_IO_FIRST (doubling) up to the slot size: the first download
+    // starts early, the later (download-bound) chunks stay large
+    int64_t first = std::min<int64_t>(chunk, RT_IO_FIRST);
+#endif
     IoSlot slots[2];
     rc = rt_io_ensure(c, chunk, hit_bytes, out_bytes, slots);
     if (rc) return rc;
@@ -68,8 +79,14 @@ int rt_io_run(rt_ctx* c, int64_t n, const HostIo& in, size_t hit_bytes, size_t o
     cudaEvent_t* in_free = c->io_ev + 2;       // [2]
     cudaEvent_t* out_free = c->io_ev + 4;      // [2]
     int64_t k = 0;
+#if RT_IO_GEOMETRIC
+    int64_t step = first;
+    for (int64_t b = 0; b < n; b += step, step = std::min(chunk, 2 * step), ++k) {
+        const int64_t m = std::min(step, n - b);
+#else
     for (int64_t b = 0; b < n; b += chunk, ++k) {
         const int64_t m = std::min(chunk, n - b);
+#endif
         const int s = (int)(k & 1);
         const IoSlot& S = slots[s];
         if (k >= 2) RT_CUDA_TRY(cudaStreamWaitEvent(si, in_free[s], 0));
