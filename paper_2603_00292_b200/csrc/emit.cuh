@@ -112,6 +112,18 @@ __device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child,
 // holds on the hardware; the tag word and the box share a 32-B sector.)
 constexpr int SLOT_INVALID = (int)0x80000000;
 
+#ifndef EMIT_ACQREL
+#define EMIT_ACQREL 1
+#endif
+__device__ __forceinline__ int atom_exch_acq_rel_cta(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.cta.shared::cta.exch.b32 %0, [%1], %2;"
+                 : "=r"(old)
+                 : "r"((unsigned)__cvta_generic_to_shared(p)), "r"(v)
+                 : "memory");
+    return old;
+}
+
 // A spin on a plain (even asm-volatile ld.global.cg) load is NOT a loop to ptxas: it
 // assumes the location cannot change and keeps at most one reload.  The re-reads must be
 // strong relaxed loads at GPU scope, which ptxas must re-issue on every iteration.
@@ -231,10 +243,17 @@ __global__ void __launch_bounds__(EMIT_T, EMIT_MINB) lbvh_emit_kernel(const K* _
             const int g = gamma - (int)B, side = left ? 0 : 1;
             s_box[g][side][0] = make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h));
             s_box[g][side][1] = make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g));
+#if EMIT_ACQREL
+            // release (publishes this side's box) + acquire (sees the sibling's) in the
+            // exchange itself instead of two sequentially consistent block fences
+            const int other = atom_exch_acq_rel_cta(&s_range[g], left ? N.l : N.r);
+            if (other < 0) break;                    // first arrival: pending in smem
+#else
             __threadfence_block();
             const int other = atomicExch(&s_range[g], left ? N.l : N.r);
             if (other < 0) break;                    // first arrival: pending in smem
             __threadfence_block();
+#endif
             s_range[g] = -2;                         // pair complete
             const int pl = left ? N.l : other, pr = left ? other : N.r;
             // the parent lies inside the block, so its boundary deltas are in smem
