@@ -308,36 +308,56 @@ def run_ours(args, ws, rank, local):
     value = rays_step * K / (t_total * 1e-3) / 1e6
 
     # -- end to end through the public API with host buffers ---------------------
-    e2e = None
+    e2e = e2e_query = None
     if not args.no_e2e:
         if C in (2, 4):
-            # GpuTlas.refit(host vertices) + closest_hit_batch(host float64 rays) of this rank's rays
-            r = prim.cpu().numpy().astype(np.float64)
-            if bands is not None:
-                rows = np.array(distributed.band_rows(H, rank, ws))
-                sel = (rows[:, None] * W + np.arange(W)[None, :]).ravel()
-                r = r[sel]
-            # the step's inputs live in pinned host memory (H2D runs as full-rate DMA)
+            from paper_2603_00292_b200 import render_frame
             from paper_2603_00292_b200._native import host_pinned_copy
-            O, D = host_pinned_copy(np.ascontiguousarray(r[:, 0:3])), host_pinned_copy(np.ascontiguousarray(r[:, 4:7]))
-            host_tris = host_pinned_copy(tl.tris)
-            closest_hit_batch(sc, O, D)
-            ke = max(1, min(K, 5))
+            host_tris = host_pinned_copy(tl.tris)           # the step's vertices in pinned host memory
+            # (1) the reference arm's own path: refit(host vertices) + render_frame('eye') -> host
+            #     float64 AccumBuffer (H2D: the vertices; D2H: the (H, W, 4) float64 sums)
+            render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
+            ke = max(3, min(K, 10))
             if ws > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(ke):
                 tl.refit(host_tris, 30)
-                closest_hit_batch(sc, O, D)
+                render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
             torch.cuda.synchronize()
             te = time.perf_counter() - t0
+            h2d, d2h = int(host_tris.nbytes), int(npix * 32)
+            path = ("GpuTlas.refit(host fp32 vertices: H2D + LBVH rebuild) + render_frame('eye') -> host float64 "
+                    "AccumBuffer (H, W, 4); the reference arm times the same calls")
+            rays_e2e = my_rays
+            # (2) the query API: refit + closest_hit_batch(host float64 rays) of this rank's rays
+            r = prim.cpu().numpy().astype(np.float64)
+            if bands is not None:
+                rows = np.array(distributed.band_rows(H, rank, ws))
+                sel = (rows[:, None] * W + np.arange(W)[None, :]).ravel()
+                r = r[sel]
+            O, D = host_pinned_copy(np.ascontiguousarray(r[:, 0:3])), host_pinned_copy(np.ascontiguousarray(r[:, 4:7]))
+            closest_hit_batch(sc, O, D)
+            kq = max(1, min(K, 5))
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(kq):
+                tl.refit(host_tris, 30)
+                closest_hit_batch(sc, O, D)
+            torch.cuda.synchronize()
+            tq = torch.tensor([time.perf_counter() - t0, float(O.shape[0])], dtype=torch.float64, device=dev)
+            if ws > 1:
+                dist.all_reduce(tq[:1], op=dist.ReduceOp.MAX)
+                dist.all_reduce(tq[1:], op=dist.ReduceOp.SUM)
             nr = O.shape[0]
-            h2d = int(host_tris.nbytes + nr * (24 + 24))        # t_min / t_max are broadcast scalars
-            d2h = int(nr * (8 + 8 + 8 + 8 + 8 + 24))
-            path = ("GpuTlas.refit(host fp32 vertices, H2D + LBVH rebuild) + closest_hit_batch(host float64 rays) "
-                    "-> host float64/int64 (t, inst, prim, u, v, normal)")
-            rays_e2e = nr
+            e2e_query = {"value": float(tq[1]) * kq / float(tq[0]) / 1e6, "unit": "Mrays/s",
+                         "h2d_bytes_per_step": int(host_tris.nbytes + nr * 48),   # t_min / t_max: scalars
+                         "d2h_bytes_per_step": int(nr * 64), "steps": kq,
+                         "path": ("GpuTlas.refit(host fp32 vertices) + closest_hit_batch(host float64 rays) -> "
+                                  "host float64/int64 (t, inst, prim, u, v, normal)")}
         else:
             # render_frame (public API): H2D of the camera/params only, D2H of the (H, W, 4) accumulation
             from paper_2603_00292_b200 import render_frame
@@ -441,6 +461,7 @@ def run_ours(args, ws, rank, local):
         **line_extra, "reduce_ms": t_reduce / K, "roofline": dominant,
         "per_ray": {"bvh4_node_fetches": n_nodes, "triangle_tests": n_tests},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+        **({"e2e_query": e2e_query} if e2e_query else {}),
         "gpu_launches": K * launches, "gpu_launches_detail": detail, "pt": pt,
     }
     print(json.dumps(line), flush=True)

@@ -108,8 +108,12 @@ def render_into(scene, accum, width, height, spp=1, integrator="pt", seed=0, cfg
 
 def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt", seed: int = 0,
                  workers: int = 1, cfg: Optional[IntegratorConfig] = None, jitter: bool = True,
-                 return_stats: bool = False, kernel: str = "mega", samples=None):
-    """Render a full frame into a fresh AccumBuffer (float64 host copy of the fp32 device sums)."""
+                 return_stats: bool = False, kernel: str = "mega", samples=None, bands=None):
+    """Render a full frame into a fresh AccumBuffer (float64 host copy of the fp32 device sums).
+
+    The fp32 sums are widened to float64 on the device (exact) and read back with one DMA
+    into pinned memory.  `bands=(stride, offset)` renders only that GPU's interleaved
+    4-row tile bands (the multi-GPU tile split); the other pixels stay 0."""
     import torch
     if width < 1 or height < 1 or spp < 1:
         raise ValueError("width, height, and spp must all be >= 1")
@@ -117,8 +121,11 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
         raise ValueError("workers must be >= 1")
     dev = torch.device("cuda", scene.tlas.ctx.device)
     acc = torch.zeros((height * width, 4), dtype=torch.float32, device=dev)
-    rays = render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples)
-    buf = AccumBuffer(width, height, acc.cpu().numpy().astype(np.float64).reshape(height, width, 4))
+    rays = render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples, bands=bands)
+    host = torch.empty((height * width, 4), dtype=torch.float64, pin_memory=True)
+    host.copy_(acc.to(torch.float64), non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    buf = AccumBuffer(width, height, host.numpy().reshape(height, width, 4))
     if return_stats:
         return buf, {"rays": rays}
     return buf
