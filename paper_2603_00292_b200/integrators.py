@@ -106,25 +106,67 @@ def render_into(scene, accum, width, height, spp=1, integrator="pt", seed=0, cfg
     return int(rays[0]) if count_rays else None
 
 
+_PIPE_CHUNKS = 4                 # row bands of a pipelined render_frame
+_PIPE_MIN_PIXELS = 1 << 20
+_COPY_STREAMS = {}
+
+
+def _copy_stream(dev):
+    import torch
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = torch.cuda.Stream(dev)
+    return _COPY_STREAMS[dev]
+
+
 def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt", seed: int = 0,
                  workers: int = 1, cfg: Optional[IntegratorConfig] = None, jitter: bool = True,
                  return_stats: bool = False, kernel: str = "mega", samples=None, bands=None):
     """Render a full frame into a fresh AccumBuffer (float64 host copy of the fp32 device sums).
 
-    The fp32 sums are widened to float64 on the device (exact) and read back with one DMA
-    into pinned memory.  `bands=(stride, offset)` renders only that GPU's interleaved
-    4-row tile bands (the multi-GPU tile split); the other pixels stay 0."""
+    The fp32 sums are widened to float64 on the device (exact) and read back by DMA into
+    pinned memory; large megakernel frames render in 4 row chunks so each chunk's readback
+    overlaps the next chunk's render (return_stats=True renders in one launch to count
+    rays).  `bands=(stride, offset)` renders only that GPU's interleaved 4-row tile bands
+    (the multi-GPU tile split); the other pixels stay 0."""
     import torch
     if width < 1 or height < 1 or spp < 1:
         raise ValueError("width, height, and spp must all be >= 1")
     if workers < 1:
         raise ValueError("workers must be >= 1")
+    if bands is not None and int(bands[0]) == 1:
+        bands = None                                 # one GPU's "split" is the whole frame
     dev = torch.device("cuda", scene.tlas.ctx.device)
-    acc = torch.zeros((height * width, 4), dtype=torch.float32, device=dev)
-    rays = render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples, bands=bands)
-    host = torch.empty((height * width, 4), dtype=torch.float64, pin_memory=True)
-    host.copy_(acc.to(torch.float64), non_blocking=True)
-    torch.cuda.current_stream(dev).synchronize()
+    npix = height * width
+    acc = torch.zeros((npix, 4), dtype=torch.float32, device=dev)
+    host = torch.empty((npix, 4), dtype=torch.float64, pin_memory=True)
+    cur = torch.cuda.current_stream(dev)
+    stride = 1 if bands is None else int(bands[0])
+    nchunk = (_PIPE_CHUNKS if (npix >= _PIPE_MIN_PIXELS and not return_stats and kernel == "mega"
+                               and height >= 8 * stride * _PIPE_CHUNKS) else 1)
+    if nchunk == 1:
+        rays = render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples,
+                           bands=bands)
+        host.copy_(acc.to(torch.float64), non_blocking=True)
+    else:
+        # row bands (whole 4-row tiles) rendered one after another; each band is widened and
+        # read back on a copy stream while the next one renders (same pixels, same values)
+        copy = _copy_stream(dev)
+        acc64 = torch.empty((npix, 4), dtype=torch.float64, device=dev)
+        # (band chunks start on multiples of 4 * stride rows, so every row keeps its band)
+        rows = -(-height // (4 * stride * nchunk)) * 4 * stride
+        for r0 in range(0, height, rows):
+            lo, hi = r0 * width, min(height, r0 + rows) * width
+            render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples,
+                        pixels=(lo, hi), count_rays=False, bands=bands)
+            acc64[lo:hi].copy_(acc[lo:hi])
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            copy.wait_event(ev)
+            with torch.cuda.stream(copy):
+                host[lo:hi].copy_(acc64[lo:hi], non_blocking=True)
+        cur.wait_stream(copy)
+        rays = None
+    cur.synchronize()
     buf = AccumBuffer(width, height, host.numpy().reshape(height, width, 4))
     if return_stats:
         return buf, {"rays": rays}

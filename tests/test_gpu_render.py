@@ -180,3 +180,18 @@ def test_render_errors(cornell_gpu):
         render_frame(cornell_gpu, 8, 8, 1, "nope")
     with pytest.raises(ValueError):
         render_frame(cornell_gpu, 8, 8, 1, kernel="nope")
+
+
+def test_render_frame_pipelined_equals_single(native):
+    """render_frame's row-band pipeline (render band k+1 while band k is read back) gives the
+    same AccumBuffer as one full-frame render (return_stats=True takes the single path)."""
+    sc = compile_scene(scenes.cornell_description())
+    for integ, spp in (("eye", 1), ("pt", 2)):
+        a = render_frame(sc, 1280, 1000, spp, integ, seed=4)
+        b, st = render_frame(sc, 1280, 1000, spp, integ, seed=4, return_stats=True)
+        assert np.array_equal(a.data, b.data) and st["rays"] >= 1280 * 1000 * spp
+    for world in (2, 3):       # tile-band split: band chunks start on multiples of 4 * world rows
+        for g in range(world):
+            a = render_frame(sc, 1280, 1000, 1, "eye", seed=4, bands=(world, g))
+            b = render_frame(sc, 1280, 1000, 1, "eye", seed=4, bands=(world, g), return_stats=True)[0]
+            assert np.array_equal(a.data, b.data)
