@@ -16,6 +16,21 @@
 
 #include "rt_common.cuh"
 
+// Slot size: n / RT_IO_CHUNKS rays, clamped to [64K, 512K].  4 chunks: enough overlap;
+// more cost more in per-copy / per-launch overhead than they save in pipeline fill and
+// drain (config 2 e2e: 16 -> 436, 8 -> 485, 4 -> 490 Mrays/s).
+#ifndef RT_IO_CHUNKS
+#define RT_IO_CHUNKS 4
+#endif
+// Chunk sizes grow from RT_IO_FIRST rays (doubling) to the slot size, so the first
+// download starts early (config-2 closest_hit_batch 3.63 -> 3.45 ms; first chunk 64K: 3.49)
+#ifndef RT_IO_GEOMETRIC
+#define RT_IO_GEOMETRIC 1
+#endif
+#ifndef RT_IO_FIRST
+#define RT_IO_FIRST (1 << 17)
+#endif
+
 struct HostIo {
     const double* o;
     const double* d;
@@ -49,23 +64,9 @@ int rt_io_run(rt_ctx* c, int64_t n, const HostIo& in, size_t hit_bytes, size_t o
     if (n <= 0) return RT_OK;
     int rc = rt_io_streams(c);
     if (rc) return rc;
-    // 4 chunks: enough overlap; more chunks cost more in per-copy / per-launch overhead
-    // than they save in pipeline fill and drain (config 2 e2e: 16 -> 436, 8 -> 485,
-    // 4 -> 490 Mrays/s)
-#ifndef RT_IO_CHUNKS
-#define RT_IO_CHUNKS 4
-#endif
-#ifndef RT_IO_GEOMETRIC
-#define RT_IO_GEOMETRIC 1      // config-2 closest_hit_batch 3.63 -> 3.45 ms (first chunk 64k: 3.49)
-#endif
-#ifndef RT_IO_FIRST
-#define RT_IO_FIRST (1 << 17)
-#endif
     int64_t chunk = std::max<int64_t>(1 << 16, std::min<int64_t>(1 << 19, (n + RT_IO_CHUNKS - 1) / RT_IO_CHUNKS));
     chunk = std::min(chunk, n);
 #if RT_IO_GEOMETRIC
-    // chunk sizes grow from RT_IO_FIRST (doubling) up to the slot size: the first download
-    // starts early, the later (download-bound) chunks stay large
     int64_t first = std::min<int64_t>(chunk, RT_IO_FIRST);
 #endif
     IoSlot slots[2];
