@@ -206,6 +206,8 @@ __global__ void __launch_bounds__(EMIT_T, EMIT_MINB) lbvh_emit_kernel(const K* _
     const int64_t B = (int64_t)blockIdx.x * EMIT_T;
     const int64_t E = (B + EMIT_T < n) ? B + EMIT_T : n;
     s_range[tid] = -1;
+    pdl_wait();                                 // the sorted keys and order
+    pdl_trigger();
     s_delta[tid] = adj_delta(keys, n, B - 1 + tid);
     if (tid == 0) {
         s_cnt = 0;
@@ -301,6 +303,7 @@ __global__ void __launch_bounds__(128) lbvh_emit_global_kernel(const K* __restri
                                                               const unsigned int* __restrict__ seg_count,
                                                               int64_t n_blocks) {
     // one warp per segment, so every item climbs concurrently (no thread takes two)
+    pdl_wait();                                 // the emit kernel's items and slot resets
     const int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     if (seg >= n_blocks) return;
     const unsigned cnt = __ldg(seg_count + seg);

@@ -26,9 +26,9 @@ def main():
     for k, bits in enumerate((63, 30, 63, 63, 30, 30)):
         sc.tlas.build(bits)
         got = sc.tlas.download()
-        same = all(np.array_equal(got[f], fresh[bits][f]) for f in fresh[bits])
-        print("rebuild", k, bits, "same" if same else "DIFFERENT", flush=True)
-        bad += not same
+        diff = [f for f in fresh[bits] if not np.array_equal(got[f], fresh[bits][f])]
+        print("rebuild", k, bits, "same" if not diff else "DIFFERENT " + ",".join(diff), flush=True)
+        bad += bool(diff)
     sys.exit(1 if bad else 0)
 
 
