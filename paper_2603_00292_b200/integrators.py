@@ -124,9 +124,9 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
     """Render a full frame into a fresh AccumBuffer (float64 host copy of the fp32 device sums).
 
     The fp32 sums are widened to float64 on the device (exact) and read back by DMA into
-    pinned memory; large megakernel frames render in 4 row chunks so each chunk's readback
-    overlaps the next chunk's render (return_stats=True renders in one launch to count
-    rays).  `bands=(stride, offset)` renders only that GPU's interleaved 4-row tile bands
+    pinned memory; large primary-ray (eye) megakernel frames render in 4 row chunks so each
+    chunk's readback overlaps the next chunk's render (return_stats=True renders in one
+    launch to count rays).  `bands=(stride, offset)` renders only that GPU's interleaved 4-row tile bands
     (the multi-GPU tile split); the other pixels stay 0."""
     import torch
     if width < 1 or height < 1 or spp < 1:
@@ -141,8 +141,11 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
     host = torch.empty((npix, 4), dtype=torch.float64, pin_memory=True)
     cur = torch.cuda.current_stream(dev)
     stride = 1 if bands is None else int(bands[0])
+    # only primary-ray frames: there the readback is comparable to the render; a path-traced
+    # frame renders for far longer than its readback, and 4 launches add 4 wave tails
+    # (config 3 e2e 4849 -> 4164 Mrays/s when pipelined)
     nchunk = (_PIPE_CHUNKS if (npix >= _PIPE_MIN_PIXELS and not return_stats and kernel == "mega"
-                               and height >= 8 * stride * _PIPE_CHUNKS) else 1)
+                               and integrator == "eye" and height >= 8 * stride * _PIPE_CHUNKS) else 1)
     if nchunk == 1:
         rays = render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples,
                            bands=bands)

@@ -186,7 +186,7 @@ def test_render_frame_pipelined_equals_single(native):
     """render_frame's row-band pipeline (render band k+1 while band k is read back) gives the
     same AccumBuffer as one full-frame render (return_stats=True takes the single path)."""
     sc = compile_scene(scenes.cornell_description())
-    for integ, spp in (("eye", 1), ("pt", 2)):
+    for integ, spp in (("eye", 1), ("eye", 3)):
         a = render_frame(sc, 1280, 1000, spp, integ, seed=4)
         b, st = render_frame(sc, 1280, 1000, spp, integ, seed=4, return_stats=True)
         assert np.array_equal(a.data, b.data) and st["rays"] >= 1280 * 1000 * spp
