@@ -60,6 +60,16 @@ def load_traffic(key, per=1.0):
         return None
 
 
+def load_issue(key):
+    """SM issue-slot utilisation (%) of the same capture (the ceiling that binds the
+    L1-resident, issue-bound traversal); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)[key].get("issue_active_pct")
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         with open(PEAKS_PATH) as f:
@@ -423,7 +433,9 @@ def run_ours(args, ws, rank, local):
                                    f"tests + 32 B accumulation RMW per ray (node/test counts: stats build of the "
                                    f"trace kernel on this rank's primary rays{'' if C in (2, 4) else '; bounce rays assumed alike'})",
                   "note": "node/triangle fetches mostly hit L1/L2 (ncu: DRAM 1-2% of peak); the bound that "
-                          "binds is SM issue/latency, see profiles/"}
+                          "binds is SM issue/latency, see profiles/",
+                  "sm_issue_active_pct": load_issue(traffic_key[0]),
+                  "sm_issue_source": "smsp__issue_active.avg.pct_of_peak_sustained_active of the same ncu capture"}
     roof_trace["frac"] = roof_trace["achieved"] / peak_gbs
     line_extra = {}
     dominant = roof_trace
@@ -436,7 +448,8 @@ def run_ours(args, ws, rank, local):
                       "traffic_source": "profiles/ncu_traffic.json (ncu --set full of one build, each kernel "
                                         "with cold caches)",
                       "bytes_formula": f"328 B/tri x {tl.n} tris (SURVEY 8(d), 30-bit keys)",
-                      "stage_ms": stages, "peak_source": peak_src}
+                      "stage_ms": stages, "peak_source": peak_src,
+                      "sm_issue_active_pct": load_issue("config2_build" if C == 2 else "config4_build")}
         roof_build["frac"] = roof_build["achieved"] / peak_gbs
         if t_build > t_render:
             dominant, other = roof_build, roof_trace

@@ -1,4 +1,4 @@
-"""DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) per kernel launch from ncu
+"""DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum) and SM issue utilisation per kernel launch from ncu
 --set full reports -> profiles/ncu_traffic.json (read by bench.py for roofline.traffic).
 
     python tools/ncu_traffic.py KEY=report.ncu-rep[:kernel-regex] ... > profiles/ncu_traffic.json
@@ -30,7 +30,8 @@ def launches(rep):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
         unit_w = rows[1][h.index("dram__bytes_write.sum")] if "dram__bytes_write.sum" in h else "byte"
         scale_w = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_w, 1)
-        res.append((d.get("Kernel Name", ""), num("dram__bytes_read.sum") * scale + num("dram__bytes_write.sum") * scale_w))
+        res.append((d.get("Kernel Name", ""), num("dram__bytes_read.sum") * scale + num("dram__bytes_write.sum") * scale_w,
+                    num("gpu__time_duration.sum"), num("smsp__issue_active.avg.pct_of_peak_sustained_active")))
     return res
 
 
@@ -38,7 +39,11 @@ out = {}
 for arg in sys.argv[1:]:
     key, spec = arg.split("=", 1)
     rep, _, rx = spec.partition(":")
-    sel = [(k, b) for k, b in launches(rep) if not rx or re.search(rx, k)]
-    out[key] = {"bytes": sum(b for _, b in sel), "launches": len(sel), "report": rep.rsplit("/", 1)[-1],
-                "kernels": sorted({re.sub(r"\(.*", "", k).replace("<unnamed>::", "") for k, _ in sel})}
+    sel = [x for x in launches(rep) if not rx or re.search(rx, x[0])]
+    dur = sum(x[2] for x in sel) or 1.0
+    out[key] = {"bytes": sum(x[1] for x in sel), "launches": len(sel), "report": rep.rsplit("/", 1)[-1],
+                # SM issue-slot utilisation (duration-weighted over the launches): the ceiling
+                # of the L1-resident, issue-bound traversal
+                "issue_active_pct": round(sum(x[2] * x[3] for x in sel) / dur, 2),
+                "kernels": sorted({re.sub(r"\(.*", "", x[0]).replace("<unnamed>::", "") for x in sel})}
 print(json.dumps(out, indent=1))
