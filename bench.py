@@ -323,9 +323,15 @@ def run_ours(args, ws, rank, local):
         if C in (2, 4):
             from paper_2603_00292_b200 import render_frame
             from paper_2603_00292_b200._native import host_pinned_copy
-            host_tris = host_pinned_copy(tl.tris)           # the step's vertices in pinned host memory
-            # (1) the reference arm's own path: refit(host vertices) + render_frame('eye') -> host
+            host_tris = host_pinned_copy(tl.tris)           # world rows, for the query path below
+            # the step's vertices in pinned host memory: the synthetic meshes are fp32 values
+            # (SURVEY 8(d)), so their fp32 array is exact and refit_mesh widens it on the device
+            mesh_v = desc.meshes["mesh"].vertices
+            host_v = host_pinned_copy(np.ascontiguousarray(mesh_v, np.float32))
+            assert np.array_equal(host_v.astype(np.float64), mesh_v)
+            # (1) the reference arm's own path: refit(mesh vertices) + render_frame('eye') -> host
             #     float64 AccumBuffer (H2D: the vertices; D2H: the (H, W, 4) float64 sums)
+            sc.refit_mesh("mesh", host_v, bits=30)
             render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
             ke = max(3, min(K, 10))
             if ws > 1:
@@ -333,13 +339,14 @@ def run_ours(args, ws, rank, local):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(ke):
-                tl.refit(host_tris, 30)
+                sc.refit_mesh("mesh", host_v, bits=30)
                 render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
             torch.cuda.synchronize()
             te = time.perf_counter() - t0
-            h2d, d2h = int(host_tris.nbytes), int(npix * 32)
-            path = ("GpuTlas.refit(host fp32 vertices: H2D + LBVH rebuild) + render_frame('eye') -> host float64 "
-                    "AccumBuffer (H, W, 4); the reference arm times the same calls")
+            h2d, d2h = int(host_v.nbytes), int(npix * 32)
+            path = ("Scene.refit_mesh(host mesh vertices, Blas.refit semantics: H2D + device world rows/normals + "
+                    "LBVH rebuild) + render_frame('eye') -> host float64 AccumBuffer (H, W, 4); the reference arm "
+                    "times compile + the same render call")
             rays_e2e = my_rays
             # (2) the query API: refit + closest_hit_batch(host float64 rays) of this rank's rays
             r = prim.cpu().numpy().astype(np.float64)

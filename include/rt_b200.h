@@ -44,6 +44,7 @@ extern "C" {
 typedef struct rt_ctx rt_ctx;
 typedef struct rt_scene rt_scene;
 typedef struct rt_tlas rt_tlas;
+typedef struct rt_mesh rt_mesh;
 
 /* Frame parameters: render_frame(scene, width, height, spp, integrator, seed,
  * workers, cfg, jitter) -- integrators.py:426-473.  Samples [s0, s1) are
@@ -106,6 +107,27 @@ int rt_scene_set_spheres(rt_ctx* ctx, rt_scene* scene, int32_t n_spheres, const 
 /* new vertex positions for the same triangles (Blas.refit(vertices), accel.py:263-283);
  * host (n, 9) fp32, copied on the context stream; the BVH must be rebuilt */
 int rt_scene_set_vertices(rt_ctx* ctx, rt_scene* scene, const float* tris);
+
+/* Device-side refit from the reference's own input (Blas.refit(vertices), accel.py:263-283):
+ * an indexed mesh whose faces stay resident on the device, instanced into the flat scene
+ * at n_inst triangle offsets.  xform: n_inst rows of 21 doubles = the instance 3x4 matrix
+ * (row-major, accel.py:311-336) then the 3x3 block of its inverse (row-major).
+ * rt_scene_refit_mesh uploads the vertices (nv, 3) (the count fixed at create) as float64,
+ * or as fp32 when vertices_f32 != 0 (widened exactly on the device), then one kernel writes
+ * every instance's world triangles (fp32) and world normals exactly as compile_scene does
+ * on the host (float64, reference operation order, no FMA; normals per accel.py:843-847
+ * from the local geometry.py:229-237 normal).  The BVH must be rebuilt. */
+int rt_mesh_create(rt_ctx* ctx, int64_t n_vertices, int64_t n_faces, const int32_t* faces, int32_t n_inst,
+                   const double* xform, const int64_t* tri_offset, rt_mesh** out);
+int rt_scene_refit_mesh(rt_ctx* ctx, rt_scene* scene, rt_mesh* mesh, int64_t n_vertices, const void* vertices,
+                        int32_t vertices_f32);
+void rt_mesh_destroy(rt_mesh* mesh);
+/* world normals of the scene's triangles recomputed on the device from its current (world)
+ * vertices, float64 in the reference order with an identity frame (after
+ * rt_scene_set_vertices, whose rows are world triangles) */
+int rt_scene_update_normals(rt_ctx* ctx, rt_scene* scene);
+/* the scene's current (n, 9) fp32 triangle rows, device -> host (synchronises) */
+int rt_scene_get_vertices(rt_ctx* ctx, rt_scene* scene, float* tris);
 
 /* ---- LBVH build (replaces _build_bvh, accel.py:68-187; K1-K5) ---------- */
 /* morton_bits: 30 or 63.  build_ms (nullable): device time of the build

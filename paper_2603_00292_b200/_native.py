@@ -106,6 +106,10 @@ def lib():
             "rt_tlas_flatten": [vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, i32, vp],
             "rt_tlas_closest_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp, vp, vp, vp, vp, vp, vp],
             "rt_tlas_any_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp],
+            "rt_mesh_create": [vp, i64, i64, vp, i32, vp, vp, vp],
+            "rt_scene_refit_mesh": [vp, vp, vp, i64, vp, i32],
+            "rt_scene_update_normals": [vp, vp],
+            "rt_scene_get_vertices": [vp, vp, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -117,6 +121,8 @@ def lib():
         L.rt_scene_destroy.restype = None
         L.rt_tlas_destroy.argtypes = [vp]
         L.rt_tlas_destroy.restype = None
+        L.rt_mesh_destroy.argtypes = [vp]
+        L.rt_mesh_destroy.restype = None
         _lib = L
         return L
 

@@ -52,7 +52,7 @@ class GpuTlas:
         self.ctx = ctx
         self.n = int(tris.shape[0])
         self.bits = bits
-        self.tris = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
+        self._tris = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
         self.normals = np.ascontiguousarray(normals, np.float32).reshape(-1, 3)
         self.tri_inst = np.ascontiguousarray(tri_inst, np.int32)
         self.tri_prim = np.ascontiguousarray(tri_prim, np.int32)
@@ -64,7 +64,7 @@ class GpuTlas:
         mc = np.ascontiguousarray(mat_color, np.float32).reshape(-1, 3)
         me = np.ascontiguousarray(mat_emissive, np.float32).reshape(-1, 3)
         h = ctypes.c_void_p()
-        check(lib().rt_scene_create(ctx.handle, self.n, ptr(self.tris), ptr(self.normals), ptr(self.tri_inst),
+        check(lib().rt_scene_create(ctx.handle, self.n, ptr(self._tris), ptr(self.normals), ptr(self.tri_inst),
                                     ptr(self.tri_prim), ptr(self.tri_mask), ptr(self.tri_material), ptr(mc),
                                     ptr(me), mc.shape[0], ctypes.byref(h)))
         self.handle = h
@@ -91,13 +91,24 @@ class GpuTlas:
             return ms.value
         return None
 
+    @property
+    def tris(self):
+        """(n, 9) fp32 world triangle rows (read back from the device after a device refit)."""
+        if self._tris is None:
+            t = np.empty((self.n, 9), np.float32)
+            check(lib().rt_scene_get_vertices(self.ctx.handle, self.handle, ptr(t)))
+            self._tris = t
+        return self._tris
+
     def refit(self, tris, bits=None):
-        """New world vertices for the same triangles (Blas.refit, accel.py:263-283): H2D + rebuild."""
+        """New world vertices for the same triangles (Blas.refit, accel.py:263-283): H2D, the
+        world normals recomputed on the device from them, rebuild."""
         tris = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
         if tris.shape[0] != self.n:
             raise ValueError(f"triangle count changed ({self.n} -> {tris.shape[0]})")
         check(lib().rt_scene_set_vertices(self.ctx.handle, self.handle, ptr(tris)))
-        self.tris = tris
+        check(lib().rt_scene_update_normals(self.ctx.handle, self.handle))
+        self._tris = tris
         self.build(bits)
 
     @classmethod
@@ -105,7 +116,7 @@ class GpuTlas:
         """Wrap a scene built on the device (rt_tlas_flatten); host geometry copies absent."""
         self = cls.__new__(cls)
         self.ctx, self.handle, self.n, self.bits = ctx, handle, int(n), bits
-        self.tris = self.normals = self.tri_inst = self.tri_prim = self.tri_mask = self.tri_material = None
+        self._tris = self.normals = self.tri_inst = self.tri_prim = self.tri_mask = self.tri_material = None
         self.inverses = self.n_instances = None
         self.world_root = (None, None)
         self.build_ms = None
@@ -164,10 +175,74 @@ class Scene:
     background: np.ndarray
     root_box: tuple
     render_tlas: object = None   # two-level scenes: the device-flattened structure rt_render walks
+    _meshes: dict = None         # flat scenes: mesh name -> _MeshRefit (device refit_mesh)
+    _light_src: tuple = None     # (desc, material index, instances) the light table came from
 
     def diagonal(self) -> float:
         d = self.root_box[1] - self.root_box[0]
         return math.sqrt(float(d @ d))
+
+    def refit_mesh(self, name, vertices, bits=None):
+        """Blas.refit(vertices) (accel.py:263-283) for every instance of mesh `name` of a flat
+        scene, on the device: the vertices go up (float64, or float32 as given: 24 or 12 B per
+        vertex; the faces stay resident), one kernel writes the instances' world triangles and world normals exactly
+        as compile_scene does on the host, and the LBVH is rebuilt.  The scene's root
+        box and normal offset keep their compile-time values, as the reference's Scene does."""
+        if self.render_tlas is not None or self._meshes is None:
+            raise ValueError("refit_mesh needs a flat scene (two-level scenes refit their Blas)")
+        if name not in self._meshes:
+            raise ValueError(f"unknown mesh {name!r}")
+        mr = self._meshes[name]
+        # float32 input goes up as is (half the bytes) and is widened exactly on the device
+        f32 = isinstance(vertices, np.ndarray) and vertices.dtype == np.float32
+        V = np.ascontiguousarray(vertices, np.float32 if f32 else np.float64).reshape(-1, 3)
+        if V.shape[0] != mr.nv:
+            raise ValueError(f"vertex count changed ({mr.nv} -> {V.shape[0]})")
+        tl = self.tlas
+        check(lib().rt_scene_refit_mesh(tl.ctx.handle, tl.handle, mr.handle(tl.ctx), mr.nv, ptr(V), 1 if f32 else 0))
+        tl._tris = None                          # the host copy is read back on demand
+        desc, mat_index, inst_list = self._light_src
+        if any(desc.materials[d.material].has_emission for d, _ in inst_list if d.mesh == name):
+            # emissive instances of this mesh: the light table follows the new vertices
+            import dataclasses
+            meshes = dict(desc.meshes)
+            meshes[name] = dataclasses.replace(meshes[name], vertices=V.astype(np.float64))
+            self._light_src = (dataclasses.replace(desc, meshes=meshes), mat_index, inst_list)
+            self.lights = _light_rows(self._light_src[0], mat_index, inst_list)
+            rows = np.ascontiguousarray(np.concatenate([self.lights.v0, self.lights.v1, self.lights.v2,
+                                                        self.lights.normal, self.lights.emissive,
+                                                        self.lights.area[:, None]], axis=1), np.float32)
+            check(lib().rt_scene_set_lights(tl.ctx.handle, tl.handle, rows.shape[0], ptr(rows)))
+        tl.build(bits)
+
+
+class _MeshRefit:
+    """One mesh of a flat scene for Scene.refit_mesh: faces + instance frames, uploaded on
+    first use (rt_mesh_create)."""
+
+    def __init__(self, nv, faces, inst):
+        self.nv = int(nv)
+        self.faces = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
+        # rows of 21 doubles: the 3x4 matrix, then the 3x3 block of its inverse
+        self.xform = np.ascontiguousarray([np.concatenate([m.reshape(12), inv[:, :3].reshape(9)]) for m, inv, _ in inst],
+                                          np.float64)
+        self.offset = np.ascontiguousarray([o for _, _, o in inst], np.int64)
+        self._h = None
+
+    def handle(self, ctx):
+        if self._h is None:
+            h = ctypes.c_void_p()
+            check(lib().rt_mesh_create(ctx.handle, self.nv, self.faces.shape[0], ptr(self.faces), len(self.offset),
+                                       ptr(self.xform), ptr(self.offset), ctypes.byref(h)))
+            self._h = h
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h and _native._lib is not None:
+                _native._lib.rt_mesh_destroy(self._h)
+        except Exception:
+            pass
 
 
 def _local_normals(V, F):
@@ -227,8 +302,6 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
         raise ValueError(f"unknown build quality {quality!r}, expected one of {tuple(QUALITIES)}")
     if two_level:
         return _compile_two_level(desc, quality, device)
-    if quality not in QUALITIES:
-        raise ValueError(f"unknown build quality {quality!r}, expected one of {tuple(QUALITIES)}")
     mat_names = list(desc.materials)
     mat_index = {n: i for i, n in enumerate(mat_names)}
     mat_color = np.array([desc.materials[n].color for n in mat_names]).reshape(-1, 3)
@@ -255,6 +328,8 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
     tris, normals, t_inst, t_prim, t_mask, t_mat = [], [], [], [], [], []
     inst_material, inst_list, inverses = [], [], []
     wlo, whi = [], []
+    mesh_inst = {}                 # mesh name -> [(3x4 matrix, inverse, first flat triangle)]
+    off = 0
     for i, decl in enumerate(desc.instances):
         V, F, rlo, rhi, ln = mesh_cache[decl.mesh]
         m = frame_to_matrix(decl.frame)
@@ -262,6 +337,8 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
             inv = invert_affine(m)
         except ValueError as exc:
             raise BuildError(f"instance {i} frame is not invertible") from exc
+        mesh_inst.setdefault(decl.mesh, []).append((m, inv, off))
+        off += F.shape[0]
         inverses.append(inv)
         inst_list.append((decl, m))
         # world AABB of the 8 root-box corners (accel.py:459-469)
@@ -336,11 +413,15 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
         rows = np.ascontiguousarray(np.concatenate([lights.v0, lights.v1, lights.v2, lights.normal, lights.emissive,
                                                     lights.area[:, None]], axis=1), np.float32)
         check(lib().rt_scene_set_lights(ctx.handle, tlas.handle, rows.shape[0], ptr(rows)))
-    return Scene(camera=desc.camera, tlas=tlas, registry=registry, mat_color=mat_color, mat_emissive=mat_emissive,
-                 inst_material=np.array(inst_material, np.int64), lights=lights,
-                 sky=np.ascontiguousarray(desc.sky, np.float64), background=np.ascontiguousarray(desc.background,
-                                                                                                 np.float64),
-                 root_box=(root_lo, root_hi))
+    sc = Scene(camera=desc.camera, tlas=tlas, registry=registry, mat_color=mat_color, mat_emissive=mat_emissive,
+               inst_material=np.array(inst_material, np.int64), lights=lights,
+               sky=np.ascontiguousarray(desc.sky, np.float64), background=np.ascontiguousarray(desc.background,
+                                                                                               np.float64),
+               root_box=(root_lo, root_hi))
+    sc._meshes = {name: _MeshRefit(mesh_cache[name][0].shape[0], mesh_cache[name][1], inst)
+                  for name, inst in mesh_inst.items()}
+    sc._light_src = (desc, mat_index, inst_list)
+    return sc
 
 
 def _compile_two_level(desc, quality, device):
