@@ -117,8 +117,10 @@ int rt_scene_set_vertices(rt_ctx* ctx, rt_scene* scene, const float* tris);
  * every instance's world triangles (fp32) and world normals exactly as compile_scene does
  * on the host (float64, reference operation order, no FMA; normals per accel.py:843-847
  * from the local geometry.py:229-237 normal).  The BVH must be rebuilt. */
+#define RT_MESH_LOCAL 1   /* a BLAS (two-level Blas.refit): one placement at offset 0, rows = the local
+                             vertices, float64 local normals into rt_scene_set_local_normals' array */
 int rt_mesh_create(rt_ctx* ctx, int64_t n_vertices, int64_t n_faces, const int32_t* faces, int32_t n_inst,
-                   const double* xform, const int64_t* tri_offset, rt_mesh** out);
+                   const double* xform, const int64_t* tri_offset, int32_t flags, rt_mesh** out);
 int rt_scene_refit_mesh(rt_ctx* ctx, rt_scene* scene, rt_mesh* mesh, int64_t n_vertices, const void* vertices,
                         int32_t vertices_f32);
 void rt_mesh_destroy(rt_mesh* mesh);

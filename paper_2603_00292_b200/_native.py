@@ -106,7 +106,7 @@ def lib():
             "rt_tlas_flatten": [vp, vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, vp, i32, vp],
             "rt_tlas_closest_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp, vp, vp, vp, vp, vp, vp],
             "rt_tlas_any_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp],
-            "rt_mesh_create": [vp, i64, i64, vp, i32, vp, vp, vp],
+            "rt_mesh_create": [vp, i64, i64, vp, i32, vp, vp, i32, vp],
             "rt_scene_refit_mesh": [vp, vp, vp, i64, vp, i32],
             "rt_scene_update_normals": [vp, vp],
             "rt_scene_get_vertices": [vp, vp, vp],

@@ -230,6 +230,7 @@ struct rt_mesh {
     int device;
     int64_t nv, nf;
     int32_t n_inst;
+    int32_t local;        // RT_MESH_LOCAL: rows = the local vertices, float64 local normals
     int3* faces;          // (nf) device
     double* xform;        // (n_inst, 21) device
     int64_t* offset;      // (n_inst) device: first flat triangle of each instance
@@ -249,7 +250,7 @@ template <typename T>
 __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __restrict__ faces,
                                   const T* __restrict__ Vt, const double* __restrict__ xform,
                                   const int64_t* __restrict__ offset, float* __restrict__ tris,
-                                  float4* __restrict__ attr) {
+                                  float4* __restrict__ attr, double* __restrict__ lnormal64) {
     const int64_t total = nf * n_inst;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
         const int32_t j = (int32_t)(q / nf);
@@ -263,10 +264,18 @@ __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __rest
         const double c[3] = {(double)Vt[3 * (int64_t)f.z], (double)Vt[3 * (int64_t)f.z + 1], (double)Vt[3 * (int64_t)f.z + 2]};
         float* t = tris + 9 * (offset[j] + k);
         const double* vs[3] = {a, b, c};
+        if (lnormal64) {       // a BLAS: its rows are the local vertices themselves (Blas._rows)
 #pragma unroll
-        for (int v = 0; v < 3; ++v)
+            for (int v = 0; v < 3; ++v)
 #pragma unroll
-            for (int r = 0; r < 3; ++r) t[3 * v + r] = __double2float_rn(dot3_affine(m + 4 * r, vs[v][0], vs[v][1], vs[v][2]));
+                for (int r = 0; r < 3; ++r) t[3 * v + r] = __double2float_rn(vs[v][r]);
+        } else {
+#pragma unroll
+            for (int v = 0; v < 3; ++v)
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+                    t[3 * v + r] = __double2float_rn(dot3_affine(m + 4 * r, vs[v][0], vs[v][1], vs[v][2]));
+        }
         // local normal (geometry.py:229-237): e0 = b - a, e1 = c - b, n = e0 x e1 / |n|
         const double e0x = __dsub_rn(b[0], a[0]), e0y = __dsub_rn(b[1], a[1]), e0z = __dsub_rn(b[2], a[2]);
         const double e1x = __dsub_rn(c[0], b[0]), e1y = __dsub_rn(c[1], b[1]), e1z = __dsub_rn(c[2], b[2]);
@@ -275,6 +284,11 @@ __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __rest
         const double nz = __dsub_rn(__dmul_rn(e0x, e1y), __dmul_rn(e0y, e1x));
         const double nlen = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(nx, nx), __dmul_rn(ny, ny)), __dmul_rn(nz, nz)));
         const double lx = __ddiv_rn(nx, nlen), ly = __ddiv_rn(ny, nlen), lz = __ddiv_rn(nz, nlen);
+        if (lnormal64) {       // the two-level kernels transform the float64 local normal per hit
+            double* ln = lnormal64 + 3 * (offset[j] + k);
+            ln[0] = lx; ln[1] = ly; ln[2] = lz;
+            continue;
+        }
         // world normal (accel.py:843-847): inverse-transpose sum, times 1 / sqrt(|w|^2)
         const double wx = __dadd_rn(__dadd_rn(__dmul_rn(inv[0], lx), __dmul_rn(inv[3], ly)), __dmul_rn(inv[6], lz));
         const double wy = __dadd_rn(__dadd_rn(__dmul_rn(inv[1], lx), __dmul_rn(inv[4], ly)), __dmul_rn(inv[7], lz));
@@ -336,9 +350,10 @@ int rt_scene_get_vertices(rt_ctx* c, rt_scene* s, float* tris) {
 }
 
 int rt_mesh_create(rt_ctx* c, int64_t n_vertices, int64_t n_faces, const int32_t* faces, int32_t n_inst,
-                   const double* xform, const int64_t* tri_offset, rt_mesh** out) {
+                   const double* xform, const int64_t* tri_offset, int32_t flags, rt_mesh** out) {
     RT_CHECK_ARG(c && faces && xform && tri_offset && out, "NULL argument");
     RT_CHECK_ARG(n_vertices >= 3 && n_faces >= 1 && n_inst >= 1, "empty mesh or no instance");
+    RT_CHECK_ARG(!(flags & RT_MESH_LOCAL) || n_inst == 1, "a local (BLAS) mesh has exactly one placement");
     for (int64_t k = 0; k < 3 * n_faces; ++k)
         RT_CHECK_ARG(faces[k] >= 0 && faces[k] < n_vertices, "face index out of range");
     RT_CUDA_TRY(cudaSetDevice(c->device));
@@ -347,6 +362,7 @@ int rt_mesh_create(rt_ctx* c, int64_t n_vertices, int64_t n_faces, const int32_t
     m->nv = n_vertices;
     m->nf = n_faces;
     m->n_inst = n_inst;
+    m->local = (flags & RT_MESH_LOCAL) ? 1 : 0;
     cudaError_t e = cudaMalloc(&m->faces, sizeof(int3) * n_faces);
     if (e == cudaSuccess) e = cudaMalloc(&m->xform, sizeof(double) * 21 * n_inst);
     if (e == cudaSuccess) e = cudaMalloc(&m->offset, sizeof(int64_t) * n_inst);
@@ -371,7 +387,12 @@ int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, 
         rt_set_error("vertex count changed (%lld -> %lld)", (long long)m->nv, (long long)n_vertices);
         return RT_EINVAL;
     }
+    if (m->local && !s->lnormal64) {
+        rt_set_error("a local (BLAS) mesh refits a scene with float64 local normals");
+        return RT_EINVAL;
+    }
     RT_CUDA_TRY(cudaSetDevice(c->device));
+    double* ln = m->local ? s->lnormal64 : nullptr;
     const size_t vbytes = (vertices_f32 ? sizeof(float) : sizeof(double)) * 3 * m->nv;
     RT_CUDA_TRY(cudaMemcpyAsync(m->verts, vertices, vbytes, cudaMemcpyHostToDevice, c->stream));
     const int64_t total = m->nf * m->n_inst;
@@ -379,10 +400,11 @@ int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, 
     if (grid > (int64_t)c->num_sms * 16) grid = (int64_t)c->num_sms * 16;
     if (vertices_f32)
         refit_mesh_kernel<float><<<(unsigned)grid, 256, 0, c->stream>>>(
-            m->nf, m->n_inst, m->faces, reinterpret_cast<const float*>(m->verts), m->xform, m->offset, s->tris, s->tri_attr);
+            m->nf, m->n_inst, m->faces, reinterpret_cast<const float*>(m->verts), m->xform, m->offset, s->tris, s->tri_attr,
+            ln);
     else
         refit_mesh_kernel<double><<<(unsigned)grid, 256, 0, c->stream>>>(m->nf, m->n_inst, m->faces, m->verts, m->xform,
-                                                                         m->offset, s->tris, s->tri_attr);
+                                                                         m->offset, s->tris, s->tri_attr, ln);
     RT_CUDA_TRY(cudaGetLastError());
     s->built = 0;
     return RT_OK;

@@ -220,8 +220,9 @@ class _MeshRefit:
     """One mesh of a flat scene for Scene.refit_mesh: faces + instance frames, uploaded on
     first use (rt_mesh_create)."""
 
-    def __init__(self, nv, faces, inst):
+    def __init__(self, nv, faces, inst, flags=0):
         self.nv = int(nv)
+        self.flags = int(flags)
         self.faces = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
         # rows of 21 doubles: the 3x4 matrix, then the 3x3 block of its inverse
         self.xform = np.ascontiguousarray([np.concatenate([m.reshape(12), inv[:, :3].reshape(9)]) for m, inv, _ in inst],
@@ -233,7 +234,7 @@ class _MeshRefit:
         if self._h is None:
             h = ctypes.c_void_p()
             check(lib().rt_mesh_create(ctx.handle, self.nv, self.faces.shape[0], ptr(self.faces), len(self.offset),
-                                       ptr(self.xform), ptr(self.offset), ctypes.byref(h)))
+                                       ptr(self.xform), ptr(self.offset), self.flags, ctypes.byref(h)))
             self._h = h
         return self._h
 

@@ -68,6 +68,7 @@ class Blas:
         self.geom_type = int(geom_type)
         self.data_offset = int(data_offset)
         self.handle = None
+        self._mesh = None          # device faces for refit (scene._MeshRefit), made on first refit
         self.version = 0
         rows = self._rows()
         n = rows.shape[0]
@@ -161,8 +162,17 @@ class Blas:
                 raise ValueError(f"vertex count changed ({self.vertices.shape[0]} -> {vertices.shape[0]})")
             self._check_finite_tris(vertices, self.faces)
             self.vertices = vertices
-            check(lib().rt_scene_set_local_normals(self.ctx.handle, self.handle,
-                                                   ptr(_local_normals64(vertices, self.faces))))
+            # faces stay on the device: the vertices go up and one kernel writes the local
+            # rows and float64 local normals (as _rows / _local_normals64 would, bit for bit)
+            if self._mesh is None:
+                from .scene import _MeshRefit
+                ident = np.hstack([np.eye(3), np.zeros((3, 1))])
+                self._mesh = _MeshRefit(vertices.shape[0], self.faces, [(ident, ident, 0)], flags=1)
+            check(lib().rt_scene_refit_mesh(self.ctx.handle, self.handle, self._mesh.handle(self.ctx),
+                                            vertices.shape[0], ptr(vertices), 0))
+            self._build()
+            self.version += 1
+            return
         else:
             if aabbs is None:
                 raise ValueError("custom refit needs updated AABBs")
