@@ -163,6 +163,7 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
 }
 
 int rt_scene_set_materials(rt_ctx* c, rt_scene* s, const float* mat_color, const float* mat_emissive) {
+    RT_CUDA_TRY(cudaSetDevice(c->device));      // the scene's buffers live on the context's device
     std::vector<float4> mc(s->n_mat), me(s->n_mat);
     for (int k = 0; k < s->n_mat; ++k) {
         mc[k] = make_float4(mat_color[3 * k], mat_color[3 * k + 1], mat_color[3 * k + 2], 0.f);
