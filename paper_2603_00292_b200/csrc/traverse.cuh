@@ -16,6 +16,28 @@
 #define RT_FMA_SLABS 1
 #endif
 
+// One BVH4 node (128 B, 128-B aligned) as four 256-bit read-only loads (sm_100's
+// LDG.E.256) instead of eight 128-bit ones.
+#ifndef RT_LDG256
+#define RT_LDG256 1
+#endif
+__device__ __forceinline__ void ldg_pair(const float4* p, float4& a, float4& b) {
+#if RT_LDG256
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+#else
+    a = __ldg(p);
+    b = __ldg(p + 1);
+#endif
+}
+#define RT_LOAD_NODE4(q)                       \
+    float4 l0, h0, l1, h1, l2, h2, l3, h3;     \
+    ldg_pair((q), l0, h0);                     \
+    ldg_pair((q) + 2, l1, h1);                 \
+    ldg_pair((q) + 4, l2, h2);                 \
+    ldg_pair((q) + 6, l3, h3)
+
 struct RayPre {
     float ox, oy, oz, tmin;
     float dx, dy, dz;          // only the sphere test reads these (dead code for triangle walks)
@@ -312,8 +334,7 @@ __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, in
         if (node >= 0) {
             // 4 slots of (lo.xyz, id), (hi.xyz, -)
             const float4* q = bvh4 + 8 * node;
-            const float4 l0 = __ldg(q), h0 = __ldg(q + 1), l1 = __ldg(q + 2), h1 = __ldg(q + 3);
-            const float4 l2 = __ldg(q + 4), h2 = __ldg(q + 5), l3 = __ldg(q + 6), h3 = __ldg(q + 7);
+            RT_LOAD_NODE4(q);
             if (STATS) ++n_visits;
             float t0 = box_enter(R, l0.x, h0.x, l0.y, h0.y, l0.z, h0.z, h.t);
             float t1 = box_enter(R, l1.x, h1.x, l1.y, h1.y, l1.z, h1.z, h.t);
@@ -379,8 +400,7 @@ __device__ __forceinline__ bool trace_any4(const float4* __restrict__ bvh4, int 
     while (node != RT_SENTINEL) {
         if (node >= 0) {
             const float4* q = bvh4 + 8 * node;
-            const float4 l0 = __ldg(q), h0 = __ldg(q + 1), l1 = __ldg(q + 2), h1 = __ldg(q + 3);
-            const float4 l2 = __ldg(q + 4), h2 = __ldg(q + 5), l3 = __ldg(q + 6), h3 = __ldg(q + 7);
+            RT_LOAD_NODE4(q);
             const bool b0 = box_enter(R, l0.x, h0.x, l0.y, h0.y, l0.z, h0.z, tmax) != INFINITY;
             const bool b1 = box_enter(R, l1.x, h1.x, l1.y, h1.y, l1.z, h1.z, tmax) != INFINITY;
             const bool b2 = box_enter(R, l2.x, h2.x, l2.y, h2.y, l2.z, h2.z, tmax) != INFINITY;
@@ -420,8 +440,7 @@ __device__ __forceinline__ void walk4(const float4* __restrict__ bvh4, int root,
     while (node != RT_SENTINEL) {
         if (node >= 0) {
             const float4* q = bvh4 + 8 * node;
-            const float4 l0 = __ldg(q), h0 = __ldg(q + 1), l1 = __ldg(q + 2), h1 = __ldg(q + 3);
-            const float4 l2 = __ldg(q + 4), h2 = __ldg(q + 5), l3 = __ldg(q + 6), h3 = __ldg(q + 7);
+            RT_LOAD_NODE4(q);
             if (STATS) ++n_visits;
             float t0 = box_enter(R, l0.x, h0.x, l0.y, h0.y, l0.z, h0.z, best_t);
             float t1 = box_enter(R, l1.x, h1.x, l1.y, h1.y, l1.z, h1.z, best_t);
@@ -462,8 +481,7 @@ __device__ __forceinline__ bool walk_any4(const float4* __restrict__ bvh4, int r
     while (node != RT_SENTINEL) {
         if (node >= 0) {
             const float4* q = bvh4 + 8 * node;
-            const float4 l0 = __ldg(q), h0 = __ldg(q + 1), l1 = __ldg(q + 2), h1 = __ldg(q + 3);
-            const float4 l2 = __ldg(q + 4), h2 = __ldg(q + 5), l3 = __ldg(q + 6), h3 = __ldg(q + 7);
+            RT_LOAD_NODE4(q);
             if (box_enter(R, l3.x, h3.x, l3.y, h3.y, l3.z, h3.z, tmax) != INFINITY) stack[++sp] = __float_as_int(l3.w);
             if (box_enter(R, l2.x, h2.x, l2.y, h2.y, l2.z, h2.z, tmax) != INFINITY) stack[++sp] = __float_as_int(l2.w);
             if (box_enter(R, l1.x, h1.x, l1.y, h1.y, l1.z, h1.z, tmax) != INFINITY) stack[++sp] = __float_as_int(l1.w);
