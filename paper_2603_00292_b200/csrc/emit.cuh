@@ -38,14 +38,27 @@ struct EmitNode {
 // children, or itself if a leaf -- with no cross-thread reads.  Layout: 4 slots
 // of 2 float4 = (lo.xyz, child id), (hi.xyz, 0); the child id is the split
 // position of an internal grandchild or ~leaf.  A half is 64 contiguous bytes.
+#ifndef RT_STG256
+#define RT_STG256 1
+#endif
 __device__ __forceinline__ void bvh4_write_half(float4* __restrict__ bvh4, int pgamma, int side, const float a_lo[3],
                                                 const float a_hi[3], int a_id, const float b_lo[3],
                                                 const float b_hi[3], int b_id) {
     float4* q = bvh4 + 8 * (int64_t)pgamma + 4 * side;
+#if RT_STG256
+    // two 256-bit stores (sm_100 STG.E.256) per 64-B half; the half is 64-B aligned
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(q), "f"(a_lo[0]), "f"(a_lo[1]),
+                 "f"(a_lo[2]), "f"(__int_as_float(a_id)), "f"(a_hi[0]), "f"(a_hi[1]), "f"(a_hi[2]), "f"(0.0f)
+                 : "memory");
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(q + 2), "f"(b_lo[0]), "f"(b_lo[1]),
+                 "f"(b_lo[2]), "f"(__int_as_float(b_id)), "f"(b_hi[0]), "f"(b_hi[1]), "f"(b_hi[2]), "f"(0.0f)
+                 : "memory");
+#else
     q[0] = make_float4(a_lo[0], a_lo[1], a_lo[2], __int_as_float(a_id));
     q[1] = make_float4(a_hi[0], a_hi[1], a_hi[2], 0.0f);
     q[2] = make_float4(b_lo[0], b_lo[1], b_lo[2], __int_as_float(b_id));
     q[3] = make_float4(b_hi[0], b_hi[1], b_hi[2], 0.0f);
+#endif
 }
 
 // a leaf writes itself + an empty slot into its parent's BVH4 node
