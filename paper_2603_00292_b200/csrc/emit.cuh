@@ -121,8 +121,7 @@ __device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child,
 // (height | (outer delta + 1) << 8 >= 0, split g >= -1; both sides' tags are invalidated
 // by the emit kernel's hand-off before this kernel runs), the exchange is relaxed, and
 // the second arrival spins on the L2 copy of its sibling's box until both tags are
-// valid.  (This relies on a 16-B aligned st.v4 landing in L2 as one access, which
-// holds on the hardware; the tag word and the box share a 32-B sector.)
+// valid.  (Records are written and read as single 256-bit accesses of one 32-B sector.)
 constexpr int SLOT_INVALID = (int)0x80000000;
 
 #ifndef EMIT_ACQREL
@@ -140,13 +139,23 @@ __device__ __forceinline__ int atom_exch_acq_rel_cta(int* p, int v) {
 // A spin on a plain (even asm-volatile ld.global.cg) load is NOT a loop to ptxas: it
 // assumes the location cannot change and keeps at most one reload.  The re-reads must be
 // strong relaxed loads at GPU scope, which ptxas must re-issue on every iteration.
-__device__ __forceinline__ float4 ld_relaxed_gpu(const float4* p) {
-    float4 v;
-    asm volatile("ld.relaxed.gpu.global.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+// A slot record is 32 B (box lo + tag, box hi + split) and moves as ONE 256-bit access.
+__device__ __forceinline__ void ld_record_relaxed(const float4* p, float4& a, float4& b) {
+    asm volatile("ld.relaxed.gpu.global.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
                  : "l"(p)
                  : "memory");
-    return v;
+}
+__device__ __forceinline__ void ld_record_cg(const float4* p, float4& a, float4& b) {
+    asm volatile("ld.global.cg.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+                 : "l"(p)
+                 : "memory");
+}
+__device__ __forceinline__ void st_record_cg(float4* p, const float4 a, const float4 b) {
+    asm volatile("st.global.cg.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(a.z),
+                 "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                 : "memory");
 }
 
 template <typename K>
@@ -162,14 +171,16 @@ __device__ void climb_global(const K* __restrict__ keys, int64_t n, int2* __rest
         // second arrival needs no key loads: one L2 round trip per level (the sibling's
         // record is read speculatively alongside the exchange)
         const int outer = (left ? N.dl : N.dr) + 1;
-        __stcg(slot_box + 4 * gamma + 2 * side, make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h | (outer << 8))));
-        __stcg(slot_box + 4 * gamma + 2 * side + 1, make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g)));
+        st_record_cg(slot_box + 4 * gamma + 2 * side,
+                     make_float4(N.lo[0], N.lo[1], N.lo[2], __int_as_float(N.h | (outer << 8))),
+                     make_float4(N.hi[0], N.hi[1], N.hi[2], __int_as_float(N.g)));
         const float4* sib = slot_box + 4 * gamma + 2 * (1 - side);
-        float4 s0 = __ldcg(sib), s1 = __ldcg(sib + 1);
+        float4 s0, s1;
+        ld_record_cg(sib, s0, s1);
         const int other = atomicExch(slot_range + gamma, left ? N.l : N.r);
         if (other < 0) return;                       // sibling subtree not finished
-        while (__float_as_int(s0.w) == SLOT_INVALID) s0 = ld_relaxed_gpu(sib);
-        while (__float_as_int(s1.w) == SLOT_INVALID) s1 = ld_relaxed_gpu(sib + 1);
+        while (__float_as_int(s0.w) == SLOT_INVALID || __float_as_int(s1.w) == SLOT_INVALID)
+            ld_record_relaxed(sib, s0, s1);
         const int pl = left ? N.l : other, pr = left ? other : N.r;
         const int sd = (__float_as_int(s0.w) >> 8) - 1;
         s0.w = __int_as_float(__float_as_int(s0.w) & 0xFF);
