@@ -10,3 +10,9 @@ ncu --set full --clock-control none --import-source on -k "$K" --launch-skip 8 -
     -o gpurun_out/r1_soup_build -f python tools/drive_build.py 2 30 soup > gpurun_out/ncu_soup_build.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r1_launches_c2.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu --no-pt --no-e2e > gpurun_out/ncu_launch_bench.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:pt_megakernel --launch-skip 1 --launch-count 1 \
+    -o gpurun_out/r1_mega_eye -f python tools/drive_render.py eye 2 > gpurun_out/ncu_eye.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:pt_megakernel --launch-skip 1 --launch-count 1 \
+    -o gpurun_out/r1_mega_pt -f python tools/drive_render.py pt 2 > gpurun_out/ncu_pt.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:pt_megakernel --launch-skip 1 --launch-count 1 \
+    -o gpurun_out/r1_soup_trace -f python tools/drive_render.py soup 2 > gpurun_out/ncu_soup.log 2>&1
