@@ -194,14 +194,19 @@ def run_reference(args, ws, rank):
         return
     cores = os.cpu_count() or 1
     desc = scene_desc(args.config, args.soup_n)
-    for _ in range(args.warmup if args.config != 4 else 0):
+    # each step is the whole config-2 workload (~1.2 s on 16 cores): warm-up and steps are
+    # capped so any --steps K --warmup W run ends within a few minutes
+    for _ in range(min(args.warmup, 2) if args.config != 4 else 0):
         cpu_sample(args.config, desc, cores)
     vals, builds = [], []
-    steps = args.steps if args.config != 4 else 1
-    for _ in range(steps):
+    t_start = time.perf_counter()
+    for _ in range(args.steps if args.config != 4 else 1):
         v, sample, b = cpu_sample(args.config, desc, cores)
         vals.append(v)
         builds.append(b)
+        if time.perf_counter() - t_start > 120.0:
+            break
+    steps = len(vals)
     value = float(np.mean(vals))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": ws,
             "steps": steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
@@ -491,7 +496,8 @@ def run_ours(args, ws, rank, local):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    # default: a timed region of >= ~0.25 s (several in-window clock samples) per config
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", type=int, choices=(2, 3, 4, 5), default=2)
@@ -503,6 +509,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps is None:
+        args.steps = 3 if args.impl == "reference" else {2: 400, 3: 10, 4: 60, 5: 3}[args.config]
     if args.impl == "reference":
         run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
         return
