@@ -161,3 +161,18 @@ def test_sass_is_sm100a():
     so = os.path.join(ROOT, "paper_2603_00292_b200", "librt_b200.so")
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_bench_roofline_inputs_are_committed():
+    """bench.py reads roofline.traffic / sm_issue_active_pct from the committed ncu capture
+    summary (profiles/ncu_traffic.json); every key it asks for exists and is positive."""
+    import importlib.util
+    import pathlib
+    root = pathlib.Path(__file__).resolve().parents[1]
+    spec = importlib.util.spec_from_file_location("bench_mod", root / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for key in ("config2_trace", "config2_build", "config3_trace_1spp", "config4_trace", "config4_build"):
+        assert bench.load_traffic(key) > 0, key
+        assert 0 < bench.load_issue(key) <= 100, key
+    assert set(bench.WORKLOADS) == {2, 3, 4, 5}
