@@ -126,8 +126,9 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
     The fp32 sums are widened to float64 on the device (exact) and read back by DMA into
     pinned memory; large primary-ray (eye) megakernel frames render in 4 row chunks so each
     chunk's readback overlaps the next chunk's render (return_stats=True renders in one
-    launch to count rays).  `bands=(stride, offset)` renders only that GPU's interleaved 4-row tile bands
-    (the multi-GPU tile split); the other pixels stay 0."""
+    launch to count rays).  `bands=(stride, offset)` renders only that GPU's interleaved
+    4-row tile bands (the multi-GPU tile split); the other pixels stay 0.  The returned
+    array lives in pinned host memory (PyTorch's caching host allocator) until freed."""
     import torch
     if width < 1 or height < 1 or spp < 1:
         raise ValueError("width, height, and spp must all be >= 1")
