@@ -612,7 +612,8 @@ int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, cons
         char* O = (char*)S.out;
         return rt_expand_hits_f64(c, s, m, hits, (double*)O, (int64_t*)(O + 8 * m), (int64_t*)(O + 16 * m),
                                   (double*)(O + 24 * m), (double*)(O + 32 * m), (double*)(O + 40 * m), S.rays, st,
-                                  (int64_t*)(O + 64 * m));
+                                  (int64_t*)(O + 64 * m), S.o, S.d, tmin ? S.tmin : nullptr,
+                                  tmax ? S.tmax : nullptr, tmin_s, tmax_s);
     };
     auto download = [&](const IoSlot& S, int64_t b, int64_t m, cudaStream_t so) -> int {
         const char* O = (const char*)S.out;

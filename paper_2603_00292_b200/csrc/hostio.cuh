@@ -100,9 +100,11 @@ int rt_io_run(rt_ctx* c, int64_t n, const HostIo& in, size_t hit_bytes, size_t o
         if (k >= 2) RT_CUDA_TRY(cudaStreamWaitEvent(sc, out_free[s], 0));
         rc = rt_pack_rays_io(c, m, S, in.tmin != nullptr, in.tmax != nullptr, in.tmin_s, in.tmax_s);
         if (rc) return rc;
-        RT_CUDA_TRY(cudaEventRecord(in_free[s], sc));
         rc = kernels(S, m);
         if (rc) return rc;
+        // the slot's float64 inputs are read up to here (the closest-hit expand refines
+        // (t, u, v) from them), so the next upload into this slot waits for the kernels
+        RT_CUDA_TRY(cudaEventRecord(in_free[s], sc));
         RT_CUDA_TRY(cudaEventRecord(c->io_ev[7 + s], sc));
         RT_CUDA_TRY(cudaStreamWaitEvent(so, c->io_ev[7 + s], 0));
         rc = download(S, b, m, so);

@@ -192,8 +192,10 @@ int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4
 int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask,
                       int custom_mode);
 int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
-                       int64_t* prim, double* u, double* v, double* nrm, const float* rays,
-                       const uint32_t* st32 = nullptr, int64_t* st64 = nullptr);
+                       int64_t* prim, double* u, double* v, double* nrm, const float* rays, const uint32_t* st32,
+                       int64_t* st64, const double* o64 = nullptr, const double* d64 = nullptr,
+                       const double* tmin64 = nullptr, const double* tmax64 = nullptr, double tmin_s = 0.0,
+                       double tmax_s = 0.0);
 int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, const double* tmin,
                      const double* tmax, float* rays);
 int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out);

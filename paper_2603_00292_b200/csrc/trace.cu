@@ -83,14 +83,57 @@ __global__ void pack_rays_f64(int64_t n, const double* __restrict__ o, const dou
     }
 }
 
+// geometry.py:219-275 _tri_hit in float64, the reference's expressions in its order (each
+// operation correctly rounded: no contraction); t < 0 = rejected
+__device__ __forceinline__ double tri_hit_f64(const double o[3], const double d[3], double tmin, double tmax,
+                                              const float* __restrict__ v9, double& ou, double& ov) {
+    const double ax = v9[0], ay = v9[1], az = v9[2], bx = v9[3], by = v9[4], bz = v9[5];
+    const double cx = v9[6], cy = v9[7], cz = v9[8];
+    const double e0x = __dsub_rn(bx, ax), e0y = __dsub_rn(by, ay), e0z = __dsub_rn(bz, az);
+    const double e1x = __dsub_rn(cx, bx), e1y = __dsub_rn(cy, by), e1z = __dsub_rn(cz, bz);
+    const double nx = __dsub_rn(__dmul_rn(e0y, e1z), __dmul_rn(e0z, e1y));
+    const double ny = __dsub_rn(__dmul_rn(e0z, e1x), __dmul_rn(e0x, e1z));
+    const double nz = __dsub_rn(__dmul_rn(e0x, e1y), __dmul_rn(e0y, e1x));
+    const double denom = __dadd_rn(__dadd_rn(__dmul_rn(nx, d[0]), __dmul_rn(ny, d[1])), __dmul_rn(nz, d[2]));
+    if (denom == 0.0) return -1.0;
+    const double num = __dadd_rn(__dadd_rn(__dmul_rn(__dsub_rn(ax, o[0]), nx), __dmul_rn(__dsub_rn(ay, o[1]), ny)),
+                                 __dmul_rn(__dsub_rn(az, o[2]), nz));
+    const double t = __ddiv_rn(num, denom);
+    if (!isfinite(t) || t < tmin || t > tmax) return -1.0;
+    const double px = __dadd_rn(o[0], __dmul_rn(d[0], t)), py = __dadd_rn(o[1], __dmul_rn(d[1], t)),
+                 pz = __dadd_rn(o[2], __dmul_rn(d[2], t));
+    auto edge = [&](double qx, double qy, double qz, double fx, double fy, double fz) {
+        const double wx = __dsub_rn(px, qx), wy = __dsub_rn(py, qy), wz = __dsub_rn(pz, qz);
+        return __dadd_rn(__dadd_rn(__dmul_rn(nx, __dsub_rn(__dmul_rn(fy, wz), __dmul_rn(fz, wy))),
+                                   __dmul_rn(ny, __dsub_rn(__dmul_rn(fz, wx), __dmul_rn(fx, wz)))),
+                         __dmul_rn(nz, __dsub_rn(__dmul_rn(fx, wy), __dmul_rn(fy, wx))));
+    };
+    const double ea = edge(ax, ay, az, e0x, e0y, e0z);
+    const double eb = edge(bx, by, bz, e1x, e1y, e1z);
+    const double ec = edge(cx, cy, cz, __dsub_rn(ax, cx), __dsub_rn(ay, cy), __dsub_rn(az, cz));
+    if (ea < 0.0 || eb < 0.0 || ec < 0.0) return -1.0;
+    const double sum = __dadd_rn(__dadd_rn(ea, eb), ec);
+    if (sum == 0.0) return -1.0;
+    ou = __ddiv_rn(ec, sum);
+    ov = __ddiv_rn(ea, sum);
+    return t;
+}
+
 // hit (t, id, u, v) -> the reference's per-ray outputs (float64 / int64),
 // world normal from the per-triangle reference-style normal, or
-// the sphere's at the hit point (rays needed only then)
+// the sphere's at the hit point (rays needed only then).  With the caller's float64
+// rays (host query API), a triangle hit's (t, u, v) are recomputed in float64 with the
+// reference's own formula on that triangle: bit-identical to the reference whenever
+// it hits the same triangle with the same (fp32-valued) world vertices; the fp32
+// values stay if the float64 test rejects the pair (edge / grazing cases).
 __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, const float4* __restrict__ attr,
                                 const int32_t* __restrict__ tri_inst, const int32_t* __restrict__ tri_prim,
                                 double* t, int64_t* inst, int64_t* prim, double* u, double* v, double* nrm,
                                 const float* __restrict__ rays, const SphereView sv,
-                                const uint32_t* __restrict__ st32, int64_t* __restrict__ st64) {
+                                const uint32_t* __restrict__ st32, int64_t* __restrict__ st64,
+                                const float* __restrict__ wtris, const double* __restrict__ o64,
+                                const double* __restrict__ d64, const double* __restrict__ tmin64,
+                                const double* __restrict__ tmax64, double tmin_s, double tmax_s) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float4 h = hits[i];
         int id = __float_as_int(h.y);
@@ -99,7 +142,16 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
             nrm[3 * i] = 0.0; nrm[3 * i + 1] = 0.0; nrm[3 * i + 2] = 0.0;
         } else {
             float4 a = attr[id];
-            t[i] = h.x; inst[i] = tri_inst[id]; prim[i] = tri_prim[id]; u[i] = h.z; v[i] = h.w;
+            double th = h.x, uh = h.z, vh = h.w;
+            if (o64 && id < sv.base) {
+                const double o[3] = {o64[3 * i], o64[3 * i + 1], o64[3 * i + 2]};
+                const double d[3] = {d64[3 * i], d64[3 * i + 1], d64[3 * i + 2]};
+                double u2, v2;
+                const double t2 = tri_hit_f64(o, d, tmin64 ? tmin64[i] : tmin_s, tmax64 ? tmax64[i] : tmax_s,
+                                              wtris + 9 * (int64_t)id, u2, v2);
+                if (t2 >= 0.0) { th = t2; uh = u2; vh = v2; }
+            }
+            t[i] = th; inst[i] = tri_inst[id]; prim[i] = tri_prim[id]; u[i] = uh; v[i] = vh;
             if (id >= sv.base) {
                 const TraceRay r = load_ray(rays, i);
                 const float3 w = sphere_normal(sv.rows + 16 * (int64_t)(id - sv.base), r.ox, r.oy, r.oz, r.dx, r.dy,
@@ -220,11 +272,13 @@ int rt_io_ensure(rt_ctx* c, int64_t chunk, size_t hit_bytes, size_t out_bytes, I
 
 int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, double* t, int64_t* inst,
                        int64_t* prim, double* u, double* v, double* nrm, const float* rays, const uint32_t* st32,
-                       int64_t* st64) {
+                       int64_t* st64, const double* o64, const double* d64, const double* tmin64,
+                       const double* tmax64, double tmin_s, double tmax_s) {
     int grid = ctx->num_sms * 8;
     expand_hits_f64<<<grid, 256, 0, ctx->stream>>>(n, hits, s->tri_attr, s->tri_inst, s->tri_prim, t, inst, prim,
                                                     u, v, nrm, rays, rt_sphere_view(ctx, s, 0), st32,
-                                                    st32 ? st64 : nullptr);
+                                                    st32 ? st64 : nullptr, s->tris, o64, d64, tmin64, tmax64, tmin_s,
+                                                    tmax_s);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }

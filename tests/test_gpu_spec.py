@@ -1,7 +1,8 @@
 """SPEC acceptance criteria checked directly on the GPU paths.
 
 * AC1: 10^5 random ray/triangle pairs against a float64
-  Moller-Trumbore, t within 1e-5 (1 + |t|) except at grazing incidence (fp32 arithmetic).  The pairs are laid out as one scene of
+  Moller-Trumbore: the same verdicts on the traversed fp32 rays, and t within 1e-5 (1 + |t|)
+  of MT on the float64 rays (the host API refines the hit in float64).  The pairs are laid out as one scene of
   10^5 triangles, each in its own unit cell 10 apart, with ray i starting in cell i and
   limited to t <= 5, so every ray can only meet its own triangle.
 * AC8: the path-traced estimate converges like 1/spp: the MSE against
@@ -54,25 +55,25 @@ def test_ac1_random_pairs_vs_moller_trumbore(native):
     t, inst, prim = closest_hit_batch(sc, O, D, t_max=5.0)[:3]
     hit = prim >= 0
     assert np.all(prim[hit] == np.arange(n)[hit])                # only its own triangle
-    # (a) MT on the ray the GPU actually traces (the API rounds rays to fp32): same verdict
-    #     on every pair, t within the AC1 bound
+    # (a) verdicts: MT on the ray the GPU actually traverses (the API rounds rays to fp32)
+    #     gives the same hit / miss on every pair
     O32, D32 = O.astype(np.float32).astype(np.float64), D.astype(np.float32).astype(np.float64)
-    tr, _, _ = _moller_trumbore(O32, D32, tri[:, 0], tri[:, 1], tri[:, 2])
-    tr = np.where(tr <= 5.0, tr, np.nan)
-    hit_ref = ~np.isnan(tr)
-    assert hit_ref.mean() > 0.5
-    assert (hit == hit_ref).mean() >= 0.99999, (hit == hit_ref).mean()
-    both = hit & hit_ref
-    # fp32 t is ill-conditioned at grazing incidence (error ~ ulp / cos): on these random
-    # pairs, many of them grazing, the bound holds for 99.97 % of the agreeing hits; the
-    # primary-ray configs meet SURVEY 8(d)'s >= 99.99 % (tests/test_gpu_trace.py)
+    tr32, _, _ = _moller_trumbore(O32, D32, tri[:, 0], tri[:, 1], tri[:, 2])
+    hit32 = ~np.isnan(np.where(tr32 <= 5.0, tr32, np.nan))
+    assert hit32.mean() > 0.5
+    assert (hit == hit32).mean() >= 0.99999, (hit == hit32).mean()
+    # (b) values: the host API recomputes (t, u, v) of the hit triangle in float64 with the
+    #     reference's formula on the caller's float64 ray, so t meets AC1's bound against MT
+    #     on those rays; only pairs the float64 test rejects (grazing / edge) keep fp32 values
+    tr, ur, vr = _moller_trumbore(O, D, tri[:, 0], tri[:, 1], tri[:, 2])
+    hit64 = ~np.isnan(np.where(tr <= 5.0, tr, np.nan))
+    both = hit & hit64
     within = np.abs(t[both] - tr[both]) <= 1e-5 * (1 + np.abs(tr[both]))
-    assert within.mean() >= 0.9995, within.mean()
-    # (b) MT on the float64 rays: the only differences are grazing / edge-adjacent pairs whose
-    #     verdict flips under the fp32 rounding of the ray itself (34 of 10^5 here; the
-    #     primary-ray configs see ~1e-5)
-    tr64, _, _ = _moller_trumbore(O, D, tri[:, 0], tri[:, 1], tri[:, 2])
-    hit64 = ~np.isnan(np.where(tr64 <= 5.0, tr64, np.nan))
+    assert within.mean() >= 0.9999, within.mean()
+    exact = np.abs(t[both] - tr[both]) <= 1e-12 * (1 + np.abs(tr[both]))
+    assert exact.mean() >= 0.999, exact.mean()
+    # (c) verdicts against the float64 rays differ only where the fp32 rounding of the ray
+    #     itself flips a grazing / edge-adjacent pair (34 of 10^5 here)
     assert (hit == hit64).mean() >= 0.999, (hit == hit64).mean()
 
 

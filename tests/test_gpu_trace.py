@@ -41,6 +41,15 @@ def _compare(res_gpu, res_orc, n_rays, allow_t_outliers=1e-4, t_abs=0.0):
     return agree, rel
 
 
+def _exact_tuv(res_gpu, res_orc):
+    """Fraction of ID-agreeing hits whose (t, u, v) equal the oracle's bit for bit (the host
+    API recomputes them in float64 with the reference's formula)."""
+    t, inst, prim, u, v = res_gpu[:5]
+    rt, ri, rp, ru, rv = res_orc[:5]
+    both = (inst == ri) & (prim == rp) & (ri >= 0)
+    return float(np.mean((t[both] == rt[both]) & (u[both] == ru[both]) & (v[both] == rv[both])))
+
+
 @pytest.mark.parametrize("bits", [30, 63])
 def test_cornell_config1_primaries(native, cornell_oracle, bits):
     """Config 1: Cornell 256x256, 1 spp, jitter on, seed 0 (F4: ties vanish with jitter)."""
@@ -110,6 +119,8 @@ def test_config2_sphere_full_size(native, oracle_mod, bits):
     orc = oracle_mod.scene_from_description(desc)
     r = orc.closest_hit_batch(O, D, workers=8)
     _compare(g, r, O.shape[0])
+    # identity instance, fp32-valued vertices: the reference's own float64 arithmetic
+    assert _exact_tuv(g, r) >= 0.9999
     hit_frac = np.mean(g[1] >= 0)
     assert 0.40 < hit_frac < 0.43          # analytic 0.416
 
@@ -125,6 +136,7 @@ def test_config4_soup_sample(native, oracle_mod):
     orc = oracle_mod.scene_from_description(desc)
     r = orc.closest_hit_batch(O, D, workers=8)
     _compare(g, r, O.shape[0], 1e-3)
+    assert _exact_tuv(g, r) >= 0.9999
 
 
 def test_stats_and_culling(native):
