@@ -208,6 +208,10 @@ int rt_raygen(rt_ctx* ctx, const rt_render_params* p, int32_t sample, float* ray
  * rows, marked with rt_scene_set_custom (Blas.from_aabbs).  Both need rt_bvh_build. */
 /* (n, 3) float64 local triangle normals in the reference's order (geometry.py:229-237, 274-275) */
 int rt_scene_set_local_normals(rt_ctx* ctx, rt_scene* blas, const double* normals);
+/* a triangle BLAS's float64 local vertices, (n, 9) in prim order (optional): with them the
+ * host two-level query recomputes each hit's (t, u, v) with the reference's own float64
+ * arithmetic (local ray from the float64 inverse, then _tri_hit) */
+int rt_scene_set_local_rows(rt_ctx* ctx, rt_scene* blas, const double* rows);
 /* custom-primitive BLAS: geometry type and the offset of its first row in the registry data */
 int rt_scene_set_custom(rt_ctx* ctx, rt_scene* blas, int32_t geom_type, int64_t data_offset);
 /* TLAS over n_inst instances: inst_blas[i] = the instance's BLAS, inv12 (n, 12) float64

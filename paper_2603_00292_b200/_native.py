@@ -98,6 +98,7 @@ def lib():
             "rt_resolve": [vp, vp, i64, i32, vp],
             "rt_multi_render": [i32, vp, vp, ctypes.POINTER(RenderParams), vp, i32, vp],
             "rt_scene_set_local_normals": [vp, vp, vp],
+            "rt_scene_set_local_rows": [vp, vp, vp],
             "rt_scene_set_custom": [vp, vp, i32, i64],
             "rt_tlas_create": [vp, i32, vp, vp, vp, vp, vp],
             "rt_tlas_update": [vp, vp, vp, vp],

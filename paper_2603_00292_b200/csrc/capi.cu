@@ -251,7 +251,8 @@ template <typename T>
 __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __restrict__ faces,
                                   const T* __restrict__ Vt, const double* __restrict__ xform,
                                   const int64_t* __restrict__ offset, float* __restrict__ tris,
-                                  float4* __restrict__ attr, double* __restrict__ lnormal64) {
+                                  float4* __restrict__ attr, double* __restrict__ lnormal64,
+                                  double* __restrict__ lrows64) {
     const int64_t total = nf * n_inst;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
         const int32_t j = (int32_t)(q / nf);
@@ -266,10 +267,14 @@ __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __rest
         float* t = tris + 9 * (offset[j] + k);
         const double* vs[3] = {a, b, c};
         if (lnormal64) {       // a BLAS: its rows are the local vertices themselves (Blas._rows)
+            double* rows64 = lrows64 ? lrows64 + 9 * (offset[j] + k) : nullptr;
 #pragma unroll
             for (int v = 0; v < 3; ++v)
 #pragma unroll
-                for (int r = 0; r < 3; ++r) t[3 * v + r] = __double2float_rn(vs[v][r]);
+                for (int r = 0; r < 3; ++r) {
+                    t[3 * v + r] = __double2float_rn(vs[v][r]);
+                    if (rows64) rows64[3 * v + r] = vs[v][r];
+                }
         } else {
 #pragma unroll
             for (int v = 0; v < 3; ++v)
@@ -402,10 +407,11 @@ int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, 
     if (vertices_f32)
         refit_mesh_kernel<float><<<(unsigned)grid, 256, 0, c->stream>>>(
             m->nf, m->n_inst, m->faces, reinterpret_cast<const float*>(m->verts), m->xform, m->offset, s->tris, s->tri_attr,
-            ln);
+            ln, m->local ? s->lrows64 : nullptr);
     else
         refit_mesh_kernel<double><<<(unsigned)grid, 256, 0, c->stream>>>(m->nf, m->n_inst, m->faces, m->verts, m->xform,
-                                                                         m->offset, s->tris, s->tri_attr, ln);
+                                                                         m->offset, s->tris, s->tri_attr, ln,
+                                                                         m->local ? s->lrows64 : nullptr);
     RT_CUDA_TRY(cudaGetLastError());
     s->built = 0;
     return RT_OK;
@@ -427,7 +433,7 @@ void rt_scene_destroy(rt_scene* s) {
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->child,
                     s->flags, s->cbounds, s->sort_scratch, s->leaf_box, s->emit_items, s->seg_count, s->lights,
                     s->spheres,
-                    s->lnormal64};
+                    s->lnormal64, s->lrows64};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;

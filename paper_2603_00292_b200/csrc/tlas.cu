@@ -25,6 +25,7 @@ struct BlasDev {
     const float4* bvh4;
     const float4* tris;       // leaf-ordered: v0.w = prim, v1.w = mask (full)
     const double* lnormal;    // (n, 3) float64 local normals (triangles)
+    const double* lrows;      // (n, 9) float64 local vertices (nullable): exact (t, u, v) refinement
     const double* data;       // custom: rows (cx, cy, cz, r) of this BLAS's prims (nullptr: not registered)
     int root4, height, kind, geom_type;
 };
@@ -244,7 +245,10 @@ __device__ __forceinline__ void world_normal_f64(const double* m, double lx, dou
 __global__ void tlas_expand_f64(int64_t n, const float4* __restrict__ hits, const float* __restrict__ rays,
                                 const InstDev* __restrict__ inst, const BlasDev* __restrict__ blas, double* t,
                                 int64_t* oinst, int64_t* oprim, double* u, double* v, double* nrm,
-                                const uint32_t* __restrict__ st32, int64_t* __restrict__ st64) {
+                                const uint32_t* __restrict__ st32, int64_t* __restrict__ st64,
+                                const double* __restrict__ o64, const double* __restrict__ d64,
+                                const double* __restrict__ tmin64, const double* __restrict__ tmax64, double tmin_s,
+                                double tmax_s) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float4 h0 = hits[2 * i], h1 = hits[2 * i + 1];
         const int ii = __float_as_int(h0.y), p = __float_as_int(h0.z);
@@ -270,7 +274,18 @@ __global__ void tlas_expand_f64(int64_t n, const float4* __restrict__ hits, cons
             for (int k = 0; k < 3; ++k) ln[k] = (o[k] + d[k] * th - row[k]) / row[3];
         }
         world_normal_f64(m, ln[0], ln[1], ln[2], nrm + 3 * i);
-        t[i] = h0.x; oinst[i] = ii; oprim[i] = p; u[i] = h0.w; v[i] = h1.x;
+        double th = h0.x, uh = h0.w, vh = h1.x;
+        if (B.kind == 0 && B.lrows && o64) {
+            // the reference's own arithmetic: the float64 world ray to local space with the
+            // float64 inverse (accel.py:804-809), then _tri_hit on the float64 local vertices
+            double o[3], d[3], u2, v2;
+            to_local_f64(m, o64[3 * i], o64[3 * i + 1], o64[3 * i + 2], d64[3 * i], d64[3 * i + 1], d64[3 * i + 2],
+                         o, d);
+            const double t2 = tri_hit_f64(o, d, tmin64 ? tmin64[i] : tmin_s, tmax64 ? tmax64[i] : tmax_s,
+                                          B.lrows + 9 * (int64_t)p, u2, v2);
+            if (t2 >= 0.0) { th = t2; uh = u2; vh = v2; }
+        }
+        t[i] = th; oinst[i] = ii; oprim[i] = p; u[i] = uh; v[i] = vh;
     }
 }
 
@@ -382,6 +397,14 @@ int rt_scene_set_local_normals(rt_ctx* c, rt_scene* s, const double* n3) {
     return RT_OK;
 }
 
+int rt_scene_set_local_rows(rt_ctx* c, rt_scene* s, const double* rows9) {
+    RT_CHECK_ARG(c && s && rows9, "NULL argument");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    if (!s->lrows64) RT_CUDA_TRY(cudaMalloc(&s->lrows64, sizeof(double) * 9 * (size_t)s->n));
+    RT_CUDA_TRY(cudaMemcpy(s->lrows64, rows9, sizeof(double) * 9 * (size_t)s->n, cudaMemcpyHostToDevice));
+    return RT_OK;
+}
+
 int rt_scene_set_custom(rt_ctx* c, rt_scene* s, int32_t geom_type, int64_t data_offset) {
     RT_CHECK_ARG(c && s && geom_type >= 0 && data_offset >= 0, "bad custom primitive description");
     s->custom = 1;
@@ -427,6 +450,7 @@ int rt_tlas_create(rt_ctx* c, int32_t n_inst, rt_scene* const* inst_blas, const 
         B.bvh4 = s->bvh4;
         B.tris = s->tri_sorted;
         B.lnormal = s->lnormal64;
+        B.lrows = s->lrows64;
         B.data = nullptr;
         B.kind = s->custom ? 1 : 0;
         B.geom_type = s->custom ? s->geom_type : -1;
@@ -471,6 +495,7 @@ int rt_tlas_update(rt_ctx* c, rt_tlas* T, const double* inv12, const float* boxe
         if (rc) return rc;
         T->hblas[b].bvh4 = T->blas[b]->bvh4;
         T->hblas[b].tris = T->blas[b]->tri_sorted;
+        T->hblas[b].lrows = T->blas[b]->lrows64;
         T->max_height = std::max(T->max_height, T->hblas[b].height);
     }
     RT_CUDA_TRY(cudaMemcpy(T->d_blas, T->hblas.data(), sizeof(BlasDev) * T->hblas.size(), cudaMemcpyHostToDevice));
@@ -658,7 +683,8 @@ int rt_tlas_closest_host(rt_ctx* c, rt_tlas* T, int64_t n, const double* o, cons
         char* O = (char*)S.out;
         tlas_expand_f64<<<c->num_sms * 4, 256, 0, c->stream>>>(
             m, hits, S.rays, T->d_inst, T->d_blas, (double*)O, (int64_t*)(O + 8 * m), (int64_t*)(O + 16 * m),
-            (double*)(O + 24 * m), (double*)(O + 32 * m), (double*)(O + 40 * m), st, (int64_t*)(O + 64 * m));
+            (double*)(O + 24 * m), (double*)(O + 32 * m), (double*)(O + 40 * m), st, (int64_t*)(O + 64 * m), S.o, S.d,
+            tmin ? S.tmin : nullptr, tmax ? S.tmax : nullptr, tmin_s, tmax_s);
         RT_CUDA_TRY(cudaGetLastError());
         return RT_OK;
     };

@@ -231,6 +231,44 @@ __device__ __forceinline__ void to_local_f64(const double* m, double ox, double 
     d[2] = __dadd_rn(__dadd_rn(__dmul_rn(m[8], dx), __dmul_rn(m[9], dy)), __dmul_rn(m[10], dz));
 }
 
+// geometry.py:219-275 _tri_hit in float64, the reference's expressions in its order (each
+// operation correctly rounded: no contraction); t < 0 = rejected.  V: the vertex type (fp32
+// world rows of a flat scene, or a BLAS's float64 local rows)
+template <typename V>
+__device__ __forceinline__ double tri_hit_f64(const double o[3], const double d[3], double tmin, double tmax,
+                                              const V* __restrict__ v9, double& ou, double& ov) {
+    const double ax = v9[0], ay = v9[1], az = v9[2], bx = v9[3], by = v9[4], bz = v9[5];
+    const double cx = v9[6], cy = v9[7], cz = v9[8];
+    const double e0x = __dsub_rn(bx, ax), e0y = __dsub_rn(by, ay), e0z = __dsub_rn(bz, az);
+    const double e1x = __dsub_rn(cx, bx), e1y = __dsub_rn(cy, by), e1z = __dsub_rn(cz, bz);
+    const double nx = __dsub_rn(__dmul_rn(e0y, e1z), __dmul_rn(e0z, e1y));
+    const double ny = __dsub_rn(__dmul_rn(e0z, e1x), __dmul_rn(e0x, e1z));
+    const double nz = __dsub_rn(__dmul_rn(e0x, e1y), __dmul_rn(e0y, e1x));
+    const double denom = __dadd_rn(__dadd_rn(__dmul_rn(nx, d[0]), __dmul_rn(ny, d[1])), __dmul_rn(nz, d[2]));
+    if (denom == 0.0) return -1.0;
+    const double num = __dadd_rn(__dadd_rn(__dmul_rn(__dsub_rn(ax, o[0]), nx), __dmul_rn(__dsub_rn(ay, o[1]), ny)),
+                                 __dmul_rn(__dsub_rn(az, o[2]), nz));
+    const double t = __ddiv_rn(num, denom);
+    if (!isfinite(t) || t < tmin || t > tmax) return -1.0;
+    const double px = __dadd_rn(o[0], __dmul_rn(d[0], t)), py = __dadd_rn(o[1], __dmul_rn(d[1], t)),
+                 pz = __dadd_rn(o[2], __dmul_rn(d[2], t));
+    auto edge = [&](double qx, double qy, double qz, double fx, double fy, double fz) {
+        const double wx = __dsub_rn(px, qx), wy = __dsub_rn(py, qy), wz = __dsub_rn(pz, qz);
+        return __dadd_rn(__dadd_rn(__dmul_rn(nx, __dsub_rn(__dmul_rn(fy, wz), __dmul_rn(fz, wy))),
+                                   __dmul_rn(ny, __dsub_rn(__dmul_rn(fz, wx), __dmul_rn(fx, wz)))),
+                         __dmul_rn(nz, __dsub_rn(__dmul_rn(fx, wy), __dmul_rn(fy, wx))));
+    };
+    const double ea = edge(ax, ay, az, e0x, e0y, e0z);
+    const double eb = edge(bx, by, bz, e1x, e1y, e1z);
+    const double ec = edge(cx, cy, cz, __dsub_rn(ax, cx), __dsub_rn(ay, cy), __dsub_rn(az, cz));
+    if (ea < 0.0 || eb < 0.0 || ec < 0.0) return -1.0;
+    const double sum = __dadd_rn(__dadd_rn(ea, eb), ec);
+    if (sum == 0.0) return -1.0;
+    ou = __ddiv_rn(ec, sum);
+    ov = __ddiv_rn(ea, sum);
+    return t;
+}
+
 // geometry.py:334-363 _sphere_hit in float64 on the world ray of a sphere instance
 static __device__ __noinline__ double sphere_hit_f64(const double* __restrict__ row, float fox, float foy, float foz,
                                                      float fdx, float fdy, float fdz, double t_min, double t_max) {

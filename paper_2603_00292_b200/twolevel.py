@@ -82,6 +82,7 @@ class Blas:
         self.handle = h
         if kind == TRIANGLES:
             check(lib().rt_scene_set_local_normals(ctx.handle, h, ptr(_local_normals64(vertices, faces))))
+            check(lib().rt_scene_set_local_rows(ctx.handle, h, ptr(np.ascontiguousarray(vertices[faces].reshape(-1, 9)))))
         else:
             check(lib().rt_scene_set_custom(ctx.handle, h, self.geom_type, self.data_offset))
         self._build()

@@ -64,7 +64,10 @@ def test_cornell_two_level_vs_reference(native):
     assert same.all()
     # triangle normals: the reference's float64 arithmetic, bit for bit
     assert np.array_equal(res[5][both], g["n"][both])
-    assert np.allclose(res[3][both], g["u"][both], atol=1e-3) and np.allclose(res[4][both], g["v"][both], atol=1e-3)
+    # (t, u, v): recomputed by the host query with the reference's float64 arithmetic (local
+    # ray from the float64 inverse, _tri_hit on the float64 local vertices): bit for bit too
+    exact = (res[0][both] == g["t"][both]) & (res[3][both] == g["u"][both]) & (res[4][both] == g["v"][both])
+    assert exact.mean() >= 0.9999, exact.mean()
     assert np.all(res[6][:, 0] >= 1) and np.all(res[6][:, 1] >= 1)
     # random rays from inside the box: all disagreements are exact cube-bottom / floor ties
     rt, ri, rp = g["rt"], g["ri"], g["rp"]
