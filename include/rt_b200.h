@@ -128,6 +128,10 @@ void rt_mesh_destroy(rt_mesh* mesh);
  * vertices, float64 in the reference order with an identity frame (after
  * rt_scene_set_vertices, whose rows are world triangles) */
 int rt_scene_update_normals(rt_ctx* ctx, rt_scene* scene);
+/* float64 world normals of a flat scene, (n, 3) (optional): the host query returns them
+ * as they are (compile_scene's reference-style float64 normals) instead of the fp32 copy
+ * used for shading; device refits keep them current */
+int rt_scene_set_normals64(rt_ctx* ctx, rt_scene* scene, const double* normals);
 /* the scene's current (n, 9) fp32 triangle rows, device -> host (synchronises) */
 int rt_scene_get_vertices(rt_ctx* ctx, rt_scene* scene, float* tris);
 

@@ -111,6 +111,7 @@ def lib():
             "rt_scene_refit_mesh": [vp, vp, vp, i64, vp, i32],
             "rt_scene_update_normals": [vp, vp],
             "rt_scene_get_vertices": [vp, vp, vp],
+            "rt_scene_set_normals64": [vp, vp, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)

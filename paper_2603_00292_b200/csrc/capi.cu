@@ -252,7 +252,7 @@ __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __rest
                                   const T* __restrict__ Vt, const double* __restrict__ xform,
                                   const int64_t* __restrict__ offset, float* __restrict__ tris,
                                   float4* __restrict__ attr, double* __restrict__ lnormal64,
-                                  double* __restrict__ lrows64) {
+                                  double* __restrict__ lrows64, double* __restrict__ wnormal64) {
     const int64_t total = nf * n_inst;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
         const int32_t j = (int32_t)(q / nf);
@@ -301,17 +301,22 @@ __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __rest
         const double wz = __dadd_rn(__dadd_rn(__dmul_rn(inv[2], lx), __dmul_rn(inv[5], ly)), __dmul_rn(inv[8], lz));
         const double il =
             __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz))));
+        const double nwx = __dmul_rn(wx, il), nwy = __dmul_rn(wy, il), nwz = __dmul_rn(wz, il);
         float4* at = attr + offset[j] + k;
         const float w = at->w;                          // material index bits stay
-        *at = make_float4(__double2float_rn(__dmul_rn(wx, il)), __double2float_rn(__dmul_rn(wy, il)),
-                          __double2float_rn(__dmul_rn(wz, il)), w);
+        *at = make_float4(__double2float_rn(nwx), __double2float_rn(nwy), __double2float_rn(nwz), w);
+        if (wnormal64) {
+            double* wn = wnormal64 + 3 * (offset[j] + k);
+            wn[0] = nwx; wn[1] = nwy; wn[2] = nwz;
+        }
     }
 }
 
 // normals of world triangles given directly (GpuTlas.refit): the same float64 expressions
 // with an identity instance frame (its inverse-transpose sum is exact, the renormalisation
 // is kept)
-__global__ void normals_from_tris_kernel(int64_t n, const float* __restrict__ tris, float4* __restrict__ attr) {
+__global__ void normals_from_tris_kernel(int64_t n, const float* __restrict__ tris, float4* __restrict__ attr,
+                                         double* __restrict__ wnormal64) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const float* t = tris + 9 * i;
         const double e0x = __dsub_rn(t[3], t[0]), e0y = __dsub_rn(t[4], t[1]), e0z = __dsub_rn(t[5], t[2]);
@@ -323,11 +328,13 @@ __global__ void normals_from_tris_kernel(int64_t n, const float* __restrict__ tr
         const double lx = __ddiv_rn(nx, nlen), ly = __ddiv_rn(ny, nlen), lz = __ddiv_rn(nz, nlen);
         const double il =
             __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(lx, lx), __dmul_rn(ly, ly)), __dmul_rn(lz, lz))));
+        const double wx = __dmul_rn(lx, il), wy = __dmul_rn(ly, il), wz = __dmul_rn(lz, il);
         float4 a = attr[i];
-        a.x = __double2float_rn(__dmul_rn(lx, il));
-        a.y = __double2float_rn(__dmul_rn(ly, il));
-        a.z = __double2float_rn(__dmul_rn(lz, il));
+        a.x = __double2float_rn(wx);
+        a.y = __double2float_rn(wy);
+        a.z = __double2float_rn(wz);
         attr[i] = a;
+        if (wnormal64) { wnormal64[3 * i] = wx; wnormal64[3 * i + 1] = wy; wnormal64[3 * i + 2] = wz; }
     }
 }
 
@@ -342,8 +349,16 @@ int rt_scene_update_normals(rt_ctx* c, rt_scene* s) {
     if (n <= 0) return RT_OK;
     int64_t grid = (n + 255) / 256;
     if (grid > (int64_t)c->num_sms * 16) grid = (int64_t)c->num_sms * 16;
-    normals_from_tris_kernel<<<(unsigned)grid, 256, 0, c->stream>>>(n, s->tris, s->tri_attr);
+    normals_from_tris_kernel<<<(unsigned)grid, 256, 0, c->stream>>>(n, s->tris, s->tri_attr, s->wnormal64);
     RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}
+
+int rt_scene_set_normals64(rt_ctx* c, rt_scene* s, const double* n3) {
+    RT_CHECK_ARG(c && s && n3, "NULL argument");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    if (!s->wnormal64) RT_CUDA_TRY(cudaMalloc(&s->wnormal64, sizeof(double) * 3 * (size_t)s->n));
+    RT_CUDA_TRY(cudaMemcpy(s->wnormal64, n3, sizeof(double) * 3 * (size_t)s->n, cudaMemcpyHostToDevice));
     return RT_OK;
 }
 
@@ -407,11 +422,12 @@ int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, 
     if (vertices_f32)
         refit_mesh_kernel<float><<<(unsigned)grid, 256, 0, c->stream>>>(
             m->nf, m->n_inst, m->faces, reinterpret_cast<const float*>(m->verts), m->xform, m->offset, s->tris, s->tri_attr,
-            ln, m->local ? s->lrows64 : nullptr);
+            ln, m->local ? s->lrows64 : nullptr, m->local ? nullptr : s->wnormal64);
     else
         refit_mesh_kernel<double><<<(unsigned)grid, 256, 0, c->stream>>>(m->nf, m->n_inst, m->faces, m->verts, m->xform,
                                                                          m->offset, s->tris, s->tri_attr, ln,
-                                                                         m->local ? s->lrows64 : nullptr);
+                                                                         m->local ? s->lrows64 : nullptr,
+                                                                         m->local ? nullptr : s->wnormal64);
     RT_CUDA_TRY(cudaGetLastError());
     s->built = 0;
     return RT_OK;
@@ -433,7 +449,7 @@ void rt_scene_destroy(rt_scene* s) {
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->child,
                     s->flags, s->cbounds, s->sort_scratch, s->leaf_box, s->emit_items, s->seg_count, s->lights,
                     s->spheres,
-                    s->lnormal64, s->lrows64};
+                    s->lnormal64, s->lrows64, s->wnormal64};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;

@@ -70,6 +70,7 @@ struct rt_scene {
     // as a bottom-level structure of a two-level rt_tlas (tlas.cu)
     double* lnormal64;              // (n, 3) float64 local normals (reference order), triangles
     double* lrows64;                // (n, 9) float64 local vertices (BLAS): the host query's exact refinement
+    double* wnormal64;              // (n, 3) float64 world normals (flat scene, nullable): host query output
     int custom;                     // 1: prims are AABBs of custom primitives (geom_type, data_offset)
     int geom_type;
     int64_t data_offset;

@@ -97,7 +97,8 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
                                 const uint32_t* __restrict__ st32, int64_t* __restrict__ st64,
                                 const float* __restrict__ wtris, const double* __restrict__ o64,
                                 const double* __restrict__ d64, const double* __restrict__ tmin64,
-                                const double* __restrict__ tmax64, double tmin_s, double tmax_s) {
+                                const double* __restrict__ tmax64, double tmin_s, double tmax_s,
+                                const double* __restrict__ wn64) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float4 h = hits[i];
         int id = __float_as_int(h.y);
@@ -121,8 +122,12 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
                 const float3 w = sphere_normal(sv.rows + 16 * (int64_t)(id - sv.base), r.ox, r.oy, r.oz, r.dx, r.dy,
                                                r.dz, h.x);
                 a.x = w.x; a.y = w.y; a.z = w.z;
+                nrm[3 * i] = a.x; nrm[3 * i + 1] = a.y; nrm[3 * i + 2] = a.z;
+            } else if (wn64) {            // the reference-style float64 world normal itself
+                nrm[3 * i] = wn64[3 * id]; nrm[3 * i + 1] = wn64[3 * id + 1]; nrm[3 * i + 2] = wn64[3 * id + 2];
+            } else {
+                nrm[3 * i] = a.x; nrm[3 * i + 1] = a.y; nrm[3 * i + 2] = a.z;
             }
-            nrm[3 * i] = a.x; nrm[3 * i + 1] = a.y; nrm[3 * i + 2] = a.z;
         }
         if (st64) { st64[2 * i] = st32[2 * i]; st64[2 * i + 1] = st32[2 * i + 1]; }
     }
@@ -242,7 +247,7 @@ int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, 
     expand_hits_f64<<<grid, 256, 0, ctx->stream>>>(n, hits, s->tri_attr, s->tri_inst, s->tri_prim, t, inst, prim,
                                                     u, v, nrm, rays, rt_sphere_view(ctx, s, 0), st32,
                                                     st32 ? st64 : nullptr, s->tris, o64, d64, tmin64, tmax64, tmin_s,
-                                                    tmax_s);
+                                                    tmax_s, s->wnormal64);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }

@@ -53,7 +53,8 @@ class GpuTlas:
         self.n = int(tris.shape[0])
         self.bits = bits
         self._tris = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
-        self.normals = np.ascontiguousarray(normals, np.float32).reshape(-1, 3)
+        normals64 = np.ascontiguousarray(normals, np.float64).reshape(-1, 3)
+        self.normals = np.ascontiguousarray(normals64, np.float32)
         self.tri_inst = np.ascontiguousarray(tri_inst, np.int32)
         self.tri_prim = np.ascontiguousarray(tri_prim, np.int32)
         self.tri_mask = np.ascontiguousarray(tri_mask, np.uint32)
@@ -68,6 +69,8 @@ class GpuTlas:
                                     ptr(self.tri_prim), ptr(self.tri_mask), ptr(self.tri_material), ptr(mc),
                                     ptr(me), mc.shape[0], ctypes.byref(h)))
         self.handle = h
+        # the float64 world normals themselves, for the host query's outputs
+        check(lib().rt_scene_set_normals64(ctx.handle, h, ptr(normals64)))
         self.build_ms = None
         # custom primitives: the last rows of `tris` are sphere instance boxes
         self.sphere_rows = np.zeros((0, 16)) if spheres is None else np.ascontiguousarray(spheres, np.float64)
@@ -353,7 +356,7 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
              m[2, 0] * V[:, 0:1] + m[2, 1] * V[:, 1:2] + m[2, 2] * V[:, 2:3] + m[2, 3])
         Wv = np.concatenate(W, axis=1)
         tris.append(Wv[F].reshape(-1, 9).astype(np.float32))
-        normals.append(_world_normals(inv, *ln).astype(np.float32))
+        normals.append(_world_normals(inv, *ln))       # float64; GpuTlas keeps both widths
         nt = F.shape[0]
         t_inst.append(np.full(nt, i, np.int32))
         t_prim.append(np.arange(nt, dtype=np.int32))
@@ -387,7 +390,7 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
             lo32 = np.where(lo32.astype(np.float64) > lo, np.nextafter(lo32, np.float32(-np.inf)), lo32)
             hi32 = np.where(hi32.astype(np.float64) < hi, np.nextafter(hi32, np.float32(np.inf)), hi32)
             tris.append(np.concatenate([lo32, hi32, lo32]).reshape(1, 9).astype(np.float32))
-            normals.append(np.zeros((1, 3), np.float32))
+            normals.append(np.zeros((1, 3)))
             inst_idx = len(desc.instances) + k
             t_inst.append(np.array([inst_idx], np.int32))
             t_prim.append(np.zeros(1, np.int32))

@@ -38,6 +38,8 @@ def _compare(res_gpu, res_orc, n_rays, allow_t_outliers=1e-4, t_abs=0.0):
     du = np.maximum(np.abs(u[both] - ru[both]), np.abs(v[both] - rv[both]))
     assert np.mean(du > UV_ABS) <= 1e-4, f"{np.mean(du > UV_ABS):.2e} of hits with |du| > {UV_ABS}"
     assert np.allclose(n[both], rn[both], atol=1e-6)
+    # (the flat query returns compile_scene's float64 world normals: the reference's values)
+    assert np.mean(np.all(n[both] == rn[both], axis=1)) >= 0.9999
     return agree, rel
 
 
