@@ -132,6 +132,11 @@ int rt_scene_update_normals(rt_ctx* ctx, rt_scene* scene);
  * as they are (compile_scene's reference-style float64 normals) instead of the fp32 copy
  * used for shading; device refits keep them current */
 int rt_scene_set_normals64(rt_ctx* ctx, rt_scene* scene, const double* normals);
+/* a flat scene's instance inverses (n_inst, 12: 3x4 row-major) and the float64 LOCAL vertices
+ * of every flat primitive (n, 9) (optional): the host query then recomputes each hit's
+ * (t, u, v) along the reference's own path (local ray, _tri_hit on local vertices).
+ * rt_scene_update_normals (new world rows) drops them; Scene.refit_mesh keeps them current. */
+int rt_scene_set_local_frames(rt_ctx* ctx, rt_scene* scene, int32_t n_inst, const double* inv12, const double* rows);
 /* the scene's current (n, 9) fp32 triangle rows, device -> host (synchronises) */
 int rt_scene_get_vertices(rt_ctx* ctx, rt_scene* scene, float* tris);
 

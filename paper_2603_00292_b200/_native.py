@@ -112,6 +112,7 @@ def lib():
             "rt_scene_update_normals": [vp, vp],
             "rt_scene_get_vertices": [vp, vp, vp],
             "rt_scene_set_normals64": [vp, vp, vp],
+            "rt_scene_set_local_frames": [vp, vp, i32, vp, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)

@@ -266,8 +266,14 @@ __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __rest
         const double c[3] = {(double)Vt[3 * (int64_t)f.z], (double)Vt[3 * (int64_t)f.z + 1], (double)Vt[3 * (int64_t)f.z + 2]};
         float* t = tris + 9 * (offset[j] + k);
         const double* vs[3] = {a, b, c};
+        double* rows64 = lrows64 ? lrows64 + 9 * (offset[j] + k) : nullptr;
+        if (rows64 && !lnormal64) {   // a flat scene keeping its local vertices for the query
+#pragma unroll
+            for (int v = 0; v < 3; ++v)
+#pragma unroll
+                for (int r = 0; r < 3; ++r) rows64[3 * v + r] = vs[v][r];
+        }
         if (lnormal64) {       // a BLAS: its rows are the local vertices themselves (Blas._rows)
-            double* rows64 = lrows64 ? lrows64 + 9 * (offset[j] + k) : nullptr;
 #pragma unroll
             for (int v = 0; v < 3; ++v)
 #pragma unroll
@@ -345,12 +351,30 @@ extern "C" {
 int rt_scene_update_normals(rt_ctx* c, rt_scene* s) {
     RT_CHECK_ARG(c && s, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
+    // new world rows: the local vertices / frames no longer describe them
+    if (s->inst_inv64) {
+        RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+        cudaFree(s->inst_inv64);
+        s->inst_inv64 = nullptr;
+    }
     const int64_t n = s->n - s->n_spheres;
     if (n <= 0) return RT_OK;
     int64_t grid = (n + 255) / 256;
     if (grid > (int64_t)c->num_sms * 16) grid = (int64_t)c->num_sms * 16;
     normals_from_tris_kernel<<<(unsigned)grid, 256, 0, c->stream>>>(n, s->tris, s->tri_attr, s->wnormal64);
     RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}
+
+int rt_scene_set_local_frames(rt_ctx* c, rt_scene* s, int32_t n_inst, const double* inv12, const double* rows9) {
+    RT_CHECK_ARG(c && s && n_inst >= 1 && inv12 && rows9, "NULL argument or no instance");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    if (s->inst_inv64) cudaFree(s->inst_inv64);
+    s->inst_inv64 = nullptr;
+    RT_CUDA_TRY(cudaMalloc(&s->inst_inv64, sizeof(double) * 12 * (size_t)n_inst));
+    RT_CUDA_TRY(cudaMemcpy(s->inst_inv64, inv12, sizeof(double) * 12 * (size_t)n_inst, cudaMemcpyHostToDevice));
+    if (!s->lrows64) RT_CUDA_TRY(cudaMalloc(&s->lrows64, sizeof(double) * 9 * (size_t)s->n));
+    RT_CUDA_TRY(cudaMemcpy(s->lrows64, rows9, sizeof(double) * 9 * (size_t)s->n, cudaMemcpyHostToDevice));
     return RT_OK;
 }
 
@@ -422,11 +446,11 @@ int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, 
     if (vertices_f32)
         refit_mesh_kernel<float><<<(unsigned)grid, 256, 0, c->stream>>>(
             m->nf, m->n_inst, m->faces, reinterpret_cast<const float*>(m->verts), m->xform, m->offset, s->tris, s->tri_attr,
-            ln, m->local ? s->lrows64 : nullptr, m->local ? nullptr : s->wnormal64);
+            ln, s->lrows64, m->local ? nullptr : s->wnormal64);
     else
         refit_mesh_kernel<double><<<(unsigned)grid, 256, 0, c->stream>>>(m->nf, m->n_inst, m->faces, m->verts, m->xform,
                                                                          m->offset, s->tris, s->tri_attr, ln,
-                                                                         m->local ? s->lrows64 : nullptr,
+                                                                         s->lrows64,
                                                                          m->local ? nullptr : s->wnormal64);
     RT_CUDA_TRY(cudaGetLastError());
     s->built = 0;
@@ -449,7 +473,7 @@ void rt_scene_destroy(rt_scene* s) {
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->child,
                     s->flags, s->cbounds, s->sort_scratch, s->leaf_box, s->emit_items, s->seg_count, s->lights,
                     s->spheres,
-                    s->lnormal64, s->lrows64, s->wnormal64};
+                    s->lnormal64, s->lrows64, s->wnormal64, s->inst_inv64};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     delete s;

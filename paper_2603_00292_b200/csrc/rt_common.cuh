@@ -71,6 +71,8 @@ struct rt_scene {
     double* lnormal64;              // (n, 3) float64 local normals (reference order), triangles
     double* lrows64;                // (n, 9) float64 local vertices (BLAS): the host query's exact refinement
     double* wnormal64;              // (n, 3) float64 world normals (flat scene, nullable): host query output
+    double* inst_inv64;             // (instances, 12) float64 inverses of a flat scene (nullable): with
+                                    // lrows64 = the local vertices per flat id, the query refines in local space
     int custom;                     // 1: prims are AABBs of custom primitives (geom_type, data_offset)
     int geom_type;
     int64_t data_offset;

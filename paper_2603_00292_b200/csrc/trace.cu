@@ -98,7 +98,8 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
                                 const float* __restrict__ wtris, const double* __restrict__ o64,
                                 const double* __restrict__ d64, const double* __restrict__ tmin64,
                                 const double* __restrict__ tmax64, double tmin_s, double tmax_s,
-                                const double* __restrict__ wn64) {
+                                const double* __restrict__ wn64, const double* __restrict__ inv64,
+                                const double* __restrict__ lrows64) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         float4 h = hits[i];
         int id = __float_as_int(h.y);
@@ -109,11 +110,22 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
             float4 a = attr[id];
             double th = h.x, uh = h.z, vh = h.w;
             if (o64 && id < sv.base) {
-                const double o[3] = {o64[3 * i], o64[3 * i + 1], o64[3 * i + 2]};
-                const double d[3] = {d64[3 * i], d64[3 * i + 1], d64[3 * i + 2]};
-                double u2, v2;
-                const double t2 = tri_hit_f64(o, d, tmin64 ? tmin64[i] : tmin_s, tmax64 ? tmax64[i] : tmax_s,
-                                              wtris + 9 * (int64_t)id, u2, v2);
+                double o[3] = {o64[3 * i], o64[3 * i + 1], o64[3 * i + 2]};
+                double d[3] = {d64[3 * i], d64[3 * i + 1], d64[3 * i + 2]};
+                double u2, v2, t2;
+                const double lo_t = tmin64 ? tmin64[i] : tmin_s, hi_t = tmax64 ? tmax64[i] : tmax_s;
+                if (inv64 && lrows64) {
+                    // exactly the reference's path: the ray to the instance's local space with
+                    // its float64 inverse (accel.py:804-809), _tri_hit on the local vertices
+                    double m[12], ol[3], dl[3];
+                    const int ins = tri_inst[id];
+#pragma unroll
+                    for (int k = 0; k < 12; ++k) m[k] = inv64[12 * (int64_t)ins + k];
+                    to_local_f64(m, o[0], o[1], o[2], d[0], d[1], d[2], ol, dl);
+                    t2 = tri_hit_f64(ol, dl, lo_t, hi_t, lrows64 + 9 * (int64_t)id, u2, v2);
+                } else {
+                    t2 = tri_hit_f64(o, d, lo_t, hi_t, wtris + 9 * (int64_t)id, u2, v2);
+                }
                 if (t2 >= 0.0) { th = t2; uh = u2; vh = v2; }
             }
             t[i] = th; inst[i] = tri_inst[id]; prim[i] = tri_prim[id]; u[i] = uh; v[i] = vh;
@@ -247,7 +259,7 @@ int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, 
     expand_hits_f64<<<grid, 256, 0, ctx->stream>>>(n, hits, s->tri_attr, s->tri_inst, s->tri_prim, t, inst, prim,
                                                     u, v, nrm, rays, rt_sphere_view(ctx, s, 0), st32,
                                                     st32 ? st64 : nullptr, s->tris, o64, d64, tmin64, tmax64, tmin_s,
-                                                    tmax_s, s->wnormal64);
+                                                    tmax_s, s->wnormal64, s->inst_inv64, s->lrows64);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }

@@ -330,6 +330,7 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
         mesh_cache[name] = (V, F, lo.min(axis=0), hi.max(axis=0), _local_normals(V, F))
 
     tris, normals, t_inst, t_prim, t_mask, t_mat = [], [], [], [], [], []
+    local_rows = []                # float64 local vertices per flat primitive (the query's refinement)
     inst_material, inst_list, inverses = [], [], []
     wlo, whi = [], []
     mesh_inst = {}                 # mesh name -> [(3x4 matrix, inverse, first flat triangle)]
@@ -356,6 +357,7 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
              m[2, 0] * V[:, 0:1] + m[2, 1] * V[:, 1:2] + m[2, 2] * V[:, 2:3] + m[2, 3])
         Wv = np.concatenate(W, axis=1)
         tris.append(Wv[F].reshape(-1, 9).astype(np.float32))
+        local_rows.append(V[F].reshape(-1, 9))
         normals.append(_world_normals(inv, *ln))       # float64; GpuTlas keeps both widths
         nt = F.shape[0]
         t_inst.append(np.full(nt, i, np.int32))
@@ -391,6 +393,7 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
             hi32 = np.where(hi32.astype(np.float64) < hi, np.nextafter(hi32, np.float32(np.inf)), hi32)
             tris.append(np.concatenate([lo32, hi32, lo32]).reshape(1, 9).astype(np.float32))
             normals.append(np.zeros((1, 3)))
+            local_rows.append(np.zeros((1, 9)))
             inst_idx = len(desc.instances) + k
             t_inst.append(np.array([inst_idx], np.int32))
             t_prim.append(np.zeros(1, np.int32))
@@ -408,6 +411,9 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
                    bits=QUALITIES[quality], root_lo=root_lo, root_hi=root_hi,
                    instances=len(desc.instances) + len(desc.spheres), inverses=np.array(inverses),
                    spheres=np.array(sph_rows) if sph_rows else None)
+    inv12 = np.ascontiguousarray(np.array(inverses, np.float64).reshape(-1, 12))
+    check(lib().rt_scene_set_local_frames(ctx.handle, tlas.handle, inv12.shape[0], ptr(inv12),
+                                          ptr(np.ascontiguousarray(np.concatenate(local_rows), np.float64))))
     registry = IntersectorRegistry()
     if desc.spheres:
         registry.register(SPHERE_GEOM_TYPE, 0, sphere_intersector,

@@ -62,6 +62,9 @@ def test_cornell_config1_primaries(native, cornell_oracle, bits):
     r = cornell_oracle.closest_hit_batch(O, D)
     agree, _ = _compare(g, r, O.shape[0], allow_t_outliers=0.0)
     assert agree == 1.0
+    # SRT instances: the query refines along the reference's own path (local ray, local
+    # float64 vertices), so t, u, v are its values bit for bit
+    assert _exact_tuv(g, r) == 1.0
 
 
 def test_cornell_golden_primaries(native):
@@ -69,7 +72,12 @@ def test_cornell_golden_primaries(native):
     sc = compile_scene(scenes.cornell_description())
     gd = golden("cornell_hits")
     g = closest_hit_batch(sc, gd["O"], gd["D"])
-    _compare(g, tuple(gd[k] for k in ("t", "inst", "prim", "u", "v", "n")), gd["O"].shape[0], 0.0)
+    ref = tuple(gd[k] for k in ("t", "inst", "prim", "u", "v", "n"))
+    _compare(g, ref, gd["O"].shape[0], 0.0)
+    # the reference's own (t, u, v, normal), bit for bit, on every agreeing hit
+    assert _exact_tuv(g, ref) == 1.0
+    both = (g[1] == ref[1]) & (g[2] == ref[2]) & (ref[1] >= 0)
+    assert np.array_equal(g[5][both], ref[5][both])
 
 
 def test_cornell_random_rays_tminmax_mask(native):
