@@ -337,8 +337,9 @@ def run_ours(args, ws, rank, local):
             assert np.array_equal(host_v.astype(np.float64), mesh_v)
             # (1) the reference arm's own path: refit(mesh vertices) + render_frame('eye') -> host
             #     float64 AccumBuffer (H2D: the vertices; D2H: the (H, W, 4) float64 sums)
-            sc.refit_mesh("mesh", host_v, bits=30)
-            render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
+            for _ in range(3):      # warm-up: device mesh, pinned readback blocks cached
+                sc.refit_mesh("mesh", host_v, bits=30)
+                render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
             ke = max(3, min(K, 30))       # ~2 ms each at config 2: enough to average out host hiccups
             gc.collect()
             if ws > 1:
@@ -362,7 +363,9 @@ def run_ours(args, ws, rank, local):
                 sel = (rows[:, None] * W + np.arange(W)[None, :]).ravel()
                 r = r[sel]
             O, D = host_pinned_copy(np.ascontiguousarray(r[:, 0:3])), host_pinned_copy(np.ascontiguousarray(r[:, 4:7]))
-            closest_hit_batch(sc, O, D)
+            for _ in range(3):      # warm-up: IO slots and pinned output blocks cached
+                tl.refit(host_tris, 30)
+                closest_hit_batch(sc, O, D)
             kq = max(1, min(K, 10))
             gc.collect()
             if ws > 1:
