@@ -27,6 +27,7 @@ extern "C" {
 #define RT_ENOMEM (-5)        /* device allocation failed     -> MemoryError  */
 #define RT_ESTATE (-6)        /* e.g. trace before build      -> RuntimeError */
 #define RT_ENCCL (-7)         /* NCCL failure (rt_multi_render) -> RuntimeError */
+#define RT_EBUILD (-8)        /* invalid geometry (Blas.from_mesh checks, accel.py:223-236) -> BuildError */
 
 #define RT_INTEG_EYE 0        /* integrators.py:129-141 _sample_eye   */
 #define RT_INTEG_AO 1         /* integrators.py:144-179 _sample_ao    (megakernel) */
@@ -124,6 +125,54 @@ int rt_mesh_create(rt_ctx* ctx, int64_t n_vertices, int64_t n_faces, const int32
 int rt_scene_refit_mesh(rt_ctx* ctx, rt_scene* scene, rt_mesh* mesh, int64_t n_vertices, const void* vertices,
                         int32_t vertices_f32);
 void rt_mesh_destroy(rt_mesh* mesh);
+/* ---- compile_scene on the device (scene.py:79-141) ----------------------
+ * rt_mesh_upload: one mesh as the reference holds it -- vertices (nv, 3) float64 and faces
+ * (nf, 3) int64, host -- goes up once and is validated on the device exactly like
+ * Blas.from_mesh (accel.py:223-236): zero faces -> "cannot build over zero primitives",
+ * an index outside [0, nv) -> "face index out of range", else the first triangle with a
+ * non-finite coordinate -> "non-finite bounds for primitive k" (all RT_EBUILD).  bounds6
+ * receives the float64 root box (lo xyz, hi xyz: the union of the triangle boxes, i.e. the
+ * reference Blas's root node bounds).  The mesh stays resident (faces as int32) for
+ * rt_scene_compile and later rt_scene_refit_mesh calls. */
+int rt_mesh_upload(rt_ctx* ctx, int64_t n_vertices, const double* vertices, int64_t n_faces, const int64_t* faces,
+                   double* bounds6, rt_mesh** out);
+int rt_mesh_info(rt_mesh* mesh, int64_t* n_vertices, int64_t* n_faces, double* bounds6);
+/* one instance of compile_scene (Instance(blas_of_mesh[decl.mesh], decl.frame, decl.mask),
+ * scene.py:91-97): matrix = frame_to_matrix(frame), inverse = invert_affine(matrix), both 3x4
+ * row-major float64 (accel.py:311-336) */
+typedef struct {
+    int32_t mesh;             /* index into the meshes array */
+    int32_t material;         /* material row */
+    uint32_t mask;            /* instance visibility mask */
+    int32_t reserved;
+    double matrix[12];
+    double inverse[12];
+} rt_instance_src;
+/* one custom primitive (a sphere instance, scene.py:101-112): its instance world AABB rounded
+ * outward to fp32 as (lo, hi, lo); row = instance inverse 3x4, local center xyz, radius */
+typedef struct {
+    float box[9];
+    int32_t material;
+    uint32_t mask;
+    double row[16];
+} rt_custom_src;
+/* The flat scene of all instances in instance order (flat id = (instance, prim) order, so the
+ * reference tie rule is "lowest flat id"), written on the device by one kernel per mesh:
+ * world fp32 rows (m . v in float64, reference operation order), float64 world normals
+ * (geometry.py:229-237 local normal, accel.py:843-847 inverse-transpose), the float64 local
+ * rows + instance inverses of the host query's refinement, ids, masks, materials; custom
+ * primitives appended.  Every mesh referenced keeps its placements for rt_scene_refit_mesh.
+ * The BVH is not built (rt_bvh_build). */
+int rt_scene_compile(rt_ctx* ctx, int32_t n_meshes, rt_mesh* const* meshes, int32_t n_inst,
+                     const rt_instance_src* instances, int32_t n_custom, const rt_custom_src* custom,
+                     const float* mat_color, const float* mat_emissive, int32_t n_mat, rt_scene** out);
+/* the scene's per-primitive ids, device -> host (any pointer may be NULL; synchronises) */
+int rt_scene_get_ids(rt_ctx* ctx, rt_scene* scene, int32_t* tri_inst, int32_t* tri_prim, uint32_t* tri_mask,
+                     int32_t* tri_material);
+/* the scene's geometry, device -> host (parity checks; any pointer may be NULL): (n, 9) fp32
+ * rows, (n, 3) fp32 shading normals, (n, 3) float64 world normals, (n, 9) float64 local rows */
+int rt_scene_get_geometry(rt_ctx* ctx, rt_scene* scene, float* tris9, float* normals3, double* normals64,
+                          double* local_rows9);
 /* world normals of the scene's triangles recomputed on the device from its current (world)
  * vertices, float64 in the reference order with an identity frame (after
  * rt_scene_set_vertices, whose rows are world triangles) */

@@ -24,6 +24,7 @@ RT_EDEPTH = -4
 RT_ENOMEM = -5
 RT_ESTATE = -6
 RT_ENCCL = -7
+RT_EBUILD = -8
 RT_SPLIT_SAMPLES = 0
 RT_SPLIT_TILES = 1
 
@@ -60,6 +61,18 @@ class RenderParams(ctypes.Structure):
                 ("normal_offset", ctypes.c_float), ("pix_lo", ctypes.c_int64),
                 ("pix_hi", ctypes.c_int64), ("band_stride", ctypes.c_int32), ("band_offset", ctypes.c_int32),
                 ("ao_count", ctypes.c_int32), ("ao_length", ctypes.c_float)]
+
+
+class InstanceSrc(ctypes.Structure):
+    """rt_instance_src (include/rt_b200.h)."""
+    _fields_ = [("mesh", ctypes.c_int32), ("material", ctypes.c_int32), ("mask", ctypes.c_uint32),
+                ("reserved", ctypes.c_int32), ("matrix", ctypes.c_double * 12), ("inverse", ctypes.c_double * 12)]
+
+
+class CustomSrc(ctypes.Structure):
+    """rt_custom_src (include/rt_b200.h)."""
+    _fields_ = [("box", ctypes.c_float * 9), ("material", ctypes.c_int32), ("mask", ctypes.c_uint32),
+                ("row", ctypes.c_double * 16)]
 
 
 def lib():
@@ -113,6 +126,11 @@ def lib():
             "rt_scene_get_vertices": [vp, vp, vp],
             "rt_scene_set_normals64": [vp, vp, vp],
             "rt_scene_set_local_frames": [vp, vp, i32, vp, vp],
+            "rt_mesh_upload": [vp, i64, vp, i64, vp, vp, vp],
+            "rt_mesh_info": [vp, vp, vp, vp],
+            "rt_scene_compile": [vp, i32, vp, i32, vp, i32, vp, vp, vp, i32, vp],
+            "rt_scene_get_ids": [vp, vp, vp, vp, vp, vp],
+            "rt_scene_get_geometry": [vp, vp, vp, vp, vp, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -136,7 +154,7 @@ def check(rc):
     msg = lib().rt_last_error().decode(errors="replace")
     if rc == RT_EINVAL:
         raise ValueError(msg)
-    if rc == RT_EDEPTH:
+    if rc in (RT_EDEPTH, RT_EBUILD):
         raise BuildError(msg)
     if rc == RT_EUNSUPPORTED:
         raise RegistryError(msg)

@@ -8,7 +8,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "librt_b200.so")
-SOURCES = ["capi.cu", "lbvh.cu", "trace.cu", "render.cu", "tlas.cu", "multi.cu"]
+SOURCES = ["capi.cu", "mesh.cu", "lbvh.cu", "trace.cu", "render.cu", "tlas.cu", "multi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # no --use_fast_math: the shading code depends on IEEE signed zeros
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

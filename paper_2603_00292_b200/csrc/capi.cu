@@ -225,247 +225,6 @@ int rt_scene_set_vertices(rt_ctx* c, rt_scene* s, const float* tris) {
     return RT_OK;
 }
 
-}  // extern "C"
-
-struct rt_mesh {
-    int device;
-    int64_t nv, nf;
-    int32_t n_inst;
-    int32_t local;        // RT_MESH_LOCAL: rows = the local vertices, float64 local normals
-    int3* faces;          // (nf) device
-    double* xform;        // (n_inst, 21) device
-    int64_t* offset;      // (n_inst) device: first flat triangle of each instance
-    double* verts;        // (nv, 3) device staging of the latest refit
-};
-
-namespace {
-
-// world triangles + world normals of every (instance, face): scene.py compile_scene's
-// float64 expressions in their evaluation order, each operation correctly rounded
-// (__dmul_rn / __dadd_rn / __dsub_rn keep nvcc from contracting them into FMAs)
-__device__ __forceinline__ double dot3_affine(const double* m, double x, double y, double z) {
-    return __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(m[0], x), __dmul_rn(m[1], y)), __dmul_rn(m[2], z)), m[3]);
-}
-
-template <typename T>
-__global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __restrict__ faces,
-                                  const T* __restrict__ Vt, const double* __restrict__ xform,
-                                  const int64_t* __restrict__ offset, float* __restrict__ tris,
-                                  float4* __restrict__ attr, double* __restrict__ lnormal64,
-                                  double* __restrict__ lrows64, double* __restrict__ wnormal64) {
-    const int64_t total = nf * n_inst;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t j = (int32_t)(q / nf);
-        const int64_t k = q - (int64_t)j * nf;
-        const double* m = xform + 21 * j;
-        const double* inv = m + 12;
-        const int3 f = faces[k];
-        // fp32 vertices widen exactly: the same float64 values compile_scene would see
-        const double a[3] = {(double)Vt[3 * (int64_t)f.x], (double)Vt[3 * (int64_t)f.x + 1], (double)Vt[3 * (int64_t)f.x + 2]};
-        const double b[3] = {(double)Vt[3 * (int64_t)f.y], (double)Vt[3 * (int64_t)f.y + 1], (double)Vt[3 * (int64_t)f.y + 2]};
-        const double c[3] = {(double)Vt[3 * (int64_t)f.z], (double)Vt[3 * (int64_t)f.z + 1], (double)Vt[3 * (int64_t)f.z + 2]};
-        float* t = tris + 9 * (offset[j] + k);
-        const double* vs[3] = {a, b, c};
-        double* rows64 = lrows64 ? lrows64 + 9 * (offset[j] + k) : nullptr;
-        if (rows64 && !lnormal64) {   // a flat scene keeping its local vertices for the query
-#pragma unroll
-            for (int v = 0; v < 3; ++v)
-#pragma unroll
-                for (int r = 0; r < 3; ++r) rows64[3 * v + r] = vs[v][r];
-        }
-        if (lnormal64) {       // a BLAS: its rows are the local vertices themselves (Blas._rows)
-#pragma unroll
-            for (int v = 0; v < 3; ++v)
-#pragma unroll
-                for (int r = 0; r < 3; ++r) {
-                    t[3 * v + r] = __double2float_rn(vs[v][r]);
-                    if (rows64) rows64[3 * v + r] = vs[v][r];
-                }
-        } else {
-#pragma unroll
-            for (int v = 0; v < 3; ++v)
-#pragma unroll
-                for (int r = 0; r < 3; ++r)
-                    t[3 * v + r] = __double2float_rn(dot3_affine(m + 4 * r, vs[v][0], vs[v][1], vs[v][2]));
-        }
-        // local normal (geometry.py:229-237): e0 = b - a, e1 = c - b, n = e0 x e1 / |n|
-        const double e0x = __dsub_rn(b[0], a[0]), e0y = __dsub_rn(b[1], a[1]), e0z = __dsub_rn(b[2], a[2]);
-        const double e1x = __dsub_rn(c[0], b[0]), e1y = __dsub_rn(c[1], b[1]), e1z = __dsub_rn(c[2], b[2]);
-        const double nx = __dsub_rn(__dmul_rn(e0y, e1z), __dmul_rn(e0z, e1y));
-        const double ny = __dsub_rn(__dmul_rn(e0z, e1x), __dmul_rn(e0x, e1z));
-        const double nz = __dsub_rn(__dmul_rn(e0x, e1y), __dmul_rn(e0y, e1x));
-        const double nlen = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(nx, nx), __dmul_rn(ny, ny)), __dmul_rn(nz, nz)));
-        const double lx = __ddiv_rn(nx, nlen), ly = __ddiv_rn(ny, nlen), lz = __ddiv_rn(nz, nlen);
-        if (lnormal64) {       // the two-level kernels transform the float64 local normal per hit
-            double* ln = lnormal64 + 3 * (offset[j] + k);
-            ln[0] = lx; ln[1] = ly; ln[2] = lz;
-            continue;
-        }
-        // world normal (accel.py:843-847): inverse-transpose sum, times 1 / sqrt(|w|^2)
-        const double wx = __dadd_rn(__dadd_rn(__dmul_rn(inv[0], lx), __dmul_rn(inv[3], ly)), __dmul_rn(inv[6], lz));
-        const double wy = __dadd_rn(__dadd_rn(__dmul_rn(inv[1], lx), __dmul_rn(inv[4], ly)), __dmul_rn(inv[7], lz));
-        const double wz = __dadd_rn(__dadd_rn(__dmul_rn(inv[2], lx), __dmul_rn(inv[5], ly)), __dmul_rn(inv[8], lz));
-        const double il =
-            __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(wx, wx), __dmul_rn(wy, wy)), __dmul_rn(wz, wz))));
-        const double nwx = __dmul_rn(wx, il), nwy = __dmul_rn(wy, il), nwz = __dmul_rn(wz, il);
-        float4* at = attr + offset[j] + k;
-        const float w = at->w;                          // material index bits stay
-        *at = make_float4(__double2float_rn(nwx), __double2float_rn(nwy), __double2float_rn(nwz), w);
-        if (wnormal64) {
-            double* wn = wnormal64 + 3 * (offset[j] + k);
-            wn[0] = nwx; wn[1] = nwy; wn[2] = nwz;
-        }
-    }
-}
-
-// normals of world triangles given directly (GpuTlas.refit): the same float64 expressions
-// with an identity instance frame (its inverse-transpose sum is exact, the renormalisation
-// is kept)
-__global__ void normals_from_tris_kernel(int64_t n, const float* __restrict__ tris, float4* __restrict__ attr,
-                                         double* __restrict__ wnormal64) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const float* t = tris + 9 * i;
-        const double e0x = __dsub_rn(t[3], t[0]), e0y = __dsub_rn(t[4], t[1]), e0z = __dsub_rn(t[5], t[2]);
-        const double e1x = __dsub_rn(t[6], t[3]), e1y = __dsub_rn(t[7], t[4]), e1z = __dsub_rn(t[8], t[5]);
-        const double nx = __dsub_rn(__dmul_rn(e0y, e1z), __dmul_rn(e0z, e1y));
-        const double ny = __dsub_rn(__dmul_rn(e0z, e1x), __dmul_rn(e0x, e1z));
-        const double nz = __dsub_rn(__dmul_rn(e0x, e1y), __dmul_rn(e0y, e1x));
-        const double nlen = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(nx, nx), __dmul_rn(ny, ny)), __dmul_rn(nz, nz)));
-        const double lx = __ddiv_rn(nx, nlen), ly = __ddiv_rn(ny, nlen), lz = __ddiv_rn(nz, nlen);
-        const double il =
-            __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(lx, lx), __dmul_rn(ly, ly)), __dmul_rn(lz, lz))));
-        const double wx = __dmul_rn(lx, il), wy = __dmul_rn(ly, il), wz = __dmul_rn(lz, il);
-        float4 a = attr[i];
-        a.x = __double2float_rn(wx);
-        a.y = __double2float_rn(wy);
-        a.z = __double2float_rn(wz);
-        attr[i] = a;
-        if (wnormal64) { wnormal64[3 * i] = wx; wnormal64[3 * i + 1] = wy; wnormal64[3 * i + 2] = wz; }
-    }
-}
-
-}  // namespace
-
-extern "C" {
-
-int rt_scene_update_normals(rt_ctx* c, rt_scene* s) {
-    RT_CHECK_ARG(c && s, "NULL argument");
-    RT_CUDA_TRY(cudaSetDevice(c->device));
-    // new world rows: the local vertices / frames no longer describe them
-    if (s->inst_inv64) {
-        RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-        cudaFree(s->inst_inv64);
-        s->inst_inv64 = nullptr;
-    }
-    const int64_t n = s->n - s->n_spheres;
-    if (n <= 0) return RT_OK;
-    int64_t grid = (n + 255) / 256;
-    if (grid > (int64_t)c->num_sms * 16) grid = (int64_t)c->num_sms * 16;
-    normals_from_tris_kernel<<<(unsigned)grid, 256, 0, c->stream>>>(n, s->tris, s->tri_attr, s->wnormal64);
-    RT_CUDA_TRY(cudaGetLastError());
-    return RT_OK;
-}
-
-int rt_scene_set_local_frames(rt_ctx* c, rt_scene* s, int32_t n_inst, const double* inv12, const double* rows9) {
-    RT_CHECK_ARG(c && s && n_inst >= 1 && inv12 && rows9, "NULL argument or no instance");
-    RT_CUDA_TRY(cudaSetDevice(c->device));
-    if (s->inst_inv64) cudaFree(s->inst_inv64);
-    s->inst_inv64 = nullptr;
-    RT_CUDA_TRY(cudaMalloc(&s->inst_inv64, sizeof(double) * 12 * (size_t)n_inst));
-    RT_CUDA_TRY(cudaMemcpy(s->inst_inv64, inv12, sizeof(double) * 12 * (size_t)n_inst, cudaMemcpyHostToDevice));
-    if (!s->lrows64) RT_CUDA_TRY(cudaMalloc(&s->lrows64, sizeof(double) * 9 * (size_t)s->n));
-    RT_CUDA_TRY(cudaMemcpy(s->lrows64, rows9, sizeof(double) * 9 * (size_t)s->n, cudaMemcpyHostToDevice));
-    return RT_OK;
-}
-
-int rt_scene_set_normals64(rt_ctx* c, rt_scene* s, const double* n3) {
-    RT_CHECK_ARG(c && s && n3, "NULL argument");
-    RT_CUDA_TRY(cudaSetDevice(c->device));
-    if (!s->wnormal64) RT_CUDA_TRY(cudaMalloc(&s->wnormal64, sizeof(double) * 3 * (size_t)s->n));
-    RT_CUDA_TRY(cudaMemcpy(s->wnormal64, n3, sizeof(double) * 3 * (size_t)s->n, cudaMemcpyHostToDevice));
-    return RT_OK;
-}
-
-int rt_scene_get_vertices(rt_ctx* c, rt_scene* s, float* tris) {
-    RT_CHECK_ARG(c && s && tris, "NULL argument");
-    RT_CUDA_TRY(cudaSetDevice(c->device));
-    RT_CUDA_TRY(cudaMemcpyAsync(tris, s->tris, sizeof(float) * 9 * s->n, cudaMemcpyDeviceToHost, c->stream));
-    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-    return RT_OK;
-}
-
-int rt_mesh_create(rt_ctx* c, int64_t n_vertices, int64_t n_faces, const int32_t* faces, int32_t n_inst,
-                   const double* xform, const int64_t* tri_offset, int32_t flags, rt_mesh** out) {
-    RT_CHECK_ARG(c && faces && xform && tri_offset && out, "NULL argument");
-    RT_CHECK_ARG(n_vertices >= 3 && n_faces >= 1 && n_inst >= 1, "empty mesh or no instance");
-    RT_CHECK_ARG(!(flags & RT_MESH_LOCAL) || n_inst == 1, "a local (BLAS) mesh has exactly one placement");
-    for (int64_t k = 0; k < 3 * n_faces; ++k)
-        RT_CHECK_ARG(faces[k] >= 0 && faces[k] < n_vertices, "face index out of range");
-    RT_CUDA_TRY(cudaSetDevice(c->device));
-    rt_mesh* m = new rt_mesh();
-    m->device = c->device;
-    m->nv = n_vertices;
-    m->nf = n_faces;
-    m->n_inst = n_inst;
-    m->local = (flags & RT_MESH_LOCAL) ? 1 : 0;
-    cudaError_t e = cudaMalloc(&m->faces, sizeof(int3) * n_faces);
-    if (e == cudaSuccess) e = cudaMalloc(&m->xform, sizeof(double) * 21 * n_inst);
-    if (e == cudaSuccess) e = cudaMalloc(&m->offset, sizeof(int64_t) * n_inst);
-    if (e == cudaSuccess) e = cudaMalloc(&m->verts, sizeof(double) * 3 * n_vertices);
-    if (e == cudaSuccess) e = cudaMemcpy(m->faces, faces, sizeof(int3) * n_faces, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(m->xform, xform, sizeof(double) * 21 * n_inst, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(m->offset, tri_offset, sizeof(int64_t) * n_inst, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-        rt_mesh_destroy(m);
-        rt_set_error("rt_mesh_create: %s", cudaGetErrorString(e));
-        return RT_ECUDA;
-    }
-    *out = m;
-    return RT_OK;
-}
-
-int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, const void* vertices,
-                        int32_t vertices_f32) {
-    RT_CHECK_ARG(c && s && m && vertices, "NULL argument");
-    RT_CHECK_ARG(m->device == c->device, "mesh and context live on different devices");
-    if (n_vertices != m->nv) {
-        rt_set_error("vertex count changed (%lld -> %lld)", (long long)m->nv, (long long)n_vertices);
-        return RT_EINVAL;
-    }
-    if (m->local && !s->lnormal64) {
-        rt_set_error("a local (BLAS) mesh refits a scene with float64 local normals");
-        return RT_EINVAL;
-    }
-    RT_CUDA_TRY(cudaSetDevice(c->device));
-    double* ln = m->local ? s->lnormal64 : nullptr;
-    const size_t vbytes = (vertices_f32 ? sizeof(float) : sizeof(double)) * 3 * m->nv;
-    RT_CUDA_TRY(cudaMemcpyAsync(m->verts, vertices, vbytes, cudaMemcpyHostToDevice, c->stream));
-    const int64_t total = m->nf * m->n_inst;
-    int64_t grid = (total + 255) / 256;
-    if (grid > (int64_t)c->num_sms * 16) grid = (int64_t)c->num_sms * 16;
-    if (vertices_f32)
-        refit_mesh_kernel<float><<<(unsigned)grid, 256, 0, c->stream>>>(
-            m->nf, m->n_inst, m->faces, reinterpret_cast<const float*>(m->verts), m->xform, m->offset, s->tris, s->tri_attr,
-            ln, s->lrows64, m->local ? nullptr : s->wnormal64);
-    else
-        refit_mesh_kernel<double><<<(unsigned)grid, 256, 0, c->stream>>>(m->nf, m->n_inst, m->faces, m->verts, m->xform,
-                                                                         m->offset, s->tris, s->tri_attr, ln,
-                                                                         s->lrows64,
-                                                                         m->local ? nullptr : s->wnormal64);
-    RT_CUDA_TRY(cudaGetLastError());
-    s->built = 0;
-    return RT_OK;
-}
-
-void rt_mesh_destroy(rt_mesh* m) {
-    if (!m) return;
-    cudaSetDevice(m->device);
-    void* ptrs[] = {m->faces, m->xform, m->offset, m->verts};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
-    delete m;
-}
-
 void rt_scene_destroy(rt_scene* s) {
     if (!s) return;
     rt_render_release(s);

@@ -45,39 +45,60 @@ class LightTable:
 
 
 class GpuTlas:
-    """Device-resident flattened scene + LBVH (replaces Tlas/TlasBundle, accel.py:439-549)."""
+    """Device-resident flattened scene + LBVH (replaces Tlas/TlasBundle, accel.py:439-549).
 
-    def __init__(self, ctx, tris, normals, tri_inst, tri_prim, tri_mask, tri_material, mat_color,
-                 mat_emissive, bits=30, root_lo=None, root_hi=None, instances=None, inverses=None, spheres=None):
+    The geometry lives on the device only (rt_scene_compile wrote it there); the host
+    views ``tris``, ``tri_inst``, ``tri_prim``, ``tri_mask``, ``tri_material`` are read
+    back on first use."""
+
+    def __init__(self, ctx, handle, n, bits=30, sphere_rows=None, n_instances=None, inverses=None, build=True):
         self.ctx = ctx
-        self.n = int(tris.shape[0])
+        self.handle = handle
+        self.n = int(n)
         self.bits = bits
-        self._tris = np.ascontiguousarray(tris, np.float32).reshape(-1, 9)
-        normals64 = np.ascontiguousarray(normals, np.float64).reshape(-1, 3)
-        self.normals = np.ascontiguousarray(normals64, np.float32)
-        self.tri_inst = np.ascontiguousarray(tri_inst, np.int32)
-        self.tri_prim = np.ascontiguousarray(tri_prim, np.int32)
-        self.tri_mask = np.ascontiguousarray(tri_mask, np.uint32)
-        self.tri_material = np.ascontiguousarray(tri_material, np.int32)
+        self.n_instances = n_instances
         self.inverses = inverses
-        self.n_instances = instances
-        self.world_root = (root_lo, root_hi)
-        mc = np.ascontiguousarray(mat_color, np.float32).reshape(-1, 3)
-        me = np.ascontiguousarray(mat_emissive, np.float32).reshape(-1, 3)
-        h = ctypes.c_void_p()
-        check(lib().rt_scene_create(ctx.handle, self.n, ptr(self._tris), ptr(self.normals), ptr(self.tri_inst),
-                                    ptr(self.tri_prim), ptr(self.tri_mask), ptr(self.tri_material), ptr(mc),
-                                    ptr(me), mc.shape[0], ctypes.byref(h)))
-        self.handle = h
-        # the float64 world normals themselves, for the host query's outputs
-        check(lib().rt_scene_set_normals64(ctx.handle, h, ptr(normals64)))
+        self._tris = None
+        self._ids = None
         self.build_ms = None
-        # custom primitives: the last rows of `tris` are sphere instance boxes
-        self.sphere_rows = np.zeros((0, 16)) if spheres is None else np.ascontiguousarray(spheres, np.float64)
+        # custom primitives: the last rows are sphere instance boxes
+        self.sphere_rows = np.zeros((0, 16)) if sphere_rows is None else np.ascontiguousarray(sphere_rows, np.float64)
         self.n_spheres = int(self.sphere_rows.shape[0])
-        if self.n_spheres:
-            check(lib().rt_scene_set_spheres(ctx.handle, h, self.n_spheres, ptr(self.sphere_rows)))
-        self.build(bits)
+        if build:
+            self.build(bits)
+
+    def _download_ids(self):
+        if self._ids is None:
+            n = self.n
+            ids = (np.empty(n, np.int32), np.empty(n, np.int32), np.empty(n, np.uint32), np.empty(n, np.int32))
+            check(lib().rt_scene_get_ids(self.ctx.handle, self.handle, *(ptr(x) for x in ids)))
+            self._ids = ids
+        return self._ids
+
+    def geometry(self):
+        """(tris (n, 9) f32, shading normals (n, 3) f32, world normals (n, 3) float64, local rows
+        (n, 9) float64) of a compiled flat scene, read back from the device (parity checks)."""
+        n = self.n
+        out = (np.empty((n, 9), np.float32), np.empty((n, 3), np.float32), np.empty((n, 3), np.float64),
+               np.empty((n, 9), np.float64))
+        check(lib().rt_scene_get_geometry(self.ctx.handle, self.handle, *(ptr(x) for x in out)))
+        return out
+
+    @property
+    def tri_inst(self):
+        return self._download_ids()[0]
+
+    @property
+    def tri_prim(self):
+        return self._download_ids()[1]
+
+    @property
+    def tri_mask(self):
+        return self._download_ids()[2]
+
+    @property
+    def tri_material(self):
+        return self._download_ids()[3]
 
     def custom_geom_types(self):
         """accel.py Tlas.custom_geom_types: geometry types of the custom BLASes present."""
@@ -116,16 +137,8 @@ class GpuTlas:
 
     @classmethod
     def from_handle(cls, ctx, handle, n, bits, sphere_rows=None):
-        """Wrap a scene built on the device (rt_tlas_flatten); host geometry copies absent."""
-        self = cls.__new__(cls)
-        self.ctx, self.handle, self.n, self.bits = ctx, handle, int(n), bits
-        self._tris = self.normals = self.tri_inst = self.tri_prim = self.tri_mask = self.tri_material = None
-        self.inverses = self.n_instances = None
-        self.world_root = (None, None)
-        self.build_ms = None
-        self.sphere_rows = np.zeros((0, 16)) if sphere_rows is None else sphere_rows
-        self.n_spheres = int(self.sphere_rows.shape[0])
-        return self
+        """Wrap a scene built on the device (rt_tlas_flatten) whose LBVH is already built."""
+        return cls(ctx, handle, n, bits, sphere_rows, build=False)
 
     def build_profiled(self, bits=None):
         """Rebuild with stage events; returns dict of device ms per stage."""
@@ -178,7 +191,7 @@ class Scene:
     background: np.ndarray
     root_box: tuple
     render_tlas: object = None   # two-level scenes: the device-flattened structure rt_render walks
-    _meshes: dict = None         # flat scenes: mesh name -> _MeshRefit (device refit_mesh)
+    _meshes: dict = None         # flat scenes: mesh name -> _DeviceMesh (device refit_mesh)
     _light_src: tuple = None     # (desc, material index, instances) the light table came from
 
     def diagonal(self) -> float:
@@ -188,9 +201,10 @@ class Scene:
     def refit_mesh(self, name, vertices, bits=None):
         """Blas.refit(vertices) (accel.py:263-283) for every instance of mesh `name` of a flat
         scene, on the device: the vertices go up (float64, or float32 as given: 24 or 12 B per
-        vertex; the faces stay resident), one kernel writes the instances' world triangles and world normals exactly
-        as compile_scene does on the host, and the LBVH is rebuilt.  The scene's root
-        box and normal offset keep their compile-time values, as the reference's Scene does."""
+        vertex; the faces stay resident since compile_scene uploaded them), one kernel writes the
+        instances' world triangles and world normals exactly as compile_scene does, and the
+        LBVH is rebuilt.  The scene's root box and normal offset keep their compile-time values
+        (the reference's flat-scene equivalent is a recompile)."""
         if self.render_tlas is not None or self._meshes is None:
             raise ValueError("refit_mesh needs a flat scene (two-level scenes refit their Blas)")
         if name not in self._meshes:
@@ -202,7 +216,7 @@ class Scene:
         if V.shape[0] != mr.nv:
             raise ValueError(f"vertex count changed ({mr.nv} -> {V.shape[0]})")
         tl = self.tlas
-        check(lib().rt_scene_refit_mesh(tl.ctx.handle, tl.handle, mr.handle(tl.ctx), mr.nv, ptr(V), 1 if f32 else 0))
+        check(lib().rt_scene_refit_mesh(tl.ctx.handle, tl.handle, mr.handle, mr.nv, ptr(V), 1 if f32 else 0))
         tl._tris = None                          # the host copy is read back on demand
         desc, mat_index, inst_list = self._light_src
         if any(desc.materials[d.material].has_emission for d, _ in inst_list if d.mesh == name):
@@ -217,6 +231,28 @@ class Scene:
                                                         self.lights.area[:, None]], axis=1), np.float32)
             check(lib().rt_scene_set_lights(tl.ctx.handle, tl.handle, rows.shape[0], ptr(rows)))
         tl.build(bits)
+
+
+class _DeviceMesh:
+    """One mesh of compile_scene, resident on the device (rt_mesh_upload): the reference's
+    float64 vertices and int64 faces went up once and were validated there (Blas.from_mesh's
+    BuildError checks, accel.py:223-236); ``bounds`` is the float64 root box."""
+
+    def __init__(self, ctx, V, F):
+        self.nv = int(V.shape[0])
+        self.nf = int(F.shape[0])
+        self.bounds = np.empty(6, np.float64)
+        self._lib = lib()
+        h = ctypes.c_void_p()
+        check(lib().rt_mesh_upload(ctx.handle, self.nv, ptr(V), self.nf, ptr(F), ptr(self.bounds), ctypes.byref(h)))
+        self.handle = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None) and _native._lib is not None:
+                _native._lib.rt_mesh_destroy(self.handle)
+        except Exception:
+            pass
 
 
 class _MeshRefit:
@@ -247,29 +283,6 @@ class _MeshRefit:
                 _native._lib.rt_mesh_destroy(self._h)
         except Exception:
             pass
-
-
-def _local_normals(V, F):
-    """geometry.py:229-237, 274-275 per face, float64, reference operation order."""
-    a, b, c = V[F[:, 0]], V[F[:, 1]], V[F[:, 2]]
-    e0 = b - a
-    e1 = c - b
-    nx = e0[:, 1] * e1[:, 2] - e0[:, 2] * e1[:, 1]
-    ny = e0[:, 2] * e1[:, 0] - e0[:, 0] * e1[:, 2]
-    nz = e0[:, 0] * e1[:, 1] - e0[:, 1] * e1[:, 0]
-    with np.errstate(invalid="ignore", divide="ignore"):
-        nlen = np.sqrt(nx * nx + ny * ny + nz * nz)
-        return nx / nlen, ny / nlen, nz / nlen
-
-
-def _world_normals(inv, lnx, lny, lnz):
-    """accel.py:843-847: inverse-transpose sum, then multiply by 1/sqrt."""
-    wnx = inv[0, 0] * lnx + inv[1, 0] * lny + inv[2, 0] * lnz
-    wny = inv[0, 1] * lnx + inv[1, 1] * lny + inv[2, 1] * lnz
-    wnz = inv[0, 2] * lnx + inv[1, 2] * lny + inv[2, 2] * lnz
-    with np.errstate(invalid="ignore", divide="ignore"):
-        inv_len = 1.0 / np.sqrt(wnx * wnx + wny * wny + wnz * wnz)
-    return np.stack([wnx * inv_len, wny * inv_len, wnz * inv_len], axis=1)
 
 
 def _light_rows(desc, mats_index, inst_list):
@@ -312,65 +325,24 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
     mat_emissive = np.array([desc.materials[n].emissive for n in mat_names]).reshape(-1, 3)
     if not desc.instances and not desc.spheres:
         raise BuildError("a scene needs at least one instance")
+    ctx = _native.Context.get(device)
 
-    # per-mesh validation and local data (Blas.from_mesh, accel.py:223-236)
-    mesh_cache = {}
-    for name, mesh in desc.meshes.items():
+    # every mesh up once, validated on the device (Blas.from_mesh, accel.py:223-236)
+    mesh_names = list(desc.meshes)
+    dmeshes = {}
+    for name in mesh_names:
+        mesh = desc.meshes[name]
         V = np.ascontiguousarray(mesh.vertices, np.float64).reshape(-1, 3)
         F = np.ascontiguousarray(mesh.faces, np.int64).reshape(-1, 3)
-        if F.shape[0] == 0:
-            raise BuildError("cannot build over zero primitives")
-        if F.min() < 0 or F.max() >= V.shape[0]:
-            raise BuildError("face index out of range")
-        tri = V[F]
-        lo, hi = tri.min(axis=1), tri.max(axis=1)
-        bad = ~np.isfinite(lo).all(axis=1) | ~np.isfinite(hi).all(axis=1)
-        if bad.any():
-            raise BuildError(f"non-finite bounds for primitive {int(np.argmax(bad))}")
-        mesh_cache[name] = (V, F, lo.min(axis=0), hi.max(axis=0), _local_normals(V, F))
+        dmeshes[name] = _DeviceMesh(ctx, V, F)
 
-    tris, normals, t_inst, t_prim, t_mask, t_mat = [], [], [], [], [], []
-    local_rows = []                # float64 local vertices per flat primitive (the query's refinement)
-    inst_material, inst_list, inverses = [], [], []
-    wlo, whi = [], []
-    mesh_inst = {}                 # mesh name -> [(3x4 matrix, inverse, first flat triangle)]
-    off = 0
-    for i, decl in enumerate(desc.instances):
-        V, F, rlo, rhi, ln = mesh_cache[decl.mesh]
-        m = frame_to_matrix(decl.frame)
-        try:
-            inv = invert_affine(m)
-        except ValueError as exc:
-            raise BuildError(f"instance {i} frame is not invertible") from exc
-        mesh_inst.setdefault(decl.mesh, []).append((m, inv, off))
-        off += F.shape[0]
-        inverses.append(inv)
-        inst_list.append((decl, m))
-        # world AABB of the 8 root-box corners (accel.py:459-469)
-        corners = np.array([[(rlo, rhi)[s & 1][0], (rlo, rhi)[(s >> 1) & 1][1], (rlo, rhi)[(s >> 2) & 1][2]]
-                            for s in range(8)])
-        pts = corners @ m[:, :3].T + m[:, 3]
-        wlo.append(pts.min(axis=0))
-        whi.append(pts.max(axis=0))
-        W = (m[0, 0] * V[:, 0:1] + m[0, 1] * V[:, 1:2] + m[0, 2] * V[:, 2:3] + m[0, 3],
-             m[1, 0] * V[:, 0:1] + m[1, 1] * V[:, 1:2] + m[1, 2] * V[:, 2:3] + m[1, 3],
-             m[2, 0] * V[:, 0:1] + m[2, 1] * V[:, 1:2] + m[2, 2] * V[:, 2:3] + m[2, 3])
-        Wv = np.concatenate(W, axis=1)
-        tris.append(Wv[F].reshape(-1, 9).astype(np.float32))
-        local_rows.append(V[F].reshape(-1, 9))
-        normals.append(_world_normals(inv, *ln))       # float64; GpuTlas keeps both widths
-        nt = F.shape[0]
-        t_inst.append(np.full(nt, i, np.int32))
-        t_prim.append(np.arange(nt, dtype=np.int32))
-        t_mask.append(np.full(nt, decl.mask, np.uint32))
-        mi = mat_index[decl.material]
-        inst_material.append(mi)
-        t_mat.append(np.full(nt, mi, np.int32))
-    # sphere instances after the mesh instances (scene.py:101-112): one custom
-    # primitive each, flat ids after every triangle; its leaf box is the world AABB
-    # of the transformed local box (accel.py:459-469), rounded outward to fp32
-    sph_rows = []
-    if desc.spheres:
+    # sphere instances after the mesh instances (scene.py:101-112): one custom primitive
+    # each, flat ids after every triangle; its leaf box is the world AABB of the
+    # transformed local box (accel.py:459-469), rounded outward to fp32
+    n_sph = len(desc.spheres) if desc.spheres else 0
+    customs = (_native.CustomSrc * max(n_sph, 1))()
+    sph_rows, sph_boxes = [], []
+    if n_sph:
         rows = np.array([[*sph.center, sph.radius] for sph in desc.spheres], dtype=np.float64)
         sphere_data(rows)                               # radius > 0 (accel.py:403-408)
         for k, sph in enumerate(desc.spheres):
@@ -380,40 +352,62 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
             except ValueError as exc:
                 raise BuildError(f"sphere {k} frame is not invertible") from exc
             c, r = rows[k, :3], rows[k, 3]
-            blo, bhi = c - r, c + r
-            corners = np.array([[(blo, bhi)[s & 1][0], (blo, bhi)[(s >> 1) & 1][1], (blo, bhi)[(s >> 2) & 1][2]]
-                                for s in range(8)])
-            pts = corners @ m[:, :3].T + m[:, 3]
-            lo, hi = pts.min(axis=0), pts.max(axis=0)
-            wlo.append(lo)
-            whi.append(hi)
-            lo32 = lo.astype(np.float32)
-            hi32 = hi.astype(np.float32)
+            lo, hi = _corner_box(c - r, c + r, m)
+            lo32, hi32 = lo.astype(np.float32), hi.astype(np.float32)
             lo32 = np.where(lo32.astype(np.float64) > lo, np.nextafter(lo32, np.float32(-np.inf)), lo32)
             hi32 = np.where(hi32.astype(np.float64) < hi, np.nextafter(hi32, np.float32(np.inf)), hi32)
-            tris.append(np.concatenate([lo32, hi32, lo32]).reshape(1, 9).astype(np.float32))
-            normals.append(np.zeros((1, 3)))
-            local_rows.append(np.zeros((1, 9)))
-            inst_idx = len(desc.instances) + k
-            t_inst.append(np.array([inst_idx], np.int32))
-            t_prim.append(np.zeros(1, np.int32))
-            t_mask.append(np.array([sph.mask], np.uint32))
-            mi = mat_index[sph.material]
-            inst_material.append(mi)
-            t_mat.append(np.array([mi], np.int32))
-            inverses.append(inv)
-            sph_rows.append(np.concatenate([inv.reshape(12), c, [r]]))
+            row = np.concatenate([inv.reshape(12), c, [r]])
+            cs = customs[k]
+            cs.box[:] = [float(x) for x in np.concatenate([lo32, hi32, lo32])]
+            cs.material = mat_index[sph.material]
+            cs.mask = int(sph.mask)
+            cs.row[:] = [float(x) for x in row]
+            sph_rows.append(row)
+            sph_boxes.append((lo, hi, inv))
+
+    # instances (Instance + Tlas frames, accel.py:339-346, 451-472)
+    n_inst = len(desc.instances)
+    srcs = (_native.InstanceSrc * max(n_inst, 1))()
+    inst_material, inst_list, inverses = [], [], []
+    wlo, whi = [], []
+    for i, decl in enumerate(desc.instances):
+        dm = dmeshes[decl.mesh]
+        m = frame_to_matrix(decl.frame)
+        try:
+            inv = invert_affine(m)
+        except ValueError as exc:
+            raise BuildError(f"instance {i} frame is not invertible") from exc
+        inverses.append(inv)
+        inst_list.append((decl, m))
+        lo, hi = _corner_box(dm.bounds[:3], dm.bounds[3:], m)
+        wlo.append(lo)
+        whi.append(hi)
+        mi = mat_index[decl.material]
+        inst_material.append(mi)
+        src = srcs[i]
+        src.mesh = mesh_names.index(decl.mesh)
+        src.material = mi
+        src.mask = int(decl.mask)
+        src.matrix[:] = [float(x) for x in m.reshape(12)]
+        src.inverse[:] = [float(x) for x in inv.reshape(12)]
+    for k, sph in enumerate(desc.spheres or ()):
+        lo, hi, inv = sph_boxes[k]
+        wlo.append(lo)
+        whi.append(hi)
+        inverses.append(inv)
+        inst_material.append(mat_index[sph.material])
     root_lo = np.min(np.array(wlo), axis=0)
     root_hi = np.max(np.array(whi), axis=0)
-    ctx = _native.Context.get(device)
-    tlas = GpuTlas(ctx, np.concatenate(tris), np.concatenate(normals), np.concatenate(t_inst),
-                   np.concatenate(t_prim), np.concatenate(t_mask), np.concatenate(t_mat), mat_color, mat_emissive,
-                   bits=QUALITIES[quality], root_lo=root_lo, root_hi=root_hi,
-                   instances=len(desc.instances) + len(desc.spheres), inverses=np.array(inverses),
-                   spheres=np.array(sph_rows) if sph_rows else None)
-    inv12 = np.ascontiguousarray(np.array(inverses, np.float64).reshape(-1, 12))
-    check(lib().rt_scene_set_local_frames(ctx.handle, tlas.handle, inv12.shape[0], ptr(inv12),
-                                          ptr(np.ascontiguousarray(np.concatenate(local_rows), np.float64))))
+
+    handles = (ctypes.c_void_p * max(len(mesh_names), 1))(*[dmeshes[nm].handle.value for nm in mesh_names])
+    mc = np.ascontiguousarray(mat_color, np.float32).reshape(-1, 3)
+    me = np.ascontiguousarray(mat_emissive, np.float32).reshape(-1, 3)
+    h = ctypes.c_void_p()
+    check(lib().rt_scene_compile(ctx.handle, len(mesh_names), handles, n_inst, srcs, n_sph, customs, ptr(mc), ptr(me),
+                                 mc.shape[0], ctypes.byref(h)))
+    n = sum(dmeshes[d.mesh].nf for d in desc.instances) + n_sph
+    tlas = GpuTlas(ctx, h, n, QUALITIES[quality], np.array(sph_rows) if sph_rows else None,
+                   n_instances=n_inst + n_sph, inverses=np.array(inverses))
     registry = IntersectorRegistry()
     if desc.spheres:
         registry.register(SPHERE_GEOM_TYPE, 0, sphere_intersector,
@@ -428,10 +422,18 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
                sky=np.ascontiguousarray(desc.sky, np.float64), background=np.ascontiguousarray(desc.background,
                                                                                                np.float64),
                root_box=(root_lo, root_hi))
-    sc._meshes = {name: _MeshRefit(mesh_cache[name][0].shape[0], mesh_cache[name][1], inst)
-                  for name, inst in mesh_inst.items()}
+    used = {d.mesh for d in desc.instances}
+    sc._meshes = {name: dm for name, dm in dmeshes.items() if name in used}
     sc._light_src = (desc, mat_index, inst_list)
     return sc
+
+
+def _corner_box(lo, hi, m):
+    """World AABB of the 8 corners of a local box under a 3x4 matrix (accel.py:459-469)."""
+    corners = np.array([[(lo, hi)[s & 1][0], (lo, hi)[(s >> 1) & 1][1], (lo, hi)[(s >> 2) & 1][2]]
+                        for s in range(8)])
+    pts = corners @ m[:, :3].T + m[:, 3]
+    return pts.min(axis=0), pts.max(axis=0)
 
 
 def _compile_two_level(desc, quality, device):

@@ -9,7 +9,6 @@ import pytest
 
 from paper_2603_00292_b200 import scenes
 from paper_2603_00292_b200.frames import SrtFrame, frame_to_matrix, invert_affine
-from paper_2603_00292_b200.scene import _local_normals, _world_normals
 from paper_2603_00292_b200.scene_io import AccumBuffer, ParseError, parse_obj, parse_scene, ppm_bytes, resolve
 from rt_helpers import golden
 
@@ -88,18 +87,19 @@ def test_parse_errors():
     assert m.faces.tolist() == [[0, 1, 2], [0, 2, 3], [3, 2, 1]]
 
 
-def test_reference_style_world_normals_bit_exact(cornell_oracle):
-    """the host normal equals the reference's closest-hit normal in float64."""
+def test_reference_style_world_normals_bit_exact(oracle_mod):
+    """the checker of rt_scene_compile (oracle.flat_world, compile_scene's numpy
+    assembly) gives the reference's closest-hit normal in float64, bit for bit."""
     g = golden("cornell_hits")
-    desc = scenes.cornell_description()
-    per_inst = []
-    for i, decl in enumerate(desc.instances):
-        mesh = desc.meshes[decl.mesh]
-        inv = invert_affine(frame_to_matrix(decl.frame))
-        per_inst.append(_world_normals(inv, *_local_normals(mesh.vertices, mesh.faces)))
+    flat = oracle_mod.flat_world(scenes.cornell_description())
+    first = {}
+    for k, i in enumerate(flat["tri_inst"]):
+        first.setdefault(int(i), k)
     hit = g["inst"] >= 0
     for inst, prim, n in zip(g["inst"][hit], g["prim"][hit], g["n"][hit]):
-        assert np.array_equal(per_inst[inst][prim], n)
+        k = first[int(inst)] + int(prim)
+        assert flat["tri_prim"][k] == prim
+        assert np.array_equal(flat["normals64"][k].view(np.uint64), n.view(np.uint64))
 
 
 def test_synthetic_meshes():
