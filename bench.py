@@ -61,14 +61,33 @@ def load_traffic(key, per=1.0):
         return None
 
 
+def load_ncu(key):
+    """The whole record of one kernel set in the committed capture (issue-slot utilisation,
+    warp instructions per launch, active threads per instruction, achieved occupancy); {}
+    if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)[key]
+    except Exception:
+        return {}
+
+
 def load_issue(key):
     """SM issue-slot utilisation (%) of the same capture (the ceiling that binds the
     L1-resident, issue-bound traversal); None if absent."""
+    return load_ncu(key).get("issue_active_pct")
+
+
+def issue_peak(sm_mhz=None):
+    """Warp-instruction issue peak of the GPU (148 SMs x 4 schedulers x 1 inst/cycle) in
+    G warp-inst/s at the maximum SM clock (MEASURED_PEAKS.json sm_max_mhz, else 1965 MHz)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f)[key].get("issue_active_pct")
+        with open(PEAKS_PATH) as f:
+            mhz = float(json.load(f).get("sm_max_mhz") or 1965.0)
+        src = "148 SMs x 4 schedulers x 1 warp-inst/cycle at MEASURED_PEAKS.json sm_max_mhz"
     except Exception:
-        return None
+        mhz, src = 1965.0, "148 SMs x 4 schedulers x 1 warp-inst/cycle at 1965 MHz (B200 max SM clock)"
+    return 148 * 4 * mhz * 1e6 / 1e9, src
 
 
 def load_peaks():
@@ -256,6 +275,7 @@ def run_ours(args, ws, rank, local):
             "strong"
     with_build = C in (2, 4)
     kernel = args.kernel
+    comm = distributed.NcclComm.get(tl.ctx) if ws > 1 else None
 
     # rays of one step (all ranks), counted once outside the timed region
     accum.zero_()
@@ -276,6 +296,23 @@ def run_ours(args, ws, rank, local):
     hit_frac = float((hits[:, 1].view(torch.int32) >= 0).double().mean())
     del hits, st
     stages = tl.build_profiled(30)
+    build63_ms = None
+    if with_build:
+        # 63-bit LBVH build time (BASELINE config 2 asks for both widths): per-build events,
+        # L2 flushed before each build like the timed steps
+        for _ in range(3):
+            tl.build(63)
+        e63 = []
+        for _ in range(20):
+            flush.fill_(3)
+            a, b = ev(), ev()
+            a.record()
+            tl.build(63)
+            b.record()
+            e63.append((a, b))
+        torch.cuda.synchronize()
+        build63_ms = float(np.mean([a.elapsed_time(b) for a, b in e63]))
+        tl.build(30)
 
     def step(e=None):
         if e:
@@ -289,7 +326,12 @@ def run_ours(args, ws, rank, local):
         if e:
             e[2].record()
         if ws > 1:
-            dist.reduce(accum, 0)
+            # the split's one exchange over librt_b200's NCCL data plane (csrc/multi.cu):
+            # tile split -> band gather into rank 0; sample split -> one reduce
+            if bands is not None:
+                comm.gather_bands(accum, W, H)
+            else:
+                comm.reduce(accum)
         if e:
             e[3].record()
 
@@ -324,39 +366,71 @@ def run_ours(args, ws, rank, local):
     value = rays_step * K / (t_total * 1e-3) / 1e6
 
     # -- end to end through the public API with host buffers ---------------------
-    e2e = e2e_query = None
+    e2e = e2e_query = e2e_refit = None
     if not args.no_e2e:
         if C in (2, 4):
+            import dataclasses
             from paper_2603_00292_b200 import render_frame
             from paper_2603_00292_b200._native import host_pinned_copy
-            host_tris = host_pinned_copy(tl.tris)           # world rows, for the query path below
-            # the step's vertices in pinned host memory: the synthetic meshes are fp32 values
-            # (SURVEY 8(d)), so their fp32 array is exact and refit_mesh widens it on the device
-            mesh_v = desc.meshes["mesh"].vertices
-            host_v = host_pinned_copy(np.ascontiguousarray(mesh_v, np.float32))
-            assert np.array_equal(host_v.astype(np.float64), mesh_v)
-            # (1) the reference arm's own path: refit(mesh vertices) + render_frame('eye') -> host
-            #     float64 AccumBuffer (H2D: the vertices; D2H: the (H, W, 4) float64 sums)
-            for _ in range(3):      # warm-up: device mesh, pinned readback blocks cached
-                sc.refit_mesh("mesh", host_v, bits=30)
-                render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
-            ke = max(3, min(K, 30))       # ~2 ms each at config 2: enough to average out host hiccups
+            from paper_2603_00292_b200.scene_io import TriangleMesh
+            mesh = desc.meshes["mesh"]
+            # the reference's own inputs in pinned host memory: float64 vertices, int64 faces
+            pinned_mesh = TriangleMesh(host_pinned_copy(np.ascontiguousarray(mesh.vertices, np.float64)),
+                                       host_pinned_copy(np.ascontiguousarray(mesh.faces, np.int64)))
+            pdesc = dataclasses.replace(desc, meshes={"mesh": pinned_mesh})
+            # (1) the reference arm's call sequence: compile_scene(desc) + render_frame('eye') ->
+            #     host float64 AccumBuffer (H2D: vertices + faces; D2H: the (H, W, 4) float64 sums)
+            def e2e_step():
+                s2 = compile_scene(pdesc, "lbvh30", device=local)
+                if bands is not None and ws > 1:     # tile split: rank 0 receives the frame
+                    distributed.render_frame_distributed(s2, W, H, 1, "eye", seed=0, kernel=kernel, mode="tiles")
+                else:
+                    render_frame(s2, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
+
+            for _ in range(3):      # warm-up: memory pool, pinned readback blocks cached
+                e2e_step()
+            ke = max(3, min(K, 20 if C == 2 else 5))
             gc.collect()
             if ws > 1:
                 dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             for _ in range(ke):
+                e2e_step()
+            torch.cuda.synchronize()
+            te = time.perf_counter() - t0
+            h2d = int(pinned_mesh.vertices.nbytes + pinned_mesh.faces.nbytes)
+            d2h = int(npix * 32)
+            path = ("compile_scene(desc with float64 vertices + int64 faces in pinned host memory, 'lbvh30': device "
+                    "validation, flatten, LBVH build) + render_frame('eye') -> host float64 AccumBuffer (H, W, 4): "
+                    "the reference arm's own call sequence")
+            rays_e2e = my_rays
+            # (2) refit path: Scene.refit_mesh(host vertices) (Blas.refit semantics) + render_frame
+            host_v = host_pinned_copy(np.ascontiguousarray(mesh.vertices, np.float32))
+            assert np.array_equal(host_v.astype(np.float64), mesh.vertices)
+            for _ in range(3):
+                sc.refit_mesh("mesh", host_v, bits=30)
+                render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
+            kr = max(3, min(K, 30))
+            gc.collect()
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(kr):
                 sc.refit_mesh("mesh", host_v, bits=30)
                 render_frame(sc, W, H, 1, "eye", seed=0, kernel=kernel, samples=samples, bands=bands)
             torch.cuda.synchronize()
-            te = time.perf_counter() - t0
-            h2d, d2h = int(host_v.nbytes), int(npix * 32)
-            path = ("Scene.refit_mesh(host mesh vertices, Blas.refit semantics: H2D + device world rows/normals + "
-                    "LBVH rebuild) + render_frame('eye') -> host float64 AccumBuffer (H, W, 4); the reference arm "
-                    "times compile + the same render call")
-            rays_e2e = my_rays
-            # (2) the query API: refit + closest_hit_batch(host float64 rays) of this rank's rays
+            tr = torch.tensor([time.perf_counter() - t0, float(my_rays)], dtype=torch.float64, device=dev)
+            if ws > 1:
+                dist.all_reduce(tr[:1], op=dist.ReduceOp.MAX)
+                dist.all_reduce(tr[1:], op=dist.ReduceOp.SUM)
+            e2e_refit = {"value": float(tr[1]) * kr / float(tr[0]) / 1e6, "unit": "Mrays/s",
+                         "h2d_bytes_per_step": int(host_v.nbytes), "d2h_bytes_per_step": int(npix * 32), "steps": kr,
+                         "path": ("Scene.refit_mesh(host fp32 mesh vertices: H2D + device world rows/normals + LBVH "
+                                  "rebuild) + render_frame('eye') -> host float64 AccumBuffer (H, W, 4)")}
+            # (3) the query API: refit + closest_hit_batch(host float64 rays) of this rank's rays
+            host_tris = host_pinned_copy(tl.tris)
             r = prim.cpu().numpy().astype(np.float64)
             if bands is not None:
                 rows = np.array(distributed.band_rows(H, rank, ws))
@@ -425,6 +499,11 @@ def run_ours(args, ws, rank, local):
             torch.cuda.synchronize()
             ms = a.elapsed_time(b)
             pt[kern] = {"ms": ms, "mrays_s": exact / (ms * 1e-3) / 1e6}
+        if not args.no_cpu:
+            # the reference's path tracing (its C restatement) on the host cores, 1 spp prefix of the same frame
+            cores = os.cpu_count() or 1
+            v, sample, _ = cpu_sample(3, scene_desc(3), cores)
+            pt["cpu_baseline"] = {"value": v, "unit": "Mrays/s", "cores": cores, "kind": "port", "sample": sample}
 
     # -- CPU baseline (rank 0, N = 1): the oracle port on the host cores --------
     cpu = None
@@ -442,19 +521,35 @@ def run_ours(args, ws, rank, local):
     traffic_key = {2: ("config2_trace", 1.0), 3: ("config3_trace_1spp", samples[1] - samples[0]),
                    5: ("config3_trace_1spp", samples[1] - samples[0]), 4: ("config4_trace", 1.0)}[C]
     trace_traffic = load_traffic(traffic_key[0], traffic_key[1]) if traffic_key[1] else None
-    roof_trace = {"kernel": "pt_megakernel (raygen + persistent 4-wide BVH walk + shade, fused)", "bound": "hbm",
-                  "achieved": bpr * rays_rank0 / (render_ms * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
+    # The traversal megakernel is latency / issue bound, not bandwidth bound (ncu: DRAM 1-2 % of
+    # peak, L1 hit rate > 80 %): its roofline is the SM instruction-issue peak.
+    # achieved = warp instructions per launch (ncu, same kernel and workload: the count is a
+    # property of the rays and the BVH) / the live launch time measured here.
+    nc = load_ncu(traffic_key[0])
+    ipeak, ipeak_src = issue_peak()
+    winst = nc.get("warp_inst")
+    hbm_ach = bpr * rays_rank0 / (render_ms * 1e-3) / 1e9
+    roof_trace = {"kernel": "pt_megakernel (raygen + persistent 4-wide BVH walk + shade, fused)", "bound": "issue",
+                  "achieved": (winst * traffic_key[1] / (render_ms * 1e-3) / 1e9) if winst else None,
+                  "peak": ipeak, "unit": "G warp-inst/s", "peak_source": ipeak_src,
+                  "achieved_source": (f"{winst:.4g} warp instructions per launch (ncu inst_executed, "
+                                      f"profiles/ncu_traffic.json[{traffic_key[0]!r}] x {traffic_key[1]}) / live "
+                                      f"launch time {render_ms:.4f} ms") if winst else "no ncu capture",
+                  "simt_threads_per_inst": nc.get("threads_per_inst"),
+                  "achieved_occupancy_pct": nc.get("achieved_occupancy_pct"),
+                  "sm_issue_active_pct_ncu": nc.get("issue_active_pct"),
                   "traffic": trace_traffic, "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch, "
                                                               "cold caches)",
-                  "bytes_per_ray": bpr, "peak_source": peak_src,
-                  "bytes_formula": f"128 B x {n_nodes:.2f} BVH4 node fetches (4 child boxes + ids) + 48 B x {n_tests:.2f} triangle "
-                                   f"tests + 32 B accumulation RMW per ray (node/test counts: stats build of the "
-                                   f"trace kernel on this rank's primary rays{'' if C in (2, 4) else '; bounce rays assumed alike'})",
-                  "note": "node/triangle fetches mostly hit L1/L2 (ncu: DRAM 1-2% of peak); the bound that "
-                          "binds is SM issue/latency, see profiles/",
-                  "sm_issue_active_pct": load_issue(traffic_key[0]),
-                  "sm_issue_source": "smsp__issue_active.avg.pct_of_peak_sustained_active of the same ncu capture"}
-    roof_trace["frac"] = roof_trace["achieved"] / peak_gbs
+                  "hbm_algorithmic": {"achieved": hbm_ach, "peak": peak_gbs, "unit": "GB/s", "frac": hbm_ach / peak_gbs,
+                                      "bytes_per_ray": bpr, "peak_source": peak_src,
+                                      "bytes_formula": f"128 B x {n_nodes:.2f} BVH4 node fetches (4 child boxes + ids) "
+                                                       f"+ 48 B x {n_tests:.2f} triangle tests + 32 B accumulation RMW "
+                                                       f"per ray (node/test counts: stats build of the trace kernel "
+                                                       f"on this rank's primary rays"
+                                                       f"{'' if C in (2, 4) else '; bounce rays assumed alike'})",
+                                      "note": "served mostly by L1/L2, so this is a walk-speed figure, not a "
+                                              "bandwidth ceiling"}}
+    roof_trace["frac"] = roof_trace["achieved"] / ipeak if winst else None
     line_extra = {}
     dominant = roof_trace
     if with_build:
@@ -467,14 +562,17 @@ def run_ours(args, ws, rank, local):
                                         "with cold caches)",
                       "bytes_formula": f"328 B/tri x {tl.n} tris (SURVEY 8(d), 30-bit keys)",
                       "stage_ms": stages, "peak_source": peak_src,
-                      "sm_issue_active_pct": load_issue("config2_build" if C == 2 else "config4_build")}
+                      "sm_issue_active_pct": load_issue("config2_build" if C == 2 else "config4_build"),
+                      "achieved_occupancy_pct": load_ncu("config2_build" if C == 2 else "config4_build").get(
+                          "achieved_occupancy_pct"),
+                      "note": "latency-bound (emit climb chains, look-back); HBM is the bound it is measured against"}
         roof_build["frac"] = roof_build["achieved"] / peak_gbs
         if t_build > t_render:
             dominant, other = roof_build, roof_trace
         else:
             other = roof_build
-        line_extra = {"lbvh_build_ms": build_ms, "trace_mrays_s": rays_step * K / (t_render * 1e-3) / 1e6,
-                      "roofline_other": other}
+        line_extra = {"lbvh_build_ms": build_ms, "lbvh63_build_ms": build63_ms,
+                      "trace_mrays_s": rays_step * K / (t_render * 1e-3) / 1e6, "roofline_other": other}
         launches = 8 + 1      # the bench builds with 30-bit keys
         detail = "per step: 8 LBVH kernels (bounds, Morton + digit histograms, 4 onesweep passes, emit+refit, " \
                  "global emit climb) + 1 megakernel (plus one memset)"
@@ -487,12 +585,14 @@ def run_ours(args, ws, rank, local):
         "ms_per_step": t_total / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (meshes generated in-process / built-in cornell.scn; no dataset)",
         "config": {"workload": WORKLOADS[C], "triangles": tl.n, "rays_per_step": rays_step,
-                   "kernel": kernel, "parallelism": (f"{'sample' if bands is None else 'tile-band'} split x{ws}"
-                                                     f" + NCCL reduce") if ws > 1 else "1 GPU",
+                   "kernel": kernel, "parallelism": (f"{'sample' if bands is None else 'tile-band'} split x{ws} + "
+                                                     f"{'NCCL reduce' if bands is None else 'NCCL band gather'} "
+                                                     f"(librt_b200 rt_comm)") if ws > 1 else "1 GPU",
                    "l2": "256 MiB buffer written between timed steps (flush)", "primary_hit_fraction": hit_frac},
         **line_extra, "reduce_ms": t_reduce / K, "roofline": dominant,
         "per_ray": {"bvh4_node_fetches": n_nodes, "triangle_tests": n_tests},
         "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks.summary(),
+        **({"e2e_refit": e2e_refit} if e2e_refit else {}),
         **({"e2e_query": e2e_query} if e2e_query else {}),
         "gpu_launches": K * launches, "gpu_launches_detail": detail, "pt": pt,
     }
@@ -506,7 +606,9 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", type=int, choices=(2, 3, 4, 5), default=2)
+    # default: config 2 (configs[1]) on one GPU; BASELINE's multi-GPU config 4 (10M soup,
+    # 4K primaries, tile split, strong scaling) when launched on N > 1 GPUs
+    ap.add_argument("--config", type=int, choices=(2, 3, 4, 5), default=None)
     ap.add_argument("--kernel", choices=("mega", "wavefront"), default="mega")
     ap.add_argument("--soup-n", type=int, default=10_000_000)
     ap.add_argument("--pt-spp", type=int, default=64)
@@ -515,6 +617,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.config is None:
+        args.config = 4 if int(os.environ.get("WORLD_SIZE", "1")) > 1 else 2
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # communicator lines (ranks, channels, NVLS / P2P transports) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if args.steps is None:
         args.steps = 3 if args.impl == "reference" else {2: 400, 3: 10, 4: 60, 5: 3}[args.config]
     if args.impl == "reference":

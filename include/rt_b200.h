@@ -169,6 +169,9 @@ int rt_scene_compile(rt_ctx* ctx, int32_t n_meshes, rt_mesh* const* meshes, int3
 /* the scene's per-primitive ids, device -> host (any pointer may be NULL; synchronises) */
 int rt_scene_get_ids(rt_ctx* ctx, rt_scene* scene, int32_t* tri_inst, int32_t* tri_prim, uint32_t* tri_mask,
                      int32_t* tri_material);
+/* a render replica of a built scene on dst's device (multi-GPU render_frame): geometry,
+ * shading tables and the built LBVH copied device to device (no host-query extras) */
+int rt_scene_clone(rt_ctx* src, rt_scene* scene, rt_ctx* dst, rt_scene** out);
 /* the scene's geometry, device -> host (parity checks; any pointer may be NULL): (n, 9) fp32
  * rows, (n, 3) fp32 shading normals, (n, 3) float64 world normals, (n, 9) float64 local rows */
 int rt_scene_get_geometry(rt_ctx* ctx, rt_scene* scene, float* tris9, float* normals3, double* normals64,
@@ -247,14 +250,34 @@ int rt_resolve(rt_ctx* ctx, const float* accum, int64_t npix, int32_t gamma, uin
  * Each device g has its own context, scene replica (identical deterministic LBVH) and
  * ZERO-initialised (H*W, 4) fp32 accumulation buffer accums[g].  split RT_SPLIT_SAMPLES:
  * device g renders global samples [s0 + g*S/n, s0 + (g+1)*S/n) (the same random numbers as
- * one GPU); RT_SPLIT_TILES: device g renders the 4-row tile bands r % n == g.  All renders
- * run concurrently, then ONE grouped ncclReduce(sum, fp32) leaves the frame in accums[0]
- * (NCCL is dlopen'ed: the process's libnccl.so.2).  rays_out (nullable): all devices'
- * closest-hit queries.  Replaces render_frame's worker split (integrators.py:426-473). */
+ * one GPU), then ONE grouped ncclReduce(sum, fp32) leaves the frame in accums[0];
+ * RT_SPLIT_TILES: device g renders the 4-row tile bands r % n == g, and only those rows go
+ * to device 0 (packed, ncclSend / ncclRecv, unpacked: the band gather below).  NCCL is
+ * dlopen'ed (the process's libnccl.so.2).  rays_out (nullable): all devices' closest-hit
+ * queries.  Replaces render_frame's worker split (integrators.py:426-473). */
 #define RT_SPLIT_SAMPLES 0
 #define RT_SPLIT_TILES 1
 int rt_multi_render(int32_t n_gpus, rt_ctx* const* ctxs, rt_scene* const* scenes, const rt_render_params* p,
                     float* const* accums, int32_t split, uint64_t* rays_out);
+/* ---- multi-GPU, one process per GPU (torch.distributed launches) --------
+ * The same exchange as rt_multi_render, one rank per call: rank 0 makes a unique id
+ * (rt_comm_unique_id), the launcher shares its RT_COMM_ID_BYTES bytes, every rank calls
+ * rt_comm_create on its context's device.  Per frame, on the context stream:
+ *   rt_comm_gather_bands  tile split: every rank's 4-row bands r % nranks == rank of its
+ *                         (H*W, 4) fp32 accum go to rank 0's accum (rank 0's own bands are
+ *                         already there); a collective: all ranks call it;
+ *   rt_comm_reduce_accum  sample split: reduce(sum) of accum into rank 0's. */
+typedef struct rt_comm rt_comm;
+#define RT_COMM_ID_BYTES 128
+int rt_comm_unique_id(uint8_t* id);
+int rt_comm_create(rt_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t* id, rt_comm** out);
+void rt_comm_destroy(rt_comm* comm);
+int rt_comm_gather_bands(rt_comm* comm, rt_ctx* ctx, float* accum, int32_t width, int32_t height);
+int rt_comm_reduce_accum(rt_comm* comm, rt_ctx* ctx, float* accum, int64_t npix);
+/* the band gather's pack (unpack = 0: compact <- rank g's rows of accum) / unpack (accum
+ * rows <- compact) on one device, without NCCL (tests); rows_out: rank g's row count */
+int rt_bands_copy(rt_ctx* ctx, float* accum, float* compact, int32_t width, int32_t height, int32_t g, int32_t G,
+                  int32_t unpack, int64_t* rows_out);
 /* primary rays of sample s for every pixel of the frame (parity tests): (W*H, 8) like rt_trace_closest */
 int rt_raygen(rt_ctx* ctx, const rt_render_params* p, int32_t sample, float* rays);
 

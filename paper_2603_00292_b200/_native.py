@@ -131,6 +131,12 @@ def lib():
             "rt_scene_compile": [vp, i32, vp, i32, vp, i32, vp, vp, vp, i32, vp],
             "rt_scene_get_ids": [vp, vp, vp, vp, vp, vp],
             "rt_scene_get_geometry": [vp, vp, vp, vp, vp, vp],
+            "rt_scene_clone": [vp, vp, vp, vp],
+            "rt_comm_unique_id": [vp],
+            "rt_comm_create": [vp, i32, i32, vp, vp],
+            "rt_comm_gather_bands": [vp, vp, vp, i32, i32],
+            "rt_comm_reduce_accum": [vp, vp, vp, i64],
+            "rt_bands_copy": [vp, vp, vp, i32, i32, i32, i32, i32, vp],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -144,6 +150,8 @@ def lib():
         L.rt_tlas_destroy.restype = None
         L.rt_mesh_destroy.argtypes = [vp]
         L.rt_mesh_destroy.restype = None
+        L.rt_comm_destroy.argtypes = [vp]
+        L.rt_comm_destroy.restype = None
         _lib = L
         return L
 

@@ -66,12 +66,20 @@ int rt_ctx_create(int device, rt_ctx** out) {
     }
     rt_ctx* c = new rt_ctx();
     memset(c, 0, sizeof *c);
+    c->mu = new std::recursive_mutex();
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     RT_CUDA_TRY(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     RT_CUDA_TRY(cudaEventCreate(&c->ev0));
     RT_CUDA_TRY(cudaEventCreate(&c->ev1));
+    {
+        // keep freed pool blocks cached (scene storage is stream-ordered pool memory)
+        cudaMemPool_t pool;
+        RT_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        RT_CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    }
     RT_CUDA_TRY(cudaMalloc(&c->d_counter, 64 * sizeof(unsigned int)));
     RT_CUDA_TRY(cudaMalloc(&c->d_error, sizeof(int)));
     RT_CUDA_TRY(cudaMemset(c->d_error, 0, sizeof(int)));
@@ -98,6 +106,7 @@ void rt_ctx_destroy(rt_ctx* c) {
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
     cudaStreamDestroy(c->own_stream);
+    delete c->mu;
     delete c;
 }
 
@@ -108,6 +117,7 @@ int rt_ctx_set_stream(rt_ctx* c, void* stream) {
 }
 
 int rt_ctx_sync(rt_ctx* c) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c, "ctx is NULL");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -116,6 +126,7 @@ int rt_ctx_sync(rt_ctx* c) {
 
 // device allocations of a scene of n primitives and n_mat materials (contents unset)
 int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && out, "ctx/out is NULL");
     RT_CHECK_ARG(n >= 1, "cannot build over zero primitives");
     RT_CHECK_ARG(n < (1ll << 30), "at most 2^30 - 1 triangles per scene");
@@ -125,10 +136,12 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
     memset(s, 0, sizeof *s);
     s->n = n;
     s->n_mat = n_mat;
+    s->device = c->device;
+    s->stream = c->stream;
     const int64_t ni = n > 1 ? n - 1 : 1;
 #define ALLOC(ptr, bytes)                                                       \
     do {                                                                        \
-        cudaError_t _e = cudaMalloc((void**)&(ptr), (bytes));                   \
+        cudaError_t _e = rt_alloc((void**)&(ptr), (bytes), c->stream, false);   \
         if (_e != cudaSuccess) {                                                \
             rt_set_error("cudaMalloc(%zu) failed: %s", (size_t)(bytes), cudaGetErrorString(_e)); \
             rt_scene_destroy(s);                                                \
@@ -158,11 +171,20 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
     ALLOC(s->emit_items, 48 * (2 * n + 512));      // EmitNode segments of EMIT_T per emit block
     ALLOC(s->seg_count, sizeof(unsigned int) * (n / 64 + 2));   // one count per emit block (EMIT_T >= 64)
 #undef ALLOC
+    {
+        cudaError_t _e = cudaStreamSynchronize(c->stream);   // the blocks are usable from any stream now
+        if (_e != cudaSuccess) {
+            rt_set_error("allocation failed: %s", cudaGetErrorString(_e));
+            rt_scene_destroy(s);
+            return RT_ENOMEM;
+        }
+    }
     *out = s;
     return RT_OK;
 }
 
 int rt_scene_set_materials(rt_ctx* c, rt_scene* s, const float* mat_color, const float* mat_emissive) {
+    RT_CTX_LOCK(c);
     RT_CUDA_TRY(cudaSetDevice(c->device));      // the scene's buffers live on the context's device
     std::vector<float4> mc(s->n_mat), me(s->n_mat);
     for (int k = 0; k < s->n_mat; ++k) {
@@ -177,6 +199,7 @@ int rt_scene_set_materials(rt_ctx* c, rt_scene* s, const float* mat_color, const
 int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normals, const int32_t* tri_inst,
                     const int32_t* tri_prim, const uint32_t* tri_mask, const int32_t* tri_material,
                     const float* mat_color, const float* mat_emissive, int32_t n_mat, rt_scene** out) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && out, "ctx/out is NULL");
     RT_CHECK_ARG(n >= 1, "cannot build over zero primitives");
     RT_CHECK_ARG(tris && normals && tri_inst && tri_prim && tri_mask && tri_material, "NULL triangle array");
@@ -218,10 +241,73 @@ int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normal
 }
 
 int rt_scene_set_vertices(rt_ctx* c, rt_scene* s, const float* tris) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && tris, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     RT_CUDA_TRY(cudaMemcpyAsync(s->tris, tris, sizeof(float) * 9 * s->n, cudaMemcpyHostToDevice, c->stream));
     s->built = 0;
+    return RT_OK;
+}
+
+// A render replica of a built scene on another context's device (multi-GPU render_frame):
+// the resident geometry, shading tables and the built LBVH are copied device to device
+// (cudaMemcpyPeer; staged through the host when the devices have no peer access), the
+// build scratch is fresh.  The host-query extras (float64 normals / local rows) are not
+// copied: a replica renders.
+int rt_scene_clone(rt_ctx* src, rt_scene* s, rt_ctx* dst, rt_scene** out) {
+    RT_CHECK_ARG(src && s && dst && out, "NULL argument");
+    if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    std::unique_lock<std::recursive_mutex> l1(*src->mu, std::defer_lock), l2(*dst->mu, std::defer_lock);
+    if (src == dst) l1.lock();
+    else if (src < dst) { l1.lock(); l2.lock(); }
+    else { l2.lock(); l1.lock(); }
+    RT_CUDA_TRY(cudaSetDevice(src->device));
+    RT_CUDA_TRY(cudaStreamSynchronize(src->stream));
+    rt_scene* d = nullptr;
+    int rc = rt_scene_alloc(dst, s->n, s->n_mat, &d);
+    if (rc) return rc;
+    const int64_t n = s->n, ni = n > 1 ? n - 1 : 1;
+    cudaStream_t st = dst->stream;
+    auto cp = [&](void* to, const void* from, size_t bytes) -> cudaError_t {
+        return cudaMemcpyPeerAsync(to, dst->device, from, src->device, bytes, st);
+    };
+    cudaError_t e = cudaSuccess;
+    if (!e) e = cp(d->tris, s->tris, sizeof(float) * 9 * n);
+    if (!e) e = cp(d->tri_attr, s->tri_attr, sizeof(float4) * n);
+    if (!e) e = cp(d->tri_inst, s->tri_inst, sizeof(int32_t) * n);
+    if (!e) e = cp(d->tri_prim, s->tri_prim, sizeof(int32_t) * n);
+    if (!e) e = cp(d->tri_mask, s->tri_mask, sizeof(uint32_t) * n);
+    if (!e) e = cp(d->mat_color, s->mat_color, sizeof(float4) * s->n_mat);
+    if (!e) e = cp(d->mat_emissive, s->mat_emissive, sizeof(float4) * s->n_mat);
+    if (!e) e = cp(d->nodes, s->nodes, sizeof(float4) * 4);
+    if (!e) e = cp(d->tri_sorted, s->tri_sorted, sizeof(float4) * 3 * n);
+    if (!e) e = cp(d->bvh4, s->bvh4, sizeof(float4) * 8 * ni);
+    if (!e) e = cp(d->child, s->child, sizeof(int2) * ni);
+    if (!e) e = cp(d->vals_a, s->vals_a, sizeof(uint32_t) * n);
+    if (!e) e = cp(d->keys_a, s->keys_a, (s->bits == 63 ? 8 : 4) * (size_t)n);
+    if (!e) e = cp(d->cbounds, s->cbounds, sizeof(float) * 16);
+    if (!e && s->n_lights) {
+        e = rt_alloc((void**)&d->lights, sizeof(float4) * 5 * s->n_lights, st);
+        if (!e) e = cp(d->lights, s->lights, sizeof(float4) * 5 * s->n_lights);
+        d->n_lights = s->n_lights;
+    }
+    if (!e && s->n_spheres) {
+        e = rt_alloc((void**)&d->spheres, sizeof(double) * 16 * s->n_spheres, st);
+        if (!e) e = cp(d->spheres, s->spheres, sizeof(double) * 16 * s->n_spheres);
+        d->n_spheres = s->n_spheres;
+    }
+    if (!e) e = cudaStreamSynchronize(st);
+    if (e) {
+        rt_scene_destroy(d);
+        rt_set_error("rt_scene_clone: %s", cudaGetErrorString(e));
+        return RT_ECUDA;
+    }
+    d->built = s->built;
+    d->bits = s->bits;
+    d->custom = s->custom;
+    d->geom_type = s->geom_type;
+    d->data_offset = s->data_offset;
+    *out = d;
     return RT_OK;
 }
 
@@ -233,12 +319,13 @@ void rt_scene_destroy(rt_scene* s) {
                     s->flags, s->cbounds, s->sort_scratch, s->leaf_box, s->emit_items, s->seg_count, s->lights,
                     s->spheres,
                     s->lnormal64, s->lrows64, s->wnormal64, s->inst_inv64};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
+    cudaSetDevice(s->device);
+    for (void* p : ptrs) rt_free(p, s->stream);
     delete s;
 }
 
 int rt_bvh_build(rt_ctx* c, rt_scene* s, int bits, float* build_ms) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(bits == 30 || bits == 63, "morton_bits must be 30 or 63");
     RT_CUDA_TRY(cudaSetDevice(c->device));
@@ -256,6 +343,7 @@ int rt_bvh_build(rt_ctx* c, rt_scene* s, int bits, float* build_ms) {
 }
 
 int rt_bvh_build_profiled(rt_ctx* c, rt_scene* s, int bits, float* stage_ms) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && stage_ms, "NULL argument");
     RT_CHECK_ARG(bits == 30 || bits == 63, "morton_bits must be 30 or 63");
     RT_CHECK_ARG(s->n > 1, "profiling needs at least two triangles");
@@ -274,6 +362,7 @@ int rt_bvh_build_profiled(rt_ctx* c, rt_scene* s, int bits, float* stage_ms) {
 }
 
 int rt_bvh_info(rt_ctx* c, rt_scene* s, float* root6, int32_t* height, int64_t* n_internal) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
     RT_CUDA_TRY(cudaSetDevice(c->device));
@@ -293,6 +382,7 @@ int rt_bvh_info(rt_ctx* c, rt_scene* s, float* root6, int32_t* height, int64_t* 
 int rt_bvh_download(rt_ctx* c, rt_scene* s, uint64_t* sorted_keys, uint32_t* order, int32_t* child,
                     int32_t* parent, float* boxes, int32_t* heights, float* cbounds, float* inv_ext,
                     uint64_t* morton) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
     RT_CUDA_TRY(cudaSetDevice(c->device));
@@ -388,6 +478,7 @@ int rt_bvh_download(rt_ctx* c, rt_scene* s, uint64_t* sorted_keys, uint32_t* ord
 
 int rt_trace_closest(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, float* hits, uint32_t ray_mask,
                      uint32_t* stats, int32_t flags) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0 && (n == 0 || (rays && hits)), "bad ray/hit buffers");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
@@ -401,6 +492,7 @@ int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, cons
                         const double* tmax, double tmin_s, double tmax_s, uint32_t ray_mask, double* t,
                         int64_t* inst, int64_t* prim, double* u, double* v, double* nrm, int64_t* stats,
                         int32_t flags) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0, "negative ray count");
     RT_CHECK_ARG(n == 0 || (o && d && t && inst && prim && u && v && nrm), "NULL ray or output buffer");
@@ -438,6 +530,7 @@ int rt_closest_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, cons
 
 int rt_trace_any(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, uint8_t* hit, uint32_t ray_mask,
                  int32_t flags) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0 && (n == 0 || (rays && hit)), "bad ray/hit buffers");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
@@ -449,6 +542,7 @@ int rt_trace_any(rt_ctx* c, rt_scene* s, int64_t n, const float* rays, uint8_t* 
 int rt_any_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const double* d, const double* tmin,
                     const double* tmax, double tmin_s, double tmax_s, uint32_t ray_mask, uint8_t* out,
                     int32_t flags) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "ctx/scene is NULL");
     RT_CHECK_ARG(n >= 0, "negative ray count");
     RT_CHECK_ARG(n == 0 || (o && d && out), "NULL ray or output buffer");
@@ -471,9 +565,10 @@ int rt_any_hit_host(rt_ctx* c, rt_scene* s, int64_t n, const double* o, const do
 // world-space emissive triangles for next-event estimation (scene.py:58-76 light rows):
 // rows of 16 floats = v0 (3), v1 (3), v2 (3), unit normal (3), emission (3), area
 int rt_scene_set_lights(rt_ctx* c, rt_scene* s, int32_t n_lights, const float* rows) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && n_lights >= 0 && (n_lights == 0 || rows), "bad light table");
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    if (s->lights) cudaFree(s->lights);
+    rt_free(s->lights, s->stream);
     s->lights = nullptr;
     s->n_lights = n_lights;
     if (n_lights == 0) return RT_OK;
@@ -486,27 +581,29 @@ int rt_scene_set_lights(rt_ctx* c, rt_scene* s, int32_t n_lights, const float* r
         L[5 * k + 3] = make_float4(r[9], r[10], r[11], 0.f);
         L[5 * k + 4] = make_float4(r[12], r[13], r[14], 0.f);
     }
-    RT_CUDA_TRY(cudaMalloc(&s->lights, sizeof(float4) * L.size()));
+    RT_CUDA_TRY(rt_alloc((void**)&s->lights, sizeof(float4) * L.size(), s->stream));
     RT_CUDA_TRY(cudaMemcpy(s->lights, L.data(), sizeof(float4) * L.size(), cudaMemcpyHostToDevice));
     return RT_OK;
 }
 
 int rt_scene_set_spheres(rt_ctx* c, rt_scene* s, int32_t n_spheres, const double* rows) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && n_spheres >= 0 && (n_spheres == 0 || rows), "bad sphere table");
     RT_CHECK_ARG(n_spheres <= s->n, "more spheres than primitives");
     for (int k = 0; k < n_spheres; ++k)
         RT_CHECK_ARG(rows[16 * k + 15] > 0.0, "sphere radius must be > 0");
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    if (s->spheres) cudaFree(s->spheres);
+    rt_free(s->spheres, s->stream);
     s->spheres = nullptr;
     s->n_spheres = n_spheres;
     if (n_spheres == 0) return RT_OK;
-    RT_CUDA_TRY(cudaMalloc(&s->spheres, sizeof(double) * 16 * (size_t)n_spheres));
+    RT_CUDA_TRY(rt_alloc((void**)&s->spheres, sizeof(double) * 16 * (size_t)n_spheres, s->stream));
     RT_CUDA_TRY(cudaMemcpy(s->spheres, rows, sizeof(double) * 16 * (size_t)n_spheres, cudaMemcpyHostToDevice));
     return RT_OK;
 }
 
 int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && p && accum, "NULL argument");
     RT_CHECK_ARG(p->width >= 1 && p->height >= 1 && p->s1 > p->s0 && p->s0 >= 0,
                  "width, height, and spp must all be >= 1");
@@ -528,6 +625,7 @@ int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, u
 }
 
 int rt_resolve(rt_ctx* c, const float* accum, int64_t npix, int32_t gamma, uint8_t* rgb) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && accum && rgb && npix >= 0, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     int rc = rt_resolve_impl(c, accum, npix, gamma, rgb);
@@ -545,6 +643,7 @@ int rt_resolve(rt_ctx* c, const float* accum, int64_t npix, int32_t gamma, uint8
 }
 
 int rt_raygen(rt_ctx* c, const rt_render_params* p, int32_t sample, float* rays) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && p && rays, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     return rt_raygen_impl(c, p, sample, rays);

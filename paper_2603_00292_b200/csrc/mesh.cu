@@ -17,6 +17,7 @@
 #include "rt_common.cuh"
 struct rt_mesh {
     int device;
+    cudaStream_t stream;  // storage: stream-ordered pool memory freed on this stream
     int64_t nv, nf;
     int32_t n_inst;
     int32_t local;        // RT_MESH_LOCAL: rows = the local vertices, float64 local normals
@@ -27,6 +28,8 @@ struct rt_mesh {
     int4* meta;           // (n_inst) device, compiled scenes: (instance id, material, mask, 0) per placement
     int64_t bounds_nv;    // rt_mesh_upload: vertices referenced by faces have float64 bounds `bounds`
     double bounds[6];
+    unsigned long long* d_red;  // (8) device: bounds re-reduced by each refit (orderable encoding)
+    int bounds_dirty;           // d_red is newer than `bounds`
 };
 
 namespace {
@@ -151,12 +154,13 @@ __global__ void normals_from_tris_kernel(int64_t n, const float* __restrict__ tr
 extern "C" {
 
 int rt_scene_update_normals(rt_ctx* c, rt_scene* s) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     // new world rows: the local vertices / frames no longer describe them
     if (s->inst_inv64) {
         RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
-        cudaFree(s->inst_inv64);
+        rt_free(s->inst_inv64, s->stream);
         s->inst_inv64 = nullptr;
     }
     const int64_t n = s->n - s->n_spheres;
@@ -169,26 +173,29 @@ int rt_scene_update_normals(rt_ctx* c, rt_scene* s) {
 }
 
 int rt_scene_set_local_frames(rt_ctx* c, rt_scene* s, int32_t n_inst, const double* inv12, const double* rows9) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && n_inst >= 1 && inv12 && rows9, "NULL argument or no instance");
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    if (s->inst_inv64) cudaFree(s->inst_inv64);
+    rt_free(s->inst_inv64, s->stream);
     s->inst_inv64 = nullptr;
-    RT_CUDA_TRY(cudaMalloc(&s->inst_inv64, sizeof(double) * 12 * (size_t)n_inst));
+    RT_CUDA_TRY(rt_alloc((void**)&s->inst_inv64, sizeof(double) * 12 * (size_t)n_inst, s->stream));
     RT_CUDA_TRY(cudaMemcpy(s->inst_inv64, inv12, sizeof(double) * 12 * (size_t)n_inst, cudaMemcpyHostToDevice));
-    if (!s->lrows64) RT_CUDA_TRY(cudaMalloc(&s->lrows64, sizeof(double) * 9 * (size_t)s->n));
+    if (!s->lrows64) RT_CUDA_TRY(rt_alloc((void**)&s->lrows64, sizeof(double) * 9 * (size_t)s->n, s->stream));
     RT_CUDA_TRY(cudaMemcpy(s->lrows64, rows9, sizeof(double) * 9 * (size_t)s->n, cudaMemcpyHostToDevice));
     return RT_OK;
 }
 
 int rt_scene_set_normals64(rt_ctx* c, rt_scene* s, const double* n3) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && n3, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    if (!s->wnormal64) RT_CUDA_TRY(cudaMalloc(&s->wnormal64, sizeof(double) * 3 * (size_t)s->n));
+    if (!s->wnormal64) RT_CUDA_TRY(rt_alloc((void**)&s->wnormal64, sizeof(double) * 3 * (size_t)s->n, s->stream));
     RT_CUDA_TRY(cudaMemcpy(s->wnormal64, n3, sizeof(double) * 3 * (size_t)s->n, cudaMemcpyHostToDevice));
     return RT_OK;
 }
 
 int rt_scene_get_vertices(rt_ctx* c, rt_scene* s, float* tris) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && tris, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     RT_CUDA_TRY(cudaMemcpyAsync(tris, s->tris, sizeof(float) * 9 * s->n, cudaMemcpyDeviceToHost, c->stream));
@@ -198,6 +205,7 @@ int rt_scene_get_vertices(rt_ctx* c, rt_scene* s, float* tris) {
 
 int rt_mesh_create(rt_ctx* c, int64_t n_vertices, int64_t n_faces, const int32_t* faces, int32_t n_inst,
                    const double* xform, const int64_t* tri_offset, int32_t flags, rt_mesh** out) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && faces && xform && tri_offset && out, "NULL argument");
     RT_CHECK_ARG(n_vertices >= 3 && n_faces >= 1 && n_inst >= 1, "empty mesh or no instance");
     RT_CHECK_ARG(!(flags & RT_MESH_LOCAL) || n_inst == 1, "a local (BLAS) mesh has exactly one placement");
@@ -210,10 +218,11 @@ int rt_mesh_create(rt_ctx* c, int64_t n_vertices, int64_t n_faces, const int32_t
     m->nf = n_faces;
     m->n_inst = n_inst;
     m->local = (flags & RT_MESH_LOCAL) ? 1 : 0;
-    cudaError_t e = cudaMalloc(&m->faces, sizeof(int3) * n_faces);
-    if (e == cudaSuccess) e = cudaMalloc(&m->xform, sizeof(double) * 21 * n_inst);
-    if (e == cudaSuccess) e = cudaMalloc(&m->offset, sizeof(int64_t) * n_inst);
-    if (e == cudaSuccess) e = cudaMalloc(&m->verts, sizeof(double) * 3 * n_vertices);
+    m->stream = c->stream;
+    cudaError_t e = rt_alloc((void**)&m->faces, sizeof(int3) * n_faces, c->stream, false);
+    if (e == cudaSuccess) e = rt_alloc((void**)&m->xform, sizeof(double) * 21 * n_inst, c->stream, false);
+    if (e == cudaSuccess) e = rt_alloc((void**)&m->offset, sizeof(int64_t) * n_inst, c->stream, false);
+    if (e == cudaSuccess) e = rt_alloc((void**)&m->verts, sizeof(double) * 3 * n_vertices, c->stream);
     if (e == cudaSuccess) e = cudaMemcpy(m->faces, faces, sizeof(int3) * n_faces, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(m->xform, xform, sizeof(double) * 21 * n_inst, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(m->offset, tri_offset, sizeof(int64_t) * n_inst, cudaMemcpyHostToDevice);
@@ -326,6 +335,44 @@ __global__ void mesh_check_kernel(int64_t nf, int64_t nv, const int64_t* __restr
     }
 }
 
+// the float64 root box of a resident mesh's current vertices (after a refit): the union of
+// its triangle boxes, as _triangle_boxes + _refit_boxes give the reference's root bounds
+template <typename T>
+__global__ void mesh_bounds_kernel(int64_t nf, const int3* __restrict__ F, const T* __restrict__ V,
+                                   unsigned long long* __restrict__ red) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nf; k += (int64_t)gridDim.x * blockDim.x) {
+        const int3 f = F[k];
+        const int64_t id[3] = {f.x, f.y, f.z};
+#pragma unroll
+        for (int v = 0; v < 3; ++v)
+#pragma unroll
+            for (int r = 0; r < 3; ++r) {
+                const double x = (double)V[3 * id[v] + r];
+                lo[r] = fmin(lo[r], x);
+                hi[r] = fmax(hi[r], x);
+            }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            lo[r] = fmin(lo[r], __shfl_xor_sync(0xFFFFFFFFu, lo[r], o));
+            hi[r] = fmax(hi[r], __shfl_xor_sync(0xFFFFFFFFu, hi[r], o));
+        }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+            if (lo[r] <= hi[r]) {
+                atomicMin(red + r, d2ord(lo[r]));
+                atomicMax(red + 3 + r, d2ord(hi[r]));
+            }
+}
+
+__global__ void red_init_kernel(unsigned long long* red) {
+    if (threadIdx.x < 8) red[threadIdx.x] = (threadIdx.x < 3 || threadIdx.x >= 6) ? ULLONG_MAX : 0ull;
+}
+
 // ids / rows of the custom primitives (sphere instances) at the end of the flat scene
 struct CustomRow {
     float box[9];
@@ -339,6 +386,7 @@ extern "C" {
 
 int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, const void* vertices,
                         int32_t vertices_f32) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && m && vertices, "NULL argument");
     RT_CHECK_ARG(m->device == c->device, "mesh and context live on different devices");
     RT_CHECK_ARG(m->n_inst >= 1 && m->xform, "mesh has no placement in a scene");
@@ -355,12 +403,25 @@ int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, 
     RT_CUDA_TRY(cudaMemcpyAsync(m->verts, vertices, vbytes, cudaMemcpyHostToDevice, c->stream));
     int rc = launch_mesh(c, s, m, vertices_f32 != 0, false);
     if (rc) return rc;
+    if (m->d_red) {       // the mesh's new root box (read back only when asked, rt_mesh_info)
+        red_init_kernel<<<1, 32, 0, c->stream>>>(m->d_red);
+        int64_t grid = (m->nf + 255) / 256;
+        if (grid > (int64_t)c->num_sms * 4) grid = (int64_t)c->num_sms * 4;
+        if (vertices_f32)
+            mesh_bounds_kernel<float><<<(unsigned)grid, 256, 0, c->stream>>>(
+                m->nf, m->faces, reinterpret_cast<const float*>(m->verts), m->d_red);
+        else
+            mesh_bounds_kernel<double><<<(unsigned)grid, 256, 0, c->stream>>>(m->nf, m->faces, m->verts, m->d_red);
+        RT_CUDA_TRY(cudaGetLastError());
+        m->bounds_dirty = 1;
+    }
     s->built = 0;
     return RT_OK;
 }
 
 int rt_mesh_upload(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_t n_faces, const int64_t* faces,
                    double* bounds6, rt_mesh** out) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && out && bounds6, "NULL argument");
     RT_CHECK_ARG(n_vertices >= 0 && n_faces >= 0 && (n_vertices == 0 || vertices) && (n_faces == 0 || faces),
                  "bad mesh arrays");
@@ -376,12 +437,13 @@ int rt_mesh_upload(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_
     m->nv = n_vertices;
     m->nf = n_faces;
     cudaStream_t st = c->stream;
+    m->stream = st;
     int64_t* f64 = nullptr;
     unsigned long long* red = nullptr;
-    cudaError_t e = cudaMalloc(&m->faces, sizeof(int3) * n_faces);
-    if (e == cudaSuccess) e = cudaMalloc(&m->verts, sizeof(double) * 3 * (n_vertices > 0 ? n_vertices : 1));
+    cudaError_t e = rt_alloc((void**)&m->faces, sizeof(int3) * n_faces, st, false);
+    if (e == cudaSuccess) e = rt_alloc((void**)&m->verts, sizeof(double) * 3 * (n_vertices > 0 ? n_vertices : 1), st, false);
     if (e == cudaSuccess) e = cudaMallocAsync(&f64, sizeof(int64_t) * 3 * n_faces, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(&red, sizeof(unsigned long long) * 8, st);
+    if (e == cudaSuccess) e = rt_alloc((void**)&red, sizeof(unsigned long long) * 8, st, false);
     if (e == cudaSuccess && n_vertices > 0)
         e = cudaMemcpyAsync(m->verts, vertices, sizeof(double) * 3 * n_vertices, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(f64, faces, sizeof(int64_t) * 3 * n_faces, cudaMemcpyHostToDevice, st);
@@ -396,7 +458,7 @@ int rt_mesh_upload(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_
     unsigned long long r[8];
     if (e == cudaSuccess) e = cudaMemcpyAsync(r, red, sizeof r, cudaMemcpyDeviceToHost, st);
     if (f64) cudaFreeAsync(f64, st);
-    if (red) cudaFreeAsync(red, st);
+    m->d_red = red;       // kept: each refit re-reduces the bounds into it
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
         rt_mesh_destroy(m);
@@ -423,6 +485,7 @@ int rt_mesh_upload(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_
 int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_t n_inst,
                      const rt_instance_src* inst, int32_t n_custom, const rt_custom_src* custom,
                      const float* mat_color, const float* mat_emissive, int32_t n_mat, rt_scene** out) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && out, "NULL argument");
     RT_CHECK_ARG(n_meshes >= 0 && n_inst >= 0 && n_custom >= 0, "negative count");
     RT_CHECK_ARG(n_inst + n_custom >= 1, "a scene needs at least one instance");
@@ -463,10 +526,10 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
     rc = rt_scene_set_materials(c, s, mat_color, mat_emissive);
     if (rc) return fail(rc);
     cudaStream_t st = c->stream;
-    cudaError_t e = cudaMalloc(&s->wnormal64, sizeof(double) * 3 * (size_t)n);
-    if (e == cudaSuccess) e = cudaMalloc(&s->lrows64, sizeof(double) * 9 * (size_t)n);
+    cudaError_t e = rt_alloc((void**)&s->wnormal64, sizeof(double) * 3 * (size_t)n, st, false);
+    if (e == cudaSuccess) e = rt_alloc((void**)&s->lrows64, sizeof(double) * 9 * (size_t)n, st, false);
     const int32_t ni = n_inst + n_custom;
-    if (e == cudaSuccess) e = cudaMalloc(&s->inst_inv64, sizeof(double) * 12 * (size_t)ni);
+    if (e == cudaSuccess) e = rt_alloc((void**)&s->inst_inv64, sizeof(double) * 12 * (size_t)ni, st);
     if (e != cudaSuccess) {
         rt_set_error("cudaMalloc failed: %s", cudaGetErrorString(e));
         return fail(RT_ENOMEM);
@@ -496,14 +559,14 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
         if (!m || ofs[k].empty()) continue;
         const int32_t cnt = (int32_t)ofs[k].size();
         if (m->n_inst != cnt) {
-            if (m->xform) cudaFree(m->xform);
-            if (m->offset) cudaFree(m->offset);
-            if (m->meta) cudaFree(m->meta);
+            rt_free(m->xform, m->stream);
+            rt_free(m->offset, m->stream);
+            rt_free(m->meta, m->stream);
             m->xform = nullptr; m->offset = nullptr; m->meta = nullptr;
             m->n_inst = 0;
-            e = cudaMalloc(&m->xform, sizeof(double) * 21 * cnt);
-            if (e == cudaSuccess) e = cudaMalloc(&m->offset, sizeof(int64_t) * cnt);
-            if (e == cudaSuccess) e = cudaMalloc(&m->meta, sizeof(int4) * cnt);
+            e = rt_alloc((void**)&m->xform, sizeof(double) * 21 * cnt, m->stream, false);
+            if (e == cudaSuccess) e = rt_alloc((void**)&m->offset, sizeof(int64_t) * cnt, m->stream, false);
+            if (e == cudaSuccess) e = rt_alloc((void**)&m->meta, sizeof(int4) * cnt, m->stream);
             if (e != cudaSuccess) break;
             m->n_inst = cnt;
         }
@@ -555,6 +618,14 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
 
 int rt_mesh_info(rt_mesh* m, int64_t* n_vertices, int64_t* n_faces, double* bounds6) {
     RT_CHECK_ARG(m, "mesh is NULL");
+    if (m->bounds_dirty && bounds6) {
+        unsigned long long r[8];
+        RT_CUDA_TRY(cudaSetDevice(m->device));
+        RT_CUDA_TRY(cudaMemcpyAsync(r, m->d_red, sizeof r, cudaMemcpyDeviceToHost, m->stream));
+        RT_CUDA_TRY(cudaStreamSynchronize(m->stream));
+        for (int k = 0; k < 6; ++k) m->bounds[k] = ord2d(r[k]);
+        m->bounds_dirty = 0;
+    }
     if (n_vertices) *n_vertices = m->nv;
     if (n_faces) *n_faces = m->nf;
     if (bounds6) memcpy(bounds6, m->bounds, sizeof m->bounds);
@@ -563,6 +634,7 @@ int rt_mesh_info(rt_mesh* m, int64_t* n_vertices, int64_t* n_faces, double* boun
 
 int rt_scene_get_ids(rt_ctx* c, rt_scene* s, int32_t* tri_inst, int32_t* tri_prim, uint32_t* tri_mask,
                      int32_t* tri_material) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -581,9 +653,8 @@ int rt_scene_get_ids(rt_ctx* c, rt_scene* s, int32_t* tri_inst, int32_t* tri_pri
 void rt_mesh_destroy(rt_mesh* m) {
     if (!m) return;
     cudaSetDevice(m->device);
-    void* ptrs[] = {m->faces, m->xform, m->offset, m->verts, m->meta};
-    for (void* p : ptrs)
-        if (p) cudaFree(p);
+    void* ptrs[] = {m->faces, m->xform, m->offset, m->verts, m->meta, m->d_red};
+    for (void* p : ptrs) rt_free(p, m->stream);
     delete m;
 }
 
@@ -591,6 +662,7 @@ void rt_mesh_destroy(rt_mesh* m) {
 
 extern "C" int rt_scene_get_geometry(rt_ctx* c, rt_scene* s, float* tris9, float* normals3, double* normals64,
                                      double* local_rows9) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     RT_CUDA_TRY(cudaStreamSynchronize(c->stream));

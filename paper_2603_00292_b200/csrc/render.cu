@@ -14,6 +14,9 @@
 namespace {
 
 constexpr int MEGA_THREADS = 128;
+#ifndef RT_SMEM_STACK
+#define RT_SMEM_STACK 0          // > 0: top entries of the megakernel's walk stack in shared memory
+#endif
 #ifndef MEGA_MIN_BLOCKS
 #define MEGA_MIN_BLOCKS 7       // 72 registers: the 4-wide walk + PT shading without spills
 #endif
@@ -160,7 +163,7 @@ __device__ __forceinline__ float sample_ao(const FrameConst& F, const float4* __
     RayPre R;
     ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
     uint32_t nt, nv;
-    const HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv, sv);
+    const HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, LocalStack{stack}, nt, nv, sv);
     ++rays;
     if (h.id < 0) return 1.0f;
     const float4 a = __ldg(attr + h.id);
@@ -200,7 +203,7 @@ __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* 
         RayPre R;
         ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
         uint32_t nt, nv;
-        const HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv, sv);
+        const HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, LocalStack{stack}, nt, nv, sv);
         ++rays;
         if (h.id < 0) {
             P.rr += P.tr * F.sky[0]; P.rg += P.tg * F.sky[1]; P.rb += P.tb * F.sky[2];
@@ -276,6 +279,13 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
         return;
     }
     int2 stack[RT_STACK4];
+#if RT_SMEM_STACK
+    // PT / eye walks: the top RT_SMEM_STACK entries in shared memory, the rest local
+    __shared__ int2 s_stack[RT_SMEM_STACK * MEGA_THREADS];
+    const SmemStack<RT_SMEM_STACK, MEGA_THREADS> walk_stack{s_stack + threadIdx.x, stack};
+#else
+    const LocalStack walk_stack{stack};
+#endif
     const int lane = threadIdx.x & 31;
     unsigned long long rays = 0;
     const int max_depth = INTEG == RT_INTEG_EYE ? 1 : F.max_depth;
@@ -303,7 +313,7 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
                         RayPre R;
                         ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
                         uint32_t nt, nv;
-                        HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, stack, nt, nv, sv);
+                        HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, walk_stack, nt, nv, sv);
                         ++rays;
                         if (!shade_bounce<SPH>(F, attr, mat_color, mat_emis, h, P, sv)) break;
                     }
@@ -378,7 +388,7 @@ __global__ void __launch_bounds__(128, 8) wf_extend(const float4* __restrict__ n
             RayPre R;
             ray_setup(R, a.x, a.y, a.z, b.x, b.y, b.z, a.w);
             uint32_t nt, nv;
-            HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, b.w, RT_FULL, stack, nt, nv, sv);
+            HitRec h = trace_ray4<false, SPH>(bvh4, root4, tris, R, b.w, RT_FULL, LocalStack{stack}, nt, nv, sv);
             W.hit[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
             }
         }
@@ -534,13 +544,19 @@ struct WaveBuffers {
 
 }  // namespace
 
-// wavefront buffers per scene (keyed by scene pointer; single-threaded contexts)
+// wavefront buffers per scene (keyed by scene pointer).  The map is shared by every
+// context, so it has its own lock (a scene is destroyed without its context).
 #include <map>
 static std::map<rt_scene*, WaveBuffers>& wave_map() {
     static std::map<rt_scene*, WaveBuffers> m;
     return m;
 }
+static std::mutex& wave_lock() {
+    static std::mutex m;
+    return m;
+}
 void rt_render_release(rt_scene* s) {
+    std::lock_guard<std::mutex> lk(wave_lock());
     auto& m = wave_map();
     auto it = m.find(s);
     if (it != m.end()) {
@@ -550,6 +566,7 @@ void rt_render_release(rt_scene* s) {
 }
 
 static int ensure_wave(rt_scene* s, int64_t npix, WaveBuffers*& out) {
+    std::lock_guard<std::mutex> lk(wave_lock());   // the entry stays put: std::map nodes are stable
     WaveBuffers& wb = wave_map()[s];
     if (wb.cap < npix) {
         if (wb.mem) cudaFree(wb.mem);
@@ -585,9 +602,17 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         rt_set_error("band_offset must be in [0, band_stride)");
         return RT_EINVAL;
     }
-    if (p->s1 <= p->s0) return RT_EINVAL;
-    if (F.nunits > 0x7FFFFFF0ll) return RT_EINVAL;
+    if (p->s1 <= p->s0) {
+        rt_set_error("empty sample window [%d, %d)", p->s0, p->s1);
+        return RT_EINVAL;
+    }
+    if (F.nunits > 0x7FFFFFF0ll) {
+        rt_set_error("too many work units (%lld) in one render", (long long)F.nunits);
+        return RT_EINVAL;
+    }
     if (F.nunits == 0 || F.npix == 0) {          // e.g. more GPUs than tile rows
+        // the ray counter of this context reads 0 for this render (rt_multi_render sums it)
+        RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter + 32, 0, sizeof(unsigned long long), ctx->stream));
         if (rays_out) *rays_out = 0;
         return RT_OK;
     }
@@ -628,7 +653,10 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         }
         if (rc) return rc;
     } else {
-        if (F.max_depth > 30) return RT_EINVAL;
+        if (F.max_depth > 30) {
+            rt_set_error("the wavefront kernel supports max_depth <= 30 (got %d); use kernel='mega'", F.max_depth);
+            return RT_EINVAL;
+        }
         WaveBuffers* wb;
         int rc = ensure_wave(s, F.nunits, wb);
         if (rc) return rc;

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+
 #include "../../include/rt_b200.h"
 
 #define RT_FULL 0xFFFFFFFFu
@@ -32,11 +34,17 @@ struct rt_ctx {
     cudaEvent_t io_ev[9];
     void* d_io;
     size_t d_io_bytes;
+    // every entry point taking the context holds this lock: the staging slots, work counters
+    // and error flag are per context, so calls on one device from several host threads
+    // (ctypes releases the GIL) are serialised instead of racing
+    std::recursive_mutex* mu;
 };
 
 struct rt_scene {
     int64_t n;
     int n_mat;
+    int device;
+    cudaStream_t stream;  // storage is stream-ordered pool memory, freed on this stream
     // inputs (resident)
     float* tris;          // (n, 9) world vertices
     float4* tri_attr;     // (n) normal.xyz, material id bits   (F9 normals)
@@ -92,6 +100,13 @@ void rt_set_error(const char* fmt, ...);
         }                                                                         \
     } while (0)
 
+#define RT_CTX_LOCK(ctx)                                                   \
+    if (!(ctx)) {                                                          \
+        rt_set_error("ctx is NULL");                                       \
+        return RT_EINVAL;                                                  \
+    }                                                                      \
+    std::lock_guard<std::recursive_mutex> _rt_ctx_guard(*(ctx)->mu)
+
 #define RT_CHECK_ARG(cond, msg)              \
     do {                                     \
         if (!(cond)) {                       \
@@ -99,6 +114,19 @@ void rt_set_error(const char* fmt, ...);
             return RT_EINVAL;                \
         }                                    \
     } while (0)
+
+// Scene / mesh storage comes from the device's stream-ordered memory pool (its release
+// threshold is raised at context creation, so freed blocks stay cached and compiling a
+// scene again costs no cudaMalloc / cudaFree).  rt_alloc synchronises the stream once the
+// allocation is enqueued, so the block is usable from any stream afterwards.
+inline cudaError_t rt_alloc(void** p, size_t bytes, cudaStream_t st, bool sync = true) {
+    cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, st);
+    if (e == cudaSuccess && sync) e = cudaStreamSynchronize(st);
+    return e;
+}
+inline void rt_free(void* p, cudaStream_t st) {
+    if (p) cudaFreeAsync(p, st);
+}
 
 // reads and clears the device error flag (synchronises the context stream)
 int rt_check_device_error(rt_ctx* ctx);

@@ -283,7 +283,22 @@ __global__ void tlas_expand_f64(int64_t n, const float4* __restrict__ hits, cons
                          o, d);
             const double t2 = tri_hit_f64(o, d, tmin64 ? tmin64[i] : tmin_s, tmax64 ? tmax64[i] : tmax_s,
                                           B.lrows + 9 * (int64_t)p, u2, v2);
-            if (t2 >= 0.0) { th = t2; uh = u2; vh = v2; }
+            const double hi_t = tmax64 ? tmax64[i] : tmax_s;
+            if (t2 >= 0.0 && t2 < hi_t) {        // [t_min, t_max): accel.py:771-773, 815-817
+                th = t2; uh = u2; vh = v2;
+            } else if (t2 >= 0.0 || tri_hit_f64(o, d, 0.0, INFINITY, B.lrows + 9 * (int64_t)p, u2, v2) >= 0.0) {
+                th = -1.0;                         // a float64 hit, outside [t_min, t_max]: a miss
+            }
+        }
+        if (o64) {
+            // the walk's fp32 window is the caller's rounded outward by a few ulps: a hit
+            // outside the exact window is not the reference's hit
+            const double lo_t = tmin64 ? tmin64[i] : tmin_s, hi_t = tmax64 ? tmax64[i] : tmax_s;
+            if (th < lo_t || !(th < hi_t)) {
+                t[i] = -1.0; oinst[i] = -1; oprim[i] = -1; u[i] = -1.0; v[i] = -1.0;
+                nrm[3 * i] = nrm[3 * i + 1] = nrm[3 * i + 2] = 0.0;
+                continue;
+            }
         }
         t[i] = th; oinst[i] = ii; oprim[i] = p; u[i] = uh; v[i] = vh;
     }
@@ -390,22 +405,25 @@ int build_top(rt_ctx* c, rt_tlas* T, const float* boxes6) {
 extern "C" {
 
 int rt_scene_set_local_normals(rt_ctx* c, rt_scene* s, const double* n3) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && n3, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    if (!s->lnormal64) RT_CUDA_TRY(cudaMalloc(&s->lnormal64, sizeof(double) * 3 * (size_t)s->n));
+    if (!s->lnormal64) RT_CUDA_TRY(rt_alloc((void**)&s->lnormal64, sizeof(double) * 3 * (size_t)s->n, s->stream));
     RT_CUDA_TRY(cudaMemcpy(s->lnormal64, n3, sizeof(double) * 3 * (size_t)s->n, cudaMemcpyHostToDevice));
     return RT_OK;
 }
 
 int rt_scene_set_local_rows(rt_ctx* c, rt_scene* s, const double* rows9) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && rows9, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    if (!s->lrows64) RT_CUDA_TRY(cudaMalloc(&s->lrows64, sizeof(double) * 9 * (size_t)s->n));
+    if (!s->lrows64) RT_CUDA_TRY(rt_alloc((void**)&s->lrows64, sizeof(double) * 9 * (size_t)s->n, s->stream));
     RT_CUDA_TRY(cudaMemcpy(s->lrows64, rows9, sizeof(double) * 9 * (size_t)s->n, cudaMemcpyHostToDevice));
     return RT_OK;
 }
 
 int rt_scene_set_custom(rt_ctx* c, rt_scene* s, int32_t geom_type, int64_t data_offset) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && s && geom_type >= 0 && data_offset >= 0, "bad custom primitive description");
     s->custom = 1;
     s->geom_type = geom_type;
@@ -415,6 +433,7 @@ int rt_scene_set_custom(rt_ctx* c, rt_scene* s, int32_t geom_type, int64_t data_
 
 int rt_tlas_create(rt_ctx* c, int32_t n_inst, rt_scene* const* inst_blas, const double* inv12, const float* boxes6,
                    const uint32_t* masks, rt_tlas** out) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && out && n_inst >= 1 && inst_blas && inv12 && boxes6 && masks, "bad tlas arguments");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     rt_tlas* T = new rt_tlas();
@@ -486,6 +505,7 @@ int rt_tlas_create(rt_ctx* c, int32_t n_inst, rt_scene* const* inst_blas, const 
 }
 
 int rt_tlas_update(rt_ctx* c, rt_tlas* T, const double* inv12, const float* boxes6) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && T && inv12 && boxes6, "NULL argument");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     // BLAS refits may have changed their roots / heights (rebuilt LBVH)
@@ -508,6 +528,7 @@ int rt_tlas_update(rt_ctx* c, rt_tlas* T, const double* inv12, const float* boxe
 }
 
 int rt_tlas_set_custom_data(rt_ctx* c, rt_tlas* T, int32_t geom_type, int64_t n_rows, const double* rows4) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && T && n_rows >= 0 && (n_rows == 0 || rows4), "bad custom data");
     RT_CUDA_TRY(cudaSetDevice(c->device));
     bool changed = false;
@@ -554,6 +575,7 @@ int rt_tlas_flatten(rt_ctx* c, rt_tlas* T, const double* mat12, const int32_t* i
                     const float* mat_emissive, int32_t n_mat, int32_t n_custom, const float* custom_boxes9,
                     const double* custom_rows16, const int32_t* custom_inst, const int32_t* custom_prim,
                     int32_t bits, rt_scene** io) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && T && mat12 && inst_material && mat_color && mat_emissive && io, "NULL argument");
     RT_CHECK_ARG(n_custom >= 0 && (n_custom == 0 || (custom_boxes9 && custom_rows16 && custom_inst && custom_prim)),
                  "bad custom primitive rows");
@@ -646,6 +668,7 @@ int rt_tlas_flatten(rt_ctx* c, rt_tlas* T, const double* mat12, const int32_t* i
 }
 
 int rt_tlas_info(rt_ctx* c, rt_tlas* T, float* root6, int32_t* height) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && T, "NULL argument");
     return rt_bvh_info(c, T->top, root6, height, nullptr);
 }
@@ -655,6 +678,7 @@ int rt_tlas_info(rt_ctx* c, rt_tlas* T, float* root6, int32_t* height) {
 int rt_tlas_closest_host(rt_ctx* c, rt_tlas* T, int64_t n, const double* o, const double* d, const double* tmin,
                          const double* tmax, double tmin_s, double tmax_s, uint32_t ray_mask, double* t,
                          int64_t* inst, int64_t* prim, double* u, double* v, double* nrm, int64_t* stats) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && T, "NULL argument");
     RT_CHECK_ARG(n >= 0, "negative ray count");
     RT_CHECK_ARG(n == 0 || (o && d && t && inst && prim && u && v && nrm), "NULL ray or output buffer");
@@ -707,6 +731,7 @@ int rt_tlas_closest_host(rt_ctx* c, rt_tlas* T, int64_t n, const double* o, cons
 // accel.py:1159-1174 any_hit_batch over a two-level structure
 int rt_tlas_any_host(rt_ctx* c, rt_tlas* T, int64_t n, const double* o, const double* d, const double* tmin,
                      const double* tmax, double tmin_s, double tmax_s, uint32_t ray_mask, uint8_t* out) {
+    RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && T, "NULL argument");
     RT_CHECK_ARG(n >= 0, "negative ray count");
     RT_CHECK_ARG(n == 0 || (o && d && out), "NULL ray or output buffer");

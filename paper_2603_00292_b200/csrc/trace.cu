@@ -7,6 +7,9 @@
 namespace {
 
 constexpr int TRACE_THREADS = 128;
+#ifndef RT_SMEM_STACK
+#define RT_SMEM_STACK 0
+#endif
 
 // One warp fetches 32 rays at a time from a global counter (one atomicAdd per
 // warp), every lane runs the while-while traversal, then the warp fetches again.
@@ -22,6 +25,12 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
         return;
     }
     int2 stack[RT_STACK4];
+#if RT_SMEM_STACK
+    __shared__ int2 s_stack[RT_SMEM_STACK * TRACE_THREADS];
+    const SmemStack<RT_SMEM_STACK, TRACE_THREADS> walk_stack{s_stack + threadIdx.x, stack};
+#else
+    const LocalStack walk_stack{stack};
+#endif
     const int lane = threadIdx.x & 31;
     while (true) {
         unsigned base = 0;
@@ -34,7 +43,7 @@ __global__ void __launch_bounds__(TRACE_THREADS, 8) trace_closest_kernel(
             RayPre R;
             ray_setup(R, r.ox, r.oy, r.oz, r.dx, r.dy, r.dz, r.tmin);
             uint32_t nt = 0, nv = 0;
-            HitRec h = trace_ray4<STATS, SPH>(bvh4, root4, tris, R, r.tmax, ray_mask, stack, nt, nv, sv);
+            HitRec h = trace_ray4<STATS, SPH>(bvh4, root4, tris, R, r.tmax, ray_mask, walk_stack, nt, nv, sv);
             hits[i] = make_float4(h.t, __int_as_float(h.id), h.u, h.v);
             if (STATS) reinterpret_cast<uint2*>(stats)[i] = make_uint2(nt, nv);
         }
@@ -77,9 +86,15 @@ __global__ void pack_rays_f64(int64_t n, const double* __restrict__ o, const dou
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const double tn = tmin ? tmin[i] : tmin_s;
         const double tm = tmax ? tmax[i] : tmax_s;
-        rays[2 * i] = make_float4((float)o[3 * i], (float)o[3 * i + 1], (float)o[3 * i + 2], (float)tn);
-        rays[2 * i + 1] = make_float4((float)d[3 * i], (float)d[3 * i + 1], (float)d[3 * i + 2],
-                                      tm > 3.0e38 ? INFINITY : (float)tm);
+        // the fp32 window contains the float64 one with a few ulps to spare (t_min rounded
+        // down, t_max up, then widened by 2^-21 relative: the fp32 triangle t carries a few
+        // ulps of error), so the walk never loses a hit the reference accepts;
+        // expand_hits_f64 re-checks the exact window
+        float tn32 = __double2float_rd(tn), tm32 = tm > 3.0e38 ? INFINITY : __double2float_ru(tm);
+        tn32 = tn32 > 0.f ? __fmul_rd(tn32, 1.0f - 0x1p-21f) : __fmul_rd(tn32, 1.0f + 0x1p-21f);
+        tm32 = tm32 > 0.f ? __fmul_ru(tm32, 1.0f + 0x1p-21f) : __fmul_ru(tm32, 1.0f - 0x1p-21f);
+        rays[2 * i] = make_float4((float)o[3 * i], (float)o[3 * i + 1], (float)o[3 * i + 2], tn32);
+        rays[2 * i + 1] = make_float4((float)d[3 * i], (float)d[3 * i + 1], (float)d[3 * i + 2], tm32);
     }
 }
 
@@ -114,19 +129,45 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
                 double d[3] = {d64[3 * i], d64[3 * i + 1], d64[3 * i + 2]};
                 double u2, v2, t2;
                 const double lo_t = tmin64 ? tmin64[i] : tmin_s, hi_t = tmax64 ? tmax64[i] : tmax_s;
+                const double* row;
+                double ol[3], dl[3];
                 if (inv64 && lrows64) {
                     // exactly the reference's path: the ray to the instance's local space with
                     // its float64 inverse (accel.py:804-809), _tri_hit on the local vertices
-                    double m[12], ol[3], dl[3];
+                    double m[12];
                     const int ins = tri_inst[id];
 #pragma unroll
                     for (int k = 0; k < 12; ++k) m[k] = inv64[12 * (int64_t)ins + k];
                     to_local_f64(m, o[0], o[1], o[2], d[0], d[1], d[2], ol, dl);
-                    t2 = tri_hit_f64(ol, dl, lo_t, hi_t, lrows64 + 9 * (int64_t)id, u2, v2);
+                    row = lrows64 + 9 * (int64_t)id;
                 } else {
-                    t2 = tri_hit_f64(o, d, lo_t, hi_t, wtris + 9 * (int64_t)id, u2, v2);
+                    for (int k = 0; k < 3; ++k) { ol[k] = o[k]; dl[k] = d[k]; }
+                    row = nullptr;
                 }
-                if (t2 >= 0.0) { th = t2; uh = u2; vh = v2; }
+                if (row) t2 = tri_hit_f64(ol, dl, lo_t, hi_t, row, u2, v2);
+                else t2 = tri_hit_f64(o, d, lo_t, hi_t, wtris + 9 * (int64_t)id, u2, v2);
+                // a hit exactly at t_max is not taken by the reference's scene-level rule
+                // (t < best_t, or t == best_t with a lower instance than best_inst = -1;
+                // accel.py:771-773, 815-817): its closest-hit window is [t_min, t_max)
+                if (t2 >= 0.0 && !(t2 < hi_t)) t2 = -1.0;
+                if (t2 >= 0.0) {
+                    th = t2; uh = u2; vh = v2;
+                } else {
+                    // rejected: outside [t_min, t_max] (the fp32 walk's window is the caller's
+                    // rounded outward by a few ulps) -> not the reference's hit, a miss; or a
+                    // geometric edge / grazing case of the float64 test -> the fp32 values stay
+                    const double t3 = row ? tri_hit_f64(ol, dl, 0.0, INFINITY, row, u2, v2)
+                                          : tri_hit_f64(o, d, 0.0, INFINITY, wtris + 9 * (int64_t)id, u2, v2);
+                    if (t3 >= 0.0 || th < lo_t || !(th < hi_t)) id = -1;
+                }
+            } else if (o64) {                                    // spheres: the exact window
+                if (th < (tmin64 ? tmin64[i] : tmin_s) || !(th < (tmax64 ? tmax64[i] : tmax_s))) id = -1;
+            }
+            if (id < 0) {
+                t[i] = -1.0; inst[i] = -1; prim[i] = -1; u[i] = -1.0; v[i] = -1.0;
+                nrm[3 * i] = 0.0; nrm[3 * i + 1] = 0.0; nrm[3 * i + 2] = 0.0;
+                if (st64) { st64[2 * i] = st32[2 * i]; st64[2 * i + 1] = st32[2 * i + 1]; }
+                continue;
             }
             t[i] = th; inst[i] = tri_inst[id]; prim[i] = tri_prim[id]; u[i] = uh; v[i] = vh;
             if (id >= sv.base) {
@@ -150,7 +191,10 @@ __global__ void expand_hits_f64(int64_t n, const float4* __restrict__ hits, cons
 int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4* hits, uint32_t mask,
                   uint32_t* stats, int custom_mode) {
     if (n <= 0) return RT_OK;
-    if ((n + 64) > 0xFFFFFFFFll) return RT_EINVAL;
+    if ((n + 64) > 0xFFFFFFFFll) {
+        rt_set_error("at most 2^32 - 65 rays per trace call (got %lld)", (long long)n);
+        return RT_EINVAL;
+    }
     cudaStream_t st = ctx->stream;
     RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), st));
     const SphereView sv = rt_sphere_view(ctx, s, custom_mode);
@@ -179,7 +223,10 @@ int rt_trace_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, float4
 int rt_trace_any_impl(rt_ctx* ctx, rt_scene* s, int64_t n, const float* rays, uint8_t* out, uint32_t mask,
                       int custom_mode) {
     if (n <= 0) return RT_OK;
-    if ((n + 64) > 0xFFFFFFFFll) return RT_EINVAL;
+    if ((n + 64) > 0xFFFFFFFFll) {
+        rt_set_error("at most 2^32 - 65 rays per trace call (got %lld)", (long long)n);
+        return RT_EINVAL;
+    }
     cudaStream_t st = ctx->stream;
     RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned int), st));
     const SphereView sv = rt_sphere_view(ctx, s, custom_mode);

@@ -97,6 +97,20 @@ __device__ __forceinline__ void ray_setup(RayPre& R, float ox, float oy, float o
     R.m22 = (kz == 2) ? sz : 0.f;
 }
 
+// packed fp32x2 FMA (sm_100 FFMA2): two independent correctly rounded FMAs in one
+// instruction, bit-identical to two FFMAs
+#ifndef RT_BOX_FFMA2
+#define RT_BOX_FFMA2 0
+#endif
+__device__ __forceinline__ void ffma2(float ax, float ay, float bx, float by, float cx, float cy, float& dx,
+                                      float& dy) {
+    asm("{\n\t.reg .b64 pa, pb, pc, pd;\n\t"
+        "mov.b64 pa, {%2, %3};\n\tmov.b64 pb, {%4, %5};\n\tmov.b64 pc, {%6, %7};\n\t"
+        "fma.rn.f32x2 pd, pa, pb, pc;\n\tmov.b64 {%0, %1}, pd;\n\t}"
+        : "=f"(dx), "=f"(dy)
+        : "f"(ax), "f"(ay), "f"(bx), "f"(by), "f"(cx), "f"(cy));
+}
+
 // slab test of one child box against [tmin, tmax]; returns entry distance or +inf on miss
 __device__ __forceinline__ float box_enter(const RayPre& R, float lox, float hix, float loy, float hiy, float loz,
                                            float hiz, float tmax) {
@@ -107,7 +121,14 @@ __device__ __forceinline__ float box_enter(const RayPre& R, float lox, float hix
     // all culling for rays with a near-zero direction component -- measured:
     // 54K node fetches for such a ray on the 10M soup -- and bounding it per axis
     // costs as many instructions as this form.)
-#if RT_FMA_SLABS
+#if RT_FMA_SLABS && RT_BOX_FFMA2
+    // (x, y) planes as packed pairs: a node slot holds (lo.x, lo.y, lo.z, id), (hi.x, hi.y, hi.z, -),
+    // so (lo.x, lo.y) and (hi.x, hi.y) are register pairs straight from the 256-bit loads
+    float tx0, ty0, tx1, ty1;
+    ffma2(lox, loy, R.ix, R.iy, R.blx, R.bly, tx0, ty0);
+    ffma2(hix, hiy, R.ix, R.iy, R.bhx, R.bhy, tx1, ty1);
+    float tz0 = __fmaf_rn(loz, R.iz, R.blz), tz1 = __fmaf_rn(hiz, R.iz, R.bhz);
+#elif RT_FMA_SLABS
     float tx0 = __fmaf_rn(lox, R.ix, R.blx), tx1 = __fmaf_rn(hix, R.ix, R.bhx);
     float ty0 = __fmaf_rn(loy, R.iy, R.bly), ty1 = __fmaf_rn(hiy, R.iy, R.bhy);
     float tz0 = __fmaf_rn(loz, R.iz, R.blz), tz1 = __fmaf_rn(hiz, R.iz, R.bhz);
@@ -350,23 +371,43 @@ __device__ __forceinline__ void cswap(float& ta, int& ca, float& tb, int& cb) {
     }
 }
 
+// Traversal stacks.  LocalStack: the whole stack in local memory (L1-resident).
+// SmemStack: the first N entries in shared memory (entry k of thread t at
+// base[k * STRIDE + t]: a warp touching one depth hits consecutive words), deeper
+// entries spill to local memory.
+struct LocalStack {
+    int2* p;
+    __device__ __forceinline__ void put(int i, int2 v) const { p[i] = v; }
+    __device__ __forceinline__ int2 get(int i) const { return p[i]; }
+};
+template <int N, int STRIDE>
+struct SmemStack {
+    int2* sm;          // shared: this thread's column
+    int2* lm;          // local overflow
+    __device__ __forceinline__ void put(int i, int2 v) const {
+        if (i < N) sm[i * STRIDE] = v;
+        else lm[i - N] = v;
+    }
+    __device__ __forceinline__ int2 get(int i) const { return i < N ? sm[i * STRIDE] : lm[i - N]; }
+};
+
 // 4-wide traversal over the BVH4 view (emit.cuh bvh4_collapse_kernel): one
 // 112-B node fetch tests 4 child boxes, children visited nearest first, so a
 // ray makes about half the dependent node fetches of the binary walk.  Same
 // triangle test, tie rule and conservative slab test as trace_ray.  The stack
 // holds at most 3 * ceil(height / 2) entries (checked by the caller).
-template <bool STATS, bool SPH>
+template <bool STATS, bool SPH, typename Stack>
 __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, int root,
                                              const float4* __restrict__ tris, const RayPre& R, float tmax,
-                                             uint32_t ray_mask, int2* stack, uint32_t& n_tests, uint32_t& n_visits,
-                                             const SphereView& sv) {
+                                             uint32_t ray_mask, const Stack& stack, uint32_t& n_tests,
+                                             uint32_t& n_visits, const SphereView& sv) {
     HitRec h;
     h.t = tmax; h.id = -1; h.u = 0.f; h.v = 0.f;
     // stack entries carry the child's entry distance: a popped entry that lies
     // beyond the closest hit found since it was pushed is skipped (leaf children
     // would otherwise be tested without re-culling)
     int sp = 0;
-    stack[0] = make_int2(RT_SENTINEL, 0);
+    stack.put(0, make_int2(RT_SENTINEL, 0));
     int node = root;
     while (node != RT_SENTINEL) {
         if (node >= 0) {
@@ -385,9 +426,9 @@ __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, in
             cswap(t0, c0, t2, c2);
             cswap(t1, c1, t3, c3);
             cswap(t1, c1, t2, c2);
-            if (t3 != INFINITY) stack[++sp] = make_int2(c3, __float_as_int(t3));
-            if (t2 != INFINITY) stack[++sp] = make_int2(c2, __float_as_int(t2));
-            if (t1 != INFINITY) stack[++sp] = make_int2(c1, __float_as_int(t1));
+            if (t3 != INFINITY) stack.put(++sp, make_int2(c3, __float_as_int(t3)));
+            if (t2 != INFINITY) stack.put(++sp, make_int2(c2, __float_as_int(t2)));
+            if (t1 != INFINITY) stack.put(++sp, make_int2(c1, __float_as_int(t1)));
             if (t0 != INFINITY) {
                 node = c0;
                 continue;
@@ -404,7 +445,7 @@ __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, in
         // pop, dropping entries entered beyond the current closest hit (the box
         // test is inclusive and widened, so ties at t are kept)
         while (true) {
-            const int2 e = stack[sp--];
+            const int2 e = stack.get(sp--);
             node = e.x;
             if (node == RT_SENTINEL || __int_as_float(e.y) <= fmaf(h.t, 1.0000008f, 1e-30f)) break;
         }

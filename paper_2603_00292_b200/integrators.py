@@ -66,6 +66,8 @@ def make_params(scene, width, height, s0, s1, integrator, seed, cfg, jitter, ker
         raise ValueError(f"unknown kernel {kernel!r}, expected one of {tuple(KERNELS)}")
     if kernel == "wavefront" and integrator not in ("eye", "pt"):
         raise ValueError(f"integrator {integrator!r} runs in the megakernel only (kernel='mega')")
+    if hasattr(scene, "sync_render"):
+        scene.sync_render()          # two-level: re-flatten after refresh_instance_bounds
     cfg, sky, off = resolve_config(scene, cfg)
     scene.camera.validate_distortion()
     p = RenderParams()
@@ -120,8 +122,17 @@ def _copy_stream(dev):
 
 def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt", seed: int = 0,
                  workers: int = 1, cfg: Optional[IntegratorConfig] = None, jitter: bool = True,
-                 return_stats: bool = False, kernel: str = "mega", samples=None, bands=None):
+                 return_stats: bool = False, kernel: str = "mega", samples=None, bands=None, gpus: int = 1):
     """Render a full frame into a fresh AccumBuffer (float64 host copy of the fp32 device sums).
+
+    ``workers`` (the reference's CPU thread count, integrators.py:426-463) is accepted and
+    validated; it cannot change the result (the reference's frames are bit-identical for any
+    worker count, SPEC AC9) and the GPU needs no host threads, so it selects nothing here.
+    ``gpus=N`` renders on GPUs [d, d+N) of the node, d = the scene's device: the scene is
+    replicated (device-to-device clone of its built LBVH), GPU g renders the interleaved
+    4-row tile bands r % N == g, and the bands are gathered into GPU d over NCCL
+    (rt_multi_render).  Every pixel's samples are summed on one GPU, so the frame is
+    bit-identical to ``gpus=1``.
 
     The fp32 sums are widened to float64 on the device (exact) and read back by DMA into
     pinned memory; large primary-ray (eye) megakernel frames render in 4 row chunks so each
@@ -134,6 +145,11 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
         raise ValueError("width, height, and spp must all be >= 1")
     if workers < 1:
         raise ValueError("workers must be >= 1")
+    if gpus < 1:
+        raise ValueError("gpus must be >= 1")
+    if gpus > 1:
+        return _render_frame_gpus(scene, width, height, spp, integrator, seed, cfg, jitter, return_stats, kernel,
+                                  samples, gpus)
     if bands is not None and int(bands[0]) == 1:
         bands = None                                 # one GPU's "split" is the whole frame
     dev = torch.device("cuda", scene.tlas.ctx.device)
@@ -171,6 +187,29 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
         cur.wait_stream(copy)
         rays = None
     cur.synchronize()
+    buf = AccumBuffer(width, height, host.numpy().reshape(height, width, 4))
+    if return_stats:
+        return buf, {"rays": rays}
+    return buf
+
+
+def _render_frame_gpus(scene, width, height, spp, integrator, seed, cfg, jitter, return_stats, kernel, samples,
+                       gpus):
+    """render_frame(gpus=N): tile split over N devices through rt_multi_render."""
+    import torch
+    from .distributed import render_frame_multi
+    if samples is not None:
+        raise ValueError("gpus > 1 renders whole sample ranges [0, spp)")
+    dev0 = (getattr(scene, "render_tlas", None) or scene.tlas).ctx.device
+    n_dev = torch.cuda.device_count()
+    if dev0 + gpus > n_dev:
+        raise ValueError(f"gpus={gpus} from device {dev0} needs {dev0 + gpus} devices, {n_dev} present")
+    reps = [scene] + [scene.replica(dev0 + g) for g in range(1, gpus)]
+    acc, rays = render_frame_multi(reps, width, height, spp, integrator, seed, cfg, jitter, kernel,
+                                   return_device=True, mode="tiles")
+    host = torch.empty((height * width, 4), dtype=torch.float64, pin_memory=True)
+    host.copy_(acc.to(torch.float64), non_blocking=True)
+    torch.cuda.current_stream(acc.device).synchronize()
     buf = AccumBuffer(width, height, host.numpy().reshape(height, width, 4))
     if return_stats:
         return buf, {"rays": rays}

@@ -61,6 +61,7 @@ class GpuTlas:
         self._tris = None
         self._ids = None
         self.build_ms = None
+        self.version = 0             # bumped by every (re)build: render replicas follow it
         # custom primitives: the last rows are sphere instance boxes
         self.sphere_rows = np.zeros((0, 16)) if sphere_rows is None else np.ascontiguousarray(sphere_rows, np.float64)
         self.n_spheres = int(self.sphere_rows.shape[0])
@@ -110,6 +111,7 @@ class GpuTlas:
         ms = ctypes.c_float(-1.0)
         check(lib().rt_bvh_build(self.ctx.handle, self.handle, bits, ctypes.byref(ms) if timed else None))
         self.bits = bits
+        self.version += 1
         if timed:
             self.build_ms = ms.value
             return ms.value
@@ -139,6 +141,16 @@ class GpuTlas:
     def from_handle(cls, ctx, handle, n, bits, sphere_rows=None):
         """Wrap a scene built on the device (rt_tlas_flatten) whose LBVH is already built."""
         return cls(ctx, handle, n, bits, sphere_rows, build=False)
+
+    def clone(self, device):
+        """A render replica on another GPU (rt_scene_clone: device-to-device copy of the
+        geometry, shading tables and built LBVH)."""
+        ctx = _native.Context.get(device)
+        h = ctypes.c_void_p()
+        check(lib().rt_scene_clone(self.ctx.handle, self.handle, ctx.handle, ctypes.byref(h)))
+        g = GpuTlas(ctx, h, self.n, self.bits, self.sphere_rows if self.n_spheres else None,
+                    n_instances=self.n_instances, inverses=self.inverses, build=False)
+        return g
 
     def build_profiled(self, bits=None):
         """Rebuild with stage events; returns dict of device ms per stage."""
@@ -189,14 +201,70 @@ class Scene:
     lights: LightTable
     sky: np.ndarray
     background: np.ndarray
-    root_box: tuple
+    root_box_: tuple             # (lo, hi) float64 at compile time; read through ``root_box``
     render_tlas: object = None   # two-level scenes: the device-flattened structure rt_render walks
     _meshes: dict = None         # flat scenes: mesh name -> _DeviceMesh (device refit_mesh)
     _light_src: tuple = None     # (desc, material index, instances) the light table came from
+    _placements: list = None     # flat scenes: (mesh name or None, 3x4 matrix, local lo, hi) per instance
+    _root_dirty: bool = False
+    _render_gen: int = -1        # two-level scenes: Tlas.generation the render copy was made from
+    _render_bits: int = 30
+    _replicas: dict = None       # device -> (source version, render replica Scene), multi-GPU render_frame
+
+    @property
+    def root_box(self):
+        """World AABB of the scene (the reference's Scene.tlas.root_box, read live: scene.py:45-48).
+
+        Flat scenes recompute it after ``refit_mesh`` from the refitted meshes' device bounds
+        (Blas.refit + refresh_instance_bounds semantics, accel.py:263-283, 477-497); two-level
+        scenes read their Tlas, which ``refresh_instance_bounds`` keeps current."""
+        if self.render_tlas is not None:
+            return self.tlas.root_box
+        if self._root_dirty:
+            wlo, whi = [], []
+            for name, m, lo, hi in self._placements:
+                if name is not None:
+                    b = self._meshes[name].device_bounds()
+                    lo, hi = b[:3], b[3:]
+                lo, hi = _corner_box(lo, hi, m)
+                wlo.append(lo)
+                whi.append(hi)
+            self.root_box_ = (np.min(np.array(wlo), axis=0), np.max(np.array(whi), axis=0))
+            self._root_dirty = False
+        return self.root_box_
 
     def diagonal(self) -> float:
-        d = self.root_box[1] - self.root_box[0]
+        lo, hi = self.root_box
+        d = hi - lo
         return math.sqrt(float(d @ d))
+
+    def replica(self, device):
+        """This scene's render copy on GPU ``device`` (multi-GPU render_frame): the built flat
+        structure cloned device to device, re-cloned after any rebuild or refit."""
+        import dataclasses
+        self.sync_render()
+        src = self.render_tlas if self.render_tlas is not None else self.tlas
+        if src.ctx.device == int(device):
+            return self
+        if self._replicas is None:
+            self._replicas = {}
+        hit = self._replicas.get(int(device))
+        if hit is not None and hit[0] == (id(src), src.version):
+            return hit[1]
+        rep = dataclasses.replace(self, tlas=src.clone(int(device)), render_tlas=None, _replicas=None,
+                                  root_box_=self.root_box, _root_dirty=False, _meshes=None)
+        self._replicas[int(device)] = ((id(src), src.version), rep)
+        return rep
+
+    def sync_render(self):
+        """Two-level scenes: bring the device-flattened render copy up to date after
+        ``Tlas.refresh_instance_bounds`` (the reference re-flattens its bundle there,
+        accel.py:497).  The query path reads the two-level structure directly."""
+        if self.render_tlas is None or self._render_gen == self.tlas.generation:
+            return
+        self.tlas.flatten(self.inst_material.astype(np.int32), self.mat_color, self.mat_emissive, self.registry,
+                          self._render_bits, into=self.render_tlas)
+        self._render_gen = self.tlas.generation
 
     def refit_mesh(self, name, vertices, bits=None):
         """Blas.refit(vertices) (accel.py:263-283) for every instance of mesh `name` of a flat
@@ -218,6 +286,7 @@ class Scene:
         tl = self.tlas
         check(lib().rt_scene_refit_mesh(tl.ctx.handle, tl.handle, mr.handle, mr.nv, ptr(V), 1 if f32 else 0))
         tl._tris = None                          # the host copy is read back on demand
+        self._root_dirty = True                  # the mesh bounds were re-reduced on the device
         desc, mat_index, inst_list = self._light_src
         if any(desc.materials[d.material].has_emission for d, _ in inst_list if d.mesh == name):
             # emissive instances of this mesh: the light table follows the new vertices
@@ -246,6 +315,12 @@ class _DeviceMesh:
         h = ctypes.c_void_p()
         check(lib().rt_mesh_upload(ctx.handle, self.nv, ptr(V), self.nf, ptr(F), ptr(self.bounds), ctypes.byref(h)))
         self.handle = h
+
+    def device_bounds(self):
+        """float64 root box of the mesh's current vertices (re-reduced on the device by each
+        refit; reading it synchronises)."""
+        check(lib().rt_mesh_info(self.handle, None, None, ptr(self.bounds)))
+        return self.bounds
 
     def __del__(self):
         try:
@@ -363,12 +438,12 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
             cs.mask = int(sph.mask)
             cs.row[:] = [float(x) for x in row]
             sph_rows.append(row)
-            sph_boxes.append((lo, hi, inv))
+            sph_boxes.append((lo, hi, inv, c - r, c + r, m))
 
     # instances (Instance + Tlas frames, accel.py:339-346, 451-472)
     n_inst = len(desc.instances)
     srcs = (_native.InstanceSrc * max(n_inst, 1))()
-    inst_material, inst_list, inverses = [], [], []
+    inst_material, inst_list, inverses, placements = [], [], [], []
     wlo, whi = [], []
     for i, decl in enumerate(desc.instances):
         dm = dmeshes[decl.mesh]
@@ -379,6 +454,7 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
             raise BuildError(f"instance {i} frame is not invertible") from exc
         inverses.append(inv)
         inst_list.append((decl, m))
+        placements.append((decl.mesh, m, None, None))
         lo, hi = _corner_box(dm.bounds[:3], dm.bounds[3:], m)
         wlo.append(lo)
         whi.append(hi)
@@ -391,7 +467,8 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
         src.matrix[:] = [float(x) for x in m.reshape(12)]
         src.inverse[:] = [float(x) for x in inv.reshape(12)]
     for k, sph in enumerate(desc.spheres or ()):
-        lo, hi, inv = sph_boxes[k]
+        lo, hi, inv, llo, lhi, m = sph_boxes[k]
+        placements.append((None, m, llo, lhi))
         wlo.append(lo)
         whi.append(hi)
         inverses.append(inv)
@@ -421,7 +498,8 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
                inst_material=np.array(inst_material, np.int64), lights=lights,
                sky=np.ascontiguousarray(desc.sky, np.float64), background=np.ascontiguousarray(desc.background,
                                                                                                np.float64),
-               root_box=(root_lo, root_hi))
+               root_box_=(root_lo, root_hi))
+    sc._placements = placements
     used = {d.mesh for d in desc.instances}
     sc._meshes = {name: dm for name, dm in dmeshes.items() if name in used}
     sc._light_src = (desc, mat_index, inst_list)
@@ -473,5 +551,5 @@ def _compile_two_level(desc, quality, device):
     return Scene(camera=desc.camera, tlas=tlas, registry=registry, mat_color=mat_color, mat_emissive=mat_emissive,
                  inst_material=np.array(inst_material, np.int64), lights=lights,
                  sky=np.ascontiguousarray(desc.sky, np.float64),
-                 background=np.ascontiguousarray(desc.background, np.float64), root_box=tlas.root_box,
-                 render_tlas=flat)
+                 background=np.ascontiguousarray(desc.background, np.float64), root_box_=tlas.root_box,
+                 render_tlas=flat, _render_gen=tlas.generation, _render_bits=QUALITIES[quality])

@@ -227,6 +227,7 @@ class Tlas:
             if not (0 <= inst.blas_id < len(self.blases)):
                 raise BuildError(f"instance {i} references unknown blas {inst.blas_id}")
         self.ctx = self.blases[self.instances[0].blas_id].ctx
+        self.generation = 0          # bumped by refresh_instance_bounds (render copies follow it)
         inv, boxes = self._frames()
         handles = (ctypes.c_void_p * len(self.instances))(*[self.blases[i.blas_id].handle.value
                                                             for i in self.instances])
@@ -278,6 +279,7 @@ class Tlas:
         inv, boxes = self._frames()
         check(lib().rt_tlas_update(self.ctx.handle, self.handle, ptr(inv), ptr(boxes)))
         self._versions = [b.version for b in self.blases]
+        self.generation += 1
 
     # -- registry binding (accel.py:1002-1008 _dispatch_for) --------------------
     def _bind(self, registry, ray_type):

@@ -1,4 +1,5 @@
-"""world_size-2 gloo tests of the multi-GPU split + reduce (CPU; the oracle stands in for the GPU renderer)."""
+"""world_size-2/3 gloo tests of the multi-GPU split + exchange (CPU; the oracle stands in for
+the GPU renderer, torch.distributed point-to-point for librt's NCCL band gather)."""
 
 import os
 import socket
@@ -49,19 +50,19 @@ def _worker(rank, world, port, mode, q):
         from paper_2603_00292_b200 import scenes
         sc = oracle.scene_from_description(scenes.cornell_description())
         acc = torch.zeros((H * W, 4), dtype=torch.float32)
-        rays, acc = D.render_split(_oracle_render_fn(sc), acc, mode, SPP)
+        rays, acc = D.render_split(_oracle_render_fn(sc), acc, mode, SPP, width=W, height=H)
         if rank == 0:
             q.put((rays, acc.numpy().copy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["samples", "tiles"])
-def test_split_and_reduce_world2(oracle_mod, mode):
+@pytest.mark.parametrize("mode,world", [("samples", 2), ("tiles", 2), ("tiles", 3)])
+def test_split_and_exchange(oracle_mod, mode, world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mode, q)) for r in range(world)]
     for p in procs:
         p.start()
     rays, acc = q.get(timeout=120)
@@ -74,6 +75,8 @@ def test_split_and_reduce_world2(oracle_mod, mode):
     assert rays == full_rays
     assert np.allclose(acc.reshape(H, W, 4), full, rtol=1e-5, atol=1e-5)
     assert np.all(acc[:, 3] == SPP)       # every pixel got every sample exactly once
+    if mode == "tiles":                   # each pixel rendered on one rank: the 1-GPU values exactly
+        assert np.array_equal(acc.reshape(H, W, 4), full.astype(np.float32))
 
 
 def test_slices_and_bands_partition():

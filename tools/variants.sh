@@ -10,7 +10,7 @@ while [ $# -ge 2 ]; do
   name=$1; defs=$2; shift 2
   out=variants/$name; mkdir -p $out
   pids=()
-  for f in capi lbvh trace render tlas multi; do
+  for f in capi mesh lbvh trace render tlas multi; do
     /usr/local/cuda/bin/nvcc $FLAGS $defs -c $CS/$f.cu -o $out/$f.o & pids+=($!)
   done
   for p in "${pids[@]}"; do wait $p; done
