@@ -4,6 +4,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <thread>
 #include <vector>
 
 #include "hostio.cuh"
@@ -22,6 +23,53 @@ size_t rt_sort_scratch_words(int64_t n);
 void rt_render_release(rt_scene* s);
 
 
+
+// Host -> device copy of a caller's array.  Pinned (page-locked) sources go as one async
+// DMA.  Large pageable ones (numpy arrays: compile_scene's float64 vertices / int64 faces)
+// are staged: host threads copy 16-MB chunks into two pinned buffers of the context while
+// the copy engine moves the previous chunk (the driver's own pageable path stages with one
+// thread: ~11 GB/s measured for the 10M soup's 960 MB).  Returns after the source may be
+// reused (the last chunk is in a pinned buffer or on the device).
+int rt_h2d(rt_ctx* c, void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return RT_OK;
+    cudaPointerAttributes a;
+    const bool pinned = cudaPointerGetAttributes(&a, src) == cudaSuccess && a.type == cudaMemoryTypeHost;
+    cudaGetLastError();                       // (unregistered pointers may set a sticky-free error)
+    constexpr size_t CHUNK = 16u << 20;
+    if (pinned || bytes <= 2 * CHUNK) {
+        RT_CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+        return RT_OK;
+    }
+    if (!c->h_stage) {
+        RT_CUDA_TRY(cudaHostAlloc(&c->h_stage, 2 * CHUNK, cudaHostAllocDefault));
+        c->h_stage_bytes = 2 * CHUNK;
+        RT_CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[0], cudaEventDisableTiming));
+        RT_CUDA_TRY(cudaEventCreateWithFlags(&c->stage_ev[1], cudaEventDisableTiming));
+    }
+    const unsigned hw = std::thread::hardware_concurrency();
+    const int nt = (int)std::max(1u, std::min(8u, hw / 2));
+    const char* s8 = static_cast<const char*>(src);
+    char* d8 = static_cast<char*>(dst);
+    for (size_t off = 0, k = 0; off < bytes; off += CHUNK, ++k) {
+        const size_t len = std::min(CHUNK, bytes - off);
+        char* buf = static_cast<char*>(c->h_stage) + (k & 1) * CHUNK;
+        if (k >= 2) RT_CUDA_TRY(cudaEventSynchronize(c->stage_ev[k & 1]));   // buffer free again
+        const size_t per = (len + nt - 1) / nt;
+        std::vector<std::thread> th;
+        for (int t = 1; t < nt; ++t) {
+            const size_t a0 = std::min(len, t * per), a1 = std::min(len, (t + 1) * per);
+            if (a1 > a0) th.emplace_back([=] { memcpy(buf + a0, s8 + off + a0, a1 - a0); });
+        }
+        memcpy(buf, s8 + off, std::min(len, per));
+        for (auto& x : th) x.join();
+        RT_CUDA_TRY(cudaMemcpyAsync(d8 + off, buf, len, cudaMemcpyHostToDevice, c->stream));
+        RT_CUDA_TRY(cudaEventRecord(c->stage_ev[k & 1], c->stream));
+    }
+    // the staging buffers are reused by the next call: their last copies must be done
+    RT_CUDA_TRY(cudaEventSynchronize(c->stage_ev[0]));
+    RT_CUDA_TRY(cudaEventSynchronize(c->stage_ev[1]));
+    return RT_OK;
+}
 
 int rt_check_device_error(rt_ctx* ctx) {
     int e = 0;
@@ -91,7 +139,11 @@ void rt_ctx_destroy(rt_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->h_stage) {
+        cudaFreeHost(c->h_stage);
+        cudaEventDestroy(c->stage_ev[0]);
+        cudaEventDestroy(c->stage_ev[1]);
+    }
     if (c->d_stage) cudaFree(c->d_stage);
     if (c->d_io) cudaFree(c->d_io);
     if (c->io_in) {
@@ -148,7 +200,7 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
             return RT_ENOMEM;                                                   \
         }                                                                       \
     } while (0)
-    ALLOC(s->tris, sizeof(float) * 9 * n);
+    ALLOC(s->tris, sizeof(float) * 9 * n + 64);     // + the last rows' 64-B gather window (lbvh.cu)
     ALLOC(s->tri_attr, sizeof(float4) * n);
     ALLOC(s->tri_inst, sizeof(int32_t) * n);
     ALLOC(s->tri_prim, sizeof(int32_t) * n);
@@ -171,6 +223,11 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
     ALLOC(s->emit_items, 48 * (2 * n + 512));      // EmitNode segments of EMIT_T per emit block
     ALLOC(s->seg_count, sizeof(unsigned int) * (n / 64 + 2));   // one count per emit block (EMIT_T >= 64)
 #undef ALLOC
+    if (reinterpret_cast<uintptr_t>(s->tris) & 31) {     // the build's 256-bit row gathers
+        rt_set_error("triangle rows are not 32-B aligned");
+        rt_scene_destroy(s);
+        return RT_ECUDA;
+    }
     {
         cudaError_t _e = cudaStreamSynchronize(c->stream);   // the blocks are usable from any stream now
         if (_e != cudaSuccess) {
@@ -236,6 +293,9 @@ int rt_scene_create(rt_ctx* c, int64_t n, const float* tris, const float* normal
         return fail(e);
     rc = rt_scene_set_materials(c, s, mat_color, mat_emissive);
     if (rc) { rt_scene_destroy(s); return rc; }
+    s->mask_uniform = 1;
+    s->mask_value = tri_mask[0];
+    for (int64_t i = 1; i < n && s->mask_uniform; ++i) s->mask_uniform = tri_mask[i] == tri_mask[0];
     *out = s;
     return RT_OK;
 }
@@ -304,6 +364,8 @@ int rt_scene_clone(rt_ctx* src, rt_scene* s, rt_ctx* dst, rt_scene** out) {
     }
     d->built = s->built;
     d->bits = s->bits;
+    d->mask_uniform = s->mask_uniform;
+    d->mask_value = s->mask_value;
     d->custom = s->custom;
     d->geom_type = s->geom_type;
     d->data_offset = s->data_offset;

@@ -217,6 +217,7 @@ constexpr int EMIT_T = EMIT_TILE;
 template <typename K>
 __global__ void __launch_bounds__(EMIT_T, EMIT_MINB) lbvh_emit_kernel(const K* __restrict__ keys, const uint32_t* __restrict__ order,
                                                            const float* __restrict__ tris, const uint32_t* __restrict__ mask,
+                                                           uint32_t umask,
                                                            int64_t n, int2* __restrict__ child,
                                                            float4* __restrict__ tri_sorted, float4* __restrict__ nodes,
                                                            float4* __restrict__ bvh4, EmitNode* __restrict__ items,
@@ -242,10 +243,10 @@ __global__ void __launch_bounds__(EMIT_T, EMIT_MINB) lbvh_emit_kernel(const K* _
     if (i < E) {
         const uint32_t id = order[i];
         float t[9];
-        load_tri(tris, id, t);
+        load_tri_gather(tris, id, t);
         tri_box(t, N.lo, N.hi);
         tri_sorted[3 * i + 0] = make_float4(t[0], t[1], t[2], __int_as_float((int)id));
-        tri_sorted[3 * i + 1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask[id]));
+        tri_sorted[3 * i + 1] = make_float4(t[3], t[4], t[5], __uint_as_float(mask ? mask[id] : umask));
         tri_sorted[3 * i + 2] = make_float4(t[6], t[7], t[8], 0.0f);
         N.l = N.r = (int)i;
         N.h = 0;

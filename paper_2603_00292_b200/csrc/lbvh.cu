@@ -96,6 +96,39 @@ __device__ __forceinline__ void load_tri(const float* tris, int64_t i, float t[9
     for (int k = 0; k < 9; ++k) t[k] = __ldg(p + k);
 }
 
+// Gather of one 36-B row by two 256-bit loads of the 32-B aligned 64-B window that
+// contains it (the row never straddles more than two sectors: 36 i mod 32 <= 28), then a
+// 3-stage barrel shift by the row's offset in the window (i mod 8 floats).  Nine scalar
+// loads of the same row issued back to back each go to L2 while the first miss is in
+// flight (ncu, 10M emit: 9.5 L2 read sectors per leaf); this asks for exactly two.
+// (The scene's row array carries 64 B of slack for the last rows' windows.)
+#ifndef RT_WIDE_GATHER
+#define RT_WIDE_GATHER 1
+#endif
+__device__ __forceinline__ void ldg256(const float* p, float w[8]) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(w[0]), "=f"(w[1]), "=f"(w[2]), "=f"(w[3]), "=f"(w[4]), "=f"(w[5]), "=f"(w[6]), "=f"(w[7])
+        : "l"(p));
+}
+__device__ __forceinline__ void load_tri_gather(const float* tris, int64_t i, float t[9]) {
+#if RT_WIDE_GATHER
+    const int64_t e = 9 * i;
+    const int o = (int)(e & 7);                 // == i & 7
+    float w[16];
+    ldg256(tris + (e - o), w);
+    ldg256(tris + (e - o) + 8, w + 8);
+    float a[12], b[10];
+#pragma unroll
+    for (int j = 0; j < 12; ++j) a[j] = (o & 4) ? w[j + 4] : w[j];
+#pragma unroll
+    for (int j = 0; j < 10; ++j) b[j] = (o & 2) ? a[j + 2] : a[j];
+#pragma unroll
+    for (int j = 0; j < 9; ++j) t[j] = (o & 1) ? b[j + 1] : b[j];
+#else
+    load_tri(tris, i, t);
+#endif
+}
+
 // Block-cooperative staging of TRI_CHUNK consecutive triangles (36 B each) into
 // shared memory with 16-B coalesced loads; the per-triangle loads of a direct
 // (n, 9) walk are 36-B strided and waste most of each sector request.
@@ -565,7 +598,8 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     EmitNode* items = (EmitNode*)s->emit_items;
     const int64_t n_blocks = (n + EMIT_T - 1) / EMIT_T;
     RT_CUDA_TRY(launch_pdl(lbvh_emit_kernel<K>, (unsigned)n_blocks, EMIT_T, st, (const K*)kin, (const uint32_t*)vin,
-                           (const float*)s->tris, (const uint32_t*)s->tri_mask, n, s->child, s->tri_sorted, s->nodes,
+                           (const float*)s->tris, s->mask_uniform ? (const uint32_t*)nullptr : (const uint32_t*)s->tri_mask,
+                           s->mask_value, n, s->child, s->tri_sorted, s->nodes,
                            s->bvh4, items, s->seg_count, (int*)s->flags, s->leaf_box));
     RT_CUDA_TRY(launch_pdl(lbvh_emit_global_kernel<K>, (unsigned)((n_blocks * 32 + 127) / 128), 128u, st,
                            (const K*)kin, n, s->child, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box,

@@ -400,8 +400,9 @@ int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, 
     }
     RT_CUDA_TRY(cudaSetDevice(c->device));
     const size_t vbytes = (vertices_f32 ? sizeof(float) : sizeof(double)) * 3 * m->nv;
-    RT_CUDA_TRY(cudaMemcpyAsync(m->verts, vertices, vbytes, cudaMemcpyHostToDevice, c->stream));
-    int rc = launch_mesh(c, s, m, vertices_f32 != 0, false);
+    int rc = rt_h2d(c, m->verts, vertices, vbytes);
+    if (rc) return rc;
+    rc = launch_mesh(c, s, m, vertices_f32 != 0, false);
     if (rc) return rc;
     if (m->d_red) {       // the mesh's new root box (read back only when asked, rt_mesh_info)
         red_init_kernel<<<1, 32, 0, c->stream>>>(m->d_red);
@@ -444,9 +445,9 @@ int rt_mesh_upload(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_
     if (e == cudaSuccess) e = rt_alloc((void**)&m->verts, sizeof(double) * 3 * (n_vertices > 0 ? n_vertices : 1), st, false);
     if (e == cudaSuccess) e = cudaMallocAsync(&f64, sizeof(int64_t) * 3 * n_faces, st);
     if (e == cudaSuccess) e = rt_alloc((void**)&red, sizeof(unsigned long long) * 8, st, false);
-    if (e == cudaSuccess && n_vertices > 0)
-        e = cudaMemcpyAsync(m->verts, vertices, sizeof(double) * 3 * n_vertices, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(f64, faces, sizeof(int64_t) * 3 * n_faces, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && n_vertices > 0 && rt_h2d(c, m->verts, vertices, sizeof(double) * 3 * n_vertices))
+        e = cudaErrorUnknown;
+    if (e == cudaSuccess && rt_h2d(c, f64, faces, sizeof(int64_t) * 3 * n_faces)) e = cudaErrorUnknown;
     unsigned long long init[8] = {ULLONG_MAX, ULLONG_MAX, ULLONG_MAX, 0, 0, 0, ULLONG_MAX, ULLONG_MAX};
     if (e == cudaSuccess) e = cudaMemcpyAsync(red, init, sizeof init, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
@@ -612,6 +613,13 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
         rt_set_error("rt_scene_compile: %s", cudaGetErrorString(e));
         return fail(RT_ECUDA);
     }
+    // one instance mask for every primitive (the usual case): the build writes it instead of
+    // gathering it per leaf
+    const uint32_t m0 = n_inst ? inst[0].mask : custom[0].mask;
+    s->mask_uniform = 1;
+    s->mask_value = m0;
+    for (int32_t i = 0; i < n_inst; ++i) s->mask_uniform &= inst[i].mask == m0 && meshes[inst[i].mesh]->nf > 0;
+    for (int32_t k = 0; k < n_custom; ++k) s->mask_uniform &= custom[k].mask == m0;
     *out = s;
     return RT_OK;
 }

@@ -23,8 +23,9 @@ struct rt_ctx {
     cudaEvent_t prof[8];           // stage events for rt_bvh_build_profiled
     int profiling;
     // pinned staging + device scratch for rt_closest_hit_host
-    void* h_stage;
+    void* h_stage;                 // rt_h2d: two pinned 16-MB chunks for pageable sources
     size_t h_stage_bytes;
+    cudaEvent_t stage_ev[2];
     void* d_stage;
     size_t d_stage_bytes;
     unsigned int* d_counter;       // persistent-kernel work counters (64 slots)
@@ -45,6 +46,8 @@ struct rt_scene {
     int n_mat;
     int device;
     cudaStream_t stream;  // storage is stream-ordered pool memory, freed on this stream
+    int mask_uniform;     // every primitive has instance mask `mask_value` (the build skips the gather)
+    uint32_t mask_value;
     // inputs (resident)
     float* tris;          // (n, 9) world vertices
     float4* tri_attr;     // (n) normal.xyz, material id bits   (F9 normals)
@@ -127,6 +130,10 @@ inline cudaError_t rt_alloc(void** p, size_t bytes, cudaStream_t st, bool sync =
 inline void rt_free(void* p, cudaStream_t st) {
     if (p) cudaFreeAsync(p, st);
 }
+
+// host -> device copy on the context stream; large pageable sources are staged through
+// pinned chunks by several host threads (capi.cu)
+int rt_h2d(rt_ctx* c, void* dst, const void* src, size_t bytes);
 
 // reads and clears the device error flag (synchronises the context stream)
 int rt_check_device_error(rt_ctx* ctx);

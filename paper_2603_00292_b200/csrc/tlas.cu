@@ -659,6 +659,9 @@ int rt_tlas_flatten(rt_ctx* c, rt_tlas* T, const double* mat12, const int32_t* i
         rt_set_error("flatten: %s", cudaGetErrorString(e));
         return bail(RT_ECUDA);
     }
+    s->mask_uniform = 1;
+    s->mask_value = T->hinst[0].mask;
+    for (int i = 1; i < T->n_inst; ++i) s->mask_uniform &= T->hinst[i].mask == s->mask_value;
     int rc = rt_scene_set_materials(c, s, mat_color, mat_emissive);
     if (!rc) rc = rt_scene_set_spheres(c, s, n_custom, n_custom ? custom_rows16 : nullptr);
     if (!rc) rc = rt_bvh_build(c, s, bits, nullptr);
