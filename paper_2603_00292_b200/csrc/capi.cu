@@ -342,7 +342,6 @@ int rt_scene_clone(rt_ctx* src, rt_scene* s, rt_ctx* dst, rt_scene** out) {
     if (!e) e = cp(d->nodes, s->nodes, sizeof(float4) * 4);
     if (!e) e = cp(d->tri_sorted, s->tri_sorted, sizeof(float4) * 3 * n);
     if (!e) e = cp(d->bvh4, s->bvh4, sizeof(float4) * 8 * ni);
-    if (!e) e = cp(d->child, s->child, sizeof(int2) * ni);
     if (!e) e = cp(d->vals_a, s->vals_a, sizeof(uint32_t) * n);
     if (!e) e = cp(d->keys_a, s->keys_a, (s->bits == 63 ? 8 : 4) * (size_t)n);
     if (!e) e = cp(d->cbounds, s->cbounds, sizeof(float) * 16);
@@ -469,13 +468,54 @@ int rt_bvh_download(rt_ctx* c, rt_scene* s, uint64_t* sorted_keys, uint32_t* ord
     if (sorted_keys && (rc = keys_to_u64(s->keys_a, sorted_keys))) return rc;
     if (order) RT_CUDA_TRY(cudaMemcpy(order, s->vals_a, 4 * n, cudaMemcpyDeviceToHost));
     if (child || parent || boxes || heights) {
-        // the build writes only child ids + the BVH4 halves + the root record; the
-        // binary view is derived here: node P's child boxes are the half its parent Q
-        // wrote into BVH4[split of Q] (side = P is Q's right child), the root's are in
-        // the root record; heights bottom-up; parents by inverting child
+        // the build writes only the BVH4 halves + the root record; the binary view is
+        // derived here.  Topology: the half a node W writes into its parent P's entry
+        // (entry index = P's split, side = W's side) records W's own split (.w of its first
+        // hi vector), so from the root's split (root record) every node's split follows,
+        // hence every range [l, r] -> children [l, g], [g + 1, r] and the Karras numbers
+        // (a left child is numbered by its right end, a right child by its left end, a
+        // leaf k by ~k).  Boxes: node P's child boxes are the half P wrote into its parent
+        // Q's entry (the root's are in the root record).  Heights bottom-up; parents by
+        // inverting child.
         const int64_t m = n - 1;
+        std::vector<float4> b4(8 * m), root(4);
+        RT_CUDA_TRY(cudaMemcpy(b4.data(), s->bvh4, sizeof(float4) * 8 * m, cudaMemcpyDeviceToHost));
+        RT_CUDA_TRY(cudaMemcpy(root.data(), s->nodes, sizeof(float4) * 4, cudaMemcpyDeviceToHost));
         std::vector<int2> ch(m);
-        RT_CUDA_TRY(cudaMemcpy(ch.data(), s->child, 8 * m, cudaMemcpyDeviceToHost));
+        {
+            struct Item { int64_t P, l, r, g; };
+            std::vector<Item> st;
+            int g0;
+            memcpy(&g0, &root[3].w, 4);
+            st.push_back({0, 0, n - 1, g0});
+            while (!st.empty()) {
+                const Item it = st.back();
+                st.pop_back();
+                if (it.g < it.l || it.g >= it.r || it.g >= m) {
+                    rt_set_error("corrupt BVH: split %lld outside node range [%lld, %lld]", (long long)it.g,
+                                 (long long)it.l, (long long)it.r);
+                    return RT_ECUDA;
+                }
+                int2 c;
+                if (it.l == it.g) {
+                    c.x = ~(int)it.l;
+                } else {
+                    c.x = (int)it.g;
+                    int gl;
+                    memcpy(&gl, &b4[8 * it.g + 1].w, 4);
+                    st.push_back({it.g, it.l, it.g, gl});
+                }
+                if (it.g + 1 == it.r) {
+                    c.y = ~(int)it.r;
+                } else {
+                    c.y = (int)(it.g + 1);
+                    int gr;
+                    memcpy(&gr, &b4[8 * it.g + 5].w, 4);
+                    st.push_back({it.g + 1, it.g + 1, it.r, gr});
+                }
+                ch[it.P] = c;
+            }
+        }
         if (child) memcpy(child, ch.data(), 8 * m);
         std::vector<int32_t> par(2 * n - 1, -1);
         for (int64_t p = 0; p < m; ++p) {
@@ -485,9 +525,6 @@ int rt_bvh_download(rt_ctx* c, rt_scene* s, uint64_t* sorted_keys, uint32_t* ord
         }
         if (parent) memcpy(parent, par.data(), 4 * (2 * n - 1));
         if (boxes) {
-            std::vector<float4> b4(8 * m), root(4);
-            RT_CUDA_TRY(cudaMemcpy(b4.data(), s->bvh4, sizeof(float4) * 8 * m, cudaMemcpyDeviceToHost));
-            RT_CUDA_TRY(cudaMemcpy(root.data(), s->nodes, sizeof(float4) * 4, cudaMemcpyDeviceToHost));
             for (int64_t p = 0; p < m; ++p) {
                 float* b = boxes + 12 * p;
                 if (p == 0) {

@@ -41,21 +41,31 @@ struct EmitNode {
 #ifndef RT_STG256
 #define RT_STG256 1
 #endif
+// 1: also write the Karras child ids per internal node (8 scattered bytes each); 0: the
+// download derives them from the BVH4 halves (see bvh4_write_half)
+#ifndef RT_EMIT_CHILD
+#define RT_EMIT_CHILD 0
+#endif
+// The half also records its writer's own BVH4 id (`self`: the writer's split, or ~leaf)
+// in the spare .w of its first hi vector: with it rt_bvh_download rebuilds the binary
+// topology (each node's children and Karras numbers) from the BVH4 view alone, so the
+// build writes no separate child array.
 __device__ __forceinline__ void bvh4_write_half(float4* __restrict__ bvh4, int pgamma, int side, const float a_lo[3],
                                                 const float a_hi[3], int a_id, const float b_lo[3],
-                                                const float b_hi[3], int b_id) {
+                                                const float b_hi[3], int b_id, int self) {
     float4* q = bvh4 + 8 * (int64_t)pgamma + 4 * side;
 #if RT_STG256
     // two 256-bit stores (sm_100 STG.E.256) per 64-B half; the half is 64-B aligned
     asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(q), "f"(a_lo[0]), "f"(a_lo[1]),
-                 "f"(a_lo[2]), "f"(__int_as_float(a_id)), "f"(a_hi[0]), "f"(a_hi[1]), "f"(a_hi[2]), "f"(0.0f)
+                 "f"(a_lo[2]), "f"(__int_as_float(a_id)), "f"(a_hi[0]), "f"(a_hi[1]), "f"(a_hi[2]),
+                 "f"(__int_as_float(self))
                  : "memory");
     asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(q + 2), "f"(b_lo[0]), "f"(b_lo[1]),
                  "f"(b_lo[2]), "f"(__int_as_float(b_id)), "f"(b_hi[0]), "f"(b_hi[1]), "f"(b_hi[2]), "f"(0.0f)
                  : "memory");
 #else
     q[0] = make_float4(a_lo[0], a_lo[1], a_lo[2], __int_as_float(a_id));
-    q[1] = make_float4(a_hi[0], a_hi[1], a_hi[2], 0.0f);
+    q[1] = make_float4(a_hi[0], a_hi[1], a_hi[2], __int_as_float(self));
     q[2] = make_float4(b_lo[0], b_lo[1], b_lo[2], __int_as_float(b_id));
     q[3] = make_float4(b_hi[0], b_hi[1], b_hi[2], 0.0f);
 #endif
@@ -68,7 +78,7 @@ __device__ __forceinline__ void bvh4_write_leaf(float4* __restrict__ bvh4, const
     // empty slot: lo = hi = +inf on every axis.  (lo = +inf, hi = -inf would be an
     // INFINITE box for the min/max slab test, which orders each slab's ends.)
     const float elo[3] = {INFINITY, INFINITY, INFINITY}, ehi[3] = {INFINITY, INFINITY, INFINITY};
-    bvh4_write_half(bvh4, left ? N.r : N.l - 1, left ? 0 : 1, N.lo, N.hi, ~N.l, elo, ehi, ~0);
+    bvh4_write_half(bvh4, left ? N.r : N.l - 1, left ? 0 : 1, N.lo, N.hi, ~N.l, elo, ehi, ~0, ~N.l);
 }
 
 // Emit the parent of N (N is the left child iff `left`) whose sibling brought
@@ -94,20 +104,24 @@ __device__ __forceinline__ bool emit_parent(int64_t n, int2* __restrict__ child,
     const int gr = (pr == gamma + 1) ? ~(gamma + 1) : (left ? gs : N.g);
     const bool root = (pl == 0 && pr == n - 1);
     const bool pleft = pdr > pdl;
+#if RT_EMIT_CHILD
     const int P = root ? 0 : (pleft ? pr : pl);
+#endif
     N.h = 1 + (N.h > hs ? N.h : hs);
     // Only the topology (child ids, 8 B) and the BVH4 half are written per node: the
     // binary node's child boxes ARE that half, so parent pointers, per-node boxes and
     // heights are derived from child + bvh4 by rt_bvh_download (parity only).  The
     // root alone writes its 64-B record (child boxes, ids, tree height, BVH4 root).
+#if RT_EMIT_CHILD
     child[P] = make_int2(cl, cr);
+#endif
     if (root) {
         nodes[0] = make_float4(llo[0], lhi[0], llo[1], lhi[1]);
         nodes[1] = make_float4(rlo[0], rhi[0], rlo[1], rhi[1]);
         nodes[2] = make_float4(llo[2], lhi[2], rlo[2], rhi[2]);
         nodes[3] = make_float4(__int_as_float(cl), __int_as_float(cr), __int_as_float(N.h), __int_as_float(gamma));
     } else {
-        bvh4_write_half(bvh4, pleft ? pr : pl - 1, pleft ? 0 : 1, llo, lhi, gl, rlo, rhi, gr);
+        bvh4_write_half(bvh4, pleft ? pr : pl - 1, pleft ? 0 : 1, llo, lhi, gl, rlo, rhi, gr, gamma);
     }
 #pragma unroll
     for (int a = 0; a < 3; ++a) { N.lo[a] = sel_min(llo[a], rlo[a]); N.hi[a] = sel_max(lhi[a], rhi[a]); }
@@ -202,8 +216,8 @@ __global__ void bvh4_single_leaf_kernel(const float4* __restrict__ nodes, float4
     const float4 a0 = nodes[0], a2 = nodes[2];
     const float lo[3] = {a0.x, a0.z, a2.x}, hi[3] = {a0.y, a0.w, a2.y};
     const float e[3] = {INFINITY, INFINITY, INFINITY};
-    bvh4_write_half(bvh4, 0, 0, lo, hi, ~0, e, e, ~0);
-    bvh4_write_half(bvh4, 0, 1, e, e, ~0, e, e, ~0);
+    bvh4_write_half(bvh4, 0, 0, lo, hi, ~0, e, e, ~0, ~0);
+    bvh4_write_half(bvh4, 0, 1, e, e, ~0, e, e, ~0, ~0);
 }
 
 #ifndef EMIT_TILE
