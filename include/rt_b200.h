@@ -278,6 +278,9 @@ int rt_comm_reduce_accum(rt_comm* comm, rt_ctx* ctx, float* accum, int64_t npix)
  * rows <- compact) on one device, without NCCL (tests); rows_out: rank g's row count */
 int rt_bands_copy(rt_ctx* ctx, float* accum, float* compact, int32_t width, int32_t height, int32_t g, int32_t G,
                   int32_t unpack, int64_t* rows_out);
+/* the first n raw PCG32 outputs of the (seed, pixel, sample) stream the kernels draw from
+ * (sampling.py:38-79 _stream_for / _pcg_next; known-answer tests) */
+int rt_stream_draws(rt_ctx* ctx, uint64_t seed, uint64_t pixel, uint64_t sample, int32_t n, uint32_t* out);
 /* primary rays of sample s for every pixel of the frame (parity tests): (W*H, 8) like rt_trace_closest */
 int rt_raygen(rt_ctx* ctx, const rt_render_params* p, int32_t sample, float* rays);
 

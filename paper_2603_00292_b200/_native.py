@@ -132,6 +132,7 @@ def lib():
             "rt_scene_get_ids": [vp, vp, vp, vp, vp, vp],
             "rt_scene_get_geometry": [vp, vp, vp, vp, vp, vp],
             "rt_scene_clone": [vp, vp, vp, vp],
+            "rt_stream_draws": [vp, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, i32, vp],
             "rt_comm_unique_id": [vp],
             "rt_comm_create": [vp, i32, i32, vp, vp],
             "rt_comm_gather_bands": [vp, vp, vp, i32, i32],

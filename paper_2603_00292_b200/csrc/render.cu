@@ -36,6 +36,7 @@ struct FrameConst {
     int tiled, tiles_x;
     int band_stride, band_offset;   // interleaved tile-row bands (multi-GPU tile split)
     int64_t row0, row1, nunits;
+    int64_t mine_rows, perm_a;      // tile-row fetch order: local row lr -> (lr * perm_a) % mine_rows
 };
 
 // unit k -> pixel; false for the padding lanes of partial edge tiles
@@ -44,7 +45,12 @@ __device__ __forceinline__ bool unit_pixel(const FrameConst& F, int64_t k, int64
     int64_t t = k >> 5;
     int l = (int)(k & 31);
     int64_t x = (t % F.tiles_x) * 8 + (l & 7);
-    int64_t trow = (t / F.tiles_x) * F.band_stride + F.band_offset;
+    // tile rows in a low-discrepancy order (golden-ratio stride): the rows fetched last are a
+    // spread sample of the frame instead of its bottom band (on the config-2 sphere the
+    // bottom rows see the pole's fan of thin triangles, and a top-to-bottom order ended
+    // every frame on them: SM activity 60-100 % of the kernel, ncu)
+    const int64_t lr = ((t / F.tiles_x) * F.perm_a) % F.mine_rows;
+    int64_t trow = lr * F.band_stride + F.band_offset;
     int64_t y = F.row0 + trow * 4 + (l >> 3);
     pix = y * F.width + x;
     return x < F.width && y < F.row1;
@@ -523,6 +529,23 @@ FrameConst make_frame(const rt_render_params* p) {
     const int64_t trows = (F.row1 - F.row0 + 3) / 4;
     const int64_t mine = trows > F.band_offset ? (trows - F.band_offset + F.band_stride - 1) / F.band_stride : 0;
     F.nunits = F.tiled ? (int64_t)F.tiles_x * mine * 32 : F.npix;
+    F.mine_rows = mine > 0 ? mine : 1;
+    F.perm_a = 1;
+#ifndef RT_TILE_PERM
+#define RT_TILE_PERM 1
+#endif
+#if RT_TILE_PERM
+    if (mine > 2) {
+        // the integer nearest mine / phi that is coprime with mine (a bijection of the rows)
+        auto gcd = [](int64_t a, int64_t b) { while (b) { int64_t t = a % b; a = b; b = t; } return a; };
+        int64_t a = (int64_t)(0.6180339887498949 * (double)mine + 0.5);
+        for (int64_t d = 0; d < mine; ++d) {
+            if (a + d < mine && a + d > 0 && gcd(a + d, mine) == 1) { a = a + d; break; }
+            if (a - d > 0 && gcd(a - d, mine) == 1) { a = a - d; break; }
+        }
+        F.perm_a = a;
+    }
+#endif
     if (F.tiled && F.band_stride > 1) {   // real pixels of this band set (ray counting)
         F.npix = 0;
         for (int64_t r = F.band_offset; r < trows; r += F.band_stride) {
@@ -724,5 +747,34 @@ int rt_raygen_impl(rt_ctx* ctx, const rt_render_params* p, int sample, float* ra
     FrameConst F = make_frame(p);
     raygen_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(F, sample, reinterpret_cast<float4*>(rays));
     RT_CUDA_TRY(cudaGetLastError());
+    return RT_OK;
+}
+
+// ---- RNG stream known-answer hook (tests): the first n raw PCG32 outputs of the
+// (seed, pixel, sample) stream the kernels draw from (sampling.py:38-79, 124-127) ----
+namespace {
+__global__ void stream_draws_kernel(uint64_t seed, uint64_t pix, uint64_t s, int n, uint32_t* out) {
+    uint64_t state, inc;
+    rt_stream_for(seed, pix, s, state, inc);
+    for (int k = 0; k < n; ++k) out[k] = rt_pcg_next(state, inc);
+}
+}  // namespace
+
+extern "C" int rt_stream_draws(rt_ctx* c, uint64_t seed, uint64_t pixel, uint64_t sample, int32_t n,
+                               uint32_t* out) {
+    RT_CTX_LOCK(c);
+    RT_CHECK_ARG(out && n >= 0 && n <= 4096, "bad output buffer");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    uint32_t* d = nullptr;
+    RT_CUDA_TRY(rt_alloc((void**)&d, sizeof(uint32_t) * (n > 0 ? n : 1), c->stream, false));
+    stream_draws_kernel<<<1, 1, 0, c->stream>>>(seed, pixel, sample, n, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, c->stream);
+    rt_free(d, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e != cudaSuccess) {
+        rt_set_error("rt_stream_draws: %s", cudaGetErrorString(e));
+        return RT_ECUDA;
+    }
     return RT_OK;
 }

@@ -86,3 +86,33 @@ def test_multi_render_sample_split(native):
     r1 = render_into(reps[0], one, 96, 64, 8, "pt", seed=2, cfg=cfg)
     assert rays == r1
     assert torch.allclose(acc.cpu(), one.cpu(), rtol=1e-5, atol=1e-5)
+
+
+def test_comm_single_rank_roundtrip(native):
+    """librt's one-process-per-GPU communicator (rt_comm_*) end to end with one rank: unique
+    id through torch.distributed (gloo), ncclCommInitRank, the reduce (identity for one
+    rank) and the band gather (a no-op) on a rendered frame."""
+    import os
+    import socket
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        sc = compile_scene(scenes.cornell_description())
+        acc = torch.zeros((64 * 48, 4), dtype=torch.float32, device="cuda")
+        rays, acc = D.render_split(lambda a, samples, bands: render_into(sc, a, 64, 48, 2, "pt", seed=4,
+                                                                          samples=samples, bands=bands),
+                                   acc, "samples", 2)
+        ref = torch.zeros_like(acc)
+        render_into(sc, ref, 64, 48, 2, "pt", seed=4)
+        comm = D.NcclComm.get(sc.tlas.ctx)
+        comm.reduce(acc)
+        comm.gather_bands(acc, 64, 48)
+        torch.cuda.synchronize()
+        assert torch.equal(acc, ref)
+    finally:
+        dist.destroy_process_group()

@@ -195,3 +195,26 @@ def test_render_frame_pipelined_equals_single(native):
             a = render_frame(sc, 1280, 1000, 1, "eye", seed=4, bands=(world, g))
             b = render_frame(sc, 1280, 1000, 1, "eye", seed=4, bands=(world, g), return_stats=True)[0]
             assert np.array_equal(a.data, b.data)
+
+
+def test_device_rng_streams_match_reference_goldens(native):
+    """a13 directly: the device's per-(seed, pixel, sample) PCG32 streams (rt_stream_draws, the
+    generator every kernel draws from) against the reference's own uniforms
+    (tests/golden/pcg.npz, RandomStream.for_sample, sampling.py:38-79, 124-127) and the
+    SURVEY 8(c) known answers: u32 * 2^-32 equals the reference's float64 uniform exactly."""
+    import ctypes
+    from paper_2603_00292_b200 import _native
+    from rt_helpers import golden
+    g = golden("pcg")
+    ctx = _native.Context.get(0)
+    for (sd, px, s), u in zip(g["streams"], g["uniforms"]):
+        out = np.zeros(8, np.uint32)
+        _native.check(_native.lib().rt_stream_draws(ctx.handle, int(sd), int(px), int(s), 8,
+                                                    out.ctypes.data_as(ctypes.c_void_p)))
+        assert np.array_equal(out.astype(np.float64) * 2.0 ** -32, u), (sd, px, s)
+    kat = {(0, 0, 0): [0.0391256813891232, 0.5700523867271841, 0.938289409969002, 0.43033390073105693],
+           (0, 1, 0): [0.808150198077783, 0.7250175778754056], (1, 12345, 63): [0.929837548173964, 0.7013872317038476]}
+    for (sd, px, s), u in kat.items():
+        out = np.zeros(len(u), np.uint32)
+        _native.check(_native.lib().rt_stream_draws(ctx.handle, sd, px, s, len(u), out.ctypes.data_as(ctypes.c_void_p)))
+        assert np.allclose(out.astype(np.float64) * 2.0 ** -32, u, rtol=0, atol=1e-15)

@@ -1,6 +1,8 @@
 """Small end-to-end workload for compute-sanitizer (memcheck / racecheck / synccheck):
-LBVH builds and in-place rebuilds (30/63-bit, spheres), closest/any hit, all integrators,
-wavefront, device resolve, two-level."""
+the device compile (upload + validation, the flatten kernel, a staged pageable upload),
+refit_mesh with its bounds reduction, LBVH builds and in-place rebuilds (30/63-bit,
+spheres), closest/any hit, all integrators, wavefront, device resolve, the render replica,
+the band pack/unpack, two-level with a refresh + render, the RNG stream hook."""
 import os
 import sys
 
@@ -34,4 +36,32 @@ bl = [Blas.from_mesh(desc.meshes[k].vertices, desc.meshes[k].faces) for k in nam
 tl = build_tlas([Instance(names.index(d.mesh), d.frame) for d in desc.instances], bl)
 closest_hit_batch(tl, O * 0.5 + 0.5, D, with_stats=True)
 any_hit_batch(tl, O * 0.5 + 0.5, D)
+# device compile of a mesh whose faces (47 MB) take the staged pageable upload, + refit_mesh
+big = scenes.sphere_description(700, 1400)
+sc = compile_scene(big)
+V = big.meshes["mesh"].vertices * 1.01
+sc.refit_mesh("mesh", V)
+sc.diagonal()                                         # the re-reduced bounds
+render_frame(sc, 32, 16, 1, "eye")
+# replica + band pack / unpack
+import ctypes  # noqa: E402
+from paper_2603_00292_b200 import _native, distributed  # noqa: E402
+cs = compile_scene(scenes.cornell_description())
+rep = cs.tlas.clone(0)
+acc = torch.zeros((40 * 30, 4), dtype=torch.float32, device="cuda")
+comp = torch.zeros_like(acc)
+for g in range(3):
+    render_into(cs, acc, 40, 30, 1, "pt", 0, IntegratorConfig(max_depth=3), bands=distributed.band_split(g, 3))
+    for unpack in (0, 1):
+        _native.check(_native.lib().rt_bands_copy(cs.tlas.ctx.handle, _native.ptr(acc), _native.ptr(comp), 40, 30,
+                                                  g, 3, unpack, None))
+out = np.zeros(8, np.uint32)
+_native.check(_native.lib().rt_stream_draws(cs.tlas.ctx.handle, 1, 2, 3, 8, out.ctypes.data_as(ctypes.c_void_p)))
+# two-level: refit + refresh, then a render through the re-flattened copy
+two = compile_scene(desc, two_level=True)
+cube = names.index("cube")
+two.tlas.blases[cube].refit(vertices=desc.meshes["cube"].vertices * 1.1)
+two.tlas.refresh_instance_bounds()
+render_frame(two, 24, 16, 2, "pt", cfg=IntegratorConfig(max_depth=3))
+torch.cuda.synchronize()
 print("sanitize driver ok")
