@@ -36,7 +36,6 @@ struct FrameConst {
     int tiled, tiles_x;
     int band_stride, band_offset;   // interleaved tile-row bands (multi-GPU tile split)
     int64_t row0, row1, nunits;
-    int64_t mine_rows, perm_a;      // tile-row fetch order: local row lr -> (lr * perm_a) % mine_rows
 };
 
 // unit k -> pixel; false for the padding lanes of partial edge tiles
@@ -45,12 +44,7 @@ __device__ __forceinline__ bool unit_pixel(const FrameConst& F, int64_t k, int64
     int64_t t = k >> 5;
     int l = (int)(k & 31);
     int64_t x = (t % F.tiles_x) * 8 + (l & 7);
-    // tile rows in a low-discrepancy order (golden-ratio stride): the rows fetched last are a
-    // spread sample of the frame instead of its bottom band (on the config-2 sphere the
-    // bottom rows see the pole's fan of thin triangles, and a top-to-bottom order ended
-    // every frame on them: SM activity 60-100 % of the kernel, ncu)
-    const int64_t lr = ((t / F.tiles_x) * F.perm_a) % F.mine_rows;
-    int64_t trow = lr * F.band_stride + F.band_offset;
+    int64_t trow = (t / F.tiles_x) * F.band_stride + F.band_offset;
     int64_t y = F.row0 + trow * 4 + (l >> 3);
     pix = y * F.width + x;
     return x < F.width && y < F.row1;
@@ -529,11 +523,6 @@ FrameConst make_frame(const rt_render_params* p) {
     const int64_t trows = (F.row1 - F.row0 + 3) / 4;
     const int64_t mine = trows > F.band_offset ? (trows - F.band_offset + F.band_stride - 1) / F.band_stride : 0;
     F.nunits = F.tiled ? (int64_t)F.tiles_x * mine * 32 : F.npix;
-    F.mine_rows = mine > 0 ? mine : 1;
-    F.perm_a = 1;
-#ifndef RT_TILE_PERM
-#define RT_TILE_PERM 1
-#endif
 #if RT_TILE_PERM
     if (mine > 2) {
         // the integer nearest mine / phi that is coprime with mine (a bijection of the rows)
