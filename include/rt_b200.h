@@ -81,6 +81,9 @@ void rt_ctx_destroy(rt_ctx* ctx);
  * the legacy default stream); a new context uses its own non-blocking stream */
 int rt_ctx_set_stream(rt_ctx* ctx, void* cuda_stream);
 int rt_ctx_sync(rt_ctx* ctx);
+/* the context's 64 device work counters after the last launch (diagnostics: [0] work units
+ * taken by the persistent kernels, [32..33] closest-hit queries of the last render (u64)) */
+int rt_ctx_counters(rt_ctx* ctx, uint32_t* out64);
 int rt_device_count(int* n);
 const char* rt_last_error(void);
 const char* rt_version(void);

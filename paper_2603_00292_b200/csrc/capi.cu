@@ -162,6 +162,15 @@ void rt_ctx_destroy(rt_ctx* c) {
     delete c;
 }
 
+int rt_ctx_counters(rt_ctx* c, uint32_t* out64) {
+    RT_CTX_LOCK(c);
+    RT_CHECK_ARG(out64, "NULL output");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    RT_CUDA_TRY(cudaMemcpyAsync(out64, c->d_counter, 64 * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return RT_OK;
+}
+
 int rt_ctx_set_stream(rt_ctx* c, void* stream) {
     RT_CHECK_ARG(c, "ctx is NULL");
     c->stream = (cudaStream_t)stream;   // used verbatim: NULL is the legacy default stream

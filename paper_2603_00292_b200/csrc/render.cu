@@ -14,6 +14,13 @@
 namespace {
 
 constexpr int MEGA_THREADS = 128;
+#ifndef RT_TIMELINE
+#define RT_TIMELINE 0           // diagnostic builds: per-warp start / end / SM / fetch count of the megakernel
+#endif
+#if RT_TIMELINE
+#define RT_TIMELINE_WARPS 8192
+__device__ unsigned long long g_timeline[4 * RT_TIMELINE_WARPS];
+#endif
 #ifndef RT_SMEM_STACK
 #define RT_SMEM_STACK 0          // > 0: top entries of the megakernel's walk stack in shared memory
 #endif
@@ -289,11 +296,19 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     const int lane = threadIdx.x & 31;
     unsigned long long rays = 0;
     const int max_depth = INTEG == RT_INTEG_EYE ? 1 : F.max_depth;
+#if RT_TIMELINE
+    unsigned long long t_start, t_end;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    unsigned n_fetch = 0;
+#endif
     while (true) {
         unsigned base = 0;
         if (lane == 0) base = atomicAdd(counter, 32u);
         base = __shfl_sync(RT_FULL, base, 0);
         if ((int64_t)base >= F.nunits) break;
+#if RT_TIMELINE
+        ++n_fetch;
+#endif
         int64_t i = (int64_t)base + lane;
         int64_t pix;
         if (i < F.nunits && unit_pixel(F, i, pix)) {
@@ -326,6 +341,18 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) rays += __shfl_xor_sync(RT_FULL, rays, off);
     if (lane == 0 && rays) atomicAdd(ray_total, rays);
+#if RT_TIMELINE
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    const unsigned w = blockIdx.x * (MEGA_THREADS / 32) + (threadIdx.x >> 5);
+    if (lane == 0 && w < RT_TIMELINE_WARPS) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_timeline[4 * w] = t_start;
+        g_timeline[4 * w + 1] = t_end;
+        g_timeline[4 * w + 2] = smid;
+        g_timeline[4 * w + 3] = n_fetch;
+    }
+#endif
 }
 
 // ---- K8: wavefront ----------------------------------------------------------
@@ -767,3 +794,12 @@ extern "C" int rt_stream_draws(rt_ctx* c, uint64_t seed, uint64_t pixel, uint64_
     }
     return RT_OK;
 }
+
+#if RT_TIMELINE
+extern "C" int rt_debug_timeline(unsigned long long* out, int32_t n_warps) {
+    RT_CHECK_ARG(out && n_warps > 0 && n_warps <= RT_TIMELINE_WARPS, "bad timeline buffer");
+    RT_CUDA_TRY(cudaDeviceSynchronize());
+    RT_CUDA_TRY(cudaMemcpyFromSymbol(out, g_timeline, sizeof(unsigned long long) * 4 * n_warps));
+    return RT_OK;
+}
+#endif

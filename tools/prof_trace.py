@@ -43,6 +43,7 @@ def main():
     acc = torch.zeros((H * W, 4), dtype=torch.float32, device="cuda")
     sc = compile_scene(scenes.sphere_description())
     out["eye1080_sphere_ms"] = timed(lambda: render_into(sc, acc, W, H, 1, "eye", count_rays=False), a.reps)
+
     sc.tlas.build(63)
     out["eye1080_sphere_lbvh63_ms"] = timed(lambda: render_into(sc, acc, W, H, 1, "eye", count_rays=False), a.reps)
     del sc
@@ -56,6 +57,7 @@ def main():
         acc4 = torch.zeros((H4 * W4, 4), dtype=torch.float32, device="cuda")
         ss = compile_scene(scenes.soup_description())
         out["eye4k_soup_ms"] = timed(lambda: render_into(ss, acc4, W4, H4, 1, "eye", count_rays=False), a.reps)
+
         ss.tlas.build(63)
         out["eye4k_soup_lbvh63_ms"] = timed(lambda: render_into(ss, acc4, W4, H4, 1, "eye", count_rays=False), a.reps)
     print(json.dumps(out))
