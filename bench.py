@@ -554,13 +554,14 @@ def run_ours(args, ws, rank, local):
     dominant = roof_trace
     if with_build:
         build_ms = t_build / K
-        build_bytes = 328.0 * tl.n
-        roof_build = {"kernel": "LBVH build (K1-K5: bounds, morton, onesweep x4, fused emit+refit)", "bound": "hbm",
+        build_bytes = 312.0 * tl.n
+        roof_build = {"kernel": "LBVH build (K1-K5: bounds, morton, onesweep x3, fused emit+refit)", "bound": "hbm",
                       "achieved": build_bytes / (build_ms * 1e-3) / 1e9, "peak": peak_gbs, "unit": "GB/s",
                       "traffic": load_traffic("config2_build") if C == 2 else load_traffic("config4_build"),
                       "traffic_source": "profiles/ncu_traffic.json (ncu --set full of one build, each kernel "
                                         "with cold caches)",
-                      "bytes_formula": f"328 B/tri x {tl.n} tris (SURVEY 8(d), 30-bit keys)",
+                      "bytes_formula": f"312 B/tri x {tl.n} tris (SURVEY 8(d) terms, 30-bit keys sorted in "
+                                       f"3 passes of 10-bit digits: 48 + 80 + 3 x 16 + 4 + 16 + 116)",
                       "stage_ms": stages, "peak_source": peak_src,
                       "sm_issue_active_pct": load_issue("config2_build" if C == 2 else "config4_build"),
                       "achieved_occupancy_pct": load_ncu("config2_build" if C == 2 else "config4_build").get(
@@ -573,8 +574,8 @@ def run_ours(args, ws, rank, local):
             other = roof_build
         line_extra = {"lbvh_build_ms": build_ms, "lbvh63_build_ms": build63_ms,
                       "trace_mrays_s": rays_step * K / (t_render * 1e-3) / 1e6, "roofline_other": other}
-        launches = 8 + 1      # the bench builds with 30-bit keys
-        detail = "per step: 8 LBVH kernels (bounds, Morton + digit histograms, 4 onesweep passes, emit+refit, " \
+        launches = 7 + 1      # the bench builds with 30-bit keys
+        detail = "per step: 7 LBVH kernels (bounds, Morton + digit histograms, 3 onesweep passes, emit+refit, " \
                  "global emit climb) + 1 megakernel (plus one memset)"
     else:
         launches = 1 if kernel == "mega" else (samples[1] - samples[0]) * (2 + 2 * cfg.max_depth)

@@ -4,9 +4,10 @@
 //   K1 lbvh_bounds     fp32 centroid bounds (block reduce + one orderable-uint
 //                      atomic per block and axis)
 //   K2 lbvh_morton     30-bit (10b/axis) or 63-bit (21b/axis) keys, no FMA
-//   K3 onesweep        LSD radix sort, 8-bit digits, one histogram pass for
-//                      all digits + one kernel per digit with decoupled
-//                      look-back and __match_any_sync warp ranking; stable
+//   K3 onesweep        LSD radix sort, one histogram pass for all digits (fused
+//                      into K2) + one kernel per digit with decoupled look-back
+//                      and warp ranking; stable.  30-bit keys: 3 passes of
+//                      10-bit digits; 63-bit keys: 8 passes of 8-bit digits
 //   K4+K5 lbvh_emit    fused Karras emission + refit in one bottom-up pass
 //                      (index fallback for equal keys, parent pointers, leaf
 //                      gather into leaf order, 64-B BVH2 nodes with both child
@@ -16,6 +17,7 @@
 // restates them on the CPU and tests/test_gpu_lbvh.py checks bit equality.
 #include <cub/block/block_scan.cuh>
 #include <cuda/atomic>
+#include <utility>
 
 #include "rt_common.cuh"
 
@@ -298,15 +300,16 @@ __device__ __forceinline__ uint64_t expand21(uint64_t v) {
 
 // K2 fused with the onesweep digit histogram of every pass (the keys are in
 // registers here, so the histogram costs no extra read of the key array)
-template <typename K, int B, int PASSES>
+template <typename K, int B, int PASSES, int DB>
 __global__ void __launch_bounds__(TRI_CHUNK) lbvh_morton_kernel(const float* __restrict__ tris, int64_t n,
                                                                const unsigned int* __restrict__ cb_enc,
                                                                float* __restrict__ cb, K* __restrict__ keys,
                                                                unsigned int* __restrict__ hist) {
-    __shared__ unsigned int s_hist[PASSES][256];
+    constexpr int NB = 1 << DB;                    // digit bins per pass
+    __shared__ unsigned int s_hist[PASSES][NB];
     __shared__ __align__(128) float s_tri[TRI_STAGES][9 * TRI_CHUNK];
     __shared__ __align__(8) uint64_t s_bar[TRI_STAGES];
-    for (int i = threadIdx.x; i < PASSES * 256; i += blockDim.x) (&s_hist[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < PASSES * NB; i += blockDim.x) (&s_hist[0][0])[i] = 0;
     const float scale = (float)(1u << B), qmax = (float)((1u << B) - 1u);
     pdl_wait();                                    // K1's centroid bounds
     pdl_trigger();
@@ -333,10 +336,10 @@ __global__ void __launch_bounds__(TRI_CHUNK) lbvh_morton_kernel(const float* __r
                 k = (K)((expand21(q[0]) << 2) | (expand21(q[1]) << 1) | expand21(q[2]));
             keys[base + threadIdx.x] = k;
 #pragma unroll
-            for (int p = 0; p < PASSES; ++p) atomicAdd(&s_hist[p][(unsigned)(k >> (8 * p)) & 0xFFu], 1u);
+            for (int p = 0; p < PASSES; ++p) atomicAdd(&s_hist[p][(unsigned)(k >> (DB * p)) & (NB - 1u)], 1u);
         }
     });
-    for (int i = threadIdx.x; i < PASSES * RADIX; i += blockDim.x) {
+    for (int i = threadIdx.x; i < PASSES * NB; i += blockDim.x) {
         unsigned v = (&s_hist[0][0])[i];
         if (v) atomicAdd(hist + i, v);
     }
@@ -482,6 +485,187 @@ if (BALLOT) {
     }
 }
 
+// ---- 30-bit keys in three passes of 10-bit digits ------------------------------
+// The same tile algorithm as onesweep_pass (bit-plane ballot ranking, decoupled
+// look-back, digit-ordered staging, contiguous runs out) with 1024 bins: one pass fewer
+// than four 8-bit passes over 30 bits (the last of which sorted 6 bits).  Each thread
+// owns 4 adjacent bins: its warp prefixes move as one 64-bit shared load, its look-back
+// status words of a predecessor tile are adjacent, and it publishes them with one 128-bit
+// store.  Per-warp digit counters are 16-bit (a warp ranks 32 x ITEMS keys).
+constexpr int R10 = 1024;
+constexpr int R10_PER = R10 / SORT_THREADS;     // bins per thread
+#ifndef SORT_LB_WIN10
+#define SORT_LB_WIN10 2   // 1 / 2 / 4 / 8 / 16: 10M sort 0.405 / 0.396 / 0.411 / 0.469 / 0.705 ms
+#endif
+#ifndef SORT_ITEMS10
+#define SORT_ITEMS10 12   // keys per thread (10 -> 12: 10M sort 0.396 -> 0.370 ms)
+#endif
+constexpr int TILE10 = SORT_THREADS * SORT_ITEMS10;
+#ifndef SORT_LB_SLEEP
+#define SORT_LB_SLEEP 0
+#endif
+__device__ __forceinline__ uint4 ld_status4(const unsigned* p) {
+    uint4 v;
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_status4(unsigned* p, unsigned a, unsigned b, unsigned c, unsigned d) {
+    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
+                 : "memory");
+}
+
+__device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ keys_in,
+                                                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+                                                uint32_t* __restrict__ vals_out, int64_t n, int shift,
+                                                const unsigned int* __restrict__ hist, unsigned int* status,
+                                                unsigned int* counter) {
+    typedef cub::BlockScan<unsigned int, SORT_THREADS> Scan;
+    constexpr int ITEMS = SORT_ITEMS10, TILE = TILE10;
+    __shared__ typename Scan::TempStorage scan_tmp;
+    __shared__ __align__(16) unsigned short s_warp[SORT_THREADS / 32][R10];
+    __shared__ unsigned int s_base[R10];
+    __shared__ unsigned short s_texcl[R10];
+    __shared__ uint32_t s_keys[TILE];
+    __shared__ uint32_t s_vals[TILE];
+    __shared__ unsigned int s_tile;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    if (tid == 0) s_tile = atomicAdd(counter, 1u);
+    {
+        uint4* z = reinterpret_cast<uint4*>(&s_warp[0][0]);
+        constexpr int NZ = (int)(sizeof(s_warp) / sizeof(uint4));
+#pragma unroll
+        for (int k = tid; k < NZ; k += SORT_THREADS) z[k] = make_uint4(0, 0, 0, 0);
+    }
+    pdl_wait();
+    pdl_trigger();
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const int64_t seg = (int64_t)tile * TILE + (int64_t)warp * (32 * ITEMS);
+    uint32_t key[ITEMS], val[ITEMS];
+    unsigned dig[ITEMS], peers[ITEMS], rank[ITEMS];
+    const unsigned lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const int64_t idx = seg + i * 32 + lane;
+        const bool ok = idx < n;
+        key[i] = ok ? keys_in[idx] : 0u;
+        val[i] = ok ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        // keys past n take the last bin: they follow every real key in the stable order, so
+        // they land behind the tile's real keys and are never written out
+        const bool ok = seg + i * 32 + lane < n;
+        dig[i] = ok ? ((key[i] >> shift) & (R10 - 1u)) : (R10 - 1u);
+        unsigned pm = RT_FULL;
+#pragma unroll
+        for (int b = 0; b < 10; ++b) {
+            const bool bit = (dig[i] >> b) & 1u;
+            const unsigned bb = __ballot_sync(RT_FULL, bit);
+            pm &= bit ? bb : ~bb;
+        }
+        peers[i] = pm;
+    }
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const unsigned below = __popc(peers[i] & lt_mask);
+        const unsigned base = s_warp[warp][dig[i]];
+        __syncwarp();
+        if (below == 0) s_warp[warp][dig[i]] = (unsigned short)(base + __popc(peers[i]));
+        __syncwarp();
+        rank[i] = base + below;
+    }
+    __syncthreads();
+    // warp prefixes of this thread's 4 bins; tc = the tile's count per bin
+    unsigned tc[R10_PER] = {0, 0, 0, 0};
+#pragma unroll
+    for (int w = 0; w < SORT_THREADS / 32; ++w) {
+        uint2* pw = reinterpret_cast<uint2*>(&s_warp[w][R10_PER * tid]);
+        const uint2 v = *pw;
+        const unsigned c[4] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16};
+        *pw = make_uint2(tc[0] | (tc[1] << 16), tc[2] | (tc[3] << 16));
+#pragma unroll
+        for (int j = 0; j < R10_PER; ++j) tc[j] += c[j];
+    }
+    // publish aggregates, look back per bin (independent windows), publish inclusive prefixes
+    unsigned* st = status + (size_t)tile * R10 + R10_PER * tid;
+    unsigned excl[R10_PER] = {0, 0, 0, 0};
+    if (tile == 0) {
+        st_status4(st, FLAG_INC | tc[0], FLAG_INC | tc[1], FLAG_INC | tc[2], FLAG_INC | tc[3]);
+    } else {
+        st_status4(st, FLAG_AGG | tc[0], FLAG_AGG | tc[1], FLAG_AGG | tc[2], FLAG_AGG | tc[3]);
+        // a predecessor's thread publishes its 4 bins in one 128-bit store, so the 4 status
+        // words it holds are always of one kind (all unpublished, all aggregate or all
+        // inclusive): the thread walks back over predecessors with one 128-bit load each
+        constexpr int LB = SORT_LB_WIN10;
+        int j = (int)tile - 1;
+        bool done = false;
+        while (!done) {
+            uint4 w[LB];
+#pragma unroll
+            for (int k = 0; k < LB; ++k)
+                w[k] = (j - k >= 0) ? ld_status4(status + (size_t)(j - k) * R10 + R10_PER * tid)
+                                    : make_uint4(0, 0, 0, 0);
+            int k = 0;
+#pragma unroll
+            for (int kk = 0; kk < LB; ++kk) {
+                if (done || k < kk) continue;            // stopped earlier in this window
+                const unsigned f = w[kk].x & ~VALUE_MASK;
+                // not yet published (or, defensively, a 128-bit store seen half-way): re-poll
+                if (f == 0 || ((w[kk].x ^ w[kk].y) | (w[kk].x ^ w[kk].z) | (w[kk].x ^ w[kk].w)) & ~VALUE_MASK) continue;
+                excl[0] += w[kk].x & VALUE_MASK;
+                excl[1] += w[kk].y & VALUE_MASK;
+                excl[2] += w[kk].z & VALUE_MASK;
+                excl[3] += w[kk].w & VALUE_MASK;
+                k = kk + 1;
+                if (f & FLAG_INC) done = true;
+            }
+            j -= k;
+#if SORT_LB_SLEEP
+            if (k == 0) __nanosleep(SORT_LB_SLEEP);   // no progress: back off instead of hammering L2
+#endif
+        }
+        st_status4(st, FLAG_INC | (excl[0] + tc[0]), FLAG_INC | (excl[1] + tc[1]), FLAG_INC | (excl[2] + tc[2]),
+                   FLAG_INC | (excl[3] + tc[3]));
+    }
+    unsigned hv[R10_PER], bin_excl[R10_PER], tile_excl[R10_PER];
+#pragma unroll
+    for (int j = 0; j < R10_PER; ++j) hv[j] = __ldg(hist + R10_PER * tid + j);
+    Scan(scan_tmp).ExclusiveSum(hv, bin_excl);
+    __syncthreads();
+    Scan(scan_tmp).ExclusiveSum(tc, tile_excl);
+#pragma unroll
+    for (int j = 0; j < R10_PER; ++j) {
+        s_base[R10_PER * tid + j] = bin_excl[j] + excl[j] - tile_excl[j];
+        s_texcl[R10_PER * tid + j] = (unsigned short)tile_excl[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const unsigned lpos = s_texcl[dig[i]] + s_warp[warp][dig[i]] + rank[i];
+        s_keys[lpos] = key[i];
+        s_vals[lpos] = val[i];
+    }
+    __syncthreads();
+    const int64_t left = n - (int64_t)tile * TILE;
+    const int cnt = left < TILE ? (int)left : TILE;
+    for (int j = tid; j < cnt; j += SORT_THREADS) {
+        const uint32_t k = s_keys[j];
+        const unsigned pos = s_base[(k >> shift) & (R10 - 1u)] + (unsigned)j;
+        keys_out[pos] = k;
+        vals_out[pos] = s_vals[j];
+    }
+}
+__global__ void __launch_bounds__(SORT_THREADS, 4) onesweep10_kernel(
+    const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, const unsigned int* __restrict__ hist, unsigned int* status,
+    unsigned int* counter) {
+    onesweep10_pass(keys_in, vals_in, keys_out, vals_out, n, shift, hist, status, counter);
+}
+
 // 30-bit keys: 64 registers -> 4 blocks per SM (10M: 4 passes 0.427 -> 0.391 ms); 63-bit
 // keys keep the single-argument bound (an explicit minBlocks = 1 costs 15 % there).
 #define ONESWEEP_ARGS                                                                                  \
@@ -543,21 +727,28 @@ __global__ void single_leaf_root(const float* tris, const uint32_t* mask, float4
     nodes[3] = make_float4(__int_as_float(~0), __int_as_float(~0), __int_as_float(1), 0.0f);
 }
 
-template <typename K, int PASSES, int B>
+// DB: digit bits per onesweep pass (30-bit keys: 3 x 10 with RT_SORT10, else 4 x 8;
+// 63-bit keys: 8 x 8)
+#ifndef RT_SORT10
+#define RT_SORT10 1
+#endif
+template <typename K, int PASSES, int B, int DB>
 int build_typed(rt_ctx* ctx, rt_scene* s) {
     const int64_t n = s->n;
     cudaStream_t st = ctx->stream;
     const int grid_stream = ctx->num_sms * TRI_BLOCKS_PER_SM;
+    constexpr int NB = 1 << DB;
     // one memset zeroes the sort scratch: digit histograms, tile counters, the
     // centroid-bound accumulators, the emit item count and the look-back status
     int gb = (int)((n + 255) / 256);
     if (gb > grid_stream) gb = grid_stream;
-    const int64_t tiles = (n + SortCfg<K>::TILE - 1) / SortCfg<K>::TILE;
-    unsigned int* hist = s->sort_scratch;                    // PASSES * 256
-    unsigned int* counters = hist + PASSES * RADIX;          // [0, 8) tile counters, [8, 14) cb_enc, [16] emit count
+    constexpr int64_t TILE = DB == 10 ? TILE10 : SortCfg<K>::TILE;
+    const int64_t tiles = (n + TILE - 1) / TILE;
+    unsigned int* hist = s->sort_scratch;                    // PASSES * NB
+    unsigned int* counters = hist + PASSES * NB;             // [0, 8) tile counters, [8, 14) cb_enc, [16] emit count
     unsigned int* cb_enc = counters + 8;
-    unsigned int* status = counters + 32;                    // PASSES * tiles * 256
-    size_t words = (size_t)PASSES * RADIX + 32 + (size_t)PASSES * tiles * RADIX;
+    unsigned int* status = counters + 32;                    // PASSES * tiles * NB
+    size_t words = (size_t)PASSES * NB + 32 + (size_t)PASSES * tiles * NB;
     RT_PROF(ctx, 0);
     RT_CUDA_TRY(cudaMemsetAsync(s->sort_scratch, 0, words * sizeof(unsigned int), st));
     // K1
@@ -566,7 +757,7 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     K* ka = (K*)s->keys_a;
     K* kb = (K*)s->keys_b;
     RT_PROF(ctx, 1);
-    RT_CUDA_TRY(launch_pdl(lbvh_morton_kernel<K, B, PASSES>, gb, 256, st, s->tris, n, cb_enc, s->cbounds, ka, hist));
+    RT_CUDA_TRY(launch_pdl(lbvh_morton_kernel<K, B, PASSES, DB>, gb, 256, st, s->tris, n, cb_enc, s->cbounds, ka, hist));
     RT_PROF(ctx, 2);
     // K3 (digit histograms already accumulated by K2)
     K* kin = ka; K* kout = kb;
@@ -578,10 +769,12 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     const bool ballot = sizeof(K) == 8 || n >= SORT_BALLOT_MIN;
     for (int p = 0; p < PASSES; ++p) {
         auto launch = [&](auto kern) {
-            return launch_pdl(kern, (unsigned)tiles, SORT_THREADS, st, kin, vin, kout, vout, n, 8 * p,
-                              hist + p * RADIX, status + (size_t)p * tiles * RADIX, counters + p);
+            return launch_pdl(kern, (unsigned)tiles, SORT_THREADS, st, kin, vin, kout, vout, n, DB * p,
+                              hist + p * NB, status + (size_t)p * tiles * NB, counters + p);
         };
-        if constexpr (sizeof(K) == 4) {
+        if constexpr (DB == 10) {
+            RT_CUDA_TRY(launch(onesweep10_kernel));
+        } else if constexpr (sizeof(K) == 4) {
             RT_CUDA_TRY(ballot ? launch(onesweep32_kernel<true>) : launch(onesweep32_kernel<false>));
         } else {
             RT_CUDA_TRY(launch(onesweep64_kernel<true>));
@@ -590,7 +783,13 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
         uint32_t* nv = (vout == s->vals_b) ? s->vals_a : s->vals_b;
         vin = vout; vout = nv;
     }
-    // PASSES is even: sorted keys in keys_a, values in vals_a
+    if (PASSES & 1) {
+        // an odd pass count leaves the sorted keys / order in the b buffers: the scene's
+        // a / b buffers trade places so keys_a / vals_a hold them (download, scene copy)
+        std::swap(s->keys_a, s->keys_b);
+        std::swap(s->vals_a, s->vals_b);
+    }
+    // sorted keys in keys_a (== kin), values in vals_a (== vin)
     // K4 + K5
     RT_PROF(ctx, 4);
     // (the global split slots are reset by the emit kernel at its hand-off boundaries)
@@ -619,11 +818,18 @@ int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits) {
         RT_CUDA_TRY(cudaGetLastError());
         return RT_OK;
     }
-    if (bits == 30) return build_typed<uint32_t, 4, 10>(ctx, s);
-    return build_typed<uint64_t, 8, 21>(ctx, s);
+#if RT_SORT10
+    if (bits == 30) return build_typed<uint32_t, 3, 10, 10>(ctx, s);
+#else
+    if (bits == 30) return build_typed<uint32_t, 4, 10, 8>(ctx, s);
+#endif
+    return build_typed<uint64_t, 8, 21, 8>(ctx, s);
 }
 
 size_t rt_sort_scratch_words(int64_t n) {
-    int64_t tiles = (n + SORT_TILE_MIN - 1) / SORT_TILE_MIN;
-    return (size_t)8 * RADIX + 32 + (size_t)8 * tiles * RADIX;
+    const int64_t tiles = (n + SORT_TILE_MIN - 1) / SORT_TILE_MIN;
+    const int64_t tiles32 = (n + TILE10 - 1) / TILE10;
+    const size_t w8 = (size_t)8 * RADIX + 32 + (size_t)8 * tiles * RADIX;
+    const size_t w10 = (size_t)3 * R10 + 32 + (size_t)3 * tiles32 * R10;
+    return w8 > w10 ? w8 : w10;
 }
