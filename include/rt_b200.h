@@ -84,6 +84,16 @@ int rt_ctx_sync(rt_ctx* ctx);
 /* the context's 64 device work counters after the last launch (diagnostics: [0] work units
  * taken by the persistent kernels, [32..33] closest-hit queries of the last render (u64)) */
 int rt_ctx_counters(rt_ctx* ctx, uint32_t* out64);
+/* tile-probe scheduling of megakernel eye renders (process-wide; render.cu): before
+ * rendering, one ray per 8x4 tile walks under a budget of walk steps and tiles that run out
+ * are rendered first.  0 disables it (row-major tiles); the default is 24 or the
+ * RT_PROBE_BUDGET environment variable.  The frame is identical either way: only the order
+ * in which tiles are rendered changes. */
+int rt_set_probe_budget(int32_t budget, int32_t* previous);
+/* the last probed eye render of the context: out4 = {tiles probed (batch-rounded), heavy
+ * tiles queued, queue pops, 1 + first tile past the probe when probing stopped early (0:
+ * it did not)} */
+int rt_probe_stats(rt_ctx* ctx, uint32_t* out4);
 int rt_device_count(int* n);
 const char* rt_last_error(void);
 const char* rt_version(void);

@@ -95,6 +95,8 @@ def lib():
             "rt_ctx_set_stream": [vp, vp],
             "rt_ctx_sync": [vp],
             "rt_ctx_counters": [vp, vp],
+            "rt_set_probe_budget": [i32, vp],
+            "rt_probe_stats": [vp, vp],
             "rt_scene_create": [vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, i32, vp],
             "rt_bvh_build": [vp, vp, ci, vp],
             "rt_bvh_build_profiled": [vp, vp, ci, vp],

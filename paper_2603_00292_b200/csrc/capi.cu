@@ -155,6 +155,7 @@ void rt_ctx_destroy(rt_ctx* c) {
     }
     cudaFree(c->d_counter);
     cudaFree(c->d_error);
+    if (c->d_probe) cudaFree(c->d_probe);
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
     cudaStreamDestroy(c->own_stream);

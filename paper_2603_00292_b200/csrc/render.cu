@@ -9,6 +9,8 @@
 // World normals come per triangle from the host (reference-style);
 // the ONB uses copysignf (signed-zero sensitive, sampling.py:175-186).  This
 // TU must not be built with --use_fast_math.
+#include <atomic>
+
 #include "traverse.cuh"
 
 namespace {
@@ -43,6 +45,12 @@ struct FrameConst {
     int tiled, tiles_x;
     int band_stride, band_offset;   // interleaved tile-row bands (multi-GPU tile split)
     int64_t row0, row1, nunits;
+    // tile-probe scheduling of single-sample tiled eye frames (see the megakernel)
+    int probe_budget;              // walk steps of a probe ray; 0 = off (row-major tiles)
+    unsigned epoch;                // this render's claim tag (claims[t] >= epoch: tile t taken)
+    unsigned* claims;              // (tiles)
+    unsigned long long* heavy_q;   // (tiles) (epoch << 32 | tile) of heavy tiles, in push order
+    unsigned* probe_ctl;           // PC_WORDS control words (zeroed per render)
 };
 
 // unit k -> pixel; false for the padding lanes of partial edge tiles
@@ -269,6 +277,57 @@ __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* 
     }
 }
 
+// ---- tile-probe scheduling (eye frames) ---------------------------------------
+// A persistent frame ends when its last walk ends.  On a dense mesh a few primary walks
+// (grazing rays along the silhouette: ~230 dependent node fetches + triangle tests against
+// a median of 8) take ~0.2 ms alone, and in row-major order the last rows' long walks start
+// when the work runs out.  So the megakernel first probes every 8x4 tile with one ray
+// walked under a budget of walk steps (a separate instantiation of the walk: the budget
+// exit is not in the rendering walk's loop); a tile whose probe runs out of budget is
+// pushed on a heavy-tile queue, and every warp takes queued heavy tiles before row-major
+// ones (whoever claims a tile first renders it).  On the config-2 sphere the probe (lane 12 of the tile) flags every tile
+// whose slowest ray needs >= 100 steps at a budget of 24 (8 % of the tiles,
+// tools/diag_probe.py).  Only the schedule changes: each pixel is rendered once, by one
+// lane, exactly as before (claims: one atomicMax of the render's epoch per tile).
+#ifndef RT_PROBE_BUDGET
+#define RT_PROBE_BUDGET 24      // walk steps; the RT_PROBE_BUDGET env overrides (0: no probe)
+#endif
+#ifndef RT_PROBE_CAP_DIV
+#define RT_PROBE_CAP_DIV 8      // heavy queue cap: tiles / 8
+#endif
+constexpr int PROBE_LANE = 12;  // (x 4, y 1) of the 8x4 tile
+// tiles per probe batch (lanes 0..15 probe): the first wave, one batch per warp, covers a
+// 1080p frame (4050 batches for 4144 warps) but only a quarter of a 4K one, so a uniformly
+// costly 4K scene pays for 66K probe walks before the stop rule can see it
+constexpr int PROBE_BATCH = 16;
+// probe control words, one per 128-B line of F.probe_ctl
+constexpr int PC_TAKEN = 0, PC_HEAD = 32, PC_TAIL = 64, PC_DONE = 96, PC_STOP = 128, PC_LIMIT = 160, PC_WORDS = 192;
+struct ProbeBudget {
+    int it, budget;
+    __device__ __forceinline__ bool tick() { return ++it > budget; }
+};
+__device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
+    return *reinterpret_cast<const volatile unsigned*>(p);
+}
+// pop a heavy tile (lane 0): -1 when none is queued.  The queue head only moves by
+// atomicAdd (a CAS loop livelocks under thousands of polling warps); a ticket taken past
+// the producers' reservations waits for its slot to be filled, or gives up once every
+// probe batch is complete (completion counts tiles: it reaches `ntiles32` exactly) and the
+// final reservation count is at or below the ticket.  The control words (F.probe_ctl) sit on
+// their own 128-B lines, away from the frame's work counter: a store into the line of the
+// work counter's atomics, once per warp, was measured to double the frame.
+__device__ __forceinline__ int64_t heavy_pop(const FrameConst& F, unsigned* pc, unsigned ntiles32) {
+    if (ld_volatile_u32(pc + PC_HEAD) >= ld_volatile_u32(pc + PC_TAIL)) return -1;
+    const unsigned h = atomicAdd(pc + PC_HEAD, 1u);
+    while (true) {
+        const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(F.heavy_q + h);
+        if ((unsigned)(e >> 32) == F.epoch) return (int64_t)(e & 0xFFFFFFFFull);
+        unsigned done;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(done) : "l"(pc + PC_DONE) : "memory");
+        if (done >= ntiles32 && h >= ld_volatile_u32(pc + PC_TAIL)) return -1;
+    }
+}
+
 // ---- K7: megakernel --------------------------------------------------------
 // Persistent warps fetch 32 pixels at a time; each lane renders samples
 // [s0, s1) of its pixel in order and adds the sums to accum once.
@@ -301,15 +360,125 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     unsigned n_fetch = 0;
 #endif
+    const bool probe_on = INTEG == RT_INTEG_EYE && F.probe_budget > 0;
+    unsigned* const pc = F.probe_ctl;
+    const int64_t ntiles = F.nunits >> 5;
+    // per-warp fetch state of the probed schedule, kept out of registers (the walk's loop is
+    // register-bound): the heavy queue is still worth polling; the first unprobed tile + 1
+    // once probing has stopped (0: not known)
+    __shared__ unsigned s_qopen[MEGA_THREADS / 32], s_limit[MEGA_THREADS / 32];
+    if (lane == 0) {
+        s_qopen[threadIdx.x >> 5] = 1u;
+        s_limit[threadIdx.x >> 5] = 0u;
+    }
+    __syncwarp();
+    // warps beyond the batch count start on row-major work (no pile-up on the batch counter)
+    bool probing = probe_on &&
+                   (int64_t)(blockIdx.x * (MEGA_THREADS / 32) + (threadIdx.x >> 5)) < (ntiles + PROBE_BATCH - 1) / PROBE_BATCH;
     while (true) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(counter, 32u);
-        base = __shfl_sync(RT_FULL, base, 0);
-        if ((int64_t)base >= F.nunits) break;
+        int64_t base;
+        if (!probe_on) {
+            unsigned b = 0;
+            if (lane == 0) b = atomicAdd(counter, 32u);
+            b = __shfl_sync(RT_FULL, b, 0);
+            if ((int64_t)b >= F.nunits) break;
+            base = b;
+        } else if (probing) {
+            // probe 32 tiles (one ray each, budgeted walk), claim and queue the heavy ones.  When
+            // more than 1/8 of the probed tiles (after the first 4096) or tiles / 8 in all come
+            // out heavy, the scene is uniformly costly (no tail to fix: the 10M soup flags 31 %)
+            // and probing stops: the remaining batches are taken and completed without walks (the
+            // completion count must reach every batch: heavy_pop's termination test), and the
+            // first batch no walk can have touched is published as PC_LIMIT + 1, below which
+            // row-major fetches still claim.  Batches are taken by acq_rel adds and the stopping
+            // warp reads the batch counter by one after its stop store, so a batch at or above
+            // the limit is always taken after the stop is visible to its prober.
+            unsigned pb = 0, stop = 0;
+            if (lane == 0) {
+                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(pb) : "l"(pc + PC_TAKEN), "r"(PROBE_BATCH) : "memory");
+                const unsigned nh = ld_volatile_u32(pc + PC_TAIL);
+                const bool seen_stop = ld_volatile_u32(pc + PC_STOP) != 0;
+                stop = seen_stop || nh >= (unsigned)(ntiles / RT_PROBE_CAP_DIV) ||
+                       (pb >= 4096u && nh * RT_PROBE_CAP_DIV > pb);
+                if (stop && !seen_stop) {
+                    *reinterpret_cast<volatile unsigned*>(pc + PC_STOP) = 1u;
+                    unsigned lim;
+                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 0;" : "=r"(lim) : "l"(pc + PC_TAKEN) : "memory");
+                    atomicMax(pc + PC_LIMIT, lim + 1u);
+                }
+            }
+            pb = __shfl_sync(RT_FULL, pb, 0);
+            stop = __shfl_sync(RT_FULL, stop, 0);
+            const int64_t t = (int64_t)pb + lane;
+            if ((int64_t)pb >= ntiles) {
+                probing = false;
+                continue;
+            }
+            bool heavy = false;
+            int64_t ppix;
+            if (!stop && lane < PROBE_BATCH && t < ntiles && unit_pixel(F, t * 32 + PROBE_LANE, ppix)) {
+                PathState P;
+                start_path(F, ppix, s0, P);
+                RayPre R;
+                ray_setup(R, P.ox, P.oy, P.oz, P.dx, P.dy, P.dz, 0.0f);
+                uint32_t nt, nv;
+                ProbeBudget y{0, F.probe_budget};
+                heavy = trace_ray4_y<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, walk_stack, nt, nv, sv, y).id ==
+                        RT_YIELDED;
+            }
+            if (heavy) {                                 // (the cap may be overshot by a batch)
+                const unsigned slot = atomicAdd(pc + PC_TAIL, 1u);
+                *reinterpret_cast<volatile unsigned long long*>(F.heavy_q + slot) =
+                    ((unsigned long long)F.epoch << 32) | (unsigned long long)t;
+            }
+            __syncwarp();
+            // this batch's queue slots before its completion count (a release reduction: a
+            // full fence here would also invalidate the SM's L1, which the walks live in)
+            if (lane == 0)
+                asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(pc + PC_DONE), "r"(PROBE_BATCH) : "memory");
+            continue;
+        } else {
+            // queued heavy tiles first (polled until the queue is drained after every probe
+            // batch completed), then row-major tiles nobody has claimed
+            long long b = 0;
+            if (lane == 0) {
+                const int w = threadIdx.x >> 5;
+                int64_t ht = -1;
+                if (s_qopen[w]) {
+                    const unsigned ntiles32 = (unsigned)((ntiles + PROBE_BATCH - 1) / PROBE_BATCH * PROBE_BATCH);
+                    const unsigned lim = ld_volatile_u32(pc + PC_LIMIT);
+                    if (lim) s_limit[w] = lim;
+                    if (lim) {
+                        // probing stopped (uniformly costly scene): the queued tiles go back to
+                        // row-major order (they are unclaimed), which L2 rewards on such scenes
+                        s_qopen[w] = 0u;
+                    } else {
+                        ht = heavy_pop(F, pc, ntiles32);
+                        if (ht < 0 && ld_volatile_u32(pc + PC_DONE) >= ntiles32 &&
+                            ld_volatile_u32(pc + PC_HEAD) >= ld_volatile_u32(pc + PC_TAIL))
+                            s_qopen[w] = 0u;
+                    }
+                }
+                if (ht >= 0) {
+                    // a popped tile is claimed here (a row-major fetch may have taken it first)
+                    b = atomicMax(F.claims + ht, F.epoch) < F.epoch ? ht * 32 : -1;
+                } else {
+                    b = atomicAdd(counter, 32u);
+                    const unsigned lim = s_limit[w];
+                    if (b < F.nunits && (lim == 0u || (b >> 5) + 1 < (long long)lim) &&
+                        atomicMax(F.claims + (b >> 5), F.epoch) >= F.epoch)
+                        b = -1;
+                }
+            }
+            b = __shfl_sync(RT_FULL, b, 0);
+            if (b >= F.nunits) break;
+            if (b < 0) continue;
+            base = b;
+        }
 #if RT_TIMELINE
         ++n_fetch;
 #endif
-        int64_t i = (int64_t)base + lane;
+        int64_t i = base + lane;
         int64_t pix;
         if (i < F.nunits && unit_pixel(F, i, pix)) {
             // accumulate sample by sample into the running sums, exactly like
@@ -550,6 +719,11 @@ FrameConst make_frame(const rt_render_params* p) {
     const int64_t trows = (F.row1 - F.row0 + 3) / 4;
     const int64_t mine = trows > F.band_offset ? (trows - F.band_offset + F.band_stride - 1) / F.band_stride : 0;
     F.nunits = F.tiled ? (int64_t)F.tiles_x * mine * 32 : F.npix;
+    F.probe_budget = 0;
+    F.epoch = 0;
+    F.claims = nullptr;
+    F.heavy_q = nullptr;
+    F.probe_ctl = nullptr;
 #if RT_TILE_PERM
     if (mine > 2) {
         // the integer nearest mine / phi that is coprime with mine (a bijection of the rows)
@@ -571,6 +745,17 @@ FrameConst make_frame(const rt_render_params* p) {
     }
     return F;
 }
+
+// walk-step budget of the eye frames' tile probe (0: no probe, row-major tiles): the
+// RT_PROBE_BUDGET environment variable, else RT_PROBE_BUDGET; rt_set_probe_budget overrides
+static std::atomic<int>& probe_budget_ref() {
+    static std::atomic<int> b([] {
+        const char* e = getenv("RT_PROBE_BUDGET");
+        return e ? atoi(e) : RT_PROBE_BUDGET;
+    }());
+    return b;
+}
+static int probe_budget() { return probe_budget_ref().load(std::memory_order_relaxed); }
 
 // device scratch for the wavefront, grown on demand and owned by the scene
 struct WaveBuffers {
@@ -660,6 +845,23 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
     RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, 64 * sizeof(unsigned int), st));
     float4* acc = reinterpret_cast<float4*>(accum);
     if (p->kernel == RT_KERNEL_MEGA) {
+        const int64_t ntiles = F.nunits >> 5;
+        if (F.integ == RT_INTEG_EYE && F.tiled && probe_budget() > 0 && ntiles > 1) {
+            if (ctx->probe_tiles < ntiles || ctx->probe_epoch == 0xFFFFFFFFu) {
+                if (ctx->d_probe) RT_CUDA_TRY(cudaFree(ctx->d_probe));
+                ctx->d_probe = nullptr;
+                RT_CUDA_TRY(cudaMalloc(&ctx->d_probe, (size_t)ntiles * 12 + PC_WORDS * 4));
+                RT_CUDA_TRY(cudaMemsetAsync(ctx->d_probe, 0, (size_t)ntiles * 12, st));
+                ctx->probe_tiles = ntiles;
+                ctx->probe_epoch = 0;
+            }
+            F.probe_budget = probe_budget();
+            F.epoch = ++ctx->probe_epoch;
+            F.heavy_q = reinterpret_cast<unsigned long long*>(ctx->d_probe);
+            F.claims = reinterpret_cast<unsigned*>(F.heavy_q + ctx->probe_tiles);
+            F.probe_ctl = F.claims + ctx->probe_tiles;
+            RT_CUDA_TRY(cudaMemsetAsync(F.probe_ctl, 0, PC_WORDS * 4, st));
+        }
         auto launch = [&](auto kern) -> int {
             int bps = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, MEGA_THREADS, 0);
@@ -803,3 +1005,25 @@ extern "C" int rt_debug_timeline(unsigned long long* out, int32_t n_warps) {
     return RT_OK;
 }
 #endif
+
+extern "C" int rt_set_probe_budget(int32_t budget, int32_t* previous) {
+    RT_CHECK_ARG(budget >= 0, "the probe budget is a walk-step count >= 0 (0: no probe)");
+    const int old = probe_budget_ref().exchange(budget);
+    if (previous) *previous = old;
+    return RT_OK;
+}
+
+extern "C" int rt_probe_stats(rt_ctx* c, uint32_t* out4) {
+    RT_CTX_LOCK(c);
+    RT_CHECK_ARG(out4, "NULL output");
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    for (int k = 0; k < 4; ++k) out4[k] = 0;
+    if (!c->d_probe) return RT_OK;
+    const unsigned* pc = reinterpret_cast<const unsigned*>(reinterpret_cast<const char*>(c->d_probe) +
+                                                           (size_t)c->probe_tiles * 12);
+    const int idx[4] = {PC_DONE, PC_TAIL, PC_HEAD, PC_LIMIT};
+    for (int k = 0; k < 4; ++k)
+        RT_CUDA_TRY(cudaMemcpyAsync(out4 + k, pc + idx[k], 4, cudaMemcpyDeviceToHost, c->stream));
+    RT_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return RT_OK;
+}

@@ -30,6 +30,9 @@ struct rt_ctx {
     size_t d_stage_bytes;
     unsigned int* d_counter;       // persistent-kernel work counters (64 slots)
     int* d_error;                  // device-side error flag
+    void* d_probe;                 // tile-probe heavy queue + claims of eye renders (render.cu), grown on demand
+    int64_t probe_tiles;
+    unsigned probe_epoch;          // claim tag of the last probed render
     // host-buffer transfer pipeline (hostio.cuh): copy-in / copy-out streams + events
     cudaStream_t io_in, io_out;
     cudaEvent_t io_ev[9];

@@ -396,11 +396,35 @@ struct SmemStack {
 // ray makes about half the dependent node fetches of the binary walk.  Same
 // triangle test, tie rule and conservative slab test as trace_ray.  The stack
 // holds at most 3 * ceil(height / 2) entries (checked by the caller).
+// Walk budget hook: Y::tick() runs before every walk step (node fetch or leaf test); when it
+// returns true the walk
+// stops and returns h.id == RT_YIELDED (the tile probe of render.cu).  NoYield folds away,
+// so trace_ray4 compiles to the plain walk.
+#define RT_YIELDED (-2)
+struct NoYield {
+    __device__ __forceinline__ bool tick() { return false; }
+};
+
+template <bool STATS, bool SPH, typename Stack, typename Y>
+__device__ __forceinline__ HitRec trace_ray4_y(const float4* __restrict__ bvh4, int root,
+                                               const float4* __restrict__ tris, const RayPre& R, float tmax,
+                                               uint32_t ray_mask, const Stack& stack, uint32_t& n_tests,
+                                               uint32_t& n_visits, const SphereView& sv, Y& y);
+
 template <bool STATS, bool SPH, typename Stack>
 __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, int root,
                                              const float4* __restrict__ tris, const RayPre& R, float tmax,
                                              uint32_t ray_mask, const Stack& stack, uint32_t& n_tests,
                                              uint32_t& n_visits, const SphereView& sv) {
+    NoYield y;
+    return trace_ray4_y<STATS, SPH>(bvh4, root, tris, R, tmax, ray_mask, stack, n_tests, n_visits, sv, y);
+}
+
+template <bool STATS, bool SPH, typename Stack, typename Y>
+__device__ __forceinline__ HitRec trace_ray4_y(const float4* __restrict__ bvh4, int root,
+                                               const float4* __restrict__ tris, const RayPre& R, float tmax,
+                                               uint32_t ray_mask, const Stack& stack, uint32_t& n_tests,
+                                               uint32_t& n_visits, const SphereView& sv, Y& y) {
     HitRec h;
     h.t = tmax; h.id = -1; h.u = 0.f; h.v = 0.f;
     // stack entries carry the child's entry distance: a popped entry that lies
@@ -410,6 +434,10 @@ __device__ __forceinline__ HitRec trace_ray4(const float4* __restrict__ bvh4, in
     stack.put(0, make_int2(RT_SENTINEL, 0));
     int node = root;
     while (node != RT_SENTINEL) {
+        if (y.tick()) {
+            h.id = RT_YIELDED;
+            return h;
+        }
         if (node >= 0) {
             // 4 slots of (lo.xyz, id), (hi.xyz, -)
             const float4* q = bvh4 + 8 * node;

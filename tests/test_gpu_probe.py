@@ -1,0 +1,90 @@
+"""Tile-probe scheduling of megakernel eye frames (csrc/render.cu, rt_set_probe_budget).
+
+The probe only reorders which 8x4 tiles are rendered first, so every frame must be
+bit-identical to the row-major schedule (budget 0): whole frames, partial edge tiles,
+several samples per pixel, pixel-range (chunked) renders and tile-band (multi-GPU) renders.
+The probe's own bookkeeping is checked through rt_probe_stats: the config-2 sphere queues
+its silhouette tiles, a uniformly costly soup stops probing early.
+"""
+
+import ctypes
+import contextlib
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2603_00292_b200 import _native, compile_scene, render_into, scenes
+
+pytestmark = pytest.mark.gpu
+
+
+@contextlib.contextmanager
+def probe_budget(b):
+    prev = ctypes.c_int32(0)
+    _native.check(_native.lib().rt_set_probe_budget(int(b), ctypes.byref(prev)))
+    try:
+        yield
+    finally:
+        _native.check(_native.lib().rt_set_probe_budget(prev.value, None))
+
+
+def probe_stats(scene):
+    out = np.zeros(4, np.uint32)
+    _native.check(_native.lib().rt_probe_stats(scene.tlas.ctx.handle, out.ctypes.data_as(ctypes.c_void_p)))
+    return {"probed": int(out[0]), "queued": int(out[1]), "popped": int(out[2]), "limit": int(out[3])}
+
+
+def frame(scene, w, h, spp=1, budget=24, **kw):
+    acc = torch.zeros((h * w, 4), dtype=torch.float32, device="cuda")
+    with probe_budget(budget):
+        render_into(scene, acc, w, h, spp, "eye", count_rays=False, **kw)
+    torch.cuda.synchronize()
+    return acc.cpu().numpy()
+
+
+@pytest.fixture(scope="module")
+def sphere(native):
+    return compile_scene(scenes.sphere_description())
+
+
+def test_sphere_frame_identical_and_silhouette_queued(sphere):
+    ref = frame(sphere, 1920, 1080, budget=0)
+    got = frame(sphere, 1920, 1080, budget=24)
+    st = probe_stats(sphere)
+    assert np.array_equal(ref, got)
+    ntiles = 240 * 270
+    assert st["limit"] == 0, st                       # the sphere never stops probing
+    assert st["probed"] >= ntiles, st
+    # the silhouette: a few percent of the tiles, all rendered from the queue
+    assert 0.01 * ntiles < st["queued"] < 0.125 * ntiles + 32, st
+    assert st["popped"] >= st["queued"], st
+
+
+@pytest.mark.parametrize("w,h,spp", [(1001, 603, 1), (640, 360, 3), (8, 4, 1), (37, 5, 2)])
+def test_ragged_frames_and_samples_identical(sphere, w, h, spp):
+    for budget in (1, 24):                            # budget 1: nearly every tile is queued
+        assert np.array_equal(frame(sphere, w, h, spp, budget=0), frame(sphere, w, h, spp, budget=budget))
+
+
+def test_pixel_ranges_and_bands_identical(sphere):
+    w, h = 1920, 1080
+    for kw in ({"pixels": (w * 200, w * 700)}, {"bands": (3, 1)}, {"bands": (4, 3)}, {"samples": (5, 6)}):
+        assert np.array_equal(frame(sphere, w, h, budget=0, **kw), frame(sphere, w, h, budget=24, **kw)), kw
+
+
+def test_uniform_soup_stops_probing(native):
+    sc = compile_scene(scenes.soup_description())
+    w, h = 3840, 2160
+    ref = frame(sc, w, h, budget=0)
+    got = frame(sc, w, h, budget=24)
+    st = probe_stats(sc)
+    assert np.array_equal(ref, got)
+    ntiles = 480 * 540
+    assert st["limit"] > 0, st                        # stopped: a large share of the probes ran out
+    assert st["probed"] == ((ntiles + 15) // 16) * 16, st   # every batch still completes
+    assert st["popped"] == 0 or st["popped"] <= st["queued"] + 4144, st
+
+
+def test_budget_is_validated(native):
+    assert _native.lib().rt_set_probe_budget(-1, None) != 0
