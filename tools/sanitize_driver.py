@@ -63,5 +63,14 @@ cube = names.index("cube")
 two.tlas.blases[cube].refit(vertices=desc.meshes["cube"].vertices * 1.1)
 two.tlas.refresh_instance_bounds()
 render_frame(two, 24, 16, 2, "pt", cfg=IntegratorConfig(max_depth=3))
+# tile-probe scheduling of eye frames: queue + claims (budget 24), near-everything heavy with
+# the cap's early stop (budget 2), probe off
+sph = compile_scene(scenes.sphere_description(200, 400))
+for b in (24, 2, 0):
+    _native.check(_native.lib().rt_set_probe_budget(b, None))
+    acc = torch.zeros((128 * 96, 4), dtype=torch.float32, device="cuda")
+    render_into(sph, acc, 128, 96, 1, "eye", count_rays=False)
+    render_into(sph, acc, 128, 96, 2, "eye", count_rays=False, bands=(2, 1))
+_native.check(_native.lib().rt_set_probe_budget(24, None))
 torch.cuda.synchronize()
 print("sanitize driver ok")
