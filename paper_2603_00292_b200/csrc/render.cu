@@ -285,10 +285,11 @@ __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* 
 // walked under a budget of walk steps (a separate instantiation of the walk: the budget
 // exit is not in the rendering walk's loop); a tile whose probe runs out of budget is
 // pushed on a heavy-tile queue, and every warp takes queued heavy tiles before row-major
-// ones (whoever claims a tile first renders it).  On the config-2 sphere the probe (lane 12 of the tile) flags every tile
-// whose slowest ray needs >= 100 steps at a budget of 24 (8 % of the tiles,
-// tools/diag_probe.py).  Only the schedule changes: each pixel is rendered once, by one
-// lane, exactly as before (claims: one atomicMax of the render's epoch per tile).
+// ones (whoever claims a tile first renders it).  On the config-2 sphere the probe (lane 12
+// of the tile) flags every tile whose slowest ray needs >= 100 steps at a budget of 24 (8 %
+// of the tiles, tools/diag_probe.py).  Only the schedule changes: each pixel is rendered
+// once, by one lane, exactly as before (claims: one atomicMax of the render's epoch per
+// tile).
 #ifndef RT_PROBE_BUDGET
 #define RT_PROBE_BUDGET 24      // walk steps; the RT_PROBE_BUDGET env overrides (0: no probe)
 #endif

@@ -5,9 +5,10 @@
 # plus the launch list of two bench.py config-2 steps.  Outputs under gpurun_out/.
 set -x
 K='regex:lbvh_|onesweep'
-ncu --set full --clock-control none --import-source on -k "$K" --launch-skip 8 --launch-count 8 \
+# one 30-bit build = 7 kernels (bounds, Morton + histograms, 3 x onesweep10, emit, global emit)
+ncu --set full --clock-control none --import-source on -k "$K" --launch-skip 7 --launch-count 7 \
     -o gpurun_out/r2_build -f python tools/drive_build.py 2 30 > gpurun_out/r2_ncu_build.log 2>&1
-ncu --set full --clock-control none --import-source on -k "$K" --launch-skip 8 --launch-count 8 \
+ncu --set full --clock-control none --import-source on -k "$K" --launch-skip 7 --launch-count 7 \
     -o gpurun_out/r2_soup_build -f python tools/drive_build.py 2 30 soup > gpurun_out/r2_ncu_soup_build.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:pt_megakernel --launch-skip 1 --launch-count 1 \
     -o gpurun_out/r2_mega_eye -f python tools/drive_render.py eye 2 > gpurun_out/r2_ncu_eye.log 2>&1
