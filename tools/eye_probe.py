@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=15)
     ap.add_argument("--soup", action="store_true")
+    ap.add_argument("--bands", type=int, default=1, help="render rank 0's share of an N-way tile-band split")
     a = ap.parse_args()
     import torch
     from paper_2603_00292_b200 import compile_scene, render_into, scenes
@@ -31,7 +32,8 @@ def main():
     for name, desc, W, H in cases:
         sc = compile_scene(desc)
         acc = torch.zeros((H * W, 4), dtype=torch.float32, device="cuda")
-        render_into(sc, acc, W, H, 1, "eye", count_rays=False)
+        bands = (a.bands, 0) if a.bands > 1 else None
+        render_into(sc, acc, W, H, 1, "eye", count_rays=False, bands=bands)
         torch.cuda.synchronize()
         out[f"{name}_sha"] = hashlib.sha1(acc.cpu().numpy().tobytes()).hexdigest()[:16]
         ts = []
@@ -39,7 +41,7 @@ def main():
             flush.fill_(k & 0xFF)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            render_into(sc, acc, W, H, 1, "eye", count_rays=False)
+            render_into(sc, acc, W, H, 1, "eye", count_rays=False, bands=bands)
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
