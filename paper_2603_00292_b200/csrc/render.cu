@@ -313,11 +313,12 @@ __device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
 // pop a heavy tile (lane 0): -1 when none is queued.  The queue head only moves by
 // atomicAdd (a CAS loop livelocks under thousands of polling warps); a ticket taken past
 // the producers' reservations waits for its slot to be filled, or gives up once every
-// probe batch is complete (completion counts tiles: it reaches `ntiles32` exactly) and the
-// final reservation count is at or below the ticket.  The control words (F.probe_ctl) sit on
+// probe batch is complete (completion counts tiles: it reaches `ntiles_b`, the tile count
+// rounded up to whole batches, exactly) and the final reservation count is at or below the
+// ticket.  The control words (F.probe_ctl) sit on
 // their own 128-B lines, away from the frame's work counter: a store into the line of the
 // work counter's atomics, once per warp, was measured to double the frame.
-__device__ __forceinline__ int64_t heavy_pop(const FrameConst& F, unsigned* pc, unsigned ntiles32) {
+__device__ __forceinline__ int64_t heavy_pop(const FrameConst& F, unsigned* pc, unsigned ntiles_b) {
     if (ld_volatile_u32(pc + PC_HEAD) >= ld_volatile_u32(pc + PC_TAIL)) return -1;
     const unsigned h = atomicAdd(pc + PC_HEAD, 1u);
     while (true) {
@@ -325,8 +326,62 @@ __device__ __forceinline__ int64_t heavy_pop(const FrameConst& F, unsigned* pc, 
         if ((unsigned)(e >> 32) == F.epoch) return (int64_t)(e & 0xFFFFFFFFull);
         unsigned done;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(done) : "l"(pc + PC_DONE) : "memory");
-        if (done >= ntiles32 && h >= ld_volatile_u32(pc + PC_TAIL)) return -1;
+        if (done >= ntiles_b && h >= ld_volatile_u32(pc + PC_TAIL)) return -1;
     }
+}
+
+// Lane 0 of a probing warp: take the next probe batch (its first tile; >= ntiles when none
+// is left) and decide whether it is walked.  When more than 1/8 of the probed tiles (after
+// the first 4096) or tiles / 8 in all came out heavy, the scene is uniformly costly (no tail
+// to fix: the 10M soup flags 31 %) and probing stops: the remaining batches are taken and
+// completed without walks (the completion count must reach every batch: heavy_pop's
+// termination test), and the first tile no walk can have touched is published (+ 1, so 0
+// means "not stopped") in PC_LIMIT: row-major fetches claim only the tiles below it.  Batches are taken by acq_rel
+// adds and the stopping warp reads the batch counter by one after its stop store, so a batch
+// at or above the limit is always taken after the stop is visible to its prober.
+__device__ __forceinline__ unsigned probe_take(const FrameConst& F, unsigned* pc, int64_t ntiles, unsigned& stop) {
+    unsigned pb;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(pb) : "l"(pc + PC_TAKEN), "r"(PROBE_BATCH)
+                 : "memory");
+    const unsigned nh = ld_volatile_u32(pc + PC_TAIL);
+    const bool seen_stop = ld_volatile_u32(pc + PC_STOP) != 0;
+    stop = seen_stop || nh >= (unsigned)(ntiles / RT_PROBE_CAP_DIV) || (pb >= 4096u && nh * RT_PROBE_CAP_DIV > pb);
+    if (stop && !seen_stop) {
+        *reinterpret_cast<volatile unsigned*>(pc + PC_STOP) = 1u;
+        unsigned lim;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 0;" : "=r"(lim) : "l"(pc + PC_TAKEN) : "memory");
+        atomicMax(pc + PC_LIMIT, lim + 1u);
+    }
+    return pb;
+}
+
+// Lane 0 of a rendering warp in a probed frame: the first unit of its next tile, -1 to fetch
+// again (the tile was taken by someone else), >= nunits when the frame is done.  Queued heavy
+// tiles come first (the queue is polled until it is drained after every probe batch
+// completed, or abandoned when probing stopped early: its tiles are unclaimed and go back to
+// row-major order, which L2 rewards on such scenes), then row-major tiles, each claimed by
+// one atomicMax of the render's epoch (tiles past the probe's limit need no claim).
+// qopen / limit: this warp's shared-memory copies (see the kernel).
+__device__ __forceinline__ long long probed_next_tile(const FrameConst& F, unsigned* counter, unsigned* pc,
+                                                      int64_t ntiles, unsigned& qopen, unsigned& limit) {
+    if (qopen) {
+        const unsigned ntiles_b = (unsigned)((ntiles + PROBE_BATCH - 1) / PROBE_BATCH * PROBE_BATCH);
+        const unsigned lim = ld_volatile_u32(pc + PC_LIMIT);
+        if (lim) {
+            limit = lim;
+            qopen = 0u;
+        } else {
+            const int64_t ht = heavy_pop(F, pc, ntiles_b);
+            if (ht >= 0) return atomicMax(F.claims + ht, F.epoch) < F.epoch ? ht * 32 : -1;
+            if (ld_volatile_u32(pc + PC_DONE) >= ntiles_b && ld_volatile_u32(pc + PC_HEAD) >= ld_volatile_u32(pc + PC_TAIL))
+                qopen = 0u;
+        }
+    }
+    const long long b = atomicAdd(counter, 32u);
+    if (b < F.nunits && (limit == 0u || (b >> 5) + 1 < (long long)limit) &&
+        atomicMax(F.claims + (b >> 5), F.epoch) >= F.epoch)
+        return -1;
+    return b;
 }
 
 // ---- K7: megakernel --------------------------------------------------------
@@ -385,36 +440,17 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
             if ((int64_t)b >= F.nunits) break;
             base = b;
         } else if (probing) {
-            // probe 32 tiles (one ray each, budgeted walk), claim and queue the heavy ones.  When
-            // more than 1/8 of the probed tiles (after the first 4096) or tiles / 8 in all come
-            // out heavy, the scene is uniformly costly (no tail to fix: the 10M soup flags 31 %)
-            // and probing stops: the remaining batches are taken and completed without walks (the
-            // completion count must reach every batch: heavy_pop's termination test), and the
-            // first batch no walk can have touched is published as PC_LIMIT + 1, below which
-            // row-major fetches still claim.  Batches are taken by acq_rel adds and the stopping
-            // warp reads the batch counter by one after its stop store, so a batch at or above
-            // the limit is always taken after the stop is visible to its prober.
+            // one probe batch: PROBE_BATCH tiles, one budgeted walk each (lanes < PROBE_BATCH),
+            // the heavy ones queued
             unsigned pb = 0, stop = 0;
-            if (lane == 0) {
-                asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(pb) : "l"(pc + PC_TAKEN), "r"(PROBE_BATCH) : "memory");
-                const unsigned nh = ld_volatile_u32(pc + PC_TAIL);
-                const bool seen_stop = ld_volatile_u32(pc + PC_STOP) != 0;
-                stop = seen_stop || nh >= (unsigned)(ntiles / RT_PROBE_CAP_DIV) ||
-                       (pb >= 4096u && nh * RT_PROBE_CAP_DIV > pb);
-                if (stop && !seen_stop) {
-                    *reinterpret_cast<volatile unsigned*>(pc + PC_STOP) = 1u;
-                    unsigned lim;
-                    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 0;" : "=r"(lim) : "l"(pc + PC_TAKEN) : "memory");
-                    atomicMax(pc + PC_LIMIT, lim + 1u);
-                }
-            }
+            if (lane == 0) pb = probe_take(F, pc, ntiles, stop);
             pb = __shfl_sync(RT_FULL, pb, 0);
             stop = __shfl_sync(RT_FULL, stop, 0);
-            const int64_t t = (int64_t)pb + lane;
             if ((int64_t)pb >= ntiles) {
                 probing = false;
                 continue;
             }
+            const int64_t t = (int64_t)pb + lane;
             bool heavy = false;
             int64_t ppix;
             if (!stop && lane < PROBE_BATCH && t < ntiles && unit_pixel(F, t * 32 + PROBE_LANE, ppix)) {
@@ -427,53 +463,23 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
                 heavy = trace_ray4_y<false, SPH>(bvh4, root4, tris, R, 1e30f, RT_FULL, walk_stack, nt, nv, sv, y).id ==
                         RT_YIELDED;
             }
-            if (heavy) {                                 // (the cap may be overshot by a batch)
+            if (heavy) {
                 const unsigned slot = atomicAdd(pc + PC_TAIL, 1u);
                 *reinterpret_cast<volatile unsigned long long*>(F.heavy_q + slot) =
                     ((unsigned long long)F.epoch << 32) | (unsigned long long)t;
             }
             __syncwarp();
-            // this batch's queue slots before its completion count (a release reduction: a
-            // full fence here would also invalidate the SM's L1, which the walks live in)
+            // the batch's queue slots before its completion count (a release reduction: a full
+            // fence here would also invalidate the SM's L1, which the walks live in)
             if (lane == 0)
                 asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(pc + PC_DONE), "r"(PROBE_BATCH) : "memory");
             continue;
         } else {
-            // queued heavy tiles first (polled until the queue is drained after every probe
-            // batch completed), then row-major tiles nobody has claimed
             long long b = 0;
-            if (lane == 0) {
-                const int w = threadIdx.x >> 5;
-                int64_t ht = -1;
-                if (s_qopen[w]) {
-                    const unsigned ntiles32 = (unsigned)((ntiles + PROBE_BATCH - 1) / PROBE_BATCH * PROBE_BATCH);
-                    const unsigned lim = ld_volatile_u32(pc + PC_LIMIT);
-                    if (lim) s_limit[w] = lim;
-                    if (lim) {
-                        // probing stopped (uniformly costly scene): the queued tiles go back to
-                        // row-major order (they are unclaimed), which L2 rewards on such scenes
-                        s_qopen[w] = 0u;
-                    } else {
-                        ht = heavy_pop(F, pc, ntiles32);
-                        if (ht < 0 && ld_volatile_u32(pc + PC_DONE) >= ntiles32 &&
-                            ld_volatile_u32(pc + PC_HEAD) >= ld_volatile_u32(pc + PC_TAIL))
-                            s_qopen[w] = 0u;
-                    }
-                }
-                if (ht >= 0) {
-                    // a popped tile is claimed here (a row-major fetch may have taken it first)
-                    b = atomicMax(F.claims + ht, F.epoch) < F.epoch ? ht * 32 : -1;
-                } else {
-                    b = atomicAdd(counter, 32u);
-                    const unsigned lim = s_limit[w];
-                    if (b < F.nunits && (lim == 0u || (b >> 5) + 1 < (long long)lim) &&
-                        atomicMax(F.claims + (b >> 5), F.epoch) >= F.epoch)
-                        b = -1;
-                }
-            }
+            if (lane == 0) b = probed_next_tile(F, counter, pc, ntiles, s_qopen[threadIdx.x >> 5], s_limit[threadIdx.x >> 5]);
             b = __shfl_sync(RT_FULL, b, 0);
             if (b >= F.nunits) break;
-            if (b < 0) continue;
+            if (b < 0) continue;                         // taken by someone else: fetch again
             base = b;
         }
 #if RT_TIMELINE
