@@ -107,8 +107,13 @@ __device__ __forceinline__ void load_tri(const float* tris, int64_t i, float t[9
 #ifndef RT_WIDE_GATHER
 #define RT_WIDE_GATHER 1
 #endif
+// The gathered row is used once: not allocating it in L1 (L1::no_allocate, or .cg) took the
+// 10M emit 0.975 -> 0.946 ms (same box, 2 x 30 builds); L1::evict_first did not help.
+#ifndef RT_GATHER_LD
+#define RT_GATHER_LD "ld.global.nc.L1::no_allocate.v8.f32"
+#endif
 __device__ __forceinline__ void ldg256(const float* p, float w[8]) {
-    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm(RT_GATHER_LD " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=f"(w[0]), "=f"(w[1]), "=f"(w[2]), "=f"(w[3]), "=f"(w[4]), "=f"(w[5]), "=f"(w[6]), "=f"(w[7])
         : "l"(p));
 }
