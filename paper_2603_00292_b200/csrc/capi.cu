@@ -233,6 +233,16 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
     ALLOC(s->emit_items, 48 * (2 * n + 512));      // EmitNode segments of EMIT_T per emit block
     ALLOC(s->seg_count, sizeof(unsigned int) * (n / 64 + 2));   // one count per emit block (EMIT_T >= 64)
 #undef ALLOC
+    {
+        // the sort scratch starts zeroed; after that every build's last kernel zeroes it again
+        // for the next build (lbvh.cu), so no build pays a memset up front
+        cudaError_t _e = cudaMemsetAsync(s->sort_scratch, 0, sizeof(unsigned int) * s->sort_scratch_words, c->stream);
+        if (_e != cudaSuccess) {
+            rt_set_error("cudaMemsetAsync failed: %s", cudaGetErrorString(_e));
+            rt_scene_destroy(s);
+            return RT_ECUDA;
+        }
+    }
     if (reinterpret_cast<uintptr_t>(s->tris) & 31) {     // the build's 256-bit row gathers
         rt_set_error("triangle rows are not 32-B aligned");
         rt_scene_destroy(s);

@@ -340,12 +340,20 @@ __global__ void __launch_bounds__(128) lbvh_emit_global_kernel(const K* __restri
                                                               int* slot_range, float4* slot_box,
                                                               const EmitNode* __restrict__ items,
                                                               const unsigned int* __restrict__ seg_count,
-                                                              int64_t n_blocks) {
+                                                              int64_t n_blocks, uint4* __restrict__ scratch,
+                                                              int64_t scratch_n16) {
     // one warp per segment, so every item climbs concurrently (no thread takes two)
     pdl_wait();                                 // the emit kernel's items and slot resets
-    const int64_t seg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    if (seg >= n_blocks) return;
-    const unsigned cnt = __ldg(seg_count + seg);
-    for (unsigned j = threadIdx.x & 31; j < cnt; j += 32)
-        climb_global(keys, n, child, nodes, bvh4, slot_range, slot_box, items[seg * EMIT_T + j]);
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t seg = gt >> 5;
+    if (seg < n_blocks) {
+        const unsigned cnt = __ldg(seg_count + seg);
+        for (unsigned j = threadIdx.x & 31; j < cnt; j += 32)
+            climb_global(keys, n, child, nodes, bvh4, slot_range, slot_box, items[seg * EMIT_T + j]);
+    }
+    // the sort scratch (digit histograms, tile counters, bounds accumulators, look-back
+    // status) is dead now: zero it for the next build here, off the climb's critical path,
+    // instead of a memset ahead of every build
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = gt; k < scratch_n16; k += stride) scratch[k] = make_uint4(0u, 0u, 0u, 0u);
 }

@@ -743,8 +743,9 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     cudaStream_t st = ctx->stream;
     const int grid_stream = ctx->num_sms * TRI_BLOCKS_PER_SM;
     constexpr int NB = 1 << DB;
-    // one memset zeroes the sort scratch: digit histograms, tile counters, the
-    // centroid-bound accumulators, the emit item count and the look-back status
+    // the sort scratch (digit histograms, tile counters, the centroid-bound accumulators and
+    // the look-back status) arrives zeroed: at allocation, then by the previous build's
+    // lbvh_emit_global_kernel
     int gb = (int)((n + 255) / 256);
     if (gb > grid_stream) gb = grid_stream;
     constexpr int64_t TILE = DB == 10 ? TILE10 : SortCfg<K>::TILE;
@@ -753,9 +754,7 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     unsigned int* counters = hist + PASSES * NB;             // [0, 8) tile counters, [8, 14) cb_enc, [16] emit count
     unsigned int* cb_enc = counters + 8;
     unsigned int* status = counters + 32;                    // PASSES * tiles * NB
-    size_t words = (size_t)PASSES * NB + 32 + (size_t)PASSES * tiles * NB;
     RT_PROF(ctx, 0);
-    RT_CUDA_TRY(cudaMemsetAsync(s->sort_scratch, 0, words * sizeof(unsigned int), st));
     // K1
     lbvh_bounds_kernel<<<gb, 256, 0, st>>>(s->tris, n, cb_enc);
     // K2
@@ -807,7 +806,8 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
                            s->bvh4, items, s->seg_count, (int*)s->flags, s->leaf_box));
     RT_CUDA_TRY(launch_pdl(lbvh_emit_global_kernel<K>, (unsigned)((n_blocks * 32 + 127) / 128), 128u, st,
                            (const K*)kin, n, s->child, s->nodes, s->bvh4, (int*)s->flags, s->leaf_box,
-                           (const EmitNode*)items, (const unsigned int*)s->seg_count, n_blocks));
+                           (const EmitNode*)items, (const unsigned int*)s->seg_count, n_blocks,
+                           reinterpret_cast<uint4*>(s->sort_scratch), (int64_t)(s->sort_scratch_words / 4)));
     RT_PROF(ctx, 6);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
@@ -836,5 +836,6 @@ size_t rt_sort_scratch_words(int64_t n) {
     const int64_t tiles32 = (n + TILE10 - 1) / TILE10;
     const size_t w8 = (size_t)8 * RADIX + 32 + (size_t)8 * tiles * RADIX;
     const size_t w10 = (size_t)3 * R10 + 32 + (size_t)3 * tiles32 * R10;
-    return w8 > w10 ? w8 : w10;
+    const size_t w = w8 > w10 ? w8 : w10;
+    return (w + 3) & ~(size_t)3;        // whole 16-B units (zeroed as uint4 by the emit hand-off)
 }
