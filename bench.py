@@ -540,7 +540,7 @@ def run_ours(args, ws, rank, local):
                   "sm_issue_active_pct_ncu": nc.get("issue_active_pct"),
                   "traffic": trace_traffic, "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch, "
                                                               "cold caches)",
-                  "hbm_algorithmic": {"achieved": hbm_ach, "peak": peak_gbs, "unit": "GB/s", "frac": hbm_ach / peak_gbs,
+                  "hbm_algorithmic": {"achieved": hbm_ach, "peak": peak_gbs, "unit": "GB/s", "ratio_to_hbm_peak": hbm_ach / peak_gbs,
                                       "bytes_per_ray": bpr, "peak_source": peak_src,
                                       "bytes_formula": f"128 B x {n_nodes:.2f} BVH4 node fetches (4 child boxes + ids) "
                                                        f"+ 48 B x {n_tests:.2f} triangle tests + 32 B accumulation RMW "
