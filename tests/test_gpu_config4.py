@@ -6,12 +6,14 @@ Two checks, SURVEY 8(d) config 4 (the config with the thinnest margin against th
   bit-plane-ballot ranking of the onesweep sort (n >= 2^21, csrc/lbvh.cu), so this is
   the test that pins that path at 30 bits.  Every downloaded field must equal
   oracle.lbvh_build (the frozen Karras restatement).
-* Hit-ID agreement on 1M rays sampled from the 3840x2160 jittered frame, against the
+* Hit-ID agreement on every ray of the 3840x2160 jittered frame (8,294,400), against the
   float64 oracle traversing the GPU's own downloaded LBVH (hits are topology-independent,
   SURVEY F2, so no 10M SAH build is needed; oracle.lbvh_as_reference_nodes wraps it in
   the reference's Blas node schema, accel.py:179-187).  Agreement is reported over all
   rays and over hit rays, as 8(d) asks.  Reference harness: accel.py:1128-1156.
 """
+
+import os
 
 import numpy as np
 import pytest
@@ -22,7 +24,7 @@ from paper_2603_00292_b200.integrators import raygen
 pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 N_TRIS = 10_000_000
-N_RAYS = 1_000_000
+N_RAYS = 3840 * 2160      # the whole frame
 ID_AGREE = 0.9999
 T_REL = 1e-5
 
@@ -45,7 +47,7 @@ def test_config4_lbvh_bit_exact_10m(native, oracle_mod, soup, bits):
     assert np.array_equal(info["root_box"], lb["root_box"])
 
 
-def test_config4_hits_10m_full_frame_sample(native, oracle_mod, soup):
+def test_config4_hits_10m_full_frame(native, oracle_mod, soup):
     sc = compile_scene(soup, "lbvh30")
     got = sc.tlas.download()
     got["root_box"] = sc.tlas.info()["root_box"]
@@ -59,11 +61,11 @@ def test_config4_hits_10m_full_frame_sample(native, oracle_mod, soup):
                                  oracle_mod.camera13(cam.origin, cam.right, cam.up, cam.distortion),
                                  blas_nodes=[nodes])
     rays = raygen(sc, 3840, 2160, sample=0, seed=0).cpu().numpy()
-    sel = np.sort(np.random.default_rng(4).choice(rays.shape[0], N_RAYS, replace=False))
-    O = rays[sel, 0:3].astype(np.float64)
-    D = rays[sel, 4:7].astype(np.float64)
+    assert rays.shape[0] == N_RAYS
+    O = rays[:, 0:3].astype(np.float64)
+    D = rays[:, 4:7].astype(np.float64)
     t, inst, prim = closest_hit_batch(sc, O, D)[:3]
-    rt, ri, rp = orc.closest_hit_batch(O, D, workers=16)[:3]
+    rt, ri, rp = orc.closest_hit_batch(O, D, workers=max(16, os.cpu_count() or 16))[:3]
     same = (inst == ri) & (prim == rp)
     hit = (ri >= 0) | (inst >= 0)
     agree_all = float(same.mean())
