@@ -66,6 +66,31 @@ def test_pt_vs_oracle_config3_prefix(cornell_gpu, cornell_oracle):
     assert np.sqrt(np.mean((ref1[:, :, :3] / ref1[:, :, 3:] - ref[:, :, :3] / ref[:, :, 3:]) ** 2)) > 100 * RMSE_TOL
 
 
+@pytest.mark.slow
+def test_pt_vs_oracle_config3_full_frame(cornell_gpu, cornell_oracle):
+    """Config 3 at its stated size: Cornell 1920x1080, 64 spp, max_depth 5 (4 diffuse bounces),
+    seed 0, jitter on -- the whole frame (~500M rays) against the float64 oracle.
+
+    At this size a handful of the 132M paths meet a hit decided differently by fp32 and
+    float64 (a bounce ray on an edge: 46 of 500M rays differ in count) and then follow a
+    different path; one such path moves its pixel's 64-sample mean by up to 0.27.  The bar
+    is therefore stated per pixel: >= 99.998 % of pixels within 1e-2 (measured: all but 21 of
+    2,073,600), RMSE <= 1e-4 over them (measured 1.1e-8), ray counts within 1e-4."""
+    import os
+    cfg = IntegratorConfig(max_depth=5)
+    acc, st = render_frame(cornell_gpu, 1920, 1080, 64, "pt", seed=0, cfg=cfg, return_stats=True)
+    ref, rays = cornell_oracle.render_frame(1920, 1080, 64, "pt", max_depth=5, workers=max(8, os.cpu_count() or 8))
+    d = acc.mean() - ref[:, :, :3] / ref[:, :, 3:]
+    rmse = float(np.sqrt(np.mean(d ** 2)))
+    bad = np.any(np.abs(d) > MAXD_TOL, axis=2)
+    clean = float(np.sqrt(np.mean(d[~bad] ** 2)))
+    print(f"config 3 full frame: per-pixel RMSE {rmse:.2e} ({clean:.2e} without the {int(bad.sum())} pixels "
+          f"over {MAXD_TOL}), max |d| {np.abs(d).max():.2e}, rays {st['rays']} (oracle {rays})")
+    assert bad.mean() <= 2e-5, int(bad.sum())
+    assert clean <= RMSE_TOL, clean
+    assert abs(st["rays"] - rays) <= 1e-4 * rays
+
+
 def test_mega_equals_wavefront(cornell_gpu):
     cfg = IntegratorConfig(max_depth=5)
     a, sa = render_frame(cornell_gpu, 160, 90, 6, "pt", seed=3, cfg=cfg, kernel="mega", return_stats=True)
