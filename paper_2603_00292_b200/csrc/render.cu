@@ -96,8 +96,9 @@ __device__ __forceinline__ void onb(float nx, float ny, float nz, float t[3], fl
 }
 
 // integrators.py:345-351 + camera.py:81-97: stream, jitter, primary ray
-__device__ __forceinline__ void start_path(const FrameConst& F, int64_t pix, int s, PathState& P) {
-    rt_stream_for(F.seed, (uint64_t)pix, (uint64_t)s, P.state, P.inc);
+__device__ __forceinline__ void start_path(const FrameConst& F, int64_t pix, int s, PathState& P,
+                                           uint64_t hp) {
+    rt_stream_from_pixel(hp, (uint64_t)s, P.state, P.inc);
     float ju = 0.0f, jv = 0.0f;
     if (F.jitter) {
         ju = rt_uniform(P.state, P.inc);
@@ -110,6 +111,10 @@ __device__ __forceinline__ void start_path(const FrameConst& F, int64_t pix, int
     P.ox = F.cam[0]; P.oy = F.cam[1]; P.oz = F.cam[2];
     P.tr = P.tg = P.tb = 1.0f;
     P.rr = P.rg = P.rb = 0.0f;
+}
+
+__device__ __forceinline__ void start_path(const FrameConst& F, int64_t pix, int s, PathState& P) {
+    start_path(F, pix, s, P, rt_stream_pixel(F.seed, (uint64_t)pix));
 }
 
 // One closest-hit result applied to the path (integrators.py:129-141 eye,
@@ -491,9 +496,10 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
             // accumulate sample by sample into the running sums, exactly like
             // the wavefront's per-wave accumulate, so both are bit-identical
             float4 a = accum[pix];
+            const uint64_t hp = rt_stream_pixel(F.seed, (uint64_t)pix);   // per pixel, not per sample
             for (int s = s0; s < s1; ++s) {
                 PathState P;
-                start_path(F, pix, s, P);
+                start_path(F, pix, s, P, hp);
                 if constexpr (INTEG == RT_INTEG_AO) {
                     const float v = sample_ao<SPH>(F, bvh4, root4, tris, attr, P, stack, rays, sv);
                     P.rr = P.rg = P.rb = v;

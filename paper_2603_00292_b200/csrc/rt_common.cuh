@@ -176,6 +176,19 @@ __device__ __forceinline__ uint32_t rt_pcg_next(uint64_t& state, uint64_t inc) {
     uint32_t rot = (uint32_t)(old >> 59);
     return __funnelshift_r(xs, xs, rot);   // rotate right
 }
+// the per-pixel part of the stream hash, mix(mix(seed) ^ pix): computed once per pixel by
+// callers that draw several samples of it
+__device__ __forceinline__ uint64_t rt_stream_pixel(uint64_t seed, uint64_t pix) {
+    return rt_mix64(rt_mix64(seed) ^ pix);
+}
+__device__ __forceinline__ void rt_stream_from_pixel(uint64_t hp, uint64_t s, uint64_t& state, uint64_t& inc) {
+    uint64_t h = rt_mix64(hp ^ s);
+    inc = (rt_mix64(h ^ 0xDA3E39CB94B95BDBull) << 1) | 1ull;
+    state = 0;
+    rt_pcg_next(state, inc);
+    state += h;
+    rt_pcg_next(state, inc);
+}
 __device__ __forceinline__ void rt_stream_for(uint64_t seed, uint64_t pix, uint64_t s, uint64_t& state,
                                               uint64_t& inc) {
     uint64_t h = rt_mix64(rt_mix64(rt_mix64(seed) ^ pix) ^ s);
