@@ -320,9 +320,9 @@ __device__ __forceinline__ unsigned ld_volatile_u32(const unsigned* p) {
 // the producers' reservations waits for its slot to be filled, or gives up once every
 // probe batch is complete (completion counts tiles: it reaches `ntiles_b`, the tile count
 // rounded up to whole batches, exactly) and the final reservation count is at or below the
-// ticket.  The control words (F.probe_ctl) sit on
-// their own 128-B lines, away from the frame's work counter: a store into the line of the
-// work counter's atomics, once per warp, was measured to double the frame.
+// ticket.  The control words (F.probe_ctl) sit on their own 128-B lines, away from the
+// frame's work counter: a store into the line of the work counter's atomics, once per warp,
+// was measured to double the frame.
 __device__ __forceinline__ int64_t heavy_pop(const FrameConst& F, unsigned* pc, unsigned ntiles_b) {
     if (ld_volatile_u32(pc + PC_HEAD) >= ld_volatile_u32(pc + PC_TAIL)) return -1;
     const unsigned h = atomicAdd(pc + PC_HEAD, 1u);
@@ -340,10 +340,11 @@ __device__ __forceinline__ int64_t heavy_pop(const FrameConst& F, unsigned* pc, 
 // the first 4096) or tiles / 8 in all came out heavy, the scene is uniformly costly (no tail
 // to fix: the 10M soup flags 31 %) and probing stops: the remaining batches are taken and
 // completed without walks (the completion count must reach every batch: heavy_pop's
-// termination test), and the first tile no walk can have touched is published (+ 1, so 0
-// means "not stopped") in PC_LIMIT: row-major fetches claim only the tiles below it.  Batches are taken by acq_rel
-// adds and the stopping warp reads the batch counter by one after its stop store, so a batch
-// at or above the limit is always taken after the stop is visible to its prober.
+// termination test), and the first tile no walk can have touched is published in PC_LIMIT
+// (+ 1, so 0 means "not stopped"): row-major fetches claim only the tiles below it.
+// Batches are taken by acq_rel adds and the stopping warp reads the batch counter by one
+// after its stop store, so a batch at or above the limit is always taken after the stop is
+// visible to its prober.
 __device__ __forceinline__ unsigned probe_take(const FrameConst& F, unsigned* pc, int64_t ntiles, unsigned& stop) {
     unsigned pb;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(pb) : "l"(pc + PC_TAKEN), "r"(PROBE_BATCH)
