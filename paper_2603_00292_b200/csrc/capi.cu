@@ -156,6 +156,7 @@ void rt_ctx_destroy(rt_ctx* c) {
     cudaFree(c->d_counter);
     cudaFree(c->d_error);
     if (c->d_probe) cudaFree(c->d_probe);
+    if (c->d_chunk_done) cudaFree(c->d_chunk_done);
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
     cudaStreamDestroy(c->own_stream);

@@ -51,6 +51,10 @@ struct FrameConst {
     unsigned* claims;              // (tiles)
     unsigned long long* heavy_q;   // (tiles) (epoch << 32 | tile) of heavy tiles, in push order
     unsigned* probe_ctl;           // PC_WORDS control words (zeroed per render)
+    // sample chunks of multi-sample frames (see the megakernel): 0 = one unit per tile
+    int chunk;                     // samples per unit
+    int nchunks;
+    unsigned* chunk_done;          // (tiles) units of the tile finished, in sample order (zeroed per render)
 };
 
 // unit k -> pixel; false for the padding lanes of partial edge tiles
@@ -295,6 +299,9 @@ __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* 
 // of the tiles, tools/diag_probe.py).  Only the schedule changes: each pixel is rendered
 // once, by one lane, exactly as before (claims: one atomicMax of the render's epoch per
 // tile).
+#ifndef RT_PT_CHUNK
+#define RT_PT_CHUNK 8           // samples per work unit of multi-sample PT / AO frames (0: whole tiles)
+#endif
 #ifndef RT_PROBE_BUDGET
 #define RT_PROBE_BUDGET 24      // walk steps; the RT_PROBE_BUDGET env overrides (0: no probe)
 #endif
@@ -439,7 +446,28 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
                    (int64_t)(blockIdx.x * (MEGA_THREADS / 32) + (threadIdx.x >> 5)) < (ntiles + PROBE_BATCH - 1) / PROBE_BATCH;
     while (true) {
         int64_t base;
-        if (!probe_on) {
+        int cs0 = s0, cs1 = s1;                     // this unit's sample window
+        int64_t ctile = -1;                         // chunked frames: the unit's tile
+        if (F.nchunks > 1) {
+            // sample-chunk units, chunk-major: unit u = (chunk u / tiles, tile u % tiles).  A
+            // tile's chunk c starts only after its chunk c - 1 has finished (chunk_done), so
+            // every pixel still accumulates its samples in order; one sweep apart, the wait is
+            // all but never taken.  The frame's tail shrinks from one tile x all samples to one
+            // tile x one chunk.
+            unsigned u = 0;
+            if (lane == 0) u = atomicAdd(counter, 1u);
+            u = __shfl_sync(RT_FULL, u, 0);
+            if ((int64_t)u >= ntiles * F.nchunks) break;
+            const int c = (int)(u / ntiles);
+            ctile = (int64_t)u - (int64_t)c * ntiles;
+            cs0 = s0 + c * F.chunk;
+            cs1 = min(s1, cs0 + F.chunk);
+            if (c > 0 && lane == 0) {
+                while (ld_volatile_u32(F.chunk_done + ctile) < (unsigned)c) __nanosleep(256);
+            }
+            __syncwarp();                           // (the sums are then read from L2, below)
+            base = ctile * 32;
+        } else if (!probe_on) {
             unsigned b = 0;
             if (lane == 0) b = atomicAdd(counter, 32u);
             b = __shfl_sync(RT_FULL, b, 0);
@@ -496,9 +524,11 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
         if (i < F.nunits && unit_pixel(F, i, pix)) {
             // accumulate sample by sample into the running sums, exactly like
             // the wavefront's per-wave accumulate, so both are bit-identical
-            float4 a = accum[pix];
+            // a chunked unit reads the sums its tile's previous chunk left in L2 (released
+            // before its chunk_done count; a full fence here would also drop the SM's L1)
+            float4 a = ctile >= 0 ? __ldcg(accum + pix) : accum[pix];
             const uint64_t hp = rt_stream_pixel(F.seed, (uint64_t)pix);   // per pixel, not per sample
-            for (int s = s0; s < s1; ++s) {
+            for (int s = cs0; s < cs1; ++s) {
                 PathState P;
                 start_path(F, pix, s, P, hp);
                 if constexpr (INTEG == RT_INTEG_AO) {
@@ -519,6 +549,11 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
                 a.x += P.rr; a.y += P.rg; a.z += P.rb; a.w += 1.0f;
             }
             accum[pix] = a;
+        }
+        if (ctile >= 0) {
+            __syncwarp();                           // every lane's sums, then one release by lane 0
+            if (lane == 0)
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(F.chunk_done + ctile) : "memory");
         }
     }
 #pragma unroll
@@ -738,6 +773,9 @@ FrameConst make_frame(const rt_render_params* p) {
     F.claims = nullptr;
     F.heavy_q = nullptr;
     F.probe_ctl = nullptr;
+    F.chunk = 0;
+    F.nchunks = 1;
+    F.chunk_done = nullptr;
 #if RT_TILE_PERM
     if (mine > 2) {
         // the integer nearest mine / phi that is coprime with mine (a bijection of the rows)
@@ -875,6 +913,18 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             F.claims = reinterpret_cast<unsigned*>(F.heavy_q + ctx->probe_tiles);
             F.probe_ctl = F.claims + ctx->probe_tiles;
             RT_CUDA_TRY(cudaMemsetAsync(F.probe_ctl, 0, PC_WORDS * 4, st));
+        }
+        if (F.integ != RT_INTEG_EYE && F.tiled && RT_PT_CHUNK > 0 && p->s1 - p->s0 > RT_PT_CHUNK && ntiles > 1) {
+            if (ctx->chunk_tiles < ntiles) {
+                if (ctx->d_chunk_done) RT_CUDA_TRY(cudaFree(ctx->d_chunk_done));
+                ctx->d_chunk_done = nullptr;
+                RT_CUDA_TRY(cudaMalloc(&ctx->d_chunk_done, sizeof(unsigned) * (size_t)ntiles));
+                ctx->chunk_tiles = ntiles;
+            }
+            RT_CUDA_TRY(cudaMemsetAsync(ctx->d_chunk_done, 0, sizeof(unsigned) * (size_t)ntiles, st));
+            F.chunk = RT_PT_CHUNK;
+            F.nchunks = (p->s1 - p->s0 + RT_PT_CHUNK - 1) / RT_PT_CHUNK;
+            F.chunk_done = reinterpret_cast<unsigned*>(ctx->d_chunk_done);
         }
         auto launch = [&](auto kern) -> int {
             int bps = 0;

@@ -33,6 +33,8 @@ struct rt_ctx {
     void* d_probe;                 // tile-probe heavy queue + claims of eye renders (render.cu), grown on demand
     int64_t probe_tiles;
     unsigned probe_epoch;          // claim tag of the last probed render
+    void* d_chunk_done;            // per-tile finished sample chunks of chunked PT frames (render.cu)
+    int64_t chunk_tiles;
     // host-buffer transfer pipeline (hostio.cuh): copy-in / copy-out streams + events
     cudaStream_t io_in, io_out;
     cudaEvent_t io_ev[9];

@@ -18,7 +18,8 @@ def main():
     W, H = 1920, 1080
     acc = torch.zeros((H * W, 4), dtype=torch.float32, device="cuda")
     for name, desc, integ, spp in (("eye_sphere", scenes.sphere_description(), "eye", 1),
-                                   ("pt_cornell", scenes.cornell_description(), "pt", 1),
+                                   ("pt_cornell", scenes.cornell_description(), "pt",
+                                    int(os.environ.get("RT_TIMELINE_PT_SPP", "1"))),
                                    ("eye_soup4k", scenes.soup_description(), "eye", 1)):
         sc = compile_scene(desc)
         if name == "eye_soup4k":
