@@ -49,6 +49,21 @@ __device__ __forceinline__ void pdl_wait() {
 #endif
 }
 template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl_smem(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                            Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = RT_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -498,56 +513,85 @@ if (BALLOT) {
 // status words of a predecessor tile are adjacent, and it publishes them with one 128-bit
 // store.  Per-warp digit counters are 16-bit (a warp ranks 32 x ITEMS keys).
 constexpr int R10 = 1024;
-constexpr int R10_PER = R10 / SORT_THREADS;     // bins per thread
 #ifndef SORT_LB_WIN10
 #define SORT_LB_WIN10 2   // 1 / 2 / 4 / 8 / 16: 10M sort 0.405 / 0.396 / 0.411 / 0.469 / 0.705 ms
 #endif
+// Tile geometry of the 10-bit pass (same box, sort ms at 1M / 10M): 256 threads x 12 keys
+// 0.065 / 0.369; 512 x 8 0.059 / 0.371; 512 x 12 0.066 / 0.325; 512 x 13 0.062 / 0.319;
+// 512 x 14 0.050 / 0.316; 512 x 15 0.051 / 0.320; 512 x 16 (spills) 0.060 / 0.343.  At 1M,
+// 7168-key tiles make 140 tiles: one per SM in a single wave (13 keys: 151 tiles, some SMs
+// take two).  Twice the threads per tile halve the tiles a look-back chain crosses.
 #ifndef SORT_ITEMS10
-#define SORT_ITEMS10 12   // keys per thread (10 -> 12: 10M sort 0.396 -> 0.370 ms)
+#define SORT_ITEMS10 14   // keys per thread
 #endif
-constexpr int TILE10 = SORT_THREADS * SORT_ITEMS10;
+#ifndef SORT_THREADS10
+#define SORT_THREADS10 512  // threads per tile of the 10-bit pass (256: 4 bins per thread; 512: 2)
+#endif
+constexpr int TILE10 = SORT_THREADS10 * SORT_ITEMS10;
 #ifndef SORT_LB_SLEEP
 #define SORT_LB_SLEEP 0
 #endif
-__device__ __forceinline__ uint4 ld_status4(const unsigned* p) {
-    uint4 v;
-    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p)
-                 : "memory");
-    return v;
+// a thread's PER adjacent look-back status words as one relaxed vector access
+template <int PER>
+__device__ __forceinline__ void ld_status_n(const unsigned* p, unsigned (&v)[PER]) {
+    if constexpr (PER == 4) {
+        asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "l"(p)
+                     : "memory");
+    } else {
+        static_assert(PER == 2, "2 or 4 bins per thread");
+        asm volatile("ld.relaxed.gpu.global.v2.u32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "l"(p) : "memory");
+    }
 }
-__device__ __forceinline__ void st_status4(unsigned* p, unsigned a, unsigned b, unsigned c, unsigned d) {
-    asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d)
-                 : "memory");
+template <int PER>
+__device__ __forceinline__ void st_status_n(unsigned* p, const unsigned (&v)[PER]) {
+    if constexpr (PER == 4) {
+        asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                     "r"(v[3])
+                     : "memory");
+    } else {
+        asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v[0]), "r"(v[1]) : "memory");
+    }
 }
 
+// shared-memory layout of the 10-bit pass (dynamic: 86 KB at 512 threads)
+template <int T>
+struct Sort10Smem {
+    typedef cub::BlockScan<unsigned int, T> Scan;
+    static constexpr int ITEMS = SORT_ITEMS10, TILE = T * SORT_ITEMS10;
+    typename Scan::TempStorage scan_tmp;
+    alignas(16) unsigned short warp[T / 32][R10];
+    unsigned int base[R10];
+    unsigned short texcl[R10];
+    uint32_t keys[TILE];
+    uint32_t vals[TILE];
+    unsigned int tile;
+};
+
+template <int T>
 __device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ keys_in,
                                                 const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
                                                 uint32_t* __restrict__ vals_out, int64_t n, int shift,
                                                 const unsigned int* __restrict__ hist, unsigned int* status,
                                                 unsigned int* counter) {
-    typedef cub::BlockScan<unsigned int, SORT_THREADS> Scan;
-    constexpr int ITEMS = SORT_ITEMS10, TILE = TILE10;
-    __shared__ typename Scan::TempStorage scan_tmp;
-    __shared__ __align__(16) unsigned short s_warp[SORT_THREADS / 32][R10];
-    __shared__ unsigned int s_base[R10];
-    __shared__ unsigned short s_texcl[R10];
-    __shared__ uint32_t s_keys[TILE];
-    __shared__ uint32_t s_vals[TILE];
-    __shared__ unsigned int s_tile;
+    typedef Sort10Smem<T> SM;
+    typedef typename SM::Scan Scan;
+    constexpr int ITEMS = SM::ITEMS, TILE = SM::TILE, PER = R10 / T;
+    extern __shared__ __align__(16) unsigned char sort10_smem[];
+    SM& sm = *reinterpret_cast<SM*>(sort10_smem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    if (tid == 0) s_tile = atomicAdd(counter, 1u);
+    if (tid == 0) sm.tile = atomicAdd(counter, 1u);
     {
-        uint4* z = reinterpret_cast<uint4*>(&s_warp[0][0]);
-        constexpr int NZ = (int)(sizeof(s_warp) / sizeof(uint4));
+        uint4* z = reinterpret_cast<uint4*>(&sm.warp[0][0]);
+        constexpr int NZ = (int)(sizeof(sm.warp) / sizeof(uint4));
 #pragma unroll
-        for (int k = tid; k < NZ; k += SORT_THREADS) z[k] = make_uint4(0, 0, 0, 0);
+        for (int k = tid; k < NZ; k += T) z[k] = make_uint4(0, 0, 0, 0);
     }
     pdl_wait();
     pdl_trigger();
     __syncthreads();
-    const unsigned tile = s_tile;
+    const unsigned tile = sm.tile;
     const int64_t seg = (int64_t)tile * TILE + (int64_t)warp * (32 * ITEMS);
     uint32_t key[ITEMS], val[ITEMS];
     unsigned dig[ITEMS], peers[ITEMS], rank[ITEMS];
@@ -577,54 +621,75 @@ __device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ key
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const unsigned below = __popc(peers[i] & lt_mask);
-        const unsigned base = s_warp[warp][dig[i]];
+        const unsigned base = sm.warp[warp][dig[i]];
         __syncwarp();
-        if (below == 0) s_warp[warp][dig[i]] = (unsigned short)(base + __popc(peers[i]));
+        if (below == 0) sm.warp[warp][dig[i]] = (unsigned short)(base + __popc(peers[i]));
         __syncwarp();
         rank[i] = base + below;
     }
     __syncthreads();
-    // warp prefixes of this thread's 4 bins; tc = the tile's count per bin
-    unsigned tc[R10_PER] = {0, 0, 0, 0};
+    // warp prefixes of this thread's PER bins; tc = the tile's count per bin
+    unsigned tc[PER];
 #pragma unroll
-    for (int w = 0; w < SORT_THREADS / 32; ++w) {
-        uint2* pw = reinterpret_cast<uint2*>(&s_warp[w][R10_PER * tid]);
-        const uint2 v = *pw;
-        const unsigned c[4] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16};
-        *pw = make_uint2(tc[0] | (tc[1] << 16), tc[2] | (tc[3] << 16));
+    for (int j = 0; j < PER; ++j) tc[j] = 0;
 #pragma unroll
-        for (int j = 0; j < R10_PER; ++j) tc[j] += c[j];
+    for (int w = 0; w < T / 32; ++w) {
+        if constexpr (PER == 4) {
+            uint2* pw = reinterpret_cast<uint2*>(&sm.warp[w][PER * tid]);
+            const uint2 v = *pw;
+            const unsigned c[4] = {v.x & 0xFFFFu, v.x >> 16, v.y & 0xFFFFu, v.y >> 16};
+            *pw = make_uint2(tc[0] | (tc[1] << 16), tc[2] | (tc[3] << 16));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tc[j] += c[j];
+        } else {
+            unsigned* pw = reinterpret_cast<unsigned*>(&sm.warp[w][PER * tid]);
+            const unsigned v = *pw;
+            *pw = tc[0] | (tc[1] << 16);
+            tc[0] += v & 0xFFFFu;
+            tc[1] += v >> 16;
+        }
     }
-    // publish aggregates, look back per bin (independent windows), publish inclusive prefixes
-    unsigned* st = status + (size_t)tile * R10 + R10_PER * tid;
-    unsigned excl[R10_PER] = {0, 0, 0, 0};
+    // publish aggregates, look back, publish inclusive prefixes.  A predecessor's thread
+    // publishes its PER bins in one vector store, so the status words it holds are always of
+    // one kind (all unpublished, all aggregate or all inclusive): the thread walks back over
+    // predecessors with one vector load each
+    unsigned* st = status + (size_t)tile * R10 + PER * tid;
+    unsigned excl[PER], pub[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) excl[j] = 0;
     if (tile == 0) {
-        st_status4(st, FLAG_INC | tc[0], FLAG_INC | tc[1], FLAG_INC | tc[2], FLAG_INC | tc[3]);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) pub[j] = FLAG_INC | tc[j];
+        st_status_n<PER>(st, pub);
     } else {
-        st_status4(st, FLAG_AGG | tc[0], FLAG_AGG | tc[1], FLAG_AGG | tc[2], FLAG_AGG | tc[3]);
-        // a predecessor's thread publishes its 4 bins in one 128-bit store, so the 4 status
-        // words it holds are always of one kind (all unpublished, all aggregate or all
-        // inclusive): the thread walks back over predecessors with one 128-bit load each
+#pragma unroll
+        for (int j = 0; j < PER; ++j) pub[j] = FLAG_AGG | tc[j];
+        st_status_n<PER>(st, pub);
         constexpr int LB = SORT_LB_WIN10;
         int j = (int)tile - 1;
         bool done = false;
         while (!done) {
-            uint4 w[LB];
+            unsigned w[LB][PER];
 #pragma unroll
-            for (int k = 0; k < LB; ++k)
-                w[k] = (j - k >= 0) ? ld_status4(status + (size_t)(j - k) * R10 + R10_PER * tid)
-                                    : make_uint4(0, 0, 0, 0);
+            for (int k = 0; k < LB; ++k) {
+                if (j - k >= 0) {
+                    ld_status_n<PER>(status + (size_t)(j - k) * R10 + PER * tid, w[k]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < PER; ++q) w[k][q] = 0;
+                }
+            }
             int k = 0;
 #pragma unroll
             for (int kk = 0; kk < LB; ++kk) {
                 if (done || k < kk) continue;            // stopped earlier in this window
-                const unsigned f = w[kk].x & ~VALUE_MASK;
-                // not yet published (or, defensively, a 128-bit store seen half-way): re-poll
-                if (f == 0 || ((w[kk].x ^ w[kk].y) | (w[kk].x ^ w[kk].z) | (w[kk].x ^ w[kk].w)) & ~VALUE_MASK) continue;
-                excl[0] += w[kk].x & VALUE_MASK;
-                excl[1] += w[kk].y & VALUE_MASK;
-                excl[2] += w[kk].z & VALUE_MASK;
-                excl[3] += w[kk].w & VALUE_MASK;
+                const unsigned f = w[kk][0] & ~VALUE_MASK;
+                unsigned mixed = 0;                      // (defensively: a vector store seen half-way)
+#pragma unroll
+                for (int q = 1; q < PER; ++q) mixed |= (w[kk][0] ^ w[kk][q]);
+                if (f == 0 || (mixed & ~VALUE_MASK)) continue;   // not yet published: re-poll
+#pragma unroll
+                for (int q = 0; q < PER; ++q) excl[q] += w[kk][q] & VALUE_MASK;
                 k = kk + 1;
                 if (f & FLAG_INC) done = true;
             }
@@ -633,42 +698,43 @@ __device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ key
             if (k == 0) __nanosleep(SORT_LB_SLEEP);   // no progress: back off instead of hammering L2
 #endif
         }
-        st_status4(st, FLAG_INC | (excl[0] + tc[0]), FLAG_INC | (excl[1] + tc[1]), FLAG_INC | (excl[2] + tc[2]),
-                   FLAG_INC | (excl[3] + tc[3]));
+#pragma unroll
+        for (int q = 0; q < PER; ++q) pub[q] = FLAG_INC | (excl[q] + tc[q]);
+        st_status_n<PER>(st, pub);
     }
-    unsigned hv[R10_PER], bin_excl[R10_PER], tile_excl[R10_PER];
+    unsigned hv[PER], bin_excl[PER], tile_excl[PER];
 #pragma unroll
-    for (int j = 0; j < R10_PER; ++j) hv[j] = __ldg(hist + R10_PER * tid + j);
-    Scan(scan_tmp).ExclusiveSum(hv, bin_excl);
+    for (int q = 0; q < PER; ++q) hv[q] = __ldg(hist + PER * tid + q);
+    Scan(sm.scan_tmp).ExclusiveSum(hv, bin_excl);
     __syncthreads();
-    Scan(scan_tmp).ExclusiveSum(tc, tile_excl);
+    Scan(sm.scan_tmp).ExclusiveSum(tc, tile_excl);
 #pragma unroll
-    for (int j = 0; j < R10_PER; ++j) {
-        s_base[R10_PER * tid + j] = bin_excl[j] + excl[j] - tile_excl[j];
-        s_texcl[R10_PER * tid + j] = (unsigned short)tile_excl[j];
+    for (int q = 0; q < PER; ++q) {
+        sm.base[PER * tid + q] = bin_excl[q] + excl[q] - tile_excl[q];
+        sm.texcl[PER * tid + q] = (unsigned short)tile_excl[q];
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
-        const unsigned lpos = s_texcl[dig[i]] + s_warp[warp][dig[i]] + rank[i];
-        s_keys[lpos] = key[i];
-        s_vals[lpos] = val[i];
+        const unsigned lpos = sm.texcl[dig[i]] + sm.warp[warp][dig[i]] + rank[i];
+        sm.keys[lpos] = key[i];
+        sm.vals[lpos] = val[i];
     }
     __syncthreads();
     const int64_t left = n - (int64_t)tile * TILE;
     const int cnt = left < TILE ? (int)left : TILE;
-    for (int j = tid; j < cnt; j += SORT_THREADS) {
-        const uint32_t k = s_keys[j];
-        const unsigned pos = s_base[(k >> shift) & (R10 - 1u)] + (unsigned)j;
+    for (int j = tid; j < cnt; j += T) {
+        const uint32_t k = sm.keys[j];
+        const unsigned pos = sm.base[(k >> shift) & (R10 - 1u)] + (unsigned)j;
         keys_out[pos] = k;
-        vals_out[pos] = s_vals[j];
+        vals_out[pos] = sm.vals[j];
     }
 }
-__global__ void __launch_bounds__(SORT_THREADS, 4) onesweep10_kernel(
+__global__ void __launch_bounds__(SORT_THREADS10, 1024 / SORT_THREADS10) onesweep10_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, const unsigned int* __restrict__ hist, unsigned int* status,
     unsigned int* counter) {
-    onesweep10_pass(keys_in, vals_in, keys_out, vals_out, n, shift, hist, status, counter);
+    onesweep10_pass<SORT_THREADS10>(keys_in, vals_in, keys_out, vals_out, n, shift, hist, status, counter);
 }
 
 // 30-bit keys: 64 registers -> 4 blocks per SM (10M: 4 passes 0.427 -> 0.391 ms); 63-bit
@@ -777,7 +843,16 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
                               hist + p * NB, status + (size_t)p * tiles * NB, counters + p);
         };
         if constexpr (DB == 10) {
-            RT_CUDA_TRY(launch(onesweep10_kernel));
+            constexpr size_t smem10 = sizeof(Sort10Smem<SORT_THREADS10>);
+            static bool attr_set[64] = {};     // the opt-in is per device
+            if (!attr_set[ctx->device & 63]) {
+                RT_CUDA_TRY(cudaFuncSetAttribute(onesweep10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem10));
+                attr_set[ctx->device & 63] = true;
+            }
+            RT_CUDA_TRY(launch_pdl_smem(onesweep10_kernel, (unsigned)tiles, SORT_THREADS10, smem10, st, kin, vin, kout,
+                                        vout, n, DB * p, hist + p * NB, status + (size_t)p * tiles * NB,
+                                        counters + p));
         } else if constexpr (sizeof(K) == 4) {
             RT_CUDA_TRY(ballot ? launch(onesweep32_kernel<true>) : launch(onesweep32_kernel<false>));
         } else {
