@@ -539,9 +539,11 @@ __device__ __forceinline__ void ld_status_n(const unsigned* p, unsigned (&v)[PER
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                      : "l"(p)
                      : "memory");
-    } else {
-        static_assert(PER == 2, "2 or 4 bins per thread");
+    } else if constexpr (PER == 2) {
         asm volatile("ld.relaxed.gpu.global.v2.u32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "l"(p) : "memory");
+    } else {
+        static_assert(PER == 1, "1, 2 or 4 bins per thread");
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v[0]) : "l"(p) : "memory");
     }
 }
 template <int PER>
@@ -550,8 +552,10 @@ __device__ __forceinline__ void st_status_n(unsigned* p, const unsigned (&v)[PER
         asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v[0]), "r"(v[1]), "r"(v[2]),
                      "r"(v[3])
                      : "memory");
-    } else {
+    } else if constexpr (PER == 2) {
         asm volatile("st.relaxed.gpu.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v[0]), "r"(v[1]) : "memory");
+    } else {
+        asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v[0]) : "memory");
     }
 }
 
@@ -641,12 +645,16 @@ __device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ key
             *pw = make_uint2(tc[0] | (tc[1] << 16), tc[2] | (tc[3] << 16));
 #pragma unroll
             for (int j = 0; j < 4; ++j) tc[j] += c[j];
-        } else {
+        } else if constexpr (PER == 2) {
             unsigned* pw = reinterpret_cast<unsigned*>(&sm.warp[w][PER * tid]);
             const unsigned v = *pw;
             *pw = tc[0] | (tc[1] << 16);
             tc[0] += v & 0xFFFFu;
             tc[1] += v >> 16;
+        } else {
+            const unsigned v = sm.warp[w][tid];
+            sm.warp[w][tid] = (unsigned short)tc[0];
+            tc[0] += v;
         }
     }
     // publish aggregates, look back, publish inclusive prefixes.  A predecessor's thread
