@@ -560,28 +560,29 @@ __device__ __forceinline__ void st_status_n(unsigned* p, const unsigned (&v)[PER
 }
 
 // shared-memory layout of the 10-bit pass (dynamic: 86 KB at 512 threads)
-template <int T>
-struct Sort10Smem {
+// K: key type; T threads per tile; DB digit bits (1 << DB bins); ITEMS keys per thread
+template <typename K, int T, int DB, int ITEMS_>
+struct SortWSmem {
     typedef cub::BlockScan<unsigned int, T> Scan;
-    static constexpr int ITEMS = SORT_ITEMS10, TILE = T * SORT_ITEMS10;
+    static constexpr int R = 1 << DB, ITEMS = ITEMS_, TILE = T * ITEMS_;
     typename Scan::TempStorage scan_tmp;
-    alignas(16) unsigned short warp[T / 32][R10];
-    unsigned int base[R10];
-    unsigned short texcl[R10];
-    uint32_t keys[TILE];
+    alignas(16) unsigned short warp[T / 32][R];
+    unsigned int base[R];
+    unsigned short texcl[R];
+    K keys[TILE];
     uint32_t vals[TILE];
     unsigned int tile;
 };
 
-template <int T>
-__device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ keys_in,
-                                                const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
-                                                uint32_t* __restrict__ vals_out, int64_t n, int shift,
-                                                const unsigned int* __restrict__ hist, unsigned int* status,
-                                                unsigned int* counter) {
-    typedef Sort10Smem<T> SM;
+template <typename K, int T, int DB, int ITEMS_>
+__device__ __forceinline__ void onesweep_wide_pass(const K* __restrict__ keys_in,
+                                                   const uint32_t* __restrict__ vals_in, K* __restrict__ keys_out,
+                                                   uint32_t* __restrict__ vals_out, int64_t n, int shift,
+                                                   const unsigned int* __restrict__ hist, unsigned int* status,
+                                                   unsigned int* counter) {
+    typedef SortWSmem<K, T, DB, ITEMS_> SM;
     typedef typename SM::Scan Scan;
-    constexpr int ITEMS = SM::ITEMS, TILE = SM::TILE, PER = R10 / T;
+    constexpr int ITEMS = SM::ITEMS, TILE = SM::TILE, R10 = SM::R, PER = R10 / T;
     extern __shared__ __align__(16) unsigned char sort10_smem[];
     SM& sm = *reinterpret_cast<SM*>(sort10_smem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -597,14 +598,15 @@ __device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ key
     __syncthreads();
     const unsigned tile = sm.tile;
     const int64_t seg = (int64_t)tile * TILE + (int64_t)warp * (32 * ITEMS);
-    uint32_t key[ITEMS], val[ITEMS];
+    K key[ITEMS];
+    uint32_t val[ITEMS];
     unsigned dig[ITEMS], peers[ITEMS], rank[ITEMS];
     const unsigned lt_mask = (1u << lane) - 1u;
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const int64_t idx = seg + i * 32 + lane;
         const bool ok = idx < n;
-        key[i] = ok ? keys_in[idx] : 0u;
+        key[i] = ok ? keys_in[idx] : (K)0;
         val[i] = ok ? (vals_in ? vals_in[idx] : (uint32_t)idx) : 0u;
     }
 #pragma unroll
@@ -612,10 +614,10 @@ __device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ key
         // keys past n take the last bin: they follow every real key in the stable order, so
         // they land behind the tile's real keys and are never written out
         const bool ok = seg + i * 32 + lane < n;
-        dig[i] = ok ? ((key[i] >> shift) & (R10 - 1u)) : (R10 - 1u);
+        dig[i] = ok ? ((unsigned)(key[i] >> shift) & (R10 - 1u)) : (R10 - 1u);
         unsigned pm = RT_FULL;
 #pragma unroll
-        for (int b = 0; b < 10; ++b) {
+        for (int b = 0; b < DB; ++b) {
             const bool bit = (dig[i] >> b) & 1u;
             const unsigned bb = __ballot_sync(RT_FULL, bit);
             pm &= bit ? bb : ~bb;
@@ -732,17 +734,45 @@ __device__ __forceinline__ void onesweep10_pass(const uint32_t* __restrict__ key
     const int64_t left = n - (int64_t)tile * TILE;
     const int cnt = left < TILE ? (int)left : TILE;
     for (int j = tid; j < cnt; j += T) {
-        const uint32_t k = sm.keys[j];
-        const unsigned pos = sm.base[(k >> shift) & (R10 - 1u)] + (unsigned)j;
+        const K k = sm.keys[j];
+        const unsigned pos = sm.base[(unsigned)(k >> shift) & (R10 - 1u)] + (unsigned)j;
         keys_out[pos] = k;
         vals_out[pos] = sm.vals[j];
     }
 }
+// 30-bit keys: 3 passes of 10-bit digits
+typedef SortWSmem<uint32_t, SORT_THREADS10, 10, SORT_ITEMS10> Sort10Smem;
 __global__ void __launch_bounds__(SORT_THREADS10, 1024 / SORT_THREADS10) onesweep10_kernel(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint32_t* __restrict__ keys_out,
     uint32_t* __restrict__ vals_out, int64_t n, int shift, const unsigned int* __restrict__ hist, unsigned int* status,
     unsigned int* counter) {
-    onesweep10_pass<SORT_THREADS10>(keys_in, vals_in, keys_out, vals_out, n, shift, hist, status, counter);
+    onesweep_wide_pass<uint32_t, SORT_THREADS10, 10, SORT_ITEMS10>(keys_in, vals_in, keys_out, vals_out, n, shift,
+                                                                    hist, status, counter);
+}
+// 63-bit keys: 7 passes of 9-bit digits (RT_SORT9), 512 threads per tile.  Keys per thread by
+// size (same box, sort ms at 1M / 10M): 6: 0.146 / 0.891; 8: 0.129 / 0.809; 10: 0.142 / 0.775;
+// 12: 0.155 / 0.763 (8 x 8-bit passes: 0.137 / 0.904) -- 8 below SORT9_BIG_N keys, 12 above
+#ifndef SORT_THREADS9
+#define SORT_THREADS9 512
+#endif
+#ifndef SORT_ITEMS9
+#define SORT_ITEMS9 8
+#endif
+#ifndef SORT_ITEMS9_BIG
+#define SORT_ITEMS9_BIG 12
+#endif
+#ifndef SORT9_BIG_N
+#define SORT9_BIG_N (1 << 22)
+#endif
+constexpr int TILE9 = SORT_THREADS9 * SORT_ITEMS9;
+constexpr int TILE9_BIG = SORT_THREADS9 * SORT_ITEMS9_BIG;
+template <int ITEMS>
+__global__ void __launch_bounds__(SORT_THREADS9, 1024 / SORT_THREADS9) onesweep9_kernel(
+    const uint64_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in, uint64_t* __restrict__ keys_out,
+    uint32_t* __restrict__ vals_out, int64_t n, int shift, const unsigned int* __restrict__ hist, unsigned int* status,
+    unsigned int* counter) {
+    onesweep_wide_pass<uint64_t, SORT_THREADS9, 9, ITEMS>(keys_in, vals_in, keys_out, vals_out, n, shift, hist,
+                                                           status, counter);
 }
 
 // 30-bit keys: 64 registers -> 4 blocks per SM (10M: 4 passes 0.427 -> 0.391 ms); 63-bit
@@ -811,6 +841,9 @@ __global__ void single_leaf_root(const float* tris, const uint32_t* mask, float4
 #ifndef RT_SORT10
 #define RT_SORT10 1
 #endif
+#ifndef RT_SORT9
+#define RT_SORT9 1          // 63-bit keys: 7 passes of 9-bit digits (else 8 x 8 bits)
+#endif
 template <typename K, int PASSES, int B, int DB>
 int build_typed(rt_ctx* ctx, rt_scene* s) {
     const int64_t n = s->n;
@@ -822,7 +855,8 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
     // lbvh_emit_global_kernel
     int gb = (int)((n + 255) / 256);
     if (gb > grid_stream) gb = grid_stream;
-    constexpr int64_t TILE = DB == 10 ? TILE10 : SortCfg<K>::TILE;
+    const bool big9 = DB == 9 && n >= SORT9_BIG_N;
+    const int64_t TILE = DB == 10 ? TILE10 : (DB == 9 ? (big9 ? TILE9_BIG : TILE9) : SortCfg<K>::TILE);
     const int64_t tiles = (n + TILE - 1) / TILE;
     unsigned int* hist = s->sort_scratch;                    // PASSES * NB
     unsigned int* counters = hist + PASSES * NB;             // [0, 8) tile counters, [8, 14) cb_enc, [16] emit count
@@ -850,17 +884,28 @@ int build_typed(rt_ctx* ctx, rt_scene* s) {
             return launch_pdl(kern, (unsigned)tiles, SORT_THREADS, st, kin, vin, kout, vout, n, DB * p,
                               hist + p * NB, status + (size_t)p * tiles * NB, counters + p);
         };
-        if constexpr (DB == 10) {
-            constexpr size_t smem10 = sizeof(Sort10Smem<SORT_THREADS10>);
-            static bool attr_set[64] = {};     // the opt-in is per device
-            if (!attr_set[ctx->device & 63]) {
-                RT_CUDA_TRY(cudaFuncSetAttribute(onesweep10_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem10));
-                attr_set[ctx->device & 63] = true;
+        if constexpr (DB == 10 || DB == 9) {
+            auto go = [&](auto kern, size_t smem, int threads, bool* attr_set) -> int {
+                if (!attr_set[ctx->device & 63]) {     // the opt-in is per device
+                    RT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    attr_set[ctx->device & 63] = true;
+                }
+                RT_CUDA_TRY(launch_pdl_smem(kern, (unsigned)tiles, threads, smem, st, kin, vin, kout, vout, n, DB * p,
+                                            hist + p * NB, status + (size_t)p * tiles * NB, counters + p));
+                return RT_OK;
+            };
+            static bool set10[64] = {}, set9[64] = {}, set9b[64] = {};
+            int rc;
+            if constexpr (DB == 10) {
+                rc = go(onesweep10_kernel, sizeof(Sort10Smem), SORT_THREADS10, set10);
+            } else if (big9) {
+                rc = go(onesweep9_kernel<SORT_ITEMS9_BIG>, sizeof(SortWSmem<uint64_t, SORT_THREADS9, 9, SORT_ITEMS9_BIG>),
+                        SORT_THREADS9, set9b);
+            } else {
+                rc = go(onesweep9_kernel<SORT_ITEMS9>, sizeof(SortWSmem<uint64_t, SORT_THREADS9, 9, SORT_ITEMS9>),
+                        SORT_THREADS9, set9);
             }
-            RT_CUDA_TRY(launch_pdl_smem(onesweep10_kernel, (unsigned)tiles, SORT_THREADS10, smem10, st, kin, vin, kout,
-                                        vout, n, DB * p, hist + p * NB, status + (size_t)p * tiles * NB,
-                                        counters + p));
+            if (rc) return rc;
         } else if constexpr (sizeof(K) == 4) {
             RT_CUDA_TRY(ballot ? launch(onesweep32_kernel<true>) : launch(onesweep32_kernel<false>));
         } else {
@@ -911,7 +956,11 @@ int rt_lbvh_build_impl(rt_ctx* ctx, rt_scene* s, int bits) {
 #else
     if (bits == 30) return build_typed<uint32_t, 4, 10, 8>(ctx, s);
 #endif
+#if RT_SORT9
+    return build_typed<uint64_t, 7, 21, 9>(ctx, s);
+#else
     return build_typed<uint64_t, 8, 21, 8>(ctx, s);
+#endif
 }
 
 size_t rt_sort_scratch_words(int64_t n) {
@@ -919,6 +968,9 @@ size_t rt_sort_scratch_words(int64_t n) {
     const int64_t tiles32 = (n + TILE10 - 1) / TILE10;
     const size_t w8 = (size_t)8 * RADIX + 32 + (size_t)8 * tiles * RADIX;
     const size_t w10 = (size_t)3 * R10 + 32 + (size_t)3 * tiles32 * R10;
-    const size_t w = w8 > w10 ? w8 : w10;
+    const int64_t tiles64 = (n + TILE9 - 1) / TILE9;
+    const size_t w9 = (size_t)7 * 512 + 32 + (size_t)7 * tiles64 * 512;
+    size_t w = w8 > w10 ? w8 : w10;
+    if (w9 > w) w = w9;
     return (w + 3) & ~(size_t)3;        // whole 16-B units (zeroed as uint4 by the emit hand-off)
 }
