@@ -4,8 +4,8 @@
 # and smoke().
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 2400 bash tools/r2_profile.sh > gpurun_out/r2c_profile.log 2>&1
-bash tools/job_r2_bench.sh r2c
-timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/r2c_pytest.log 2>&1
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2c_smoke.log 2>&1
+timeout 2400 bash tools/r2_profile.sh > gpurun_out/r2d_profile.log 2>&1
+bash tools/job_r2_bench.sh r2d
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/r2d_pytest.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2d_smoke.log 2>&1
 echo done
