@@ -149,6 +149,17 @@ void rt_mesh_destroy(rt_mesh* mesh);
  * rt_scene_compile and later rt_scene_refit_mesh calls. */
 int rt_mesh_upload(rt_ctx* ctx, int64_t n_vertices, const double* vertices, int64_t n_faces, const int64_t* faces,
                    double* bounds6, rt_mesh** out);
+/* rt_mesh_upload in two halves: _async enqueues the copies and the validation on the
+ * context stream and returns the mesh (argument errors and zero faces are reported here);
+ * the host arrays must stay valid until _finish, which reads the verdict back (the same
+ * RT_EBUILD errors; the caller then destroys the mesh) and fills bounds6.  rt_scene_compile
+ * (and rt_bvh_build after it) may be called between the two: their kernels run behind the
+ * validation on the stream and the compile writes nothing for a mesh that fails it; the scene is usable only after every one of its
+ * meshes finished successfully (a mesh whose _finish failed is refused, RT_ESTATE): that
+ * _finish also synchronises the stream the scene was allocated on. */
+int rt_mesh_upload_async(rt_ctx* ctx, int64_t n_vertices, const double* vertices, int64_t n_faces,
+                         const int64_t* faces, rt_mesh** out);
+int rt_mesh_upload_finish(rt_ctx* ctx, rt_mesh* mesh, double* bounds6);
 int rt_mesh_info(rt_mesh* mesh, int64_t* n_vertices, int64_t* n_faces, double* bounds6);
 /* one instance of compile_scene (Instance(blas_of_mesh[decl.mesh], decl.frame, decl.mask),
  * scene.py:91-97): matrix = frame_to_matrix(frame), inverse = invert_affine(matrix), both 3x4

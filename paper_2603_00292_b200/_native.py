@@ -130,6 +130,8 @@ def lib():
             "rt_scene_set_normals64": [vp, vp, vp],
             "rt_scene_set_local_frames": [vp, vp, i32, vp, vp],
             "rt_mesh_upload": [vp, i64, vp, i64, vp, vp, vp],
+            "rt_mesh_upload_async": [vp, i64, vp, i64, vp, vp],
+            "rt_mesh_upload_finish": [vp, vp, vp],
             "rt_mesh_info": [vp, vp, vp, vp],
             "rt_scene_compile": [vp, i32, vp, i32, vp, i32, vp, vp, vp, i32, vp],
             "rt_scene_get_ids": [vp, vp, vp, vp, vp, vp],

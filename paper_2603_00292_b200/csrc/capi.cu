@@ -157,6 +157,10 @@ void rt_ctx_destroy(rt_ctx* c) {
     cudaFree(c->d_error);
     if (c->d_probe) cudaFree(c->d_probe);
     if (c->d_chunk_done) cudaFree(c->d_chunk_done);
+    if (c->h_tab) {
+        cudaFreeHost(c->h_tab);
+        cudaEventDestroy(c->tab_ev);
+    }
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
     cudaStreamDestroy(c->own_stream);
@@ -188,7 +192,11 @@ int rt_ctx_sync(rt_ctx* c) {
 }
 
 // device allocations of a scene of n primitives and n_mat materials (contents unset)
-int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
+int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) { return rt_scene_alloc_ex(c, n, n_mat, out, 1); }
+
+// sync = 0: the caller synchronises the context stream before the scene is used from
+// another stream (rt_scene_compile behind pending mesh uploads: rt_mesh_upload_finish)
+int rt_scene_alloc_ex(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out, int sync) {
     RT_CTX_LOCK(c);
     RT_CHECK_ARG(c && out, "ctx/out is NULL");
     RT_CHECK_ARG(n >= 1, "cannot build over zero primitives");
@@ -249,7 +257,7 @@ int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out) {
         rt_scene_destroy(s);
         return RT_ECUDA;
     }
-    {
+    if (sync) {
         cudaError_t _e = cudaStreamSynchronize(c->stream);   // the blocks are usable from any stream now
         if (_e != cudaSuccess) {
             rt_set_error("allocation failed: %s", cudaGetErrorString(_e));
@@ -269,8 +277,10 @@ int rt_scene_set_materials(rt_ctx* c, rt_scene* s, const float* mat_color, const
         mc[k] = make_float4(mat_color[3 * k], mat_color[3 * k + 1], mat_color[3 * k + 2], 0.f);
         me[k] = make_float4(mat_emissive[3 * k], mat_emissive[3 * k + 1], mat_emissive[3 * k + 2], 0.f);
     }
-    RT_CUDA_TRY(cudaMemcpy(s->mat_color, mc.data(), sizeof(float4) * s->n_mat, cudaMemcpyHostToDevice));
-    RT_CUDA_TRY(cudaMemcpy(s->mat_emissive, me.data(), sizeof(float4) * s->n_mat, cudaMemcpyHostToDevice));
+    // (pageable sources are staged before an async H2D returns: the vectors may go)
+    RT_CUDA_TRY(cudaMemcpyAsync(s->mat_color, mc.data(), sizeof(float4) * s->n_mat, cudaMemcpyHostToDevice, c->stream));
+    RT_CUDA_TRY(
+        cudaMemcpyAsync(s->mat_emissive, me.data(), sizeof(float4) * s->n_mat, cudaMemcpyHostToDevice, c->stream));
     return RT_OK;
 }
 

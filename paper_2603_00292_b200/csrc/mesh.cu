@@ -30,6 +30,7 @@ struct rt_mesh {
     double bounds[6];
     unsigned long long* d_red;  // (8) device: bounds re-reduced by each refit (orderable encoding)
     int bounds_dirty;           // d_red is newer than `bounds`
+    int pending;                // rt_mesh_upload_async: validation not read back yet
 };
 
 namespace {
@@ -48,7 +49,11 @@ __global__ void refit_mesh_kernel(int64_t nf, int32_t n_inst, const int3* __rest
                                   float4* __restrict__ attr, double* __restrict__ lnormal64,
                                   double* __restrict__ lrows64, double* __restrict__ wnormal64,
                                   const int4* __restrict__ meta, int32_t* __restrict__ tri_inst,
-                                  int32_t* __restrict__ tri_prim, uint32_t* __restrict__ tri_mask) {
+                                  int32_t* __restrict__ tri_prim, uint32_t* __restrict__ tri_mask,
+                                  const unsigned long long* __restrict__ verdict) {
+    // a compile enqueued behind its mesh's validation (rt_mesh_upload_async) writes nothing
+    // for a mesh that failed it (its narrowed faces may point anywhere)
+    if (verdict && (verdict[6] != ULLONG_MAX || verdict[7] != ULLONG_MAX)) return;
     const int64_t total = nf * n_inst;
     for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
         const int32_t j = (int32_t)(q / nf);
@@ -247,15 +252,16 @@ int launch_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, bool f32, bool with_meta) {
     int64_t grid = (total + 255) / 256;
     if (grid > (int64_t)c->num_sms * 16) grid = (int64_t)c->num_sms * 16;
     const int4* meta = with_meta ? m->meta : nullptr;
+    const unsigned long long* verdict = m->pending ? m->d_red : nullptr;
     double* wn = m->local ? nullptr : s->wnormal64;
     if (f32)
         refit_mesh_kernel<float><<<(unsigned)grid, 256, 0, c->stream>>>(
             m->nf, m->n_inst, m->faces, reinterpret_cast<const float*>(m->verts), m->xform, m->offset, s->tris,
-            s->tri_attr, ln, s->lrows64, wn, meta, s->tri_inst, s->tri_prim, s->tri_mask);
+            s->tri_attr, ln, s->lrows64, wn, meta, s->tri_inst, s->tri_prim, s->tri_mask, verdict);
     else
         refit_mesh_kernel<double><<<(unsigned)grid, 256, 0, c->stream>>>(
             m->nf, m->n_inst, m->faces, m->verts, m->xform, m->offset, s->tris, s->tri_attr, ln, s->lrows64, wn,
-            meta, s->tri_inst, s->tri_prim, s->tri_mask);
+            meta, s->tri_inst, s->tri_prim, s->tri_mask, verdict);
     RT_CUDA_TRY(cudaGetLastError());
     return RT_OK;
 }
@@ -420,10 +426,60 @@ int rt_scene_refit_mesh(rt_ctx* c, rt_scene* s, rt_mesh* m, int64_t n_vertices, 
     return RT_OK;
 }
 
-int rt_mesh_upload(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_t n_faces, const int64_t* faces,
-                   double* bounds6, rt_mesh** out) {
-    RT_CTX_LOCK(c);
-    RT_CHECK_ARG(c && out && bounds6, "NULL argument");
+}  // extern "C"
+
+// rt_mesh_upload's two halves: the copies, the validation kernel and the root-box reduction
+// enqueued on the context stream; then one small read-back and the verdict.  Between them
+// the host is free (rt_mesh_upload_async / rt_mesh_upload_finish): compile_scene prepares
+// its instance tables while the mesh crosses PCIe.
+// rt_scene_compile's small host tables (materials, instance frames, offsets, ids) go up
+// from one pinned staging buffer: an async copy from pageable memory waits for the copy
+// engine to drain (here: the meshes' own uploads still in flight), a pinned one is queued
+struct TableStage {
+    struct Item { void* dst; size_t off, bytes; };
+    std::vector<char> host;
+    std::vector<Item> items;
+    void add(void* dst, const void* src, size_t bytes) {
+        const size_t off = (host.size() + 255) & ~(size_t)255;
+        host.resize(off + bytes);
+        memcpy(host.data() + off, src, bytes);
+        items.push_back({dst, off, bytes});
+    }
+    cudaError_t flush(rt_ctx* c) {
+        if (host.empty()) return cudaSuccess;
+        cudaError_t e = cudaSuccess;
+        if (c->h_tab_bytes < host.size()) {
+            if (c->h_tab) {
+                cudaEventSynchronize(c->tab_ev);
+                cudaFreeHost(c->h_tab);
+                c->h_tab = nullptr;
+                c->h_tab_bytes = 0;
+            } else {
+                e = cudaEventCreateWithFlags(&c->tab_ev, cudaEventDisableTiming);
+                if (e != cudaSuccess) return e;
+            }
+            size_t cap = 64 << 10;
+            while (cap < host.size()) cap *= 2;
+            e = cudaHostAlloc(&c->h_tab, cap, cudaHostAllocDefault);
+            if (e != cudaSuccess) return e;
+            c->h_tab_bytes = cap;
+        } else {
+            e = cudaEventSynchronize(c->tab_ev);   // the previous compile's copies are done
+            if (e != cudaSuccess) return e;
+        }
+        memcpy(c->h_tab, host.data(), host.size());
+        for (const Item& it : items) {
+            e = cudaMemcpyAsync(it.dst, static_cast<char*>(c->h_tab) + it.off, it.bytes, cudaMemcpyHostToDevice,
+                                c->stream);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaEventRecord(c->tab_ev, c->stream);
+    }
+};
+
+static int mesh_upload_enqueue(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_t n_faces,
+                               const int64_t* faces, rt_mesh** out) {
+    RT_CHECK_ARG(c && out, "NULL argument");
     RT_CHECK_ARG(n_vertices >= 0 && n_faces >= 0 && (n_vertices == 0 || vertices) && (n_faces == 0 || faces),
                  "bad mesh arrays");
     if (n_faces == 0) {
@@ -448,39 +504,86 @@ int rt_mesh_upload(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_
     if (e == cudaSuccess && n_vertices > 0 && rt_h2d(c, m->verts, vertices, sizeof(double) * 3 * n_vertices))
         e = cudaErrorUnknown;
     if (e == cudaSuccess && rt_h2d(c, f64, faces, sizeof(int64_t) * 3 * n_faces)) e = cudaErrorUnknown;
-    unsigned long long init[8] = {ULLONG_MAX, ULLONG_MAX, ULLONG_MAX, 0, 0, 0, ULLONG_MAX, ULLONG_MAX};
-    if (e == cudaSuccess) e = cudaMemcpyAsync(red, init, sizeof init, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) {
+        red_init_kernel<<<1, 32, 0, st>>>(red);
         int64_t grid = (n_faces + 255) / 256;
         if (grid > (int64_t)c->num_sms * 8) grid = (int64_t)c->num_sms * 8;
         mesh_check_kernel<<<(unsigned)grid, 256, 0, st>>>(n_faces, n_vertices, f64, m->verts, m->faces, red);
         e = cudaGetLastError();
     }
-    unsigned long long r[8];
-    if (e == cudaSuccess) e = cudaMemcpyAsync(r, red, sizeof r, cudaMemcpyDeviceToHost, st);
     if (f64) cudaFreeAsync(f64, st);
     m->d_red = red;       // kept: each refit re-reduces the bounds into it
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
+        cudaStreamSynchronize(st);
         rt_mesh_destroy(m);
         rt_set_error("rt_mesh_upload: %s", cudaGetErrorString(e));
         return RT_ECUDA;
     }
+    m->pending = 1;
+    *out = m;
+    return RT_OK;
+}
+
+static int mesh_upload_finish(rt_mesh* m, double* bounds6) {
+    RT_CHECK_ARG(m, "mesh is NULL");
+    if (!m->pending) {
+        if (bounds6) memcpy(bounds6, m->bounds, sizeof m->bounds);
+        if (m->bounds_nv == m->nv) return RT_OK;
+        rt_set_error("mesh was not uploaded by rt_mesh_upload_async");
+        return RT_ESTATE;
+    }
+    RT_CUDA_TRY(cudaSetDevice(m->device));
+    unsigned long long r[8];
+    cudaError_t e = cudaMemcpyAsync(r, m->d_red, sizeof r, cudaMemcpyDeviceToHost, m->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(m->stream);
+    if (e != cudaSuccess) {
+        rt_set_error("rt_mesh_upload: %s", cudaGetErrorString(e));
+        return RT_ECUDA;
+    }
+    m->pending = 0;
     if (r[6] != ULLONG_MAX) {
-        rt_mesh_destroy(m);
         rt_set_error("face index out of range");
         return RT_EBUILD;
     }
     if (r[7] != ULLONG_MAX) {
-        rt_mesh_destroy(m);
         rt_set_error("non-finite bounds for primitive %llu", r[7]);
         return RT_EBUILD;
     }
     for (int k = 0; k < 6; ++k) m->bounds[k] = ord2d(r[k]);
-    m->bounds_nv = n_vertices;
-    memcpy(bounds6, m->bounds, sizeof m->bounds);
+    m->bounds_nv = m->nv;
+    if (bounds6) memcpy(bounds6, m->bounds, sizeof m->bounds);
+    return RT_OK;
+}
+
+extern "C" {
+
+int rt_mesh_upload(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_t n_faces, const int64_t* faces,
+                   double* bounds6, rt_mesh** out) {
+    RT_CTX_LOCK(c);
+    RT_CHECK_ARG(c && out && bounds6, "NULL argument");
+    rt_mesh* m = nullptr;
+    int rc = mesh_upload_enqueue(c, n_vertices, vertices, n_faces, faces, &m);
+    if (rc) return rc;
+    rc = mesh_upload_finish(m, bounds6);
+    if (rc) {
+        rt_mesh_destroy(m);
+        return rc;
+    }
     *out = m;
     return RT_OK;
+}
+
+int rt_mesh_upload_async(rt_ctx* c, int64_t n_vertices, const double* vertices, int64_t n_faces,
+                         const int64_t* faces, rt_mesh** out) {
+    RT_CTX_LOCK(c);
+    return mesh_upload_enqueue(c, n_vertices, vertices, n_faces, faces, out);
+}
+
+int rt_mesh_upload_finish(rt_ctx* c, rt_mesh* m, double* bounds6) {
+    RT_CTX_LOCK(c);
+    RT_CHECK_ARG(c && m, "NULL argument");
+    RT_CHECK_ARG(m->device == c->device, "mesh and context live on different devices");
+    return mesh_upload_finish(m, bounds6);
 }
 
 int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_t n_inst,
@@ -498,6 +601,10 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
         if (d.mesh < 0 || d.mesh >= n_meshes || !meshes[d.mesh]) {
             rt_set_error("instance %d references unknown mesh %d", i, d.mesh);
             return RT_EINVAL;
+        }
+        if (!meshes[d.mesh]->pending && meshes[d.mesh]->bounds_nv != meshes[d.mesh]->nv && !meshes[d.mesh]->local) {
+            rt_set_error("instance %d: mesh %d failed its validation", i, d.mesh);
+            return RT_ESTATE;
         }
         if (meshes[d.mesh]->device != c->device || meshes[d.mesh]->local) {
             rt_set_error("instance %d: mesh lives on another device or is a BLAS mesh", i);
@@ -518,19 +625,29 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
     }
     RT_CUDA_TRY(cudaSetDevice(c->device));
     rt_scene* s = nullptr;
-    int rc = rt_scene_alloc(c, n, n_mat, &s);
+    bool pending = false;                         // validation still in flight: rt_mesh_upload_finish syncs
+    for (int32_t k = 0; k < n_meshes; ++k) pending |= meshes[k] && meshes[k]->pending;
+    int rc = rt_scene_alloc_ex(c, n, n_mat, &s, pending ? 0 : 1);
     if (rc) return rc;
     auto fail = [&](int code) {
         rt_scene_destroy(s);
         return code;
     };
-    rc = rt_scene_set_materials(c, s, mat_color, mat_emissive);
-    if (rc) return fail(rc);
+    TableStage tab;
+    {
+        std::vector<float4> mc(n_mat), me(n_mat);
+        for (int k = 0; k < n_mat; ++k) {
+            mc[k] = make_float4(mat_color[3 * k], mat_color[3 * k + 1], mat_color[3 * k + 2], 0.f);
+            me[k] = make_float4(mat_emissive[3 * k], mat_emissive[3 * k + 1], mat_emissive[3 * k + 2], 0.f);
+        }
+        tab.add(s->mat_color, mc.data(), sizeof(float4) * n_mat);
+        tab.add(s->mat_emissive, me.data(), sizeof(float4) * n_mat);
+    }
     cudaStream_t st = c->stream;
     cudaError_t e = rt_alloc((void**)&s->wnormal64, sizeof(double) * 3 * (size_t)n, st, false);
     if (e == cudaSuccess) e = rt_alloc((void**)&s->lrows64, sizeof(double) * 9 * (size_t)n, st, false);
     const int32_t ni = n_inst + n_custom;
-    if (e == cudaSuccess) e = rt_alloc((void**)&s->inst_inv64, sizeof(double) * 12 * (size_t)ni, st);
+    if (e == cudaSuccess) e = rt_alloc((void**)&s->inst_inv64, sizeof(double) * 12 * (size_t)ni, st, false);
     if (e != cudaSuccess) {
         rt_set_error("cudaMalloc failed: %s", cudaGetErrorString(e));
         return fail(RT_ENOMEM);
@@ -554,7 +671,7 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
         meta[d.mesh].push_back(make_int4(i, d.material, (int)d.mask, 0));
         off += meshes[d.mesh]->nf;
     }
-    e = cudaMemcpyAsync(s->inst_inv64, inv.data(), sizeof(double) * inv.size(), cudaMemcpyHostToDevice, st);
+    tab.add(s->inst_inv64, inv.data(), sizeof(double) * inv.size());
     for (int32_t k = 0; k < n_meshes && e == cudaSuccess; ++k) {
         rt_mesh* m = meshes[k];
         if (!m || ofs[k].empty()) continue;
@@ -567,15 +684,18 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
             m->n_inst = 0;
             e = rt_alloc((void**)&m->xform, sizeof(double) * 21 * cnt, m->stream, false);
             if (e == cudaSuccess) e = rt_alloc((void**)&m->offset, sizeof(int64_t) * cnt, m->stream, false);
-            if (e == cudaSuccess) e = rt_alloc((void**)&m->meta, sizeof(int4) * cnt, m->stream);
+            if (e == cudaSuccess) e = rt_alloc((void**)&m->meta, sizeof(int4) * cnt, m->stream, false);
             if (e != cudaSuccess) break;
             m->n_inst = cnt;
         }
-        // pageable sources: these copies complete before returning, so the vectors may go
-        e = cudaMemcpy(m->xform, xf[k].data(), sizeof(double) * 21 * cnt, cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemcpy(m->offset, ofs[k].data(), sizeof(int64_t) * cnt, cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemcpy(m->meta, meta[k].data(), sizeof(int4) * cnt, cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) break;
+        tab.add(m->xform, xf[k].data(), sizeof(double) * 21 * cnt);
+        tab.add(m->offset, ofs[k].data(), sizeof(int64_t) * cnt);
+        tab.add(m->meta, meta[k].data(), sizeof(int4) * cnt);
+    }
+    if (e == cudaSuccess) e = tab.flush(c);       // every table, then the kernels that read them
+    for (int32_t k = 0; k < n_meshes && e == cudaSuccess; ++k) {
+        rt_mesh* m = meshes[k];
+        if (!m || ofs[k].empty()) continue;
         rc = launch_mesh(c, s, m, false, true);
         if (rc) return fail(rc);
     }
@@ -608,8 +728,12 @@ int rt_scene_compile(rt_ctx* c, int32_t n_meshes, rt_mesh* const* meshes, int32_
             if (rc) return fail(rc);
         }
     }
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();   // (kernel faults surface at the next sync)
+    // every block usable from any stream before the scene is returned -- or, with uploads
+    // pending, after their rt_mesh_upload_finish (a stream sync)
+    if (e == cudaSuccess && !pending) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
+        cudaStreamSynchronize(st);
         rt_set_error("rt_scene_compile: %s", cudaGetErrorString(e));
         return fail(RT_ECUDA);
     }
@@ -661,6 +785,7 @@ int rt_scene_get_ids(rt_ctx* c, rt_scene* s, int32_t* tri_inst, int32_t* tri_pri
 void rt_mesh_destroy(rt_mesh* m) {
     if (!m) return;
     cudaSetDevice(m->device);
+    if (m->pending) cudaStreamSynchronize(m->stream);   // its copies may still read the host arrays
     void* ptrs[] = {m->faces, m->xform, m->offset, m->verts, m->meta, m->d_red};
     for (void* p : ptrs) rt_free(p, m->stream);
     delete m;

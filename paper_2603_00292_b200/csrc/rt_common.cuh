@@ -35,6 +35,9 @@ struct rt_ctx {
     unsigned probe_epoch;          // claim tag of the last probed render
     void* d_chunk_done;            // per-tile finished sample chunks of chunked PT frames (render.cu)
     int64_t chunk_tiles;
+    void* h_tab;                   // pinned staging of rt_scene_compile's small tables (mesh.cu)
+    size_t h_tab_bytes;
+    cudaEvent_t tab_ev;            // its last copies (the buffer is rewritten only after them)
     // host-buffer transfer pipeline (hostio.cuh): copy-in / copy-out streams + events
     cudaStream_t io_in, io_out;
     cudaEvent_t io_ev[9];
@@ -144,6 +147,7 @@ int rt_h2d(rt_ctx* c, void* dst, const void* src, size_t bytes);
 int rt_check_device_error(rt_ctx* ctx);
 // scene storage for n primitives (contents unset) / material table upload
 extern "C" int rt_scene_alloc(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out);
+extern "C" int rt_scene_alloc_ex(rt_ctx* c, int64_t n, int32_t n_mat, rt_scene** out, int sync);
 extern "C" int rt_scene_set_materials(rt_ctx* c, rt_scene* s, const float* mat_color, const float* mat_emissive);
 
 // --------------------------------------------------------------------------

@@ -307,14 +307,27 @@ class _DeviceMesh:
     float64 vertices and int64 faces went up once and were validated there (Blas.from_mesh's
     BuildError checks, accel.py:223-236); ``bounds`` is the float64 root box."""
 
-    def __init__(self, ctx, V, F):
+    def __init__(self, ctx, V, F, wait=True):
         self.nv = int(V.shape[0])
         self.nf = int(F.shape[0])
         self.bounds = np.empty(6, np.float64)
         self._lib = lib()
+        self._ctx = ctx
         h = ctypes.c_void_p()
-        check(lib().rt_mesh_upload(ctx.handle, self.nv, ptr(V), self.nf, ptr(F), ptr(self.bounds), ctypes.byref(h)))
+        check(lib().rt_mesh_upload_async(ctx.handle, self.nv, ptr(V), self.nf, ptr(F), ctypes.byref(h)))
         self.handle = h
+        self._src = (V, F)           # the copies read them until finish()
+        if wait:
+            self.finish()
+
+    def finish(self):
+        """Read the device validation back (BuildError as Blas.from_mesh) and the root box."""
+        if self._src is not None:
+            try:
+                check(lib().rt_mesh_upload_finish(self._ctx.handle, self.handle, ptr(self.bounds)))
+            finally:
+                self._src = None
+        return self
 
     def device_bounds(self):
         """float64 root box of the mesh's current vertices (re-reduced on the device by each
@@ -409,63 +422,99 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
         mesh = desc.meshes[name]
         V = np.ascontiguousarray(mesh.vertices, np.float64).reshape(-1, 3)
         F = np.ascontiguousarray(mesh.faces, np.int64).reshape(-1, 3)
-        dmeshes[name] = _DeviceMesh(ctx, V, F)
+        try:
+            dmeshes[name] = _DeviceMesh(ctx, V, F, wait=False)   # validated below, after the host-side tables
+        except Exception:
+            for dm in dmeshes.values():                          # earlier meshes' verdicts come first
+                dm.finish()
+            raise
 
-    # sphere instances after the mesh instances (scene.py:101-112): one custom primitive
-    # each, flat ids after every triangle; its leaf box is the world AABB of the
-    # transformed local box (accel.py:459-469), rounded outward to fp32
-    n_sph = len(desc.spheres) if desc.spheres else 0
-    customs = (_native.CustomSrc * max(n_sph, 1))()
-    sph_rows, sph_boxes = [], []
-    if n_sph:
-        rows = np.array([[*sph.center, sph.radius] for sph in desc.spheres], dtype=np.float64)
-        sphere_data(rows)                               # radius > 0 (accel.py:403-408)
-        for k, sph in enumerate(desc.spheres):
-            m = frame_to_matrix(sph.frame)
+    # host-side tables while the meshes cross PCIe; any error here is raised after the
+    # meshes' own verdicts, as the reference builds every Blas before the instances
+    try:
+        # sphere instances after the mesh instances (scene.py:101-112): one custom primitive
+        # each, flat ids after every triangle; its leaf box is the world AABB of the
+        # transformed local box (accel.py:459-469), rounded outward to fp32
+        n_sph = len(desc.spheres) if desc.spheres else 0
+        customs = (_native.CustomSrc * max(n_sph, 1))()
+        sph_rows, sph_boxes = [], []
+        if n_sph:
+            rows = np.array([[*sph.center, sph.radius] for sph in desc.spheres], dtype=np.float64)
+            sphere_data(rows)                               # radius > 0 (accel.py:403-408)
+            for k, sph in enumerate(desc.spheres):
+                m = frame_to_matrix(sph.frame)
+                try:
+                    inv = invert_affine(m)
+                except ValueError as exc:
+                    raise BuildError(f"sphere {k} frame is not invertible") from exc
+                c, r = rows[k, :3], rows[k, 3]
+                lo, hi = _corner_box(c - r, c + r, m)
+                lo32, hi32 = lo.astype(np.float32), hi.astype(np.float32)
+                lo32 = np.where(lo32.astype(np.float64) > lo, np.nextafter(lo32, np.float32(-np.inf)), lo32)
+                hi32 = np.where(hi32.astype(np.float64) < hi, np.nextafter(hi32, np.float32(np.inf)), hi32)
+                row = np.concatenate([inv.reshape(12), c, [r]])
+                cs = customs[k]
+                cs.box[:] = [float(x) for x in np.concatenate([lo32, hi32, lo32])]
+                cs.material = mat_index[sph.material]
+                cs.mask = int(sph.mask)
+                cs.row[:] = [float(x) for x in row]
+                sph_rows.append(row)
+                sph_boxes.append((lo, hi, inv, c - r, c + r, m))
+
+        # instances (Instance + Tlas frames, accel.py:339-346, 451-472)
+        n_inst = len(desc.instances)
+        srcs = (_native.InstanceSrc * max(n_inst, 1))()
+        inst_material, inst_list, inverses, placements = [], [], [], []
+        wlo, whi = [], []
+        for i, decl in enumerate(desc.instances):
+            m = frame_to_matrix(decl.frame)
             try:
                 inv = invert_affine(m)
             except ValueError as exc:
-                raise BuildError(f"sphere {k} frame is not invertible") from exc
-            c, r = rows[k, :3], rows[k, 3]
-            lo, hi = _corner_box(c - r, c + r, m)
-            lo32, hi32 = lo.astype(np.float32), hi.astype(np.float32)
-            lo32 = np.where(lo32.astype(np.float64) > lo, np.nextafter(lo32, np.float32(-np.inf)), lo32)
-            hi32 = np.where(hi32.astype(np.float64) < hi, np.nextafter(hi32, np.float32(np.inf)), hi32)
-            row = np.concatenate([inv.reshape(12), c, [r]])
-            cs = customs[k]
-            cs.box[:] = [float(x) for x in np.concatenate([lo32, hi32, lo32])]
-            cs.material = mat_index[sph.material]
-            cs.mask = int(sph.mask)
-            cs.row[:] = [float(x) for x in row]
-            sph_rows.append(row)
-            sph_boxes.append((lo, hi, inv, c - r, c + r, m))
+                raise BuildError(f"instance {i} frame is not invertible") from exc
+            inverses.append(inv)
+            inst_list.append((decl, m))
+            placements.append((decl.mesh, m, None, None))
+            mi = mat_index[decl.material]
+            inst_material.append(mi)
+            src = srcs[i]
+            src.mesh = mesh_names.index(decl.mesh)
+            src.material = mi
+            src.mask = int(decl.mask)
+            src.matrix[:] = [float(x) for x in m.reshape(12)]
+            src.inverse[:] = [float(x) for x in inv.reshape(12)]
+    except Exception:
+        for name in mesh_names:
+            dmeshes[name].finish()
+        raise
 
-    # instances (Instance + Tlas frames, accel.py:339-346, 451-472)
-    n_inst = len(desc.instances)
-    srcs = (_native.InstanceSrc * max(n_inst, 1))()
-    inst_material, inst_list, inverses, placements = [], [], [], []
-    wlo, whi = [], []
-    for i, decl in enumerate(desc.instances):
+    # the flat scene written on the device behind the meshes' validation (nothing is written
+    # for a mesh that fails it), then the verdicts and root boxes
+    handles = (ctypes.c_void_p * max(len(mesh_names), 1))(*[dmeshes[nm].handle.value for nm in mesh_names])
+    mc = np.ascontiguousarray(mat_color, np.float32).reshape(-1, 3)
+    me = np.ascontiguousarray(mat_emissive, np.float32).reshape(-1, 3)
+    h = ctypes.c_void_p()
+    try:
+        check(lib().rt_scene_compile(ctx.handle, len(mesh_names), handles, n_inst, srcs, n_sph, customs, ptr(mc),
+                                     ptr(me), mc.shape[0], ctypes.byref(h)))
+    except Exception:
+        for name in mesh_names:
+            dmeshes[name].finish()
+        raise
+    try:
+        # the LBVH build is queued behind the flat-scene kernels before the verdicts are read
+        # (a scene whose mesh fails is destroyed unbuilt-in-effect: nothing reads it)
+        check(lib().rt_bvh_build(ctx.handle, h, QUALITIES[quality], None))
+        for name in mesh_names:
+            dmeshes[name].finish()
+    except Exception:
+        lib().rt_scene_destroy(h)
+        raise
+    for decl, m in inst_list:
         dm = dmeshes[decl.mesh]
-        m = frame_to_matrix(decl.frame)
-        try:
-            inv = invert_affine(m)
-        except ValueError as exc:
-            raise BuildError(f"instance {i} frame is not invertible") from exc
-        inverses.append(inv)
-        inst_list.append((decl, m))
-        placements.append((decl.mesh, m, None, None))
         lo, hi = _corner_box(dm.bounds[:3], dm.bounds[3:], m)
         wlo.append(lo)
         whi.append(hi)
-        mi = mat_index[decl.material]
-        inst_material.append(mi)
-        src = srcs[i]
-        src.mesh = mesh_names.index(decl.mesh)
-        src.material = mi
-        src.mask = int(decl.mask)
-        src.matrix[:] = [float(x) for x in m.reshape(12)]
-        src.inverse[:] = [float(x) for x in inv.reshape(12)]
     for k, sph in enumerate(desc.spheres or ()):
         lo, hi, inv, llo, lhi, m = sph_boxes[k]
         placements.append((None, m, llo, lhi))
@@ -475,16 +524,10 @@ def compile_scene(desc, quality: str = "lbvh30", device: int = 0, two_level: boo
         inst_material.append(mat_index[sph.material])
     root_lo = np.min(np.array(wlo), axis=0)
     root_hi = np.max(np.array(whi), axis=0)
-
-    handles = (ctypes.c_void_p * max(len(mesh_names), 1))(*[dmeshes[nm].handle.value for nm in mesh_names])
-    mc = np.ascontiguousarray(mat_color, np.float32).reshape(-1, 3)
-    me = np.ascontiguousarray(mat_emissive, np.float32).reshape(-1, 3)
-    h = ctypes.c_void_p()
-    check(lib().rt_scene_compile(ctx.handle, len(mesh_names), handles, n_inst, srcs, n_sph, customs, ptr(mc), ptr(me),
-                                 mc.shape[0], ctypes.byref(h)))
     n = sum(dmeshes[d.mesh].nf for d in desc.instances) + n_sph
     tlas = GpuTlas(ctx, h, n, QUALITIES[quality], np.array(sph_rows) if sph_rows else None,
-                   n_instances=n_inst + n_sph, inverses=np.array(inverses))
+                   n_instances=n_inst + n_sph, inverses=np.array(inverses), build=False)
+    tlas.version = 1                                   # built above
     registry = IntersectorRegistry()
     if desc.spheres:
         registry.register(SPHERE_GEOM_TYPE, 0, sphere_intersector,

@@ -99,6 +99,33 @@ def test_build_errors_match_reference_messages(native):
         compile_scene(_one_mesh(V2, F3))
 
 
+def test_build_error_order_and_recovery(native):
+    """The meshes are validated behind the instance tables and the flat-scene kernels
+    (rt_mesh_upload_async): a bad mesh still wins over a bad instance (the reference builds
+    every Blas first), a failed mesh writes nothing, and the next compile is exact."""
+    import dataclasses
+    V = np.random.default_rng(1).normal(size=(30, 3))
+    F = np.arange(30).reshape(-1, 3)
+    F2 = F.copy()
+    F2[6, 2] = 10 ** 9
+    bad = _one_mesh(V, F2)
+    bad_inst = dataclasses.replace(bad, instances=[dataclasses.replace(bad.instances[0], material="no-such")])
+    with pytest.raises(BuildError, match="^face index out of range$"):
+        compile_scene(bad_inst)
+    with pytest.raises(KeyError):                 # a good mesh: the instance's own error
+        compile_scene(dataclasses.replace(_one_mesh(V, F), instances=bad_inst.instances))
+    two = dataclasses.replace(bad, meshes={"a": TriangleMesh(V, F), "mesh": bad.meshes["mesh"]})
+    with pytest.raises(BuildError, match="^face index out of range$"):
+        compile_scene(two)
+    good = _one_mesh(V, F)
+    a = compile_scene(good).tlas.geometry()
+    with pytest.raises(BuildError):
+        compile_scene(bad)
+    b = compile_scene(good).tlas.geometry()
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
 def test_compile_time_config_sizes(native):
     """compile_scene from the reference's float64 / int64 host arrays:
     printed for the record (1M sphere, 10M soup)."""

@@ -27,13 +27,19 @@ def main():
     for _ in range(5):
         render_frame(compile_scene(pdesc, "lbvh30"), W, H, 1, "eye")
     torch.cuda.synchronize()
+    def step(i):                                # the scene dies with the step (as in bench.py)
+        with record_function(f"step{i}"):
+            with record_function("compile_scene"):
+                s2 = compile_scene(pdesc, "lbvh30")
+            with record_function("render_frame"):
+                render_frame(s2, W, H, 1, "eye")
+
+    for i in range(3):
+        step(i)
+    torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         for i in range(3):
-            with record_function(f"step{i}"):
-                with record_function("compile_scene"):
-                    s2 = compile_scene(pdesc, "lbvh30")
-                with record_function("render_frame"):
-                    render_frame(s2, W, H, 1, "eye")
+            step(i)
     ev = [e for e in prof.events()]
     steps = sorted([e for e in ev if e.name.startswith("step")], key=lambda e: e.time_range.start)
     last = steps[-1]
@@ -57,6 +63,10 @@ def main():
         agg[e.name][1] += (e.time_range.end - e.time_range.start) / 1e3
     for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
         print(f"  api {k}: {n} calls, {t:.3f} ms")
+    for e in sorted(api, key=lambda e: e.time_range.start):   # the host calls that block
+        d = (e.time_range.end - e.time_range.start) / 1e3
+        if d > 0.02:
+            print(f"  slow api {(e.time_range.start - t0) / 1e3:8.3f} .. {(e.time_range.end - t0) / 1e3:8.3f} ms  {e.name}")
 
 
 if __name__ == "__main__":
