@@ -73,4 +73,20 @@ for b in (24, 2, 0):
     render_into(sph, acc, 128, 96, 2, "eye", count_rays=False, bands=(2, 1))
 _native.check(_native.lib().rt_set_probe_budget(24, None))
 torch.cuda.synchronize()
+# meshes failing their (asynchronous) validation: the compile and the build are queued behind
+# it, and the compile kernel must write nothing for them (out-of-range faces, non-finite rows)
+import dataclasses  # noqa: E402
+from paper_2603_00292_b200 import BuildError  # noqa: E402
+from paper_2603_00292_b200.scene_io import TriangleMesh  # noqa: E402
+Vb = rng.normal(size=(300, 3))
+for bad_F, bad_V in ((np.arange(300).reshape(-1, 3) * 1000, Vb), (np.arange(300).reshape(-1, 3), np.where(Vb > 2, np.nan, Vb))):
+    d0 = scenes.single_mesh_description(TriangleMesh(bad_V, bad_F), (0, 0, 3), (1, 0, 0), (0, 1, 0))
+    try:
+        compile_scene(d0)
+        raise SystemExit("expected a BuildError")
+    except BuildError:
+        pass
+good = compile_scene(scenes.single_mesh_description(TriangleMesh(Vb, np.arange(300).reshape(-1, 3)), (0, 0, 3),
+                                                    (1, 0, 0), (0, 1, 0)))
+render_frame(good, 24, 16, 1, "eye")
 print("sanitize driver ok")
