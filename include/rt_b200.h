@@ -266,6 +266,15 @@ int rt_scene_set_lights(rt_ctx* ctx, rt_scene* scene, int32_t n_lights, const fl
  * place (sample order per pixel).  rays_out (nullable): closest-hit queries issued. */
 int rt_render(rt_ctx* ctx, rt_scene* scene, const rt_render_params* p, float* accum,
               uint64_t* rays_out);
+/* render_frame in one call (integrators.py:426-473): the frame rendered from zero sums and
+ * delivered, synchronously, into host_out = a HOST (H*W, 4) float64 AccumBuffer array
+ * (pinned memory for an overlapped copy); pixels outside p's pixel range / band set are 0.
+ * The values are the exact float64 widening of the fp32 sums rt_render accumulates.  Eye
+ * frames in the megakernel write their float64 rows directly; a whole eye frame with
+ * n_chunks > 1 (<= 8, and rays_out NULL) renders in n_chunks row chunks, each copied out
+ * while the next renders.  rays_out (nullable): closest-hit queries of the frame. */
+int rt_render_host(rt_ctx* ctx, rt_scene* scene, const rt_render_params* p, double* host_out,
+                   int32_t n_chunks, uint64_t* rays_out);
 /* device resolve (scene_io.py:349-355): accum (npix, 4) f32 running sums -> rgb (npix, 3)
  * uint8, mean clamped to [0, 1], ^(1/2.2) when gamma != 0, round-half-even of 255 v;
  * both device buffers.  RT_EINVAL if a pixel has zero samples (AccumBuffer.mean). */

@@ -106,6 +106,7 @@ def lib():
             "rt_trace_closest": [vp, vp, i64, vp, vp, u32, vp, i32],
             "rt_closest_hit_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp, vp, vp, vp, vp, vp, vp, i32],
             "rt_render": [vp, vp, ctypes.POINTER(RenderParams), vp, vp],
+            "rt_render_host": [vp, vp, ctypes.POINTER(RenderParams), vp, i32, vp],
             "rt_trace_any": [vp, vp, i64, vp, vp, u32, i32],
             "rt_any_hit_host": [vp, vp, i64, vp, vp, vp, vp, f64, f64, u32, vp, i32],
             "rt_scene_set_lights": [vp, vp, i32, vp],

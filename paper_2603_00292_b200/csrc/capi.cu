@@ -157,6 +157,7 @@ void rt_ctx_destroy(rt_ctx* c) {
     cudaFree(c->d_error);
     if (c->d_probe) cudaFree(c->d_probe);
     if (c->d_chunk_done) cudaFree(c->d_chunk_done);
+    if (c->d_rb) cudaFree(c->d_rb);
     if (c->h_tab) {
         cudaFreeHost(c->h_tab);
         cudaEventDestroy(c->tab_ev);
@@ -732,9 +733,7 @@ int rt_scene_set_spheres(rt_ctx* c, rt_scene* s, int32_t n_spheres, const double
     return RT_OK;
 }
 
-int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out) {
-    RT_CTX_LOCK(c);
-    RT_CHECK_ARG(c && s && p && accum, "NULL argument");
+static int render_args(rt_ctx* c, rt_scene* s, const rt_render_params* p) {
     RT_CHECK_ARG(p->width >= 1 && p->height >= 1 && p->s1 > p->s0 && p->s0 >= 0,
                  "width, height, and spp must all be >= 1");
     RT_CHECK_ARG(p->integrator == RT_INTEG_EYE || p->integrator == RT_INTEG_AO || p->integrator == RT_INTEG_PT ||
@@ -747,11 +746,30 @@ int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, u
     RT_CHECK_ARG(p->max_depth >= 1, "max_depth must be >= 1");
     RT_CHECK_ARG(p->kernel == RT_KERNEL_MEGA || p->kernel == RT_KERNEL_WAVEFRONT, "unknown kernel");
     if (!s->built) { rt_set_error("BVH not built"); return RT_ESTATE; }
+    return RT_OK;
+}
+
+int rt_render(rt_ctx* c, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out) {
+    RT_CTX_LOCK(c);
+    RT_CHECK_ARG(c && s && p && accum, "NULL argument");
+    int rc = render_args(c, s, p);
+    if (rc) return rc;
     RT_CUDA_TRY(cudaSetDevice(c->device));
-    int rc = rt_render_impl(c, s, p, accum, rays_out);
+    rc = rt_render_impl(c, s, p, accum, rays_out);
     if (rc) return rc;
     if (rays_out) return rt_check_device_error(c);
     return RT_OK;
+}
+
+int rt_render_host(rt_ctx* c, rt_scene* s, const rt_render_params* p, double* host_out, int32_t n_chunks,
+                   uint64_t* rays_out) {
+    RT_CTX_LOCK(c);
+    RT_CHECK_ARG(c && s && p && host_out, "NULL argument");
+    RT_CHECK_ARG(n_chunks >= 1, "n_chunks must be >= 1");
+    int rc = render_args(c, s, p);
+    if (rc) return rc;
+    RT_CUDA_TRY(cudaSetDevice(c->device));
+    return rt_render_host_impl(c, s, p, host_out, n_chunks, rays_out);
 }
 
 int rt_resolve(rt_ctx* c, const float* accum, int64_t npix, int32_t gamma, uint8_t* rgb) {

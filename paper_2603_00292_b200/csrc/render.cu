@@ -55,6 +55,9 @@ struct FrameConst {
     int chunk;                     // samples per unit
     int nchunks;
     unsigned* chunk_done;          // (tiles) units of the tile finished, in sample order (zeroed per render)
+    // eye frames of render_frame (rt_render_host): each pixel's sums from zero, written once
+    // as float64 rows here (the fp32 accum is neither read nor written)
+    double4* out64;
 };
 
 // unit k -> pixel; false for the padding lanes of partial edge tiles
@@ -398,9 +401,18 @@ __device__ __forceinline__ long long probed_next_tile(const FrameConst& F, unsig
 }
 
 // ---- K7: megakernel --------------------------------------------------------
+// float64 copy of fp32 sums (render_frame's readback of every frame but the eye frames)
+__global__ void widen_kernel(const float4* __restrict__ acc, double4* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const float4 a = __ldcs(acc + i);
+        out[i] = make_double4(a.x, a.y, a.z, a.w);
+    }
+}
+
 // Persistent warps fetch 32 pixels at a time; each lane renders samples
 // [s0, s1) of its pixel in order and adds the sums to accum once.
-template <int INTEG, bool SPH>
+// OUT64: sums from zero written as float64 rows to F.out64 (rt_render_host, eye frames)
+template <int INTEG, bool SPH, bool OUT64 = false>
 __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     const FrameConst F, int s0, int s1, const float4* __restrict__ nodes, const float4* __restrict__ bvh4,
     const float4* __restrict__ tris, const float4* __restrict__ attr, const float4* __restrict__ mat_color,
@@ -526,7 +538,7 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
             // the wavefront's per-wave accumulate, so both are bit-identical
             // a chunked unit reads the sums its tile's previous chunk left in L2 (released
             // before its chunk_done count; a full fence here would also drop the SM's L1)
-            float4 a = ctile >= 0 ? __ldcg(accum + pix) : accum[pix];
+            float4 a = OUT64 ? make_float4(0.f, 0.f, 0.f, 0.f) : ctile >= 0 ? __ldcg(accum + pix) : accum[pix];
             const uint64_t hp = rt_stream_pixel(F.seed, (uint64_t)pix);   // per pixel, not per sample
             for (int s = cs0; s < cs1; ++s) {
                 PathState P;
@@ -548,7 +560,10 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
                 }
                 a.x += P.rr; a.y += P.rg; a.z += P.rb; a.w += 1.0f;
             }
-            accum[pix] = a;
+            if constexpr (OUT64)
+                F.out64[pix] = make_double4(a.x, a.y, a.z, a.w);
+            else
+                accum[pix] = a;
         }
         if (ctile >= 0) {
             __syncwarp();                           // every lane's sums, then one release by lane 0
@@ -776,6 +791,7 @@ FrameConst make_frame(const rt_render_params* p) {
     F.chunk = 0;
     F.nchunks = 1;
     F.chunk_done = nullptr;
+    F.out64 = nullptr;
 #if RT_TILE_PERM
     if (mine > 2) {
         // the integer nearest mine / phi that is coprime with mine (a bijection of the rows)
@@ -867,7 +883,8 @@ static int ensure_wave(rt_scene* s, int64_t npix, WaveBuffers*& out) {
     return RT_OK;
 }
 
-int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out) {
+int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out,
+                   double* out64) {
     FrameConst F = make_frame(p);
     const int64_t hi = (p->pix_hi > 0) ? p->pix_hi : (int64_t)p->width * p->height;
     if (F.pix_lo < 0 || hi <= F.pix_lo || hi > (int64_t)p->width * p->height) {
@@ -926,6 +943,13 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             F.nchunks = (p->s1 - p->s0 + RT_PT_CHUNK - 1) / RT_PT_CHUNK;
             F.chunk_done = reinterpret_cast<unsigned*>(ctx->d_chunk_done);
         }
+        if (out64) {
+            if (F.integ != RT_INTEG_EYE || F.nchunks > 1) {
+                rt_set_error("float64 output is for eye frames");
+                return RT_EINVAL;
+            }
+            F.out64 = reinterpret_cast<double4*>(out64);
+        }
         auto launch = [&](auto kern) -> int {
             int bps = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, MEGA_THREADS, 0);
@@ -944,7 +968,11 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         const bool sph = s->n_spheres > 0;   // triangle-only scenes run the walk without the sphere branch
         switch (F.integ) {
             case RT_INTEG_EYE:
-                rc = sph ? launch(pt_megakernel<RT_INTEG_EYE, true>) : launch(pt_megakernel<RT_INTEG_EYE, false>);
+                if (out64)
+                    rc = sph ? launch(pt_megakernel<RT_INTEG_EYE, true, true>)
+                             : launch(pt_megakernel<RT_INTEG_EYE, false, true>);
+                else
+                    rc = sph ? launch(pt_megakernel<RT_INTEG_EYE, true>) : launch(pt_megakernel<RT_INTEG_EYE, false>);
                 break;
             case RT_INTEG_AO:
                 rc = sph ? launch(pt_megakernel<RT_INTEG_AO, true>) : launch(pt_megakernel<RT_INTEG_AO, false>);
@@ -958,6 +986,10 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         }
         if (rc) return rc;
     } else {
+        if (out64) {
+            rt_set_error("float64 output runs in the megakernel");
+            return RT_EINVAL;
+        }
         if (F.max_depth > 30) {
             rt_set_error("the wavefront kernel supports max_depth <= 30 (got %d); use kernel='mega'", F.max_depth);
             return RT_EINVAL;
@@ -1016,6 +1048,77 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
         RT_CUDA_TRY(cudaStreamSynchronize(st));
     }
     return RT_OK;
+}
+
+// render_frame in one call: the frame rendered from zero sums and delivered to the host as
+// (npix, 4) float64 rows.  Eye frames in the megakernel write the float64 rows themselves;
+// with n_chunks > 1 a whole eye frame renders in row chunks and each chunk's rows are copied
+// out on the copy stream while the next chunk renders (the 32 B/pixel readback outlasts the
+// render).  Every other frame renders into fp32 sums that are widened on the device and
+// copied once.
+int rt_render_host_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, double* host_out, int n_chunks,
+                        uint64_t* rays_out) {
+    const int64_t npix = (int64_t)p->width * p->height;
+    const int stride = p->band_stride > 1 ? p->band_stride : 1;
+    const bool whole = p->pix_lo == 0 && (p->pix_hi == 0 || p->pix_hi == npix);
+    const bool direct = p->integrator == RT_INTEG_EYE && p->kernel == RT_KERNEL_MEGA;
+    int nc = direct && whole && !rays_out && n_chunks > 1 ? n_chunks : 1;
+    if (nc > 8) nc = 8;
+    if ((int64_t)p->height < 8LL * stride * nc) nc = 1;
+    cudaStream_t st = ctx->stream;
+    if (ctx->rb_pix < npix) {           // float64 rows + fp32 sums, grown on demand
+        if (ctx->d_rb) RT_CUDA_TRY(cudaFree(ctx->d_rb));
+        ctx->d_rb = nullptr;
+        ctx->rb_pix = 0;
+        RT_CUDA_TRY(cudaMalloc(&ctx->d_rb, 48 * (size_t)npix));
+        ctx->rb_pix = npix;
+    }
+    double* out64 = reinterpret_cast<double*>(ctx->d_rb);
+    float* acc32 = reinterpret_cast<float*>(out64 + 4 * ctx->rb_pix);
+    unsigned long long* d_rays = reinterpret_cast<unsigned long long*>(ctx->d_counter + 32);
+    if (direct) {
+        // pixels outside the band set / pixel range stay 0 (the kernel writes only its own)
+        if (!whole || stride > 1) RT_CUDA_TRY(cudaMemsetAsync(out64, 0, 32 * (size_t)npix, st));
+        if (nc == 1) {
+            int rc = rt_render_impl(ctx, s, p, nullptr, nullptr, out64);
+            if (rc) return rc;
+            RT_CUDA_TRY(cudaMemcpyAsync(host_out, out64, 32 * (size_t)npix, cudaMemcpyDeviceToHost, st));
+        } else {
+            int rc = rt_io_streams(ctx);
+            if (rc) return rc;
+            cudaStream_t cp = ctx->io_out;
+            // chunks of whole 4-row tile bands (multiples of 4 * stride rows keep every band)
+            const int64_t rows = ((int64_t)p->height + 4LL * stride * nc - 1) / (4LL * stride * nc) * 4 * stride;
+            int k = 0;
+            for (int64_t r0 = 0; r0 < p->height; r0 += rows, ++k) {
+                const int64_t r1 = r0 + rows < p->height ? r0 + rows : p->height;
+                rt_render_params q = *p;
+                q.pix_lo = r0 * p->width;
+                q.pix_hi = r1 * p->width;
+                rc = rt_render_impl(ctx, s, &q, nullptr, nullptr, out64);
+                if (rc) return rc;
+                RT_CUDA_TRY(cudaEventRecord(ctx->io_ev[k], st));
+                RT_CUDA_TRY(cudaStreamWaitEvent(cp, ctx->io_ev[k], 0));
+                RT_CUDA_TRY(cudaMemcpyAsync(host_out + 4 * q.pix_lo, out64 + 4 * q.pix_lo,
+                                            32 * (size_t)(q.pix_hi - q.pix_lo), cudaMemcpyDeviceToHost, cp));
+            }
+            RT_CUDA_TRY(cudaEventRecord(ctx->io_ev[8], cp));
+            RT_CUDA_TRY(cudaStreamWaitEvent(st, ctx->io_ev[8], 0));   // later work follows the copies
+        }
+    } else {
+        RT_CUDA_TRY(cudaMemsetAsync(acc32, 0, 16 * (size_t)npix, st));
+        int rc = rt_render_impl(ctx, s, p, acc32, nullptr);
+        if (rc) return rc;
+        widen_kernel<<<ctx->num_sms * 8, 256, 0, st>>>(reinterpret_cast<const float4*>(acc32),
+                                                        reinterpret_cast<double4*>(out64), npix);
+        RT_CUDA_TRY(cudaGetLastError());
+        RT_CUDA_TRY(cudaMemcpyAsync(host_out, out64, 32 * (size_t)npix, cudaMemcpyDeviceToHost, st));
+    }
+    if (rays_out) RT_CUDA_TRY(cudaMemcpyAsync(rays_out, d_rays, sizeof(uint64_t), cudaMemcpyDeviceToHost, st));
+    int err = 0;                                // the device error flag rides on the same sync
+    RT_CUDA_TRY(cudaMemcpyAsync(&err, ctx->d_error, sizeof err, cudaMemcpyDeviceToHost, st));
+    RT_CUDA_TRY(cudaStreamSynchronize(st));
+    return err ? rt_check_device_error(ctx) : RT_OK;
 }
 
 int rt_resolve_impl(rt_ctx* ctx, const float* accum, int64_t npix, int gamma, uint8_t* rgb) {

@@ -35,6 +35,8 @@ struct rt_ctx {
     unsigned probe_epoch;          // claim tag of the last probed render
     void* d_chunk_done;            // per-tile finished sample chunks of chunked PT frames (render.cu)
     int64_t chunk_tiles;
+    void* d_rb;                    // rt_render_host: float64 rows + fp32 sums of a frame
+    int64_t rb_pix;                // pixels d_rb holds
     void* h_tab;                   // pinned staging of rt_scene_compile's small tables (mesh.cu)
     size_t h_tab_bytes;
     cudaEvent_t tab_ev;            // its last copies (the buffer is rewritten only after them)
@@ -259,6 +261,10 @@ int rt_expand_hits_f64(rt_ctx* ctx, rt_scene* s, int64_t n, const float4* hits, 
                        double tmax_s = 0.0);
 int rt_pack_rays_f64(rt_ctx* ctx, int64_t n, const double* o, const double* d, const double* tmin,
                      const double* tmax, float* rays);
-int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out);
+int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* accum, uint64_t* rays_out,
+                   double* out64 = nullptr);
+int rt_render_host_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, double* host_out, int n_chunks,
+                        uint64_t* rays_out);
+int rt_io_streams(rt_ctx* c);
 int rt_raygen_impl(rt_ctx* ctx, const rt_render_params* p, int sample, float* rays);
 int rt_resolve_impl(rt_ctx* ctx, const float* accum, int64_t npix, int gamma, uint8_t* rgb);

@@ -108,16 +108,8 @@ def render_into(scene, accum, width, height, spp=1, integrator="pt", seed=0, cfg
     return int(rays[0]) if count_rays else None
 
 
-_PIPE_CHUNKS = 4                 # row bands of a pipelined render_frame
+_PIPE_CHUNKS = 4                 # row chunks of a pipelined eye render_frame (rt_render_host)
 _PIPE_MIN_PIXELS = 1 << 20
-_COPY_STREAMS = {}
-
-
-def _copy_stream(dev):
-    import torch
-    if dev not in _COPY_STREAMS:
-        _COPY_STREAMS[dev] = torch.cuda.Stream(dev)
-    return _COPY_STREAMS[dev]
 
 
 def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt", seed: int = 0,
@@ -134,10 +126,11 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
     (rt_multi_render).  Every pixel's samples are summed on one GPU, so the frame is
     bit-identical to ``gpus=1``.
 
-    The fp32 sums are widened to float64 on the device (exact) and read back by DMA into
-    pinned memory; large primary-ray (eye) megakernel frames render in 4 row chunks so each
-    chunk's readback overlaps the next chunk's render (return_stats=True renders in one
-    launch to count rays).  `bands=(stride, offset)` renders only that GPU's interleaved
+    One native call (rt_render_host) renders and reads back: eye frames in the megakernel
+    write their float64 rows directly (the exact widening of the fp32 sums), other frames
+    are widened on the device; the rows reach pinned memory by DMA.  Large eye frames render
+    in 4 row chunks so each chunk's readback overlaps the next chunk's render
+    (return_stats=True renders in one launch to count rays).  `bands=(stride, offset)` renders only that GPU's interleaved
     4-row tile bands (the multi-GPU tile split); the other pixels stay 0.  The returned
     array lives in pinned host memory (PyTorch's caching host allocator) until freed."""
     import torch
@@ -152,41 +145,21 @@ def render_frame(scene, width: int, height: int, spp: int, integrator: str = "pt
                                   samples, gpus)
     if bands is not None and int(bands[0]) == 1:
         bands = None                                 # one GPU's "split" is the whole frame
-    dev = torch.device("cuda", scene.tlas.ctx.device)
     npix = height * width
-    acc = torch.zeros((npix, 4), dtype=torch.float32, device=dev)
     host = torch.empty((npix, 4), dtype=torch.float64, pin_memory=True)
-    cur = torch.cuda.current_stream(dev)
-    stride = 1 if bands is None else int(bands[0])
-    # only primary-ray frames: there the readback is comparable to the render; a path-traced
-    # frame renders for far longer than its readback, and 4 launches add 4 wave tails
+    s0, s1 = (0, spp) if samples is None else samples
+    p = make_params(scene, width, height, s0, s1, integrator, seed, cfg, jitter, kernel)
+    if bands is not None:
+        p.band_stride, p.band_offset = int(bands[0]), int(bands[1])
+    # only primary-ray frames pipeline their readback: there it is comparable to the render;
+    # a path-traced frame renders for far longer than its readback, and chunks add wave tails
     # (config 3 e2e 4849 -> 4164 Mrays/s when pipelined)
-    nchunk = (_PIPE_CHUNKS if (npix >= _PIPE_MIN_PIXELS and not return_stats and kernel == "mega"
-                               and integrator == "eye" and height >= 8 * stride * _PIPE_CHUNKS) else 1)
-    if nchunk == 1:
-        rays = render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples,
-                           bands=bands)
-        host.copy_(acc.to(torch.float64), non_blocking=True)
-    else:
-        # row bands (whole 4-row tiles) rendered one after another; each band is widened and
-        # read back on a copy stream while the next one renders (same pixels, same values)
-        copy = _copy_stream(dev)
-        acc64 = torch.empty((npix, 4), dtype=torch.float64, device=dev)
-        # (band chunks start on multiples of 4 * stride rows, so every row keeps its band)
-        rows = -(-height // (4 * stride * nchunk)) * 4 * stride
-        for r0 in range(0, height, rows):
-            lo, hi = r0 * width, min(height, r0 + rows) * width
-            render_into(scene, acc, width, height, spp, integrator, seed, cfg, jitter, kernel, samples,
-                        pixels=(lo, hi), count_rays=False, bands=bands)
-            acc64[lo:hi].copy_(acc[lo:hi])
-            ev = torch.cuda.Event()
-            ev.record(cur)
-            copy.wait_event(ev)
-            with torch.cuda.stream(copy):
-                host[lo:hi].copy_(acc64[lo:hi], non_blocking=True)
-        cur.wait_stream(copy)
-        rays = None
-    cur.synchronize()
+    nc = _PIPE_CHUNKS if integrator == "eye" and npix >= _PIPE_MIN_PIXELS and not return_stats else 1
+    ray_count = np.zeros(1, np.uint64)
+    flat = getattr(scene, "render_tlas", None) or scene.tlas
+    check(lib().rt_render_host(flat.ctx.handle, flat.handle, p, ptr(host), nc,
+                               ptr(ray_count) if return_stats else None))
+    rays = int(ray_count[0]) if return_stats else None
     buf = AccumBuffer(width, height, host.numpy().reshape(height, width, 4))
     if return_stats:
         return buf, {"rays": rays}
