@@ -559,6 +559,23 @@ __device__ __forceinline__ void st_status_n(unsigned* p, const unsigned (&v)[PER
     }
 }
 
+#ifndef RT_SORT_TL
+#define RT_SORT_TL 0          // diagnostic builds: per-tile phase timestamps of the last wide pass
+#endif
+#if RT_SORT_TL
+#define RT_SORT_TL_TILES 4096
+__device__ unsigned long long g_sort_tl[5 * RT_SORT_TL_TILES];
+__device__ __forceinline__ unsigned long long sort_tl_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SORT_TL_MARK(k, v) \
+    if (threadIdx.x == 0 && sm.tile < RT_SORT_TL_TILES) g_sort_tl[5 * sm.tile + (k)] = (v)
+#else
+#define SORT_TL_MARK(k, v)
+#endif
+
 // shared-memory layout of the 10-bit pass (dynamic: 86 KB at 512 threads)
 // K: key type; T threads per tile; DB digit bits (1 << DB bins); ITEMS keys per thread
 template <typename K, int T, int DB, int ITEMS_>
@@ -586,6 +603,9 @@ __device__ __forceinline__ void onesweep_wide_pass(const K* __restrict__ keys_in
     extern __shared__ __align__(16) unsigned char sort10_smem[];
     SM& sm = *reinterpret_cast<SM*>(sort10_smem);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#if RT_SORT_TL
+    const unsigned long long tl0 = sort_tl_now();
+#endif
     if (tid == 0) sm.tile = atomicAdd(counter, 1u);
     {
         uint4* z = reinterpret_cast<uint4*>(&sm.warp[0][0]);
@@ -596,6 +616,8 @@ __device__ __forceinline__ void onesweep_wide_pass(const K* __restrict__ keys_in
     pdl_wait();
     pdl_trigger();
     __syncthreads();
+    SORT_TL_MARK(0, tl0);
+    SORT_TL_MARK(1, sort_tl_now());
     const unsigned tile = sm.tile;
     const int64_t seg = (int64_t)tile * TILE + (int64_t)warp * (32 * ITEMS);
     K key[ITEMS];
@@ -634,6 +656,7 @@ __device__ __forceinline__ void onesweep_wide_pass(const K* __restrict__ keys_in
         rank[i] = base + below;
     }
     __syncthreads();
+    SORT_TL_MARK(2, sort_tl_now());
     // warp prefixes of this thread's PER bins; tc = the tile's count per bin
     unsigned tc[PER];
 #pragma unroll
@@ -717,6 +740,7 @@ __device__ __forceinline__ void onesweep_wide_pass(const K* __restrict__ keys_in
     for (int q = 0; q < PER; ++q) hv[q] = __ldg(hist + PER * tid + q);
     Scan(sm.scan_tmp).ExclusiveSum(hv, bin_excl);
     __syncthreads();
+    SORT_TL_MARK(3, sort_tl_now());
     Scan(sm.scan_tmp).ExclusiveSum(tc, tile_excl);
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
@@ -739,6 +763,10 @@ __device__ __forceinline__ void onesweep_wide_pass(const K* __restrict__ keys_in
         keys_out[pos] = k;
         vals_out[pos] = sm.vals[j];
     }
+#if RT_SORT_TL
+    __syncthreads();
+    SORT_TL_MARK(4, sort_tl_now());
+#endif
 }
 // 30-bit keys: 3 passes of 10-bit digits
 typedef SortWSmem<uint32_t, SORT_THREADS10, 10, SORT_ITEMS10> Sort10Smem;
@@ -974,3 +1002,11 @@ size_t rt_sort_scratch_words(int64_t n) {
     if (w9 > w) w = w9;
     return (w + 3) & ~(size_t)3;        // whole 16-B units (zeroed as uint4 by the emit hand-off)
 }
+
+#if RT_SORT_TL
+extern "C" int rt_debug_sort_timeline(unsigned long long* out, int32_t n_tiles) {
+    if (n_tiles > RT_SORT_TL_TILES) n_tiles = RT_SORT_TL_TILES;
+    RT_CUDA_TRY(cudaMemcpyFromSymbol(out, g_sort_tl, sizeof(unsigned long long) * 5 * n_tiles));
+    return RT_OK;
+}
+#endif
