@@ -303,6 +303,9 @@ __device__ __forceinline__ void sample_ptnee(const FrameConst& F, const float4* 
 // once, by one lane, exactly as before (claims: one atomicMax of the render's epoch per
 // tile).
 #ifndef RT_PT_CHUNK
+#ifndef RT_RENDER_PDL
+#define RT_RENDER_PDL 1         // counters zeroed by a kernel, frame launched with programmatic dependent launch
+#endif
 #define RT_PT_CHUNK 8           // samples per work unit of multi-sample PT / AO frames (0: whole tiles)
 #endif
 #ifndef RT_PROBE_BUDGET
@@ -401,6 +404,16 @@ __device__ __forceinline__ long long probed_next_tile(const FrameConst& F, unsig
 }
 
 // ---- K7: megakernel --------------------------------------------------------
+// the megakernel's work counters and probe control words, zeroed by a kernel launched with
+// programmatic dependent launch (it and the megakernel queue behind the previous kernel --
+// e.g. the LBVH build's last -- without two memset nodes and their launch gaps)
+__global__ void render_ctl_zero_kernel(unsigned* __restrict__ counter, unsigned* __restrict__ probe_ctl) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous kernel (the BVH, a frame) is done
+    const int t = threadIdx.x;
+    if (t < 64) counter[t] = 0u;
+    if (probe_ctl && t < PC_WORDS) probe_ctl[t] = 0u;
+}
+
 // float64 copy of fp32 sums (render_frame's readback of every frame but the eye frames)
 __global__ void widen_kernel(const float4* __restrict__ acc, double4* __restrict__ out, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -419,6 +432,7 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     const float4* __restrict__ mat_emis, const float4* __restrict__ lights, int n_lights,
     float4* __restrict__ accum, unsigned int* counter, unsigned long long* ray_total, int* err,
     const SphereView sv) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // zeroed counters (and the BVH) first
     const int height = __float_as_int(__ldg(nodes + 3).z);
     const int root4 = __float_as_int(__ldg(nodes + 3).w);
     if (height + 1 > RT_STACK) {
@@ -911,7 +925,6 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
     }
     cudaStream_t st = ctx->stream;
     unsigned long long* d_rays = reinterpret_cast<unsigned long long*>(ctx->d_counter + 32);
-    RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, 64 * sizeof(unsigned int), st));
     float4* acc = reinterpret_cast<float4*>(accum);
     if (p->kernel == RT_KERNEL_MEGA) {
         const int64_t ntiles = F.nunits >> 5;
@@ -928,8 +941,7 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             F.epoch = ++ctx->probe_epoch;
             F.heavy_q = reinterpret_cast<unsigned long long*>(ctx->d_probe);
             F.claims = reinterpret_cast<unsigned*>(F.heavy_q + ctx->probe_tiles);
-            F.probe_ctl = F.claims + ctx->probe_tiles;
-            RT_CUDA_TRY(cudaMemsetAsync(F.probe_ctl, 0, PC_WORDS * 4, st));
+            F.probe_ctl = F.claims + ctx->probe_tiles;   // (zeroed by render_ctl_zero_kernel below)
         }
         if (F.integ != RT_INTEG_EYE && F.tiled && RT_PT_CHUNK > 0 && p->s1 - p->s0 > RT_PT_CHUNK && ntiles > 1) {
             if (ctx->chunk_tiles < ntiles) {
@@ -950,6 +962,20 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             }
             F.out64 = reinterpret_cast<double4*>(out64);
         }
+        // counters + probe words zeroed, then the frame: both launched with programmatic
+        // stream serialization (each waits in-kernel for its predecessor: griddepcontrol.wait)
+        cudaLaunchAttribute pdl[1];
+        pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        pdl[0].val.programmaticStreamSerializationAllowed = RT_RENDER_PDL;
+        {
+            cudaLaunchConfig_t zc = {};
+            zc.gridDim = dim3(1);
+            zc.blockDim = dim3(256);
+            zc.stream = st;
+            zc.attrs = pdl;
+            zc.numAttrs = 1;
+            RT_CUDA_TRY(cudaLaunchKernelEx(&zc, render_ctl_zero_kernel, ctx->d_counter, F.probe_ctl));
+        }
         auto launch = [&](auto kern) -> int {
             int bps = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, MEGA_THREADS, 0);
@@ -957,11 +983,17 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             int64_t grid = (int64_t)ctx->num_sms * bps;
             int64_t want = (F.nunits + MEGA_THREADS - 1) / MEGA_THREADS;
             if (grid > want) grid = want;
-            kern<<<(unsigned)grid, MEGA_THREADS, 0, st>>>(F, p->s0, p->s1, s->nodes, s->bvh4, s->tri_sorted,
-                                                          s->tri_attr, s->mat_color, s->mat_emissive, s->lights,
-                                                          s->n_lights, acc, ctx->d_counter, d_rays, ctx->d_error,
-                                                          rt_sphere_view(ctx, s, 0));
-            RT_CUDA_TRY(cudaGetLastError());
+            cudaLaunchConfig_t mc = {};
+            mc.gridDim = dim3((unsigned)grid);
+            mc.blockDim = dim3(MEGA_THREADS);
+            mc.stream = st;
+            mc.attrs = pdl;
+            mc.numAttrs = 1;
+            RT_CUDA_TRY(cudaLaunchKernelEx(&mc, kern, F, p->s0, p->s1, (const float4*)s->nodes, (const float4*)s->bvh4,
+                                           (const float4*)s->tri_sorted, (const float4*)s->tri_attr,
+                                           (const float4*)s->mat_color, (const float4*)s->mat_emissive,
+                                           (const float4*)s->lights, s->n_lights, acc, ctx->d_counter, d_rays,
+                                           ctx->d_error, rt_sphere_view(ctx, s, 0)));
             return RT_OK;
         };
         int rc;
@@ -994,6 +1026,7 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             rt_set_error("the wavefront kernel supports max_depth <= 30 (got %d); use kernel='mega'", F.max_depth);
             return RT_EINVAL;
         }
+        RT_CUDA_TRY(cudaMemsetAsync(ctx->d_counter, 0, 64 * sizeof(unsigned int), st));
         WaveBuffers* wb;
         int rc = ensure_wave(s, F.nunits, wb);
         if (rc) return rc;
