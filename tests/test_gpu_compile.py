@@ -140,3 +140,41 @@ def test_compile_time_config_sizes(native):
         print(f"compile_scene({label}, lbvh30): {1e3 * dt:.1f} ms (incl. H2D of float64 vertices + int64 faces, "
               f"device validation, flatten, LBVH build)")
         assert sc.tlas.n in (1_000_000, 10_000_000)
+
+
+def test_async_upload_abi(native):
+    """rt_mesh_upload_async / rt_mesh_upload_finish at the C ABI: the verdict arrives at
+    finish (BuildError code), a failed mesh is refused by rt_scene_compile (RT_ESTATE), a
+    second finish is a no-op, and a pending mesh can be destroyed safely."""
+    import ctypes
+    from paper_2603_00292_b200 import _native
+    L = _native.lib()
+    ctx = _native.Context.get(0)
+    V = np.random.default_rng(2).normal(size=(30, 3))
+    F = np.arange(30, dtype=np.int64).reshape(-1, 3)
+    bounds = np.zeros(6)
+    m = ctypes.c_void_p()
+    assert L.rt_mesh_upload_async(ctx.handle, 30, _native.ptr(V), 10, _native.ptr(F), ctypes.byref(m)) == 0
+    assert L.rt_mesh_upload_finish(ctx.handle, m, _native.ptr(bounds)) == 0
+    assert np.array_equal(bounds, np.concatenate([V.min(0), V.max(0)]))
+    assert L.rt_mesh_upload_finish(ctx.handle, m, _native.ptr(bounds)) == 0       # again: no-op
+    L.rt_mesh_destroy(m)
+    F2 = F.copy()
+    F2[3, 0] = 30
+    bad = ctypes.c_void_p()
+    assert L.rt_mesh_upload_async(ctx.handle, 30, _native.ptr(V), 10, _native.ptr(F2), ctypes.byref(bad)) == 0
+    rc = L.rt_mesh_upload_finish(ctx.handle, bad, _native.ptr(bounds))
+    assert rc != 0 and L.rt_last_error().decode() == "face index out of range"
+    src = (_native.InstanceSrc * 1)()
+    src[0].mesh, src[0].material, src[0].mask = 0, 0, 0xFFFFFFFF
+    src[0].matrix[:] = [1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0]
+    src[0].inverse[:] = [1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0]
+    col = np.ones((1, 3), np.float32)
+    h = ctypes.c_void_p()
+    rc = L.rt_scene_compile(ctx.handle, 1, (ctypes.c_void_p * 1)(bad.value), 1, src, 0, None, _native.ptr(col),
+                            _native.ptr(col), 1, ctypes.byref(h))
+    assert rc != 0 and "failed its validation" in L.rt_last_error().decode()
+    L.rt_mesh_destroy(bad)
+    pend = ctypes.c_void_p()
+    assert L.rt_mesh_upload_async(ctx.handle, 30, _native.ptr(V), 10, _native.ptr(F), ctypes.byref(pend)) == 0
+    L.rt_mesh_destroy(pend)                                                    # still pending: waits
