@@ -158,10 +158,8 @@ void rt_ctx_destroy(rt_ctx* c) {
     if (c->d_probe) cudaFree(c->d_probe);
     if (c->d_chunk_done) cudaFree(c->d_chunk_done);
     if (c->d_rb) cudaFree(c->d_rb);
-    if (c->h_tab) {
-        cudaFreeHost(c->h_tab);
-        cudaEventDestroy(c->tab_ev);
-    }
+    if (c->h_tab) cudaFreeHost(c->h_tab);
+    if (c->tab_ev) cudaEventDestroy(c->tab_ev);
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
     cudaStreamDestroy(c->own_stream);

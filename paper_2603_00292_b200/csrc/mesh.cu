@@ -448,15 +448,16 @@ struct TableStage {
     cudaError_t flush(rt_ctx* c) {
         if (host.empty()) return cudaSuccess;
         cudaError_t e = cudaSuccess;
+        if (!c->tab_ev) {
+            e = cudaEventCreateWithFlags(&c->tab_ev, cudaEventDisableTiming);
+            if (e != cudaSuccess) return e;
+        }
         if (c->h_tab_bytes < host.size()) {
             if (c->h_tab) {
                 cudaEventSynchronize(c->tab_ev);
                 cudaFreeHost(c->h_tab);
                 c->h_tab = nullptr;
                 c->h_tab_bytes = 0;
-            } else {
-                e = cudaEventCreateWithFlags(&c->tab_ev, cudaEventDisableTiming);
-                if (e != cudaSuccess) return e;
             }
             size_t cap = 64 << 10;
             while (cap < host.size()) cap *= 2;
