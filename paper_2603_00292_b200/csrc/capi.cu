@@ -409,7 +409,7 @@ void rt_scene_destroy(rt_scene* s) {
                     s->nodes, s->tri_sorted, s->bvh4, s->keys_a, s->keys_b, s->vals_a, s->vals_b, s->child,
                     s->flags, s->cbounds, s->sort_scratch, s->leaf_box, s->emit_items, s->seg_count, s->lights,
                     s->spheres,
-                    s->lnormal64, s->lrows64, s->wnormal64, s->inst_inv64};
+                    s->lnormal64, s->lrows64, s->wnormal64, s->inst_inv64, s->probe_hint};
     cudaSetDevice(s->device);
     for (void* p : ptrs) rt_free(p, s->stream);
     delete s;

@@ -51,6 +51,7 @@ struct FrameConst {
     unsigned* claims;              // (tiles)
     unsigned long long* heavy_q;   // (tiles) (epoch << 32 | tile) of heavy tiles, in push order
     unsigned* probe_ctl;           // PC_WORDS control words (zeroed per render)
+    unsigned* probe_hint;          // the scene's "last probed frame stopped" word
     // sample chunks of multi-sample frames (see the megakernel): 0 = one unit per tile
     int chunk;                     // samples per unit
     int nchunks;
@@ -320,7 +321,13 @@ constexpr int PROBE_LANE = 12;  // (x 4, y 1) of the 8x4 tile
 // costly 4K scene pays for 66K probe walks before the stop rule can see it
 constexpr int PROBE_BATCH = 16;
 // probe control words, one per 128-B line of F.probe_ctl
-constexpr int PC_TAKEN = 0, PC_HEAD = 32, PC_TAIL = 64, PC_DONE = 96, PC_STOP = 128, PC_LIMIT = 160, PC_WORDS = 192;
+constexpr int PC_TAKEN = 0, PC_HEAD = 32, PC_TAIL = 64, PC_DONE = 96, PC_STOP = 128, PC_LIMIT = 160, PC_MODE = 192,
+              PC_WORDS = 224;
+// A scene whose last probed frame stopped probing (uniformly costly: the 10M soup) renders its
+// next frames row-major without probes, re-probing every RT_PROBE_REPROBE-th frame
+#ifndef RT_PROBE_REPROBE
+#define RT_PROBE_REPROBE 8
+#endif
 struct ProbeBudget {
     int it, budget;
     __device__ __forceinline__ bool tick() { return ++it > budget; }
@@ -367,6 +374,7 @@ __device__ __forceinline__ unsigned probe_take(const FrameConst& F, unsigned* pc
     stop = seen_stop || nh >= (unsigned)(ntiles / RT_PROBE_CAP_DIV) || (pb >= 4096u && nh * RT_PROBE_CAP_DIV > pb);
     if (stop && !seen_stop) {
         *reinterpret_cast<volatile unsigned*>(pc + PC_STOP) = 1u;
+        *reinterpret_cast<volatile unsigned*>(F.probe_hint) = 1u;   // the scene's next frames skip the probe
         unsigned lim;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 0;" : "=r"(lim) : "l"(pc + PC_TAKEN) : "memory");
         atomicMax(pc + PC_LIMIT, lim + 1u);
@@ -407,11 +415,22 @@ __device__ __forceinline__ long long probed_next_tile(const FrameConst& F, unsig
 // the megakernel's work counters and probe control words, zeroed by a kernel launched with
 // programmatic dependent launch (it and the megakernel queue behind the previous kernel --
 // e.g. the LBVH build's last -- without two memset nodes and their launch gaps)
-__global__ void render_ctl_zero_kernel(unsigned* __restrict__ counter, unsigned* __restrict__ probe_ctl) {
+// It also decides whether this eye frame probes (PC_MODE): not when the scene's last probed
+// frame stopped probing, except every RT_PROBE_REPROBE-th frame; a probing frame clears the
+// scene's hint (its own stop sets it again).
+__global__ void render_ctl_zero_kernel(unsigned* __restrict__ counter, unsigned* __restrict__ probe_ctl,
+                                       unsigned* __restrict__ hint, unsigned epoch) {
     asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous kernel (the BVH, a frame) is done
     const int t = threadIdx.x;
     if (t < 64) counter[t] = 0u;
-    if (probe_ctl && t < PC_WORDS) probe_ctl[t] = 0u;
+    if (probe_ctl && t < PC_WORDS) {
+        unsigned v = 0u;
+        if (t == PC_MODE) {
+            v = (*hint == 0u || epoch % RT_PROBE_REPROBE == 0u) ? 1u : 0u;
+            if (v) *hint = 0u;
+        }
+        probe_ctl[t] = v;
+    }
 }
 
 // float64 copy of fp32 sums (render_frame's readback of every frame but the eye frames)
@@ -455,8 +474,8 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     unsigned n_fetch = 0;
 #endif
-    const bool probe_on = INTEG == RT_INTEG_EYE && F.probe_budget > 0;
     unsigned* const pc = F.probe_ctl;
+    const bool probe_on = INTEG == RT_INTEG_EYE && F.probe_budget > 0 && __ldcg(pc + PC_MODE) != 0u;
     const int64_t ntiles = F.nunits >> 5;
     // per-warp fetch state of the probed schedule, kept out of registers (the walk's loop is
     // register-bound): the heavy queue is still worth polling; the first unprobed tile + 1
@@ -802,6 +821,7 @@ FrameConst make_frame(const rt_render_params* p) {
     F.claims = nullptr;
     F.heavy_q = nullptr;
     F.probe_ctl = nullptr;
+    F.probe_hint = nullptr;
     F.chunk = 0;
     F.nchunks = 1;
     F.chunk_done = nullptr;
@@ -942,6 +962,11 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             F.heavy_q = reinterpret_cast<unsigned long long*>(ctx->d_probe);
             F.claims = reinterpret_cast<unsigned*>(F.heavy_q + ctx->probe_tiles);
             F.probe_ctl = F.claims + ctx->probe_tiles;   // (zeroed by render_ctl_zero_kernel below)
+            if (!s->probe_hint) {
+                RT_CUDA_TRY(rt_alloc((void**)&s->probe_hint, sizeof(unsigned), st, false));
+                RT_CUDA_TRY(cudaMemsetAsync(s->probe_hint, 0, sizeof(unsigned), st));
+            }
+            F.probe_hint = s->probe_hint;
         }
         if (F.integ != RT_INTEG_EYE && F.tiled && RT_PT_CHUNK > 0 && p->s1 - p->s0 > RT_PT_CHUNK && ntiles > 1) {
             if (ctx->chunk_tiles < ntiles) {
@@ -974,7 +999,8 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             zc.stream = st;
             zc.attrs = pdl;
             zc.numAttrs = 1;
-            RT_CUDA_TRY(cudaLaunchKernelEx(&zc, render_ctl_zero_kernel, ctx->d_counter, F.probe_ctl));
+            RT_CUDA_TRY(cudaLaunchKernelEx(&zc, render_ctl_zero_kernel, ctx->d_counter, F.probe_ctl, F.probe_hint,
+                                           F.epoch));
         }
         auto launch = [&](auto kern) -> int {
             int bps = 0;

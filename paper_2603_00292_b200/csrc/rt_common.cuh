@@ -52,6 +52,7 @@ struct rt_ctx {
 };
 
 struct rt_scene {
+    unsigned* probe_hint;  // device word: the last probed eye frame of this scene stopped probing (render.cu)
     int64_t n;
     int n_mat;
     int device;

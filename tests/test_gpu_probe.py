@@ -4,7 +4,8 @@ The probe only reorders which 8x4 tiles are rendered first, so every frame must 
 bit-identical to the row-major schedule (budget 0): whole frames, partial edge tiles,
 several samples per pixel, pixel-range (chunked) renders and tile-band (multi-GPU) renders.
 The probe's own bookkeeping is checked through rt_probe_stats: the config-2 sphere queues
-its silhouette tiles, a uniformly costly soup stops probing early.
+its silhouette tiles, a uniformly costly soup stops probing early -- and its next frames skip
+the probe but for every 8th.
 """
 
 import ctypes
@@ -84,6 +85,12 @@ def test_uniform_soup_stops_probing(native):
     assert st["limit"] > 0, st                        # stopped: a large share of the probes ran out
     assert st["probed"] == ((ntiles + 15) // 16) * 16, st   # every batch still completes
     assert st["popped"] == 0 or st["popped"] <= st["queued"] + 4144, st
+    # the scene's next frames skip the probe (row-major), re-probing every 8th frame
+    probed = []
+    for _ in range(8):
+        assert np.array_equal(frame(sc, w, h, budget=24), ref)
+        probed.append(probe_stats(sc)["probed"])
+    assert sum(p > 0 for p in probed) == 1, probed
 
 
 def test_budget_is_validated(native):

@@ -1,0 +1,14 @@
+#!/bin/bash
+# Probe-skip hint A/B on one box: a scene whose last probed frame stopped probing renders
+# row-major (default: re-probe every 8th frame) vs probing every frame (variants/noskip).
+cd "$(dirname "$0")/.."
+timeout 600 python -m pytest tests/test_gpu_probe.py tests/test_gpu_readback.py -x -q 2>&1 | tail -1
+for r in 1 2; do
+  for lib in "" variants/noskip/librt_b200.so; do
+    echo "== ${lib:-default}"; RT_B200_LIB=$lib timeout 300 python tools/eye_probe.py --soup --reps 17 2>&1 | tail -1
+  done
+done
+for lib in "" variants/noskip/librt_b200.so; do
+  echo "== bench c4 ${lib:-default}"; RT_B200_LIB=$lib timeout 600 python bench.py --config 4 --no-cpu --no-pt --no-e2e --steps 60 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(round(d['value'],1), round(d['ms_per_step'],4), round(d['trace_mrays_s'],1))"
+  echo "== bench c2 ${lib:-default}"; RT_B200_LIB=$lib timeout 600 python bench.py --no-cpu --no-pt --no-e2e --steps 400 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(round(d['value'],1), round(d['ms_per_step'],4), round(d['trace_mrays_s'],1))"
+done
