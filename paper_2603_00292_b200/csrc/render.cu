@@ -322,11 +322,20 @@ constexpr int PROBE_LANE = 12;  // (x 4, y 1) of the 8x4 tile
 constexpr int PROBE_BATCH = 16;
 // probe control words, one per 128-B line of F.probe_ctl
 constexpr int PC_TAKEN = 0, PC_HEAD = 32, PC_TAIL = 64, PC_DONE = 96, PC_STOP = 128, PC_LIMIT = 160, PC_MODE = 192,
-              PC_WORDS = 224;
+              PC_QTAG = 193, PC_ZERO = 224;
+// persistent across frames (not zeroed): the last complete heavy-tile queue (length, tag,
+// valid) and the epoch of the last frame
+constexpr int PC_QLEN = 224, PC_QEPOCH = 225, PC_QVALID = 226, PC_EPOCH = 227, PC_WORDS = 256;
+// frame modes (PC_MODE): row-major, probed (probe batches + heavy queue), replay (the heavy
+// queue of the scene's last complete probe, no probe walks)
+constexpr unsigned PM_ROW = 0, PM_PROBE = 1, PM_REPLAY = 2;
 // A scene whose last probed frame stopped probing (uniformly costly: the 10M soup) renders its
 // next frames row-major without probes, re-probing every RT_PROBE_REPROBE-th frame
 #ifndef RT_PROBE_REPROBE
 #define RT_PROBE_REPROBE 8
+#endif
+#ifndef RT_PROBE_REPLAY
+#define RT_PROBE_REPLAY 1       // replay the last complete heavy-tile queue of the same scene
 #endif
 struct ProbeBudget {
     int it, budget;
@@ -348,7 +357,7 @@ __device__ __forceinline__ int64_t heavy_pop(const FrameConst& F, unsigned* pc, 
     const unsigned h = atomicAdd(pc + PC_HEAD, 1u);
     while (true) {
         const unsigned long long e = *reinterpret_cast<volatile unsigned long long*>(F.heavy_q + h);
-        if ((unsigned)(e >> 32) == F.epoch) return (int64_t)(e & 0xFFFFFFFFull);
+        if ((unsigned)(e >> 32) == ld_volatile_u32(pc + PC_QTAG)) return (int64_t)(e & 0xFFFFFFFFull);
         unsigned done;
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(done) : "l"(pc + PC_DONE) : "memory");
         if (done >= ntiles_b && h >= ld_volatile_u32(pc + PC_TAIL)) return -1;
@@ -415,21 +424,51 @@ __device__ __forceinline__ long long probed_next_tile(const FrameConst& F, unsig
 // the megakernel's work counters and probe control words, zeroed by a kernel launched with
 // programmatic dependent launch (it and the megakernel queue behind the previous kernel --
 // e.g. the LBVH build's last -- without two memset nodes and their launch gaps)
-// It also decides whether this eye frame probes (PC_MODE): not when the scene's last probed
-// frame stopped probing, except every RT_PROBE_REPROBE-th frame; a probing frame clears the
-// scene's hint (its own stop sets it again).
-__global__ void render_ctl_zero_kernel(unsigned* __restrict__ counter, unsigned* __restrict__ probe_ctl,
-                                       unsigned* __restrict__ hint, unsigned epoch) {
+// It also sets this eye frame's mode (PC_MODE).  Row-major when the scene's last probed
+// frame stopped probing (the hint); a replay of the last complete heavy-tile queue when the
+// previous probe-capable frame was of the same scene and tile geometry (replay_ok) and its
+// queue is complete (a probe that ran to the end, or a replay of one); else a probed frame,
+// which clears the hint (its own stop sets it again).  Every RT_PROBE_REPROBE-th frame
+// probes.  A replay frame starts with every probe batch counted done and the old queue's
+// length and tag (its tiles are claimed with this frame's epoch as usual).
+__global__ void render_ctl_zero_kernel(unsigned* __restrict__ counter, unsigned* __restrict__ pc,
+                                       unsigned* __restrict__ hint, unsigned epoch, int replay_ok,
+                                       unsigned ntiles_b) {
     asm volatile("griddepcontrol.wait;" ::: "memory");   // the previous kernel (the BVH, a frame) is done
+    __shared__ unsigned s_mode, s_qlen, s_qtag;
     const int t = threadIdx.x;
     if (t < 64) counter[t] = 0u;
-    if (probe_ctl && t < PC_WORDS) {
-        unsigned v = 0u;
-        if (t == PC_MODE) {
-            v = (*hint == 0u || epoch % RT_PROBE_REPROBE == 0u) ? 1u : 0u;
-            if (v) *hint = 0u;
+    if (!pc) return;
+    if (t == 0) {
+        const unsigned pm = pc[PC_MODE];
+        if (pm == PM_PROBE && pc[PC_STOP] == 0u) {         // the previous frame's complete queue
+            pc[PC_QLEN] = pc[PC_TAIL];
+            pc[PC_QEPOCH] = pc[PC_EPOCH];
+            pc[PC_QVALID] = 1u;
+        } else if (pm != PM_REPLAY) {
+            pc[PC_QVALID] = 0u;
         }
-        probe_ctl[t] = v;
+        const bool reprobe = epoch % RT_PROBE_REPROBE == 0u;
+        unsigned mode;
+        if (*hint != 0u && !reprobe) mode = PM_ROW;
+        else if (replay_ok && pc[PC_QVALID] && !reprobe) mode = PM_REPLAY;
+        else {
+            mode = PM_PROBE;
+            *hint = 0u;
+        }
+        pc[PC_EPOCH] = epoch;
+        s_mode = mode;
+        s_qlen = pc[PC_QLEN];
+        s_qtag = mode == PM_REPLAY ? pc[PC_QEPOCH] : epoch;
+    }
+    __syncthreads();
+    if (t < PC_ZERO) {
+        unsigned v = 0u;
+        if (t == PC_MODE) v = s_mode;
+        else if (t == PC_QTAG) v = s_qtag;
+        else if (s_mode == PM_REPLAY && t == PC_TAIL) v = s_qlen;
+        else if (s_mode == PM_REPLAY && t == PC_DONE) v = ntiles_b;
+        pc[t] = v;
     }
 }
 
@@ -475,7 +514,8 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     unsigned n_fetch = 0;
 #endif
     unsigned* const pc = F.probe_ctl;
-    const bool probe_on = INTEG == RT_INTEG_EYE && F.probe_budget > 0 && __ldcg(pc + PC_MODE) != 0u;
+    const unsigned pmode = INTEG == RT_INTEG_EYE && F.probe_budget > 0 ? __ldcg(pc + PC_MODE) : PM_ROW;
+    const bool probe_on = pmode != PM_ROW;
     const int64_t ntiles = F.nunits >> 5;
     // per-warp fetch state of the probed schedule, kept out of registers (the walk's loop is
     // register-bound): the heavy queue is still worth polling; the first unprobed tile + 1
@@ -487,7 +527,7 @@ __global__ void __launch_bounds__(MEGA_THREADS, MEGA_MIN_BLOCKS) pt_megakernel(
     }
     __syncwarp();
     // warps beyond the batch count start on row-major work (no pile-up on the batch counter)
-    bool probing = probe_on &&
+    bool probing = pmode == PM_PROBE &&
                    (int64_t)(blockIdx.x * (MEGA_THREADS / 32) + (threadIdx.x >> 5)) < (ntiles + PROBE_BATCH - 1) / PROBE_BATCH;
     while (true) {
         int64_t base;
@@ -948,14 +988,16 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
     float4* acc = reinterpret_cast<float4*>(accum);
     if (p->kernel == RT_KERNEL_MEGA) {
         const int64_t ntiles = F.nunits >> 5;
+        bool rb_replay = false;
         if (F.integ == RT_INTEG_EYE && F.tiled && probe_budget() > 0 && ntiles > 1) {
             if (ctx->probe_tiles < ntiles || ctx->probe_epoch == 0xFFFFFFFFu) {
                 if (ctx->d_probe) RT_CUDA_TRY(cudaFree(ctx->d_probe));
                 ctx->d_probe = nullptr;
                 RT_CUDA_TRY(cudaMalloc(&ctx->d_probe, (size_t)ntiles * 12 + PC_WORDS * 4));
-                RT_CUDA_TRY(cudaMemsetAsync(ctx->d_probe, 0, (size_t)ntiles * 12, st));
+                RT_CUDA_TRY(cudaMemsetAsync(ctx->d_probe, 0, (size_t)ntiles * 12 + PC_WORDS * 4, st));
                 ctx->probe_tiles = ntiles;
                 ctx->probe_epoch = 0;
+                ctx->lp_scene = nullptr;
             }
             F.probe_budget = probe_budget();
             F.epoch = ++ctx->probe_epoch;
@@ -967,6 +1009,13 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
                 RT_CUDA_TRY(cudaMemsetAsync(s->probe_hint, 0, sizeof(unsigned), st));
             }
             F.probe_hint = s->probe_hint;
+            // the heavy-tile queue of this scene's last probe can be replayed when the tiles
+            // are the same ones (scene, tile geometry and probe budget unchanged)
+            const int64_t key[4] = {F.tiles_x * 1000003 + ntiles, F.row0 * 1000003 + F.row1,
+                                    (int64_t)F.band_stride * 1000003 + F.band_offset, F.probe_budget};
+            rb_replay = ctx->lp_scene == s && memcmp(ctx->lp_key, key, sizeof key) == 0;
+            ctx->lp_scene = s;
+            memcpy(ctx->lp_key, key, sizeof key);
         }
         if (F.integ != RT_INTEG_EYE && F.tiled && RT_PT_CHUNK > 0 && p->s1 - p->s0 > RT_PT_CHUNK && ntiles > 1) {
             if (ctx->chunk_tiles < ntiles) {
@@ -999,8 +1048,9 @@ int rt_render_impl(rt_ctx* ctx, rt_scene* s, const rt_render_params* p, float* a
             zc.stream = st;
             zc.attrs = pdl;
             zc.numAttrs = 1;
+            const unsigned ntiles_b = (unsigned)((ntiles + PROBE_BATCH - 1) / PROBE_BATCH * PROBE_BATCH);
             RT_CUDA_TRY(cudaLaunchKernelEx(&zc, render_ctl_zero_kernel, ctx->d_counter, F.probe_ctl, F.probe_hint,
-                                           F.epoch));
+                                           F.epoch, (int)(rb_replay && RT_PROBE_REPLAY), ntiles_b));
         }
         auto launch = [&](auto kern) -> int {
             int bps = 0;

@@ -33,6 +33,8 @@ struct rt_ctx {
     void* d_probe;                 // tile-probe heavy queue + claims of eye renders (render.cu), grown on demand
     int64_t probe_tiles;
     unsigned probe_epoch;          // claim tag of the last probed render
+    const void* lp_scene;          // the last probe-capable eye frame: scene and tile geometry
+    int64_t lp_key[4];             // (a replay of its heavy-tile queue needs the same ones)
     void* d_chunk_done;            // per-tile finished sample chunks of chunked PT frames (render.cu)
     int64_t chunk_tiles;
     void* d_rb;                    // rt_render_host: float64 rows + fp32 sums of a frame

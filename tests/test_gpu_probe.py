@@ -62,6 +62,20 @@ def test_sphere_frame_identical_and_silhouette_queued(sphere):
     assert st["popped"] >= st["queued"], st
 
 
+def test_repeated_frames_replay_identical(sphere):
+    """Frames of the same scene and tile geometry replay the last complete heavy-tile queue
+    (no probe walks; every 8th frame probes again): identical frames, the same queue."""
+    ref = frame(sphere, 1920, 1080, budget=0)
+    queued = set()
+    for _ in range(10):
+        assert np.array_equal(frame(sphere, 1920, 1080, budget=24), ref)
+        queued.add(probe_stats(sphere)["queued"])
+    other = frame(sphere, 1280, 720, budget=0)          # another geometry in between: probes again
+    assert np.array_equal(frame(sphere, 1280, 720, budget=24), other)
+    assert np.array_equal(frame(sphere, 1920, 1080, budget=24), ref)
+    assert len(queued) <= 2, queued                     # (a re-probe may queue a few tiles differently)
+
+
 @pytest.mark.parametrize("w,h,spp", [(1001, 603, 1), (640, 360, 3), (8, 4, 1), (37, 5, 2)])
 def test_ragged_frames_and_samples_identical(sphere, w, h, spp):
     for budget in (1, 24):                            # budget 1: nearly every tile is queued
