@@ -5,7 +5,7 @@
 # unchanged since the r2d ncu captures.)
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-bash tools/job_r2_bench.sh r2e
-timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/r2e_pytest.log 2>&1
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2e_smoke.log 2>&1
+bash tools/job_r2_bench.sh ${1:-r2e}
+timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/${1:-r2e}_pytest.log 2>&1
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${1:-r2e}_smoke.log 2>&1
 echo done
