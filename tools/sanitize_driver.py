@@ -89,4 +89,14 @@ for bad_F, bad_V in ((np.arange(300).reshape(-1, 3) * 1000, Vb), (np.arange(300)
 good = compile_scene(scenes.single_mesh_description(TriangleMesh(Vb, np.arange(300).reshape(-1, 3)), (0, 0, 3),
                                                     (1, 0, 0), (0, 1, 0)))
 render_frame(good, 24, 16, 1, "eye")
+# eye frames of one scene and geometry in a row: probe, heavy-queue replays, a re-probe; and
+# a uniformly costly soup (probe stop, then row-major frames under the hint)
+sph = compile_scene(scenes.sphere_description(120, 240))
+acc = torch.zeros((96 * 64, 4), dtype=torch.float32, device="cuda")
+for _ in range(10):
+    render_into(sph, acc, 96, 64, 1, "eye", count_rays=False)
+soup = compile_scene(scenes.soup_description(200000))
+acc = torch.zeros((640 * 480, 4), dtype=torch.float32, device="cuda")
+for _ in range(3):
+    render_into(soup, acc, 640, 480, 1, "eye", count_rays=False)
 print("sanitize driver ok")
